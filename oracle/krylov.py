@@ -1,0 +1,81 @@
+"""ORACLE (test infrastructure only) — flexible GMRES (right preconditioning).
+
+PAPER.md §3.3 Algorithm 1 (Arnoldi with modified Gram-Schmidt: "h_{i,j} = (w, v_i);
+w := w - h_{i,j} v_i; h_{j+1,j} := ||w||; v_{j+1} = w / h_{j+1,j}", then "minimize over
+||beta e_1 - H_k y||") in its flexible form (§6.3 "Flexible GMRES algorithm, which also
+allows for variable preconditioning"): the preconditioned vectors z_j = P v_j are stored
+and the solution is u_k = u_0 + Z_k y_k.  The least-squares problem is solved with
+complex Givens rotations; |g_{j+1}| is the residual norm ||b - A u_j||.
+
+Inner product (w, v) = sum conj(v) w (np.vdot(v, w)).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, history=None):
+    """Solve A x = b.  Returns (x, iterations, converged)."""
+    shape = b.shape
+    bvec = b.ravel()
+    bnorm = np.linalg.norm(bvec)
+    x = np.zeros_like(bvec) if x0 is None else x0.ravel().astype(np.complex128).copy()
+    if bnorm == 0.0:
+        return x.reshape(shape), 0, True
+    r = bvec - apply_A(x.reshape(shape)).ravel() if x0 is not None else bvec.copy()
+    beta = np.linalg.norm(r)
+    if history is not None:
+        history.append(beta / bnorm)
+    if beta / bnorm <= tol:
+        return x.reshape(shape), 0, True
+    V = [r / beta]
+    Z = []
+    H = np.zeros((maxit + 1, maxit), dtype=np.complex128)
+    cs = np.zeros(maxit)
+    sn = np.zeros(maxit, dtype=np.complex128)
+    g = np.zeros(maxit + 1, dtype=np.complex128)
+    g[0] = beta
+    its = 0
+    converged = False
+    for j in range(maxit):
+        z = apply_P(V[j].reshape(shape)).ravel()
+        Z.append(z)
+        w = apply_A(z.reshape(shape)).ravel()
+        for i in range(j + 1):                         # modified Gram-Schmidt
+            H[i, j] = np.vdot(V[i], w)
+            w = w - H[i, j] * V[i]
+        H[j + 1, j] = np.linalg.norm(w)
+        for i in range(j):                             # previous rotations
+            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -np.conj(sn[i]) * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = t
+        a, bb = H[j, j], H[j + 1, j]
+        den = np.sqrt(abs(a) ** 2 + abs(bb) ** 2)
+        if abs(a) == 0.0:
+            cs[j], sn[j] = 0.0, 1.0
+        else:
+            cs[j] = abs(a) / den
+            sn[j] = (a / abs(a)) * np.conj(bb) / den
+        H[j, j] = cs[j] * a + sn[j] * bb
+        H[j + 1, j] = 0.0
+        g[j + 1] = -np.conj(sn[j]) * g[j]
+        g[j] = cs[j] * g[j]
+        its = j + 1
+        res = abs(g[j + 1]) / bnorm
+        if history is not None:
+            history.append(res)
+        if res <= tol:
+            converged = True
+            break
+        hn = np.real(bb)
+        if hn == 0.0:                                   # happy breakdown
+            converged = True
+            break
+        V.append(w / hn)
+    m = its
+    y = np.zeros(m, dtype=np.complex128)
+    for i in range(m - 1, -1, -1):                     # back substitution
+        y[i] = (g[i] - np.dot(H[i, i + 1:m], y[i + 1:m])) / H[i, i]
+    for i in range(m):
+        x = x + y[i] * Z[i]
+    return x.reshape(shape), its, converged

@@ -1,0 +1,123 @@
+"""ORACLE (test infrastructure only) — A-DEF1 two-level deflation + CSLP, FGMRES outer.
+
+PAPER.md §3.2.2 Eq. 3.21: P_{A-DEF1} = M^{-1}_{h,(beta1,beta2)} P_h + Q_h with
+P_h = I - A_h Q_h, Q_h = I_{2h}^h A_{2h}^{-1} I_h^{2h}, Z = I_{2h}^h (bilinear).
+§5.2 Eq. 5.3-5.5 give the matrix-free order: v1 = I_h^{2h} v (restriction),
+v2 = A_{2h}^{-1} v1 (coarse-grid problem, Eq. 5.6, "by Krylov subspace methods ... CSLP
+preconditioned"), v' = I_{2h}^h v2 (interpolation).
+§6 preamble: "The (CSLP-preconditioned) GMRES is employed for approximating the inverse of
+the coarse-grid operator"; §6.3: with a flexible outer method the coarse tolerance may be
+loose (1e-1) while the outer solution still meets 1e-6.
+
+Readings:
+  R10 E = A_{2h} uses the paper's scaling I_h^{2h} A_h I_{2h}^h (= Z^T A Z / 4 since the
+      full weighting is Z^T / 4); Q_h is the same operator as Z (Z^T A Z)^{-1} Z^T.
+  R11 The coarse problem E e = c is solved by right-preconditioned FGMRES from e = 0 to the
+      relative residual inner_tol, preconditioned by one CSLP V-cycle starting at level 1
+      of the CSLP hierarchy (mesh 2h); inner_solver="direct" replaces it by a dense solve.
+  R12 Outer FGMRES from u0 = 0 stops at ||b - A u||/||b|| <= tol (right preconditioning:
+      the Arnoldi residual is the true residual).
+"""
+from __future__ import annotations
+
+import dataclasses
+import time
+
+import numpy as np
+import scipy.linalg
+
+from .coarse import apply_coarse_E
+from .krylov import fgmres
+from .multigrid import build_hierarchy, vcycle
+from .operators import apply_A
+from .transfer import coarse_shape, prolong_bilinear, restrict_fw
+
+
+@dataclasses.dataclass
+class SolverParams:
+    beta: tuple = (1.0, 0.5)
+    omega: float = 0.8
+    nu_pre: int = 1
+    nu_post: int = 1
+    coarse_op: str = "galerkin"       # galerkin | red_o2 | red_o4
+    inner_solver: str = "fgmres"      # fgmres | direct
+    inner_tol: float = 1e-1
+    inner_maxit: int = 200
+    tol: float = 1e-6
+    maxit: int = 600
+    max_levels: int = 64
+
+
+class Solver:
+    def __init__(self, k, h, bc, params: SolverParams | None = None):
+        self.k = np.asarray(k, dtype=np.float64)
+        self.h = float(h)
+        self.bc = bc
+        self.p = params or SolverParams()
+        self.levels = build_hierarchy(self.k, self.h, bc, self.p.beta, self.p.max_levels)
+        if len(self.levels) < 2:
+            raise ValueError("deflation needs a coarsenable fine grid")
+        self.cshape = coarse_shape(self.k.shape, bc)
+        self._Edense = None
+        self._Elu = None
+        self.inner_its = []
+
+    # --- operators --------------------------------------------------------------------
+    def A(self, u):
+        return apply_A(u, self.k, self.h, self.bc)
+
+    def E(self, x):
+        return apply_coarse_E(x, self.k, self.h, self.bc, self.p.coarse_op)
+
+    def vcycle(self, f, level=0):
+        return vcycle(self.levels, f, level, self.p.omega, self.p.nu_pre, self.p.nu_post)
+
+    def E_dense(self):
+        if self._Edense is None:
+            n = self.cshape[0] * self.cshape[1]
+            Ed = np.zeros((n, n), dtype=np.complex128)
+            for c in range(n):
+                e = np.zeros(n, dtype=np.complex128)
+                e[c] = 1.0
+                Ed[:, c] = self.E(e.reshape(self.cshape)).ravel()
+            self._Edense = Ed
+        return self._Edense
+
+    def coarse_solve(self, c):
+        """e ~= E^{-1} c (Eq. 5.6), reading R11."""
+        if self.p.inner_solver == "direct":
+            if self._Elu is None:
+                self._Elu = scipy.linalg.lu_factor(self.E_dense())
+            return scipy.linalg.lu_solve(self._Elu, c.ravel()).reshape(self.cshape)
+        e, its, _ = fgmres(self.E, lambda v: self.vcycle(v, 1), c, self.p.inner_tol, self.p.inner_maxit)
+        self.inner_its.append(its)
+        return e
+
+    def Q(self, v):
+        """Q_h v = I_{2h}^h A_{2h}^{-1} I_h^{2h} v (Eq. 5.3-5.5)."""
+        v1 = restrict_fw(v, self.bc)
+        v2 = self.coarse_solve(v1)
+        return prolong_bilinear(v2, self.k.shape, self.bc)
+
+    def adef1(self, v):
+        """P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v (Eq. 3.21)."""
+        q = self.Q(v)
+        t = v - self.A(q)
+        return self.vcycle(t, 0) + q
+
+    # --- solve ------------------------------------------------------------------------
+    def solve(self, b, history=None):
+        self.inner_its = []
+        t0 = time.perf_counter()
+        x, its, conv = fgmres(self.A, self.adef1, np.asarray(b, dtype=np.complex128),
+                              self.p.tol, self.p.maxit, history=history)
+        t1 = time.perf_counter()
+        r = np.asarray(b) - self.A(x)
+        relres = np.linalg.norm(r) / np.linalg.norm(b) if np.linalg.norm(b) > 0 else 0.0
+        return x, {"outer_iterations": its, "converged": conv, "relres": float(relres),
+                   "inner_iterations": list(self.inner_its), "seconds": t1 - t0}
+
+
+def solve(problem, params: SolverParams | None = None, history=None):
+    s = Solver(problem.k, problem.h, problem.bc, params)
+    return s.solve(problem.b, history)

@@ -1,0 +1,93 @@
+"""Pins for oracle/coarse.py (deflation coarse operators) and the deflation identities."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import random_field, random_k
+from tests.test_oracle_transfer import _dense, _interp_1d
+from tests.test_oracle_operators import _T1
+
+
+def _A_dense(shape, h, kval, bc):
+    ny, nx = shape
+    A = (np.kron(np.eye(ny), _T1(nx, h, kval, bc)) + np.kron(_T1(ny, h, kval, bc), np.eye(nx))) / h**2
+    return A - kval**2 * np.eye(nx * ny)
+
+
+@pytest.mark.parametrize("bc,shape", [("dirichlet", (7, 11)), ("sommerfeld", (9, 7))])
+def test_galerkin_equals_dense_RAP(bc, shape):
+    """E = I_h^{2h} A_h I_{2h}^h (§3.2.1) with all three factors assembled densely from
+    independent textbook forms (Kronecker sum for A, tensor linear interpolation for Z,
+    Z^T/4 for the restriction)."""
+    h, kval = 1 / 8, 5.0
+    Z = np.kron(_interp_1d(shape[0], bc), _interp_1d(shape[1], bc))
+    A = _A_dense(shape, h, kval, bc)
+    E = (Z.T / 4) @ A @ Z
+    k = np.full(shape, kval)
+    cshape = oracle.coarse_shape(shape, bc)
+    Eo = _dense(lambda x: oracle.apply_coarse_E(x, k, h, bc, "galerkin"), cshape)
+    np.testing.assert_allclose(Eo, E, rtol=1e-13, atol=1e-10)
+
+
+def test_galerkin_tensor_closed_form():
+    """For a tensor-product operator the Galerkin coarse operator is the tensor product of
+    1D Galerkin operators.  In 1D (FW/linear) R1 P1 = [1 6 1]/8 and R1 T P1 = [-1 2 -1]/4,
+    so for homogeneous Dirichlet and constant k:
+      E = [ (R1TP1)_y (x) (R1P1)_x + (R1P1)_y (x) (R1TP1)_x ] / h^2 - k^2 (R1P1)_y (x) (R1P1)_x.
+    (Classic result; at H = 2h the interior Laplacian row is [-1 2 -1]/H^2 (x) [1 6 1]/8.)"""
+    shape, h, kval = (15, 7), 1 / 16, 11.0
+    def m1(n):
+        return (6 * np.eye(n) + np.eye(n, k=1) + np.eye(n, k=-1)) / 8
+    def t1(n):
+        return (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)) / 4
+    nyc, nxc = oracle.coarse_shape(shape, "dirichlet")
+    E = (np.kron(t1(nyc), m1(nxc)) + np.kron(m1(nyc), t1(nxc))) / h**2 - kval**2 * np.kron(m1(nyc), m1(nxc))
+    k = np.full(shape, kval)
+    Eo = _dense(lambda x: oracle.apply_coarse_E(x, k, h, "dirichlet", "galerkin"), (nyc, nxc))
+    np.testing.assert_allclose(Eo, E, rtol=1e-13, atol=1e-9)
+
+
+def test_red_o2_is_coarse_helmholtz():
+    """ReD-O2 (§5.2.3) = the Eq. 2.7 stencil at mesh width 2h with the coarse wavenumber."""
+    shape, h = (9, 13), 0.05
+    k = random_k(shape, 9)
+    x = random_field(oracle.coarse_shape(shape, "sommerfeld"), 2)
+    kc = oracle.coarse_k(k, "sommerfeld")
+    np.testing.assert_array_equal(oracle.apply_coarse_E(x, k, h, "sommerfeld", "red_o2"),
+                                  oracle.apply_A(x, kc, 2 * h, "sommerfeld"))
+
+
+def test_red_o4_fourth_order():
+    """Eq. 5.11 is the 4th-order central Laplacian: on u = sin(pi x) sin(2 pi y) the interior
+    error against -Delta u - k^2 u decays like H^4 (log-log slope 4 +- 0.2)."""
+    errs, Hs = [], []
+    for n in (16, 32, 64):
+        h = 1.0 / (2 * n)                           # fine grid; coarse H = 1/n
+        nf = 2 * n - 1
+        k = np.full((nf, nf), 3.0)
+        H = 2 * h
+        xc = np.arange(1, n) * H
+        X, Y = np.meshgrid(xc, xc)
+        u = np.sin(math.pi * X) * np.sin(2 * math.pi * Y) + 0j
+        y = oracle.apply_coarse_E(u, k, h, "dirichlet", "red_o4")
+        exact = (5 * math.pi**2 - 9.0) * u
+        errs.append(np.max(np.abs(y - exact)[2:-2, 2:-2]))
+        Hs.append(H)
+    slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
+    assert abs(slope - 4.0) < 0.2, slope
+
+
+@pytest.mark.parametrize("bc,shape", [("dirichlet", (15, 15)), ("sommerfeld", (9, 17))])
+def test_deflation_identities(bc, shape):
+    """With E = Z^T A Z (up to the 1/4) solved exactly:  P_h A Z = 0 (P_h = I - A Q_h) and
+    P_{A-DEF1} A Z x = Z x (Eq. 3.21: M^{-1} P_h A Z x + Q_h A Z x)."""
+    k = random_k(shape, 5, 5.0, 15.0)
+    s = oracle.Solver(k, 1 / 16, bc, oracle.SolverParams(inner_solver="direct"))
+    xc = random_field(s.cshape, 3)
+    Zx = oracle.prolong_bilinear(xc, shape, bc)
+    AZx = s.A(Zx)
+    np.testing.assert_allclose(s.Q(AZx), Zx, rtol=0, atol=1e-10 * np.abs(Zx).max())
+    np.testing.assert_allclose(AZx - s.A(s.Q(AZx)), 0, atol=1e-9 * np.abs(AZx).max())
+    np.testing.assert_allclose(s.adef1(AZx), Zx, atol=1e-9 * np.abs(Zx).max())

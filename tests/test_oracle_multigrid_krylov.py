@@ -1,0 +1,83 @@
+"""Pins for oracle/multigrid.py (V-cycle) and oracle/krylov.py (FGMRES)."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import mp_problem, random_field, random_k
+from tests.test_oracle_coarse import _A_dense
+from tests.test_oracle_transfer import _interp_1d
+
+
+def _M_dense(shape, h, kval, bc, beta):
+    """M = A + (1 - beta1 - i beta2) k^2 I from the Kronecker-sum A (Eq. 3.1, reading R3)."""
+    return _A_dense(shape, h, kval, bc) + (1 - beta[0] - 1j * beta[1]) * kval**2 * np.eye(shape[0] * shape[1])
+
+
+@pytest.mark.parametrize("bc,shape", [("dirichlet", (7, 15)), ("sommerfeld", (9, 9))])
+def test_two_grid_vcycle_equals_dense_operator(bc, shape):
+    """With two levels and an exact coarse solve, one V(1,1) cycle from u = 0 is the dense
+    two-grid operator  B = (I - w D^-1 M)[w D^-1 + P M_c^-1 R (I - M w D^-1)] + w D^-1
+    (pre-smooth, residual, FW restriction, coarse solve, bilinear correction, post-smooth)."""
+    h, kval, beta, w = 1 / 16, 9.0, (1.0, 0.5), 0.8
+    M = _M_dense(shape, h, kval, bc, beta)
+    cshape = oracle.coarse_shape(shape, bc)
+    Mc = _M_dense(cshape, 2 * h, kval, bc, beta)
+    Z = np.kron(_interp_1d(shape[0], bc), _interp_1d(shape[1], bc))
+    R = Z.T / 4
+    Dinv = np.diag(1.0 / np.diag(M))
+    I = np.eye(M.shape[0])
+    B = (I - w * Dinv @ M) @ (w * Dinv + Z @ np.linalg.solve(Mc, R @ (I - M @ (w * Dinv)))) + w * Dinv
+    levels = oracle.build_hierarchy(np.full(shape, kval), h, bc, beta, max_levels=2)
+    f = random_field(shape, 11)
+    np.testing.assert_allclose(oracle.vcycle(levels, f).ravel(), B @ f.ravel(), rtol=1e-12, atol=1e-12 * np.abs(B @ f.ravel()).max())
+
+
+def test_vcycle_linear_and_zero():
+    shape, h = (31, 31), 1 / 32
+    levels = oracle.build_hierarchy(random_k(shape, 2), h, "dirichlet")
+    assert [L.shape for L in levels] == [(31, 31), (15, 15), (7, 7), (3, 3), (1, 1)]
+    assert not np.any(oracle.vcycle(levels, np.zeros(shape, complex)))
+    a, b = random_field(shape, 1), random_field(shape, 2)
+    np.testing.assert_allclose(oracle.vcycle(levels, a - 2j * b),
+                               oracle.vcycle(levels, a) - 2j * oracle.vcycle(levels, b), rtol=1e-12, atol=1e-14)
+
+
+def test_jacobi_first_sweep():
+    """R9: from u = 0 one damped Jacobi sweep is u = w D^-1 f; the exact solution is a fixed point."""
+    shape, h = (5, 5), 0.1
+    L = oracle.Level(shape, h, np.full(shape, 3.0), "sommerfeld", (1.0, 0.5))
+    D = oracle.jacobi_diagonal(L)
+    M = _M_dense(shape, h, 3.0, "sommerfeld", (1.0, 0.5))
+    np.testing.assert_allclose(D.ravel(), np.diag(M), rtol=1e-15)
+    u = random_field(shape, 1)
+    f = L.M(u)
+    np.testing.assert_allclose(u + 0.8 * (f - L.M(u)) / D, u, rtol=1e-15)
+
+
+def test_fgmres_dense_exactness():
+    """Full GMRES is exact in n steps: random dense 20x20 system, identity preconditioner."""
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((20, 20)) + 1j * rng.standard_normal((20, 20)) + 6 * np.eye(20)
+    b = rng.standard_normal(20) + 0j
+    hist = []
+    x, its, conv = oracle.fgmres(lambda v: A @ v, lambda v: v, b, 1e-12, 40, history=hist)
+    assert conv and its <= 20
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-10)
+    assert all(hist[i + 1] <= hist[i] * (1 + 1e-12) for i in range(len(hist) - 1))
+    x, its, conv = oracle.fgmres(lambda v: v, lambda v: v, b, 1e-12, 5)
+    assert its == 1 and np.allclose(x, b)
+    x, its, conv = oracle.fgmres(lambda v: A @ v, lambda v: v, np.zeros(20, complex), 1e-6, 5)
+    assert its == 0 and not np.any(x)
+
+
+@pytest.mark.parametrize("bc", ["dirichlet", "sommerfeld"])
+@pytest.mark.parametrize("op", ["galerkin", "red_o2", "red_o4"])
+def test_solver_matches_dense_solve(bc, op):
+    """Brute force on a tiny grid: A-DEF1/CSLP FGMRES at tol 1e-11 reproduces the dense
+    solution of the Kronecker-assembled A (relative error << 1e-6)."""
+    p = mp_problem(12.0, 16, bc)
+    A = _A_dense(p.shape, p.h, 12.0, bc)
+    xd = np.linalg.solve(A, p.b.ravel())
+    x, rep = oracle.solve(p, oracle.SolverParams(coarse_op=op, tol=1e-11, inner_tol=1e-3))
+    assert rep["converged"] and rep["relres"] < 1e-10
+    assert np.linalg.norm(x.ravel() - xd) / np.linalg.norm(xd) < 1e-8
