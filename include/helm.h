@@ -1,0 +1,126 @@
+/*
+ * helm.h — C ABI of the B200 (sm_100a) hot path of arXiv:2308.06152:
+ * matrix-free two-level deflation (A-DEF1) + CSLP-multigrid preconditioned FGMRES for the
+ * 2D finite-difference Helmholtz equation  -Delta u - k(x,y)^2 u = b  (Eq. 2.1).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Complex numbers are complex128 stored interleaved (re, im) as two doubles; a "field"
+ *    is an array of nx*ny such numbers, row-major a[j*nx + i] with x (i) contiguous, the
+ *    (i, j) grid ordering of PAPER.md §4.  Pointers named *_dev are DEVICE pointers
+ *    (cudaMalloc / torch CUDA storage) owned by the caller; *_host are host pointers.
+ *  - Unknowns: Dirichlet grids hold the interior nodes only (homogeneous data g = 0);
+ *    Sommerfeld grids hold every node including the boundary (§2.1).
+ *  - Level 0 is the fine grid; level l has mesh width 2^l h (standard vertex-centred
+ *    coarsening, §4).  Level 1 is also the deflation coarse grid.
+ *  - All work is enqueued on the stream given to helm_setup (NULL = legacy default stream).
+ *    Entry points that return scalars (helm_solve) synchronise that stream.
+ *  - Return value: 0 on success, a negative HELM_E* code on failure; helm_last_error()
+ *    returns a thread-local message.  No entry point falls back to the CPU: if the device
+ *    or the kernels are unavailable the call fails.
+ *  - A helm_ctx is not thread-safe; use one per host thread / stream.
+ */
+#ifndef HELM_H
+#define HELM_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HELM_BC_DIRICHLET 0   /* PAPER.md Eq. 2.2 (homogeneous) */
+#define HELM_BC_SOMMERFELD 1  /* PAPER.md Eq. 2.3, ghost elimination Eq. 2.8-2.10 */
+
+#define HELM_COARSE_GALERKIN 0 /* E = I_h^{2h} A_h I_{2h}^h, stored 9-point stencil (§3.2.1, §5.2.2) */
+#define HELM_COARSE_RED_O2 1   /* second-order re-discretisation at 2h (§5.2.3) */
+#define HELM_COARSE_RED_O4 2   /* fourth-order re-discretisation, Eq. 5.11 (§5.2.3) */
+
+#define HELM_OK 0
+#define HELM_EINVAL -1   /* invalid argument (shape, parameter, null pointer) */
+#define HELM_ECUDA -2    /* CUDA runtime error (no device, launch failure, OOM) */
+#define HELM_ESHAPE -3   /* grid not coarsenable / coarsest grid too large */
+
+typedef struct helm_ctx_s* helm_ctx;
+
+/* Grid of unknowns (§2.1): nx*ny unknowns, uniform mesh width h, boundary kind. */
+typedef struct {
+  int nx, ny;
+  double h;
+  int bc; /* HELM_BC_* */
+} helm_grid;
+
+/* Method parameters (§3.1, §3.2.2, §6).  helm_default_params() fills the
+ * configuration of BASELINE.json configs[0]: shift (1, 0.5), omega 0.8, V(1,1),
+ * Galerkin E, inner CSLP-FGMRES to 1e-1. */
+typedef struct {
+  double beta1, beta2; /* CSLP shift M = -Delta - (beta1 + i beta2) k^2 (Eq. 3.1) */
+  double omega;        /* damped-Jacobi relaxation (0.8, §3.1) */
+  int nu_pre, nu_post; /* smoothing sweeps (1, 1) */
+  int coarse_op;       /* HELM_COARSE_* */
+  double inner_tol;    /* relative residual of the coarse solve E e = c (§6.3) */
+  int inner_maxit;     /* cap on inner FGMRES iterations per coarse solve */
+  int max_levels;      /* cap on multigrid levels (>= 2) */
+  int restart;         /* outer FGMRES basis size; 0 = no restart (full FGMRES) */
+  int max_coarsest;    /* largest coarsest grid (unknowns) solved by the dense inverse */
+} helm_params;
+
+typedef struct {
+  int outer_iterations;   /* FGMRES iterations to reach tol (PAPER.md "#iter") */
+  int converged;          /* 1 if ||b - A x|| / ||b|| <= tol by the Arnoldi estimate */
+  double relres;          /* final Arnoldi residual estimate / ||b|| */
+  int inner_solves;       /* coarse solves performed (one per outer iteration) */
+  long long inner_iterations_total;
+  int inner_iterations_max;
+  int restarts;
+  double seconds;         /* host wall time of the solve (stream synchronised) */
+} helm_report;
+
+void helm_default_params(helm_params* p);
+
+/* Build the solver: copies k (nx*ny float64 wavenumbers at the unknowns, host or device
+ * per k_on_device) to device memory, builds the multigrid hierarchy (coarse k sampled at
+ * coincident nodes), the deflation coarse operator and the coarsest dense inverse.
+ * `stream` is a cudaStream_t (may be NULL).  The context owns all internal workspace. */
+int helm_setup(helm_ctx* out, const helm_grid* grid, const double* k, int k_on_device,
+               const helm_params* params, void* stream);
+void helm_destroy(helm_ctx ctx);
+
+int helm_num_levels(helm_ctx ctx);
+int helm_level_info(helm_ctx ctx, int level, int* nx, int* ny, double* h);
+
+/* y = A_h x on level 0 (Algorithm 2, Eq. 2.7/2.9/2.10).  x, y: device fields. */
+int helm_apply_A(helm_ctx ctx, const double* x_dev, double* y_dev);
+/* y = M_l x, the CSLP operator of level l (Eq. 3.1, re-discretised on coarse levels). */
+int helm_apply_M(helm_ctx ctx, int level, const double* x_dev, double* y_dev);
+/* Full-weighting restriction level l -> l+1 (Eq. 3.8) and bilinear prolongation
+ * level l+1 -> l (Eq. 3.9); for l = 0 these are Z^T/4 and Z of the deflation. */
+int helm_restrict(helm_ctx ctx, int level, const double* fine_dev, double* coarse_dev);
+int helm_prolong(helm_ctx ctx, int level, const double* coarse_dev, double* fine_dev);
+/* y = E x on level 1, E the configured deflation coarse operator (§5.2). */
+int helm_apply_E(helm_ctx ctx, const double* x_dev, double* y_dev);
+/* u = one V(nu_pre, nu_post) cycle approximating M_l^{-1} f, starting at level l (§3.1). */
+int helm_vcycle(helm_ctx ctx, int level, const double* f_dev, double* u_dev);
+/* z = P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v, Q = Z E^{-1} Z^T (Eq. 3.21, Eq. 5.3-5.5),
+ * E^{-1} by CSLP-preconditioned FGMRES to inner_tol (writes the inner count to
+ * *inner_its if non-NULL). */
+int helm_deflate(helm_ctx ctx, const double* v_dev, double* z_dev, int* inner_its);
+/* Solve A x = b by A-DEF1-preconditioned FGMRES from x0 = 0 to ||b - A x||/||b|| <= tol.
+ * b, x: device fields (x may not alias b).  rep may be NULL. */
+int helm_solve(helm_ctx ctx, const double* b_dev, double* x_dev, double tol, int maxit, helm_report* rep);
+/* Same with host buffers: H2D copy of b, solve, D2H copy of x (end-to-end path). */
+int helm_solve_host(helm_ctx ctx, const double* b_host, double* x_host, double tol, int maxit,
+                    helm_report* rep);
+
+/* Write `bytes` to a scratch buffer (> L2) on the context stream: L2 flush between timed steps. */
+int helm_flush_l2(helm_ctx ctx, size_t bytes);
+/* Number of kernels this context launched since creation (bench.py's gpu_launches). */
+long long helm_launch_count(helm_ctx ctx);
+
+const char* helm_last_error(void);
+const char* helm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELM_H */

@@ -1,0 +1,498 @@
+// Device kernels of the B200 (sm_100a) hot path.  complex128 is stored as interleaved
+// double2 (re, im); grids are row-major a[j*nx + i] (x contiguous), the (i, j) grid
+// ordering of PAPER.md §4.  Every kernel here is bandwidth-bound stencil / BLAS-1 work:
+// no tensor cores.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace helm {
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+// conj(a) * b
+__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  double d = 1.0 / fma(b.x, b.x, b.y * b.y);
+  return make_double2(fma(a.x, b.x, a.y * b.y) * d, fma(a.y, b.x, -a.x * b.y) * d);
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // a*b + c
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+
+enum { BC_DIRICHLET = 0, BC_SOMMERFELD = 1 };
+
+// Geometry of one grid level.
+struct Geo {
+  int nx, ny;
+  double h;
+  int bc;
+};
+
+// Multipliers of PAPER.md Algorithm 2 at unknown (i, j) for the operator
+//   -Delta_h - s I(k^2),  s = sr + i si   (s = 1: A_h, Eq. 2.7; s = beta: CSLP M_h, Eq. 3.1)
+// with Dirichlet (zero boundary neighbours) or first-order Sommerfeld ghost elimination
+// (Eq. 2.8-2.10: outward multiplier 0, inward -2/h^2, centre -2ik/h per boundary side).
+struct Coef {
+  double2 ap;
+  double aw, ae, as, an;
+};
+
+__device__ __forceinline__ Coef coef_at(const Geo& g, int i, int j, double kk, double sr, double si) {
+  const double ih2 = 1.0 / (g.h * g.h);
+  Coef c;
+  const double k2 = kk * kk;
+  c.ap = make_double2(4.0 * ih2 - sr * k2, -si * k2);
+  c.aw = (i > 0) ? -ih2 : 0.0;
+  c.ae = (i < g.nx - 1) ? -ih2 : 0.0;
+  c.as = (j > 0) ? -ih2 : 0.0;
+  c.an = (j < g.ny - 1) ? -ih2 : 0.0;
+  if (g.bc == BC_SOMMERFELD) {
+    const double t = 2.0 * kk / g.h;
+    if (i == 0)        { c.ae = -2.0 * ih2; c.ap.y -= t; }
+    if (i == g.nx - 1) { c.aw = -2.0 * ih2; c.ap.y -= t; }
+    if (j == 0)        { c.an = -2.0 * ih2; c.ap.y -= t; }
+    if (j == g.ny - 1) { c.as = -2.0 * ih2; c.ap.y -= t; }
+  }
+  return c;
+}
+
+__device__ __forceinline__ double2 stencil_apply(const Geo& g, const double2* __restrict__ u, int i, int j,
+                                                 const Coef& c) {
+  const size_t p = (size_t)j * g.nx + i;
+  double2 v = cmul(c.ap, u[p]);
+  if (c.aw != 0.0) v = cadd(v, cscale(c.aw, u[p - 1]));
+  if (c.ae != 0.0) v = cadd(v, cscale(c.ae, u[p + 1]));
+  if (c.as != 0.0) v = cadd(v, cscale(c.as, u[p - g.nx]));
+  if (c.an != 0.0) v = cadd(v, cscale(c.an, u[p + g.nx]));
+  return v;
+}
+
+// ------------------------------------------------------------------ operator kernels
+// mode 0: y = Op u ;  mode 1: y = f - Op u (residual)
+template <int MODE>
+__global__ void k_apply_op(Geo g, const double2* __restrict__ u, const double2* __restrict__ f,
+                           double2* __restrict__ y, const double* __restrict__ k, double sr, double si) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const size_t p = (size_t)j * g.nx + i;
+  Coef c = coef_at(g, i, j, k[p], sr, si);
+  double2 v = stencil_apply(g, u, i, j, c);
+  if (MODE == 1) v = csub(f[p], v);
+  y[p] = v;
+}
+
+// u = omega * f / D   (first damped-Jacobi sweep from u = 0)
+__global__ void k_jacobi0(Geo g, const double2* __restrict__ f, double2* __restrict__ u,
+                          const double* __restrict__ k, double sr, double si, double omega) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const size_t p = (size_t)j * g.nx + i;
+  Coef c = coef_at(g, i, j, k[p], sr, si);
+  u[p] = cscale(omega, cdiv(f[p], c.ap));
+}
+
+// unew = u + omega * (f - M u) / D  (+ optional add of `q`, used to fuse z = M^-1 t + q)
+__global__ void k_jacobi(Geo g, const double2* __restrict__ u, const double2* __restrict__ f,
+                         double2* __restrict__ unew, const double* __restrict__ k, double sr, double si,
+                         double omega, const double2* __restrict__ addq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const size_t p = (size_t)j * g.nx + i;
+  Coef c = coef_at(g, i, j, k[p], sr, si);
+  double2 r = csub(f[p], stencil_apply(g, u, i, j, c));
+  double2 v = cadd(u[p], cscale(omega, cdiv(r, c.ap)));
+  if (addq) v = cadd(v, addq[p]);
+  unew[p] = v;
+}
+
+// Full weighting (Eq. 3.8), gather at fine node (2I+o, 2J+o); out-of-array taps dropped.
+__global__ void k_restrict(Geo gf, Geo gc, int o, const double2* __restrict__ v, double2* __restrict__ vc) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y * blockDim.y + threadIdx.y;
+  if (I >= gc.nx || J >= gc.ny) return;
+  const int ci = 2 * I + o, cj = 2 * J + o;
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int b = -1; b <= 1; ++b) {
+    const int jj = cj + b;
+    if (jj < 0 || jj >= gf.ny) continue;
+#pragma unroll
+    for (int a = -1; a <= 1; ++a) {
+      const int ii = ci + a;
+      if (ii < 0 || ii >= gf.nx) continue;
+      const double w = (a == 0 ? 2.0 : 1.0) * (b == 0 ? 2.0 : 1.0) * (1.0 / 16.0);
+      s = cadd(s, cscale(w, v[(size_t)jj * gf.nx + ii]));
+    }
+  }
+  vc[(size_t)J * gc.nx + I] = s;
+}
+
+// Bilinear interpolation (Eq. 3.9) as a gather at each fine node:
+//   y = P e  (MODE 0)  or  y = base + P e  (MODE 1)
+template <int MODE>
+__global__ void k_prolong(Geo gf, Geo gc, int o, const double2* __restrict__ e, const double2* __restrict__ base,
+                          double2* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= gf.nx || j >= gf.ny) return;
+  const int ri = i - o, rj = j - o;           // position relative to coarse node 0
+  // coarse candidates: I0 = floor(ri/2) and I0+1 when ri is odd
+  double2 s = make_double2(0.0, 0.0);
+  const int I0 = (ri >= 0) ? (ri >> 1) : -1;   // ri = -1 only for Dirichlet i = 0
+  const int J0 = (rj >= 0) ? (rj >> 1) : -1;
+  const bool oddx = (ri & 1) != 0, oddy = (rj & 1) != 0;
+  for (int bj = 0; bj <= (oddy ? 1 : 0); ++bj) {
+    const int J = J0 + bj;
+    if (J < 0 || J >= gc.ny) continue;
+    const double wy = oddy ? 0.5 : 1.0;
+    for (int ai = 0; ai <= (oddx ? 1 : 0); ++ai) {
+      const int I = I0 + ai;
+      if (I < 0 || I >= gc.nx) continue;
+      const double wx = oddx ? 0.5 : 1.0;
+      s = cadd(s, cscale(wx * wy, e[(size_t)J * gc.nx + I]));
+    }
+  }
+  const size_t p = (size_t)j * gf.nx + i;
+  if (MODE == 1) s = cadd(s, base[p]);
+  y[p] = s;
+}
+
+// Coarse wavenumber sampled at coincident fine nodes (re-discretisation, §5.1).
+__global__ void k_sample_k(Geo gf, Geo gc, int o, const double* __restrict__ kf, double* __restrict__ kc) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y * blockDim.y + threadIdx.y;
+  if (I >= gc.nx || J >= gc.ny) return;
+  kc[(size_t)J * gc.nx + I] = kf[(size_t)(2 * J + o) * gf.nx + (2 * I + o)];
+}
+
+// ------------------------------------------------------------------ Galerkin coarse stencil
+// E = R A P (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; §5.2.2 stencil operation):
+// its 9 coefficients per coarse node, evaluated once from the definition
+//   E[(I,J),(I+dx,J+dy)] = sum_a R[(I,J),a] sum_{b in nbr(a)} A[a,b] P[b,(I+dx,J+dy)]
+// and stored SoA: coef[d*nc + p], d = (dy+1)*3 + (dx+1).
+__global__ void k_galerkin_coef(Geo gf, Geo gc, int o, const double* __restrict__ kf, double2* __restrict__ coef) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y * blockDim.y + threadIdx.y;
+  if (I >= gc.nx || J >= gc.ny) return;
+  double2 acc[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) acc[d] = make_double2(0.0, 0.0);
+  const int ci = 2 * I + o, cj = 2 * J + o;
+  for (int b = -1; b <= 1; ++b) {
+    const int aj = cj + b;
+    if (aj < 0 || aj >= gf.ny) continue;
+    for (int a = -1; a <= 1; ++a) {
+      const int ai = ci + a;
+      if (ai < 0 || ai >= gf.nx) continue;
+      const double rw = (a == 0 ? 2.0 : 1.0) * (b == 0 ? 2.0 : 1.0) * (1.0 / 16.0);
+      Coef c = coef_at(gf, ai, aj, kf[(size_t)aj * gf.nx + ai], 1.0, 0.0);
+      // the 5 fine neighbours b of a with A[a,b]
+      const int bi[5] = {ai, ai - 1, ai + 1, ai, ai};
+      const int bjv[5] = {aj, aj, aj, aj - 1, aj + 1};
+      const double2 aval[5] = {c.ap, make_double2(c.aw, 0), make_double2(c.ae, 0), make_double2(c.as, 0),
+                               make_double2(c.an, 0)};
+      for (int q = 0; q < 5; ++q) {
+        if (q > 0 && aval[q].x == 0.0) continue;
+        const int xi = bi[q], yj = bjv[q];
+        if (xi < 0 || xi >= gf.nx || yj < 0 || yj >= gf.ny) continue;
+        // P[b, (I', J')] nonzero for coarse nodes within distance 1 of b in node units
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int Jp = J + dy;
+          if (Jp < 0 || Jp >= gc.ny) continue;
+          const int ddy = yj - (2 * Jp + o);
+          if (ddy < -1 || ddy > 1) continue;
+          const double wy = ddy == 0 ? 1.0 : 0.5;
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int Ip = I + dx;
+            if (Ip < 0 || Ip >= gc.nx) continue;
+            const int ddx = xi - (2 * Ip + o);
+            if (ddx < -1 || ddx > 1) continue;
+            const double wx = ddx == 0 ? 1.0 : 0.5;
+            const int d = (dy + 1) * 3 + (dx + 1);
+            acc[d] = cadd(acc[d], cscale(rw * wx * wy, aval[q]));
+          }
+        }
+      }
+    }
+  }
+  const size_t nc = (size_t)gc.nx * gc.ny;
+  const size_t p = (size_t)J * gc.nx + I;
+#pragma unroll
+  for (int d = 0; d < 9; ++d) coef[d * nc + p] = acc[d];
+}
+
+// y = E x with the stored 9-point Galerkin stencil (MODE 1: y = f - E x).
+template <int MODE>
+__global__ void k_apply_9pt(Geo gc, const double2* __restrict__ coef, const double2* __restrict__ x,
+                            const double2* __restrict__ f, double2* __restrict__ y) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y * blockDim.y + threadIdx.y;
+  if (I >= gc.nx || J >= gc.ny) return;
+  const size_t nc = (size_t)gc.nx * gc.ny;
+  const size_t p = (size_t)J * gc.nx + I;
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int Jp = J + dy;
+    if (Jp < 0 || Jp >= gc.ny) continue;
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int Ip = I + dx;
+      if (Ip < 0 || Ip >= gc.nx) continue;
+      const int d = (dy + 1) * 3 + (dx + 1);
+      s = cfma(coef[d * nc + p], x[(size_t)Jp * gc.nx + Ip], s);
+    }
+  }
+  if (MODE == 1) s = csub(f[p], s);
+  y[p] = s;
+}
+
+// ReD-O4 (Eq. 5.11, reading R5: centre 5/H^2 - k^2) where the 5-wide cross fits,
+// second-order Helmholtz stencil elsewhere (reading R6).
+template <int MODE>
+__global__ void k_apply_red_o4(Geo g, const double2* __restrict__ x, const double2* __restrict__ f,
+                               double2* __restrict__ y, const double* __restrict__ k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const size_t p = (size_t)j * g.nx + i;
+  bool fits;
+  if (g.bc == BC_DIRICHLET) fits = (i >= 1 && i <= g.nx - 2 && j >= 1 && j <= g.ny - 2);
+  else fits = (i >= 2 && i <= g.nx - 3 && j >= 2 && j <= g.ny - 3);
+  double2 v;
+  if (fits) {
+    auto at = [&](int ii, int jj) -> double2 {
+      if (ii < 0 || ii >= g.nx || jj < 0 || jj >= g.ny) return make_double2(0.0, 0.0);
+      return x[(size_t)jj * g.nx + ii];
+    };
+    const double2 c = x[p];
+    double2 d1 = cadd(cadd(at(i - 1, j), at(i + 1, j)), cadd(at(i, j - 1), at(i, j + 1)));
+    double2 d2 = cadd(cadd(at(i - 2, j), at(i + 2, j)), cadd(at(i, j - 2), at(i, j + 2)));
+    const double s = 1.0 / (12.0 * g.h * g.h);
+    const double kk = k[p];
+    v = make_double2(s * (60.0 * c.x - 16.0 * d1.x + d2.x) - kk * kk * c.x,
+                     s * (60.0 * c.y - 16.0 * d1.y + d2.y) - kk * kk * c.y);
+  } else {
+    Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
+    v = stencil_apply(g, x, i, j, c);
+  }
+  if (MODE == 1) v = csub(f[p], v);
+  y[p] = v;
+}
+
+// ------------------------------------------------------------------ coarsest dense solve
+// Dense M of the coarsest level, row-major n x n (row = unknown p).
+__global__ void k_dense_op(Geo g, const double* __restrict__ k, double sr, double si, double2* __restrict__ Md) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const size_t n = (size_t)g.nx * g.ny;
+  const size_t p = (size_t)j * g.nx + i;
+  Coef c = coef_at(g, i, j, k[p], sr, si);
+  double2* row = Md + p * n;
+  row[p] = c.ap;
+  if (c.aw != 0.0) row[p - 1] = make_double2(c.aw, 0.0);
+  if (c.ae != 0.0) row[p + 1] = make_double2(c.ae, 0.0);
+  if (c.as != 0.0) row[p - g.nx] = make_double2(c.as, 0.0);
+  if (c.an != 0.0) row[p + g.nx] = make_double2(c.an, 0.0);
+}
+
+// Gauss-Jordan with partial pivoting on the augmented [M | I] (n x 2n, row-major).
+__global__ void k_gj_pivot(const double2* __restrict__ Aug, int n, int col, int* __restrict__ piv) {
+  // one block: argmax_{r >= col} |Aug[r][col]|
+  __shared__ double sv[1024];
+  __shared__ int si[1024];
+  double best = -1.0;
+  int bi = col;
+  for (int r = col + threadIdx.x; r < n; r += blockDim.x) {
+    double2 a = Aug[(size_t)r * 2 * n + col];
+    double m = a.x * a.x + a.y * a.y;
+    if (m > best) { best = m; bi = r; }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      if (sv[threadIdx.x + s] > sv[threadIdx.x] ||
+          (sv[threadIdx.x + s] == sv[threadIdx.x] && si[threadIdx.x + s] < si[threadIdx.x])) {
+        sv[threadIdx.x] = sv[threadIdx.x + s];
+        si[threadIdx.x] = si[threadIdx.x + s];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *piv = si[0];
+}
+
+__global__ void k_gj_swap_scale(double2* __restrict__ Aug, int n, int col, const int* __restrict__ piv,
+                                double2* __restrict__ colbuf) {
+  const int p = *piv;
+  const int w = 2 * n;
+  // swap rows col and p, then scale row col by 1/pivot; one block
+  for (int c = threadIdx.x; c < w; c += blockDim.x) {
+    double2 a = Aug[(size_t)col * w + c];
+    double2 b = Aug[(size_t)p * w + c];
+    Aug[(size_t)col * w + c] = b;
+    Aug[(size_t)p * w + c] = a;
+  }
+  __syncthreads();
+  __shared__ double2 pv;
+  if (threadIdx.x == 0) pv = Aug[(size_t)col * w + col];
+  __syncthreads();
+  const double2 inv = cdiv(make_double2(1.0, 0.0), pv);
+  for (int c = threadIdx.x; c < w; c += blockDim.x) Aug[(size_t)col * w + c] = cmul(Aug[(size_t)col * w + c], inv);
+  __syncthreads();
+  // save column col (multipliers) for the elimination step
+  for (int r = threadIdx.x; r < n; r += blockDim.x) colbuf[r] = Aug[(size_t)r * w + col];
+}
+
+__global__ void k_gj_eliminate(double2* __restrict__ Aug, int n, int col, const double2* __restrict__ colbuf) {
+  const int w = 2 * n;
+  const size_t total = (size_t)n * w;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / w), c = (int)(t % w);
+    if (r == col) continue;
+    const double2 m = colbuf[r];
+    if (m.x == 0.0 && m.y == 0.0) continue;
+    Aug[t] = csub(Aug[t], cmul(m, Aug[(size_t)col * w + c]));
+  }
+}
+
+__global__ void k_gj_extract(const double2* __restrict__ Aug, int n, double2* __restrict__ Minv) {
+  const size_t total = (size_t)n * n;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / n), c = (int)(t % n);
+    Minv[t] = Aug[(size_t)r * 2 * n + n + c];
+  }
+}
+
+// y = Minv f, one warp per row.
+__global__ void k_gemv(const double2* __restrict__ Minv, int n, const double2* __restrict__ f, double2* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const double2* row = Minv + (size_t)warp * n;
+  double2 s = make_double2(0.0, 0.0);
+  for (int c = lane; c < n; c += 32) s = cfma(row[c], f[c], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+  }
+  if (lane == 0) y[warp] = s;
+}
+
+// ------------------------------------------------------------------ BLAS-1 (Krylov)
+// partial[c*nb + b] = sum over block b's slice of conj(V_c) w, for c in [c0, c0+NV)
+// V_c = V + c*ld.  Deterministic: fixed grid, fixed in-block tree, fixed second stage.
+template <int NV>
+__global__ void k_multidot_partial(const double2* __restrict__ V, size_t ld, int nvec, const double2* __restrict__ w,
+                                   size_t n, double2* __restrict__ partial) {
+  const int c0 = blockIdx.y * NV;
+  double2 acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const double2 we = w[e];
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      if (c0 + q < nvec) {
+        const double2 v = V[(size_t)(c0 + q) * ld + e];
+        acc[q].x += v.x * we.x + v.y * we.y;
+        acc[q].y += v.x * we.y - v.y * we.x;
+      }
+  }
+  __shared__ double2 red[NV][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double2 s = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    }
+    if (lane == 0) red[q][wid] = s;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double2 s = lane < nw ? red[q][lane] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      }
+      if (lane == 0 && c0 + q < nvec) partial[(size_t)(c0 + q) * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// out[c] (+)= sum_b partial[c*nb + b]   (one warp per c).  If `accum`, adds to out.
+__global__ void k_multidot_final(const double2* __restrict__ partial, int nb, int nvec, double2* __restrict__ out,
+                                 int accum) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nvec) return;
+  double2 s = make_double2(0.0, 0.0);
+  for (int b = lane; b < nb; b += 32) s = cadd(s, partial[(size_t)c * nb + b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+  }
+  if (lane == 0) out[c] = accum ? cadd(out[c], s) : s;
+}
+
+// w += sign * sum_c coeff[c] * V_c   (sign = -1 for Gram-Schmidt, +1 for x += Z y)
+__global__ void k_multi_axpy(const double2* __restrict__ V, size_t ld, int nvec, const double2* __restrict__ coeff,
+                             double sign, double2* __restrict__ w, size_t n) {
+  extern __shared__ double2 sc[];
+  for (int c = threadIdx.x; c < nvec; c += blockDim.x) sc[c] = cscale(sign, coeff[c]);
+  __syncthreads();
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    double2 s = w[e];
+    for (int c = 0; c < nvec; ++c) s = cfma(sc[c], V[(size_t)c * ld + e], s);
+    w[e] = s;
+  }
+}
+
+// v = w / sqrt(re(nrm2[0]))   (nrm2 computed on device; no host round trip)
+__global__ void k_normalize(const double2* __restrict__ w, const double2* __restrict__ nrm2, double2* __restrict__ v,
+                            size_t n) {
+  const double s = 1.0 / sqrt(nrm2[0].x);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    v[e] = cscale(s, w[e]);
+}
+
+__global__ void k_scale_copy(const double2* __restrict__ x, double s, double2* __restrict__ y, size_t n) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    y[e] = cscale(s, x[e]);
+}
+
+// y = a + b
+__global__ void k_add(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ y, size_t n) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    y[e] = cadd(a[e], b[e]);
+}
+
+__global__ void k_l2flush(uint4* buf, size_t n, unsigned v) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    buf[e] = make_uint4(v, v, v, v);
+}
+
+}  // namespace helm

@@ -1,0 +1,248 @@
+"""Thin ctypes binding of libhelm.so (include/helm.h).  Argument marshalling only: every
+step of the hot path runs in the CUDA kernels of the library.  Fields are torch
+complex128 CUDA tensors of shape (ny, nx) (row-major, x contiguous); PyTorch provides
+device memory and streams, nothing else.  There is no CPU fallback: if the library or a
+CUDA device is missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libhelm.so")
+
+HELM_BC_DIRICHLET = 0
+HELM_BC_SOMMERFELD = 1
+COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2}
+BCS = {"dirichlet": HELM_BC_DIRICHLET, "sommerfeld": HELM_BC_SOMMERFELD}
+
+
+class helm_grid(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("h", ctypes.c_double), ("bc", ctypes.c_int)]
+
+
+class helm_params(ctypes.Structure):
+    _fields_ = [("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("omega", ctypes.c_double),
+                ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("coarse_op", ctypes.c_int),
+                ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int), ("max_levels", ctypes.c_int),
+                ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int)]
+
+
+class helm_report(ctypes.Structure):
+    _fields_ = [("outer_iterations", ctypes.c_int), ("converged", ctypes.c_int), ("relres", ctypes.c_double),
+                ("inner_solves", ctypes.c_int), ("inner_iterations_total", ctypes.c_longlong),
+                ("inner_iterations_max", ctypes.c_int), ("restarts", ctypes.c_int), ("seconds", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+EXPORTS = {
+    "helm_default_params": (None, [ctypes.POINTER(helm_params)]),
+    "helm_setup": (_I, [ctypes.POINTER(_P), ctypes.POINTER(helm_grid), _P, _I, ctypes.POINTER(helm_params), _P]),
+    "helm_destroy": (None, [_P]),
+    "helm_num_levels": (_I, [_P]),
+    "helm_level_info": (_I, [_P, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_D)]),
+    "helm_apply_A": (_I, [_P, _P, _P]),
+    "helm_apply_M": (_I, [_P, _I, _P, _P]),
+    "helm_restrict": (_I, [_P, _I, _P, _P]),
+    "helm_prolong": (_I, [_P, _I, _P, _P]),
+    "helm_apply_E": (_I, [_P, _P, _P]),
+    "helm_vcycle": (_I, [_P, _I, _P, _P]),
+    "helm_deflate": (_I, [_P, _P, _P, ctypes.POINTER(_I)]),
+    "helm_solve": (_I, [_P, _P, _P, _D, _I, ctypes.POINTER(helm_report)]),
+    "helm_solve_host": (_I, [_P, _P, _P, _D, _I, ctypes.POINTER(helm_report)]),
+    "helm_flush_l2": (_I, [_P, ctypes.c_size_t]),
+    "helm_launch_count": (ctypes.c_longlong, [_P]),
+    "helm_last_error": (ctypes.c_char_p, []),
+    "helm_build_info": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+def load_library(path: str = _LIB_PATH):
+    """Load libhelm.so and bind every symbol of include/helm.h (raises if any is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class HelmError(RuntimeError):
+    pass
+
+
+def _check(rc):
+    if rc != 0:
+        raise HelmError(f"libhelm error {rc}: {_lib.helm_last_error().decode()}")
+
+
+def default_params(**overrides) -> helm_params:
+    lib = load_library()
+    p = helm_params()
+    lib.helm_default_params(ctypes.byref(p))
+    for key, val in overrides.items():
+        if key == "coarse_op" and isinstance(val, str):
+            val = COARSE_OPS[val]
+        if key == "beta":
+            p.beta1, p.beta2 = val
+            continue
+        if not hasattr(p, key):
+            raise KeyError(key)
+        setattr(p, key, val)
+    return p
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Helm:
+    """One solver context (helm_setup ... helm_destroy)."""
+
+    def __init__(self, nx: int, ny: int, h: float, bc: str, k, params: helm_params | dict | None = None,
+                 stream=None):
+        import torch
+        self.torch = torch
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise HelmError("no CUDA device: libhelm has no CPU fallback")
+        self.lib = lib
+        self.nx, self.ny, self.h, self.bc = int(nx), int(ny), float(h), bc
+        if isinstance(params, dict) or params is None:
+            params = default_params(**(params or {}))
+        self.params = params
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        kt = torch.as_tensor(np.ascontiguousarray(k, dtype=np.float64)) if not isinstance(k, torch.Tensor) else k
+        kt = kt.to(device="cuda", dtype=torch.float64).contiguous()
+        assert kt.shape == (self.ny, self.nx)
+        g = helm_grid(self.nx, self.ny, self.h, BCS[bc])
+        ctx = ctypes.c_void_p()
+        _check(lib.helm_setup(ctypes.byref(ctx), ctypes.byref(g), _ptr(kt), 1, ctypes.byref(params),
+                              ctypes.c_void_p(self.stream.cuda_stream)))
+        self.ctx = ctx
+        self.levels = [self.level_info(l) for l in range(lib.helm_num_levels(ctx))]
+
+    # -- helpers --------------------------------------------------------------------
+    def level_info(self, l):
+        nx, ny, h = _I(), _I(), _D()
+        _check(self.lib.helm_level_info(self.ctx, l, ctypes.byref(nx), ctypes.byref(ny), ctypes.byref(h)))
+        return (ny.value, nx.value, h.value)
+
+    def field(self, level=0):
+        ny, nx, _ = self.levels[level]
+        return self.torch.zeros((ny, nx), dtype=self.torch.complex128, device="cuda")
+
+    def _in(self, x, level=0):
+        t = self.torch
+        x = t.as_tensor(x).to(device="cuda", dtype=t.complex128).contiguous()
+        assert tuple(x.shape) == self.levels[level][:2], (x.shape, self.levels[level])
+        return x
+
+    # -- the C ABI, one method per entry point -----------------------------------------
+    def helm_apply_A(self, x, y=None):
+        x = self._in(x)
+        y = self.field(0) if y is None else y
+        _check(self.lib.helm_apply_A(self.ctx, _ptr(x), _ptr(y)))
+        return y
+
+    def helm_apply_M(self, level, x, y=None):
+        x = self._in(x, level)
+        y = self.field(level) if y is None else y
+        _check(self.lib.helm_apply_M(self.ctx, level, _ptr(x), _ptr(y)))
+        return y
+
+    def helm_restrict(self, level, v):
+        v = self._in(v, level)
+        y = self.field(level + 1)
+        _check(self.lib.helm_restrict(self.ctx, level, _ptr(v), _ptr(y)))
+        return y
+
+    def helm_prolong(self, level, e):
+        e = self._in(e, level + 1)
+        y = self.field(level)
+        _check(self.lib.helm_prolong(self.ctx, level, _ptr(e), _ptr(y)))
+        return y
+
+    def helm_apply_E(self, x):
+        x = self._in(x, 1)
+        y = self.field(1)
+        _check(self.lib.helm_apply_E(self.ctx, _ptr(x), _ptr(y)))
+        return y
+
+    def helm_vcycle(self, level, f, u=None):
+        f = self._in(f, level)
+        u = self.field(level) if u is None else u
+        _check(self.lib.helm_vcycle(self.ctx, level, _ptr(f), _ptr(u)))
+        return u
+
+    def helm_deflate(self, v, z=None):
+        v = self._in(v)
+        z = self.field(0) if z is None else z
+        its = _I()
+        _check(self.lib.helm_deflate(self.ctx, _ptr(v), _ptr(z), ctypes.byref(its)))
+        return z, its.value
+
+    def helm_solve(self, b, tol=1e-6, maxit=600, x=None):
+        b = self._in(b)
+        x = self.field(0) if x is None else x
+        rep = helm_report()
+        _check(self.lib.helm_solve(self.ctx, _ptr(b), _ptr(x), float(tol), int(maxit), ctypes.byref(rep)))
+        return x, rep.as_dict()
+
+    def helm_solve_host(self, b_host: np.ndarray, x_host: np.ndarray | None = None, tol=1e-6, maxit=600):
+        """End-to-end: b and x are host (numpy complex128, ideally pinned) arrays."""
+        b_host = np.ascontiguousarray(b_host, dtype=np.complex128)
+        x_host = np.empty_like(b_host) if x_host is None else x_host
+        rep = helm_report()
+        _check(self.lib.helm_solve_host(self.ctx, b_host.ctypes.data_as(_P), x_host.ctypes.data_as(_P),
+                                        float(tol), int(maxit), ctypes.byref(rep)))
+        return x_host, rep.as_dict()
+
+    def helm_flush_l2(self, nbytes=256 << 20):
+        _check(self.lib.helm_flush_l2(self.ctx, nbytes))
+
+    def helm_launch_count(self):
+        return int(self.lib.helm_launch_count(self.ctx))
+
+    # short aliases
+    apply_A = helm_apply_A
+    apply_M = helm_apply_M
+    restrict = helm_restrict
+    prolong = helm_prolong
+    apply_E = helm_apply_E
+    vcycle = helm_vcycle
+    deflate = helm_deflate
+    solve = helm_solve
+    solve_host = helm_solve_host
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.helm_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def helm_setup(problem, params=None, stream=None) -> Helm:
+    """Build a context from a workloads.Problem-like object (k, h, bc, nx, ny)."""
+    return Helm(problem.nx, problem.ny, problem.h, problem.bc, problem.k, params, stream)

@@ -1,0 +1,184 @@
+"""GPU parity: libhelm.so (through its C ABI / ctypes binding) against the oracle, element by
+element, on the same seeded inputs.  Tolerances (from BASELINE.json
+north_star): a single operator apply within 1e-12 relative L2; outer iteration counts
+within +-1; final solutions within 1e-6 relative L2."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workloads import config_problem, mp_problem, random_field, random_k, wedge_problem
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 1e-12
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def gpu(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+class P:
+    """A small problem description with an arbitrary k field."""
+
+    def __init__(self, nx, ny, h, bc, k):
+        self.nx, self.ny, self.h, self.bc, self.k = nx, ny, h, bc, k
+
+    @property
+    def shape(self):
+        return (self.ny, self.nx)
+
+
+GRIDS = [
+    P(31, 31, 1 / 32, "dirichlet", np.full((31, 31), 20.0)),
+    P(45, 37, 1 / 46, "dirichlet", random_k((37, 45), 1, 10, 60)),          # ragged, variable k
+    P(33, 65, 1 / 64, "sommerfeld", random_k((65, 33), 2, 5, 40)),
+    P(3, 3, 1 / 4, "dirichlet", np.full((3, 3), 2.0)),                       # smallest Dirichlet
+    P(3, 5, 1 / 4, "sommerfeld", random_k((5, 3), 3, 1, 3)),                 # smallest Sommerfeld
+    P(129, 257, 1 / 256, "sommerfeld", random_k((257, 129), 4, 10, 150)),
+]
+IDS = ["c0", "dir45x37", "som33x65", "dir3", "som3x5", "som129x257"]
+
+
+@pytest.fixture(params=list(range(len(GRIDS))), ids=IDS)
+def case(request, lib):
+    p = GRIDS[request.param]
+    H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k)
+    yield p, H
+    H.close()
+
+
+def test_apply_A(case):
+    p, H = case
+    for seed in range(3):
+        u = random_field(p.shape, seed)
+        y = H.apply_A(gpu(u)).cpu().numpy()
+        assert rel(y, oracle.apply_A(u, p.k, p.h, p.bc)) < OP_TOL
+
+
+def test_levels_and_M(case):
+    p, H = case
+    levels = oracle.build_hierarchy(p.k, p.h, p.bc)
+    assert [L.shape for L in levels] == [lv[:2] for lv in H.levels]
+    for l, L in enumerate(levels):
+        assert H.levels[l][2] == pytest.approx(L.h, rel=1e-15)
+        u = random_field(L.shape, 10 + l)
+        y = H.apply_M(l, gpu(u)).cpu().numpy()
+        assert rel(y, oracle.apply_M(u, L.k, L.h, p.bc, (1.0, 0.5))) < OP_TOL
+
+
+def test_transfers(case):
+    p, H = case
+    levels = oracle.build_hierarchy(p.k, p.h, p.bc)
+    for l in range(len(levels) - 1):
+        v = random_field(levels[l].shape, 20 + l)
+        assert rel(H.restrict(l, gpu(v)).cpu().numpy(), oracle.restrict_fw(v, p.bc)) < 1e-14
+        e = random_field(levels[l + 1].shape, 30 + l)
+        assert rel(H.prolong(l, gpu(e)).cpu().numpy(), oracle.prolong_bilinear(e, levels[l].shape, p.bc)) < 1e-14
+
+
+@pytest.mark.parametrize("op", ["galerkin", "red_o2", "red_o4"])
+def test_coarse_operator(lib, op):
+    for p in GRIDS:
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"coarse_op": op})
+        x = random_field(H.levels[1][:2], 5)
+        y = H.apply_E(gpu(x)).cpu().numpy()
+        yo = oracle.apply_coarse_E(x, p.k, p.h, p.bc, op)
+        assert rel(y, yo) < OP_TOL, (op, p.shape, p.bc)
+        H.close()
+
+
+def test_vcycle(case):
+    p, H = case
+    levels = oracle.build_hierarchy(p.k, p.h, p.bc)
+    for l in range(min(2, len(levels))):
+        f = random_field(levels[l].shape, 40 + l)
+        u = H.vcycle(l, gpu(f)).cpu().numpy()
+        assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11
+
+
+@pytest.mark.parametrize("op", ["galerkin", "red_o4"])
+def test_deflate(lib, op):
+    """z = P_{A-DEF1} v with the inner coarse solve at a tight tolerance (1e-10), so both
+    sides run to the same well-defined E^{-1} c."""
+    for p in GRIDS[:3]:
+        prm = {"coarse_op": op, "inner_tol": 1e-10, "inner_maxit": 400}
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, prm)
+        s = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, inner_tol=1e-10, inner_maxit=400))
+        v = random_field(p.shape, 7)
+        z, its = H.deflate(gpu(v))
+        zo = s.adef1(v)
+        assert rel(z.cpu().numpy(), zo) < 1e-8, (op, p.shape)
+        assert abs(its - s.inner_its[-1]) <= 1
+        H.close()
+
+
+SOLVE_CASES = [
+    ("c0_tiny", "galerkin"), ("c0_tiny", "red_o2"), ("c0_tiny", "red_o4"),
+    ("mp_som_k20", "galerkin"), ("mp_som_k40", "red_o4"),
+    ("c1_k50", "galerkin"), ("c1_k50", "red_o4"),
+    ("wedge_f10", "galerkin"),
+]
+
+
+def _problem(name):
+    if name == "mp_som_k20":
+        return mp_problem(20.0, 32, "sommerfeld")
+    if name == "mp_som_k40":
+        return mp_problem(40.0, 64, "sommerfeld")
+    if name == "wedge_f10":
+        return wedge_problem(10.0)
+    return config_problem(name)
+
+
+@pytest.mark.parametrize("name,op", SOLVE_CASES)
+def test_solve(lib, name, op):
+    p = _problem(name)
+    H = lib.helm_setup(p, {"coarse_op": op})
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=400)
+    xo, rep_o = oracle.solve(p, oracle.SolverParams(coarse_op=op))
+    assert rep["converged"] and rep_o["converged"]
+    assert abs(rep["outer_iterations"] - rep_o["outer_iterations"]) <= 1, (rep, rep_o["outer_iterations"])
+    x = x.cpu().numpy()
+    assert rel(x, xo) < 1e-6
+    # true residual of the GPU solution, measured by the oracle's operator
+    assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
+    H.close()
+
+
+def test_zero_rhs(lib):
+    p = config_problem("c0_tiny")
+    H = lib.helm_setup(p)
+    x, rep = H.solve(torch.zeros(p.shape, dtype=torch.complex128, device="cuda"))
+    assert rep["outer_iterations"] == 0 and rep["converged"] and not torch.any(x != 0)
+    H.close()
+
+
+def test_solve_host_matches_device(lib):
+    p = config_problem("c0_tiny")
+    H = lib.helm_setup(p)
+    xd, rd = H.solve(gpu(p.b))
+    xh, rh = H.solve_host(p.b)
+    assert rd["outer_iterations"] == rh["outer_iterations"]
+    np.testing.assert_array_equal(xd.cpu().numpy(), xh)
+    H.close()
+
+
+def test_invalid_arguments(lib):
+    with pytest.raises(lib.HelmError):
+        lib.Helm(4, 4, 0.2, "dirichlet", np.ones((4, 4)))          # even: not coarsenable
+    p = config_problem("c0_tiny")
+    with pytest.raises(lib.HelmError):
+        lib.helm_setup(p, {"max_levels": 1})
+    H = lib.helm_setup(p)
+    b = gpu(p.b)
+    with pytest.raises(lib.HelmError):
+        H.solve(b, x=b)                                             # aliasing
+    H.close()
