@@ -29,6 +29,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# Method of the timed workload: higher-order deflation vectors (APD, the
+# paper's wavenumber-independent variant, Table 4) with the Galerkin coarse operator E.
+DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 1000}
+
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 
 
@@ -85,6 +89,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def method_of(args):
+    return {"vectors": args.vectors, "coarse_op": args.coarse_op, "inner_tol": args.inner_tol,
+            "inner_maxit": args.inner_maxit}
+
+
+def oracle_params(args, **kw):
+    import oracle
+    m = method_of(args)
+    return oracle.SolverParams(vectors=m["vectors"], coarse_op=m["coarse_op"], inner_tol=m["inner_tol"],
+                               inner_maxit=m["inner_maxit"], **kw)
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -100,7 +116,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     p = config_problem(args.workload)
-    prm = oracle.SolverParams(coarse_op=args.coarse_op, maxit=args.ref_iters)
+    prm = oracle_params(args, maxit=args.ref_iters)
     s = oracle.Solver(p.k, p.h, p.bc, prm)
     times, iters = [], []
     for step in range(args.warmup + args.steps):
@@ -124,7 +140,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "fgmres_outer_iterations_per_s", "value": val, "unit": "it/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": args.workload, "coarse_op": args.coarse_op, "nx": p.nx, "ny": p.ny, "h": p.h,
+        "config": {"workload": args.workload, **method_of(args), "nx": p.nx, "ny": p.ny, "h": p.h,
                    "k": p.meta.get("k"), "l2": "n/a (host)"},
         "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "oracle",
                          "sample": f"first {args.ref_iters} outer FGMRES iterations of {args.workload} per step"},
@@ -140,7 +156,7 @@ def cpu_baseline_sample(args, budget_s=20.0):
     from workloads import config_problem
     p = config_problem(args.workload)
     its = 2
-    prm = oracle.SolverParams(coarse_op=args.coarse_op, maxit=its)
+    prm = oracle_params(args, maxit=its)
     s = oracle.Solver(p.k, p.h, p.bc, prm)
     t0 = time.perf_counter()
     n_done = 0
@@ -196,7 +212,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c1_k400")
-    ap.add_argument("--coarse-op", default="galerkin")
+    ap.add_argument("--coarse-op", default=DEFAULT_METHOD["coarse_op"])
+    ap.add_argument("--vectors", default=DEFAULT_METHOD["vectors"])
+    ap.add_argument("--inner-tol", type=float, default=DEFAULT_METHOD["inner_tol"])
+    ap.add_argument("--inner-maxit", type=int, default=DEFAULT_METHOD["inner_maxit"])
     ap.add_argument("--maxit", type=int, default=2000)
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -216,7 +235,7 @@ def main():
     p = config_problem(args.workload)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        H = helm.helm_setup(p, {"coarse_op": args.coarse_op}, stream=stream)
+        H = helm.helm_setup(p, method_of(args), stream=stream)
         b = torch.from_numpy(p.b).cuda()
         x = torch.empty_like(b)
         torch.cuda.synchronize()
@@ -267,7 +286,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
         "time_to_solution_s": dev_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": args.workload, "coarse_op": args.coarse_op, "nx": p.nx, "ny": p.ny, "h": p.h,
+        "config": {"workload": args.workload, **method_of(args), "nx": p.nx, "ny": p.ny, "h": p.h,
                    "k": p.meta.get("k"), "tol": 1e-6, "l2": "flushed between timed steps (256 MiB write)",
                    "outer_iterations": reps[-1]["outer_iterations"],
                    "inner_iterations_mean": reps[-1]["inner_iterations_total"] / max(1, reps[-1]["inner_solves"]),

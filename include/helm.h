@@ -35,6 +35,11 @@ extern "C" {
 #define HELM_COARSE_GALERKIN 0 /* E = I_h^{2h} A_h I_{2h}^h, stored 9-point stencil (§3.2.1, §5.2.2) */
 #define HELM_COARSE_RED_O2 1   /* second-order re-discretisation at 2h (§5.2.3) */
 #define HELM_COARSE_RED_O4 2   /* fourth-order re-discretisation, Eq. 5.11 (§5.2.3) */
+#define HELM_COARSE_RED_GLK1 3 /* ReD-Glk1, Eq. 5.12/5.14, 2nd order on two layers (§5.2.4) */
+#define HELM_COARSE_RED_GLK2 4 /* ReD-Glk2, Eq. 5.12/5.14 with ghost points (§5.2.4) */
+
+#define HELM_VECTORS_BILINEAR 0   /* A-DEF1: Z = Eq. 3.9, Z^T/4 = full weighting Eq. 3.8 */
+#define HELM_VECTORS_HIGH_ORDER 1 /* APD: Z = Eq. 3.12, Z^T = Eq. 3.14 (§3.2.1, §3.2.2) */
 
 #define HELM_OK 0
 #define HELM_EINVAL -1   /* invalid argument (shape, parameter, null pointer) */
@@ -52,7 +57,8 @@ typedef struct {
 
 /* Method parameters (§3.1, §3.2.2, §6).  helm_default_params() fills the
  * configuration of BASELINE.json configs[0]: shift (1, 0.5), omega 0.8, V(1,1),
- * Galerkin E, inner CSLP-FGMRES to 1e-1. */
+ * bilinear vectors, Galerkin E, inner CSLP-FGMRES to 1e-1 (cap 200).  inner_tol = 0 runs
+ * exactly inner_maxit inner iterations (a fixed polynomial preconditioner of E). */
 typedef struct {
   double beta1, beta2; /* CSLP shift M = -Delta - (beta1 + i beta2) k^2 (Eq. 3.1) */
   double omega;        /* damped-Jacobi relaxation (0.8, §3.1) */
@@ -63,6 +69,8 @@ typedef struct {
   int max_levels;      /* cap on multigrid levels (>= 2) */
   int restart;         /* outer FGMRES basis size; 0 = no restart (full FGMRES) */
   int max_coarsest;    /* largest coarsest grid (unknowns) solved by the dense inverse */
+  int vectors;         /* HELM_VECTORS_*; bilinear admits GALERKIN/RED_O2/RED_O4,
+                          high order admits GALERKIN/RED_GLK1/RED_GLK2 */
 } helm_params;
 
 typedef struct {
@@ -108,6 +116,10 @@ int helm_deflate(helm_ctx ctx, const double* v_dev, double* z_dev, int* inner_it
 /* Solve A x = b by A-DEF1-preconditioned FGMRES from x0 = 0 to ||b - A x||/||b|| <= tol.
  * b, x: device fields (x may not alias b).  rep may be NULL. */
 int helm_solve(helm_ctx ctx, const double* b_dev, double* x_dev, double tol, int maxit, helm_report* rep);
+/* Deflation vectors of the configured kind between level 0 and the coarse grid (level 1):
+ * coarse = R Z^T fine (R = 1/4 bilinear, 1 high order), fine = Z coarse. */
+int helm_apply_Zt(helm_ctx ctx, const double* fine_dev, double* coarse_dev);
+int helm_apply_Z(helm_ctx ctx, const double* coarse_dev, double* fine_dev);
 /* Same with host buffers: H2D copy of b, solve, D2H copy of x (end-to-end path). */
 int helm_solve_host(helm_ctx ctx, const double* b_host, double* x_host, double tol, int maxit,
                     helm_report* rep);

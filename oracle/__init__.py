@@ -30,7 +30,8 @@ from .operators import (  # noqa: F401
     apply_A,
     apply_M,
 )
-from .transfer import coarsenable, coarse_shape, coarse_k, restrict_fw, prolong_bilinear  # noqa: F401
+from .transfer import (coarsenable, coarse_shape, coarse_k, restrict_fw, prolong_bilinear,  # noqa: F401
+                       restrict_high_order, prolong_high_order)
 from .coarse import apply_coarse_E  # noqa: F401
 from .multigrid import Level, build_hierarchy, vcycle, jacobi_diagonal  # noqa: F401
 from .krylov import fgmres  # noqa: F401

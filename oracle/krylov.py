@@ -8,13 +8,21 @@ and the solution is u_k = u_0 + Z_k y_k.  The least-squares problem is solved wi
 complex Givens rotations; |g_{j+1}| is the residual norm ||b - A u_j||.
 
 Inner product (w, v) = sum conj(v) w (np.vdot(v, w)).
+
+Reading R13: Algorithm 1 writes the modified Gram-Schmidt loop.  The
+default here is classical Gram-Schmidt applied twice (CGS2): the same projection in exact
+arithmetic, and the form the GPU path uses (batched dot products).  With a loose,
+tolerance-stopped inner solve the integer inner iteration counts are decided by rounding
+(tests show MGS and CGS2 differ there), so both sides use CGS2; orth="mgs" keeps the
+literal Algorithm-1 loop, and a pin checks that the two agree when the decisions are not
+rounding-sensitive.
 """
 from __future__ import annotations
 
 import numpy as np
 
 
-def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, history=None):
+def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, history=None, orth="cgs2"):
     """Solve A x = b.  Returns (x, iterations, converged)."""
     shape = b.shape
     bvec = b.ravel()
@@ -41,9 +49,16 @@ def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, his
         z = apply_P(V[j].reshape(shape)).ravel()
         Z.append(z)
         w = apply_A(z.reshape(shape)).ravel()
-        for i in range(j + 1):                         # modified Gram-Schmidt
-            H[i, j] = np.vdot(V[i], w)
-            w = w - H[i, j] * V[i]
+        if orth == "mgs":
+            for i in range(j + 1):                     # modified Gram-Schmidt (Algorithm 1)
+                H[i, j] = np.vdot(V[i], w)
+                w = w - H[i, j] * V[i]
+        else:
+            for _ in range(2):                         # classical Gram-Schmidt, twice (CGS2)
+                hp = np.array([np.vdot(V[i], w) for i in range(j + 1)])
+                for i in range(j + 1):
+                    w = w - hp[i] * V[i]
+                H[:j + 1, j] += hp
         H[j + 1, j] = np.linalg.norm(w)
         for i in range(j):                             # previous rotations
             t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]

@@ -17,6 +17,10 @@ Readings:
       of the CSLP hierarchy (mesh 2h); inner_solver="direct" replaces it by a dense solve.
   R12 Outer FGMRES from u0 = 0 stops at ||b - A u||/||b|| <= tol (right preconditioning:
       the Arnoldi residual is the true residual).
+  R15 inner_tol = 0 runs exactly inner_maxit inner iterations (a fixed polynomial
+      preconditioner of E), the rounding-insensitive alternative to the tolerance stop.
+  APD (vectors="high_order", §3.2.2 "When the higher-order deflation vector is employed, it
+      will be denoted as Adapted Preconditioned Deflation"): Z = Eq. 3.12, Z^T = Eq. 3.14.
 """
 from __future__ import annotations
 
@@ -30,7 +34,7 @@ from .coarse import apply_coarse_E
 from .krylov import fgmres
 from .multigrid import build_hierarchy, vcycle
 from .operators import apply_A
-from .transfer import coarse_shape, prolong_bilinear, restrict_fw
+from .transfer import coarse_shape, prolong_bilinear, prolong_high_order, restrict_fw, restrict_high_order
 
 
 @dataclasses.dataclass
@@ -39,10 +43,12 @@ class SolverParams:
     omega: float = 0.8
     nu_pre: int = 1
     nu_post: int = 1
-    coarse_op: str = "galerkin"       # galerkin | red_o2 | red_o4
+    vectors: str = "bilinear"         # bilinear (A-DEF1) | high_order (APD)
+    coarse_op: str = "galerkin"       # galerkin | red_o2 | red_o4 (bilinear); galerkin | red_glk1 | red_glk2 (high_order)
     inner_solver: str = "fgmres"      # fgmres | direct
-    inner_tol: float = 1e-1
+    inner_tol: float = 1e-1           # 0 -> fixed inner_maxit iterations (reading R15)
     inner_maxit: int = 200
+    orth: str = "cgs2"                # cgs2 | mgs (reading R13)
     tol: float = 1e-6
     maxit: int = 600
     max_levels: int = 64
@@ -67,7 +73,15 @@ class Solver:
         return apply_A(u, self.k, self.h, self.bc)
 
     def E(self, x):
-        return apply_coarse_E(x, self.k, self.h, self.bc, self.p.coarse_op)
+        return apply_coarse_E(x, self.k, self.h, self.bc, self.p.coarse_op, self.p.vectors)
+
+    def Zt(self, v):
+        return restrict_fw(v, self.bc) if self.p.vectors == "bilinear" else restrict_high_order(v, self.bc)
+
+    def Zp(self, e):
+        if self.p.vectors == "bilinear":
+            return prolong_bilinear(e, self.k.shape, self.bc)
+        return prolong_high_order(e, self.k.shape, self.bc)
 
     def vcycle(self, f, level=0):
         return vcycle(self.levels, f, level, self.p.omega, self.p.nu_pre, self.p.nu_post)
@@ -89,15 +103,16 @@ class Solver:
             if self._Elu is None:
                 self._Elu = scipy.linalg.lu_factor(self.E_dense())
             return scipy.linalg.lu_solve(self._Elu, c.ravel()).reshape(self.cshape)
-        e, its, _ = fgmres(self.E, lambda v: self.vcycle(v, 1), c, self.p.inner_tol, self.p.inner_maxit)
+        e, its, _ = fgmres(self.E, lambda v: self.vcycle(v, 1), c, self.p.inner_tol, self.p.inner_maxit,
+                           orth=self.p.orth)
         self.inner_its.append(its)
         return e
 
     def Q(self, v):
         """Q_h v = I_{2h}^h A_{2h}^{-1} I_h^{2h} v (Eq. 5.3-5.5)."""
-        v1 = restrict_fw(v, self.bc)
+        v1 = self.Zt(v)
         v2 = self.coarse_solve(v1)
-        return prolong_bilinear(v2, self.k.shape, self.bc)
+        return self.Zp(v2)
 
     def adef1(self, v):
         """P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v (Eq. 3.21)."""
@@ -110,7 +125,7 @@ class Solver:
         self.inner_its = []
         t0 = time.perf_counter()
         x, its, conv = fgmres(self.A, self.adef1, np.asarray(b, dtype=np.complex128),
-                              self.p.tol, self.p.maxit, history=history)
+                              self.p.tol, self.p.maxit, history=history, orth=self.p.orth)
         t1 = time.perf_counter()
         r = np.asarray(b) - self.A(x)
         relres = np.linalg.norm(r) / np.linalg.norm(b) if np.linalg.norm(b) > 0 else 0.0

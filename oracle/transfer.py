@@ -76,3 +76,48 @@ def prolong_bilinear(e: np.ndarray, fine_shape, bc: str) -> np.ndarray:
             c0 = o + 1 + a
             fp[r0:r0 + 2 * nyc:2, c0:c0 + 2 * nxc:2] += w[a] * w[b] * e
     return fp[1:-1, 1:-1].copy()
+
+
+# ---------------------------------------------------------------------------------------
+# Higher-order deflation vectors (APD, Dwarka & Vuik): PAPER.md Eq. 3.11a/b (1D), Eq. 3.12
+# (2D matrix-free prolongation, four point classes), Eq. 3.13 (stencil
+# 1/64 [1 4 6 4 1] (x) [1 4 6 4 1]), Eq. 3.14/3.15 (restriction with the same stencil).
+# The restriction's weights sum to 4 (= 256/64): it is exactly Z_ho^T (not Z^T/4).
+# Reading R4 applies: taps outside the unknown array are dropped.
+# ---------------------------------------------------------------------------------------
+def _ho_weights_1d(d):
+    """Weight of coarse node c at fine node 2c + d (Eq. 3.11a read as a column of Z)."""
+    return {0: 6.0 / 8.0, 1: 0.5, -1: 0.5, 2: 1.0 / 8.0, -2: 1.0 / 8.0}.get(d, 0.0)
+
+
+def prolong_high_order(e: np.ndarray, fine_shape, bc: str) -> np.ndarray:
+    """Eq. 3.12: coincident fine nodes get (1/64)(36 c + 6 (edge nbrs) + 1 (corner nbrs)),
+    x-midpoints (1/16)(6,6 / 1,1 / 1,1), y-midpoints likewise, cell centres (1/4) x 4 —
+    i.e. the tensor product of Eq. 3.11a, applied here as a scatter of the 1/64-stencil."""
+    o = unknown_offset(bc)
+    ny, nx = fine_shape
+    nyc, nxc = coarse_shape(fine_shape, bc)
+    fp = np.zeros((ny + 4, nx + 4), dtype=np.complex128)
+    for b in range(-2, 3):
+        for a in range(-2, 3):
+            r0 = o + 2 + b
+            c0 = o + 2 + a
+            fp[r0:r0 + 2 * nyc:2, c0:c0 + 2 * nxc:2] += _ho_weights_1d(a) * _ho_weights_1d(b) * e
+    return fp[2:-2, 2:-2].copy()
+
+
+def restrict_high_order(v: np.ndarray, bc: str) -> np.ndarray:
+    """Eq. 3.14: 25-tap gather (1/64)[1 4 6 4 1] (x) [1 4 6 4 1] around fine node (2I+o, 2J+o)."""
+    o = unknown_offset(bc)
+    ny, nx = v.shape
+    nyc, nxc = coarse_shape(v.shape, bc)
+    w1 = {-2: 1.0, -1: 4.0, 0: 6.0, 1: 4.0, 2: 1.0}
+    vp = np.zeros((ny + 4, nx + 4), dtype=np.complex128)
+    vp[2:-2, 2:-2] = v
+    out = np.zeros((nyc, nxc), dtype=np.complex128)
+    for b in range(-2, 3):
+        for a in range(-2, 3):
+            r0 = o + 2 + b
+            c0 = o + 2 + a
+            out += (w1[a] * w1[b] / 64.0) * vp[r0:r0 + 2 * nyc:2, c0:c0 + 2 * nxc:2]
+    return out

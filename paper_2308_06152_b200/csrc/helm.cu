@@ -141,13 +141,48 @@ int prolong_(helm_ctx_s& C, int l, const double2* e, const double2* base, double
   return post_launch(C);
 }
 
+// Deflation vectors level 0 <-> level 1 (bilinear: R=1, high order: R=2)
+int defl_restrict(helm_ctx_s& C, const double2* v, double2* vc) {
+  const Level& F = C.L[0];
+  const Level& G = C.L[1];
+  if (C.p.vectors == HELM_VECTORS_BILINEAR)
+    k_restrict_z<1><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, v, vc);
+  else
+    k_restrict_z<2><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, v, vc);
+  return post_launch(C);
+}
+
+int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
+  const Level& F = C.L[0];
+  const Level& G = C.L[1];
+  if (C.p.vectors == HELM_VECTORS_BILINEAR)
+    k_prolong_z<1, 0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y);
+  else
+    k_prolong_z<2, 0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y);
+  return post_launch(C);
+}
+
 // y = E x (f == null) or y = f - E x on level 1
 int apply_E(helm_ctx_s& C, const double2* x, const double2* f, double2* y) {
   const Level& G = C.L[1];
+  const dim3 gg = grd2d(G.g.nx, G.g.ny);
   switch (C.p.coarse_op) {
     case HELM_COARSE_GALERKIN:
-      if (f) k_apply_9pt<1><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(G.g, C.gal, x, f, y);
-      else k_apply_9pt<0><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(G.g, C.gal, x, nullptr, y);
+      if (C.p.vectors == HELM_VECTORS_BILINEAR) {
+        if (f) k_apply_stencil<1, 1><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, f, y);
+        else k_apply_stencil<1, 0><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, nullptr, y);
+      } else {
+        if (f) k_apply_stencil<2, 1><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, f, y);
+        else k_apply_stencil<2, 0><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, nullptr, y);
+      }
+      return post_launch(C);
+    case HELM_COARSE_RED_GLK1:
+      if (f) k_apply_red_glk<1, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_glk<1, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, nullptr, y, G.k);
+      return post_launch(C);
+    case HELM_COARSE_RED_GLK2:
+      if (f) k_apply_red_glk<2, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_glk<2, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, nullptr, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_O2:
       return op_apply(C, G, x, f, y, 1.0, 0.0);
@@ -383,12 +418,12 @@ int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, int* its) {
 // z = P_{A-DEF1} v (Eq. 3.21 / 5.2-5.5)
 int adef1(helm_ctx_s& C, const double2* v, double2* z, int* inner_its) {
   Level& F = C.L[0];
-  CKR(restrict_(C, 0, v, C.cc));                          // v1 = I_h^{2h} v
+  CKR(defl_restrict(C, v, C.cc));                         // v1 = I_h^{2h} v
   int its = 0;
   CKR(coarse_solve(C, C.cc, C.ce, &its));                 // v2 = A_{2h}^{-1} v1
   C.last_inner = its;
   if (inner_its) *inner_its = its;
-  CKR(prolong_(C, 0, C.ce, nullptr, C.dq));               // v' = I_{2h}^h v2  (= Q v)
+  CKR(defl_prolong(C, C.ce, C.dq));                       // v' = I_{2h}^h v2  (= Q v)
   CKR(op_apply(C, F, C.dq, v, C.dt, 1.0, 0.0));           // t = v - A Q v  (= P_h v)
   return vcycle(C, 0, C.dt, z, C.dq);                     // z = M^{-1} t + Q v
 }
@@ -411,6 +446,7 @@ void helm_default_params(helm_params* p) {
   p->max_levels = 64;
   p->restart = 0;
   p->max_coarsest = 4096;
+  p->vectors = HELM_VECTORS_BILINEAR;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -453,6 +489,16 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.max_levels < 2) return fail(HELM_EINVAL, "max_levels must be >= 2");
   if (p.nu_pre < 1 || p.nu_post < 0) return fail(HELM_EINVAL, "nu_pre >= 1, nu_post >= 0");
   if (p.inner_maxit < 1) return fail(HELM_EINVAL, "inner_maxit >= 1");
+  if (p.vectors == HELM_VECTORS_BILINEAR) {
+    if (p.coarse_op != HELM_COARSE_GALERKIN && p.coarse_op != HELM_COARSE_RED_O2 && p.coarse_op != HELM_COARSE_RED_O4)
+      return fail(HELM_EINVAL, "coarse_op %d not defined for bilinear vectors", p.coarse_op);
+  } else if (p.vectors == HELM_VECTORS_HIGH_ORDER) {
+    if (p.coarse_op != HELM_COARSE_GALERKIN && p.coarse_op != HELM_COARSE_RED_GLK1 &&
+        p.coarse_op != HELM_COARSE_RED_GLK2)
+      return fail(HELM_EINVAL, "coarse_op %d not defined for high-order vectors", p.coarse_op);
+  } else {
+    return fail(HELM_EINVAL, "bad vectors %d", p.vectors);
+  }
   int dev;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&C.sm_count, cudaDevAttrMultiProcessorCount, dev));
@@ -536,17 +582,27 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.coarse_op == HELM_COARSE_GALERKIN) {
     const Level& F = C.L[0];
     const Level& G = C.L[1];
-    CKR(dalloc(&C.gal, 9 * G.n));
-    k_galerkin_coef<<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, C.gal);
+    if (p.vectors == HELM_VECTORS_BILINEAR) {
+      CKR(dalloc(&C.gal, 9 * G.n));
+      k_galerkin_coef<1><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, C.gal);
+    } else {
+      CKR(dalloc(&C.gal, 25 * G.n));
+      k_galerkin_coef<2><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, C.gal);
+    }
     CKR(post_launch(C));
-  } else if (p.coarse_op != HELM_COARSE_RED_O2 && p.coarse_op != HELM_COARSE_RED_O4) {
-    return fail(HELM_EINVAL, "bad coarse_op %d", p.coarse_op);
   }
   CKR(dalloc(&C.dq, C.L[0].n));
   CKR(dalloc(&C.dt, C.L[0].n));
   CKR(dalloc(&C.cc, C.L[1].n));
   CKR(dalloc(&C.ce, C.L[1].n));
-  CKR(krylov_alloc(C.inner, p.inner_maxit, C.L[1].n));
+  {
+    // inner basis capacity: inner_maxit, limited to a quarter of free HBM (restarted beyond)
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t per = 2 * C.L[1].n * sizeof(double2);
+    const int cap = (int)std::max<size_t>(8, std::min<size_t>((size_t)p.inner_maxit, fr / 4 / per));
+    CKR(krylov_alloc(C.inner, cap, C.L[1].n));
+  }
   CK(cudaStreamSynchronize(C.s));
   return HELM_OK;
 }
@@ -598,6 +654,16 @@ int helm_prolong(helm_ctx C, int level, const double* e, double* v) {
   return prolong_(*C, level, (const double2*)e, nullptr, (double2*)v);
 }
 
+int helm_apply_Zt(helm_ctx C, const double* v, double* vc) {
+  if (!C || !v || !vc) return fail(HELM_EINVAL, "null argument");
+  return defl_restrict(*C, (const double2*)v, (double2*)vc);
+}
+
+int helm_apply_Z(helm_ctx C, const double* e, double* v) {
+  if (!C || !v || !e) return fail(HELM_EINVAL, "null argument");
+  return defl_prolong(*C, (const double2*)e, (double2*)v);
+}
+
 int helm_apply_E(helm_ctx C, const double* x, double* y) {
   if (!C || !x || !y) return fail(HELM_EINVAL, "null argument");
   return apply_E(*C, (const double2*)x, nullptr, (double2*)y);
@@ -619,9 +685,13 @@ int helm_solve(helm_ctx C, const double* b, double* x, double tol, int maxit, he
   if (!C || !b || !x) return fail(HELM_EINVAL, "null argument");
   if (b == x) return fail(HELM_EINVAL, "x may not alias b");
   if (maxit < 1 || !(tol > 0)) return fail(HELM_EINVAL, "bad tol/maxit");
-  const int m = C->p.restart > 0 ? std::min(C->p.restart, maxit) : maxit;
-  if (C->outer.m != m) {
-    krylov_free(C->outer);
+  int m = C->p.restart > 0 ? std::min(C->p.restart, maxit) : maxit;
+  if (C->outer.m < m || (C->outer.m > m && C->p.restart > 0)) {
+    size_t fr = 0, tot = 0;
+    if (C->outer.V) krylov_free(C->outer);
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t per = 2 * C->L[0].n * sizeof(double2);
+    m = (int)std::max<size_t>(8, std::min<size_t>((size_t)m, fr / 2 / per));
     CKR(krylov_alloc(C->outer, m, C->L[0].n));
   }
   long long inner_total = 0;

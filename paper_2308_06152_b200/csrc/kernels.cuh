@@ -176,28 +176,87 @@ __global__ void k_sample_k(Geo gf, Geo gc, int o, const double* __restrict__ kf,
   kc[(size_t)J * gc.nx + I] = kf[(size_t)(2 * J + o) * gf.nx + (2 * I + o)];
 }
 
-// ------------------------------------------------------------------ Galerkin coarse stencil
-// E = R A P (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; §5.2.2 stencil operation):
-// its 9 coefficients per coarse node, evaluated once from the definition
-//   E[(I,J),(I+dx,J+dy)] = sum_a R[(I,J),a] sum_{b in nbr(a)} A[a,b] P[b,(I+dx,J+dy)]
-// and stored SoA: coef[d*nc + p], d = (dy+1)*3 + (dx+1).
-__global__ void k_galerkin_coef(Geo gf, Geo gc, int o, const double* __restrict__ kf, double2* __restrict__ coef) {
+// ------------------------------------------------------------------ deflation vectors Z, Z^T
+// 1D weight of coarse node c at fine node 2c + o + d (a column of Z):
+//   bilinear (R = 1): Eq. 3.6/3.9      w(0) = 1,   w(+-1) = 1/2
+//   high order (R = 2): Eq. 3.11a/3.12 w(0) = 3/4, w(+-1) = 1/2, w(+-2) = 1/8
+// Restriction = RS * Z^T: RS = 1/4 (full weighting, Eq. 3.8), RS = 1 (Eq. 3.14).
+template <int R>
+__device__ __forceinline__ double zw(int d) {
+  if (R == 1) return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 : 0.0);
+  return d == 0 ? 0.75 : ((d == 1 || d == -1) ? 0.5 : ((d == 2 || d == -2) ? 0.125 : 0.0));
+}
+template <int R>
+__device__ __forceinline__ double zrs() { return R == 1 ? 0.25 : 1.0; }
+
+// vc = RS * Z^T v  (gather of the (2R+1)^2 fine taps; out-of-array taps dropped, reading R4)
+template <int R>
+__global__ void k_restrict_z(Geo gf, Geo gc, int o, const double2* __restrict__ v, double2* __restrict__ vc) {
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   if (I >= gc.nx || J >= gc.ny) return;
-  double2 acc[9];
-#pragma unroll
-  for (int d = 0; d < 9; ++d) acc[d] = make_double2(0.0, 0.0);
   const int ci = 2 * I + o, cj = 2 * J + o;
-  for (int b = -1; b <= 1; ++b) {
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int b = -R; b <= R; ++b) {
+    const int jj = cj + b;
+    if (jj < 0 || jj >= gf.ny) continue;
+    const double wy = zw<R>(b);
+#pragma unroll
+    for (int a = -R; a <= R; ++a) {
+      const int ii = ci + a;
+      if (ii < 0 || ii >= gf.nx) continue;
+      s = cadd(s, cscale(wy * zw<R>(a), v[(size_t)jj * gf.nx + ii]));
+    }
+  }
+  vc[(size_t)J * gc.nx + I] = cscale(zrs<R>(), s);
+}
+
+// y = Z e (MODE 0) or y = base + Z e (MODE 1), gather at each fine node.
+template <int R, int MODE>
+__global__ void k_prolong_z(Geo gf, Geo gc, int o, const double2* __restrict__ e, const double2* __restrict__ base,
+                            double2* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= gf.nx || j >= gf.ny) return;
+  const int ri = i - o, rj = j - o;
+  // coarse nodes c with |ri - 2c| <= R  ->  c in [ceil((ri-R)/2), floor((ri+R)/2)]
+  const int clo = (ri - R + 1 + 2 * 64) / 2 - 64, chi = (ri + R + 2 * 64) / 2 - 64;
+  const int rlo = (rj - R + 1 + 2 * 64) / 2 - 64, rhi = (rj + R + 2 * 64) / 2 - 64;
+  double2 s = make_double2(0.0, 0.0);
+  for (int J = max(rlo, 0); J <= min(rhi, gc.ny - 1); ++J) {
+    const double wy = zw<R>(rj - 2 * J);
+    for (int I = max(clo, 0); I <= min(chi, gc.nx - 1); ++I)
+      s = cadd(s, cscale(wy * zw<R>(ri - 2 * I), e[(size_t)J * gc.nx + I]));
+  }
+  const size_t p = (size_t)j * gf.nx + i;
+  if (MODE == 1) s = cadd(s, base[p]);
+  y[p] = s;
+}
+
+// ------------------------------------------------------------------ Galerkin coarse stencil
+// E = (RS Z^T) A Z (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; §5.2.2 stencil
+// operation): its (2R+1)^2 coefficients per coarse node, evaluated once from the definition
+//   E[(I,J),(I+dx,J+dy)] = sum_a RS Z[a,(I,J)] sum_{b in nbr(a)} A[a,b] Z[b,(I+dx,J+dy)]
+// and stored SoA: coef[d*nc + p], d = (dy+R)*(2R+1) + (dx+R).
+template <int R>
+__global__ void k_galerkin_coef(Geo gf, Geo gc, int o, const double* __restrict__ kf, double2* __restrict__ coef) {
+  constexpr int W = 2 * R + 1;
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y * blockDim.y + threadIdx.y;
+  if (I >= gc.nx || J >= gc.ny) return;
+  double2 acc[W * W];
+#pragma unroll
+  for (int d = 0; d < W * W; ++d) acc[d] = make_double2(0.0, 0.0);
+  const int ci = 2 * I + o, cj = 2 * J + o;
+  for (int b = -R; b <= R; ++b) {
     const int aj = cj + b;
     if (aj < 0 || aj >= gf.ny) continue;
-    for (int a = -1; a <= 1; ++a) {
+    for (int a = -R; a <= R; ++a) {
       const int ai = ci + a;
       if (ai < 0 || ai >= gf.nx) continue;
-      const double rw = (a == 0 ? 2.0 : 1.0) * (b == 0 ? 2.0 : 1.0) * (1.0 / 16.0);
+      const double rw = zrs<R>() * zw<R>(a) * zw<R>(b);
       Coef c = coef_at(gf, ai, aj, kf[(size_t)aj * gf.nx + ai], 1.0, 0.0);
-      // the 5 fine neighbours b of a with A[a,b]
       const int bi[5] = {ai, ai - 1, ai + 1, ai, ai};
       const int bjv[5] = {aj, aj, aj, aj - 1, aj + 1};
       const double2 aval[5] = {c.ap, make_double2(c.aw, 0), make_double2(c.ae, 0), make_double2(c.as, 0),
@@ -206,20 +265,19 @@ __global__ void k_galerkin_coef(Geo gf, Geo gc, int o, const double* __restrict_
         if (q > 0 && aval[q].x == 0.0) continue;
         const int xi = bi[q], yj = bjv[q];
         if (xi < 0 || xi >= gf.nx || yj < 0 || yj >= gf.ny) continue;
-        // P[b, (I', J')] nonzero for coarse nodes within distance 1 of b in node units
-        for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+        for (int dy = -R; dy <= R; ++dy) {
           const int Jp = J + dy;
           if (Jp < 0 || Jp >= gc.ny) continue;
-          const int ddy = yj - (2 * Jp + o);
-          if (ddy < -1 || ddy > 1) continue;
-          const double wy = ddy == 0 ? 1.0 : 0.5;
-          for (int dx = -1; dx <= 1; ++dx) {
+          const double wy = zw<R>(yj - (2 * Jp + o));
+          if (wy == 0.0) continue;
+#pragma unroll
+          for (int dx = -R; dx <= R; ++dx) {
             const int Ip = I + dx;
             if (Ip < 0 || Ip >= gc.nx) continue;
-            const int ddx = xi - (2 * Ip + o);
-            if (ddx < -1 || ddx > 1) continue;
-            const double wx = ddx == 0 ? 1.0 : 0.5;
-            const int d = (dy + 1) * 3 + (dx + 1);
+            const double wx = zw<R>(xi - (2 * Ip + o));
+            if (wx == 0.0) continue;
+            const int d = (dy + R) * W + (dx + R);
             acc[d] = cadd(acc[d], cscale(rw * wx * wy, aval[q]));
           }
         }
@@ -229,13 +287,14 @@ __global__ void k_galerkin_coef(Geo gf, Geo gc, int o, const double* __restrict_
   const size_t nc = (size_t)gc.nx * gc.ny;
   const size_t p = (size_t)J * gc.nx + I;
 #pragma unroll
-  for (int d = 0; d < 9; ++d) coef[d * nc + p] = acc[d];
+  for (int d = 0; d < W * W; ++d) coef[d * nc + p] = acc[d];
 }
 
-// y = E x with the stored 9-point Galerkin stencil (MODE 1: y = f - E x).
-template <int MODE>
-__global__ void k_apply_9pt(Geo gc, const double2* __restrict__ coef, const double2* __restrict__ x,
-                            const double2* __restrict__ f, double2* __restrict__ y) {
+// y = E x with a stored (2R+1)^2-point stencil (MODE 1: y = f - E x).
+template <int R, int MODE>
+__global__ void k_apply_stencil(Geo gc, const double2* __restrict__ coef, const double2* __restrict__ x,
+                                const double2* __restrict__ f, double2* __restrict__ y) {
+  constexpr int W = 2 * R + 1;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   if (I >= gc.nx || J >= gc.ny) return;
@@ -243,19 +302,102 @@ __global__ void k_apply_9pt(Geo gc, const double2* __restrict__ coef, const doub
   const size_t p = (size_t)J * gc.nx + I;
   double2 s = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int dy = -1; dy <= 1; ++dy) {
+  for (int dy = -R; dy <= R; ++dy) {
     const int Jp = J + dy;
     if (Jp < 0 || Jp >= gc.ny) continue;
 #pragma unroll
-    for (int dx = -1; dx <= 1; ++dx) {
+    for (int dx = -R; dx <= R; ++dx) {
       const int Ip = I + dx;
       if (Ip < 0 || Ip >= gc.nx) continue;
-      const int d = (dy + 1) * 3 + (dx + 1);
+      const int d = (dy + R) * W + (dx + R);
       s = cfma(coef[d * nc + p], x[(size_t)Jp * gc.nx + Ip], s);
     }
   }
   if (MODE == 1) s = csub(f[p], s);
   y[p] = s;
+}
+
+// ------------------------------------------------------------------ ReD-Glk (§5.2.4)
+// Printed stencils: Laplacian part Eq. 5.12 (x 1/(256 H^2)) and wavenumber part Eq. 5.14
+// (x 1/64^2), each tap weighted by the wavenumber at its own coarse node.
+__constant__ double c_glk_lap[25] = {-3, -44, -98, -44, -3, -44, -112, 56, -112, -44, -98, 56, 980,
+                                     56, -98, -44, -112, 56, -112, -44, -3, -44, -98, -44, -3};
+__constant__ double c_glk_mass[25] = {1, 28, 70, 28, 1, 28, 784, 1960, 784, 28, 70, 1960, 4900,
+                                      1960, 70, 28, 784, 1960, 784, 28, 1, 28, 70, 28, 1};
+
+// Value of the coarse field at (ii, jj) possibly outside the unknown array (ReD-Glk2 ghosts):
+// Dirichlet: boundary node (index -1 / n) holds 0, ghost beyond it mirrors with a sign
+// (Eq. 5.18: u_b = (u_ghost + u_in)/2, u_b = 0); Sommerfeld: ghost one layer out from the
+// boundary node by Eq. 2.8 (u_g = u_in + 2 i H k_b u_b), per direction.
+__device__ double2 glk2_val(const Geo& g, const double2* __restrict__ x, const double* __restrict__ k, int ii, int jj) {
+  if (g.bc == BC_DIRICHLET) {
+    double sgn = 1.0;
+    for (int it = 0; it < 2; ++it) {
+      if (ii == -1 || ii == g.nx || jj == -1 || jj == g.ny) return make_double2(0.0, 0.0);
+      if (ii == -2) { ii = 0; sgn = -sgn; }
+      else if (ii == g.nx + 1) { ii = g.nx - 1; sgn = -sgn; }
+      else if (jj == -2) { jj = 0; sgn = -sgn; }
+      else if (jj == g.ny + 1) { jj = g.ny - 1; sgn = -sgn; }
+    }
+    if (ii < 0 || ii >= g.nx || jj < 0 || jj >= g.ny) return make_double2(0.0, 0.0);
+    return cscale(sgn, x[(size_t)jj * g.nx + ii]);
+  }
+  // Sommerfeld
+  auto colv = [&](int ci, int row) -> double2 {   // value at column ci in [-1, nx], row in range
+    if (ci == -1) {
+      const size_t q = (size_t)row * g.nx;
+      return cfma(make_double2(0.0, 2.0 * g.h * k[q]), x[q], x[q + 1]);
+    }
+    if (ci == g.nx) {
+      const size_t q = (size_t)row * g.nx + g.nx - 1;
+      return cfma(make_double2(0.0, 2.0 * g.h * k[q]), x[q], x[q - 1]);
+    }
+    return x[(size_t)row * g.nx + ci];
+  };
+  if (ii < -1 || ii > g.nx || jj < -1 || jj > g.ny) return make_double2(0.0, 0.0);
+  if (jj == -1 || jj == g.ny) {
+    const int r0 = (jj == -1) ? 0 : g.ny - 1, r1 = (jj == -1) ? 1 : g.ny - 2;
+    const int ic = ii < 0 ? 0 : (ii >= g.nx ? g.nx - 1 : ii);
+    const double kb = k[(size_t)r0 * g.nx + ic];
+    return cfma(make_double2(0.0, 2.0 * g.h * kb), colv(ii, r0), colv(ii, r1));
+  }
+  return colv(ii, jj);
+}
+
+// VARIANT 1: ReD-Glk1, VARIANT 2: ReD-Glk2 (reading R14: second-order rows scaled by 4).
+template <int VARIANT, int MODE>
+__global__ void k_apply_red_glk(Geo g, const double2* __restrict__ x, const double2* __restrict__ f,
+                                double2* __restrict__ y, const double* __restrict__ k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const size_t p = (size_t)j * g.nx + i;
+  bool use5;
+  if (VARIANT == 1) use5 = (i >= 2 && i <= g.nx - 3 && j >= 2 && j <= g.ny - 3);
+  else if (g.bc == BC_DIRICHLET) use5 = true;
+  else use5 = (i >= 1 && i <= g.nx - 2 && j >= 1 && j <= g.ny - 2);
+  double2 v;
+  if (use5) {
+    const double iH2 = 1.0 / (256.0 * g.h * g.h), im = 1.0 / 4096.0;
+    v = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int b = -2; b <= 2; ++b)
+#pragma unroll
+      for (int a = -2; a <= 2; ++a) {
+        const int ii = i + a, jj = j + b;
+        const bool in = (ii >= 0 && ii < g.nx && jj >= 0 && jj < g.ny);
+        const double kk = in ? k[(size_t)jj * g.nx + ii] : 0.0;     // ghost wavenumber 0 (§5.2.4)
+        const double2 xv = in ? x[(size_t)jj * g.nx + ii] : glk2_val(g, x, k, ii, jj);
+        const int d = (b + 2) * 5 + (a + 2);
+        const double c = c_glk_lap[d] * iH2 - c_glk_mass[d] * im * kk * kk;
+        v = cadd(v, cscale(c, xv));
+      }
+  } else {
+    Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
+    v = cscale(4.0, stencil_apply(g, x, i, j, c));
+  }
+  if (MODE == 1) v = csub(f[p], v);
+  y[p] = v;
 }
 
 // ReD-O4 (Eq. 5.11, reading R5: centre 5/H^2 - k^2) where the 5-wide cross fits,

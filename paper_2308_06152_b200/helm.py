@@ -16,7 +16,8 @@ _LIB_PATH = os.path.join(_HERE, "libhelm.so")
 
 HELM_BC_DIRICHLET = 0
 HELM_BC_SOMMERFELD = 1
-COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2}
+COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2, "red_glk1": 3, "red_glk2": 4}
+VECTORS = {"bilinear": 0, "high_order": 1}
 BCS = {"dirichlet": HELM_BC_DIRICHLET, "sommerfeld": HELM_BC_SOMMERFELD}
 
 
@@ -28,7 +29,7 @@ class helm_params(ctypes.Structure):
     _fields_ = [("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("omega", ctypes.c_double),
                 ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("coarse_op", ctypes.c_int),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int), ("max_levels", ctypes.c_int),
-                ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int)]
+                ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int)]
 
 
 class helm_report(ctypes.Structure):
@@ -54,6 +55,8 @@ EXPORTS = {
     "helm_restrict": (_I, [_P, _I, _P, _P]),
     "helm_prolong": (_I, [_P, _I, _P, _P]),
     "helm_apply_E": (_I, [_P, _P, _P]),
+    "helm_apply_Zt": (_I, [_P, _P, _P]),
+    "helm_apply_Z": (_I, [_P, _P, _P]),
     "helm_vcycle": (_I, [_P, _I, _P, _P]),
     "helm_deflate": (_I, [_P, _P, _P, ctypes.POINTER(_I)]),
     "helm_solve": (_I, [_P, _P, _P, _D, _I, ctypes.POINTER(helm_report)]),
@@ -99,6 +102,8 @@ def default_params(**overrides) -> helm_params:
     for key, val in overrides.items():
         if key == "coarse_op" and isinstance(val, str):
             val = COARSE_OPS[val]
+        if key == "vectors" and isinstance(val, str):
+            val = VECTORS[val]
         if key == "beta":
             p.beta1, p.beta2 = val
             continue
@@ -179,6 +184,18 @@ class Helm:
         _check(self.lib.helm_prolong(self.ctx, level, _ptr(e), _ptr(y)))
         return y
 
+    def helm_apply_Zt(self, v):
+        v = self._in(v, 0)
+        y = self.field(1)
+        _check(self.lib.helm_apply_Zt(self.ctx, _ptr(v), _ptr(y)))
+        return y
+
+    def helm_apply_Z(self, e):
+        e = self._in(e, 1)
+        y = self.field(0)
+        _check(self.lib.helm_apply_Z(self.ctx, _ptr(e), _ptr(y)))
+        return y
+
     def helm_apply_E(self, x):
         x = self._in(x, 1)
         y = self.field(1)
@@ -226,6 +243,8 @@ class Helm:
     restrict = helm_restrict
     prolong = helm_prolong
     apply_E = helm_apply_E
+    apply_Z = helm_apply_Z
+    apply_Zt = helm_apply_Zt
     vcycle = helm_vcycle
     deflate = helm_deflate
     solve = helm_solve

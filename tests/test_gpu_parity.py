@@ -84,14 +84,25 @@ def test_transfers(case):
         assert rel(H.prolong(l, gpu(e)).cpu().numpy(), oracle.prolong_bilinear(e, levels[l].shape, p.bc)) < 1e-14
 
 
-@pytest.mark.parametrize("op", ["galerkin", "red_o2", "red_o4"])
-def test_coarse_operator(lib, op):
+VARIANTS = [("bilinear", "galerkin"), ("bilinear", "red_o2"), ("bilinear", "red_o4"),
+            ("high_order", "galerkin"), ("high_order", "red_glk1"), ("high_order", "red_glk2")]
+
+
+@pytest.mark.parametrize("vec,op", VARIANTS)
+def test_coarse_operator_and_vectors(lib, vec, op):
     for p in GRIDS:
-        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"coarse_op": op})
-        x = random_field(H.levels[1][:2], 5)
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"coarse_op": op, "vectors": vec})
+        cs = H.levels[1][:2]
+        x = random_field(cs, 5)
         y = H.apply_E(gpu(x)).cpu().numpy()
-        yo = oracle.apply_coarse_E(x, p.k, p.h, p.bc, op)
-        assert rel(y, yo) < OP_TOL, (op, p.shape, p.bc)
+        yo = oracle.apply_coarse_E(x, p.k, p.h, p.bc, op, vec)
+        assert rel(y, yo) < OP_TOL, (vec, op, p.shape, p.bc)
+        v = random_field(p.shape, 6)
+        zt = oracle.restrict_fw(v, p.bc) if vec == "bilinear" else oracle.restrict_high_order(v, p.bc)
+        assert rel(H.apply_Zt(gpu(v)).cpu().numpy(), zt) < 1e-14
+        z = oracle.prolong_bilinear(x, p.shape, p.bc) if vec == "bilinear" else \
+            oracle.prolong_high_order(x, p.shape, p.bc)
+        assert rel(H.apply_Z(gpu(x)).cpu().numpy(), z) < 1e-14
         H.close()
 
 
@@ -104,14 +115,16 @@ def test_vcycle(case):
         assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11
 
 
-@pytest.mark.parametrize("op", ["galerkin", "red_o4"])
-def test_deflate(lib, op):
+@pytest.mark.parametrize("vec,op", [("bilinear", "galerkin"), ("bilinear", "red_o4"), ("high_order", "galerkin"),
+                                    ("high_order", "red_glk2")])
+def test_deflate(lib, vec, op):
     """z = P_{A-DEF1} v with the inner coarse solve at a tight tolerance (1e-10), so both
     sides run to the same well-defined E^{-1} c."""
     for p in GRIDS[:3]:
-        prm = {"coarse_op": op, "inner_tol": 1e-10, "inner_maxit": 400}
+        prm = {"coarse_op": op, "inner_tol": 1e-10, "inner_maxit": 400, "vectors": vec}
         H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, prm)
-        s = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, inner_tol=1e-10, inner_maxit=400))
+        s = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, inner_tol=1e-10, inner_maxit=400,
+                                                              vectors=vec))
         v = random_field(p.shape, 7)
         z, its = H.deflate(gpu(v))
         zo = s.adef1(v)
@@ -120,11 +133,19 @@ def test_deflate(lib, op):
         H.close()
 
 
+# (problem, vectors, coarse op, inner_tol, inner_maxit).  inner_tol = 0 runs a fixed number
+# of inner iterations (reading R15): no rounding-decided integer, so the solutions must agree
+# to 1e-6.  Tolerance-stopped cases check the iteration count (+-1) and the true residual;
+# their solution parity is asserted only when every inner count matched.
 SOLVE_CASES = [
-    ("c0_tiny", "galerkin"), ("c0_tiny", "red_o2"), ("c0_tiny", "red_o4"),
-    ("mp_som_k20", "galerkin"), ("mp_som_k40", "red_o4"),
-    ("c1_k50", "galerkin"), ("c1_k50", "red_o4"),
-    ("wedge_f10", "galerkin"),
+    ("c0_tiny", "bilinear", "galerkin", 1e-1, 200), ("c0_tiny", "bilinear", "red_o2", 1e-1, 200),
+    ("c0_tiny", "bilinear", "red_o4", 1e-1, 200), ("c0_tiny", "bilinear", "galerkin", 0.0, 20),
+    ("mp_som_k20", "bilinear", "galerkin", 1e-1, 200), ("mp_som_k40", "bilinear", "red_o4", 0.0, 30),
+    ("c1_k50", "bilinear", "galerkin", 0.0, 40), ("c1_k50", "bilinear", "red_o4", 0.0, 40),
+    ("c1_k50", "high_order", "galerkin", 0.0, 60), ("c1_k50", "high_order", "red_glk2", 0.0, 60),
+    ("c1_k50", "high_order", "galerkin", 1e-1, 200),
+    ("mp_som_k40", "high_order", "galerkin", 1e-1, 200), ("mp_som_k40", "high_order", "red_glk1", 0.0, 30),
+    ("wedge_f10", "bilinear", "galerkin", 0.0, 40), ("wedge_f10", "high_order", "red_glk2", 1e-1, 300),
 ]
 
 
@@ -138,18 +159,23 @@ def _problem(name):
     return config_problem(name)
 
 
-@pytest.mark.parametrize("name,op", SOLVE_CASES)
-def test_solve(lib, name, op):
+@pytest.mark.parametrize("name,vec,op,itol,imax", SOLVE_CASES)
+def test_solve(lib, name, vec, op, itol, imax):
     p = _problem(name)
-    H = lib.helm_setup(p, {"coarse_op": op})
+    H = lib.helm_setup(p, {"coarse_op": op, "vectors": vec, "inner_tol": itol, "inner_maxit": imax})
     x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=400)
-    xo, rep_o = oracle.solve(p, oracle.SolverParams(coarse_op=op))
+    so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
+                                                           inner_maxit=imax, maxit=400))
+    xo, rep_o = so.solve(p.b)
     assert rep["converged"] and rep_o["converged"]
     assert abs(rep["outer_iterations"] - rep_o["outer_iterations"]) <= 1, (rep, rep_o["outer_iterations"])
     x = x.cpu().numpy()
-    assert rel(x, xo) < 1e-6
     # true residual of the GPU solution, measured by the oracle's operator
     assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
+    same_path = itol == 0.0 or (rep["outer_iterations"] == rep_o["outer_iterations"] and
+                                rep["inner_iterations_total"] == sum(rep_o["inner_iterations"]))
+    if same_path:
+        assert rel(x, xo) < 1e-6
     H.close()
 
 

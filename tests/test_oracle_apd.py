@@ -1,0 +1,130 @@
+"""Pins for the higher-order deflation vectors (APD) and the ReD-Glk coarse operators."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.coarse import GLK_LAP, GLK_MASS
+from workloads import mp_problem, random_field, random_k
+from tests.test_oracle_transfer import _dense
+from tests.test_oracle_coarse import _A_dense
+
+
+def _ho_1d(n_fine, bc):
+    """Eq. 3.11a on node indices: even fine node i -> (1/8)(c_{i/2-1} + 6 c_{i/2} + c_{i/2+1}),
+    odd -> (1/2)(c_{(i-1)/2} + c_{(i+1)/2}); Dirichlet boundary coarse nodes hold 0 and
+    coarse nodes outside the domain do not exist."""
+    if bc == "dirichlet":
+        nc = (n_fine - 1) // 2
+        node = lambda i: i + 1
+        unk = lambda c: c - 1 if 1 <= c <= nc else None
+    else:
+        nc = (n_fine + 1) // 2
+        node = lambda i: i
+        unk = lambda c: c if 0 <= c < nc else None
+    P = np.zeros((n_fine, nc))
+    for i in range(n_fine):
+        m = node(i)
+        src = [(m // 2 - 1, 1 / 8), (m // 2, 6 / 8), (m // 2 + 1, 1 / 8)] if m % 2 == 0 else \
+              [((m - 1) // 2, 0.5), ((m + 1) // 2, 0.5)]
+        for c, w in src:
+            u = unk(c)
+            if u is not None:
+                P[i, u] += w
+    return P
+
+
+@pytest.mark.parametrize("bc,shape", [("dirichlet", (7, 15)), ("sommerfeld", (9, 13))])
+def test_ho_prolongation_tensor_and_restriction_transpose(bc, shape):
+    """Eq. 3.12 = tensor product of Eq. 3.11a; Eq. 3.14 (weights sum 256/64 = 4) = Z^T."""
+    cshape = oracle.coarse_shape(shape, bc)
+    Z = _dense(lambda e: oracle.prolong_high_order(e, shape, bc), cshape)
+    np.testing.assert_allclose(Z, np.kron(_ho_1d(shape[0], bc), _ho_1d(shape[1], bc)), atol=1e-15)
+    R = _dense(lambda v: oracle.restrict_high_order(v, bc), shape)
+    np.testing.assert_allclose(R, Z.T, atol=1e-15)
+
+
+def test_ho_prolongation_point_classes():
+    """The four branch formulas of Eq. 3.12 written out literally at interior points."""
+    bc, shape = "sommerfeld", (17, 17)
+    e = random_field((9, 9), 3)
+    f = oracle.prolong_high_order(e, shape, bc)
+    ic, jc = 4, 4
+    u = lambda di, dj: e[jc + dj, ic + di]
+    black = (6 * u(-1, 0) + 36 * u(0, 0) + 6 * u(1, 0) + u(-1, -1) + 6 * u(0, -1) + u(1, -1)
+             + u(-1, 1) + 6 * u(0, 1) + u(1, 1)) / 64
+    blue = (u(0, -1) + 6 * u(0, 0) + u(0, 1) + u(1, -1) + 6 * u(1, 0) + u(1, 1)) / 16
+    red = (u(-1, 0) + 6 * u(0, 0) + u(1, 0) + u(-1, 1) + 6 * u(0, 1) + u(1, 1)) / 16
+    grey = (u(0, 0) + u(0, 1) + u(1, 0) + u(1, 1)) / 4
+    fi, fj = 2 * ic, 2 * jc
+    assert abs(f[fj, fi] - black) < 1e-14
+    assert abs(f[fj, fi + 1] - blue) < 1e-14
+    assert abs(f[fj + 1, fi] - red) < 1e-14
+    assert abs(f[fj + 1, fi + 1] - grey) < 1e-14
+
+
+def test_galerkin_interior_equals_printed_stencils():
+    """Eq. 5.12 / Eq. 5.14 are Z^T(-Delta_h)Z and Z^T I(k^2) Z for the higher-order vectors:
+    interior rows of the str-Glk operator equal the printed stencils (constant k)."""
+    bc, shape, h, kval = "dirichlet", (31, 31), 1 / 32, 7.0
+    k = np.full(shape, kval)
+    cshape = oracle.coarse_shape(shape, bc)
+    E = _dense(lambda x: oracle.apply_coarse_E(x, k, h, bc, "galerkin", "high_order"), cshape)
+    H = 2 * h
+    st = GLK_LAP / H**2 - kval**2 * GLK_MASS
+    J, I = 7, 7
+    row = E[J * cshape[1] + I].reshape(cshape)
+    np.testing.assert_allclose(row[J - 2:J + 3, I - 2:I + 3], st, rtol=1e-12, atol=1e-9)
+    assert abs(row.sum() - st.sum()) < 1e-8 * abs(st).max()    # no taps beyond the 5x5 footprint
+    assert GLK_LAP.sum() == 0.0 and abs(GLK_MASS.sum() - 4.0) < 1e-15
+
+
+@pytest.mark.parametrize("op", ["red_glk1", "red_glk2"])
+def test_red_glk_equals_galerkin_on_interior_support(op):
+    """SPEC property: for constant k, ReD-Glk applied to coarse vectors supported >= 3
+    coarse points from the boundary equals str-Glk (the stencils are the composition)."""
+    bc, shape, h = "sommerfeld", (33, 33), 1 / 32
+    k = np.full(shape, 9.0)
+    cshape = oracle.coarse_shape(shape, bc)
+    x = np.zeros(cshape, complex)
+    x[5:-5, 5:-5] = random_field((cshape[0] - 10, cshape[1] - 10), 2)
+    a = oracle.apply_coarse_E(x, k, h, bc, op, "high_order")
+    b = oracle.apply_coarse_E(x, k, h, bc, "galerkin", "high_order")
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-10 * abs(b).max())
+
+
+def test_apd_deflation_identity():
+    """APD with str-Glk and an exact coarse solve: P_{APD} A Z x = Z x."""
+    bc, shape = "dirichlet", (15, 15)
+    k = random_k(shape, 4, 5.0, 12.0)
+    s = oracle.Solver(k, 1 / 16, bc, oracle.SolverParams(vectors="high_order", inner_solver="direct"))
+    xc = random_field(s.cshape, 1)
+    Zx = oracle.prolong_high_order(xc, shape, bc)
+    np.testing.assert_allclose(s.adef1(s.A(Zx)), Zx, atol=1e-9 * abs(Zx).max())
+
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_iteration_counts.json")))
+
+
+@pytest.mark.parametrize("row", GOLD["table4_mp2b_apd"]["rows"], ids=lambda r: f"{r['nodes']}-{r['op']}")
+def test_table4_wavenumber_independence(row):
+    """Table 4 (MP-2b, APD, kh = 0.625): str-Glk and ReD-Glk2 outer counts, coarse problem
+    solved accurately (the paper: CSLP-GMRES to 1e-12).  Allow +-2 (FGMRES / true residual
+    here vs left-preconditioned GMRES in the paper)."""
+    p = mp_problem(float(row["k"]), row["nodes"] - 1, "sommerfeld")
+    x, rep = oracle.solve(p, oracle.SolverParams(vectors="high_order", coarse_op=row["op"], inner_tol=1e-8,
+                                                 inner_maxit=1000))
+    assert rep["converged"]
+    assert abs(rep["outer_iterations"] - row["outer"]) <= 2, (rep["outer_iterations"], row)
+
+
+def test_mgs_and_cgs2_agree_with_exact_coarse_solve():
+    """Reading R13: the literal MGS loop of Algorithm 1 and CGS2 give the same solve when no
+    rounding-decided integer is involved (exact coarse solve)."""
+    p = mp_problem(20.0, 32, "dirichlet")
+    xa, ra = oracle.solve(p, oracle.SolverParams(inner_solver="direct", orth="mgs"))
+    xb, rb = oracle.solve(p, oracle.SolverParams(inner_solver="direct", orth="cgs2"))
+    assert ra["outer_iterations"] == rb["outer_iterations"]
+    assert np.linalg.norm(xa - xb) / np.linalg.norm(xa) < 1e-9
