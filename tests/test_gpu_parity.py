@@ -133,10 +133,12 @@ def test_deflate(lib, vec, op):
         H.close()
 
 
-# (problem, vectors, coarse op, inner_tol, inner_maxit).  inner_tol = 0 runs a fixed number
-# of inner iterations (reading R15): no rounding-decided integer, so the solutions must agree
-# to 1e-6.  Tolerance-stopped cases check the iteration count (+-1) and the true residual;
-# their solution parity is asserted only when every inner count matched.
+# (problem, vectors, coarse op, inner_tol, inner_maxit).  At the paper's outer tolerance 1e-6
+# both sides must take the same outer iteration count (+-1) and the GPU solution must meet the
+# true residual.  The solutions themselves are compared at a tight outer tolerance (1e-10,
+# reading R16): two valid 1e-6 solutions of this indefinite system legitimately differ by
+# cond(A) x 1e-6 (~7e-6 for c1_k50; the oracle's own MGS and CGS2 variants differ by that
+# much), while at 1e-10 both are within ~1e-9 of the unique discrete solution.
 SOLVE_CASES = [
     ("c0_tiny", "bilinear", "galerkin", 1e-1, 200), ("c0_tiny", "bilinear", "red_o2", 1e-1, 200),
     ("c0_tiny", "bilinear", "red_o4", 1e-1, 200), ("c0_tiny", "bilinear", "galerkin", 0.0, 20),
@@ -172,10 +174,12 @@ def test_solve(lib, name, vec, op, itol, imax):
     x = x.cpu().numpy()
     # true residual of the GPU solution, measured by the oracle's operator
     assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
-    same_path = itol == 0.0 or (rep["outer_iterations"] == rep_o["outer_iterations"] and
-                                rep["inner_iterations_total"] == sum(rep_o["inner_iterations"]))
-    if same_path:
-        assert rel(x, xo) < 1e-6
+    xt, rep_t = H.solve(gpu(p.b), tol=1e-10, maxit=600)
+    so_t = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
+                                                             inner_maxit=imax, maxit=600, tol=1e-10))
+    xo_t, rep_ot = so_t.solve(p.b)
+    assert rep_t["converged"] and rep_ot["converged"]
+    assert rel(xt.cpu().numpy(), xo_t) < 1e-6
     H.close()
 
 
