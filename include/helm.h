@@ -13,8 +13,9 @@
  *    Sommerfeld grids hold every node including the boundary (§2.1).
  *  - Level 0 is the fine grid; level l has mesh width 2^l h (standard vertex-centred
  *    coarsening, §4).  Level 1 is also the deflation coarse grid.
- *  - All work is enqueued on the stream given to helm_setup (NULL = legacy default stream).
- *    Entry points that return scalars (helm_solve) synchronise that stream.
+ *  - Operator entry points enqueue on the stream given to helm_setup (NULL = legacy default
+ *    stream).  helm_solve / helm_solve_host run on a private stream ordered after that stream
+ *    and synchronise before returning (they return scalars in helm_report).
  *  - Return value: 0 on success, a negative HELM_E* code on failure; helm_last_error()
  *    returns a thread-local message.  No entry point falls back to the CPU: if the device
  *    or the kernels are unavailable the call fails.
@@ -71,6 +72,11 @@ typedef struct {
   int max_coarsest;    /* largest coarsest grid (unknowns) solved by the dense inverse */
   int vectors;         /* HELM_VECTORS_*; bilinear admits GALERKIN/RED_O2/RED_O4,
                           high order admits GALERKIN/RED_GLK1/RED_GLK2 */
+  int graph;           /* 1 (default): helm_solve runs as one CUDA graph whose outer and inner
+                          loops are conditional while nodes (no host sync inside a solve);
+                          0: the same kernels with host-polled loops */
+  int tail_max_n;      /* V-cycle levels with at most this many unknowns (and everything
+                          below them) run in one single-CTA kernel; 0 disables (default 8192) */
 } helm_params;
 
 typedef struct {
@@ -82,6 +88,7 @@ typedef struct {
   int inner_iterations_max;
   int restarts;
   double seconds;         /* host wall time of the solve (stream synchronised) */
+  long long kernels;      /* kernels executed by the solve (graph replays counted per node run) */
 } helm_report;
 
 void helm_default_params(helm_params* p);
@@ -113,8 +120,12 @@ int helm_vcycle(helm_ctx ctx, int level, const double* f_dev, double* u_dev);
  * E^{-1} by CSLP-preconditioned FGMRES to inner_tol (writes the inner count to
  * *inner_its if non-NULL). */
 int helm_deflate(helm_ctx ctx, const double* v_dev, double* z_dev, int* inner_its);
-/* Solve A x = b by A-DEF1-preconditioned FGMRES from x0 = 0 to ||b - A x||/||b|| <= tol.
- * b, x: device fields (x may not alias b).  rep may be NULL. */
+/* Solve A x = b by A-DEF1/APD-preconditioned FGMRES from x0 = 0 to ||b - A x||/||b|| <= tol
+ * (Algorithm 1 flexible form, Eq. 3.21).  The Arnoldi process, the Givens
+ * least-squares update and both convergence tests run on the device; the whole solve is one
+ * CUDA graph (params.graph = 1).  Orthogonalisation: classical Gram-Schmidt twice with the
+ * second pass delayed one iteration (two sweeps over the basis per iteration; R13).  b, x: device fields (x may not
+ * alias b).  rep may be NULL. */
 int helm_solve(helm_ctx ctx, const double* b_dev, double* x_dev, double tol, int maxit, helm_report* rep);
 /* Deflation vectors of the configured kind between level 0 and the coarse grid (level 1):
  * coarse = R Z^T fine (R = 1/4 bilinear, 1 high order), fine = Z coarse. */
@@ -126,8 +137,23 @@ int helm_solve_host(helm_ctx ctx, const double* b_host, double* x_host, double t
 
 /* Write `bytes` to a scratch buffer (> L2) on the context stream: L2 flush between timed steps. */
 int helm_flush_l2(helm_ctx ctx, size_t bytes);
-/* Number of kernels this context launched since creation (bench.py's gpu_launches). */
+/* Number of kernels this context launched since creation (bench.py's gpu_launches); a graph
+ * solve adds the kernels its replay executed. */
 long long helm_launch_count(helm_ctx ctx);
+
+/* Kernel timing for the roofline (bench.py): launches kernel `which` `reps` times on the
+ * context stream at this context's sizes (level 0 / level `arg` / level 1 / inner basis), each bracketed by
+ * CUDA events (after an L2 flush if `flush`), and returns the mean device time per launch and
+ * the algorithmic bytes per launch.  `arg` = number of basis vectors for the
+ * Gram-Schmidt kernels (1..inner_maxit).  Operates on internal scratch buffers only. */
+#define HELM_KB_APPLY_A 0
+#define HELM_KB_VC_DOWN 1    /* fused V-cycle down leg on level `arg` */
+#define HELM_KB_VC_UP 2      /* fused V-cycle up leg on level `arg` */
+#define HELM_KB_APPLY_E 3
+#define HELM_KB_GS_DOTS 4    /* delayed-CGS2 pass 1 over `arg` basis vectors */
+#define HELM_KB_GS_UPDATE 5  /* delayed-CGS2 pass 2 over `arg - 1` basis vectors */
+int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, double* us_per_launch,
+                      double* bytes_per_launch);
 
 const char* helm_last_error(void);
 const char* helm_build_info(void);

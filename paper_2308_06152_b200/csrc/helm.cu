@@ -1,5 +1,8 @@
-// Host side of the C ABI declared in include/helm.h: hierarchy setup, kernel orchestration
-// of the V-cycle, the A-DEF1 deflation operator, and flexible GMRES (outer and inner).
+// Host side of the C ABI declared in include/helm.h: hierarchy setup, orchestration of the
+// fused V-cycle (§3.1), the A-DEF1 / APD deflation operator (Eq. 3.21, Eq. 5.2-5.5) and the
+// device-resident flexible GMRES (Algorithm 1, flexible form).  A solve is captured once into
+// a CUDA graph whose outer and inner (coarse-solve) loops are conditional while nodes driven
+// by the device-side convergence test: no host synchronisation inside a solve.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -8,12 +11,15 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/helm.h"
 #include "kernels.cuh"
+#include "krylov.cuh"
+#include "vcycle.cuh"
 
 using namespace helm;
 using cplx = std::complex<double>;
@@ -39,9 +45,9 @@ int fail(int code, const char* fmt, ...) {
                                        cudaGetErrorString(e_));                               \
   } while (0)
 
-#define CKR(expr)              \
-  do {                         \
-    int r_ = (expr);           \
+#define CKR(expr)                 \
+  do {                            \
+    int r_ = (expr);              \
     if (r_ != HELM_OK) return r_; \
   } while (0)
 
@@ -52,42 +58,64 @@ struct Level {
   double* k = nullptr;
   double2* f = nullptr;  // rhs when this level is reached by recursion
   double2* u = nullptr;  // solution when reached by recursion
-  double2* t = nullptr;  // scratch
+  double2* s = nullptr;  // scratch (pre-smoothed iterate)
+  double2* t = nullptr;  // scratch (residual / correction)
 };
 
-struct Krylov {
-  int m = 0;       // basis capacity
+// One device-resident FGMRES instance (basis, Hessenberg, rotations, state).
+struct Fgm {
+  int m = 0;
   size_t n = 0;
-  double2* V = nullptr;   // (m+1) x n
-  double2* Z = nullptr;   // m x n
-  std::vector<cplx> H;    // (m+1) x m, column-major H[i + j*(m+1)]
-  std::vector<double> cs;
-  std::vector<cplx> sn, g;
+  double2* V = nullptr;      // (m+1) x n
+  double2* Z = nullptr;      // m x n
+  double2* H = nullptr;      // (m+1) x m, column-major
+  double2* g = nullptr;      // m+1
+  double2* sn = nullptr;     // m
+  double* cs = nullptr;      // m
+  double2* y = nullptr;      // m
+  double2* dots1 = nullptr;  // 2m+4: pass-1 dot products (a_c, b_c interleaved)
+  double2* coef = nullptr;   // 2m+4: pass-2 coefficients
+  double2* sc2 = nullptr;    // 2: 1/beta, h_jj
+  double2* rawc = nullptr;   // m+2: raw Hessenberg column awaiting its delayed correction
+  double2* nrm = nullptr;    // 2
+  double2* part = nullptr;   // max((m+2) * gx, gu) partials
+  GsGeom geo{};              // Gram-Schmidt launch geometry
+  FgmState* st = nullptr;
 };
 
 }  // namespace
 
 struct helm_ctx_s {
-  cudaStream_t s = nullptr;
+  cudaStream_t s = nullptr;       // stream work is enqueued on (the capture stream while capturing)
+  cudaStream_t user = nullptr;    // stream given to helm_setup
+  cudaStream_t own = nullptr;     // private stream (graphs need a non-legacy stream)
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  int depth = 0;                  // conditional-body nesting while capturing
+  bool capturing = false;
   helm_params p{};
   std::vector<Level> L;
+  LevelDesc* dlev = nullptr;      // device copy of the level descriptors (tail kernel)
+  int tail_lt = -1;               // first level run by the single-CTA tail (-1: none)
+  std::vector<size_t> tail_smem;  // dynamic shared memory of the tail started at each level
   double2* Minv = nullptr;
   int ncoarsest = 0;
-  double2* gal = nullptr;          // Galerkin 9-point coefficients on level 1
   double2 *dq = nullptr, *dt = nullptr;   // fine scratch for A-DEF1
   double2 *cc = nullptr, *ce = nullptr;   // coarse rhs / solution
-  double2 *bx = nullptr, *xx = nullptr;   // device b/x for helm_solve_host
-  Krylov outer, inner;
-  double2* partial = nullptr;      // multidot partials
-  size_t partial_cap = 0;
-  double2* dres = nullptr;         // device scalar results
-  cplx* hres = nullptr;            // pinned host mirror
-  size_t dres_cap = 0;
+  double2 *bbuf = nullptr, *xbuf = nullptr;  // solve input/output (graph-stable addresses)
+  Fgm outer, inner;
+  FgmState* hst = nullptr;        // pinned host mirror of a state
   uint4* flush = nullptr;
   size_t flush_n = 0;
-  long long launches = 0;
-  int last_inner = 0;
+  long long launches = 0;         // kernels launched (graph replays: kernels executed)
   int sm_count = 148;
+  // cached solve graphs: [0] first cycle (x0 = 0), [1] restart cycle
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  double g_tol = -1.0;
+  int g_maxit = -1;
+  // kernels captured per region (graph replays execute a data-dependent number of them)
+  long long body_launches[4] = {0, 0, 0, 0};
+  long long cnt_top = 0, cnt_outer = 0, cnt_inner = 0;
+  long long cnt[2][3] = {{0, 0, 0}, {0, 0, 0}};
 };
 
 namespace {
@@ -119,10 +147,12 @@ int dalloc(T** p, size_t count) {
   return HELM_OK;
 }
 
+bool fused_vcycle(const helm_ctx_s& C) { return C.p.nu_pre == 1 && C.p.nu_post == 1; }
+
 // ------------------------------------------------------------------ operator launches
-int op_apply(helm_ctx_s& C, const Level& L, const double2* u, const double2* f, double2* y, double sr, double si) {
-  if (f) k_apply_op<1><<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, u, f, y, L.k, sr, si);
-  else k_apply_op<0><<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, u, nullptr, y, L.k, sr, si);
+int op_apply(helm_ctx_s& C, const Level& L, DVec u, DVec f, DVec y, double sr, double si) {
+  if (f.p) k_apply_op<1><<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, u, f, y, L.k, sr, si);
+  else k_apply_op<0><<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, u, DVec(), y, L.k, sr, si);
   return post_launch(C);
 }
 
@@ -133,16 +163,16 @@ int restrict_(helm_ctx_s& C, int l, const double2* v, double2* vc) {
   return post_launch(C);
 }
 
-int prolong_(helm_ctx_s& C, int l, const double2* e, const double2* base, double2* y) {
+int prolong_(helm_ctx_s& C, int l, const double2* e, const double2* base, DVec y, const double2* addq) {
   const Level& F = C.L[l];
   const Level& G = C.L[l + 1];
-  if (base) k_prolong<1><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, base, y);
-  else k_prolong<0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y);
+  if (base) k_prolong<1><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, base, y, addq);
+  else k_prolong<0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y, addq);
   return post_launch(C);
 }
 
 // Deflation vectors level 0 <-> level 1 (bilinear: R=1, high order: R=2)
-int defl_restrict(helm_ctx_s& C, const double2* v, double2* vc) {
+int defl_restrict(helm_ctx_s& C, DVec v, double2* vc) {
   const Level& F = C.L[0];
   const Level& G = C.L[1];
   if (C.p.vectors == HELM_VECTORS_BILINEAR)
@@ -162,270 +192,327 @@ int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
   return post_launch(C);
 }
 
-// y = E x (f == null) or y = f - E x on level 1
-int apply_E(helm_ctx_s& C, const double2* x, const double2* f, double2* y) {
+constexpr int GLK_TX = 16, GLK_TY = 8;   // coarse outputs per k_galerkin_apply CTA
+
+// y = E x (f.p == null) or y = f - E x on level 1
+int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
   const Level& G = C.L[1];
   const dim3 gg = grd2d(G.g.nx, G.g.ny);
+  const bool res = f.p != nullptr;
   switch (C.p.coarse_op) {
-    case HELM_COARSE_GALERKIN:
+    case HELM_COARSE_GALERKIN: {
+      const Level& F = C.L[0];
+      const dim3 gt((G.g.nx + GLK_TX - 1) / GLK_TX, (G.g.ny + GLK_TY - 1) / GLK_TY);
       if (C.p.vectors == HELM_VECTORS_BILINEAR) {
-        if (f) k_apply_stencil<1, 1><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, f, y);
-        else k_apply_stencil<1, 0><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, nullptr, y);
+        if (res) k_galerkin_apply<1, 1, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
+        else k_galerkin_apply<1, 0, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
       } else {
-        if (f) k_apply_stencil<2, 1><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, f, y);
-        else k_apply_stencil<2, 0><<<gg, blk2d(), 0, C.s>>>(G.g, C.gal, x, nullptr, y);
+        if (res) k_galerkin_apply<2, 1, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
+        else k_galerkin_apply<2, 0, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
       }
       return post_launch(C);
+    }
     case HELM_COARSE_RED_GLK1:
-      if (f) k_apply_red_glk<1, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_glk<1, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, nullptr, y, G.k);
+      if (res) k_apply_red_glk<1, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_glk<1, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_GLK2:
-      if (f) k_apply_red_glk<2, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_glk<2, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, nullptr, y, G.k);
+      if (res) k_apply_red_glk<2, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_glk<2, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_O2:
       return op_apply(C, G, x, f, y, 1.0, 0.0);
     case HELM_COARSE_RED_O4:
-      if (f) k_apply_red_o4<1><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_o4<0><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(G.g, x, nullptr, y, G.k);
+      if (res) k_apply_red_o4<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_o4<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
       return post_launch(C);
   }
   return fail(HELM_EINVAL, "bad coarse_op");
 }
 
 // ------------------------------------------------------------------ V-cycle (§3.1)
-int vcycle(helm_ctx_s& C, int l, const double2* f, double2* u, const double2* addq) {
+constexpr size_t TAIL_SMEM_MAX = 200 * 1024;
+constexpr int DOWN_TX = 16, DOWN_TY = 8;   // coarse points per k_vc_down CTA
+constexpr int UP_TX = 32, UP_TY = 8;       // fine points per k_vc_up CTA
+
+// u_out = V-cycle approximation of M_l^{-1} f (+ addq), starting at level l.
+int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   const int last = (int)C.L.size() - 1;
   Level& L = C.L[l];
   const double sr = C.p.beta1, si = C.p.beta2, w = C.p.omega;
+  if (C.tail_lt >= 0 && l >= C.tail_lt) {
+    k_vc_tail<<<1, 1024, C.tail_smem[l], C.s>>>(C.dlev, l, last, f, u_out, addq, sr, si, w, C.p.nu_pre, C.p.nu_post,
+                                                 C.Minv);
+    return post_launch(C);
+  }
   if (l == last) {
     const int n = (int)L.n;
-    k_gemv<<<(n * 32 + 255) / 256, 256, 0, C.s>>>(C.Minv, n, f, u);
-    CKR(post_launch(C));
-    if (addq) {
-      k_add<<<grid1d(C, L.n), 256, 0, C.s>>>(u, addq, u, L.n);
-      CKR(post_launch(C));
-    }
-    return HELM_OK;
+    k_gemv<<<(n * 32 + 255) / 256, 256, 0, C.s>>>(C.Minv, n, f, u_out, addq);
+    return post_launch(C);
   }
-  // pre-smoothing from u = 0 (reading R9)
-  double2* cur = (C.p.nu_pre % 2 == 1) ? u : L.t;
+  Level& G = C.L[l + 1];
+  if (fused_vcycle(C)) {
+    dim3 gd((G.g.nx + DOWN_TX - 1) / DOWN_TX, (G.g.ny + DOWN_TY - 1) / DOWN_TY);
+    k_vc_down<DOWN_TX, DOWN_TY><<<gd, 256, 0, C.s>>>(L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+    CKR(post_launch(C));
+    CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
+    dim3 gu((L.g.nx + UP_TX - 1) / UP_TX, (L.g.ny + UP_TY - 1) / UP_TY);
+    k_vc_up<UP_TX, UP_TY><<<gu, 256, 0, C.s>>>(L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+    return post_launch(C);
+  }
+  // generic sweep counts
+  double2* cur = L.s;
   k_jacobi0<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, f, cur, L.k, sr, si, w);
   CKR(post_launch(C));
-  for (int s = 1; s < C.p.nu_pre; ++s) {
-    double2* nxt = (cur == u) ? L.t : u;
-    k_jacobi<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, cur, f, nxt, L.k, sr, si, w, nullptr);
+  for (int sw = 1; sw < C.p.nu_pre; ++sw) {
+    double2* nxt = (cur == L.s) ? L.t : L.s;
+    k_jacobi<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, cur, f, DVec(nxt), L.k, sr, si, w, nullptr);
     CKR(post_launch(C));
     cur = nxt;
   }
-  // residual -> restriction -> recursion
-  CKR(op_apply(C, L, u, f, L.t, sr, si));
-  Level& G = C.L[l + 1];
-  CKR(restrict_(C, l, L.t, G.f));
-  CKR(vcycle(C, l + 1, G.f, G.u, nullptr));
-  // correction + post-smoothing; the last write lands in u
+  double2* ob = (cur == L.s) ? L.t : L.s;
+  CKR(op_apply(C, L, DVec(cur), f, DVec(ob), sr, si));
+  CKR(restrict_(C, l, ob, G.f));
+  CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
   const int np = C.p.nu_post;
-  cur = (np % 2 == 1) ? L.t : u;
-  CKR(prolong_(C, l, G.u, u, cur));
-  for (int s = 0; s < np; ++s) {
-    double2* nxt = (cur == u) ? L.t : u;
-    const double2* q = (s == np - 1) ? addq : nullptr;
-    k_jacobi<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, cur, f, nxt, L.k, sr, si, w, q);
+  if (np == 0) return prolong_(C, l, G.u, cur, u_out, addq);
+  CKR(prolong_(C, l, G.u, cur, DVec(ob), nullptr));
+  double2* src = ob;
+  for (int sw = 0; sw < np; ++sw) {
+    const bool lastsw = (sw == np - 1);
+    DVec dst = lastsw ? u_out : DVec((src == ob) ? cur : ob);
+    k_jacobi<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, src, f, dst, L.k, sr, si, w, lastsw ? addq : nullptr);
     CKR(post_launch(C));
-    cur = nxt;
-  }
-  if (np == 0 && addq) {
-    k_add<<<grid1d(C, L.n), 256, 0, C.s>>>(u, addq, u, L.n);
-    CKR(post_launch(C));
+    src = dst.p;
   }
   return HELM_OK;
 }
 
-// ------------------------------------------------------------------ BLAS-1 helpers
-int ensure_scratch(helm_ctx_s& C, size_t partial_elems, size_t dres_elems) {
-  if (partial_elems > C.partial_cap) {
-    if (C.partial) cudaFree(C.partial);
-    CKR(dalloc(&C.partial, partial_elems));
-    C.partial_cap = partial_elems;
-  }
-  if (dres_elems > C.dres_cap) {
-    if (C.dres) cudaFree(C.dres);
-    if (C.hres) cudaFreeHost(C.hres);
-    CKR(dalloc(&C.dres, dres_elems));
-    CK(cudaMallocHost((void**)&C.hres, dres_elems * sizeof(cplx)));
-    C.dres_cap = dres_elems;
-  }
-  return HELM_OK;
-}
-
-constexpr int NV = 8;
-
-// out[c] = V_c^H w, c < nvec   (out is a device pointer)
-int multidot(helm_ctx_s& C, const double2* V, size_t ld, int nvec, const double2* w, size_t n, double2* out) {
-  const int nb = std::min(grid1d(C, n), 2 * C.sm_count);
-  dim3 g(nb, (nvec + NV - 1) / NV);
-  k_multidot_partial<NV><<<g, 256, 0, C.s>>>(V, ld, nvec, w, n, C.partial);
-  CKR(post_launch(C));
-  k_multidot_final<<<(nvec * 32 + 255) / 256, 256, 0, C.s>>>(C.partial, nb, nvec, out, 0);
-  return post_launch(C);
-}
-
-int multi_axpy(helm_ctx_s& C, const double2* V, size_t ld, int nvec, const double2* coeff, double sign, double2* w,
-               size_t n) {
-  k_multi_axpy<<<grid1d(C, n), 256, nvec * sizeof(double2), C.s>>>(V, ld, nvec, coeff, sign, w, n);
-  return post_launch(C);
-}
-
-int fetch(helm_ctx_s& C, int count) {
-  CK(cudaMemcpyAsync(C.hres, C.dres, count * sizeof(cplx), cudaMemcpyDeviceToHost, C.s));
-  CK(cudaStreamSynchronize(C.s));
-  return HELM_OK;
-}
-
-int krylov_alloc(Krylov& K, int m, size_t n) {
+// ------------------------------------------------------------------ device FGMRES
+int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   K.m = m;
   K.n = n;
   CKR(dalloc(&K.V, (size_t)(m + 1) * n));
   CKR(dalloc(&K.Z, (size_t)m * n));
-  K.H.assign((size_t)(m + 1) * m, cplx(0, 0));
-  K.cs.assign(m, 0.0);
-  K.sn.assign(m, cplx(0, 0));
-  K.g.assign(m + 1, cplx(0, 0));
+  CKR(dalloc(&K.H, (size_t)(m + 1) * m));
+  CKR(dalloc(&K.g, (size_t)m + 1));
+  CKR(dalloc(&K.sn, (size_t)m));
+  CKR(dalloc(&K.cs, (size_t)m));
+  CKR(dalloc(&K.y, (size_t)m));
+  CKR(dalloc(&K.dots1, (size_t)2 * m + 4));
+  CKR(dalloc(&K.coef, (size_t)2 * m + 4));
+  CKR(dalloc(&K.sc2, 2));
+  CKR(dalloc(&K.rawc, (size_t)m + 2));
+  CKR(dalloc(&K.nrm, 2));
+  K.geo = gs_geom((long long)n, C.sm_count);
+  CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * K.geo.gx, (size_t)K.geo.gu)));
+  CKR(dalloc(&K.st, 1));
+  CK(cudaMemsetAsync(K.st, 0, sizeof(FgmState), C.s));
+  const size_t smem = (size_t)(m + 2) * sizeof(double2);
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t usmem = (size_t)(2 * m + 2) * sizeof(double2);
+  const size_t asmem = dcgs_smem(m);
+  if (asmem > 227 * 1024 || usmem > 227 * 1024)
+    return fail(HELM_EINVAL, "Krylov basis of %d columns exceeds the Arnoldi kernels' shared memory", m);
+  if (usmem > 48 * 1024) CK(cudaFuncSetAttribute(k_dcgs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem));
+  if (asmem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_dcgs_stepA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+    CK(cudaFuncSetAttribute(k_dcgs_stepB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+  }
   return HELM_OK;
 }
 
-void krylov_free(Krylov& K) {
-  if (K.V) cudaFree(K.V);
-  if (K.Z) cudaFree(K.Z);
-  K.V = K.Z = nullptr;
+void fgm_free(Fgm& K) {
+  cudaFree(K.V);
+  cudaFree(K.Z);
+  cudaFree(K.H);
+  cudaFree(K.g);
+  cudaFree(K.sn);
+  cudaFree(K.cs);
+  cudaFree(K.y);
+  cudaFree(K.dots1);
+  cudaFree(K.coef);
+  cudaFree(K.sc2);
+  cudaFree(K.rawc);
+  cudaFree(K.nrm);
+  cudaFree(K.part);
+  cudaFree(K.st);
+  K = Fgm();
 }
 
-// Flexible GMRES (Algorithm 1 in flexible form, §6.3), x0 = 0, restarted when the
-// basis capacity is exhausted.  Arnoldi orthogonalisation by classical Gram-Schmidt with one
-// re-orthogonalisation pass (CGS2, batched dots; DESIGN.md §5 deviation from Alg. 1's MGS).
-template <class OpA, class OpP>
-int fgmres(helm_ctx_s& C, Krylov& K, OpA&& A, OpP&& P, const double2* b, double2* x, size_t n, double tol, int maxit,
-           int* its_out, double* relres_out, int* conv_out, int* restarts_out) {
-  const int m = K.m;
-  CKR(ensure_scratch(C, (size_t)((m + NV) / NV * NV + NV) * 2 * C.sm_count, (size_t)(2 * m + 8)));
-  CK(cudaMemsetAsync(x, 0, n * sizeof(double2), C.s));
-  // ||b||
-  CKR(multidot(C, b, n, 1, b, n, C.dres));
-  CKR(fetch(C, 1));
-  const double bnorm = std::sqrt(C.hres[0].real());
-  int its = 0, restarts = 0, conv = 0;
-  double relres = 0.0;
-  if (bnorm == 0.0) {
-    *its_out = 0; *relres_out = 0.0; *conv_out = 1; if (restarts_out) *restarts_out = 0;
+int gs_dots(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, DVec w, int want_norm,
+            double2* out, const int* gate) {
+  const GsGeom& g = K.geo;
+  k_gs_dots<<<dim3(g.gx, g.gy), GS_THREADS, 0, C.s>>>(V, (long long)K.n, nptr, nadd, w, (long long)K.n, g.chunk,
+                                                        want_norm, K.part, gate);
+  CKR(post_launch(C));
+  const int maxout = K.m + 2;
+  k_gs_reduce<<<(maxout * 32 + 255) / 256, 256, 0, C.s>>>(K.part, g.gx, nptr, nadd, 1, want_norm ? 1 : 0, out, gate);
+  return post_launch(C);
+}
+
+// w_out = w_in + sign * V coeff; with want_norm the per-block |w_out|^2 partials are left in
+// K.part[0 .. geo.gu) for k_fgm_arnoldi.
+int gs_update(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, const double2* coeff, double sign,
+              DVec win, DVec wout, int want_norm, const int* gate) {
+  const size_t smem = (size_t)(K.m + 2) * sizeof(double2);
+  k_gs_update<<<K.geo.gu, GS_THREADS, smem, C.s>>>(V, (long long)K.n, nptr, nadd, coeff, sign, win, wout,
+                                                    (long long)K.n, want_norm, K.part, gate);
+  return post_launch(C);
+}
+
+int read_state(helm_ctx_s& C, FgmState* st) {
+  CK(cudaMemcpyAsync(C.hst, st, sizeof(FgmState), cudaMemcpyDeviceToHost, C.s));
+  CK(cudaStreamSynchronize(C.s));
+  return HELM_OK;
+}
+
+// A device-controlled while loop: begin(h, use_h) sets the condition, body(h, use_h) runs
+// while it holds.  Capturing: a conditional while node; otherwise the host polls the state.
+template <class Begin, class Body>
+int run_while(helm_ctx_s& C, FgmState* st, Begin&& begin, Body&& body) {
+  if (!C.capturing) {
+    CKR(begin(cudaGraphConditionalHandle(0), 0));
+    for (;;) {
+      CKR(read_state(C, st));
+      if (!C.hst->cond) break;
+      CKR(body(cudaGraphConditionalHandle(0), 0));
+    }
     return HELM_OK;
   }
-  double beta = bnorm;
-  // V_0 = b / beta
-  k_scale_copy<<<grid1d(C, n), 256, 0, C.s>>>(b, 1.0 / beta, K.V, n);
-  CKR(post_launch(C));
-  while (true) {
-    std::fill(K.H.begin(), K.H.end(), cplx(0, 0));
-    std::fill(K.g.begin(), K.g.end(), cplx(0, 0));
-    K.g[0] = beta;
-    int j = 0;
-    bool done = false;
-    for (; j < m && its < maxit; ++j) {
-      double2* vj = K.V + (size_t)j * n;
-      double2* zj = K.Z + (size_t)j * n;
-      double2* w = K.V + (size_t)(j + 1) * n;
-      CKR(P(vj, zj));
-      CKR(A(zj, w));
-      const int nv = j + 1;
-      // CGS2
-      CKR(multidot(C, K.V, n, nv, w, n, C.dres));
-      CKR(multi_axpy(C, K.V, n, nv, C.dres, -1.0, w, n));
-      CKR(multidot(C, K.V, n, nv, w, n, C.dres + nv));
-      CKR(multi_axpy(C, K.V, n, nv, C.dres + nv, -1.0, w, n));
-      CKR(multidot(C, w, n, 1, w, n, C.dres + 2 * nv));
-      k_normalize<<<grid1d(C, n), 256, 0, C.s>>>(w, C.dres + 2 * nv, w, n);
-      CKR(post_launch(C));
-      CKR(fetch(C, 2 * nv + 1));
-      const size_t ld = (size_t)m + 1;
-      for (int i = 0; i < nv; ++i) K.H[i + j * ld] = C.hres[i] + C.hres[nv + i];
-      const double hn = std::sqrt(std::max(0.0, C.hres[2 * nv].real()));
-      K.H[(j + 1) + j * ld] = hn;
-      for (int i = 0; i < j; ++i) {
-        cplx t = K.cs[i] * K.H[i + j * ld] + K.sn[i] * K.H[i + 1 + j * ld];
-        K.H[i + 1 + j * ld] = -std::conj(K.sn[i]) * K.H[i + j * ld] + K.cs[i] * K.H[i + 1 + j * ld];
-        K.H[i + j * ld] = t;
-      }
-      cplx a = K.H[j + j * ld];
-      double bb = hn;
-      double den = std::sqrt(std::norm(a) + bb * bb);
-      if (std::abs(a) == 0.0) { K.cs[j] = 0.0; K.sn[j] = 1.0; }
-      else { K.cs[j] = std::abs(a) / den; K.sn[j] = (a / std::abs(a)) * bb / den; }
-      K.H[j + j * ld] = K.cs[j] * a + K.sn[j] * bb;
-      K.H[(j + 1) + j * ld] = 0.0;
-      K.g[j + 1] = -std::conj(K.sn[j]) * K.g[j];
-      K.g[j] = K.cs[j] * K.g[j];
-      its++;
-      relres = std::abs(K.g[j + 1]) / bnorm;
-      if (relres <= tol || hn == 0.0) { done = true; conv = 1; ++j; break; }
-    }
-    // y = H^{-1} g ; x += Z y
-    const int mm = j;
-    const size_t ld = (size_t)m + 1;
-    std::vector<cplx> y(mm);
-    for (int i = mm - 1; i >= 0; --i) {
-      cplx s = K.g[i];
-      for (int q = i + 1; q < mm; ++q) s -= K.H[i + q * ld] * y[q];
-      y[i] = s / K.H[i + i * ld];
-    }
-    if (mm > 0) {
-      CK(cudaMemcpyAsync(C.dres, y.data(), mm * sizeof(cplx), cudaMemcpyHostToDevice, C.s));
-      CKR(multi_axpy(C, K.Z, n, mm, C.dres, 1.0, x, n));
-    }
-    if (done || its >= maxit) break;
-    // restart: r = b - A x ; V_0 = r / ||r||
-    ++restarts;
-    double2* r = K.V;
-    CKR(A(x, r));
-    k_scale_copy<<<grid1d(C, n), 256, 0, C.s>>>(r, -1.0, r, n);
-    CKR(post_launch(C));
-    k_add<<<grid1d(C, n), 256, 0, C.s>>>(r, b, r, n);
-    CKR(post_launch(C));
-    CKR(multidot(C, r, n, 1, r, n, C.dres));
-    CKR(fetch(C, 1));
-    beta = std::sqrt(C.hres[0].real());
-    relres = beta / bnorm;
-    if (relres <= tol) { conv = 1; break; }
-    k_scale_copy<<<grid1d(C, n), 256, 0, C.s>>>(r, 1.0 / beta, K.V, n);
-    CKR(post_launch(C));
-  }
-  *its_out = its;
-  *relres_out = relres;
-  *conv_out = conv;
-  if (restarts_out) *restarts_out = restarts;
+  cudaStreamCaptureStatus cst;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(C.s, &cst, nullptr, &g, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  CKR(begin(h, 1));
+  CK(cudaStreamGetCaptureInfo(C.s, &cst, nullptr, &g, &deps, &nd));
+  std::vector<cudaGraphNode_t> dv(deps, deps + nd);
+  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, dv.data(), dv.size(), &cp));
+  cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(C.s, &node, 1, cudaStreamSetCaptureDependencies));
+  if (C.depth >= 4) return fail(HELM_EINVAL, "conditional nesting too deep");
+  cudaStream_t side = C.side[C.depth];
+  CK(cudaStreamBeginCaptureToGraph(side, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  cudaStream_t saved = C.s;
+  C.s = side;
+  const int d = C.depth++;
+  const long long l0 = C.launches;
+  int r = body(h, 1);
+  C.body_launches[d] += C.launches - l0;
+  C.depth--;
+  C.s = saved;
+  cudaGraph_t outg;
+  cudaError_t e = cudaStreamEndCapture(side, &outg);
+  if (r != HELM_OK) return r;
+  if (e != cudaSuccess) return fail(HELM_ECUDA, "body capture: %s", cudaGetErrorString(e));
   return HELM_OK;
 }
 
-// e = E^{-1} c on level 1 by CSLP(V-cycle from level 1)-preconditioned FGMRES (reading R11).
-int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, int* its) {
-  const Level& G = C.L[1];
-  auto A = [&](const double2* x, double2* y) { return apply_E(C, x, nullptr, y); };
-  auto P = [&](const double2* v, double2* z) { return vcycle(C, 1, v, z, nullptr); };
-  double rr;
-  int conv;
-  return fgmres(C, C.inner, A, P, c, e, G.n, C.p.inner_tol, C.p.inner_maxit, its, &rr, &conv, nullptr);
+// One FGMRES cycle for A x = b with x0 = 0 (first) or the current x (restart), x (+)= Z y.
+// opA(x, f, y): y = A x (f null) or y = f - A x;  opP(v, z): z = P v.
+
+template <class OpA, class OpP>
+int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x, bool first, FgmState* outer_stats) {
+  const size_t n = K.n;
+  FgmState* st = K.st;
+  auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    if (first) {
+      CKR(gs_dots(C, K, nullptr, nullptr, 0, b, 1, K.nrm, nullptr));
+      k_fgm_begin<<<1, 32, 0, C.s>>>(st, K.nrm, 1, K.g, h, use_h);
+      CKR(post_launch(C));
+      k_scale_dvec<<<grid1d(C, n), 256, 0, C.s>>>(b, &st->inv_beta, DVec(K.V), (long long)n, nullptr);
+      return post_launch(C);
+    }
+    CKR(opA(DVec(x), b, DVec(K.V)));
+    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(K.V), 1, K.nrm, nullptr));
+    k_fgm_begin<<<1, 32, 0, C.s>>>(st, K.nrm, 0, K.g, h, use_h);
+    CKR(post_launch(C));
+    k_scale_dvec<<<grid1d(C, n), 256, 0, C.s>>>(DVec(K.V), &st->inv_beta, DVec(K.V), (long long)n, nullptr);
+    return post_launch(C);
+  };
+  auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    const long long ln = (long long)n;
+    DVec vj(K.V, &st->j, ln), zj(K.Z, &st->j, ln), w(K.V + n, &st->j, ln);
+    CKR(opP(vj, zj));
+    CKR(opA(zj, DVec(), w));
+    // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
+    const GsGeom& gg = K.geo;
+    k_dcgs_dots<<<dim3(gg.gx, gg.gy), GS_THREADS, 0, C.s>>>(K.V, ln, &st->j, 1, vj, w, ln, gg.chunk, K.part);
+    CKR(post_launch(C));
+    k_gs_reduce<<<((2 * K.m + 2) * 32 + 255) / 256, 256, 0, C.s>>>(K.part, gg.gx, &st->j, 1, 2, 0, K.dots1, nullptr);
+    CKR(post_launch(C));
+    const size_t asm_ = dcgs_smem(K.m);
+    k_dcgs_stepA<<<1, 32, asm_, C.s>>>(st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc);
+    CKR(post_launch(C));
+    k_dcgs_update<<<gg.gu, GS_THREADS, (size_t)(2 * K.m + 2) * sizeof(double2), C.s>>>(K.V, ln, &st->j, K.coef, K.sc2,
+                                                                                      vj, w, ln, K.part);
+    CKR(post_launch(C));
+    k_dcgs_stepB<<<1, 32, asm_, C.s>>>(st, K.H, K.cs, K.sn, K.g, K.dots1, K.sc2, K.part, gg.gu, K.rawc, h, use_h);
+    CKR(post_launch(C));
+    // v~_{j+1} = w' / h_{j+1,j}   (st->j has advanced)
+    k_scale_dvec<<<grid1d(C, n), 256, 0, C.s>>>(DVec(K.V, &st->j, ln), &st->inv_hn, DVec(K.V, &st->j, ln), ln,
+                                                 &st->done);
+    return post_launch(C);
+  };
+  CKR(run_while(C, st, begin, body));
+  k_fgm_backsub<<<1, 32, 0, C.s>>>(st, K.H, K.g, K.y, outer_stats);
+  CKR(post_launch(C));
+  // x = (x or 0) + Z y
+  return gs_update(C, K, K.Z, &st->ncols, 0, K.y, 1.0, first ? DVec() : DVec(x), DVec(x), 0, nullptr);
 }
 
-// z = P_{A-DEF1} v (Eq. 3.21 / 5.2-5.5)
-int adef1(helm_ctx_s& C, const double2* v, double2* z, int* inner_its) {
+// e = E^{-1} c on level 1 by CSLP(V-cycle from level 1)-preconditioned FGMRES from e = 0
+// (reading R11), no restart (capacity inner_maxit, as the oracle).
+int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_stats) {
+  Fgm& K = C.inner;
+  k_fgm_reset<<<1, 1, 0, C.s>>>(K.st, C.p.inner_tol, C.p.inner_maxit, K.m);
+  CKR(post_launch(C));
+  auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y); };
+  auto opP = [&](DVec v, DVec z) { return vcycle(C, 1, v, z, nullptr); };
+  return fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats);
+}
+
+// z = P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v  (Eq. 3.21 / 5.2-5.5)
+int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
   Level& F = C.L[0];
-  CKR(defl_restrict(C, v, C.cc));                         // v1 = I_h^{2h} v
-  int its = 0;
-  CKR(coarse_solve(C, C.cc, C.ce, &its));                 // v2 = A_{2h}^{-1} v1
-  C.last_inner = its;
-  if (inner_its) *inner_its = its;
-  CKR(defl_prolong(C, C.ce, C.dq));                       // v' = I_{2h}^h v2  (= Q v)
-  CKR(op_apply(C, F, C.dq, v, C.dt, 1.0, 0.0));           // t = v - A Q v  (= P_h v)
-  return vcycle(C, 0, C.dt, z, C.dq);                     // z = M^{-1} t + Q v
+  CKR(defl_restrict(C, v, C.cc));                              // v1 = I_h^{2h} v
+  CKR(coarse_solve(C, C.cc, C.ce, outer_stats));               // v2 = A_{2h}^{-1} v1
+  CKR(defl_prolong(C, C.ce, C.dq));                            // v' = I_{2h}^h v2  (= Q v)
+  CKR(op_apply(C, F, DVec(C.dq), v, DVec(C.dt), 1.0, 0.0));    // t = v - A Q v  (= P_h v)
+  return vcycle(C, 0, DVec(C.dt), z, C.dq);                    // z = M^{-1} t + Q v
+}
+
+// Outer solve of A x = b (bbuf -> xbuf); one FGMRES cycle per call (restarts: host loop).
+int outer_cycle(helm_ctx_s& C, bool first) {
+  Level& F = C.L[0];
+  auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, F, x, f, y, 1.0, 0.0); };
+  auto opP = [&](DVec v, DVec z) { return adef1(C, v, z, C.outer.st); };
+  return fgmres_cycle(C, C.outer, opA, opP, DVec(C.bbuf), C.xbuf, first, nullptr);
+}
+
+int ensure_outer(helm_ctx_s& C, int maxit) {
+  int m = C.p.restart > 0 ? std::min(C.p.restart, maxit) : maxit;
+  if (C.outer.V && C.outer.m == m) return HELM_OK;
+  if (C.outer.V && C.p.restart <= 0 && C.outer.m >= m) return HELM_OK;
+  if (C.outer.V) fgm_free(C.outer);
+  for (auto& ex : C.gexec)
+    if (ex) {
+      cudaGraphExecDestroy(ex);
+      ex = nullptr;
+    }
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  const size_t per = 2 * C.L[0].n * sizeof(double2);
+  m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), fr / 2 / per));
+  return fgm_alloc(C, C.outer, m, C.L[0].n);
 }
 
 }  // namespace
@@ -447,34 +534,40 @@ void helm_default_params(helm_params* p) {
   p->restart = 0;
   p->max_coarsest = 4096;
   p->vectors = HELM_VECTORS_BILINEAR;
+  p->graph = 1;
+  p->tail_max_n = 8192;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
 
-const char* helm_build_info(void) { return "libhelm sm_100a complex128"; }
+const char* helm_build_info(void) { return "libhelm sm_100a complex128 (device FGMRES, CUDA-graph loops)"; }
 
 static void destroy_ctx(helm_ctx_s* C) {
   if (!C) return;
+  for (auto ex : C->gexec)
+    if (ex) cudaGraphExecDestroy(ex);
   for (auto& L : C->L) {
     cudaFree(L.k);
     cudaFree(L.f);
     cudaFree(L.u);
+    cudaFree(L.s);
     cudaFree(L.t);
   }
+  cudaFree(C->dlev);
   cudaFree(C->Minv);
-  cudaFree(C->gal);
   cudaFree(C->dq);
   cudaFree(C->dt);
   cudaFree(C->cc);
   cudaFree(C->ce);
-  cudaFree(C->bx);
-  cudaFree(C->xx);
-  cudaFree(C->partial);
-  cudaFree(C->dres);
+  cudaFree(C->bbuf);
+  cudaFree(C->xbuf);
   cudaFree(C->flush);
-  if (C->hres) cudaFreeHost(C->hres);
-  krylov_free(C->outer);
-  krylov_free(C->inner);
+  if (C->hst) cudaFreeHost(C->hst);
+  fgm_free(C->outer);
+  fgm_free(C->inner);
+  for (auto& sd : C->side)
+    if (sd) cudaStreamDestroy(sd);
+  if (C->own) cudaStreamDestroy(C->own);
   delete C;
 }
 
@@ -502,6 +595,10 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   int dev;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&C.sm_count, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaStreamCreateWithFlags(&C.own, cudaStreamNonBlocking));
+  for (auto& sd : C.side) CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  C.s = C.user;
+  CK(cudaMallocHost((void**)&C.hst, sizeof(FgmState)));
   // hierarchy (reading R7)
   Level L0;
   L0.g = Geo{grid->nx, grid->ny, grid->h, grid->bc};
@@ -525,6 +622,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   for (size_t l = 0; l < C.L.size(); ++l) {
     Level& Lv = C.L[l];
     CKR(dalloc(&Lv.k, Lv.n));
+    CKR(dalloc(&Lv.s, Lv.n));
     CKR(dalloc(&Lv.t, Lv.n));
     if (l > 0) {
       CKR(dalloc(&Lv.f, Lv.n));
@@ -538,6 +636,33 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     Level& G = C.L[l];
     k_sample_k<<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, G.k);
     CKR(post_launch(C));
+  }
+  // level descriptors for the single-CTA tail
+  {
+    std::vector<LevelDesc> ds(C.L.size());
+    for (size_t l = 0; l < C.L.size(); ++l) {
+      const Level& Lv = C.L[l];
+      ds[l] = LevelDesc{Lv.g, Lv.o, Lv.k};
+    }
+    CKR(dalloc(&C.dlev, ds.size()));
+    CK(cudaMemcpyAsync(C.dlev, ds.data(), ds.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, C.s));
+    CK(cudaStreamSynchronize(C.s));
+    // tail: the first level (>= 1) from which every remaining level fits in one CTA's shared
+    // memory (and has at most tail_max_n unknowns); the coarsest solve must be small
+    C.tail_lt = -1;
+    const int last = (int)C.L.size() - 1;
+    if (C.L.back().n <= 1024 && p.tail_max_n > 0 && last - 0 < TAIL_MAX_LEVELS) {
+      for (int l = 1; l <= last; ++l)
+        if ((long long)C.L[l].n <= p.tail_max_n && tail_smem_bytes(ds.data(), l, last) <= TAIL_SMEM_MAX) {
+          C.tail_lt = l;
+          break;
+        }
+    }
+    if (C.tail_lt >= 0) {
+      C.tail_smem.assign(C.L.size(), 0);
+      for (int l = C.tail_lt; l <= last; ++l) C.tail_smem[l] = tail_smem_bytes(ds.data(), l, last);
+      CK(cudaFuncSetAttribute(k_vc_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TAIL_SMEM_MAX));
+    }
   }
   // coarsest dense inverse (reading R8): Gauss-Jordan with partial pivoting on device
   {
@@ -556,7 +681,6 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     CK(cudaMemsetAsync(Md, 0, (size_t)n * n * sizeof(double2), C.s));
     k_dense_op<<<grd2d(Lc.g.nx, Lc.g.ny), blk2d(), 0, C.s>>>(Lc.g, Lc.k, p.beta1, p.beta2, Md);
     CKR(post_launch(C));
-    // Aug = [Md | I]
     std::vector<cplx> eye((size_t)n * 2 * n, cplx(0, 0));
     for (int r = 0; r < n; ++r) eye[(size_t)r * 2 * n + n + r] = 1.0;
     CK(cudaMemcpyAsync(Aug, eye.data(), eye.size() * sizeof(cplx), cudaMemcpyHostToDevice, C.s));
@@ -578,31 +702,14 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     cudaFree(colbuf);
     cudaFree(piv);
   }
-  // deflation coarse operator
-  if (p.coarse_op == HELM_COARSE_GALERKIN) {
-    const Level& F = C.L[0];
-    const Level& G = C.L[1];
-    if (p.vectors == HELM_VECTORS_BILINEAR) {
-      CKR(dalloc(&C.gal, 9 * G.n));
-      k_galerkin_coef<1><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, C.gal);
-    } else {
-      CKR(dalloc(&C.gal, 25 * G.n));
-      k_galerkin_coef<2><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, C.gal);
-    }
-    CKR(post_launch(C));
-  }
   CKR(dalloc(&C.dq, C.L[0].n));
   CKR(dalloc(&C.dt, C.L[0].n));
   CKR(dalloc(&C.cc, C.L[1].n));
   CKR(dalloc(&C.ce, C.L[1].n));
-  {
-    // inner basis capacity: inner_maxit, limited to a quarter of free HBM (restarted beyond)
-    size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot));
-    const size_t per = 2 * C.L[1].n * sizeof(double2);
-    const int cap = (int)std::max<size_t>(8, std::min<size_t>((size_t)p.inner_maxit, fr / 4 / per));
-    CKR(krylov_alloc(C.inner, cap, C.L[1].n));
-  }
+  CKR(dalloc(&C.bbuf, C.L[0].n));
+  CKR(dalloc(&C.xbuf, C.L[0].n));
+  // inner FGMRES: full (unrestarted) basis of inner_maxit columns, as the oracle (reading R11)
+  CKR(fgm_alloc(C, C.inner, p.inner_maxit, C.L[1].n));
   CK(cudaStreamSynchronize(C.s));
   return HELM_OK;
 }
@@ -614,7 +721,7 @@ int helm_setup(helm_ctx* out, const helm_grid* grid, const double* k, int k_on_d
   helm_ctx_s* C = new helm_ctx_s();
   if (params) C->p = *params;
   else helm_default_params(&C->p);
-  C->s = (cudaStream_t)stream;
+  C->user = (cudaStream_t)stream;
   int r = setup_impl(*C, grid, k, k_on_device);
   if (r != HELM_OK) {
     destroy_ctx(C);
@@ -636,12 +743,12 @@ int helm_level_info(helm_ctx C, int level, int* nx, int* ny, double* h) {
 
 int helm_apply_A(helm_ctx C, const double* x, double* y) {
   if (!C || !x || !y) return fail(HELM_EINVAL, "null argument");
-  return op_apply(*C, C->L[0], (const double2*)x, nullptr, (double2*)y, 1.0, 0.0);
+  return op_apply(*C, C->L[0], DVec((const double2*)x), DVec(), DVec((double2*)y), 1.0, 0.0);
 }
 
 int helm_apply_M(helm_ctx C, int level, const double* x, double* y) {
   if (!C || !x || !y || level < 0 || level >= (int)C->L.size()) return fail(HELM_EINVAL, "bad argument");
-  return op_apply(*C, C->L[level], (const double2*)x, nullptr, (double2*)y, C->p.beta1, C->p.beta2);
+  return op_apply(*C, C->L[level], DVec((const double2*)x), DVec(), DVec((double2*)y), C->p.beta1, C->p.beta2);
 }
 
 int helm_restrict(helm_ctx C, int level, const double* v, double* vc) {
@@ -651,12 +758,12 @@ int helm_restrict(helm_ctx C, int level, const double* v, double* vc) {
 
 int helm_prolong(helm_ctx C, int level, const double* e, double* v) {
   if (!C || !v || !e || level < 0 || level + 1 >= (int)C->L.size()) return fail(HELM_EINVAL, "bad argument");
-  return prolong_(*C, level, (const double2*)e, nullptr, (double2*)v);
+  return prolong_(*C, level, (const double2*)e, nullptr, DVec((double2*)v), nullptr);
 }
 
 int helm_apply_Zt(helm_ctx C, const double* v, double* vc) {
   if (!C || !v || !vc) return fail(HELM_EINVAL, "null argument");
-  return defl_restrict(*C, (const double2*)v, (double2*)vc);
+  return defl_restrict(*C, DVec((const double2*)v), (double2*)vc);
 }
 
 int helm_apply_Z(helm_ctx C, const double* e, double* v) {
@@ -666,75 +773,159 @@ int helm_apply_Z(helm_ctx C, const double* e, double* v) {
 
 int helm_apply_E(helm_ctx C, const double* x, double* y) {
   if (!C || !x || !y) return fail(HELM_EINVAL, "null argument");
-  return apply_E(*C, (const double2*)x, nullptr, (double2*)y);
+  return apply_E(*C, DVec((const double2*)x), DVec(), DVec((double2*)y));
 }
 
 int helm_vcycle(helm_ctx C, int level, const double* f, double* u) {
   if (!C || !f || !u || level < 0 || level >= (int)C->L.size()) return fail(HELM_EINVAL, "bad argument");
-  if (level > 0 && (f == (const double*)C->L[level].f || u == (double*)C->L[level].u))
-    return fail(HELM_EINVAL, "aliasing internal buffers");
-  return vcycle(*C, level, (const double2*)f, (double2*)u, nullptr);
+  for (size_t l = (size_t)level; l < C->L.size(); ++l) {
+    const Level& Lv = C->L[l];
+    const double* bufs[4] = {(const double*)Lv.f, (const double*)Lv.u, (const double*)Lv.s, (const double*)Lv.t};
+    for (const double* b : bufs)
+      if (b && (f == b || u == b)) return fail(HELM_EINVAL, "aliasing internal buffers");
+  }
+  return vcycle(*C, level, DVec((const double2*)f), DVec((double2*)u), nullptr);
 }
 
 int helm_deflate(helm_ctx C, const double* v, double* z, int* inner_its) {
   if (!C || !v || !z) return fail(HELM_EINVAL, "null argument");
-  return adef1(*C, (const double2*)v, (double2*)z, inner_its);
+  CKR(adef1(*C, DVec((const double2*)v), DVec((double2*)z), nullptr));
+  if (inner_its) {
+    CKR(read_state(*C, C->inner.st));
+    *inner_its = C->hst->its;
+  }
+  return HELM_OK;
+}
+
+// Capture one outer FGMRES cycle (first: from x = 0; else a restart from the current x).
+static int capture_cycle(helm_ctx_s& C, bool first, cudaGraphExec_t* out) {
+  C.capturing = true;
+  C.body_launches[0] = C.body_launches[1] = 0;
+  CK(cudaStreamBeginCapture(C.s, cudaStreamCaptureModeRelaxed));
+  const long long l0 = C.launches;
+  int r = outer_cycle(C, first);
+  cudaGraph_t g;
+  cudaError_t e = cudaStreamEndCapture(C.s, &g);
+  C.capturing = false;
+  const long long total = C.launches - l0;
+  C.launches = l0;
+  if (r != HELM_OK) return r;
+  if (e != cudaSuccess) return fail(HELM_ECUDA, "solve capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(HELM_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  // kernels per replay = top + outer_its * (outer body excl. inner loop) + inner_its * inner body
+  C.cnt_top = total - C.body_launches[0];
+  C.cnt_outer = C.body_launches[0] - C.body_launches[1];
+  C.cnt_inner = C.body_launches[1];
+  if (getenv("HELM_DEBUG_COUNTS"))
+    fprintf(stderr, "[helm] captured kernels: total %lld top %lld outer-body %lld inner-body %lld\n", total, C.cnt_top,
+            C.cnt_outer, C.cnt_inner);
+  return HELM_OK;
+}
+
+static int solve_device(helm_ctx_s& C, double tol, int maxit, helm_report* rep) {
+  CKR(ensure_outer(C, maxit));
+  const bool use_graph = C.p.graph != 0;
+  if (use_graph && (C.g_tol != tol || C.g_maxit != maxit)) {
+    for (auto& ex : C.gexec)
+      if (ex) {
+        cudaGraphExecDestroy(ex);
+        ex = nullptr;
+      }
+    C.g_tol = tol;
+    C.g_maxit = maxit;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  k_fgm_reset<<<1, 1, 0, C.s>>>(C.outer.st, tol, maxit, C.outer.m);
+  CKR(post_launch(C));
+  int cycles = 0;
+  long long kernels = 1;
+  for (bool first = true;; first = false) {
+    if (use_graph) {
+      const int gi = first ? 0 : 1;
+      if (!C.gexec[gi]) {
+        CKR(capture_cycle(C, first, &C.gexec[gi]));
+        C.cnt[gi][0] = C.cnt_top;
+        C.cnt[gi][1] = C.cnt_outer;
+        C.cnt[gi][2] = C.cnt_inner;
+      }
+      const int its0 = cycles == 0 ? 0 : C.hst->its;
+      const long long in0 = cycles == 0 ? 0 : C.hst->inner_total;
+      CK(cudaGraphLaunch(C.gexec[gi], C.s));
+      CKR(read_state(C, C.outer.st));
+      kernels += C.cnt[gi][0] + (C.hst->its - its0) * C.cnt[gi][1] + (C.hst->inner_total - in0) * C.cnt[gi][2];
+    } else {
+      const long long l0 = C.launches;
+      CKR(outer_cycle(C, first));
+      CKR(read_state(C, C.outer.st));
+      kernels += C.launches - l0;
+      if (getenv("HELM_DEBUG_COUNTS"))
+        fprintf(stderr, "[helm] eager cycle: kernels %lld its %d inner_total %lld\n", C.launches - l0, C.hst->its,
+                C.hst->inner_total);
+    }
+    ++cycles;
+    if (C.hst->conv || C.hst->its >= maxit) break;
+  }
+  if (use_graph) C.launches += kernels;
+  auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    const FgmState& s = *C.hst;
+    rep->outer_iterations = s.its;
+    rep->converged = s.conv;
+    rep->relres = s.relres;
+    rep->inner_solves = s.inner_solves;
+    rep->inner_iterations_total = s.inner_total;
+    rep->inner_iterations_max = s.inner_max;
+    rep->restarts = cycles - 1;
+    rep->seconds = std::chrono::duration<double>(t1 - t0).count();
+    rep->kernels = kernels;
+  }
+  return HELM_OK;
 }
 
 int helm_solve(helm_ctx C, const double* b, double* x, double tol, int maxit, helm_report* rep) {
   if (!C || !b || !x) return fail(HELM_EINVAL, "null argument");
   if (b == x) return fail(HELM_EINVAL, "x may not alias b");
-  if (maxit < 1 || !(tol > 0)) return fail(HELM_EINVAL, "bad tol/maxit");
-  int m = C->p.restart > 0 ? std::min(C->p.restart, maxit) : maxit;
-  if (C->outer.m < m || (C->outer.m > m && C->p.restart > 0)) {
-    size_t fr = 0, tot = 0;
-    if (C->outer.V) krylov_free(C->outer);
-    CK(cudaMemGetInfo(&fr, &tot));
-    const size_t per = 2 * C->L[0].n * sizeof(double2);
-    m = (int)std::max<size_t>(8, std::min<size_t>((size_t)m, fr / 2 / per));
-    CKR(krylov_alloc(C->outer, m, C->L[0].n));
+  if (maxit < 1 || !(tol >= 0)) return fail(HELM_EINVAL, "bad tol/maxit");
+  const size_t n = C->L[0].n;
+  CK(cudaMemcpyAsync(C->bbuf, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, C->s));
+  CK(cudaMemsetAsync(C->xbuf, 0, n * sizeof(double2), C->s));
+  // the graph runs on the private stream: order it after the caller's stream and back
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, C->s));
+  cudaStream_t user = C->s;
+  CK(cudaStreamWaitEvent(C->own, ev, 0));
+  C->s = C->own;
+  int r = solve_device(*C, tol, maxit, rep);
+  C->s = user;
+  if (r == HELM_OK) {
+    CK(cudaEventRecord(ev, C->own));
+    CK(cudaStreamWaitEvent(user, ev, 0));
+    CK(cudaMemcpyAsync(x, C->xbuf, n * sizeof(double2), cudaMemcpyDeviceToDevice, user));
+    CK(cudaStreamSynchronize(user));
   }
-  long long inner_total = 0;
-  int inner_max = 0, inner_solves = 0;
-  auto A = [&](const double2* u, double2* y) { return op_apply(*C, C->L[0], u, nullptr, y, 1.0, 0.0); };
-  auto P = [&](const double2* v, double2* z) {
-    int its = 0;
-    int r = adef1(*C, v, z, &its);
-    inner_total += its;
-    inner_max = std::max(inner_max, its);
-    inner_solves++;
-    return r;
-  };
-  auto t0 = std::chrono::steady_clock::now();
-  int its = 0, conv = 0, restarts = 0;
-  double relres = 0;
-  CKR(fgmres(*C, C->outer, A, P, (const double2*)b, (double2*)x, C->L[0].n, tol, maxit, &its, &relres, &conv,
-             &restarts));
-  CK(cudaStreamSynchronize(C->s));
-  auto t1 = std::chrono::steady_clock::now();
-  if (rep) {
-    rep->outer_iterations = its;
-    rep->converged = conv;
-    rep->relres = relres;
-    rep->inner_solves = inner_solves;
-    rep->inner_iterations_total = inner_total;
-    rep->inner_iterations_max = inner_max;
-    rep->restarts = restarts;
-    rep->seconds = std::chrono::duration<double>(t1 - t0).count();
-  }
-  return HELM_OK;
+  cudaEventDestroy(ev);
+  return r;
 }
 
 int helm_solve_host(helm_ctx C, const double* b_host, double* x_host, double tol, int maxit, helm_report* rep) {
   if (!C || !b_host || !x_host) return fail(HELM_EINVAL, "null argument");
+  if (maxit < 1 || !(tol >= 0)) return fail(HELM_EINVAL, "bad tol/maxit");
   const size_t n = C->L[0].n;
-  if (!C->bx) CKR(dalloc(&C->bx, n));
-  if (!C->xx) CKR(dalloc(&C->xx, n));
-  CK(cudaMemcpyAsync(C->bx, b_host, n * sizeof(double2), cudaMemcpyHostToDevice, C->s));
-  CKR(helm_solve(C, (const double*)C->bx, (double*)C->xx, tol, maxit, rep));
-  CK(cudaMemcpyAsync(x_host, C->xx, n * sizeof(double2), cudaMemcpyDeviceToHost, C->s));
-  CK(cudaStreamSynchronize(C->s));
-  return HELM_OK;
+  cudaStream_t user = C->s;
+  C->s = C->own;
+  CK(cudaStreamSynchronize(user));
+  CK(cudaMemcpyAsync(C->bbuf, b_host, n * sizeof(double2), cudaMemcpyHostToDevice, C->s));
+  CK(cudaMemsetAsync(C->xbuf, 0, n * sizeof(double2), C->s));
+  int r = solve_device(*C, tol, maxit, rep);
+  if (r == HELM_OK) {
+    CK(cudaMemcpyAsync(x_host, C->xbuf, n * sizeof(double2), cudaMemcpyDeviceToHost, C->s));
+    CK(cudaStreamSynchronize(C->s));
+  }
+  C->s = user;
+  return r;
 }
 
 int helm_flush_l2(helm_ctx C, size_t bytes) {
@@ -750,5 +941,99 @@ int helm_flush_l2(helm_ctx C, size_t bytes) {
 }
 
 long long helm_launch_count(helm_ctx C) { return C ? C->launches : 0; }
+
+int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, double* us_per_launch,
+                      double* bytes_per_launch) {
+  if (!C || reps < 1 || !us_per_launch) return fail(HELM_EINVAL, "bad argument");
+  helm_ctx_s& X = *C;
+  const Level& F = X.L[0];
+  const Level& G = X.L[1];
+  Fgm& K = X.inner;
+  double bytes = 0.0;
+  int* dn = nullptr;
+  const int lv = (which == HELM_KB_VC_DOWN || which == HELM_KB_VC_UP) ? arg : 0;
+  if ((which == HELM_KB_VC_DOWN || which == HELM_KB_VC_UP) && (lv < 0 || lv + 1 >= (int)X.L.size()))
+    return fail(HELM_EINVAL, "level %d has no coarser level", lv);
+  if (which == HELM_KB_GS_DOTS || which == HELM_KB_GS_UPDATE) {
+    if (arg < 1 || arg > K.m) return fail(HELM_EINVAL, "nvec must be in [1, inner_maxit]");
+    CKR(dalloc(&dn, 1));
+    const int v = arg - 1;   // kernels use nvec = *dn + 1
+    CK(cudaMemcpyAsync(dn, &v, sizeof(int), cudaMemcpyHostToDevice, X.s));
+  }
+  auto launch = [&]() -> int {
+    switch (which) {
+      case HELM_KB_APPLY_A:
+        bytes = (double)F.n * 40.0;
+        return op_apply(X, F, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
+      case HELM_KB_VC_DOWN: {
+        const Level& Fl = X.L[lv];
+        const Level& Gl = X.L[lv + 1];
+        bytes = (double)Fl.n * 40.0 + (double)Gl.n * 16.0;
+        dim3 gd((Gl.g.nx + DOWN_TX - 1) / DOWN_TX, (Gl.g.ny + DOWN_TY - 1) / DOWN_TY);
+        k_vc_down<DOWN_TX, DOWN_TY><<<gd, 256, 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
+                                                           X.p.omega, Fl.s, Gl.f);
+        return post_launch(X);
+      }
+      case HELM_KB_VC_UP: {
+        const Level& Fl = X.L[lv];
+        const Level& Gl = X.L[lv + 1];
+        bytes = (double)Fl.n * 56.0 + (double)Gl.n * 16.0;
+        dim3 gu((Fl.g.nx + UP_TX - 1) / UP_TX, (Fl.g.ny + UP_TY - 1) / UP_TY);
+        k_vc_up<UP_TX, UP_TY><<<gu, 256, 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1,
+                                                     X.p.beta2, X.p.omega, nullptr, DVec(lv == 0 ? X.bbuf : Fl.u));
+        return post_launch(X);
+      }
+      case HELM_KB_APPLY_E: {
+        const int R = (X.p.vectors == HELM_VECTORS_BILINEAR) ? 1 : 2;
+        (void)R;
+        // x + y, plus the wavenumbers: 4 fine k per coarse unknown (Galerkin) or 1 coarse k
+        const double kb = (X.p.coarse_op == HELM_COARSE_GALERKIN) ? (double)F.n * 8.0 : (double)G.n * 8.0;
+        bytes = (double)G.n * 32.0 + kb;
+        return apply_E(X, DVec(X.cc), DVec(), DVec(X.ce));
+      }
+      case HELM_KB_GS_DOTS:
+        bytes = (double)G.n * 16.0 * (arg + 1);
+        k_dcgs_dots<<<dim3(K.geo.gx, K.geo.gy), GS_THREADS, 0, X.s>>>(K.V, (long long)K.n, dn, 1,
+                                                                      DVec(K.V + (size_t)(arg - 1) * K.n),
+                                                                      DVec(K.V + (size_t)arg * K.n), (long long)K.n,
+                                                                      K.geo.chunk, K.part);
+        return post_launch(X);
+      case HELM_KB_GS_UPDATE: {
+        bytes = (double)G.n * 16.0 * (arg + 3);
+        k_dcgs_update<<<K.geo.gu, GS_THREADS, (size_t)(2 * K.m + 2) * sizeof(double2), X.s>>>(
+            K.V, (long long)K.n, dn, K.coef, K.sc2, DVec(K.V + (size_t)(arg - 1) * K.n), DVec(K.V + (size_t)arg * K.n),
+            (long long)K.n, K.part);
+        return post_launch(X);
+      }
+    }
+    return fail(HELM_EINVAL, "unknown kernel id %d", which);
+  };
+  if (which == HELM_KB_GS_UPDATE) {
+    CK(cudaMemsetAsync(K.coef, 0, (size_t)(2 * K.m + 4) * sizeof(double2), X.s));
+    const double2 sc[2] = {make_double2(1.0, 0.0), make_double2(0.0, 0.0)};
+    CK(cudaMemcpyAsync(K.sc2, sc, sizeof sc, cudaMemcpyHostToDevice, X.s));
+  }
+  CKR(launch());   // warm-up
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double total_ms = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    if (flush) CKR(helm_flush_l2(C, 256u << 20));
+    CK(cudaEventRecord(e0, X.s));
+    CKR(launch());
+    CK(cudaEventRecord(e1, X.s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    total_ms += ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (dn) cudaFree(dn);
+  *us_per_launch = 1e3 * total_ms / reps;
+  if (bytes_per_launch) *bytes_per_launch = bytes;
+  return HELM_OK;
+}
 
 }  // extern "C"

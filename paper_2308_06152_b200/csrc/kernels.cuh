@@ -29,6 +29,20 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // a
 
 enum { BC_DIRICHLET = 0, BC_SOMMERFELD = 1 };
 
+// A field pointer that may be indexed by a device-resident counter: address = p + (*idx) * stride.
+// Krylov kernels captured once into a CUDA graph read the current basis slot (V[j], Z[j]) this
+// way, so one graph serves every iteration of the device-controlled FGMRES loop.
+struct DVec {
+  double2* p;
+  const int* idx;
+  long long stride;
+  __host__ __device__ DVec(double2* p_ = nullptr) : p(p_), idx(nullptr), stride(0) {}
+  __host__ __device__ DVec(const double2* p_) : p(const_cast<double2*>(p_)), idx(nullptr), stride(0) {}
+  __host__ __device__ DVec(double2* p_, const int* i, long long s) : p(p_), idx(i), stride(s) {}
+  __device__ __forceinline__ double2* get() const { return idx ? p + (long long)(*idx) * stride : p; }
+};
+
+
 // Geometry of one grid level.
 struct Geo {
   int nx, ny;
@@ -78,11 +92,13 @@ __device__ __forceinline__ double2 stencil_apply(const Geo& g, const double2* __
 // ------------------------------------------------------------------ operator kernels
 // mode 0: y = Op u ;  mode 1: y = f - Op u (residual)
 template <int MODE>
-__global__ void k_apply_op(Geo g, const double2* __restrict__ u, const double2* __restrict__ f,
-                           double2* __restrict__ y, const double* __restrict__ k, double sr, double si) {
+__global__ void k_apply_op(Geo g, DVec uv, DVec fv, DVec yv, const double* __restrict__ k, double sr, double si) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ u = uv.get();
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
   const size_t p = (size_t)j * g.nx + i;
   Coef c = coef_at(g, i, j, k[p], sr, si);
   double2 v = stencil_apply(g, u, i, j, c);
@@ -91,23 +107,26 @@ __global__ void k_apply_op(Geo g, const double2* __restrict__ u, const double2* 
 }
 
 // u = omega * f / D   (first damped-Jacobi sweep from u = 0)
-__global__ void k_jacobi0(Geo g, const double2* __restrict__ f, double2* __restrict__ u,
+__global__ void k_jacobi0(Geo g, DVec fv, double2* __restrict__ u,
                           const double* __restrict__ k, double sr, double si, double omega) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ f = fv.get();
   const size_t p = (size_t)j * g.nx + i;
   Coef c = coef_at(g, i, j, k[p], sr, si);
   u[p] = cscale(omega, cdiv(f[p], c.ap));
 }
 
 // unew = u + omega * (f - M u) / D  (+ optional add of `q`, used to fuse z = M^-1 t + q)
-__global__ void k_jacobi(Geo g, const double2* __restrict__ u, const double2* __restrict__ f,
-                         double2* __restrict__ unew, const double* __restrict__ k, double sr, double si,
+__global__ void k_jacobi(Geo g, const double2* __restrict__ u, DVec fv,
+                         DVec unewv, const double* __restrict__ k, double sr, double si,
                          double omega, const double2* __restrict__ addq) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ unew = unewv.get();
   const size_t p = (size_t)j * g.nx + i;
   Coef c = coef_at(g, i, j, k[p], sr, si);
   double2 r = csub(f[p], stencil_apply(g, u, i, j, c));
@@ -142,7 +161,7 @@ __global__ void k_restrict(Geo gf, Geo gc, int o, const double2* __restrict__ v,
 //   y = P e  (MODE 0)  or  y = base + P e  (MODE 1)
 template <int MODE>
 __global__ void k_prolong(Geo gf, Geo gc, int o, const double2* __restrict__ e, const double2* __restrict__ base,
-                          double2* __restrict__ y) {
+                          DVec yv, const double2* __restrict__ addq) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= gf.nx || j >= gf.ny) return;
@@ -165,7 +184,8 @@ __global__ void k_prolong(Geo gf, Geo gc, int o, const double2* __restrict__ e, 
   }
   const size_t p = (size_t)j * gf.nx + i;
   if (MODE == 1) s = cadd(s, base[p]);
-  y[p] = s;
+  if (addq) s = cadd(s, addq[p]);
+  yv.get()[p] = s;
 }
 
 // Coarse wavenumber sampled at coincident fine nodes (re-discretisation, §5.1).
@@ -191,10 +211,11 @@ __device__ __forceinline__ double zrs() { return R == 1 ? 0.25 : 1.0; }
 
 // vc = RS * Z^T v  (gather of the (2R+1)^2 fine taps; out-of-array taps dropped, reading R4)
 template <int R>
-__global__ void k_restrict_z(Geo gf, Geo gc, int o, const double2* __restrict__ v, double2* __restrict__ vc) {
+__global__ void k_restrict_z(Geo gf, Geo gc, int o, DVec vv, double2* __restrict__ vc) {
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   if (I >= gc.nx || J >= gc.ny) return;
+  const double2* __restrict__ v = vv.get();
   const int ci = 2 * I + o, cj = 2 * J + o;
   double2 s = make_double2(0.0, 0.0);
 #pragma unroll
@@ -234,87 +255,83 @@ __global__ void k_prolong_z(Geo gf, Geo gc, int o, const double2* __restrict__ e
   y[p] = s;
 }
 
-// ------------------------------------------------------------------ Galerkin coarse stencil
-// E = (RS Z^T) A Z (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; §5.2.2 stencil
-// operation): its (2R+1)^2 coefficients per coarse node, evaluated once from the definition
-//   E[(I,J),(I+dx,J+dy)] = sum_a RS Z[a,(I,J)] sum_{b in nbr(a)} A[a,b] Z[b,(I+dx,J+dy)]
-// and stored SoA: coef[d*nc + p], d = (dy+R)*(2R+1) + (dx+R).
-template <int R>
-__global__ void k_galerkin_coef(Geo gf, Geo gc, int o, const double* __restrict__ kf, double2* __restrict__ coef) {
-  constexpr int W = 2 * R + 1;
-  const int I = blockIdx.x * blockDim.x + threadIdx.x;
-  const int J = blockIdx.y * blockDim.y + threadIdx.y;
-  if (I >= gc.nx || J >= gc.ny) return;
-  double2 acc[W * W];
-#pragma unroll
-  for (int d = 0; d < W * W; ++d) acc[d] = make_double2(0.0, 0.0);
-  const int ci = 2 * I + o, cj = 2 * J + o;
-  for (int b = -R; b <= R; ++b) {
-    const int aj = cj + b;
-    if (aj < 0 || aj >= gf.ny) continue;
-    for (int a = -R; a <= R; ++a) {
-      const int ai = ci + a;
-      if (ai < 0 || ai >= gf.nx) continue;
-      const double rw = zrs<R>() * zw<R>(a) * zw<R>(b);
-      Coef c = coef_at(gf, ai, aj, kf[(size_t)aj * gf.nx + ai], 1.0, 0.0);
-      const int bi[5] = {ai, ai - 1, ai + 1, ai, ai};
-      const int bjv[5] = {aj, aj, aj, aj - 1, aj + 1};
-      const double2 aval[5] = {c.ap, make_double2(c.aw, 0), make_double2(c.ae, 0), make_double2(c.as, 0),
-                               make_double2(c.an, 0)};
-      for (int q = 0; q < 5; ++q) {
-        if (q > 0 && aval[q].x == 0.0) continue;
-        const int xi = bi[q], yj = bjv[q];
-        if (xi < 0 || xi >= gf.nx || yj < 0 || yj >= gf.ny) continue;
-#pragma unroll
-        for (int dy = -R; dy <= R; ++dy) {
-          const int Jp = J + dy;
-          if (Jp < 0 || Jp >= gc.ny) continue;
-          const double wy = zw<R>(yj - (2 * Jp + o));
-          if (wy == 0.0) continue;
-#pragma unroll
-          for (int dx = -R; dx <= R; ++dx) {
-            const int Ip = I + dx;
-            if (Ip < 0 || Ip >= gc.nx) continue;
-            const double wx = zw<R>(xi - (2 * Ip + o));
-            if (wx == 0.0) continue;
-            const int d = (dy + R) * W + (dx + R);
-            acc[d] = cadd(acc[d], cscale(rw * wx * wy, aval[q]));
-          }
-        }
+// ------------------------------------------------------------------ Galerkin coarse operator
+// y = E x = RS Z^T A Z x (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; str-Glk §5.2.1,
+// Eq. 5.7a-c: interpolation, fine-grid operator, restriction) applied matrix-free in ONE kernel:
+// for a tile of TCX x TCY coarse outputs, x (coarse, with halo) -> t = Z x on the fine footprint
+// plus one node -> s = A t on the footprint -> y = RS Z^T s, all in shared memory.  HBM traffic
+// per coarse unknown: x 16 + k 4 x 8 + y 16 B (the paper's three passes, or a stored 25-point
+// stencil, would move ~10x more).  MODE 1: y = f - E x.
+__device__ __forceinline__ int ceildiv2(int a) { return (a >= 0) ? ((a + 1) >> 1) : -((-a) >> 1); }
+
+template <int R, int MODE, int TCX, int TCY>
+__global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
+                                                        DVec fv, DVec yv) {
+  constexpr int SX = 2 * TCX - 1 + 2 * R, SY = 2 * TCY - 1 + 2 * R;   // s = A t region
+  constexpr int TXR = SX + 2, TYR = SY + 2;                          // t = Z x region (A halo)
+  constexpr int CXW = TCX + 2 * R, CYW = TCY + 2 * R;                 // coarse x region
+  __shared__ double2 sx[CYW * CXW];
+  __shared__ double2 stt[TYR * TXR];
+  __shared__ double2 ss[SY * SX];
+  const double2* __restrict__ x = xv.get();
+  const int I0 = blockIdx.x * TCX, J0 = blockIdx.y * TCY;
+  const int fx0s = 2 * I0 + o - R, fy0s = 2 * J0 + o - R;
+  const int fx0t = fx0s - 1, fy0t = fy0s - 1;
+  const int cx0 = I0 - R, cy0 = J0 - R;
+  for (int t = threadIdx.x; t < CXW * CYW; t += blockDim.x) {
+    const int I = cx0 + t % CXW, J = cy0 + t / CXW;
+    sx[t] = (I >= 0 && I < gc.nx && J >= 0 && J < gc.ny) ? x[(size_t)J * gc.nx + I] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < TXR * TYR; t += blockDim.x) {
+    const int fx = fx0t + t % TXR, fy = fy0t + t / TXR;
+    double2 v = make_double2(0.0, 0.0);
+    if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
+      const int ri = fx - o, rj = fy - o;
+      const int ilo = ceildiv2(ri - R), ihi = (ri + R + 2 * 64) / 2 - 64;
+      const int jlo = ceildiv2(rj - R), jhi = (rj + R + 2 * 64) / 2 - 64;
+      for (int J = jlo; J <= jhi; ++J) {
+        const double wy = zw<R>(rj - 2 * J);
+        for (int I = ilo; I <= ihi; ++I)
+          v = cadd(v, cscale(wy * zw<R>(ri - 2 * I), sx[(J - cy0) * CXW + (I - cx0)]));
       }
     }
+    stt[t] = v;
   }
-  const size_t nc = (size_t)gc.nx * gc.ny;
-  const size_t p = (size_t)J * gc.nx + I;
-#pragma unroll
-  for (int d = 0; d < W * W; ++d) coef[d * nc + p] = acc[d];
-}
-
-// y = E x with a stored (2R+1)^2-point stencil (MODE 1: y = f - E x).
-template <int R, int MODE>
-__global__ void k_apply_stencil(Geo gc, const double2* __restrict__ coef, const double2* __restrict__ x,
-                                const double2* __restrict__ f, double2* __restrict__ y) {
-  constexpr int W = 2 * R + 1;
-  const int I = blockIdx.x * blockDim.x + threadIdx.x;
-  const int J = blockIdx.y * blockDim.y + threadIdx.y;
-  if (I >= gc.nx || J >= gc.ny) return;
-  const size_t nc = (size_t)gc.nx * gc.ny;
-  const size_t p = (size_t)J * gc.nx + I;
-  double2 s = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int dy = -R; dy <= R; ++dy) {
-    const int Jp = J + dy;
-    if (Jp < 0 || Jp >= gc.ny) continue;
-#pragma unroll
-    for (int dx = -R; dx <= R; ++dx) {
-      const int Ip = I + dx;
-      if (Ip < 0 || Ip >= gc.nx) continue;
-      const int d = (dy + R) * W + (dx + R);
-      s = cfma(coef[d * nc + p], x[(size_t)Jp * gc.nx + Ip], s);
+  __syncthreads();
+  for (int t = threadIdx.x; t < SX * SY; t += blockDim.x) {
+    const int ix = t % SX, iy = t / SX;
+    const int fx = fx0s + ix, fy = fy0s + iy;
+    double2 v = make_double2(0.0, 0.0);   // reading R4: restriction taps outside the array dropped
+    if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
+      const Coef c = coef_at(gf, fx, fy, kf[(size_t)fy * gf.nx + fx], 1.0, 0.0);
+      const int q = (iy + 1) * TXR + (ix + 1);
+      v = cmul(c.ap, stt[q]);
+      if (c.aw != 0.0) v = cadd(v, cscale(c.aw, stt[q - 1]));
+      if (c.ae != 0.0) v = cadd(v, cscale(c.ae, stt[q + 1]));
+      if (c.as != 0.0) v = cadd(v, cscale(c.as, stt[q - TXR]));
+      if (c.an != 0.0) v = cadd(v, cscale(c.an, stt[q + TXR]));
     }
+    ss[t] = v;
   }
-  if (MODE == 1) s = csub(f[p], s);
-  y[p] = s;
+  __syncthreads();
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
+  for (int t = threadIdx.x; t < TCX * TCY; t += blockDim.x) {
+    const int I = I0 + t % TCX, J = J0 + t / TCX;
+    if (I >= gc.nx || J >= gc.ny) continue;
+    const int ix = 2 * (I - I0) + R, iy = 2 * (J - J0) + R;
+    double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int b = -R; b <= R; ++b) {
+      const double wy = zw<R>(b);
+#pragma unroll
+      for (int a = -R; a <= R; ++a) s = cadd(s, cscale(wy * zw<R>(a), ss[(iy + b) * SX + ix + a]));
+    }
+    s = cscale(zrs<R>(), s);
+    const size_t p = (size_t)J * gc.nx + I;
+    y[p] = (MODE == 1) ? csub(f[p], s) : s;
+  }
 }
 
 // ------------------------------------------------------------------ ReD-Glk (§5.2.4)
@@ -366,11 +383,13 @@ __device__ double2 glk2_val(const Geo& g, const double2* __restrict__ x, const d
 
 // VARIANT 1: ReD-Glk1, VARIANT 2: ReD-Glk2 (reading R14: second-order rows scaled by 4).
 template <int VARIANT, int MODE>
-__global__ void k_apply_red_glk(Geo g, const double2* __restrict__ x, const double2* __restrict__ f,
-                                double2* __restrict__ y, const double* __restrict__ k) {
+__global__ void k_apply_red_glk(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ x = xv.get();
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
   const size_t p = (size_t)j * g.nx + i;
   bool use5;
   if (VARIANT == 1) use5 = (i >= 2 && i <= g.nx - 3 && j >= 2 && j <= g.ny - 3);
@@ -403,11 +422,13 @@ __global__ void k_apply_red_glk(Geo g, const double2* __restrict__ x, const doub
 // ReD-O4 (Eq. 5.11, reading R5: centre 5/H^2 - k^2) where the 5-wide cross fits,
 // second-order Helmholtz stencil elsewhere (reading R6).
 template <int MODE>
-__global__ void k_apply_red_o4(Geo g, const double2* __restrict__ x, const double2* __restrict__ f,
-                               double2* __restrict__ y, const double* __restrict__ k) {
+__global__ void k_apply_red_o4(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ x = xv.get();
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
   const size_t p = (size_t)j * g.nx + i;
   bool fits;
   if (g.bc == BC_DIRICHLET) fits = (i >= 1 && i <= g.nx - 2 && j >= 1 && j <= g.ny - 2);
@@ -521,10 +542,12 @@ __global__ void k_gj_extract(const double2* __restrict__ Aug, int n, double2* __
 }
 
 // y = Minv f, one warp per row.
-__global__ void k_gemv(const double2* __restrict__ Minv, int n, const double2* __restrict__ f, double2* __restrict__ y) {
+__global__ void k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv, const double2* __restrict__ addq) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n) return;
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
   const double2* row = Minv + (size_t)warp * n;
   double2 s = make_double2(0.0, 0.0);
   for (int c = lane; c < n; c += 32) s = cfma(row[c], f[c], s);
@@ -533,108 +556,13 @@ __global__ void k_gemv(const double2* __restrict__ Minv, int n, const double2* _
     s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
     s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
   }
-  if (lane == 0) y[warp] = s;
-}
-
-// ------------------------------------------------------------------ BLAS-1 (Krylov)
-// partial[c*nb + b] = sum over block b's slice of conj(V_c) w, for c in [c0, c0+NV)
-// V_c = V + c*ld.  Deterministic: fixed grid, fixed in-block tree, fixed second stage.
-template <int NV>
-__global__ void k_multidot_partial(const double2* __restrict__ V, size_t ld, int nvec, const double2* __restrict__ w,
-                                   size_t n, double2* __restrict__ partial) {
-  const int c0 = blockIdx.y * NV;
-  double2 acc[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) acc[q] = make_double2(0.0, 0.0);
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
-    const double2 we = w[e];
-#pragma unroll
-    for (int q = 0; q < NV; ++q)
-      if (c0 + q < nvec) {
-        const double2 v = V[(size_t)(c0 + q) * ld + e];
-        acc[q].x += v.x * we.x + v.y * we.y;
-        acc[q].y += v.x * we.y - v.y * we.x;
-      }
-  }
-  __shared__ double2 red[NV][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    double2 s = acc[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-    }
-    if (lane == 0) red[q][wid] = s;
-  }
-  __syncthreads();
-  if (wid == 0) {
-    const int nw = blockDim.x >> 5;
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      double2 s = lane < nw ? red[q][lane] : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-      }
-      if (lane == 0 && c0 + q < nvec) partial[(size_t)(c0 + q) * gridDim.x + blockIdx.x] = s;
-    }
-  }
-}
-
-// out[c] (+)= sum_b partial[c*nb + b]   (one warp per c).  If `accum`, adds to out.
-__global__ void k_multidot_final(const double2* __restrict__ partial, int nb, int nvec, double2* __restrict__ out,
-                                 int accum) {
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (c >= nvec) return;
-  double2 s = make_double2(0.0, 0.0);
-  for (int b = lane; b < nb; b += 32) s = cadd(s, partial[(size_t)c * nb + b]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-  }
-  if (lane == 0) out[c] = accum ? cadd(out[c], s) : s;
-}
-
-// w += sign * sum_c coeff[c] * V_c   (sign = -1 for Gram-Schmidt, +1 for x += Z y)
-__global__ void k_multi_axpy(const double2* __restrict__ V, size_t ld, int nvec, const double2* __restrict__ coeff,
-                             double sign, double2* __restrict__ w, size_t n) {
-  extern __shared__ double2 sc[];
-  for (int c = threadIdx.x; c < nvec; c += blockDim.x) sc[c] = cscale(sign, coeff[c]);
-  __syncthreads();
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
-    double2 s = w[e];
-    for (int c = 0; c < nvec; ++c) s = cfma(sc[c], V[(size_t)c * ld + e], s);
-    w[e] = s;
-  }
-}
-
-// v = w / sqrt(re(nrm2[0]))   (nrm2 computed on device; no host round trip)
-__global__ void k_normalize(const double2* __restrict__ w, const double2* __restrict__ nrm2, double2* __restrict__ v,
-                            size_t n) {
-  const double s = 1.0 / sqrt(nrm2[0].x);
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
-    v[e] = cscale(s, w[e]);
-}
-
-__global__ void k_scale_copy(const double2* __restrict__ x, double s, double2* __restrict__ y, size_t n) {
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
-    y[e] = cscale(s, x[e]);
+  if (lane == 0) y[warp] = addq ? cadd(s, addq[warp]) : s;
 }
 
 // y = a + b
 __global__ void k_add(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ y, size_t n) {
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     y[e] = cadd(a[e], b[e]);
-}
-
-__global__ void k_l2flush(uint4* buf, size_t n, unsigned v) {
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
-    buf[e] = make_uint4(v, v, v, v);
 }
 
 }  // namespace helm

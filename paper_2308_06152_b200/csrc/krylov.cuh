@@ -1,0 +1,559 @@
+// Device-resident flexible GMRES (Algorithm 1 in flexible form, §6.3): the Arnoldi
+// process, the Givens-rotated Hessenberg least-squares problem and the convergence test all
+// live on the device, so the whole solve (outer loop, and the inner coarse solve nested in
+// every outer iteration) runs as one CUDA graph with conditional while nodes and no host
+// round trip per iteration.
+//
+// Orthogonalisation (reading R13): classical Gram-Schmidt applied twice with the
+// second pass delayed by one iteration (DCGS2, Bielich-Langou-Thomas-Swirydowicz-Yamazaki-
+// Boman): iteration j projects w = A z_j against the final V_0..V_{j-1} and the not yet
+// reorthogonalised v~_j while, in the same two sweeps over the basis, it reorthogonalises v~_j:
+//   pass 1: a = V^H v~_j, b = V^H w                      (one read of V)
+//   pass 2: v_j = (v~_j - V a)/beta, w' = w - V b - h_jj v_j  (one read of V)
+// Column j-1 of the Hessenberg matrix is corrected for the reorthogonalisation of v~_j and its
+// Givens rotation recomputed; FGMRES tolerates the preconditioned vectors z_j having been formed
+// from v~_j (the relation A Z = V H holds for any Z).  The reductions are deterministic (fixed
+// chunking, fixed warp trees, one warp per output in a second stage).
+#pragma once
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace helm {
+
+constexpr int GS_NV = 8;         // basis vectors per sweep of a chunk in the dot pass
+constexpr int GS_THREADS = 256;
+constexpr int GS_WARPS = GS_THREADS / 32;
+
+struct FgmState {
+  int j;        // current Arnoldi column
+  int ncols;    // columns completed in this cycle
+  int its;      // iterations over all cycles
+  int done;     // loop finished (converged, breakdown, maxit or basis full)
+  int conv;     // converged (relres <= tol or happy breakdown)
+  int reorth;   // this column needs the second Gram-Schmidt pass
+  int nreorth;  // columns that took it
+  int maxit, m;
+  int cond;     // mirror of the graph conditional (host-loop mode reads it)
+  double tol, bnorm, beta, relres, hn, inv_hn, inv_beta;
+  // inner-solve statistics accumulated into the outer state
+  long long inner_total;
+  int inner_max, inner_solves;
+};
+
+__device__ __forceinline__ double2 warp_sum2(double2 s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+  }
+  return s;
+}
+
+// Launch geometry of the Gram-Schmidt passes for a vector length n (host side).
+struct GsGeom {
+  long long chunk;  // elements per dots block (x)
+  int gx, gy;       // dots grid: element chunks x vector slices
+  int gu;           // update grid (blocks of 32 elements x 8 vector slices)
+};
+
+inline GsGeom gs_geom(long long n, int sms) {
+  GsGeom g;
+  long long chunk = (n + 1023) / 1024;
+  chunk = ((chunk + 127) / 128) * 128;
+  if (chunk < 256) chunk = 256;
+  g.chunk = chunk;
+  g.gx = (int)((n + chunk - 1) / chunk);
+  const int target = 4 * sms;
+  g.gy = std::max(1, std::min(32, (target + g.gx - 1) / g.gx));
+  const long long tiles = (n + 31) / 32;
+  g.gu = (int)std::max<long long>(1, std::min<long long>(tiles, (long long)target));
+  return g;
+}
+
+// Pass "dots": part[c * gx + bx] = sum over chunk bx of conj(V_c) . w, for c < nvec, and, if
+// want_norm, part[nvec * gx + bx] = chunk sum of |w|^2.  Warp (y, w) of the grid handles the
+// outputs c = 8 y + w + 8 gy t; each lane streams 4 elements per step (coalesced 512 B rows).
+__global__ void __launch_bounds__(GS_THREADS) k_gs_dots(const double2* __restrict__ V, long long ld,
+                                                        const int* __restrict__ nptr, int nadd, DVec wv, long long n,
+                                                        long long chunk, int want_norm, double2* __restrict__ part,
+                                                        const int* __restrict__ gate) {
+  if (gate && !*gate) return;
+  const int nvec = (nptr ? *nptr : 0) + nadd;
+  const int ntot = nvec + (want_norm ? 1 : 0);
+  const double2* __restrict__ w = wv.get();
+  const long long e0 = (long long)blockIdx.x * chunk;
+  const long long e1 = min(n, e0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx = gridDim.x;
+  for (int c = blockIdx.y * GS_WARPS + warp; c < ntot; c += gridDim.y * GS_WARPS) {
+    double2 acc = make_double2(0.0, 0.0);
+    const bool isnorm = (c == nvec);
+    const double2* __restrict__ vc = V + (long long)c * ld;
+    for (long long e = e0 + lane; e < e1; e += 128) {
+      double2 vv[4], ww[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const long long ee = e + 32 * t;
+        ww[t] = ee < e1 ? w[ee] : make_double2(0.0, 0.0);
+        vv[t] = ee < e1 ? (isnorm ? ww[t] : vc[ee]) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        acc.x = fma(vv[t].x, ww[t].x, fma(vv[t].y, ww[t].y, acc.x));
+        acc.y = fma(vv[t].x, ww[t].y, fma(-vv[t].y, ww[t].x, acc.y));
+      }
+    }
+    acc = warp_sum2(acc);
+    if (lane == 0) part[(long long)c * gx + blockIdx.x] = acc;
+  }
+}
+
+// out[c] = sum of the P partials of output c, c < mult (*nptr + nadd) + extra; one warp per output.
+__global__ void __launch_bounds__(256) k_gs_reduce(const double2* __restrict__ part, long long P,
+                                                   const int* __restrict__ nptr, int nadd, int mult, int extra,
+                                                   double2* __restrict__ out, const int* __restrict__ gate) {
+  if (gate && !*gate) return;
+  const int ntot = mult * ((nptr ? *nptr : 0) + nadd) + extra;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= ntot) return;
+  double2 s = make_double2(0.0, 0.0);
+  for (long long b = lane; b < P; b += 32) s = cadd(s, part[(long long)c * P + b]);
+  s = warp_sum2(s);
+  if (lane == 0) out[c] = s;
+}
+
+// Pass "update": w_out = (w_in or 0) + sign * sum_{c < nvec} coeff[c] V_c, and, if want_norm,
+// per-block partials of ||w_out||^2 into part[block].  A block owns tiles of 32 elements; its
+// 8 warps split the basis (warp s takes c = s, s+8, ...) and their sums are combined in a
+// fixed order through shared memory.  w_in may alias w_out.
+__global__ void __launch_bounds__(GS_THREADS) k_gs_update(const double2* __restrict__ V, long long ld,
+                                                          const int* __restrict__ nptr, int nadd,
+                                                          const double2* __restrict__ coeff, double sign, DVec winv,
+                                                          DVec woutv, long long n, int want_norm,
+                                                          double2* __restrict__ part, const int* __restrict__ gate) {
+  extern __shared__ double2 sc[];
+  __shared__ double2 red[GS_WARPS][32];
+  __shared__ double nred[32];
+  if (gate && !*gate) return;
+  const int nvec = (nptr ? *nptr : 0) + nadd;
+  const double2* win = winv.get();
+  double2* wout = woutv.get();
+  for (int c = threadIdx.x; c < nvec; c += GS_THREADS) sc[c] = cscale(sign, coeff[c]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  double nrm = 0.0;
+  const long long tiles = (n + 31) / 32;
+  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const long long e = tile * 32 + lane;
+    double2 s = make_double2(0.0, 0.0);
+    if (e < n) {
+      const double2* vp = V + e;
+      int c = sl;
+      for (; c + 8 * 3 < nvec; c += 8 * 4) {
+        const double2 v0 = vp[(long long)(c + 0) * ld];
+        const double2 v1 = vp[(long long)(c + 8) * ld];
+        const double2 v2 = vp[(long long)(c + 16) * ld];
+        const double2 v3 = vp[(long long)(c + 24) * ld];
+        s = cfma(sc[c + 0], v0, s);
+        s = cfma(sc[c + 8], v1, s);
+        s = cfma(sc[c + 16], v2, s);
+        s = cfma(sc[c + 24], v3, s);
+      }
+      for (; c < nvec; c += 8) s = cfma(sc[c], vp[(long long)c * ld], s);
+    }
+    red[sl][lane] = s;
+    __syncthreads();
+    if (sl == 0 && e < n) {
+      double2 t = win ? win[e] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < GS_WARPS; ++q) t = cadd(t, red[q][lane]);
+      wout[e] = t;
+      nrm = fma(t.x, t.x, fma(t.y, t.y, nrm));
+    }
+    __syncthreads();
+  }
+  if (want_norm && sl == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if (lane == 0) part[blockIdx.x] = make_double2(nrm, 0.0);
+  }
+  (void)nred;
+}
+
+__device__ __forceinline__ void fgm_set_cond(FgmState* st, cudaGraphConditionalHandle h, int use_h, int v) {
+  st->cond = v;
+  if (use_h) cudaGraphSetConditional(h, v);
+}
+
+// ---------------------------------------------------------------- delayed CGS2 (two passes)
+// Pass 1 of iteration j: for c <= j (V_j = the not yet reorthogonalised v~_j):
+//   part[(2c) gx + bx] = chunk sum of conj(V_c) . v~_j,  part[(2c+1) gx + bx] = conj(V_c) . w
+// One read of the basis; v~_j and w come from L1/L2.
+__global__ void __launch_bounds__(GS_THREADS) k_dcgs_dots(const double2* __restrict__ V, long long ld,
+                                                          const int* __restrict__ nptr, int nadd, DVec xv, DVec wv,
+                                                          long long n, long long chunk, double2* __restrict__ part) {
+  const int nvec = (nptr ? *nptr : 0) + nadd;
+  const double2* __restrict__ x = xv.get();
+  const double2* __restrict__ w = wv.get();
+  const long long e0 = (long long)blockIdx.x * chunk;
+  const long long e1 = min(n, e0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx = gridDim.x;
+  for (int c = blockIdx.y * GS_WARPS + warp; c < nvec; c += gridDim.y * GS_WARPS) {
+    double2 ax = make_double2(0.0, 0.0), aw = make_double2(0.0, 0.0);
+    const double2* __restrict__ vc = V + (long long)c * ld;
+    for (long long e = e0 + lane; e < e1; e += 128) {
+      double2 vv[4], xx[4], ww[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const long long ee = e + 32 * t;
+        const bool ok = ee < e1;
+        vv[t] = ok ? vc[ee] : make_double2(0.0, 0.0);
+        xx[t] = ok ? x[ee] : make_double2(0.0, 0.0);
+        ww[t] = ok ? w[ee] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        ax.x = fma(vv[t].x, xx[t].x, fma(vv[t].y, xx[t].y, ax.x));
+        ax.y = fma(vv[t].x, xx[t].y, fma(-vv[t].y, xx[t].x, ax.y));
+        aw.x = fma(vv[t].x, ww[t].x, fma(vv[t].y, ww[t].y, aw.x));
+        aw.y = fma(vv[t].x, ww[t].y, fma(-vv[t].y, ww[t].x, aw.y));
+      }
+    }
+    ax = warp_sum2(ax);
+    aw = warp_sum2(aw);
+    if (lane == 0) {
+      part[(long long)(2 * c) * gx + blockIdx.x] = ax;
+      part[(long long)(2 * c + 1) * gx + blockIdx.x] = aw;
+    }
+  }
+}
+
+// Pass 2 of iteration j (j = *jptr): with coef[2c] = a_c, coef[2c+1] = b_c (c < j) and the
+// scalars sc2 = {1/beta, h_jj}:
+//   v_j = (v~_j - sum_c a_c V_c) / beta          (written over v~_j: the delayed reorthogonalisation)
+//   w'  = w - sum_c b_c V_c - h_jj v_j           (written over w)
+// and per-block partials of ||w'||^2 into part[block].  One read of V_0..V_{j-1}.
+__global__ void __launch_bounds__(GS_THREADS) k_dcgs_update(const double2* __restrict__ V, long long ld,
+                                                            const int* __restrict__ jptr,
+                                                            const double2* __restrict__ coef,
+                                                            const double2* __restrict__ sc2, DVec xv, DVec wv,
+                                                            long long n, double2* __restrict__ part) {
+  extern __shared__ double2 sab[];
+  __shared__ double2 reda[GS_WARPS][32];
+  __shared__ double2 redb[GS_WARPS][32];
+  const int j = *jptr;
+  double2* x = xv.get();
+  double2* w = wv.get();
+  for (int c = threadIdx.x; c < 2 * j; c += GS_THREADS) sab[c] = coef[c];
+  __syncthreads();
+  const double ib = sc2[0].x;
+  const double2 hjj = sc2[1];
+  const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  double nrm = 0.0;
+  const long long tiles = (n + 31) / 32;
+  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const long long e = tile * 32 + lane;
+    double2 sa = make_double2(0.0, 0.0), sb = make_double2(0.0, 0.0);
+    if (e < n) {
+      const double2* vp = V + e;
+      int c = sl;
+      for (; c + 8 * 3 < j; c += 8 * 4) {
+        const double2 v0 = vp[(long long)(c + 0) * ld];
+        const double2 v1 = vp[(long long)(c + 8) * ld];
+        const double2 v2 = vp[(long long)(c + 16) * ld];
+        const double2 v3 = vp[(long long)(c + 24) * ld];
+        sa = cfma(sab[2 * (c + 0)], v0, sa);
+        sb = cfma(sab[2 * (c + 0) + 1], v0, sb);
+        sa = cfma(sab[2 * (c + 8)], v1, sa);
+        sb = cfma(sab[2 * (c + 8) + 1], v1, sb);
+        sa = cfma(sab[2 * (c + 16)], v2, sa);
+        sb = cfma(sab[2 * (c + 16) + 1], v2, sb);
+        sa = cfma(sab[2 * (c + 24)], v3, sa);
+        sb = cfma(sab[2 * (c + 24) + 1], v3, sb);
+      }
+      for (; c < j; c += 8) {
+        const double2 v0 = vp[(long long)c * ld];
+        sa = cfma(sab[2 * c], v0, sa);
+        sb = cfma(sab[2 * c + 1], v0, sb);
+      }
+    }
+    reda[sl][lane] = sa;
+    redb[sl][lane] = sb;
+    __syncthreads();
+    if (sl == 0 && e < n) {
+      double2 ta = make_double2(0.0, 0.0), tb = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < GS_WARPS; ++q) {
+        ta = cadd(ta, reda[q][lane]);
+        tb = cadd(tb, redb[q][lane]);
+      }
+      const double2 v = cscale(ib, cadd(x[e], ta));
+      const double2 wp = csub(cadd(w[e], tb), cmul(hjj, v));
+      x[e] = v;
+      w[e] = wp;
+      nrm = fma(wp.x, wp.x, fma(wp.y, wp.y, nrm));
+    }
+    __syncthreads();
+  }
+  if (sl == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if (lane == 0) part[blockIdx.x] = make_double2(nrm, 0.0);
+  }
+}
+
+// Apply rotations G_0..G_{nrot-1} to a raw Hessenberg column (in shared memory, lane 0).
+__device__ __forceinline__ double2 rotate_column(double2* col, int nrot, const double* scs, const double2* ssn) {
+  double2 a = col[0];
+  for (int i = 0; i < nrot; ++i) {
+    const double2 b = col[i + 1];
+    const double c = scs[i];
+    const double2 s = ssn[i];
+    col[i] = cadd(cscale(c, a), cmul(s, b));
+    a = csub(cscale(c, b), cmul(make_double2(s.x, -s.y), a));
+  }
+  return a;   // rotated entry at position nrot (before the new rotation)
+}
+
+// New rotation annihilating the real sub-diagonal hn under entry a; updates g, returns |g_{j+1}|.
+__device__ __forceinline__ double new_rotation(int j, double2 a, double hn, double* cs, double2* sn, double2* g,
+                                               double2* colj) {
+  const double am = sqrt(a.x * a.x + a.y * a.y);
+  const double den = sqrt(am * am + hn * hn);
+  double c;
+  double2 s;
+  if (am == 0.0) {
+    c = 0.0;
+    s = make_double2(1.0, 0.0);
+  } else {
+    c = am / den;
+    s = make_double2(a.x / am * hn / den, a.y / am * hn / den);
+  }
+  cs[j] = c;
+  sn[j] = s;
+  *colj = cadd(cscale(c, a), cscale(hn, s));
+  const double2 gj = g[j];
+  const double2 gn1 = make_double2(-(s.x * gj.x + s.y * gj.y), -(s.x * gj.y - s.y * gj.x));  // -conj(s) g_j
+  g[j + 1] = gn1;
+  g[j] = cscale(c, gj);
+  return sqrt(gn1.x * gn1.x + gn1.y * gn1.y);
+}
+
+__host__ __device__ inline size_t dcgs_smem(int m) { return (size_t)(2 * m + 4) * 16 + (size_t)(m + 1) * 8; }
+
+// Step A (after pass 1): beta, h_jj, the pass-2 coefficients, and the delayed correction of
+// column j-1:  A z_{j-1} = V h + h_{j,j-1} v~_j = V (h + h_{j,j-1} a) + (h_{j,j-1} beta) v_j.
+// The rotation of column j-1 is undone on g and recomputed from the corrected column.
+// dots[2c] = a_c = V_c^H v~_j, dots[2c+1] = b_c = V_c^H w (c <= j); out: coef (a, b for c < j),
+// sc2 = {1/beta, h_jj}.  rawc holds the raw (unrotated) column j-1 from step B.
+__global__ void __launch_bounds__(32) k_dcgs_stepA(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                                   const double2* __restrict__ dots, double2* __restrict__ coef,
+                                                   double2* __restrict__ sc2, double2* __restrict__ rawc) {
+  extern __shared__ double2 sdc[];
+  const int m = st->m;
+  double2* scol = sdc;                       // m + 2
+  double2* ssn = sdc + (m + 2);              // m + 2
+  double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
+  const int lane = threadIdx.x;
+  const int j = st->j;
+  // ||a||^2 and a^H b over c < j
+  double na = 0.0;
+  double2 ab = make_double2(0.0, 0.0);
+  for (int c = lane; c < j; c += 32) {
+    const double2 a = dots[2 * c], b = dots[2 * c + 1];
+    na = fma(a.x, a.x, fma(a.y, a.y, na));
+    ab.x = fma(a.x, b.x, fma(a.y, b.y, ab.x));
+    ab.y = fma(a.x, b.y, fma(-a.y, b.x, ab.y));
+    coef[2 * c] = make_double2(-a.x, -a.y);   // pass 2 accumulates +coef * V
+    coef[2 * c + 1] = make_double2(-b.x, -b.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
+  ab = warp_sum2(ab);
+  const double alpha = dots[2 * j].x;
+  const double2 d = dots[2 * j + 1];
+  double b2 = alpha - na;
+  if (!(b2 > 0.0)) b2 = alpha;               // guard (cannot happen for an orthonormal basis)
+  const double beta = sqrt(b2);
+  const double2 hjj = cscale(1.0 / beta, csub(d, ab));
+  if (lane == 0) {
+    sc2[0] = make_double2(1.0 / beta, 0.0);
+    sc2[1] = hjj;
+    if (j == 0) g[0] = cscale(beta, g[0]);   // r = ||r|| v~_0 = (||r|| beta) v_0
+  }
+  if (j == 0) return;
+  // delayed correction of column j-1
+  const int jm = j - 1;
+  const double hold = rawc[j].x;             // h_{j,j-1} (real)
+  for (int c = lane; c < j; c += 32) {
+    const double2 a = dots[2 * c];
+    scol[c] = cadd(rawc[c], cscale(hold, a));
+  }
+  for (int i = lane; i < jm; i += 32) {
+    ssn[i] = sn[i];
+    scs[i] = cs[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const double hnew = hold * beta;
+    scol[j] = make_double2(hnew, 0.0);
+    // undo the old rotation G_{j-1} on g: g_{j-1}^old = c g_{j-1} - s g_j
+    const double c0 = cs[jm];
+    const double2 s0 = sn[jm];
+    const double2 gjm = g[jm], gj = g[j];
+    g[jm] = csub(cscale(c0, gjm), cmul(s0, gj));
+    g[j] = make_double2(0.0, 0.0);
+    for (int c = 0; c <= j; ++c) rawc[c] = scol[c];   // corrected raw column (kept for the record)
+    const double2 a = rotate_column(scol, jm, scs, ssn);
+    double2 hjj1;
+    const double gn = new_rotation(jm, a, hnew, cs, sn, g, &hjj1);
+    scol[jm] = hjj1;
+    scol[j] = make_double2(0.0, 0.0);
+    st->relres = st->bnorm > 0.0 ? gn / st->bnorm : 0.0;
+  }
+  __syncwarp();
+  const int ld = m + 1;
+  double2* Hc = H + (long long)jm * ld;
+  for (int i = lane; i <= j; i += 32) Hc[i] = scol[i];
+}
+
+// Step B (after pass 2): column j = [b_0..b_{j-1}, h_jj] with h_{j+1,j} = ||w'|| (from the
+// pass-2 partials), its rotations, the residual estimate and the loop decision.
+__global__ void __launch_bounds__(32) k_dcgs_stepB(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                                   const double2* __restrict__ dots, const double2* __restrict__ sc2,
+                                                   const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
+                                                   cudaGraphConditionalHandle h, int use_h) {
+  extern __shared__ double2 sdc[];
+  const int m = st->m;
+  double2* scol = sdc;
+  double2* ssn = sdc + (m + 2);
+  double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
+  const int lane = threadIdx.x;
+  const int j = st->j;
+  double nsum = 0.0;
+  for (int b = lane; b < np; b += 32) nsum += npart[b].x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+  const double hn = sqrt(fmax(nsum, 0.0));
+  for (int c = lane; c < j; c += 32) scol[c] = dots[2 * c + 1];
+  for (int i = lane; i < j; i += 32) {
+    ssn[i] = sn[i];
+    scs[i] = cs[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    scol[j] = sc2[1];
+    for (int c = 0; c <= j; ++c) rawc[c] = scol[c];
+    rawc[j + 1] = make_double2(hn, 0.0);
+    const double2 a = rotate_column(scol, j, scs, ssn);
+    double2 rjj;
+    const double gn = new_rotation(j, a, hn, cs, sn, g, &rjj);
+    scol[j] = rjj;
+    scol[j + 1] = make_double2(0.0, 0.0);
+    st->its += 1;
+    st->ncols = j + 1;
+    st->relres = st->bnorm > 0.0 ? gn / st->bnorm : 0.0;
+    st->hn = hn;
+    st->inv_hn = hn > 0.0 ? 1.0 / hn : 0.0;
+    int done = 0;
+    if (st->relres <= st->tol || hn == 0.0) {
+      done = 1;
+      st->conv = 1;
+    } else if (st->its >= st->maxit || j + 1 >= st->m) {
+      done = 1;
+    }
+    st->done = done;
+    st->j = j + 1;
+    fgm_set_cond(st, h, use_h, !done);
+  }
+  __syncwarp();
+  const int ld = m + 1;
+  double2* Hc = H + (long long)j * ld;
+  for (int i = lane; i <= j + 1; i += 32) Hc[i] = scol[i];
+}
+
+// y = x * (*scale)   (x may alias y; DVec slots)
+__global__ void k_scale_dvec(DVec xv, const double* __restrict__ scale, DVec yv, long long n,
+                             const int* __restrict__ skip_if) {
+  if (skip_if && *skip_if) return;
+  const double s = *scale;
+  const double2* x = xv.get();
+  double2* y = yv.get();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    y[e] = cscale(s, x[e]);
+}
+
+
+// Start of a cycle: beta = ||r|| from nrm2 (real part); set_bnorm: bnorm = beta (zero initial
+// guess, first cycle).  Resets the cycle (j = 0, g_0 = beta) and sets the loop condition.
+__global__ void k_fgm_begin(FgmState* st, const double2* __restrict__ nrm2, int set_bnorm, double2* __restrict__ g,
+                            cudaGraphConditionalHandle h, int use_h) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double beta = sqrt(fmax(nrm2[0].x, 0.0));
+  if (set_bnorm) st->bnorm = beta;
+  st->beta = beta;
+  st->j = 0;
+  st->ncols = 0;
+  st->reorth = 0;
+  g[0] = make_double2(beta, 0.0);
+  const double bn = st->bnorm;
+  st->relres = bn > 0.0 ? beta / bn : 0.0;
+  st->inv_beta = beta > 0.0 ? 1.0 / beta : 0.0;
+  int done = 0;
+  if (bn == 0.0 || st->relres <= st->tol) {
+    done = 1;
+    st->conv = 1;
+  } else if (st->its >= st->maxit) {
+    done = 1;
+  }
+  st->done = done;
+  fgm_set_cond(st, h, use_h, !done);
+}
+
+// Back substitution y = R^{-1} g over the ncols completed columns (one warp), and the
+// inner-solve statistics when `outer` is given.
+__global__ void k_fgm_backsub(FgmState* st, const double2* __restrict__ H, const double2* __restrict__ g,
+                              double2* __restrict__ y, FgmState* outer) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int mm = st->ncols;
+  const int ld = st->m + 1;
+  for (int i = mm - 1; i >= 0; --i) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = i + 1 + lane; q < mm; q += 32) s = cfma(H[(long long)q * ld + i], y[q], s);
+    s = warp_sum2(s);
+    if (lane == 0) y[i] = cdiv(csub(g[i], s), H[(long long)i * ld + i]);
+    __syncwarp();
+  }
+  if (lane == 0 && outer) {
+    outer->inner_total += st->its;
+    outer->inner_max = max(outer->inner_max, st->its);
+    outer->inner_solves += 1;
+  }
+}
+
+// Reset a state at the start of a solve: its = 0, conv = 0, tol/maxit from the host values.
+__global__ void k_fgm_reset(FgmState* st, double tol, int maxit, int m) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  st->its = 0;
+  st->conv = 0;
+  st->done = 0;
+  st->nreorth = 0;
+  st->tol = tol;
+  st->maxit = maxit;
+  st->m = m;
+  st->inner_total = 0;
+  st->inner_max = 0;
+  st->inner_solves = 0;
+  st->relres = 0.0;
+}
+
+__global__ void k_l2flush(uint4* buf, size_t n, unsigned v) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    buf[e] = make_uint4(v, v, v, v);
+}
+
+}  // namespace helm

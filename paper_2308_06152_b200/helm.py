@@ -29,13 +29,15 @@ class helm_params(ctypes.Structure):
     _fields_ = [("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("omega", ctypes.c_double),
                 ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("coarse_op", ctypes.c_int),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int), ("max_levels", ctypes.c_int),
-                ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int)]
+                ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int),
+                ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int)]
 
 
 class helm_report(ctypes.Structure):
     _fields_ = [("outer_iterations", ctypes.c_int), ("converged", ctypes.c_int), ("relres", ctypes.c_double),
                 ("inner_solves", ctypes.c_int), ("inner_iterations_total", ctypes.c_longlong),
-                ("inner_iterations_max", ctypes.c_int), ("restarts", ctypes.c_int), ("seconds", ctypes.c_double)]
+                ("inner_iterations_max", ctypes.c_int), ("restarts", ctypes.c_int), ("seconds", ctypes.c_double),
+                ("kernels", ctypes.c_longlong)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -63,6 +65,7 @@ EXPORTS = {
     "helm_solve_host": (_I, [_P, _P, _P, _D, _I, ctypes.POINTER(helm_report)]),
     "helm_flush_l2": (_I, [_P, ctypes.c_size_t]),
     "helm_launch_count": (ctypes.c_longlong, [_P]),
+    "helm_bench_kernel": (_I, [_P, _I, _I, _I, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "helm_last_error": (ctypes.c_char_p, []),
     "helm_build_info": (ctypes.c_char_p, []),
 }
@@ -233,6 +236,15 @@ class Helm:
 
     def helm_flush_l2(self, nbytes=256 << 20):
         _check(self.lib.helm_flush_l2(self.ctx, nbytes))
+
+    KERNELS = {"apply_A": 0, "vc_down": 1, "vc_up": 2, "apply_E": 3, "gs_dots": 4, "gs_update": 5}
+
+    def helm_bench_kernel(self, which, arg=1, reps=20, flush=True):
+        """(mean us per launch, algorithmic bytes per launch) of one kernel at this context's sizes."""
+        us, nb = _D(), _D()
+        _check(self.lib.helm_bench_kernel(self.ctx, self.KERNELS.get(which, which), int(arg), int(reps), int(flush),
+                                          ctypes.byref(us), ctypes.byref(nb)))
+        return us.value, nb.value
 
     def helm_launch_count(self):
         return int(self.lib.helm_launch_count(self.ctx))

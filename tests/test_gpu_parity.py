@@ -107,12 +107,26 @@ def test_coarse_operator_and_vectors(lib, vec, op):
 
 
 def test_vcycle(case):
+    """Fused down/up kernels + single-CTA tail (default), every starting level."""
     p, H = case
     levels = oracle.build_hierarchy(p.k, p.h, p.bc)
-    for l in range(min(2, len(levels))):
+    for l in range(len(levels)):
         f = random_field(levels[l].shape, 40 + l)
         u = H.vcycle(l, gpu(f)).cpu().numpy()
-        assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11
+        assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11, l
+
+
+@pytest.mark.parametrize("nu,tail", [((1, 1), 0), ((2, 2), 8192), ((2, 2), 0), ((1, 0), 8192), ((3, 1), 0)])
+def test_vcycle_variants(lib, nu, tail):
+    """Generic sweep counts (unfused kernels) and the per-level path without the tail."""
+    for p in (GRIDS[1], GRIDS[2], GRIDS[5]):
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"nu_pre": nu[0], "nu_post": nu[1], "tail_max_n": tail})
+        levels = oracle.build_hierarchy(p.k, p.h, p.bc)
+        for l in range(min(3, len(levels))):
+            f = random_field(levels[l].shape, 50 + l)
+            u = H.vcycle(l, gpu(f)).cpu().numpy()
+            assert rel(u, oracle.vcycle(levels, f, l, nu_pre=nu[0], nu_post=nu[1])) < 1e-11, (p.shape, l, nu, tail)
+        H.close()
 
 
 @pytest.mark.parametrize("vec,op", [("bilinear", "galerkin"), ("bilinear", "red_o4"), ("high_order", "galerkin"),
@@ -180,6 +194,37 @@ def test_solve(lib, name, vec, op, itol, imax):
     xo_t, rep_ot = so_t.solve(p.b)
     assert rep_t["converged"] and rep_ot["converged"]
     assert rel(xt.cpu().numpy(), xo_t) < 1e-6
+    H.close()
+
+
+@pytest.mark.parametrize("name,vec,op", [("c0_tiny", "bilinear", "galerkin"), ("mp_som_k40", "high_order", "red_glk2"),
+                                         ("wedge_f10", "high_order", "galerkin")])
+def test_graph_and_host_loop_agree(lib, name, vec, op):
+    """The CUDA-graph solve (conditional while nodes) and the host-polled loop run the same
+    kernels in the same order: identical iteration counts and bitwise-identical solutions."""
+    p = _problem(name)
+    prm = {"coarse_op": op, "vectors": vec, "inner_tol": 1e-1, "inner_maxit": 300}
+    Hg = lib.helm_setup(p, dict(prm, graph=1))
+    He = lib.helm_setup(p, dict(prm, graph=0))
+    xg, rg = Hg.solve(gpu(p.b), tol=1e-6, maxit=200)
+    xe, re_ = He.solve(gpu(p.b), tol=1e-6, maxit=200)
+    for key in ("outer_iterations", "inner_iterations_total", "inner_iterations_max", "converged"):
+        assert rg[key] == re_[key], key
+    assert torch.equal(xg, xe)
+    assert rg["kernels"] == re_["kernels"] > 0
+    xg2, rg2 = Hg.solve(gpu(p.b), tol=1e-6, maxit=200)      # graph replay
+    assert torch.equal(xg2, xg)
+    Hg.close()
+    He.close()
+
+
+def test_restarted_outer(lib):
+    """Outer FGMRES(m) restarts (host loop of graph-captured cycles) still meet the tolerance."""
+    p = config_problem("c1_k50")
+    H = lib.helm_setup(p, {"vectors": "high_order", "restart": 4, "inner_tol": 1e-1, "inner_maxit": 200})
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=200)
+    assert rep["converged"] and rep["restarts"] >= 1
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
     H.close()
 
 

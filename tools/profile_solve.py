@@ -1,0 +1,31 @@
+"""One solve of a workload (for ncu launch lists / captures): setup, one solve, print report.
+  python tools/profile_solve.py --workload c1_k100 --inner-maxit 100 [--graph 1] [--warm 0]"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2308_06152_b200 import helm  # noqa: E402
+from workloads import config_problem  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c1_k100")
+ap.add_argument("--vectors", default="high_order")
+ap.add_argument("--coarse-op", default="galerkin")
+ap.add_argument("--inner-tol", type=float, default=1e-1)
+ap.add_argument("--inner-maxit", type=int, default=100)
+ap.add_argument("--graph", type=int, default=1)
+ap.add_argument("--warm", type=int, default=0)
+args = ap.parse_args()
+p = config_problem(args.workload)
+H = helm.helm_setup(p, {"vectors": args.vectors, "coarse_op": args.coarse_op, "inner_tol": args.inner_tol,
+                        "inner_maxit": args.inner_maxit, "graph": args.graph})
+b = torch.from_numpy(p.b).cuda()
+for _ in range(args.warm + 1):
+    x, rep = H.solve(b, 1e-6, 2000)
+torch.cuda.synchronize()
+print(json.dumps(rep))
