@@ -38,6 +38,10 @@ extern "C" {
 #define HELM_COARSE_RED_O4 2   /* fourth-order re-discretisation, Eq. 5.11 (§5.2.3) */
 #define HELM_COARSE_RED_GLK1 3 /* ReD-Glk1, Eq. 5.12/5.14, 2nd order on two layers (§5.2.4) */
 #define HELM_COARSE_RED_GLK2 4 /* ReD-Glk2, Eq. 5.12/5.14 with ghost points (§5.2.4) */
+#define HELM_COARSE_RED_O6 5   /* sixth-order re-discretisation, Eq. 5.10 (§5.2.3) */
+#define HELM_COARSE_RED_CMPO4 6 /* compact fourth-order re-discretisation, Eq. 5.19 (§5.2.5) */
+/* The re-discretised operators (RED_O2/O4/O6/CMPO4) replace A_{2h} as printed for either kind of
+ * deflation vectors (no factor 4 for the higher-order vectors; reading R21). */
 
 #define HELM_VECTORS_BILINEAR 0   /* A-DEF1: Z = Eq. 3.9, Z^T/4 = full weighting Eq. 3.8 */
 #define HELM_VECTORS_HIGH_ORDER 1 /* APD: Z = Eq. 3.12, Z^T = Eq. 3.14 (§3.2.1, §3.2.2) */
@@ -70,8 +74,8 @@ typedef struct {
   int max_levels;      /* cap on multigrid levels (>= 2) */
   int restart;         /* outer FGMRES basis size; 0 = no restart (full FGMRES) */
   int max_coarsest;    /* largest coarsest grid (unknowns) solved by the dense inverse */
-  int vectors;         /* HELM_VECTORS_*; bilinear admits GALERKIN/RED_O2/RED_O4,
-                          high order admits GALERKIN/RED_GLK1/RED_GLK2 */
+  int vectors;         /* HELM_VECTORS_*; RED_GLK1/RED_GLK2 need the higher-order vectors,
+                          every other coarse_op works with both kinds */
   int graph;           /* 1 (default): helm_solve runs as one CUDA graph whose outer and inner
                           loops are conditional while nodes (no host sync inside a solve);
                           0: the same kernels with host-polled loops */

@@ -11,6 +11,11 @@ A_{2h} = I_h^{2h} A_h I_{2h}^h" and §5.2 (matrix-free coarse operators):
               with second-order stencils where the cross does not fit (§5.2.3 "the
               stencils for the boundary grid points will be changed to that of the
               second-order re-discretization method").
+  "red_o6"    ReD-O6, §5.2.3 Eq. 5.10 (sixth-order Laplacian, 13 taps on a 7-wide cross),
+              same boundary rule (reading R6).
+  "red_cmpo4" ReD-cmpO4, §5.2.5 Eq. 5.19 with the Singer-Turkel coefficients (gamma = 1):
+              a 9-point compact stencil; Sommerfeld ghosts by the fourth-order condition
+              u_0 = 2ikh(1 - k^2h^2/6) u_1 + u_2 and the corner ghost u_00 = (u_10 + u_01)/2.
 
 Reading R5: Eq. 5.11 prints the centre as "60 - k^2 (2h)^2" inside the
 prefactor 1/(12 (2h)^2); a consistent discretisation of -Delta - k^2 needs
@@ -27,7 +32,8 @@ from .operators import apply_A
 from .transfer import (coarse_k, coarse_shape, prolong_bilinear, prolong_high_order, restrict_fw,
                        restrict_high_order)
 
-COARSE_OPS = ("galerkin", "red_o2", "red_o4", "red_glk1", "red_glk2")
+COARSE_OPS = ("galerkin", "red_o2", "red_o4", "red_o6", "red_cmpo4", "red_glk1", "red_glk2")
+RED_OPS = ("red_o2", "red_o4", "red_o6", "red_cmpo4")   # re-discretisations of A at mesh 2h
 
 # PAPER.md Eq. 5.12 (Laplacian part, printed) and Eq. 5.14 (wavenumber part, printed).
 GLK_LAP = np.array([[-3, -44, -98, -44, -3],
@@ -106,14 +112,83 @@ def _red_o4(x, kc, H, bc):
     return np.where(fits, y4, y2)
 
 
+def _red_o6(x, kc, H, bc):
+    """ReD-O6: -(2u_{i-3} - 27u_{i-2} + 270u_{i-1} - 490u_i + 270u_{i+1} - 27u_{i+2} + 2u_{i+3})/(180H^2)
+    per direction (Eq. 5.10) minus k^2 at the centre; second-order stencil where the
+    7-wide cross does not fit in the closed domain (reading R6)."""
+    ny, nx = x.shape
+    y2 = apply_A(x, kc, H, bc)
+    xp = np.zeros((ny + 6, nx + 6), dtype=np.complex128)
+    xp[3:-3, 3:-3] = x
+    c = xp[3:-3, 3:-3]
+
+    def ring(d):
+        return (xp[3:-3, 3 - d:xp.shape[1] - 3 - d] + xp[3:-3, 3 + d:xp.shape[1] - 3 + d] +
+                xp[3 - d:xp.shape[0] - 3 - d, 3:-3] + xp[3 + d:xp.shape[0] - 3 + d, 3:-3])
+    y6 = (980.0 * c - 270.0 * ring(1) + 27.0 * ring(2) - 2.0 * ring(3)) / (180.0 * H * H) - kc * kc * c
+    fits = np.zeros((ny, nx), dtype=bool)
+    if bc == "dirichlet":
+        fits[2:ny - 2, 2:nx - 2] = True
+    else:
+        fits[3:ny - 3, 3:nx - 3] = True
+    return np.where(fits, y6, y2)
+
+
+# PAPER.md Eq. 5.19 with the Singer-Turkel coefficients (gamma = 1, PAPER.md:772-776)
+CMP_GAMMA = 1.0
+CMP_A = {"0": 10.0 / 3.0, "s": -2.0 / 3.0, "c": -1.0 / 6.0}
+CMP_B = {"0": 2.0 / 3.0 + CMP_GAMMA / 36.0, "s": 1.0 / 12.0 - CMP_GAMMA / 72.0, "c": CMP_GAMMA / 144.0}
+
+
+def _red_cmpo4(x, kc, H, bc):
+    """ReD-cmpO4: y = (1/H^2) sum a_tap u_tap - k_c^2 sum b_tap u_tap over the 3x3 compact
+    stencil (a_0, a_s, a_c / b_0, b_s, b_c), k_c the wavenumber of the centre node (reading
+    R19: Eq. 5.19 carries one k^2 per stencil).  Dirichlet: taps on the boundary hold 0.
+    Sommerfeld: ghost nodes one layer outside the domain from the fourth-order condition
+    u_ghost = u_inner + 2 i k H (1 - k^2 H^2 / 6) u_boundary (k of the boundary node), the corner
+    ghost as the mean of its two edge-ghost neighbours."""
+    ny, nx = x.shape
+    X = np.zeros((ny + 2, nx + 2), dtype=np.complex128)
+    X[1:-1, 1:-1] = x
+    if bc == "sommerfeld":
+        fac = lambda kk: 2j * kk * H * (1.0 - kk * kk * H * H / 6.0)
+        X[1:-1, 0] = x[:, 1] + fac(kc[:, 0]) * x[:, 0]
+        X[1:-1, -1] = x[:, -2] + fac(kc[:, -1]) * x[:, -1]
+        X[0, 1:-1] = x[1, :] + fac(kc[0, :]) * x[0, :]
+        X[-1, 1:-1] = x[-2, :] + fac(kc[-1, :]) * x[-1, :]
+        X[0, 0] = 0.5 * (X[0, 1] + X[1, 0])
+        X[0, -1] = 0.5 * (X[0, -2] + X[1, -1])
+        X[-1, 0] = 0.5 * (X[-1, 1] + X[-2, 0])
+        X[-1, -1] = 0.5 * (X[-1, -2] + X[-2, -1])
+    c = X[1:-1, 1:-1]
+    side = X[1:-1, :-2] + X[1:-1, 2:] + X[:-2, 1:-1] + X[2:, 1:-1]
+    corner = X[:-2, :-2] + X[:-2, 2:] + X[2:, :-2] + X[2:, 2:]
+    lap = (CMP_A["0"] * c + CMP_A["s"] * side + CMP_A["c"] * corner) / (H * H)
+    mass = CMP_B["0"] * c + CMP_B["s"] * side + CMP_B["c"] * corner
+    return lap - kc * kc * mass
+
+
 def apply_coarse_E(x: np.ndarray, k_fine: np.ndarray, h: float, bc: str, op: str = "galerkin",
                    vectors: str = "bilinear") -> np.ndarray:
     """y = E x on the deflation coarse grid (mesh width 2h).
     vectors="bilinear": A-DEF1 (Z = Eq. 3.9, R = Eq. 3.8 = Z^T/4);
-    vectors="high_order": APD (Z = Eq. 3.12, R = Eq. 3.14 = Z^T)."""
+    vectors="high_order": APD (Z = Eq. 3.12, R = Eq. 3.14 = Z^T).
+    The re-discretised operators (RED_OPS) are the same for both vector kinds: they replace
+    A_{2h} as printed, without the factor 4 that Z^T A Z carries for the higher-order vectors
+    (reading R21; "P_h is no longer a projection")."""
     fine_shape = k_fine.shape
     if x.shape != coarse_shape(fine_shape, bc):
         raise ValueError("x is not on the coarse grid")
+    if op in RED_OPS:
+        kc = coarse_k(k_fine, bc)
+        H = 2.0 * h
+        if op == "red_o2":
+            return apply_A(x, kc, H, bc)
+        if op == "red_o4":
+            return _red_o4(x, kc, H, bc)
+        if op == "red_o6":
+            return _red_o6(x, kc, H, bc)
+        return _red_cmpo4(x, kc, H, bc)
     if vectors == "high_order":
         if op == "galerkin":
             return restrict_high_order(apply_A(prolong_high_order(x, fine_shape, bc), k_fine, h, bc), bc)
@@ -124,9 +199,4 @@ def apply_coarse_E(x: np.ndarray, k_fine: np.ndarray, h: float, bc: str, op: str
         v1 = prolong_bilinear(x, fine_shape, bc)      # Eq. 5.7a
         v2 = apply_A(v1, k_fine, h, bc)               # Eq. 5.7b
         return restrict_fw(v2, bc)                    # Eq. 5.7c
-    kc = coarse_k(k_fine, bc)
-    if op == "red_o2":
-        return apply_A(x, kc, 2.0 * h, bc)
-    if op == "red_o4":
-        return _red_o4(x, kc, 2.0 * h, bc)
     raise ValueError(op)

@@ -226,6 +226,14 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       if (res) k_apply_red_o4<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
       else k_apply_red_o4<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
       return post_launch(C);
+    case HELM_COARSE_RED_O6:
+      if (res) k_apply_red_o6<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_o6<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      return post_launch(C);
+    case HELM_COARSE_RED_CMPO4:
+      if (res) k_apply_red_cmpo4<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      else k_apply_red_cmpo4<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      return post_launch(C);
   }
   return fail(HELM_EINVAL, "bad coarse_op");
 }
@@ -582,14 +590,12 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.max_levels < 2) return fail(HELM_EINVAL, "max_levels must be >= 2");
   if (p.nu_pre < 1 || p.nu_post < 0) return fail(HELM_EINVAL, "nu_pre >= 1, nu_post >= 0");
   if (p.inner_maxit < 1) return fail(HELM_EINVAL, "inner_maxit >= 1");
+  if (p.coarse_op < HELM_COARSE_GALERKIN || p.coarse_op > HELM_COARSE_RED_CMPO4)
+    return fail(HELM_EINVAL, "bad coarse_op %d", p.coarse_op);
   if (p.vectors == HELM_VECTORS_BILINEAR) {
-    if (p.coarse_op != HELM_COARSE_GALERKIN && p.coarse_op != HELM_COARSE_RED_O2 && p.coarse_op != HELM_COARSE_RED_O4)
-      return fail(HELM_EINVAL, "coarse_op %d not defined for bilinear vectors", p.coarse_op);
-  } else if (p.vectors == HELM_VECTORS_HIGH_ORDER) {
-    if (p.coarse_op != HELM_COARSE_GALERKIN && p.coarse_op != HELM_COARSE_RED_GLK1 &&
-        p.coarse_op != HELM_COARSE_RED_GLK2)
-      return fail(HELM_EINVAL, "coarse_op %d not defined for high-order vectors", p.coarse_op);
-  } else {
+    if (p.coarse_op == HELM_COARSE_RED_GLK1 || p.coarse_op == HELM_COARSE_RED_GLK2)
+      return fail(HELM_EINVAL, "ReD-Glk (coarse_op %d) is defined for the higher-order vectors only", p.coarse_op);
+  } else if (p.vectors != HELM_VECTORS_HIGH_ORDER) {
     return fail(HELM_EINVAL, "bad vectors %d", p.vectors);
   }
   int dev;

@@ -454,6 +454,108 @@ __global__ void k_apply_red_o4(Geo g, DVec xv, DVec fv, DVec yv, const double* _
   y[p] = v;
 }
 
+// ReD-O6 (Eq. 5.10: 7-point sixth-order second derivative per direction, centre k^2)
+// where the 7-wide cross fits in the closed domain, second-order stencil elsewhere (reading R6).
+template <int MODE>
+__global__ void k_apply_red_o6(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ x = xv.get();
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
+  const size_t p = (size_t)j * g.nx + i;
+  bool fits;
+  if (g.bc == BC_DIRICHLET) fits = (i >= 2 && i <= g.nx - 3 && j >= 2 && j <= g.ny - 3);
+  else fits = (i >= 3 && i <= g.nx - 4 && j >= 3 && j <= g.ny - 4);
+  double2 v;
+  if (fits) {
+    auto at = [&](int ii, int jj) -> double2 {
+      if (ii < 0 || ii >= g.nx || jj < 0 || jj >= g.ny) return make_double2(0.0, 0.0);
+      return x[(size_t)jj * g.nx + ii];
+    };
+    auto ring = [&](int d) -> double2 {
+      return cadd(cadd(at(i - d, j), at(i + d, j)), cadd(at(i, j - d), at(i, j + d)));
+    };
+    const double2 c = x[p];
+    const double2 r1 = ring(1), r2 = ring(2), r3 = ring(3);
+    const double s = 1.0 / (180.0 * g.h * g.h);
+    const double kk = k[p];
+    v = make_double2(s * (980.0 * c.x - 270.0 * r1.x + 27.0 * r2.x - 2.0 * r3.x) - kk * kk * c.x,
+                     s * (980.0 * c.y - 270.0 * r1.y + 27.0 * r2.y - 2.0 * r3.y) - kk * kk * c.y);
+  } else {
+    Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
+    v = stencil_apply(g, x, i, j, c);
+  }
+  if (MODE == 1) v = csub(f[p], v);
+  y[p] = v;
+}
+
+// ReD-cmpO4 (Eq. 5.19, Singer-Turkel coefficients with gamma = 1):
+//   y = (1/H^2) sum a_tap u_tap - k_c^2 sum b_tap u_tap over the 3x3 compact stencil, k_c the
+// centre wavenumber (reading R19).  Dirichlet: boundary taps hold 0.  Sommerfeld: ghosts from
+// u_ghost = u_inner + 2 i k H (1 - k^2 H^2/6) u_boundary, corner ghost = mean of its two edge
+// ghosts.
+__device__ __forceinline__ double2 cmp_ghost_fac(double kk, double H) {
+  return make_double2(0.0, 2.0 * kk * H * (1.0 - kk * kk * H * H / 6.0));
+}
+
+// value at (ii, jj) in [-1, nx] x [-1, ny] for the Sommerfeld compact stencil
+__device__ __forceinline__ double2 cmp_val(const Geo& g, const double2* __restrict__ x, const double* __restrict__ k,
+                                           int ii, int jj) {
+  auto inside = [&](int a, int b) { return a >= 0 && a < g.nx && b >= 0 && b < g.ny; };
+  auto X = [&](int a, int b) { return x[(size_t)b * g.nx + a]; };
+  auto edge = [&](int a, int b) -> double2 {   // exactly one of a, b is outside by one layer
+    if (a == -1) return cfma(cmp_ghost_fac(k[(size_t)b * g.nx + 0], g.h), X(0, b), X(1, b));
+    if (a == g.nx) return cfma(cmp_ghost_fac(k[(size_t)b * g.nx + g.nx - 1], g.h), X(g.nx - 1, b), X(g.nx - 2, b));
+    if (b == -1) return cfma(cmp_ghost_fac(k[a], g.h), X(a, 0), X(a, 1));
+    return cfma(cmp_ghost_fac(k[(size_t)(g.ny - 1) * g.nx + a], g.h), X(a, g.ny - 1), X(a, g.ny - 2));
+  };
+  if (inside(ii, jj)) return X(ii, jj);
+  const bool ox = (ii < 0 || ii >= g.nx), oy = (jj < 0 || jj >= g.ny);
+  if (ox && oy) {   // corner ghost: mean of the two adjacent edge ghosts
+    const int ai = ii < 0 ? 0 : g.nx - 1, bj = jj < 0 ? 0 : g.ny - 1;
+    return cscale(0.5, cadd(edge(ai, jj), edge(ii, bj)));
+  }
+  return edge(ii, jj);
+}
+
+template <int MODE>
+__global__ void k_apply_red_cmpo4(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const double2* __restrict__ x = xv.get();
+  const double2* __restrict__ f = fv.get();
+  double2* __restrict__ y = yv.get();
+  const size_t p = (size_t)j * g.nx + i;
+  constexpr double A0 = 10.0 / 3.0, AS = -2.0 / 3.0, AC = -1.0 / 6.0;
+  constexpr double B0 = 2.0 / 3.0 + 1.0 / 36.0, BS = 1.0 / 12.0 - 1.0 / 72.0, BC = 1.0 / 144.0;
+  double2 c, side, corner;
+  if (g.bc == BC_DIRICHLET) {
+    auto at = [&](int ii, int jj) -> double2 {
+      if (ii < 0 || ii >= g.nx || jj < 0 || jj >= g.ny) return make_double2(0.0, 0.0);
+      return x[(size_t)jj * g.nx + ii];
+    };
+    c = x[p];
+    side = cadd(cadd(at(i - 1, j), at(i + 1, j)), cadd(at(i, j - 1), at(i, j + 1)));
+    corner = cadd(cadd(at(i - 1, j - 1), at(i + 1, j - 1)), cadd(at(i - 1, j + 1), at(i + 1, j + 1)));
+  } else {
+    c = x[p];
+    side = cadd(cadd(cmp_val(g, x, k, i - 1, j), cmp_val(g, x, k, i + 1, j)),
+                cadd(cmp_val(g, x, k, i, j - 1), cmp_val(g, x, k, i, j + 1)));
+    corner = cadd(cadd(cmp_val(g, x, k, i - 1, j - 1), cmp_val(g, x, k, i + 1, j - 1)),
+                  cadd(cmp_val(g, x, k, i - 1, j + 1), cmp_val(g, x, k, i + 1, j + 1)));
+  }
+  const double iH2 = 1.0 / (g.h * g.h);
+  const double k2 = k[p] * k[p];
+  const double2 lap = cscale(iH2, cadd(cadd(cscale(A0, c), cscale(AS, side)), cscale(AC, corner)));
+  const double2 mass = cadd(cadd(cscale(B0, c), cscale(BS, side)), cscale(BC, corner));
+  double2 v = csub(lap, cscale(k2, mass));
+  if (MODE == 1) v = csub(f[p], v);
+  y[p] = v;
+}
+
 // ------------------------------------------------------------------ coarsest dense solve
 // Dense M of the coarsest level, row-major n x n (row = unknown p).
 __global__ void k_dense_op(Geo g, const double* __restrict__ k, double sr, double si, double2* __restrict__ Md) {

@@ -84,8 +84,10 @@ def test_transfers(case):
         assert rel(H.prolong(l, gpu(e)).cpu().numpy(), oracle.prolong_bilinear(e, levels[l].shape, p.bc)) < 1e-14
 
 
-VARIANTS = [("bilinear", "galerkin"), ("bilinear", "red_o2"), ("bilinear", "red_o4"),
-            ("high_order", "galerkin"), ("high_order", "red_glk1"), ("high_order", "red_glk2")]
+VARIANTS = [("bilinear", "galerkin"), ("bilinear", "red_o2"), ("bilinear", "red_o4"), ("bilinear", "red_o6"),
+            ("bilinear", "red_cmpo4"), ("high_order", "galerkin"), ("high_order", "red_glk1"),
+            ("high_order", "red_glk2"), ("high_order", "red_o2"), ("high_order", "red_o4"), ("high_order", "red_o6"),
+            ("high_order", "red_cmpo4")]
 
 
 @pytest.mark.parametrize("vec,op", VARIANTS)
@@ -162,6 +164,8 @@ SOLVE_CASES = [
     ("c1_k50", "high_order", "galerkin", 1e-1, 200),
     ("mp_som_k40", "high_order", "galerkin", 1e-1, 200), ("mp_som_k40", "high_order", "red_glk1", 0.0, 30),
     ("wedge_f10", "bilinear", "galerkin", 0.0, 40), ("wedge_f10", "high_order", "red_glk2", 1e-1, 300),
+    ("mp_som_k40", "high_order", "red_cmpo4", 1e-1, 200), ("mp_som_k40", "high_order", "red_o6", 0.0, 40),
+    ("wedge_f10", "high_order", "red_cmpo4", 0.0, 40), ("c1_k50", "bilinear", "red_o6", 1e-1, 200),
 ]
 
 
@@ -252,6 +256,8 @@ def test_invalid_arguments(lib):
     p = config_problem("c0_tiny")
     with pytest.raises(lib.HelmError):
         lib.helm_setup(p, {"max_levels": 1})
+    with pytest.raises(lib.HelmError):
+        lib.helm_setup(p, {"vectors": "bilinear", "coarse_op": "red_glk2"})   # ReD-Glk needs APD vectors
     H = lib.helm_setup(p)
     b = gpu(p.b)
     with pytest.raises(lib.HelmError):

@@ -128,3 +128,16 @@ def test_mgs_and_cgs2_agree_with_exact_coarse_solve():
     xb, rb = oracle.solve(p, oracle.SolverParams(inner_solver="direct", orth="cgs2"))
     assert ra["outer_iterations"] == rb["outer_iterations"]
     assert np.linalg.norm(xa - xb) / np.linalg.norm(xa) < 1e-9
+
+
+@pytest.mark.parametrize("row", GOLD["table4_mp2b_apd_red"]["rows"], ids=lambda r: f"{r['nodes']}-{r['op']}")
+def test_table4_rediscretised_coarse_operators(row):
+    """Table 4 (MP-2b, APD, kh = 0.625): the re-discretised coarse operators ReD-O2/O4/cmpO4
+    need 2-3x the outer iterations of str-Glk.  The printed counts pin the reading that they
+    replace A_2h unscaled (R21): with the factor 4 of Z^T A Z the counts would fall to the
+    str-Glk level (7).  Band +-3 (FGMRES with the true residual here, R12)."""
+    p = mp_problem(float(row["k"]), row["nodes"] - 1, "sommerfeld")
+    x, rep = oracle.solve(p, oracle.SolverParams(vectors="high_order", coarse_op=row["op"], inner_tol=1e-8,
+                                                 inner_maxit=1000))
+    assert rep["converged"]
+    assert abs(rep["outer_iterations"] - row["outer"]) <= 3, (rep["outer_iterations"], row)

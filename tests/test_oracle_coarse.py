@@ -91,3 +91,74 @@ def test_deflation_identities(bc, shape):
     np.testing.assert_allclose(s.Q(AZx), Zx, rtol=0, atol=1e-10 * np.abs(Zx).max())
     np.testing.assert_allclose(AZx - s.A(s.Q(AZx)), 0, atol=1e-9 * np.abs(AZx).max())
     np.testing.assert_allclose(s.adef1(AZx), Zx, atol=1e-9 * np.abs(Zx).max())
+
+
+def test_red_o6_sixth_order():
+    """ReD-O6 (Eq. 5.10, 7-point central second derivative per direction): on
+    u = sin(pi x) sin(2 pi y) the interior error against -Delta u - k^2 u decays like H^6."""
+    errs, Hs = [], []
+    for n in (16, 32, 64):
+        h = 1.0 / (2 * n)
+        nf = 2 * n - 1
+        k = np.full((nf, nf), 3.0)
+        H = 2 * h
+        xc = np.arange(1, n) * H
+        X, Y = np.meshgrid(xc, xc)
+        u = np.sin(math.pi * X) * np.sin(2 * math.pi * Y) + 0j
+        y = oracle.apply_coarse_E(u, k, h, "dirichlet", "red_o6")
+        exact = (5 * math.pi**2 - 9.0) * u
+        errs.append(np.max(np.abs(y - exact)[3:-3, 3:-3]))
+        Hs.append(H)
+    slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
+    assert abs(slope - 6.0) < 0.3, slope
+
+
+def test_cmpo4_coefficients_meet_appendix_b_constraints():
+    """PAPER.md Appendix B Eq. B.1/B.2: a_0 + 4a_s + 4a_c = 0, a_s + 2a_c = -1,
+    b_0 + 4b_s + 4b_c = 1 for the Singer-Turkel coefficients of §5.2.5."""
+    from oracle.coarse import CMP_A, CMP_B
+    assert abs(CMP_A["0"] + 4 * CMP_A["s"] + 4 * CMP_A["c"]) < 1e-15
+    assert abs(CMP_A["s"] + 2 * CMP_A["c"] + 1.0) < 1e-15
+    assert abs(CMP_B["0"] + 4 * CMP_B["s"] + 4 * CMP_B["c"] - 1.0) < 1e-15
+
+
+def _plane_wave(n, kval, theta, bc):
+    h = 1.0 / (2 * n)
+    H = 2 * h
+    if bc == "dirichlet":
+        nf = 2 * n - 1
+        xc = np.arange(1, n) * H
+    else:
+        nf = 2 * n + 1
+        xc = np.arange(0, n + 1) * H
+    X, Y = np.meshgrid(xc, xc)
+    u = np.exp(1j * kval * (X * math.cos(theta) + Y * math.sin(theta)))
+    return h, H, np.full((nf, nf), kval), u
+
+
+def test_cmpo4_fourth_order_on_helmholtz_solutions():
+    """The compact scheme (Singer & Turkel) is fourth-order for solutions of the Helmholtz
+    equation: on a plane wave exp(ik(x cos t + y sin t)) the interior residual decays like H^4."""
+    errs, Hs = [], []
+    for n in (16, 32, 64):
+        h, H, k, u = _plane_wave(n, 6.0, 0.7, "dirichlet")
+        y = oracle.apply_coarse_E(u, k, h, "dirichlet", "red_cmpo4")
+        errs.append(np.max(np.abs(y)[1:-1, 1:-1]))
+        Hs.append(H)
+    slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
+    assert abs(slope - 4.0) < 0.25, slope
+
+
+def test_cmpo4_sommerfeld_ghost_is_high_order_for_outgoing_waves():
+    """The fourth-order Sommerfeld ghost u_0 = 2ikh(1 - k^2h^2/6) u_1 + u_2
+    is exact to O(h^5) for the wave leaving through the boundary, so on the left edge (away
+    from corners) the residual of exp(-ikx) decays like H^3 (ghost error / H^2), much faster
+    than the first-order condition would allow (H^1)."""
+    errs, Hs = [], []
+    for n in (16, 32, 64):
+        h, H, k, u = _plane_wave(n, 6.0, math.pi, "sommerfeld")
+        y = oracle.apply_coarse_E(u, k, h, "sommerfeld", "red_cmpo4")
+        errs.append(np.max(np.abs(y[2:-2, 0])))
+        Hs.append(H)
+    slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
+    assert slope > 2.7, slope
