@@ -81,6 +81,8 @@ typedef struct {
                           0: the same kernels with host-polled loops */
   int tail_max_n;      /* V-cycle levels with at most this many unknowns (and everything
                           below them) run in one single-CTA kernel; 0 disables (default 8192) */
+  int pdl;             /* 1 (default): launches carry programmatic stream serialization, so a
+                          kernel's CTAs are scheduled while its predecessor drains */
 } helm_params;
 
 typedef struct {
@@ -139,7 +141,8 @@ int helm_apply_Z(helm_ctx ctx, const double* coarse_dev, double* fine_dev);
 int helm_solve_host(helm_ctx ctx, const double* b_host, double* x_host, double tol, int maxit,
                     helm_report* rep);
 
-/* Write `bytes` to a scratch buffer (> L2) on the context stream: L2 flush between timed steps. */
+/* Read a `bytes`-sized scratch buffer (> L2) on the context stream: L2 flush between timed steps
+ * (reads, so the evicted lines are clean and the next kernel pays no write-backs). */
 int helm_flush_l2(helm_ctx ctx, size_t bytes);
 /* Number of kernels this context launched since creation (bench.py's gpu_launches); a graph
  * solve adds the kernels its replay executed. */
@@ -158,6 +161,15 @@ long long helm_launch_count(helm_ctx ctx);
 #define HELM_KB_GS_UPDATE 5  /* delayed-CGS2 pass 2 over `arg - 1` basis vectors */
 int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, double* us_per_launch,
                       double* bytes_per_launch);
+
+/* Warm in-graph cost of a region of the path: `reps` back-to-back instances captured into one
+ * CUDA graph (as inside a solve), replayed; returns the mean device time per instance.
+ * HELM_GB_VCYCLE: one V-cycle from level `arg`; HELM_GB_APPLY_E: one E apply (level 1);
+ * HELM_GB_APPLY_A: one A apply (level 0).  Internal scratch buffers only. */
+#define HELM_GB_VCYCLE 0
+#define HELM_GB_APPLY_E 1
+#define HELM_GB_APPLY_A 2
+int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 const char* helm_last_error(void);
 const char* helm_build_info(void);

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/helm.h"
@@ -78,6 +79,7 @@ struct Fgm {
   double2* sc2 = nullptr;    // 2: 1/beta, h_jj
   double2* rawc = nullptr;   // m+2: raw Hessenberg column awaiting its delayed correction
   double2* nrm = nullptr;    // 2
+  unsigned* cnt = nullptr;   // 2 last-block tickets (reduce/step A, update/step B)
   double2* part = nullptr;   // max((m+2) * gx, gu) partials
   GsGeom geo{};              // Gram-Schmidt launch geometry
   FgmState* st = nullptr;
@@ -107,6 +109,7 @@ struct helm_ctx_s {
   uint4* flush = nullptr;
   size_t flush_n = 0;
   long long launches = 0;         // kernels launched (graph replays: kernels executed)
+  cudaError_t launch_err = cudaSuccess;
   int sm_count = 148;
   // cached solve graphs: [0] first cycle (x0 = 0), [1] restart cycle
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -128,8 +131,33 @@ int grid1d(const helm_ctx_s& C, size_t n) {
   return (int)std::max<size_t>(1, std::min(b, cap));
 }
 
+// Launch on the context stream.  With params.pdl the launch carries programmatic stream
+// serialization (PDL): the kernel's CTAs may be scheduled while its predecessor drains and
+// wait in griddepcontrol.wait (first statement of every kernel) until the predecessor's
+// results are visible; in a captured graph this becomes a programmatic edge.
+template <typename... KArgs, typename... Args>
+void launch_k(helm_ctx_s& C, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = C.s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = C.p.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess && C.launch_err == cudaSuccess) C.launch_err = e;
+}
+
 int post_launch(helm_ctx_s& C) {
   C.launches++;
+  if (C.launch_err != cudaSuccess) {
+    const cudaError_t le = C.launch_err;
+    C.launch_err = cudaSuccess;
+    return fail(HELM_ECUDA, "kernel launch: %s", cudaGetErrorString(le));
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HELM_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
   return HELM_OK;
@@ -151,23 +179,24 @@ bool fused_vcycle(const helm_ctx_s& C) { return C.p.nu_pre == 1 && C.p.nu_post =
 
 // ------------------------------------------------------------------ operator launches
 int op_apply(helm_ctx_s& C, const Level& L, DVec u, DVec f, DVec y, double sr, double si) {
-  if (f.p) k_apply_op<1><<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, u, f, y, L.k, sr, si);
-  else k_apply_op<0><<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, u, DVec(), y, L.k, sr, si);
+  const unsigned blocks = (unsigned)((L.n + 255) / 256);
+  if (f.p) launch_k(C, k_apply_op<1>, blocks, 256, 0, L.g, u, f, y, L.k, sr, si);
+  else launch_k(C, k_apply_op<0>, blocks, 256, 0, L.g, u, DVec(), y, L.k, sr, si);
   return post_launch(C);
 }
 
 int restrict_(helm_ctx_s& C, int l, const double2* v, double2* vc) {
   const Level& F = C.L[l];
   const Level& G = C.L[l + 1];
-  k_restrict<<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, v, vc);
+  launch_k(C, k_restrict, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, v, vc);
   return post_launch(C);
 }
 
 int prolong_(helm_ctx_s& C, int l, const double2* e, const double2* base, DVec y, const double2* addq) {
   const Level& F = C.L[l];
   const Level& G = C.L[l + 1];
-  if (base) k_prolong<1><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, base, y, addq);
-  else k_prolong<0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y, addq);
+  if (base) launch_k(C, k_prolong<1>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, base, y, addq);
+  else launch_k(C, k_prolong<0>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, nullptr, y, addq);
   return post_launch(C);
 }
 
@@ -176,9 +205,9 @@ int defl_restrict(helm_ctx_s& C, DVec v, double2* vc) {
   const Level& F = C.L[0];
   const Level& G = C.L[1];
   if (C.p.vectors == HELM_VECTORS_BILINEAR)
-    k_restrict_z<1><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, v, vc);
+    launch_k(C, k_restrict_z<1>, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, v, vc);
   else
-    k_restrict_z<2><<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, v, vc);
+    launch_k(C, k_restrict_z<2>, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, v, vc);
   return post_launch(C);
 }
 
@@ -186,9 +215,9 @@ int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
   const Level& F = C.L[0];
   const Level& G = C.L[1];
   if (C.p.vectors == HELM_VECTORS_BILINEAR)
-    k_prolong_z<1, 0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y);
+    launch_k(C, k_prolong_z<1, 0>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, nullptr, y);
   else
-    k_prolong_z<2, 0><<<grd2d(F.g.nx, F.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, e, nullptr, y);
+    launch_k(C, k_prolong_z<2, 0>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, nullptr, y);
   return post_launch(C);
 }
 
@@ -204,35 +233,35 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       const Level& F = C.L[0];
       const dim3 gt((G.g.nx + GLK_TX - 1) / GLK_TX, (G.g.ny + GLK_TY - 1) / GLK_TY);
       if (C.p.vectors == HELM_VECTORS_BILINEAR) {
-        if (res) k_galerkin_apply<1, 1, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
-        else k_galerkin_apply<1, 0, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
+        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
       } else {
-        if (res) k_galerkin_apply<2, 1, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
-        else k_galerkin_apply<2, 0, GLK_TX, GLK_TY><<<gt, 256, 0, C.s>>>(F.g, G.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
+        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
       }
       return post_launch(C);
     }
     case HELM_COARSE_RED_GLK1:
-      if (res) k_apply_red_glk<1, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_glk<1, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      if (res) launch_k(C, k_apply_red_glk<1, 1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_glk<1, 0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_GLK2:
-      if (res) k_apply_red_glk<2, 1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_glk<2, 0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      if (res) launch_k(C, k_apply_red_glk<2, 1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_glk<2, 0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_O2:
       return op_apply(C, G, x, f, y, 1.0, 0.0);
     case HELM_COARSE_RED_O4:
-      if (res) k_apply_red_o4<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_o4<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      if (res) launch_k(C, k_apply_red_o4<1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_o4<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_O6:
-      if (res) k_apply_red_o6<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_o6<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      if (res) launch_k(C, k_apply_red_o6<1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_o6<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_CMPO4:
-      if (res) k_apply_red_cmpo4<1><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
-      else k_apply_red_cmpo4<0><<<gg, blk2d(), 0, C.s>>>(G.g, x, f, y, G.k);
+      if (res) launch_k(C, k_apply_red_cmpo4<1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_cmpo4<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
   }
   return fail(HELM_EINVAL, "bad coarse_op");
@@ -249,32 +278,32 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   Level& L = C.L[l];
   const double sr = C.p.beta1, si = C.p.beta2, w = C.p.omega;
   if (C.tail_lt >= 0 && l >= C.tail_lt) {
-    k_vc_tail<<<1, 1024, C.tail_smem[l], C.s>>>(C.dlev, l, last, f, u_out, addq, sr, si, w, C.p.nu_pre, C.p.nu_post,
+    launch_k(C, k_vc_tail, 1, 1024, C.tail_smem[l], C.dlev, l, last, f, u_out, addq, sr, si, w, C.p.nu_pre, C.p.nu_post,
                                                  C.Minv);
     return post_launch(C);
   }
   if (l == last) {
     const int n = (int)L.n;
-    k_gemv<<<(n * 32 + 255) / 256, 256, 0, C.s>>>(C.Minv, n, f, u_out, addq);
+    launch_k(C, k_gemv, (n * 32 + 255) / 256, 256, 0, C.Minv, n, f, u_out, addq);
     return post_launch(C);
   }
   Level& G = C.L[l + 1];
   if (fused_vcycle(C)) {
     dim3 gd((G.g.nx + DOWN_TX - 1) / DOWN_TX, (G.g.ny + DOWN_TY - 1) / DOWN_TY);
-    k_vc_down<DOWN_TX, DOWN_TY><<<gd, 256, 0, C.s>>>(L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+    launch_k(C, k_vc_down<DOWN_TX, DOWN_TY>, gd, 256, 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
     CKR(post_launch(C));
     CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
     dim3 gu((L.g.nx + UP_TX - 1) / UP_TX, (L.g.ny + UP_TY - 1) / UP_TY);
-    k_vc_up<UP_TX, UP_TY><<<gu, 256, 0, C.s>>>(L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+    launch_k(C, k_vc_up<UP_TX, UP_TY>, gu, 256, 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
     return post_launch(C);
   }
   // generic sweep counts
   double2* cur = L.s;
-  k_jacobi0<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, f, cur, L.k, sr, si, w);
+  launch_k(C, k_jacobi0, grd2d(L.g.nx, L.g.ny), blk2d(), 0, L.g, f, cur, L.k, sr, si, w);
   CKR(post_launch(C));
   for (int sw = 1; sw < C.p.nu_pre; ++sw) {
     double2* nxt = (cur == L.s) ? L.t : L.s;
-    k_jacobi<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, cur, f, DVec(nxt), L.k, sr, si, w, nullptr);
+    launch_k(C, k_jacobi, grd2d(L.g.nx, L.g.ny), blk2d(), 0, L.g, cur, f, DVec(nxt), L.k, sr, si, w, nullptr);
     CKR(post_launch(C));
     cur = nxt;
   }
@@ -289,7 +318,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   for (int sw = 0; sw < np; ++sw) {
     const bool lastsw = (sw == np - 1);
     DVec dst = lastsw ? u_out : DVec((src == ob) ? cur : ob);
-    k_jacobi<<<grd2d(L.g.nx, L.g.ny), blk2d(), 0, C.s>>>(L.g, src, f, dst, L.k, sr, si, w, lastsw ? addq : nullptr);
+    launch_k(C, k_jacobi, grd2d(L.g.nx, L.g.ny), blk2d(), 0, L.g, src, f, dst, L.k, sr, si, w, lastsw ? addq : nullptr);
     CKR(post_launch(C));
     src = dst.p;
   }
@@ -297,6 +326,18 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
 }
 
 // ------------------------------------------------------------------ device FGMRES
+// Raise a kernel's dynamic shared-memory limit to its maximum (227 KB minus its static usage);
+// fails if `need` does not fit.
+int raise_dyn_smem(const void* func, size_t need) {
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, func));
+  const size_t cap = 227 * 1024 - fa.sharedSizeBytes;
+  if (need > cap) return fail(HELM_EINVAL, "Krylov basis too large for the kernels' shared memory (%zu > %zu B)", need, cap);
+  if ((size_t)fa.maxDynamicSharedSizeBytes < cap)
+    CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+  return HELM_OK;
+}
+
 int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   K.m = m;
   K.n = n;
@@ -316,19 +357,24 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * K.geo.gx, (size_t)K.geo.gu)));
   CKR(dalloc(&K.st, 1));
   CK(cudaMemsetAsync(K.st, 0, sizeof(FgmState), C.s));
+  // dynamic shared memory grows with the basis; the limits are raised once to the largest
+  // the kernels can take (a per-function attribute is process-wide: never lower it)
   const size_t smem = (size_t)(m + 2) * sizeof(double2);
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const size_t usmem = (size_t)(2 * m + 2) * sizeof(double2);
+  const size_t usmem = std::max((size_t)(2 * m + 2) * sizeof(double2), dcgs_smem(m));
+  const size_t dsmem = (size_t)(2 * m + 4) * sizeof(double2);
   const size_t asmem = dcgs_smem(m);
-  if (asmem > 227 * 1024 || usmem > 227 * 1024)
-    return fail(HELM_EINVAL, "Krylov basis of %d columns exceeds the Arnoldi kernels' shared memory", m);
-  if (usmem > 48 * 1024) CK(cudaFuncSetAttribute(k_dcgs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem));
-  if (asmem > 48 * 1024) {
-    CK(cudaFuncSetAttribute(k_dcgs_stepA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-    CK(cudaFuncSetAttribute(k_dcgs_stepB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-  }
+  CKR(raise_dyn_smem((const void*)k_gs_update, smem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_update, usmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
+  CKR(dalloc(&K.cnt, 2));
+  CK(cudaMemsetAsync(K.cnt, 0, 2 * sizeof(unsigned), C.s));
   return HELM_OK;
 }
+
+size_t dcgs_update_smem(int m) { return std::max((size_t)(2 * m + 2) * sizeof(double2), dcgs_smem(m)); }
+
+size_t dcgs_dots_smem(const Fgm& K) { return K.geo.chunk > DC_SUB ? (size_t)(2 * K.m + 4) * sizeof(double2) : 0; }
 
 void fgm_free(Fgm& K) {
   cudaFree(K.V);
@@ -344,6 +390,7 @@ void fgm_free(Fgm& K) {
   cudaFree(K.rawc);
   cudaFree(K.nrm);
   cudaFree(K.part);
+  cudaFree(K.cnt);
   cudaFree(K.st);
   K = Fgm();
 }
@@ -351,11 +398,11 @@ void fgm_free(Fgm& K) {
 int gs_dots(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, DVec w, int want_norm,
             double2* out, const int* gate) {
   const GsGeom& g = K.geo;
-  k_gs_dots<<<dim3(g.gx, g.gy), GS_THREADS, 0, C.s>>>(V, (long long)K.n, nptr, nadd, w, (long long)K.n, g.chunk,
+  launch_k(C, k_gs_dots, dim3(g.gx, g.gy), GS_THREADS, 0, V, (long long)K.n, nptr, nadd, w, (long long)K.n, g.chunk,
                                                         want_norm, K.part, gate);
   CKR(post_launch(C));
   const int maxout = K.m + 2;
-  k_gs_reduce<<<(maxout * 32 + 255) / 256, 256, 0, C.s>>>(K.part, g.gx, nptr, nadd, 1, want_norm ? 1 : 0, out, gate);
+  launch_k(C, k_gs_reduce, (maxout * 32 + 255) / 256, 256, 0, K.part, g.gx, nptr, nadd, 1, want_norm ? 1 : 0, out, gate);
   return post_launch(C);
 }
 
@@ -364,7 +411,7 @@ int gs_dots(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, 
 int gs_update(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, const double2* coeff, double sign,
               DVec win, DVec wout, int want_norm, const int* gate) {
   const size_t smem = (size_t)(K.m + 2) * sizeof(double2);
-  k_gs_update<<<K.geo.gu, GS_THREADS, smem, C.s>>>(V, (long long)K.n, nptr, nadd, coeff, sign, win, wout,
+  launch_k(C, k_gs_update, K.geo.gu, GS_THREADS, smem, V, (long long)K.n, nptr, nadd, coeff, sign, win, wout,
                                                     (long long)K.n, want_norm, K.part, gate);
   return post_launch(C);
 }
@@ -434,44 +481,42 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
   auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     if (first) {
       CKR(gs_dots(C, K, nullptr, nullptr, 0, b, 1, K.nrm, nullptr));
-      k_fgm_begin<<<1, 32, 0, C.s>>>(st, K.nrm, 1, K.g, h, use_h);
+      launch_k(C, k_fgm_begin, 1, 32, 0, st, K.nrm, 1, K.g, h, use_h);
       CKR(post_launch(C));
-      k_scale_dvec<<<grid1d(C, n), 256, 0, C.s>>>(b, &st->inv_beta, DVec(K.V), (long long)n, nullptr);
+      launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, b, &st->inv_beta, DVec(K.V), (long long)n, nullptr);
       return post_launch(C);
     }
     CKR(opA(DVec(x), b, DVec(K.V)));
     CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(K.V), 1, K.nrm, nullptr));
-    k_fgm_begin<<<1, 32, 0, C.s>>>(st, K.nrm, 0, K.g, h, use_h);
+    launch_k(C, k_fgm_begin, 1, 32, 0, st, K.nrm, 0, K.g, h, use_h);
     CKR(post_launch(C));
-    k_scale_dvec<<<grid1d(C, n), 256, 0, C.s>>>(DVec(K.V), &st->inv_beta, DVec(K.V), (long long)n, nullptr);
+    launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, DVec(K.V), &st->inv_beta, DVec(K.V), (long long)n, nullptr);
     return post_launch(C);
   };
   auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     const long long ln = (long long)n;
-    DVec vj(K.V, &st->j, ln), zj(K.Z, &st->j, ln), w(K.V + n, &st->j, ln);
+    // v~_j is consumed through the scale 1/h_{j,j-1} left by the previous step B (no
+    // normalisation pass); pass 2 writes the final v_j over it
+    DVec vj(K.V, &st->j, ln, &st->inv_hn), zj(K.Z, &st->j, ln), w(K.V + n, &st->j, ln);
     CKR(opP(vj, zj));
     CKR(opA(zj, DVec(), w));
     // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
     const GsGeom& gg = K.geo;
-    k_dcgs_dots<<<dim3(gg.gx, gg.gy), GS_THREADS, 0, C.s>>>(K.V, ln, &st->j, 1, vj, w, ln, gg.chunk, K.part);
+    launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, &st->j, 1, vj, w, ln, gg.chunk,
+                                                                           K.part);
     CKR(post_launch(C));
-    k_gs_reduce<<<((2 * K.m + 2) * 32 + 255) / 256, 256, 0, C.s>>>(K.part, gg.gx, &st->j, 1, 2, 0, K.dots1, nullptr);
-    CKR(post_launch(C));
+    // reduction of the pass-1 partials + step A (last block), pass 2 + step B (last block)
     const size_t asm_ = dcgs_smem(K.m);
-    k_dcgs_stepA<<<1, 32, asm_, C.s>>>(st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc);
+    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H, K.cs,
+             K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.cnt);
     CKR(post_launch(C));
-    k_dcgs_update<<<gg.gu, GS_THREADS, (size_t)(2 * K.m + 2) * sizeof(double2), C.s>>>(K.V, ln, &st->j, K.coef, K.sc2,
-                                                                                      vj, w, ln, K.part);
-    CKR(post_launch(C));
-    k_dcgs_stepB<<<1, 32, asm_, C.s>>>(st, K.H, K.cs, K.sn, K.g, K.dots1, K.sc2, K.part, gg.gu, K.rawc, h, use_h);
-    CKR(post_launch(C));
-    // v~_{j+1} = w' / h_{j+1,j}   (st->j has advanced)
-    k_scale_dvec<<<grid1d(C, n), 256, 0, C.s>>>(DVec(K.V, &st->j, ln), &st->inv_hn, DVec(K.V, &st->j, ln), ln,
-                                                 &st->done);
+    launch_k(C, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
+             (const double2*)K.coef, (const double2*)K.sc2, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g,
+             (const double2*)K.dots1, K.rawc, K.cnt + 1, h, use_h);
     return post_launch(C);
   };
   CKR(run_while(C, st, begin, body));
-  k_fgm_backsub<<<1, 32, 0, C.s>>>(st, K.H, K.g, K.y, outer_stats);
+  launch_k(C, k_fgm_backsub, 1, 32, 0, st, K.H, K.g, K.y, outer_stats);
   CKR(post_launch(C));
   // x = (x or 0) + Z y
   return gs_update(C, K, K.Z, &st->ncols, 0, K.y, 1.0, first ? DVec() : DVec(x), DVec(x), 0, nullptr);
@@ -481,7 +526,7 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
 // (reading R11), no restart (capacity inner_maxit, as the oracle).
 int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_stats) {
   Fgm& K = C.inner;
-  k_fgm_reset<<<1, 1, 0, C.s>>>(K.st, C.p.inner_tol, C.p.inner_maxit, K.m);
+  launch_k(C, k_fgm_reset, 1, 1, 0, K.st, C.p.inner_tol, C.p.inner_maxit, K.m);
   CKR(post_launch(C));
   auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y); };
   auto opP = [&](DVec v, DVec z) { return vcycle(C, 1, v, z, nullptr); };
@@ -544,6 +589,7 @@ void helm_default_params(helm_params* p) {
   p->vectors = HELM_VECTORS_BILINEAR;
   p->graph = 1;
   p->tail_max_n = 8192;
+  p->pdl = 1;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -584,6 +630,8 @@ void helm_destroy(helm_ctx ctx) { destroy_ctx(ctx); }
 static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int k_on_device) {
   const helm_params& p = C.p;
   if (grid->nx < 1 || grid->ny < 1 || !(grid->h > 0)) return fail(HELM_EINVAL, "bad grid");
+  if ((unsigned long long)grid->nx * (unsigned long long)grid->ny >= (1ull << 32))
+    return fail(HELM_EINVAL, "grid of %dx%d unknowns exceeds 32-bit linear indexing", grid->nx, grid->ny);
   if (grid->bc != HELM_BC_DIRICHLET && grid->bc != HELM_BC_SOMMERFELD) return fail(HELM_EINVAL, "bad bc");
   if (grid->bc == HELM_BC_SOMMERFELD && (grid->nx < 2 || grid->ny < 2))
     return fail(HELM_EINVAL, "Sommerfeld grid needs >= 2 nodes per direction");
@@ -640,7 +688,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   for (size_t l = 1; l < C.L.size(); ++l) {
     const Level& F = C.L[l - 1];
     Level& G = C.L[l];
-    k_sample_k<<<grd2d(G.g.nx, G.g.ny), blk2d(), 0, C.s>>>(F.g, G.g, F.o, F.k, G.k);
+    launch_k(C, k_sample_k, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, F.k, G.k);
     CKR(post_launch(C));
   }
   // level descriptors for the single-CTA tail
@@ -667,7 +715,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     if (C.tail_lt >= 0) {
       C.tail_smem.assign(C.L.size(), 0);
       for (int l = C.tail_lt; l <= last; ++l) C.tail_smem[l] = tail_smem_bytes(ds.data(), l, last);
-      CK(cudaFuncSetAttribute(k_vc_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TAIL_SMEM_MAX));
+      CKR(raise_dyn_smem((const void*)k_vc_tail, TAIL_SMEM_MAX));
     }
   }
   // coarsest dense inverse (reading R8): Gauss-Jordan with partial pivoting on device
@@ -685,7 +733,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     CKR(dalloc(&piv, 1));
     CKR(dalloc(&C.Minv, (size_t)n * n));
     CK(cudaMemsetAsync(Md, 0, (size_t)n * n * sizeof(double2), C.s));
-    k_dense_op<<<grd2d(Lc.g.nx, Lc.g.ny), blk2d(), 0, C.s>>>(Lc.g, Lc.k, p.beta1, p.beta2, Md);
+    launch_k(C, k_dense_op, grd2d(Lc.g.nx, Lc.g.ny), blk2d(), 0, Lc.g, Lc.k, p.beta1, p.beta2, Md);
     CKR(post_launch(C));
     std::vector<cplx> eye((size_t)n * 2 * n, cplx(0, 0));
     for (int r = 0; r < n; ++r) eye[(size_t)r * 2 * n + n + r] = 1.0;
@@ -693,14 +741,14 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     CK(cudaMemcpy2DAsync(Aug, 2 * n * sizeof(double2), Md, n * sizeof(double2), n * sizeof(double2), n,
                          cudaMemcpyDeviceToDevice, C.s));
     for (int col = 0; col < n; ++col) {
-      k_gj_pivot<<<1, 1024, 0, C.s>>>(Aug, n, col, piv);
+      launch_k(C, k_gj_pivot, 1, 1024, 0, Aug, n, col, piv);
       CKR(post_launch(C));
-      k_gj_swap_scale<<<1, 1024, 0, C.s>>>(Aug, n, col, piv, colbuf);
+      launch_k(C, k_gj_swap_scale, 1, 1024, 0, Aug, n, col, piv, colbuf);
       CKR(post_launch(C));
-      k_gj_eliminate<<<grid1d(C, (size_t)n * 2 * n), 256, 0, C.s>>>(Aug, n, col, colbuf);
+      launch_k(C, k_gj_eliminate, grid1d(C, (size_t)n * 2 * n), 256, 0, Aug, n, col, colbuf);
       CKR(post_launch(C));
     }
-    k_gj_extract<<<grid1d(C, (size_t)n * n), 256, 0, C.s>>>(Aug, n, C.Minv);
+    launch_k(C, k_gj_extract, grid1d(C, (size_t)n * n), 256, 0, Aug, n, C.Minv);
     CKR(post_launch(C));
     CK(cudaStreamSynchronize(C.s));
     cudaFree(Md);
@@ -843,7 +891,7 @@ static int solve_device(helm_ctx_s& C, double tol, int maxit, helm_report* rep) 
     C.g_maxit = maxit;
   }
   auto t0 = std::chrono::steady_clock::now();
-  k_fgm_reset<<<1, 1, 0, C.s>>>(C.outer.st, tol, maxit, C.outer.m);
+  launch_k(C, k_fgm_reset, 1, 1, 0, C.outer.st, tol, maxit, C.outer.m);
   CKR(post_launch(C));
   int cycles = 0;
   long long kernels = 1;
@@ -939,14 +987,84 @@ int helm_flush_l2(helm_ctx C, size_t bytes) {
   const size_t n = (bytes + 15) / 16;
   if (n > C->flush_n) {
     if (C->flush) cudaFree(C->flush);
-    CKR(dalloc(&C->flush, n));
+    CKR(dalloc(&C->flush, n + (size_t)C->sm_count * 8));
+    CK(cudaMemsetAsync(C->flush, 0, (n + (size_t)C->sm_count * 8) * sizeof(uint4), C->s));
     C->flush_n = n;
   }
-  k_l2flush<<<C->sm_count * 8, 256, 0, C->s>>>(C->flush, n, (unsigned)C->launches);
+  k_l2flush<<<C->sm_count * 8, 256, 0, C->s>>>(C->flush, n, reinterpret_cast<unsigned*>(C->flush + n));
   return post_launch(*C);
 }
 
 long long helm_launch_count(helm_ctx C) { return C ? C->launches : 0; }
+
+int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_region) {
+  if (!C || reps < 1 || !us_per_region) return fail(HELM_EINVAL, "bad argument");
+  helm_ctx_s& X = *C;
+  if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
+  const Level& F = X.L[0];
+  const Level& G = X.L[1];
+  cudaStream_t saved = X.s;
+  X.s = X.own;
+  X.capturing = true;
+  CK(cudaStreamBeginCapture(X.s, cudaStreamCaptureModeRelaxed));
+  int r = HELM_OK;
+  for (int i = 0; i < reps && r == HELM_OK; ++i) {
+    switch (which) {
+      case HELM_GB_VCYCLE: {
+        const Level& L = X.L[arg];
+        // input/output: scratch fields of the level above (level 0: the A-DEF1 scratch)
+        double2* fin = arg == 0 ? X.dt : X.L[arg - 1].s;
+        double2* uout = arg == 0 ? X.dq : X.L[arg - 1].t;
+        (void)L;
+        r = vcycle(X, arg, DVec(fin), DVec(uout), nullptr);
+        break;
+      }
+      case HELM_GB_APPLY_E:
+        r = apply_E(X, DVec(X.cc), DVec(), DVec(X.ce));
+        break;
+      case HELM_GB_APPLY_A:
+        r = op_apply(X, F, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
+        break;
+      default:
+        r = fail(HELM_EINVAL, "unknown region %d", which);
+    }
+  }
+  (void)G;
+  cudaGraph_t g;
+  cudaError_t e = cudaStreamEndCapture(X.s, &g);
+  X.capturing = false;
+  if (r != HELM_OK) {
+    X.s = saved;
+    return r;
+  }
+  if (e != cudaSuccess) {
+    X.s = saved;
+    return fail(HELM_ECUDA, "bench capture: %s", cudaGetErrorString(e));
+  }
+  cudaGraphExec_t ex;
+  e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    X.s = saved;
+    return fail(HELM_ECUDA, "bench instantiate: %s", cudaGetErrorString(e));
+  }
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaGraphLaunch(ex, X.s));   // warm-up
+  CK(cudaEventRecord(e0, X.s));
+  for (int t = 0; t < 3; ++t) CK(cudaGraphLaunch(ex, X.s));
+  CK(cudaEventRecord(e1, X.s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ex);
+  X.s = saved;
+  *us_per_region = 1e3 * ms / (3.0 * reps);
+  return HELM_OK;
+}
 
 int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, double* us_per_launch,
                       double* bytes_per_launch) {
@@ -999,16 +1117,17 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
       }
       case HELM_KB_GS_DOTS:
         bytes = (double)G.n * 16.0 * (arg + 1);
-        k_dcgs_dots<<<dim3(K.geo.gx, K.geo.gy), GS_THREADS, 0, X.s>>>(K.V, (long long)K.n, dn, 1,
+        k_dcgs_dots<<<dim3(K.geo.gx, K.geo.gy), DC_THREADS, dcgs_dots_smem(K), X.s>>>(K.V, (long long)K.n, dn, 1,
                                                                       DVec(K.V + (size_t)(arg - 1) * K.n),
                                                                       DVec(K.V + (size_t)arg * K.n), (long long)K.n,
                                                                       K.geo.chunk, K.part);
         return post_launch(X);
       case HELM_KB_GS_UPDATE: {
         bytes = (double)G.n * 16.0 * (arg + 3);
-        k_dcgs_update<<<K.geo.gu, GS_THREADS, (size_t)(2 * K.m + 2) * sizeof(double2), X.s>>>(
+        k_dcgs_update<<<K.geo.gu, DU_THREADS, dcgs_update_smem(K.m), X.s>>>(
             K.V, (long long)K.n, dn, K.coef, K.sc2, DVec(K.V + (size_t)(arg - 1) * K.n), DVec(K.V + (size_t)arg * K.n),
-            (long long)K.n, K.part);
+            (long long)K.n, K.part, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+            cudaGraphConditionalHandle(0), 0);
         return post_launch(X);
       }
     }

@@ -8,6 +8,15 @@
 
 namespace helm {
 
+// Programmatic dependent launch (PDL): every kernel first waits until the grids it depends on
+// have completed and their writes are visible (a no-op when launched without the attribute),
+// then lets its own dependents be scheduled (they block in the same wait until this grid ends).
+#define HELM_PDL_ENTRY()                                      \
+  do {                                                        \
+    asm volatile("griddepcontrol.wait;" ::: "memory");        \
+    asm volatile("griddepcontrol.launch_dependents;" :::);    \
+  } while (0)
+
 // ------------------------------------------------------------------ complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -32,14 +41,20 @@ enum { BC_DIRICHLET = 0, BC_SOMMERFELD = 1 };
 // A field pointer that may be indexed by a device-resident counter: address = p + (*idx) * stride.
 // Krylov kernels captured once into a CUDA graph read the current basis slot (V[j], Z[j]) this
 // way, so one graph serves every iteration of the device-controlled FGMRES loop.
+// An optional device-resident scale `sc` is applied by the kernels that read the field through
+// it (value = *sc * p[i]): the FGMRES basis vector v~_{j+1} = w'/||w'|| is consumed without a
+// separate normalisation pass.
 struct DVec {
   double2* p;
   const int* idx;
   long long stride;
-  __host__ __device__ DVec(double2* p_ = nullptr) : p(p_), idx(nullptr), stride(0) {}
-  __host__ __device__ DVec(const double2* p_) : p(const_cast<double2*>(p_)), idx(nullptr), stride(0) {}
-  __host__ __device__ DVec(double2* p_, const int* i, long long s) : p(p_), idx(i), stride(s) {}
+  const double* sc;
+  __host__ __device__ DVec(double2* p_ = nullptr) : p(p_), idx(nullptr), stride(0), sc(nullptr) {}
+  __host__ __device__ DVec(const double2* p_) : p(const_cast<double2*>(p_)), idx(nullptr), stride(0), sc(nullptr) {}
+  __host__ __device__ DVec(double2* p_, const int* i, long long s, const double* scale = nullptr)
+      : p(p_), idx(i), stride(s), sc(scale) {}
   __device__ __forceinline__ double2* get() const { return idx ? p + (long long)(*idx) * stride : p; }
+  __device__ __forceinline__ double scale() const { return sc ? *sc : 1.0; }
 };
 
 
@@ -90,38 +105,46 @@ __device__ __forceinline__ double2 stencil_apply(const Geo& g, const double2* __
 }
 
 // ------------------------------------------------------------------ operator kernels
-// mode 0: y = Op u ;  mode 1: y = f - Op u (residual)
+// mode 0: y = Op u ;  mode 1: y = f - Op u (residual).  Linear indexing: each warp touches
+// 512 contiguous, 512-byte-aligned bytes of u, k and y (rows of odd length would misalign a
+// 2D tiling); the y-neighbours u[p -+ nx] come from L2 (the rows are re-read by the CTAs of
+// the adjacent rows shortly after), so HBM sees u, k and y once: 40 (56) B per unknown.
 template <int MODE>
-__global__ void k_apply_op(Geo g, DVec uv, DVec fv, DVec yv, const double* __restrict__ k, double sr, double si) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= g.nx || j >= g.ny) return;
+__global__ void __launch_bounds__(256) k_apply_op(Geo g, DVec uv, DVec fv, DVec yv, const double* __restrict__ k,
+                                                  double sr, double si) {
+  HELM_PDL_ENTRY();
+  const unsigned n = (unsigned)g.nx * (unsigned)g.ny;
+  const unsigned p = blockIdx.x * 256u + threadIdx.x;
+  if (p >= n) return;
   const double2* __restrict__ u = uv.get();
   const double2* __restrict__ f = fv.get();
   double2* __restrict__ y = yv.get();
-  const size_t p = (size_t)j * g.nx + i;
+  const int j = (int)(p / (unsigned)g.nx);
+  const int i = (int)(p - (unsigned)j * (unsigned)g.nx);
   Coef c = coef_at(g, i, j, k[p], sr, si);
   double2 v = stencil_apply(g, u, i, j, c);
-  if (MODE == 1) v = csub(f[p], v);
+  if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;
 }
 
 // u = omega * f / D   (first damped-Jacobi sweep from u = 0)
 __global__ void k_jacobi0(Geo g, DVec fv, double2* __restrict__ u,
                           const double* __restrict__ k, double sr, double si, double omega) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
   const double2* __restrict__ f = fv.get();
   const size_t p = (size_t)j * g.nx + i;
   Coef c = coef_at(g, i, j, k[p], sr, si);
-  u[p] = cscale(omega, cdiv(f[p], c.ap));
+  u[p] = cscale(omega, cdiv(cscale(fv.scale(), f[p]), c.ap));
 }
 
 // unew = u + omega * (f - M u) / D  (+ optional add of `q`, used to fuse z = M^-1 t + q)
 __global__ void k_jacobi(Geo g, const double2* __restrict__ u, DVec fv,
                          DVec unewv, const double* __restrict__ k, double sr, double si,
                          double omega, const double2* __restrict__ addq) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
@@ -129,7 +152,7 @@ __global__ void k_jacobi(Geo g, const double2* __restrict__ u, DVec fv,
   double2* __restrict__ unew = unewv.get();
   const size_t p = (size_t)j * g.nx + i;
   Coef c = coef_at(g, i, j, k[p], sr, si);
-  double2 r = csub(f[p], stencil_apply(g, u, i, j, c));
+  double2 r = csub(cscale(fv.scale(), f[p]), stencil_apply(g, u, i, j, c));
   double2 v = cadd(u[p], cscale(omega, cdiv(r, c.ap)));
   if (addq) v = cadd(v, addq[p]);
   unew[p] = v;
@@ -137,6 +160,7 @@ __global__ void k_jacobi(Geo g, const double2* __restrict__ u, DVec fv,
 
 // Full weighting (Eq. 3.8), gather at fine node (2I+o, 2J+o); out-of-array taps dropped.
 __global__ void k_restrict(Geo gf, Geo gc, int o, const double2* __restrict__ v, double2* __restrict__ vc) {
+  HELM_PDL_ENTRY();
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   if (I >= gc.nx || J >= gc.ny) return;
@@ -162,6 +186,7 @@ __global__ void k_restrict(Geo gf, Geo gc, int o, const double2* __restrict__ v,
 template <int MODE>
 __global__ void k_prolong(Geo gf, Geo gc, int o, const double2* __restrict__ e, const double2* __restrict__ base,
                           DVec yv, const double2* __restrict__ addq) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= gf.nx || j >= gf.ny) return;
@@ -190,6 +215,7 @@ __global__ void k_prolong(Geo gf, Geo gc, int o, const double2* __restrict__ e, 
 
 // Coarse wavenumber sampled at coincident fine nodes (re-discretisation, §5.1).
 __global__ void k_sample_k(Geo gf, Geo gc, int o, const double* __restrict__ kf, double* __restrict__ kc) {
+  HELM_PDL_ENTRY();
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   if (I >= gc.nx || J >= gc.ny) return;
@@ -212,10 +238,12 @@ __device__ __forceinline__ double zrs() { return R == 1 ? 0.25 : 1.0; }
 // vc = RS * Z^T v  (gather of the (2R+1)^2 fine taps; out-of-array taps dropped, reading R4)
 template <int R>
 __global__ void k_restrict_z(Geo gf, Geo gc, int o, DVec vv, double2* __restrict__ vc) {
+  HELM_PDL_ENTRY();
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   if (I >= gc.nx || J >= gc.ny) return;
   const double2* __restrict__ v = vv.get();
+  const double vs = vv.scale();
   const int ci = 2 * I + o, cj = 2 * J + o;
   double2 s = make_double2(0.0, 0.0);
 #pragma unroll
@@ -230,13 +258,14 @@ __global__ void k_restrict_z(Geo gf, Geo gc, int o, DVec vv, double2* __restrict
       s = cadd(s, cscale(wy * zw<R>(a), v[(size_t)jj * gf.nx + ii]));
     }
   }
-  vc[(size_t)J * gc.nx + I] = cscale(zrs<R>(), s);
+  vc[(size_t)J * gc.nx + I] = cscale(zrs<R>() * vs, s);
 }
 
 // y = Z e (MODE 0) or y = base + Z e (MODE 1), gather at each fine node.
 template <int R, int MODE>
 __global__ void k_prolong_z(Geo gf, Geo gc, int o, const double2* __restrict__ e, const double2* __restrict__ base,
                             double2* __restrict__ y) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= gf.nx || j >= gf.ny) return;
@@ -264,15 +293,38 @@ __global__ void k_prolong_z(Geo gf, Geo gc, int o, const double2* __restrict__ e
 // stencil, would move ~10x more).  MODE 1: y = f - E x.
 __device__ __forceinline__ int ceildiv2(int a) { return (a >= 0) ? ((a + 1) >> 1) : -((-a) >> 1); }
 
+__device__ __forceinline__ int floordiv2i(int a) { return (a >= 0) ? (a >> 1) : -((-a + 1) >> 1); }
+
+// 1D interpolation of a coarse line at relative fine position r = fine - o (taps at coarse
+// floor(r/2) - 1 .. floor(r/2) + 2 with the weights zw<R>; zero weights skipped at compile time
+// of the unrolled loop).  `at(I)` returns the coarse value (0 outside the array).
+template <int R, class At>
+__device__ __forceinline__ double2 interp1(int r, At&& at) {
+  const int Ib = floordiv2i(r);
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int d = -1; d <= 2; ++d) {
+    const double w = zw<R>(r - 2 * (Ib + d));
+    if (w != 0.0) s = cadd(s, cscale(w, at(Ib + d)));
+  }
+  return s;
+}
+
 template <int R, int MODE, int TCX, int TCY>
 __global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
                                                         DVec fv, DVec yv) {
-  constexpr int SX = 2 * TCX - 1 + 2 * R, SY = 2 * TCY - 1 + 2 * R;   // s = A t region
+  HELM_PDL_ENTRY();
+  constexpr int SX = 2 * TCX - 1 + 2 * R, SY = 2 * TCY - 1 + 2 * R;   // s = A t region (fine)
   constexpr int TXR = SX + 2, TYR = SY + 2;                          // t = Z x region (A halo)
   constexpr int CXW = TCX + 2 * R, CYW = TCY + 2 * R;                 // coarse x region
-  __shared__ double2 sx[CYW * CXW];
-  __shared__ double2 stt[TYR * TXR];
-  __shared__ double2 ss[SY * SX];
+  // tx (x-interpolated coarse rows) is dead once t is formed: s = A t reuses its storage
+  constexpr int TXN = CYW * TXR, SSN = SY * SX;
+  __shared__ double2 sx[CYW * CXW];              // x on the coarse region
+  __shared__ double2 txss[TXN > SSN ? TXN : SSN]; // tx, then s
+  __shared__ double2 stt[TYR * TXR];             // t = Z x
+  __shared__ double2 ry[TCY * SX];               // s restricted along y (coarse rows, fine columns)
+  double2* const tx = txss;
+  double2* const ss = txss;
   const double2* __restrict__ x = xv.get();
   const int I0 = blockIdx.x * TCX, J0 = blockIdx.y * TCY;
   const int fx0s = 2 * I0 + o - R, fy0s = 2 * J0 + o - R;
@@ -283,18 +335,30 @@ __global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, c
     sx[t] = (I >= 0 && I < gc.nx && J >= 0 && J < gc.ny) ? x[(size_t)J * gc.nx + I] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < TXR * TYR; t += blockDim.x) {
-    const int fx = fx0t + t % TXR, fy = fy0t + t / TXR;
+  // Z is the tensor product of the 1D interpolations (Eq. 3.9 / 3.12): along x ...
+  for (int t = threadIdx.x; t < CYW * TXR; t += blockDim.x) {
+    const int row = t / TXR, fx = fx0t + t % TXR;
     double2 v = make_double2(0.0, 0.0);
-    if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
-      const int ri = fx - o, rj = fy - o;
-      const int ilo = ceildiv2(ri - R), ihi = (ri + R + 2 * 64) / 2 - 64;
-      const int jlo = ceildiv2(rj - R), jhi = (rj + R + 2 * 64) / 2 - 64;
-      for (int J = jlo; J <= jhi; ++J) {
-        const double wy = zw<R>(rj - 2 * J);
-        for (int I = ilo; I <= ihi; ++I)
-          v = cadd(v, cscale(wy * zw<R>(ri - 2 * I), sx[(J - cy0) * CXW + (I - cx0)]));
-      }
+    if (fx >= 0 && fx < gf.nx) {
+      const double2* line = sx + row * CXW;
+      v = interp1<R>(fx - o, [&](int I) {
+        const int li = I - cx0;
+        return (li >= 0 && li < CXW) ? line[li] : make_double2(0.0, 0.0);
+      });
+    }
+    tx[t] = v;
+  }
+  __syncthreads();
+  // ... then along y
+  for (int t = threadIdx.x; t < TYR * TXR; t += blockDim.x) {
+    const int col = t % TXR, fy = fy0t + t / TXR;
+    const int fx = fx0t + col;
+    double2 v = make_double2(0.0, 0.0);
+    if (fy >= 0 && fy < gf.ny && fx >= 0 && fx < gf.nx) {
+      v = interp1<R>(fy - o, [&](int J) {
+        const int lj = J - cy0;
+        return (lj >= 0 && lj < CYW) ? tx[lj * TXR + col] : make_double2(0.0, 0.0);
+      });
     }
     stt[t] = v;
   }
@@ -315,22 +379,29 @@ __global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, c
     ss[t] = v;
   }
   __syncthreads();
+  // Z^T = tensor product of the transposed 1D interpolations: along y ...
+  for (int t = threadIdx.x; t < TCY * SX; t += blockDim.x) {
+    const int jl = t / SX, ix = t % SX;
+    const int iy = 2 * jl + R;
+    double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int b = -R; b <= R; ++b) v = cadd(v, cscale(zw<R>(b), ss[(iy + b) * SX + ix]));
+    ry[t] = v;
+  }
+  __syncthreads();
+  // ... then along x
   const double2* __restrict__ f = fv.get();
   double2* __restrict__ y = yv.get();
   for (int t = threadIdx.x; t < TCX * TCY; t += blockDim.x) {
     const int I = I0 + t % TCX, J = J0 + t / TCX;
     if (I >= gc.nx || J >= gc.ny) continue;
-    const int ix = 2 * (I - I0) + R, iy = 2 * (J - J0) + R;
+    const int ix = 2 * (I - I0) + R, jl = J - J0;
     double2 s = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int b = -R; b <= R; ++b) {
-      const double wy = zw<R>(b);
-#pragma unroll
-      for (int a = -R; a <= R; ++a) s = cadd(s, cscale(wy * zw<R>(a), ss[(iy + b) * SX + ix + a]));
-    }
+    for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
     s = cscale(zrs<R>(), s);
     const size_t p = (size_t)J * gc.nx + I;
-    y[p] = (MODE == 1) ? csub(f[p], s) : s;
+    y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
   }
 }
 
@@ -384,6 +455,7 @@ __device__ double2 glk2_val(const Geo& g, const double2* __restrict__ x, const d
 // VARIANT 1: ReD-Glk1, VARIANT 2: ReD-Glk2 (reading R14: second-order rows scaled by 4).
 template <int VARIANT, int MODE>
 __global__ void k_apply_red_glk(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
@@ -415,7 +487,7 @@ __global__ void k_apply_red_glk(Geo g, DVec xv, DVec fv, DVec yv, const double* 
     Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
     v = cscale(4.0, stencil_apply(g, x, i, j, c));
   }
-  if (MODE == 1) v = csub(f[p], v);
+  if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;
 }
 
@@ -423,6 +495,7 @@ __global__ void k_apply_red_glk(Geo g, DVec xv, DVec fv, DVec yv, const double* 
 // second-order Helmholtz stencil elsewhere (reading R6).
 template <int MODE>
 __global__ void k_apply_red_o4(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
@@ -450,7 +523,7 @@ __global__ void k_apply_red_o4(Geo g, DVec xv, DVec fv, DVec yv, const double* _
     Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
     v = stencil_apply(g, x, i, j, c);
   }
-  if (MODE == 1) v = csub(f[p], v);
+  if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;
 }
 
@@ -458,6 +531,7 @@ __global__ void k_apply_red_o4(Geo g, DVec xv, DVec fv, DVec yv, const double* _
 // where the 7-wide cross fits in the closed domain, second-order stencil elsewhere (reading R6).
 template <int MODE>
 __global__ void k_apply_red_o6(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
@@ -487,7 +561,7 @@ __global__ void k_apply_red_o6(Geo g, DVec xv, DVec fv, DVec yv, const double* _
     Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
     v = stencil_apply(g, x, i, j, c);
   }
-  if (MODE == 1) v = csub(f[p], v);
+  if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;
 }
 
@@ -522,6 +596,7 @@ __device__ __forceinline__ double2 cmp_val(const Geo& g, const double2* __restri
 
 template <int MODE>
 __global__ void k_apply_red_cmpo4(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
@@ -552,13 +627,14 @@ __global__ void k_apply_red_cmpo4(Geo g, DVec xv, DVec fv, DVec yv, const double
   const double2 lap = cscale(iH2, cadd(cadd(cscale(A0, c), cscale(AS, side)), cscale(AC, corner)));
   const double2 mass = cadd(cadd(cscale(B0, c), cscale(BS, side)), cscale(BC, corner));
   double2 v = csub(lap, cscale(k2, mass));
-  if (MODE == 1) v = csub(f[p], v);
+  if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;
 }
 
 // ------------------------------------------------------------------ coarsest dense solve
 // Dense M of the coarsest level, row-major n x n (row = unknown p).
 __global__ void k_dense_op(Geo g, const double* __restrict__ k, double sr, double si, double2* __restrict__ Md) {
+  HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= g.nx || j >= g.ny) return;
@@ -575,6 +651,7 @@ __global__ void k_dense_op(Geo g, const double* __restrict__ k, double sr, doubl
 
 // Gauss-Jordan with partial pivoting on the augmented [M | I] (n x 2n, row-major).
 __global__ void k_gj_pivot(const double2* __restrict__ Aug, int n, int col, int* __restrict__ piv) {
+  HELM_PDL_ENTRY();
   // one block: argmax_{r >= col} |Aug[r][col]|
   __shared__ double sv[1024];
   __shared__ int si[1024];
@@ -603,6 +680,7 @@ __global__ void k_gj_pivot(const double2* __restrict__ Aug, int n, int col, int*
 
 __global__ void k_gj_swap_scale(double2* __restrict__ Aug, int n, int col, const int* __restrict__ piv,
                                 double2* __restrict__ colbuf) {
+  HELM_PDL_ENTRY();
   const int p = *piv;
   const int w = 2 * n;
   // swap rows col and p, then scale row col by 1/pivot; one block
@@ -624,6 +702,7 @@ __global__ void k_gj_swap_scale(double2* __restrict__ Aug, int n, int col, const
 }
 
 __global__ void k_gj_eliminate(double2* __restrict__ Aug, int n, int col, const double2* __restrict__ colbuf) {
+  HELM_PDL_ENTRY();
   const int w = 2 * n;
   const size_t total = (size_t)n * w;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
@@ -636,6 +715,7 @@ __global__ void k_gj_eliminate(double2* __restrict__ Aug, int n, int col, const 
 }
 
 __global__ void k_gj_extract(const double2* __restrict__ Aug, int n, double2* __restrict__ Minv) {
+  HELM_PDL_ENTRY();
   const size_t total = (size_t)n * n;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
     const int r = (int)(t / n), c = (int)(t % n);
@@ -645,6 +725,7 @@ __global__ void k_gj_extract(const double2* __restrict__ Aug, int n, double2* __
 
 // y = Minv f, one warp per row.
 __global__ void k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv, const double2* __restrict__ addq) {
+  HELM_PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -653,6 +734,7 @@ __global__ void k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv
   const double2* row = Minv + (size_t)warp * n;
   double2 s = make_double2(0.0, 0.0);
   for (int c = lane; c < n; c += 32) s = cfma(row[c], f[c], s);
+  s = cscale(fv.scale(), s);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
@@ -663,6 +745,7 @@ __global__ void k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv
 
 // y = a + b
 __global__ void k_add(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ y, size_t n) {
+  HELM_PDL_ENTRY();
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     y[e] = cadd(a[e], b[e]);
 }

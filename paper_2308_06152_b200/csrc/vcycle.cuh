@@ -38,11 +38,13 @@ template <int TCX, int TCY>
 __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
                                                  double sr, double si, double omega, double2* __restrict__ u,
                                                  double2* __restrict__ fc) {
+  HELM_PDL_ENTRY();
   constexpr int RX = 2 * TCX + 3, RY = 2 * TCY + 3;  // u region
   constexpr int QX = 2 * TCX + 1, QY = 2 * TCY + 1;  // r region
   __shared__ double2 su[RY * RX];
   __shared__ double2 sq[QY * QX];
   const double2* __restrict__ f = fv.get();
+  const double fs = fv.scale();
   const int I0 = blockIdx.x * TCX, J0 = blockIdx.y * TCY;
   const int gx0 = 2 * I0 + o - 2, gy0 = 2 * J0 + o - 2;
   // fine points whose pre-smoothed u this CTA owns (a partition of the fine grid)
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, c
     if (x >= 0 && x < F.nx && y >= 0 && y < F.ny) {
       const size_t p = (size_t)y * F.nx + x;
       const Coef c = coef_at(F, x, y, k[p], sr, si);
-      uv = cscale(omega, cdiv(f[p], c.ap));   // reading R9: first sweep from u = 0
+      uv = cscale(omega, cdiv(cscale(fs, f[p]), c.ap));   // reading R9: first sweep from u = 0
       if (x >= xs && x < xe && y >= ys && y < ye) u[p] = uv;
     }
     su[t] = uv;
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, c
       const size_t p = (size_t)y * F.nx + x;
       const Coef c = coef_at(F, x, y, k[p], sr, si);
       const int q = (iy + 1) * RX + (ix + 1);
-      rv = csub(f[p], stencil5(c, su[q], su[q - 1], su[q + 1], su[q - RX], su[q + RX]));
+      rv = csub(cscale(fs, f[p]), stencil5(c, su[q], su[q - 1], su[q + 1], su[q - RX], su[q + RX]));
     }
     sq[t] = rv;
   }
@@ -99,11 +101,13 @@ __global__ void __launch_bounds__(256) k_vc_up(Geo F, Geo G, int o, const double
                                                const double2* __restrict__ e, DVec fv,
                                                const double* __restrict__ k, double sr, double si, double omega,
                                                const double2* __restrict__ addq, DVec yv) {
+  HELM_PDL_ENTRY();
   constexpr int RX = TX + 2, RY = TY + 2;
   constexpr int CX = TX / 2 + 3, CY = TY / 2 + 3;
   __shared__ double2 se[CY * CX];
   __shared__ double2 s1[RY * RX];
   const double2* __restrict__ f = fv.get();
+  const double fs = fv.scale();
   double2* __restrict__ y = yv.get();
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int cx0 = floordiv2(x0 - 1 - o), cy0 = floordiv2(y0 - 1 - o);
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(256) k_vc_up(Geo F, Geo G, int o, const double
     const size_t p = (size_t)yy * F.nx + x;
     const Coef c = coef_at(F, x, yy, k[p], sr, si);
     const int q = (t / TX + 1) * RX + (t % TX + 1);
-    const double2 r = csub(f[p], stencil5(c, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
+    const double2 r = csub(cscale(fs, f[p]), stencil5(c, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
     double2 v = cadd(s1[q], cscale(omega, cdiv(r, c.ap)));
     if (addq) v = cadd(v, addq[p]);
     y[p] = v;
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
                                                   DVec uv, const double2* __restrict__ addq, double sr, double si,
                                                   double omega, int nu_pre, int nu_post,
                                                   const double2* __restrict__ Minv) {
+  HELM_PDL_ENTRY();
   extern __shared__ double2 tsm[];
   __shared__ TailLevel T[TAIL_MAX_LEVELS];
   __shared__ int curi[TAIL_MAX_LEVELS];   // 0: pre-smoothed iterate in s, 1: in t
@@ -224,7 +229,8 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
   }
   {
     const int n = T[0].g.nx * T[0].g.ny;
-    for (int p = threadIdx.x; p < n; p += blockDim.x) T[0].f[p] = fin[p];
+    const double fs = fv.scale();
+    for (int p = threadIdx.x; p < n; p += blockDim.x) T[0].f[p] = cscale(fs, fin[p]);
   }
   __syncthreads();
   // ---- down

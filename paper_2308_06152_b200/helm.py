@@ -30,7 +30,7 @@ class helm_params(ctypes.Structure):
                 ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("coarse_op", ctypes.c_int),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int),
-                ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int)]
+                ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int), ("pdl", ctypes.c_int)]
 
 
 class helm_report(ctypes.Structure):
@@ -66,6 +66,7 @@ EXPORTS = {
     "helm_flush_l2": (_I, [_P, ctypes.c_size_t]),
     "helm_launch_count": (ctypes.c_longlong, [_P]),
     "helm_bench_kernel": (_I, [_P, _I, _I, _I, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
+    "helm_bench_graph": (_I, [_P, _I, _I, _I, ctypes.POINTER(_D)]),
     "helm_last_error": (ctypes.c_char_p, []),
     "helm_build_info": (ctypes.c_char_p, []),
 }
@@ -245,6 +246,15 @@ class Helm:
         _check(self.lib.helm_bench_kernel(self.ctx, self.KERNELS.get(which, which), int(arg), int(reps), int(flush),
                                           ctypes.byref(us), ctypes.byref(nb)))
         return us.value, nb.value
+
+    REGIONS = {"vcycle": 0, "apply_E": 1, "apply_A": 2}
+
+    def helm_bench_graph(self, which, arg=0, reps=50):
+        """Mean in-graph device time (us) of one instance of a region (warm, back-to-back)."""
+        us = _D()
+        _check(self.lib.helm_bench_graph(self.ctx, self.REGIONS.get(which, which), int(arg), int(reps),
+                                         ctypes.byref(us)))
+        return us.value
 
     def helm_launch_count(self):
         return int(self.lib.helm_launch_count(self.ctx))
