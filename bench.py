@@ -32,8 +32,11 @@ sys.path.insert(0, ROOT)
 # Method of the timed workload: higher-order deflation vectors (APD, the
 # paper's wavenumber-independent variant, Table 4) with the Galerkin coarse operator E; the
 # coarse problem solved by CSLP-FGMRES to 1e-1 (§6.3, the GCR/FGMRES setting) capped
-# at 50 iterations, the inner counts the paper reports for that setting (Tables 9-10).
-DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 50}
+# at 50 iterations, the inner counts the paper reports for that setting (Tables 9-10); the
+# CSLP hierarchy stops at the first level with <= 512 unknowns (§4 "predefined
+# coarsest grid size"), solved exactly (R8).
+DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 50,
+                  "coarsest_n": 512}
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 
@@ -93,14 +96,14 @@ class ClockSampler:
 
 def method_of(args):
     return {"vectors": args.vectors, "coarse_op": args.coarse_op, "inner_tol": args.inner_tol,
-            "inner_maxit": args.inner_maxit}
+            "inner_maxit": args.inner_maxit, "coarsest_n": args.coarsest_n}
 
 
 def oracle_params(args, **kw):
     import oracle
     m = method_of(args)
     return oracle.SolverParams(vectors=m["vectors"], coarse_op=m["coarse_op"], inner_tol=m["inner_tol"],
-                               inner_maxit=m["inner_maxit"], **kw)
+                               inner_maxit=m["inner_maxit"], coarsest_n=m["coarsest_n"], **kw)
 
 
 def dist_env():
@@ -176,37 +179,45 @@ def cpu_baseline_sample(args, n_outer=1):
 
 
 def kernel_roofline(H, rep, peaks, reps=20):
-    """Per-kernel device time (CUDA events on the library stream, L2 flushed before each
-    launch, at the sizes the workload runs them) and algorithmic bytes.  The
-    kernel with the largest estimated share of a step is the `roofline` line.  Launch counts
-    per step come from the solve's own iteration counts: every inner iteration runs one E
-    apply, the fused V-cycle legs on levels 1.. (above the single-CTA tail) and the two
-    delayed-CGS2 sweeps over j+1 basis vectors (mean j = half the mean inner count: the cost
-    is linear in j); every outer iteration runs the level-0 legs and two A applies."""
+    """The roofline line of the step's dominant component, measured live here with CUDA events.
+
+    The solve is a chain of small dependent kernels, so each component is timed the way it runs
+    inside the solve: `reps` back-to-back instances captured into one CUDA graph and replayed
+    (helm_bench_graph, warm).  Components: one delayed-CGS2 step of the inner FGMRES at the
+    mean basis size (pass 1, reduction + step A, pass 2 + step B), one V-cycle from level 1,
+    one E apply, one A apply.  Counts per step come from the solve's own iteration counts.
+    Algorithmic bytes: DCGS2 step (2j + 7) * 16 n1; V-cycle sum over levels of
+    (40 + 56) n_l + 32 n_{l+1} plus the dense coarsest inverse; E 32 n1 + 8 n0; A 40 n0.  The
+    isolated per-kernel timings (L2 flushed before each launch) are reported beside it."""
     inner_its = rep["inner_iterations_total"]
     outer_its = rep["outer_iterations"]
     jm = max(1, int(round(rep["inner_iterations_total"] / max(1, rep["inner_solves"]) / 2)))
+    lv = [ny * nx for (ny, nx, _) in H.levels]
+    n0, n1 = lv[0], lv[1]
+    vbytes = sum(96.0 * lv[l] + 32.0 * lv[l + 1] for l in range(1, len(lv) - 1)) + 16.0 * lv[-1] ** 2
+    comps = [("dcgs2 step (inner, j=%d)" % jm, "dcgs", jm, 10, inner_its, (2 * jm + 7) * 16.0 * n1),
+             ("V-cycle from level 1 (inner preconditioner)", "vcycle", 1, 20, inner_its + outer_its, vbytes),
+             ("galerkin_apply E (level 1)", "apply_E", 0, 50, inner_its, 32.0 * n1 + 8.0 * n0),
+             ("apply_op A (level 0)", "apply_A", 0, 50, 2 * outer_its, 40.0 * n0)]
     rows = {}
-    todo = [("gs_dots", jm + 1, inner_its, "dcgs_dots (inner, j=%d)" % jm),
-            ("gs_update", jm + 1, inner_its, "dcgs_update (inner, j=%d)" % jm),
-            ("apply_E", 1, inner_its, "galerkin_apply E (level 1)"),
-            ("apply_A", 1, 2 * outer_its, "apply_op A (level 0)"),
-            ("vc_down", 0, outer_its, "vc_down level 0"), ("vc_up", 0, outer_its, "vc_up level 0")]
-    for lv in range(1, len(H.levels) - 1):
-        if H.levels[lv][0] * H.levels[lv][1] <= 8192:
-            break
-        todo += [("vc_down", lv, inner_its + outer_its, "vc_down level %d" % lv),
-                 ("vc_up", lv, inner_its + outer_its, "vc_up level %d" % lv)]
-    for name, arg, count, label in todo:
-        us, nbytes = H.helm_bench_kernel(name, arg=arg, reps=reps, flush=True)
+    for label, region, arg, nrep, count, nbytes in comps:
+        us = H.helm_bench_graph(region, arg, nrep)
         gbs = nbytes / (us * 1e-6) / 1e9
         rows[label] = {"kernel": label, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                        "frac": gbs / peaks["hbm_gbs"], "traffic": None, "bytes_per_launch": nbytes,
                        "us_per_launch": us, "launches_per_step": count, "est_ms_per_step": count * us * 1e-3,
-                       "peak_src": peaks["src"]}
+                       "timing": "in-graph, warm (helm_bench_graph)", "peak_src": peaks["src"]}
     dom = max(rows.values(), key=lambda r: r["est_ms_per_step"])
-    return dict(dom), {k: {kk: v[kk] for kk in ("achieved", "frac", "us_per_launch", "launches_per_step",
-                                                  "est_ms_per_step")} for k, v in rows.items()}
+    iso = {}
+    for name, arg in (("gs_dots", jm + 1), ("gs_update", jm + 1), ("apply_E", 0), ("apply_A", 0), ("vc_down", 0),
+                      ("vc_up", 0), ("vc_down", 1), ("vc_up", 1)):
+        us, nbytes = H.helm_bench_kernel(name, arg=arg, reps=reps, flush=True)
+        gbs = nbytes / (us * 1e-6) / 1e9
+        iso[f"{name}[{arg}]"] = {"us": us, "GB/s": gbs, "frac": gbs / peaks["hbm_gbs"]}
+    return dict(dom), {"components": {k: {kk: v[kk] for kk in ("achieved", "frac", "us_per_launch",
+                                                              "launches_per_step", "est_ms_per_step")}
+                                      for k, v in rows.items()},
+                       "isolated_kernels_l2_flushed": iso}
 
 
 def microbench(peaks, n=16385, reps=10):
@@ -240,6 +251,7 @@ def main():
     ap.add_argument("--vectors", default=DEFAULT_METHOD["vectors"])
     ap.add_argument("--inner-tol", type=float, default=DEFAULT_METHOD["inner_tol"])
     ap.add_argument("--inner-maxit", type=int, default=DEFAULT_METHOD["inner_maxit"])
+    ap.add_argument("--coarsest-n", type=int, default=DEFAULT_METHOD["coarsest_n"])
     ap.add_argument("--maxit", type=int, default=2000)
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

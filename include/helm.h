@@ -43,6 +43,9 @@ extern "C" {
 /* The re-discretised operators (RED_O2/O4/O6/CMPO4) replace A_{2h} as printed for either kind of
  * deflation vectors (no factor 4 for the higher-order vectors; reading R21). */
 
+#define HELM_OUTER_FGMRES 0 /* flexible GMRES, Algorithm 1 (flexible form, §6.3) */
+#define HELM_OUTER_GCR 1    /* preconditioned GCR, PAPER.md:427 and §6.3 */
+
 #define HELM_VECTORS_BILINEAR 0   /* A-DEF1: Z = Eq. 3.9, Z^T/4 = full weighting Eq. 3.8 */
 #define HELM_VECTORS_HIGH_ORDER 1 /* APD: Z = Eq. 3.12, Z^T = Eq. 3.14 (§3.2.1, §3.2.2) */
 
@@ -79,10 +82,19 @@ typedef struct {
   int graph;           /* 1 (default): helm_solve runs as one CUDA graph whose outer and inner
                           loops are conditional while nodes (no host sync inside a solve);
                           0: the same kernels with host-polled loops */
-  int tail_max_n;      /* V-cycle levels with at most this many unknowns (and everything
-                          below them) run in one single-CTA kernel; 0 disables (default 8192) */
+  int tail_max_n;      /* V-cycle levels with at most this many unknowns (and everything below
+                          them) run in one thread-block-cluster kernel whose CTAs hold the
+                          levels in distributed shared memory; 0 (default) runs every level with
+                          the per-level fused kernels */
   int pdl;             /* 1 (default): launches carry programmatic stream serialization, so a
                           kernel's CTAs are scheduled while its predecessor drains */
+  int coarsest_n;      /* coarsening stops at the first level with at most this many unknowns
+                          (§4 "predefined coarsest grid size"; 0 = as far as possible) */
+  int coop;            /* 1: for vectors up to 4M unknowns each delayed-CGS2 step is one cooperative
+                          kernel (grid barriers between its phases) instead of three; measured
+                          slower on B200 than the kernel chain, so 0 by default */
+  int outer;           /* HELM_OUTER_FGMRES (default) or HELM_OUTER_GCR; the coarse solve is
+                          always CSLP-preconditioned FGMRES */
 } helm_params;
 
 typedef struct {
@@ -126,7 +138,8 @@ int helm_vcycle(helm_ctx ctx, int level, const double* f_dev, double* u_dev);
  * E^{-1} by CSLP-preconditioned FGMRES to inner_tol (writes the inner count to
  * *inner_its if non-NULL). */
 int helm_deflate(helm_ctx ctx, const double* v_dev, double* z_dev, int* inner_its);
-/* Solve A x = b by A-DEF1/APD-preconditioned FGMRES from x0 = 0 to ||b - A x||/||b|| <= tol
+/* Solve A x = b by A-DEF1/APD-preconditioned FGMRES (or GCR, params.outer) from x0 = 0 to
+ * ||b - A x||/||b|| <= tol
  * (Algorithm 1 flexible form, Eq. 3.21).  The Arnoldi process, the Givens
  * least-squares update and both convergence tests run on the device; the whole solve is one
  * CUDA graph (params.graph = 1).  Orthogonalisation: classical Gram-Schmidt twice with the
@@ -169,6 +182,8 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_VCYCLE 0
 #define HELM_GB_APPLY_E 1
 #define HELM_GB_APPLY_A 2
+#define HELM_GB_DCGS 3      /* one delayed-CGS2 step (pass 1, reduction + step A, pass 2 + step B)
+                               of the inner FGMRES from column `arg` (arg + reps < inner_maxit) */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 const char* helm_last_error(void);

@@ -94,3 +94,51 @@ def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, his
     for i in range(m):
         x = x + y[i] * Z[i]
     return x.reshape(shape), its, converged
+
+
+def gcr(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, history=None):
+    """Preconditioned generalised conjugate residual method ("the preconditioned
+    Generalized Conjugate Residual method (GCR) [Eisenstat 1983] ... allows for variable
+    preconditioning inherently"; §6.3 uses it as the outer method).  From x0 = 0:
+        z_k = P r_k,  c_k = A z_k,
+        c_k, z_k orthogonalised against c_0..c_{k-1} (classical Gram-Schmidt twice, the same
+        coefficients applied to z_k), then scaled by 1/||c_k||,
+        beta = (r_k, c_k),  x += beta z_k,  r -= beta c_k,
+    until ||r|| / ||b|| <= tol.  Returns (x, iterations, converged)."""
+    shape = b.shape
+    bvec = b.ravel()
+    bnorm = np.linalg.norm(bvec)
+    x = np.zeros_like(bvec)
+    if bnorm == 0.0:
+        return x.reshape(shape), 0, True
+    r = bvec.copy()
+    if history is not None:
+        history.append(1.0)
+    C, Zs = [], []
+    its, conv = 0, False
+    for k in range(maxit):
+        z = apply_P(r.reshape(shape)).ravel()
+        c = apply_A(z.reshape(shape)).ravel()
+        for _ in range(2):                                   # CGS2
+            al = np.array([np.vdot(ci, c) for ci in C])
+            for i in range(len(C)):
+                c = c - al[i] * C[i]
+                z = z - al[i] * Zs[i]
+        nc = np.linalg.norm(c)
+        its = k + 1
+        if nc == 0.0:                                        # breakdown: P r in the kernel of A
+            break
+        c = c / nc
+        z = z / nc
+        beta = np.vdot(c, r)
+        x = x + beta * z
+        r = r - beta * c
+        C.append(c)
+        Zs.append(z)
+        res = np.linalg.norm(r) / bnorm
+        if history is not None:
+            history.append(res)
+        if res <= tol:
+            conv = True
+            break
+    return x.reshape(shape), its, conv

@@ -9,8 +9,11 @@ M_H in the same way that the matrix M_h is obtained on the fine mesh").
 §4: coarsening stops at a predefined coarsest grid.
 
 Readings:
-  R7  Coarsening continues while both directions are coarsenable (odd unknown count >= 3)
-      and `max_levels` is not reached; the coarse wavenumber is sampled at coincident nodes.
+  R7  Coarsening continues while both directions are coarsenable (odd unknown count >= 3),
+      `max_levels` is not reached and the current level has more than `coarsest_n` unknowns
+      (§4: "after reaching a manually predefined coarsest grid size ... the coarsening
+      operation will stop"; 0 = coarsen as far as possible); the coarse wavenumber is sampled
+      at coincident nodes.
   R8  The coarsest problem is solved exactly (dense LU, np.linalg.solve).  The paper's
       full-GMRES to 1e-8 on the coarsest level approximates this solve.
   R9  The V-cycle starts from a zero initial guess, so the first pre-smoothing sweep is
@@ -56,9 +59,10 @@ def _dense_matrix(level: Level) -> np.ndarray:
 
 
 def build_hierarchy(k: np.ndarray, h: float, bc: str, beta=(1.0, 0.5), max_levels: int = 64,
-                    max_coarsest: int = 4096):
+                    max_coarsest: int = 4096, coarsest_n: int = 0):
     levels = [Level(k.shape, h, k, bc, tuple(beta))]
-    while len(levels) < max_levels and coarsenable(levels[-1].shape, bc):
+    while (len(levels) < max_levels and coarsenable(levels[-1].shape, bc)
+           and levels[-1].shape[0] * levels[-1].shape[1] > coarsest_n):
         L = levels[-1]
         levels.append(Level(coarse_shape(L.shape, bc), 2.0 * L.h, coarse_k(L.k, bc), bc, tuple(beta)))
     C = levels[-1]

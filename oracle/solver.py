@@ -31,7 +31,7 @@ import numpy as np
 import scipy.linalg
 
 from .coarse import apply_coarse_E
-from .krylov import fgmres
+from .krylov import fgmres, gcr
 from .multigrid import build_hierarchy, vcycle
 from .operators import apply_A
 from .transfer import coarse_shape, prolong_bilinear, prolong_high_order, restrict_fw, restrict_high_order
@@ -52,6 +52,8 @@ class SolverParams:
     tol: float = 1e-6
     maxit: int = 600
     max_levels: int = 64
+    coarsest_n: int = 0               # stop coarsening at the first level with <= coarsest_n unknowns (R7)
+    outer: str = "fgmres"             # fgmres | gcr (§6.3)
 
 
 class Solver:
@@ -60,7 +62,8 @@ class Solver:
         self.h = float(h)
         self.bc = bc
         self.p = params or SolverParams()
-        self.levels = build_hierarchy(self.k, self.h, bc, self.p.beta, self.p.max_levels)
+        self.levels = build_hierarchy(self.k, self.h, bc, self.p.beta, self.p.max_levels,
+                                      coarsest_n=self.p.coarsest_n)
         if len(self.levels) < 2:
             raise ValueError("deflation needs a coarsenable fine grid")
         self.cshape = coarse_shape(self.k.shape, bc)
@@ -124,8 +127,12 @@ class Solver:
     def solve(self, b, history=None):
         self.inner_its = []
         t0 = time.perf_counter()
-        x, its, conv = fgmres(self.A, self.adef1, np.asarray(b, dtype=np.complex128),
-                              self.p.tol, self.p.maxit, history=history, orth=self.p.orth)
+        if self.p.outer == "gcr":
+            x, its, conv = gcr(self.A, self.adef1, np.asarray(b, dtype=np.complex128), self.p.tol, self.p.maxit,
+                               history=history)
+        else:
+            x, its, conv = fgmres(self.A, self.adef1, np.asarray(b, dtype=np.complex128),
+                                  self.p.tol, self.p.maxit, history=history, orth=self.p.orth)
         t1 = time.perf_counter()
         r = np.asarray(b) - self.A(x)
         relres = np.linalg.norm(r) / np.linalg.norm(b) if np.linalg.norm(b) > 0 else 0.0

@@ -80,6 +80,8 @@ struct Fgm {
   double2* rawc = nullptr;   // m+2: raw Hessenberg column awaiting its delayed correction
   double2* nrm = nullptr;    // 2
   unsigned* cnt = nullptr;   // 2 last-block tickets (reduce/step A, update/step B)
+  int coop = 0;              // > 0: grid of the cooperative one-kernel DCGS2 step
+  double2* npart = nullptr;  // pass-2 norm partials of the cooperative step
   double2* part = nullptr;   // max((m+2) * gx, gu) partials
   GsGeom geo{};              // Gram-Schmidt launch geometry
   FgmState* st = nullptr;
@@ -98,12 +100,14 @@ struct helm_ctx_s {
   std::vector<Level> L;
   LevelDesc* dlev = nullptr;      // device copy of the level descriptors (tail kernel)
   int tail_lt = -1;               // first level run by the single-CTA tail (-1: none)
-  std::vector<size_t> tail_smem;  // dynamic shared memory of the tail started at each level
+  std::vector<size_t> tail_smem;  // dynamic shared memory (per CTA) of the tail started at each level
+  int tail_cs = 1;                // CTAs in the tail's thread-block cluster
   double2* Minv = nullptr;
   int ncoarsest = 0;
   double2 *dq = nullptr, *dt = nullptr;   // fine scratch for A-DEF1
   double2 *cc = nullptr, *ce = nullptr;   // coarse rhs / solution
   double2 *bbuf = nullptr, *xbuf = nullptr;  // solve input/output (graph-stable addresses)
+  double2* rbuf = nullptr;        // GCR residual
   Fgm outer, inner;
   FgmState* hst = nullptr;        // pinned host mirror of a state
   uint4* flush = nullptr;
@@ -145,6 +149,44 @@ void launch_k(helm_ctx_s& C, void (*kern)(KArgs...), dim3 grid, dim3 block, size
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = C.p.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess && C.launch_err == cudaSuccess) C.launch_err = e;
+}
+
+// Launch one thread-block cluster of `cs` CTAs (the whole grid), PDL attribute as launch_k.
+template <typename... KArgs, typename... Args>
+void launch_cluster(helm_ctx_s& C, void (*kern)(KArgs...), int cs, int threads, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = C.s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = C.p.pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess && C.launch_err == cudaSuccess) C.launch_err = e;
+}
+
+// Cooperative launch (all CTAs co-resident; grid-wide barriers inside the kernel).
+template <typename... KArgs, typename... Args>
+void launch_coop(helm_ctx_s& C, void (*kern)(KArgs...), int grid, int threads, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = C.s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
@@ -233,11 +275,11 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       const Level& F = C.L[0];
       const dim3 gt((G.g.nx + GLK_TX - 1) / GLK_TX, (G.g.ny + GLK_TY - 1) / GLK_TY);
       if (C.p.vectors == HELM_VECTORS_BILINEAR) {
-        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
-        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
+        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
       } else {
-        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
-        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, 256, 0, F.g, G.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
+        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
       }
       return post_launch(C);
     }
@@ -278,7 +320,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   Level& L = C.L[l];
   const double sr = C.p.beta1, si = C.p.beta2, w = C.p.omega;
   if (C.tail_lt >= 0 && l >= C.tail_lt) {
-    launch_k(C, k_vc_tail, 1, 1024, C.tail_smem[l], C.dlev, l, last, f, u_out, addq, sr, si, w, C.p.nu_pre, C.p.nu_post,
+    launch_cluster(C, k_vc_tail, C.tail_cs, 1024, C.tail_smem[l], C.dlev, l, last, f, u_out, addq, sr, si, w, C.p.nu_pre, C.p.nu_post,
                                                  C.Minv);
     return post_launch(C);
   }
@@ -289,12 +331,24 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   }
   Level& G = C.L[l + 1];
   if (fused_vcycle(C)) {
-    dim3 gd((G.g.nx + DOWN_TX - 1) / DOWN_TX, (G.g.ny + DOWN_TY - 1) / DOWN_TY);
-    launch_k(C, k_vc_down<DOWN_TX, DOWN_TY>, gd, 256, 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+    // small levels: smaller tiles so that more SMs share the (latency-bound) work
+    const bool small = (size_t)((G.g.nx + DOWN_TX - 1) / DOWN_TX) * ((G.g.ny + DOWN_TY - 1) / DOWN_TY) < (size_t)2 * C.sm_count;
+    if (small) {
+      dim3 gd((G.g.nx + 7) / 8, (G.g.ny + 3) / 4);
+      launch_k(C, k_vc_down<8, 4>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+    } else {
+      dim3 gd((G.g.nx + DOWN_TX - 1) / DOWN_TX, (G.g.ny + DOWN_TY - 1) / DOWN_TY);
+      launch_k(C, k_vc_down<DOWN_TX, DOWN_TY>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+    }
     CKR(post_launch(C));
     CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
-    dim3 gu((L.g.nx + UP_TX - 1) / UP_TX, (L.g.ny + UP_TY - 1) / UP_TY);
-    launch_k(C, k_vc_up<UP_TX, UP_TY>, gu, 256, 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+    if (small) {
+      dim3 gu((L.g.nx + 15) / 16, (L.g.ny + 7) / 8);
+      launch_k(C, k_vc_up<16, 8>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+    } else {
+      dim3 gu((L.g.nx + UP_TX - 1) / UP_TX, (L.g.ny + UP_TY - 1) / UP_TY);
+      launch_k(C, k_vc_up<UP_TX, UP_TY>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+    }
     return post_launch(C);
   }
   // generic sweep counts
@@ -367,6 +421,17 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   CKR(raise_dyn_smem((const void*)k_dcgs_update, usmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
+  // cooperative one-kernel step for small vectors (latency-bound regime)
+  K.coop = 0;
+  if (C.p.coop && n <= ((size_t)1 << 22)) {
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_step, DC_THREADS, asmem));
+    if (bps > 0) {
+      K.coop = bps * C.sm_count;
+      CKR(dalloc(&K.npart, (size_t)K.coop));
+    }
+  }
   CKR(dalloc(&K.cnt, 2));
   CK(cudaMemsetAsync(K.cnt, 0, 2 * sizeof(unsigned), C.s));
   return HELM_OK;
@@ -391,6 +456,7 @@ void fgm_free(Fgm& K) {
   cudaFree(K.nrm);
   cudaFree(K.part);
   cudaFree(K.cnt);
+  cudaFree(K.npart);
   cudaFree(K.st);
   K = Fgm();
 }
@@ -502,17 +568,23 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
     CKR(opA(zj, DVec(), w));
     // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
     const GsGeom& gg = K.geo;
-    launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, &st->j, 1, vj, w, ln, gg.chunk,
-                                                                           K.part);
-    CKR(post_launch(C));
-    // reduction of the pass-1 partials + step A (last block), pass 2 + step B (last block)
     const size_t asm_ = dcgs_smem(K.m);
-    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H, K.cs,
-             K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.cnt);
-    CKR(post_launch(C));
-    launch_k(C, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
-             (const double2*)K.coef, (const double2*)K.sc2, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g,
-             (const double2*)K.dots1, K.rawc, K.cnt + 1, h, use_h);
+    if (K.coop > 0) {
+      // the whole step in one cooperative kernel (grid-wide barriers between its phases)
+      launch_coop(C, k_dcgs_step, K.coop, DC_THREADS, asm_, (const double2*)K.V, ln, st, vj, w, ln, gg.chunk, gg.gx,
+                  gg.gy, K.part, K.npart, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, h, use_h);
+    } else {
+      launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, &st->j, 1, vj, w, ln,
+               gg.chunk, K.part);
+      CKR(post_launch(C));
+      // reduction of the pass-1 partials + step A (last block), pass 2 + step B (last block)
+      launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H,
+               K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.cnt);
+      CKR(post_launch(C));
+      launch_k(C, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
+               (const double2*)K.coef, (const double2*)K.sc2, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g,
+               (const double2*)K.dots1, K.rawc, K.cnt + 1, h, use_h);
+    }
     return post_launch(C);
   };
   CKR(run_while(C, st, begin, body));
@@ -543,8 +615,47 @@ int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
   return vcycle(C, 0, DVec(C.dt), z, C.dq);                    // z = M^{-1} t + Q v
 }
 
-// Outer solve of A x = b (bbuf -> xbuf); one FGMRES cycle per call (restarts: host loop).
+// One cycle of preconditioned GCR (§6.3; oracle/krylov.py gcr): z = P r, c = A z,
+// CGS2 of c against the stored c's with the same coefficients applied to z, normalise,
+// x += beta z, r -= beta c.  C basis in K.V, Z basis in K.Z, residual in C.rbuf.
+int gcr_cycle(helm_ctx_s& C, bool first) {
+  Fgm& K = C.outer;
+  FgmState* st = K.st;
+  const size_t n = K.n;
+  const long long ln = (long long)n;
+  Level& F = C.L[0];
+  const int gp = grid1d(C, n);
+  auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    if (first) CK(cudaMemcpyAsync(C.rbuf, C.bbuf, n * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
+    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(C.rbuf), 1, K.nrm, nullptr));
+    launch_k(C, k_gcr_begin, 1, 32, 0, st, (const double2*)K.nrm, first ? 1 : 0, h, use_h);
+    return post_launch(C);
+  };
+  auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    DVec zj(K.Z, &st->j, ln), cj(K.V, &st->j, ln);
+    CKR(adef1(C, DVec(C.rbuf), zj, C.outer.st));               // z_j = P r
+    CKR(op_apply(C, F, zj, DVec(), cj, 1.0, 0.0));             // c_j = A z_j
+    for (int pass = 0; pass < 2; ++pass) {                     // CGS2, same coefficients on z_j
+      double2* al = pass == 0 ? K.dots1 : K.coef;
+      CKR(gs_dots(C, K, K.V, &st->j, 0, cj, 0, al, nullptr));
+      CKR(gs_update(C, K, K.V, &st->j, 0, al, -1.0, cj, cj, 0, nullptr));
+      CKR(gs_update(C, K, K.Z, &st->j, 0, al, -1.0, zj, zj, 0, nullptr));
+    }
+    launch_k(C, k_gcr_pair, gp, 256, 0, cj, (const double2*)C.rbuf, ln, K.part);
+    CKR(post_launch(C));
+    launch_k(C, k_gcr_scalars, 1, 32, 0, (const double2*)K.part, gp, K.sc2, st);
+    CKR(post_launch(C));
+    launch_k(C, k_gcr_finish, gp, 256, 0, cj, zj, C.xbuf, C.rbuf, (const double2*)K.sc2, ln, K.part);
+    CKR(post_launch(C));
+    launch_k(C, k_gcr_check, 1, 32, 0, st, (const double2*)K.part, gp, h, use_h);
+    return post_launch(C);
+  };
+  return run_while(C, st, begin, body);
+}
+
+// Outer solve of A x = b (bbuf -> xbuf); one FGMRES (or GCR) cycle per call (restarts: host loop).
 int outer_cycle(helm_ctx_s& C, bool first) {
+  if (C.p.outer == HELM_OUTER_GCR) return gcr_cycle(C, first);
   Level& F = C.L[0];
   auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, F, x, f, y, 1.0, 0.0); };
   auto opP = [&](DVec v, DVec z) { return adef1(C, v, z, C.outer.st); };
@@ -588,7 +699,10 @@ void helm_default_params(helm_params* p) {
   p->max_coarsest = 4096;
   p->vectors = HELM_VECTORS_BILINEAR;
   p->graph = 1;
-  p->tail_max_n = 8192;
+  p->tail_max_n = 0;
+  p->coarsest_n = 0;
+  p->coop = 0;
+  p->outer = HELM_OUTER_FGMRES;
   p->pdl = 1;
 }
 
@@ -615,6 +729,7 @@ static void destroy_ctx(helm_ctx_s* C) {
   cudaFree(C->ce);
   cudaFree(C->bbuf);
   cudaFree(C->xbuf);
+  cudaFree(C->rbuf);
   cudaFree(C->flush);
   if (C->hst) cudaFreeHost(C->hst);
   fgm_free(C->outer);
@@ -638,6 +753,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.max_levels < 2) return fail(HELM_EINVAL, "max_levels must be >= 2");
   if (p.nu_pre < 1 || p.nu_post < 0) return fail(HELM_EINVAL, "nu_pre >= 1, nu_post >= 0");
   if (p.inner_maxit < 1) return fail(HELM_EINVAL, "inner_maxit >= 1");
+  if (p.outer != HELM_OUTER_FGMRES && p.outer != HELM_OUTER_GCR) return fail(HELM_EINVAL, "bad outer %d", p.outer);
   if (p.coarse_op < HELM_COARSE_GALERKIN || p.coarse_op > HELM_COARSE_RED_CMPO4)
     return fail(HELM_EINVAL, "bad coarse_op %d", p.coarse_op);
   if (p.vectors == HELM_VECTORS_BILINEAR) {
@@ -661,6 +777,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   C.L.push_back(L0);
   while ((int)C.L.size() < p.max_levels) {
     const Level& F = C.L.back();
+    if (p.coarsest_n > 0 && (long long)F.n <= p.coarsest_n) break;   // predefined coarsest size (R7)
     int cx = coarse_n(F.g.nx, F.g.bc), cy = coarse_n(F.g.ny, F.g.bc);
     if (cx < 0 || cy < 0) break;
     Level G;
@@ -701,21 +818,44 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     CKR(dalloc(&C.dlev, ds.size()));
     CK(cudaMemcpyAsync(C.dlev, ds.data(), ds.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, C.s));
     CK(cudaStreamSynchronize(C.s));
-    // tail: the first level (>= 1) from which every remaining level fits in one CTA's shared
-    // memory (and has at most tail_max_n unknowns); the coarsest solve must be small
+    // tail: one thread-block cluster (16 CTAs, non-portable size, if the device schedules it;
+    // else 8, else 1) runs every level from tail_lt down; tail_lt is the first level (>= 1)
+    // from which all remaining levels fit in the cluster's shared memories (and have at most
+    // tail_max_n unknowns); the coarsest solve must be small.
     C.tail_lt = -1;
     const int last = (int)C.L.size() - 1;
-    if (C.L.back().n <= 1024 && p.tail_max_n > 0 && last - 0 < TAIL_MAX_LEVELS) {
+    if (C.L.back().n <= 1024 && p.tail_max_n > 0 && last < TAIL_MAX_LEVELS) {
+      CKR(raise_dyn_smem((const void*)k_vc_tail, TAIL_SMEM_MAX));
+      CK(cudaFuncSetAttribute((const void*)k_vc_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      C.tail_cs = 1;
+      for (int cs : {16, 8}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = TAIL_SMEM_MAX;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_vc_tail, &cfg) == cudaSuccess && ncl >= 1) {
+          C.tail_cs = cs;
+          break;
+        }
+        cudaGetLastError();
+      }
       for (int l = 1; l <= last; ++l)
-        if ((long long)C.L[l].n <= p.tail_max_n && tail_smem_bytes(ds.data(), l, last) <= TAIL_SMEM_MAX) {
+        if ((long long)C.L[l].n <= p.tail_max_n && tail_smem_bytes(ds.data(), l, last, C.tail_cs) <= TAIL_SMEM_MAX) {
           C.tail_lt = l;
           break;
         }
     }
     if (C.tail_lt >= 0) {
       C.tail_smem.assign(C.L.size(), 0);
-      for (int l = C.tail_lt; l <= last; ++l) C.tail_smem[l] = tail_smem_bytes(ds.data(), l, last);
-      CKR(raise_dyn_smem((const void*)k_vc_tail, TAIL_SMEM_MAX));
+      for (int l = C.tail_lt; l <= last; ++l) C.tail_smem[l] = tail_smem_bytes(ds.data(), l, last, C.tail_cs);
     }
   }
   // coarsest dense inverse (reading R8): Gauss-Jordan with partial pivoting on device
@@ -762,6 +902,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   CKR(dalloc(&C.ce, C.L[1].n));
   CKR(dalloc(&C.bbuf, C.L[0].n));
   CKR(dalloc(&C.xbuf, C.L[0].n));
+  CKR(dalloc(&C.rbuf, C.L[0].n));
   // inner FGMRES: full (unrestarted) basis of inner_maxit columns, as the oracle (reading R11)
   CKR(fgm_alloc(C, C.inner, p.inner_maxit, C.L[1].n));
   CK(cudaStreamSynchronize(C.s));
@@ -1001,6 +1142,7 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
   if (!C || reps < 1 || !us_per_region) return fail(HELM_EINVAL, "bad argument");
   helm_ctx_s& X = *C;
   if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
+  if (which == HELM_GB_DCGS && (arg < 0 || arg + reps >= X.inner.m)) return fail(HELM_EINVAL, "bad column");
   const Level& F = X.L[0];
   const Level& G = X.L[1];
   cudaStream_t saved = X.s;
@@ -1025,6 +1167,35 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
       case HELM_GB_APPLY_A:
         r = op_apply(X, F, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
         break;
+      case HELM_GB_DCGS: {
+        // one delayed-CGS2 step of the inner FGMRES at column j = arg (+ the reps before it)
+        Fgm& K = X.inner;
+        FgmState* st = K.st;
+        if (i == 0) {
+          launch_k(X, k_fgm_reset, 1, 1, 0, st, 0.0, 1 << 30, K.m);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+          launch_k(X, k_set_j, 1, 1, 0, st, arg);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+        }
+        const long long ln = (long long)K.n;
+        DVec vj(K.V, &st->j, ln, &st->inv_hn), w(K.V + K.n, &st->j, ln);
+        const GsGeom& gg = K.geo;
+        launch_k(X, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, (const int*)&st->j, 1,
+                 vj, w, ln, gg.chunk, K.part);
+        r = post_launch(X);
+        if (r != HELM_OK) break;
+        launch_k(X, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, dcgs_smem(K.m), K.part, (long long)gg.gx,
+                 st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.cnt);
+        r = post_launch(X);
+        if (r != HELM_OK) break;
+        launch_k(X, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
+                 (const double2*)K.coef, (const double2*)K.sc2, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g,
+                 (const double2*)K.dots1, K.rawc, K.cnt + 1, cudaGraphConditionalHandle(0), 0);
+        r = post_launch(X);
+        break;
+      }
       default:
         r = fail(HELM_EINVAL, "unknown region %d", which);
     }
@@ -1094,7 +1265,7 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         const Level& Gl = X.L[lv + 1];
         bytes = (double)Fl.n * 40.0 + (double)Gl.n * 16.0;
         dim3 gd((Gl.g.nx + DOWN_TX - 1) / DOWN_TX, (Gl.g.ny + DOWN_TY - 1) / DOWN_TY);
-        k_vc_down<DOWN_TX, DOWN_TY><<<gd, 256, 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
+        k_vc_down<DOWN_TX, DOWN_TY><<<gd, dim3(32, 8), 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
                                                            X.p.omega, Fl.s, Gl.f);
         return post_launch(X);
       }
@@ -1103,7 +1274,7 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         const Level& Gl = X.L[lv + 1];
         bytes = (double)Fl.n * 56.0 + (double)Gl.n * 16.0;
         dim3 gu((Fl.g.nx + UP_TX - 1) / UP_TX, (Fl.g.ny + UP_TY - 1) / UP_TY);
-        k_vc_up<UP_TX, UP_TY><<<gu, 256, 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1,
+        k_vc_up<UP_TX, UP_TY><<<gu, dim3(32, 8), 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1,
                                                      X.p.beta2, X.p.omega, nullptr, DVec(lv == 0 ? X.bbuf : Fl.u));
         return post_launch(X);
       }

@@ -121,8 +121,21 @@ __global__ void __launch_bounds__(256) k_apply_op(Geo g, DVec uv, DVec fv, DVec 
   double2* __restrict__ y = yv.get();
   const int j = (int)(p / (unsigned)g.nx);
   const int i = (int)(p - (unsigned)j * (unsigned)g.nx);
-  Coef c = coef_at(g, i, j, k[p], sr, si);
-  double2 v = stencil_apply(g, u, i, j, c);
+  const double kk = k[p];
+  double2 v;
+  if (i > 0 && i < g.nx - 1 && j > 0 && j < g.ny - 1) {
+    // interior: constant off-diagonal multipliers, no boundary branches (same operation order)
+    const double ih2 = 1.0 / (g.h * g.h);
+    const double k2 = kk * kk;
+    v = cmul(make_double2(4.0 * ih2 - sr * k2, -si * k2), u[p]);
+    v = cadd(v, cscale(-ih2, u[p - 1]));
+    v = cadd(v, cscale(-ih2, u[p + 1]));
+    v = cadd(v, cscale(-ih2, u[p - g.nx]));
+    v = cadd(v, cscale(-ih2, u[p + g.nx]));
+  } else {
+    const Coef c = coef_at(g, i, j, kk, sr, si);
+    v = stencil_apply(g, u, i, j, c);
+  }
   if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;
 }
@@ -310,98 +323,120 @@ __device__ __forceinline__ double2 interp1(int r, At&& at) {
   return s;
 }
 
+// 1D interpolation weights at relative fine position r (coarse taps floor(r/2) - 1, +0, +1):
+// even r: (1/8, 3/4, 1/8) higher order, (0, 1, 0) bilinear; odd r: (0, 1/2, 1/2) both.
+template <int R>
+__device__ __forceinline__ void interp_w(int r, double& wm, double& w0, double& wp) {
+  const bool odd = (r & 1) != 0;
+  wm = odd ? 0.0 : (R == 2 ? 0.125 : 0.0);
+  w0 = odd ? 0.5 : (R == 2 ? 0.75 : 1.0);
+  wp = odd ? 0.5 : (R == 2 ? 0.125 : 0.0);
+}
+
+// Block = 32 x 8 threads; every phase walks its region row by row (threadIdx.y) and column by
+// column (threadIdx.x), so no division/modulo in the index math.
 template <int R, int MODE, int TCX, int TCY>
 __global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
                                                         DVec fv, DVec yv) {
   HELM_PDL_ENTRY();
   constexpr int SX = 2 * TCX - 1 + 2 * R, SY = 2 * TCY - 1 + 2 * R;   // s = A t region (fine)
   constexpr int TXR = SX + 2, TYR = SY + 2;                          // t = Z x region (A halo)
-  constexpr int CXW = TCX + 2 * R, CYW = TCY + 2 * R;                 // coarse x region
-  // tx (x-interpolated coarse rows) is dead once t is formed: s = A t reuses its storage
+  constexpr int CXW = TCX + 2 * R + 2, CYW = TCY + 2 * R + 2;         // coarse x region (+1 pad each side)
   constexpr int TXN = CYW * TXR, SSN = SY * SX;
-  __shared__ double2 sx[CYW * CXW];              // x on the coarse region
-  __shared__ double2 txss[TXN > SSN ? TXN : SSN]; // tx, then s
-  __shared__ double2 stt[TYR * TXR];             // t = Z x
-  __shared__ double2 ry[TCY * SX];               // s restricted along y (coarse rows, fine columns)
+  __shared__ double2 sx[CYW * CXW];
+  __shared__ double2 txss[TXN > SSN ? TXN : SSN];   // tx (x-interpolated coarse rows), later s = A t
+  __shared__ double2 stt[TYR * TXR];               // t = Z x
+  __shared__ double2 ry[TCY * SX];                 // s restricted along y
   double2* const tx = txss;
   double2* const ss = txss;
+  const int tx_ = threadIdx.x, ty_ = threadIdx.y;
   const double2* __restrict__ x = xv.get();
   const int I0 = blockIdx.x * TCX, J0 = blockIdx.y * TCY;
   const int fx0s = 2 * I0 + o - R, fy0s = 2 * J0 + o - R;
   const int fx0t = fx0s - 1, fy0t = fy0s - 1;
-  const int cx0 = I0 - R, cy0 = J0 - R;
-  for (int t = threadIdx.x; t < CXW * CYW; t += blockDim.x) {
-    const int I = cx0 + t % CXW, J = cy0 + t / CXW;
-    sx[t] = (I >= 0 && I < gc.nx && J >= 0 && J < gc.ny) ? x[(size_t)J * gc.nx + I] : make_double2(0.0, 0.0);
+  const int cx0 = I0 - R - 1, cy0 = J0 - R - 1;   // coarse index of sx column / row 0
+  const double2 zero = make_double2(0.0, 0.0);
+  for (int r = ty_; r < CYW; r += 8) {
+    const int J = cy0 + r;
+    const bool jin = (J >= 0 && J < gc.ny);
+    for (int c = tx_; c < CXW; c += 32) {
+      const int I = cx0 + c;
+      sx[r * CXW + c] = (jin && I >= 0 && I < gc.nx) ? x[(size_t)J * gc.nx + I] : zero;
+    }
   }
   __syncthreads();
-  // Z is the tensor product of the 1D interpolations (Eq. 3.9 / 3.12): along x ...
-  for (int t = threadIdx.x; t < CYW * TXR; t += blockDim.x) {
-    const int row = t / TXR, fx = fx0t + t % TXR;
-    double2 v = make_double2(0.0, 0.0);
-    if (fx >= 0 && fx < gf.nx) {
-      const double2* line = sx + row * CXW;
-      v = interp1<R>(fx - o, [&](int I) {
-        const int li = I - cx0;
-        return (li >= 0 && li < CXW) ? line[li] : make_double2(0.0, 0.0);
-      });
+  // Z = tensor product of the 1D interpolations (Eq. 3.9 / 3.12): along x ...
+  for (int c = tx_; c < TXR; c += 32) {
+    const int fx = fx0t + c;
+    const int rr = fx - o;
+    const int li = floordiv2i(rr) - cx0;
+    double wm, w0, wp;
+    interp_w<R>(rr, wm, w0, wp);
+    if (fx < 0 || fx >= gf.nx) wm = w0 = wp = 0.0;
+    for (int r = ty_; r < CYW; r += 8) {
+      const double2* line = sx + r * CXW + li;
+      tx[r * TXR + c] = cadd(cadd(cscale(wm, line[-1]), cscale(w0, line[0])), cscale(wp, line[1]));
     }
-    tx[t] = v;
   }
   __syncthreads();
   // ... then along y
-  for (int t = threadIdx.x; t < TYR * TXR; t += blockDim.x) {
-    const int col = t % TXR, fy = fy0t + t / TXR;
-    const int fx = fx0t + col;
-    double2 v = make_double2(0.0, 0.0);
-    if (fy >= 0 && fy < gf.ny && fx >= 0 && fx < gf.nx) {
-      v = interp1<R>(fy - o, [&](int J) {
-        const int lj = J - cy0;
-        return (lj >= 0 && lj < CYW) ? tx[lj * TXR + col] : make_double2(0.0, 0.0);
-      });
-    }
-    stt[t] = v;
+  for (int r = ty_; r < TYR; r += 8) {
+    const int fy = fy0t + r;
+    const int rr = fy - o;
+    const int lj = floordiv2i(rr) - cy0;
+    double wm, w0, wp;
+    interp_w<R>(rr, wm, w0, wp);
+    if (fy < 0 || fy >= gf.ny) wm = w0 = wp = 0.0;
+    for (int c = tx_; c < TXR; c += 32)
+      stt[r * TXR + c] = cadd(cadd(cscale(wm, tx[(lj - 1) * TXR + c]), cscale(w0, tx[lj * TXR + c])),
+                              cscale(wp, tx[(lj + 1) * TXR + c]));
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < SX * SY; t += blockDim.x) {
-    const int ix = t % SX, iy = t / SX;
-    const int fx = fx0s + ix, fy = fy0s + iy;
-    double2 v = make_double2(0.0, 0.0);   // reading R4: restriction taps outside the array dropped
-    if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
-      const Coef c = coef_at(gf, fx, fy, kf[(size_t)fy * gf.nx + fx], 1.0, 0.0);
-      const int q = (iy + 1) * TXR + (ix + 1);
-      v = cmul(c.ap, stt[q]);
-      if (c.aw != 0.0) v = cadd(v, cscale(c.aw, stt[q - 1]));
-      if (c.ae != 0.0) v = cadd(v, cscale(c.ae, stt[q + 1]));
-      if (c.as != 0.0) v = cadd(v, cscale(c.as, stt[q - TXR]));
-      if (c.an != 0.0) v = cadd(v, cscale(c.an, stt[q + TXR]));
+  for (int r = ty_; r < SY; r += 8) {
+    const int fy = fy0s + r;
+    for (int c = tx_; c < SX; c += 32) {
+      const int fx = fx0s + c;
+      double2 v = zero;   // reading R4: restriction taps outside the array dropped
+      if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
+        const Coef cf = coef_at(gf, fx, fy, kf[(size_t)fy * gf.nx + fx], 1.0, 0.0);
+        const int q = (r + 1) * TXR + (c + 1);
+        v = cmul(cf.ap, stt[q]);
+        if (cf.aw != 0.0) v = cadd(v, cscale(cf.aw, stt[q - 1]));
+        if (cf.ae != 0.0) v = cadd(v, cscale(cf.ae, stt[q + 1]));
+        if (cf.as != 0.0) v = cadd(v, cscale(cf.as, stt[q - TXR]));
+        if (cf.an != 0.0) v = cadd(v, cscale(cf.an, stt[q + TXR]));
+      }
+      ss[r * SX + c] = v;
     }
-    ss[t] = v;
   }
   __syncthreads();
   // Z^T = tensor product of the transposed 1D interpolations: along y ...
-  for (int t = threadIdx.x; t < TCY * SX; t += blockDim.x) {
-    const int jl = t / SX, ix = t % SX;
+  for (int jl = ty_; jl < TCY; jl += 8) {
     const int iy = 2 * jl + R;
-    double2 v = make_double2(0.0, 0.0);
+    for (int c = tx_; c < SX; c += 32) {
+      double2 v = zero;
 #pragma unroll
-    for (int b = -R; b <= R; ++b) v = cadd(v, cscale(zw<R>(b), ss[(iy + b) * SX + ix]));
-    ry[t] = v;
+      for (int b = -R; b <= R; ++b) v = cadd(v, cscale(zw<R>(b), ss[(iy + b) * SX + c]));
+      ry[jl * SX + c] = v;
+    }
   }
   __syncthreads();
   // ... then along x
   const double2* __restrict__ f = fv.get();
   double2* __restrict__ y = yv.get();
-  for (int t = threadIdx.x; t < TCX * TCY; t += blockDim.x) {
-    const int I = I0 + t % TCX, J = J0 + t / TCX;
-    if (I >= gc.nx || J >= gc.ny) continue;
-    const int ix = 2 * (I - I0) + R, jl = J - J0;
-    double2 s = make_double2(0.0, 0.0);
+  for (int jl = ty_; jl < TCY; jl += 8) {
+    const int J = J0 + jl;
+    for (int il = tx_; il < TCX; il += 32) {
+      const int I = I0 + il;
+      if (I >= gc.nx || J >= gc.ny) continue;
+      const int ix = 2 * il + R;
+      double2 s = zero;
 #pragma unroll
-    for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
-    s = cscale(zrs<R>(), s);
-    const size_t p = (size_t)J * gc.nx + I;
-    y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
+      for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
+      s = cscale(zrs<R>(), s);
+      const size_t p = (size_t)J * gc.nx + I;
+      y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
+    }
   }
 }
 

@@ -17,7 +17,11 @@
 #pragma once
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace helm {
 
@@ -227,25 +231,22 @@ constexpr int DC_SUB = 256;               // elements per sub-chunk (8 per lane,
 // and streams two basis vectors at a time (16 independent 16-byte loads per lane in flight).
 // chunk is a multiple of DC_SUB; with more than one sub-chunk per block the per-vector sums
 // go through shared memory (each vector is owned by one warp: no races).
-__global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restrict__ V, long long ld,
-                                                          const int* __restrict__ nptr, int nadd, DVec xv, DVec wv,
-                                                          long long n, long long chunk, double2* __restrict__ part) {
-  HELM_PDL_ENTRY();
-  extern __shared__ double2 dacc[];
-  const int nvec = (nptr ? *nptr : 0) + nadd;
-  const double2* __restrict__ x = xv.get();
-  const double xs = xv.scale();
-  const double2* __restrict__ w = wv.get();
-  const long long e0 = (long long)blockIdx.x * chunk;
+// One work item = (chunk bx, vector slice y of gy), executed by a whole 128-thread block.
+__device__ __forceinline__ void dcgs_dots_item(const double2* __restrict__ V, long long ld, int nvec,
+                                               const double2* __restrict__ x, double xs,
+                                               const double2* __restrict__ w, long long n, long long chunk,
+                                               double2* __restrict__ part, int gx, int bx, int y, int gy,
+                                               double2* dacc) {
+  const long long e0 = (long long)bx * chunk;
   const long long e1 = min(n, e0 + chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gx = gridDim.x;
-  const int cstep = gridDim.y * DC_WARPS;
-  const int c0 = blockIdx.y * DC_WARPS + warp;
+  const int cstep = gy * DC_WARPS;
+  const int c0 = y * DC_WARPS + warp;
   const bool multi = (e1 - e0) > DC_SUB;
-  if (multi)
+  if (multi) {
     for (int c = threadIdx.x; c < 2 * nvec; c += DC_THREADS) dacc[c] = make_double2(0.0, 0.0);
-  if (multi) __syncthreads();
+    __syncthreads();
+  }
   for (long long sub = e0; sub < e1; sub += DC_SUB) {
     double2 xr[8], wr[8];
 #pragma unroll
@@ -266,28 +267,28 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restr
         a[t] = ok ? va[32 * t] : make_double2(0.0, 0.0);
         b[t] = (ok && two) ? vb[32 * t] : make_double2(0.0, 0.0);
       }
-      double2 ax = make_double2(0.0, 0.0), aw = ax, bx = ax, bw = ax;
+      double2 ax = make_double2(0.0, 0.0), aw = ax, bxx = ax, bw = ax;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         ax.x = fma(a[t].x, xr[t].x, fma(a[t].y, xr[t].y, ax.x));
         ax.y = fma(a[t].x, xr[t].y, fma(-a[t].y, xr[t].x, ax.y));
         aw.x = fma(a[t].x, wr[t].x, fma(a[t].y, wr[t].y, aw.x));
         aw.y = fma(a[t].x, wr[t].y, fma(-a[t].y, wr[t].x, aw.y));
-        bx.x = fma(b[t].x, xr[t].x, fma(b[t].y, xr[t].y, bx.x));
-        bx.y = fma(b[t].x, xr[t].y, fma(-b[t].y, xr[t].x, bx.y));
+        bxx.x = fma(b[t].x, xr[t].x, fma(b[t].y, xr[t].y, bxx.x));
+        bxx.y = fma(b[t].x, xr[t].y, fma(-b[t].y, xr[t].x, bxx.y));
         bw.x = fma(b[t].x, wr[t].x, fma(b[t].y, wr[t].y, bw.x));
         bw.y = fma(b[t].x, wr[t].y, fma(-b[t].y, wr[t].x, bw.y));
       }
       ax = warp_sum2(ax);
       aw = warp_sum2(aw);
-      bx = warp_sum2(bx);
+      bxx = warp_sum2(bxx);
       bw = warp_sum2(bw);
       if (c == nvec - 1) {        // V_j is v~_j itself: read through the same scale as x
         ax = cscale(xs, ax);
         aw = cscale(xs, aw);
       }
       if (two && c2 == nvec - 1) {
-        bx = cscale(xs, bx);
+        bxx = cscale(xs, bxx);
         bw = cscale(xs, bw);
       }
       if (lane == 0) {
@@ -295,15 +296,15 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restr
           dacc[2 * c] = cadd(dacc[2 * c], ax);
           dacc[2 * c + 1] = cadd(dacc[2 * c + 1], aw);
           if (two) {
-            dacc[2 * c2] = cadd(dacc[2 * c2], bx);
+            dacc[2 * c2] = cadd(dacc[2 * c2], bxx);
             dacc[2 * c2 + 1] = cadd(dacc[2 * c2 + 1], bw);
           }
         } else {
-          part[(long long)(2 * c) * gx + blockIdx.x] = ax;
-          part[(long long)(2 * c + 1) * gx + blockIdx.x] = aw;
+          part[(long long)(2 * c) * gx + bx] = ax;
+          part[(long long)(2 * c + 1) * gx + bx] = aw;
           if (two) {
-            part[(long long)(2 * c2) * gx + blockIdx.x] = bx;
-            part[(long long)(2 * c2 + 1) * gx + blockIdx.x] = bw;
+            part[(long long)(2 * c2) * gx + bx] = bxx;
+            part[(long long)(2 * c2 + 1) * gx + bx] = bw;
           }
         }
       }
@@ -311,8 +312,19 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restr
   }
   if (multi) {
     __syncthreads();
-    for (int c = threadIdx.x; c < 2 * nvec; c += DC_THREADS) part[(long long)c * gx + blockIdx.x] = dacc[c];
+    for (int c = threadIdx.x; c < 2 * nvec; c += DC_THREADS) part[(long long)c * gx + bx] = dacc[c];
+    __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restrict__ V, long long ld,
+                                                          const int* __restrict__ nptr, int nadd, DVec xv, DVec wv,
+                                                          long long n, long long chunk, double2* __restrict__ part) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 dacc[];
+  const int nvec = (nptr ? *nptr : 0) + nadd;
+  dcgs_dots_item(V, ld, nvec, xv.get(), xv.scale(), wv.get(), n, chunk, part, gridDim.x, blockIdx.x, blockIdx.y,
+                 gridDim.y, dacc);
 }
 
 // Pass 2 of iteration j (j = *jptr): with coef[2c] = -a_c/beta, coef[2c+1] = -b_c (c < j)
@@ -327,6 +339,93 @@ constexpr int DU_THREADS = 128;
 constexpr int DU_WARPS = DU_THREADS / 32;
 constexpr int DU_ELEMS = 256;
 
+struct DuRed {
+  double2 v[DU_WARPS][2][DU_ELEMS];
+};
+
+// one 256-element tile; sab = coefficients in shared memory; returns this thread's |w'|^2 share
+__device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V, long long ld, int j,
+                                                   const double2* sab, double ib, double2 hjj, double2* x, double2* w,
+                                                   long long n, long long tile, DuRed& red) {
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const long long eb = tile * DU_ELEMS + lane;
+  double2 sa[8], sb[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) sa[q] = sb[q] = make_double2(0.0, 0.0);
+  int c = wq;
+  for (; c + DU_WARPS < j; c += 2 * DU_WARPS) {
+    const double2 ca0 = sab[2 * c], cb0 = sab[2 * c + 1];
+    const double2 ca1 = sab[2 * (c + DU_WARPS)], cb1 = sab[2 * (c + DU_WARPS) + 1];
+    const double2* v0p = V + (long long)c * ld + eb;
+    const double2* v1p = V + (long long)(c + DU_WARPS) * ld + eb;
+    double2 v0[8], v1[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const bool ok = eb + 32 * q < n;
+      v0[q] = ok ? v0p[32 * q] : make_double2(0.0, 0.0);
+      v1[q] = ok ? v1p[32 * q] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      sa[q] = cfma(ca0, v0[q], sa[q]);
+      sb[q] = cfma(cb0, v0[q], sb[q]);
+      sa[q] = cfma(ca1, v1[q], sa[q]);
+      sb[q] = cfma(cb1, v1[q], sb[q]);
+    }
+  }
+  if (c < j) {
+    const double2 ca0 = sab[2 * c], cb0 = sab[2 * c + 1];
+    const double2* v0p = V + (long long)c * ld + eb;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 v0 = (eb + 32 * q < n) ? v0p[32 * q] : make_double2(0.0, 0.0);
+      sa[q] = cfma(ca0, v0, sa[q]);
+      sb[q] = cfma(cb0, v0, sb[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    red.v[wq][0][lane + 32 * q] = sa[q];
+    red.v[wq][1][lane + 32 * q] = sb[q];
+  }
+  __syncthreads();
+  double nrm = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < DU_ELEMS / DU_THREADS; ++rr) {
+    const int el = threadIdx.x + DU_THREADS * rr;
+    const long long e = tile * DU_ELEMS + el;
+    if (e < n) {
+      double2 ta = make_double2(0.0, 0.0), tb = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < DU_WARPS; ++q) {
+        ta = cadd(ta, red.v[q][0][el]);
+        tb = cadd(tb, red.v[q][1][el]);
+      }
+      const double2 v = cadd(cscale(ib, x[e]), ta);
+      const double2 wp = csub(cadd(w[e], tb), cmul(hjj, v));
+      x[e] = v;
+      w[e] = wp;
+      nrm = fma(wp.x, wp.x, fma(wp.y, wp.y, nrm));
+    }
+  }
+  __syncthreads();
+  return nrm;
+}
+
+// block sum of a per-thread double (any blockDim <= 1024, multiple of 32), result in thread 0
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double bs[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) bs[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += bs[q];
+  __syncthreads();
+  return t;
+}
+
 __global__ void __launch_bounds__(DU_THREADS) k_dcgs_update(const double2* __restrict__ V, long long ld,
                                                             const int* __restrict__ jptr,
                                                             const double2* __restrict__ coef,
@@ -338,92 +437,85 @@ __global__ void __launch_bounds__(DU_THREADS) k_dcgs_update(const double2* __res
                                                             cudaGraphConditionalHandle hcond, int use_h) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 sab[];
-  __shared__ double2 red[DU_WARPS][2][DU_ELEMS];
-  __shared__ double nred[DU_WARPS];
+  __shared__ DuRed red;
   const int j = *jptr;
-  double2* x = xv.get();
-  double2* w = wv.get();
   for (int c = threadIdx.x; c < 2 * j; c += DU_THREADS) sab[c] = coef[c];
   __syncthreads();
   const double ib = sc2[0].x * xv.scale();
   const double2 hjj = sc2[1];
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  double2* x = xv.get();
+  double2* w = wv.get();
   double nrm = 0.0;
   const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
-  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const long long eb = tile * DU_ELEMS + lane;
-    double2 sa[8], sb[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) sa[q] = sb[q] = make_double2(0.0, 0.0);
-    int c = wq;
-    for (; c + DU_WARPS < j; c += 2 * DU_WARPS) {
-      const double2 ca0 = sab[2 * c], cb0 = sab[2 * c + 1];
-      const double2 ca1 = sab[2 * (c + DU_WARPS)], cb1 = sab[2 * (c + DU_WARPS) + 1];
-      const double2* v0p = V + (long long)c * ld + eb;
-      const double2* v1p = V + (long long)(c + DU_WARPS) * ld + eb;
-      double2 v0[8], v1[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const bool ok = eb + 32 * q < n;
-        v0[q] = ok ? v0p[32 * q] : make_double2(0.0, 0.0);
-        v1[q] = ok ? v1p[32 * q] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        sa[q] = cfma(ca0, v0[q], sa[q]);
-        sb[q] = cfma(cb0, v0[q], sb[q]);
-        sa[q] = cfma(ca1, v1[q], sa[q]);
-        sb[q] = cfma(cb1, v1[q], sb[q]);
-      }
-    }
-    if (c < j) {
-      const double2 ca0 = sab[2 * c], cb0 = sab[2 * c + 1];
-      const double2* v0p = V + (long long)c * ld + eb;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double2 v0 = (eb + 32 * q < n) ? v0p[32 * q] : make_double2(0.0, 0.0);
-        sa[q] = cfma(ca0, v0, sa[q]);
-        sb[q] = cfma(cb0, v0, sb[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      red[wq][0][lane + 32 * q] = sa[q];
-      red[wq][1][lane + 32 * q] = sb[q];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < DU_ELEMS / DU_THREADS; ++r) {
-      const int el = threadIdx.x + DU_THREADS * r;
-      const long long e = tile * DU_ELEMS + el;
-      if (e < n) {
-        double2 ta = make_double2(0.0, 0.0), tb = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < DU_WARPS; ++q) {
-          ta = cadd(ta, red[q][0][el]);
-          tb = cadd(tb, red[q][1][el]);
-        }
-        const double2 v = cadd(cscale(ib, x[e]), ta);
-        const double2 wp = csub(cadd(w[e], tb), cmul(hjj, v));
-        x[e] = v;
-        w[e] = wp;
-        nrm = fma(wp.x, wp.x, fma(wp.y, wp.y, nrm));
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-  if (lane == 0) nred[wq] = nrm;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int q = 0; q < DU_WARPS; ++q) t += nred[q];
-    part[blockIdx.x] = make_double2(t, 0.0);
-  }
+  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x)
+    nrm += dcgs_update_tile(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
+  const double t = block_sum(nrm);
+  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
   // step B in the last block to finish (sab is free again: it doubles as step B's scratch)
   if (st && last_block(counter) && threadIdx.x < 32)
     dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, part, gridDim.x, rawc, hcond, use_h, sab);
+}
+
+// The whole delayed-CGS2 step of one iteration as ONE cooperative kernel (small grids, where
+// the three-kernel form is launch-latency bound): pass 1 over all (chunk, slice) items, grid
+// barrier, the 2(j+1) reductions, barrier, step A (block 0), barrier, pass 2 over all tiles,
+// barrier, step B (block 0).  Same arithmetic and summation order as the three kernels.
+__global__ void __launch_bounds__(DC_THREADS) k_dcgs_step(const double2* __restrict__ V, long long ld, FgmState* st,
+                                                          DVec xv, DVec wv, long long n, long long chunk, int gx,
+                                                          int gy, double2* __restrict__ part,
+                                                          double2* __restrict__ npart, double2* H, double* cs,
+                                                          double2* sn, double2* g, double2* __restrict__ dots,
+                                                          double2* __restrict__ coef, double2* __restrict__ sc2,
+                                                          double2* __restrict__ rawc,
+                                                          cudaGraphConditionalHandle hcond, int use_h) {
+  HELM_PDL_ENTRY();
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double2 dsm[];
+  __shared__ DuRed red;
+  const int j = st->j;
+  const int nvec = j + 1;
+  // pass 1
+  {
+    const double2* x = xv.get();
+    const double xs = xv.scale();
+    const double2* w = wv.get();
+    for (int item = blockIdx.x; item < gx * gy; item += gridDim.x)
+      dcgs_dots_item(V, ld, nvec, x, xs, w, n, chunk, part, gx, item % gx, item / gx, gy, dsm);
+  }
+  grid.sync();
+  // reductions: one warp per output
+  {
+    const int ntot = 2 * nvec;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (DC_THREADS / 32);
+    for (int c = blockIdx.x * (DC_THREADS / 32) + (threadIdx.x >> 5); c < ntot; c += nw) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int b = lane; b < gx; b += 32) s = cadd(s, part[(long long)c * gx + b]);
+      s = warp_sum2(s);
+      if (lane == 0) dots[c] = s;
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 32) dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, dsm);
+  grid.sync();
+  // pass 2
+  {
+    for (int c = threadIdx.x; c < 2 * j; c += DC_THREADS) dsm[c] = coef[c];
+    __syncthreads();
+    const double ib = sc2[0].x * xv.scale();
+    const double2 hjj = sc2[1];
+    double2* x = xv.get();
+    double2* w = wv.get();
+    double nrm = 0.0;
+    const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x)
+      nrm += dcgs_update_tile(V, ld, j, dsm, ib, hjj, x, w, n, tile, red);
+    const double t = block_sum(nrm);
+    if (threadIdx.x == 0) npart[blockIdx.x] = make_double2(t, 0.0);
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 32)
+    dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, npart, gridDim.x, rawc, hcond, use_h, dsm);
 }
 
 // Pass-1 reduction (2(j+1) outputs, one warp each) with step A in the last block to finish.
@@ -679,6 +771,134 @@ __global__ void k_fgm_backsub(FgmState* st, const double2* __restrict__ H, const
     outer->inner_max = max(outer->inner_max, st->its);
     outer->inner_solves += 1;
   }
+}
+
+// ---------------------------------------------------------------- GCR outer (§6.3)
+// Partials of |c|^2 and c^H r per block (part[2b], part[2b+1]).
+__global__ void __launch_bounds__(256) k_gcr_pair(DVec cv, const double2* __restrict__ r, long long n,
+                                                  double2* __restrict__ part) {
+  HELM_PDL_ENTRY();
+  const double2* c = cv.get();
+  double2 nc = make_double2(0.0, 0.0), cr = make_double2(0.0, 0.0);
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+    const double2 ce = c[e], re = r[e];
+    nc.x = fma(ce.x, ce.x, fma(ce.y, ce.y, nc.x));
+    cr.x = fma(ce.x, re.x, fma(ce.y, re.y, cr.x));
+    cr.y = fma(ce.x, re.y, fma(-ce.y, re.x, cr.y));
+  }
+  __shared__ double2 sh[2][8];
+  nc = warp_sum2(nc);
+  cr = warp_sum2(cr);
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = nc;
+    sh[1][threadIdx.x >> 5] = cr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 a = make_double2(0.0, 0.0), b = a;
+    for (int q = 0; q < 8; ++q) {
+      a = cadd(a, sh[0][q]);
+      b = cadd(b, sh[1][q]);
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// sc[0] = 1/||c||, sc[1] = beta = c_n^H r = (c^H r)/||c||   (one warp)
+__global__ void k_gcr_scalars(const double2* __restrict__ part, int np, double2* __restrict__ sc, FgmState* st) {
+  HELM_PDL_ENTRY();
+  double2 a = make_double2(0.0, 0.0), b = a;
+  for (int q = threadIdx.x; q < np; q += 32) {
+    a = cadd(a, part[2 * q]);
+    b = cadd(b, part[2 * q + 1]);
+  }
+  a = warp_sum2(a);
+  b = warp_sum2(b);
+  if (threadIdx.x == 0) {
+    const double nc = sqrt(fmax(a.x, 0.0));
+    const double inv = nc > 0.0 ? 1.0 / nc : 0.0;
+    sc[0] = make_double2(inv, 0.0);
+    sc[1] = cscale(inv, b);
+    st->hn = nc;
+  }
+}
+
+// c_n = c/||c||, z_n = z/||c|| (stored), x += beta z_n, r -= beta c_n, partials of |r|^2.
+__global__ void __launch_bounds__(256) k_gcr_finish(DVec cv, DVec zv, double2* __restrict__ x, double2* __restrict__ r,
+                                                    const double2* __restrict__ sc, long long n,
+                                                    double2* __restrict__ part) {
+  HELM_PDL_ENTRY();
+  double2* c = cv.get();
+  double2* z = zv.get();
+  const double inv = sc[0].x;
+  const double2 beta = sc[1];
+  double nr = 0.0;
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+    const double2 cn = cscale(inv, c[e]);
+    const double2 zn = cscale(inv, z[e]);
+    c[e] = cn;
+    z[e] = zn;
+    x[e] = cfma(beta, zn, x[e]);
+    const double2 re = csub(r[e], cmul(beta, cn));
+    r[e] = re;
+    nr = fma(re.x, re.x, fma(re.y, re.y, nr));
+  }
+  const double t = block_sum(nr);
+  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
+}
+
+// ||r|| from the partials; loop decision (one warp).
+__global__ void k_gcr_check(FgmState* st, const double2* __restrict__ part, int np, cudaGraphConditionalHandle h,
+                            int use_h) {
+  HELM_PDL_ENTRY();
+  double s = 0.0;
+  for (int q = threadIdx.x; q < np; q += 32) s += part[q].x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) {
+    const int j = st->j;
+    st->its += 1;
+    st->ncols = j + 1;
+    st->relres = st->bnorm > 0.0 ? sqrt(fmax(s, 0.0)) / st->bnorm : 0.0;
+    int done = 0;
+    if (st->relres <= st->tol || st->hn == 0.0) {
+      done = 1;
+      st->conv = st->relres <= st->tol ? 1 : 0;
+    } else if (st->its >= st->maxit || j + 1 >= st->m) {
+      done = 1;
+    }
+    st->done = done;
+    st->j = j + 1;
+    fgm_set_cond(st, h, use_h, !done);
+  }
+}
+
+// GCR begin: relres from ||r||^2 (nrm2), j = 0; first cycle sets bnorm = ||r|| (x0 = 0, r = b).
+__global__ void k_gcr_begin(FgmState* st, const double2* __restrict__ nrm2, int first, cudaGraphConditionalHandle h,
+                            int use_h) {
+  HELM_PDL_ENTRY();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double rn = sqrt(fmax(nrm2[0].x, 0.0));
+  if (first) st->bnorm = rn;
+  st->j = 0;
+  st->ncols = 0;
+  st->relres = st->bnorm > 0.0 ? rn / st->bnorm : 0.0;
+  int done = 0;
+  if (st->bnorm == 0.0 || st->relres <= st->tol) {
+    done = 1;
+    st->conv = 1;
+  } else if (st->its >= st->maxit) {
+    done = 1;
+  }
+  st->done = done;
+  fgm_set_cond(st, h, use_h, !done);
+}
+
+__global__ void k_set_j(FgmState* st, int j) {
+  HELM_PDL_ENTRY();
+  st->j = j;
+  st->inv_hn = 1.0;
 }
 
 // Reset a state at the start of a solve: its = 0, conv = 0, tol/maxit from the host values.

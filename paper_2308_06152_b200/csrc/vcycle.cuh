@@ -13,7 +13,11 @@
 // Valid for nu_pre = nu_post = 1 (the paper's setting); other sweep counts use the generic
 // kernels of kernels.cuh.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace helm {
 
@@ -31,9 +35,29 @@ __device__ __forceinline__ double2 stencil5(const Coef& c, double2 uc, double2 u
   return v;
 }
 
+// Interior points (all four neighbours inside the grid, no boundary row) share the multipliers
+// aw = ae = as = an = -1/h^2; only the centre depends on k.  A CTA whose whole region is
+// interior takes a branch-free path (uniform per CTA: no divergence).
+__device__ __forceinline__ double2 interior_ap(double ih2, double kk, double sr, double si) {
+  const double k2 = kk * kk;
+  return make_double2(4.0 * ih2 - sr * k2, -si * k2);
+}
+
+__device__ __forceinline__ double2 interior_stencil(double ih2, double2 ap, double2 uc, double2 uw, double2 ue,
+                                                    double2 us, double2 un) {
+  // same operation order as stencil5 with nonzero multipliers
+  double2 v = cmul(ap, uc);
+  v = cadd(v, cscale(-ih2, uw));
+  v = cadd(v, cscale(-ih2, ue));
+  v = cadd(v, cscale(-ih2, us));
+  v = cadd(v, cscale(-ih2, un));
+  return v;
+}
+
 // ------------------------------------------------------------------ down leg
-// CTA = TCX x TCY coarse points.  Fine footprint of the restriction: fine nodes
-// 2I+o-1 .. 2I+o+1; the residual there needs u one node further out.
+// CTA = TCX x TCY coarse points, 32 x 8 threads.  Fine footprint of the restriction: fine nodes
+// 2I+o-1 .. 2I+o+1; the residual there needs u one node further out.  f (scaled) and k of the
+// region are kept in shared memory for the residual phase.
 template <int TCX, int TCY>
 __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
                                                  double sr, double si, double omega, double2* __restrict__ u,
@@ -42,7 +66,10 @@ __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, c
   constexpr int RX = 2 * TCX + 3, RY = 2 * TCY + 3;  // u region
   constexpr int QX = 2 * TCX + 1, QY = 2 * TCY + 1;  // r region
   __shared__ double2 su[RY * RX];
+  __shared__ double2 sf[RY * RX];
+  __shared__ double sk[RY * RX];
   __shared__ double2 sq[QY * QX];
+  const int tx = threadIdx.x, ty = threadIdx.y;
   const double2* __restrict__ f = fv.get();
   const double fs = fv.scale();
   const int I0 = blockIdx.x * TCX, J0 = blockIdx.y * TCY;
@@ -52,50 +79,67 @@ __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, c
   const int xe = (I0 + TCX >= G.nx) ? F.nx : 2 * (I0 + TCX) + o - 1;
   const int ys = (J0 == 0) ? 0 : 2 * J0 + o - 1;
   const int ye = (J0 + TCY >= G.ny) ? F.ny : 2 * (J0 + TCY) + o - 1;
-  for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
-    const int ix = t % RX, iy = t / RX;
-    const int x = gx0 + ix, y = gy0 + iy;
-    double2 uv = czero();
-    if (x >= 0 && x < F.nx && y >= 0 && y < F.ny) {
-      const size_t p = (size_t)y * F.nx + x;
-      const Coef c = coef_at(F, x, y, k[p], sr, si);
-      uv = cscale(omega, cdiv(cscale(fs, f[p]), c.ap));   // reading R9: first sweep from u = 0
-      if (x >= xs && x < xe && y >= ys && y < ye) u[p] = uv;
-    }
-    su[t] = uv;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < QX * QY; t += blockDim.x) {
-    const int ix = t % QX, iy = t / QX;
-    const int x = gx0 + 1 + ix, y = gy0 + 1 + iy;
-    double2 rv = czero();                      // reading R4: out-of-array taps dropped
-    if (x >= 0 && x < F.nx && y >= 0 && y < F.ny) {
-      const size_t p = (size_t)y * F.nx + x;
-      const Coef c = coef_at(F, x, y, k[p], sr, si);
-      const int q = (iy + 1) * RX + (ix + 1);
-      rv = csub(cscale(fs, f[p]), stencil5(c, su[q], su[q - 1], su[q + 1], su[q - RX], su[q + RX]));
-    }
-    sq[t] = rv;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < TCX * TCY; t += blockDim.x) {
-    const int I = I0 + t % TCX, J = J0 + t / TCX;
-    if (I >= G.nx || J >= G.ny) continue;
-    const int ix = 2 * (I - I0) + 1, iy = 2 * (J - J0) + 1;
-    double2 s = czero();
-#pragma unroll
-    for (int b = -1; b <= 1; ++b)
-#pragma unroll
-      for (int a = -1; a <= 1; ++a) {
-        const double w = (a == 0 ? 2.0 : 1.0) * (b == 0 ? 2.0 : 1.0) * (1.0 / 16.0);
-        s = cadd(s, cscale(w, sq[(iy + b) * QX + ix + a]));
+  const bool interior = gx0 >= 1 && gx0 + RX <= F.nx - 1 && gy0 >= 1 && gy0 + RY <= F.ny - 1;
+  const double ih2 = 1.0 / (F.h * F.h);
+  const int tid = ty * 32 + tx;
+  for (int t = tid; t < RX * RY; t += 256) {
+    {
+      const int iy = t / RX, ix = t - iy * RX;   // compile-time divisor
+      const int x = gx0 + ix, y = gy0 + iy;
+      double2 uv = czero(), fvv = czero();
+      double kk = 0.0;
+      if (interior || (x >= 0 && x < F.nx && y >= 0 && y < F.ny)) {
+        const size_t p = (size_t)y * F.nx + x;
+        kk = k[p];
+        fvv = cscale(fs, f[p]);
+        const double2 ap = interior ? interior_ap(ih2, kk, sr, si) : coef_at(F, x, y, kk, sr, si).ap;
+        uv = cscale(omega, cdiv(fvv, ap));   // reading R9: first sweep from u = 0
+        if (x >= xs && x < xe && y >= ys && y < ye) u[p] = uv;
       }
-    fc[(size_t)J * G.nx + I] = s;
+      su[t] = uv;
+      sf[t] = fvv;
+      sk[t] = kk;
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < QX * QY; t += 256) {
+    {
+      const int iy = t / QX, ix = t - iy * QX;
+      const int x = gx0 + 1 + ix, y = gy0 + 1 + iy;
+      const int q = (iy + 1) * RX + (ix + 1);
+      double2 rv = czero();                      // reading R4: out-of-array taps dropped
+      if (interior) {
+        rv = csub(sf[q], interior_stencil(ih2, interior_ap(ih2, sk[q], sr, si), su[q], su[q - 1], su[q + 1],
+                                          su[q - RX], su[q + RX]));
+      } else if (x >= 0 && x < F.nx && y >= 0 && y < F.ny) {
+        const Coef c = coef_at(F, x, y, sk[q], sr, si);
+        rv = csub(sf[q], stencil5(c, su[q], su[q - 1], su[q + 1], su[q - RX], su[q + RX]));
+      }
+      sq[iy * QX + ix] = rv;
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < TCX * TCY; t += 256) {
+    {
+      const int jl = t / TCX, il = t - jl * TCX;
+      const int I = I0 + il, J = J0 + jl;
+      if (I >= G.nx || J >= G.ny) continue;
+      const int ix = 2 * il + 1, iy = 2 * jl + 1;
+      double2 s = czero();
+#pragma unroll
+      for (int b = -1; b <= 1; ++b)
+#pragma unroll
+        for (int a = -1; a <= 1; ++a) {
+          const double w = (a == 0 ? 2.0 : 1.0) * (b == 0 ? 2.0 : 1.0) * (1.0 / 16.0);
+          s = cadd(s, cscale(w, sq[(iy + b) * QX + ix + a]));
+        }
+      fc[(size_t)J * G.nx + I] = s;
+    }
   }
 }
 
 // ------------------------------------------------------------------ up leg
-// CTA = TX x TY fine points; u1 is formed on the tile plus a 1-node halo.
+// CTA = TX x TY fine points, 32 x 8 threads; u1 is formed on the tile plus a 1-node halo.
 template <int TX, int TY>
 __global__ void __launch_bounds__(256) k_vc_up(Geo F, Geo G, int o, const double2* __restrict__ u,
                                                const double2* __restrict__ e, DVec fv,
@@ -106,69 +150,103 @@ __global__ void __launch_bounds__(256) k_vc_up(Geo F, Geo G, int o, const double
   constexpr int CX = TX / 2 + 3, CY = TY / 2 + 3;
   __shared__ double2 se[CY * CX];
   __shared__ double2 s1[RY * RX];
+  const int tx = threadIdx.x, ty = threadIdx.y;
   const double2* __restrict__ f = fv.get();
   const double fs = fv.scale();
   double2* __restrict__ y = yv.get();
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int cx0 = floordiv2(x0 - 1 - o), cy0 = floordiv2(y0 - 1 - o);
-  for (int t = threadIdx.x; t < CX * CY; t += blockDim.x) {
-    const int I = cx0 + t % CX, J = cy0 + t / CX;
-    se[t] = (I >= 0 && I < G.nx && J >= 0 && J < G.ny) ? e[(size_t)J * G.nx + I] : czero();
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
-    const int x = x0 - 1 + t % RX, yy = y0 - 1 + t / RX;
-    double2 v = czero();
-    if (x >= 0 && x < F.nx && yy >= 0 && yy < F.ny) {
-      const int ri = x - o, rj = yy - o;
-      const int Ia = floordiv2(ri), Ja = floordiv2(rj);
-      const bool ox = (ri & 1) != 0, oy = (rj & 1) != 0;
-      const int lx = Ia - cx0, ly = Ja - cy0;
-      double2 s;
-      if (!ox && !oy) {
-        s = se[ly * CX + lx];
-      } else if (ox && !oy) {
-        s = cadd(cscale(0.5, se[ly * CX + lx]), cscale(0.5, se[ly * CX + lx + 1]));
-      } else if (!ox && oy) {
-        s = cadd(cscale(0.5, se[ly * CX + lx]), cscale(0.5, se[(ly + 1) * CX + lx]));
-      } else {
-        s = cadd(cadd(cscale(0.25, se[ly * CX + lx]), cscale(0.25, se[ly * CX + lx + 1])),
-                 cadd(cscale(0.25, se[(ly + 1) * CX + lx]), cscale(0.25, se[(ly + 1) * CX + lx + 1])));
-      }
-      v = cadd(s, u[(size_t)yy * F.nx + x]);
+  const bool interior = x0 >= 2 && x0 + TX <= F.nx - 2 && y0 >= 2 && y0 + TY <= F.ny - 2 &&
+                        cx0 >= 0 && cx0 + CX <= G.nx && cy0 >= 0 && cy0 + CY <= G.ny;
+  const double ih2 = 1.0 / (F.h * F.h);
+  const int tid = ty * 32 + tx;
+  for (int t = tid; t < CX * CY; t += 256) {
+    {
+      const int r = t / CX, c = t - r * CX;
+      const int J = cy0 + r, I = cx0 + c;
+      se[r * CX + c] =
+          (interior || (I >= 0 && I < G.nx && J >= 0 && J < G.ny)) ? e[(size_t)J * G.nx + I] : czero();
     }
-    s1[t] = v;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) {
-    const int x = x0 + t % TX, yy = y0 + t / TX;
-    if (x >= F.nx || yy >= F.ny) continue;
-    const size_t p = (size_t)yy * F.nx + x;
-    const Coef c = coef_at(F, x, yy, k[p], sr, si);
-    const int q = (t / TX + 1) * RX + (t % TX + 1);
-    const double2 r = csub(cscale(fs, f[p]), stencil5(c, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
-    double2 v = cadd(s1[q], cscale(omega, cdiv(r, c.ap)));
-    if (addq) v = cadd(v, addq[p]);
-    y[p] = v;
+  for (int t = tid; t < RX * RY; t += 256) {
+    {
+      const int r = t / RX, c = t - r * RX;
+      const int yy = y0 - 1 + r;
+      const int rj = yy - o;
+      const int Ja = floordiv2(rj);
+      const bool oy = (rj & 1) != 0;
+      const int ly = Ja - cy0;
+      const int x = x0 - 1 + c;
+      double2 v = czero();
+      if (interior || (x >= 0 && x < F.nx && yy >= 0 && yy < F.ny)) {
+        const int ri = x - o;
+        const int Ia = floordiv2(ri);
+        const bool ox = (ri & 1) != 0;
+        const int lx = Ia - cx0;
+        const double2* e0 = se + ly * CX + lx;
+        // bilinear (Eq. 3.9): weights 1, 1/2 or 1/4 by parity; same operation order as before
+        double2 s;
+        if (!ox && !oy) {
+          s = e0[0];
+        } else if (ox && !oy) {
+          s = cadd(cscale(0.5, e0[0]), cscale(0.5, e0[1]));
+        } else if (!ox && oy) {
+          s = cadd(cscale(0.5, e0[0]), cscale(0.5, e0[CX]));
+        } else {
+          s = cadd(cadd(cscale(0.25, e0[0]), cscale(0.25, e0[1])), cadd(cscale(0.25, e0[CX]), cscale(0.25, e0[CX + 1])));
+        }
+        v = cadd(s, u[(size_t)yy * F.nx + x]);
+      }
+      s1[r * RX + c] = v;
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < TY; r += 8) {
+    const int yy = y0 + r;
+    if (yy >= F.ny) continue;
+    for (int c = tx; c < TX; c += 32) {
+      const int x = x0 + c;
+      if (x >= F.nx) continue;
+      const size_t p = (size_t)yy * F.nx + x;
+      const int q = (r + 1) * RX + (c + 1);
+      const double kk = k[p];
+      double2 ap, res;
+      if (interior) {
+        ap = interior_ap(ih2, kk, sr, si);
+        res = csub(cscale(fs, f[p]), interior_stencil(ih2, ap, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
+      } else {
+        const Coef cf = coef_at(F, x, yy, kk, sr, si);
+        ap = cf.ap;
+        res = csub(cscale(fs, f[p]), stencil5(cf, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
+      }
+      double2 v = cadd(s1[q], cscale(omega, cdiv(res, ap)));
+      if (addq) v = cadd(v, addq[p]);
+      y[p] = v;
+    }
   }
 }
 
-// ------------------------------------------------------------------ single-CTA tail
-// The remaining levels lt..last of a V-cycle (small grids) in one CTA with every array of
-// those levels (k, f, u and two scratch fields) in shared memory: the stages of a level are
-// separated by __syncthreads(); only the input f, the output u (+ q) and the coarsest dense
-// inverse touch global memory.
+// ------------------------------------------------------------------ cluster tail
+// The remaining levels lt..last of a V-cycle (small grids) run in ONE thread-block cluster of
+// CS CTAs (CS = 16 on B200, one CTA per SM): every level's arrays (f, u, two scratch fields and
+// k) are partitioned by rows across the cluster's shared memories; a stencil tap in a row owned
+// by another CTA is read through distributed shared memory (DSMEM); stages are separated by
+// cluster barriers.  Only the input f, the output u (+ q) and the dense coarsest inverse touch
+// global memory.  CS = 1 degenerates to a single-CTA tail.
 struct LevelDesc {
   Geo g;
   int o;
   const double* k;
 };
 
-// Shared-memory bytes the tail needs for levels lt..last (host and device agree on layout).
-__host__ __device__ inline size_t tail_smem_bytes(const LevelDesc* Ls, int lt, int last) {
+__host__ __device__ inline int tail_rpc(int ny, int cs) { return (ny + cs - 1) / cs; }
+
+// Shared-memory bytes per CTA for levels lt..last with a cluster of cs CTAs.
+__host__ __device__ inline size_t tail_smem_bytes(const LevelDesc* Ls, int lt, int last, int cs) {
   size_t b = 0;
   for (int l = lt; l <= last; ++l) {
-    const size_t n = (size_t)Ls[l].g.nx * Ls[l].g.ny;
+    const size_t n = (size_t)tail_rpc(Ls[l].g.ny, cs) * Ls[l].g.nx;
     b += n * 4 * sizeof(double2) + ((n * sizeof(double) + 15) / 16) * 16;   // keep 16-byte alignment
   }
   return b;
@@ -177,43 +255,72 @@ __host__ __device__ inline size_t tail_smem_bytes(const LevelDesc* Ls, int lt, i
 struct TailLevel {
   Geo g;
   int o;
+  int rpc;          // rows per CTA
+  int r0, r1;       // rows owned by this CTA
   double* k;
   double2 *f, *u, *s, *t;
 };
 
-__device__ __forceinline__ void tail_jacobi(const TailLevel& L, const double2* u, const double2* f, double2* out,
-                                            const double2* addq, double sr, double si, double omega) {
-  const int n = L.g.nx * L.g.ny;
-  for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    const int i = p % L.g.nx, j = p / L.g.nx;
-    const Coef c = coef_at(L.g, i, j, L.k[p], sr, si);
-    const double2 r = csub(f[p], stencil_apply(L.g, u, i, j, c));
-    double2 v = cadd(u[p], cscale(omega, cdiv(r, c.ap)));
-    if (addq) v = cadd(v, addq[p]);
-    out[p] = v;
-  }
+constexpr int TAIL_MAX_LEVELS = 24;
+
+// Pointer to element (i, j) of a level array whose local (this CTA's) base is `base`.
+__device__ __forceinline__ double2* tail_at(cg::cluster_group& cl, const TailLevel& L, double2* base, int i, int j,
+                                            unsigned rank) {
+  const int owner = j / L.rpc;
+  double2* p = base + (size_t)(j - owner * L.rpc) * L.g.nx + i;
+  return (owner == (int)rank) ? p : cl.map_shared_rank(p, owner);
 }
 
-constexpr int TAIL_MAX_LEVELS = 24;
+// Stencil of the level operator at (i, j) reading `arr` through DSMEM where needed.
+__device__ __forceinline__ double2 tail_stencil(cg::cluster_group& cl, const TailLevel& L, double2* arr, int i, int j,
+                                                unsigned rank, const Coef& c) {
+  const double2* row = arr + (size_t)(j - L.r0) * L.g.nx;   // own row
+  double2 v = cmul(c.ap, row[i]);
+  if (c.aw != 0.0) v = cadd(v, cscale(c.aw, row[i - 1]));
+  if (c.ae != 0.0) v = cadd(v, cscale(c.ae, row[i + 1]));
+  if (c.as != 0.0) v = cadd(v, cscale(c.as, *tail_at(cl, L, arr, i, j - 1, rank)));
+  if (c.an != 0.0) v = cadd(v, cscale(c.an, *tail_at(cl, L, arr, i, j + 1, rank)));
+  return v;
+}
+
+__device__ __forceinline__ void tail_jacobi(cg::cluster_group& cl, const TailLevel& L, double2* u, const double2* f,
+                                            double2* out, double sr, double si, double omega, unsigned rank) {
+  const int nx = L.g.nx;
+  const int n = (L.r1 - L.r0) * nx;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const int i = p % nx, j = L.r0 + p / nx;
+    const Coef c = coef_at(L.g, i, j, L.k[p], sr, si);
+    const double2 r = csub(f[p], tail_stencil(cl, L, u, i, j, rank, c));
+    out[p] = cadd(u[p], cscale(omega, cdiv(r, c.ap)));
+  }
+}
 
 __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ Ls, int lt, int last, DVec fv,
                                                   DVec uv, const double2* __restrict__ addq, double sr, double si,
                                                   double omega, int nu_pre, int nu_post,
                                                   const double2* __restrict__ Minv) {
   HELM_PDL_ENTRY();
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  const int cs = (int)cl.num_blocks();
   extern __shared__ double2 tsm[];
   __shared__ TailLevel T[TAIL_MAX_LEVELS];
   __shared__ int curi[TAIL_MAX_LEVELS];   // 0: pre-smoothed iterate in s, 1: in t
   double2* const uout = uv.get();
   const double2* const fin = fv.get();
+  const double fsc = fv.scale();
   const int nl = last - lt + 1;
   if (threadIdx.x == 0) {
     char* p = reinterpret_cast<char*>(tsm);
     for (int q = 0; q < nl; ++q) {
       const LevelDesc D = Ls[lt + q];
-      const size_t n = (size_t)D.g.nx * D.g.ny;
+      const int rpc = tail_rpc(D.g.ny, cs);
+      const size_t n = (size_t)rpc * D.g.nx;
       T[q].g = D.g;
       T[q].o = D.o;
+      T[q].rpc = rpc;
+      T[q].r0 = min(D.g.ny, (int)rank * rpc);
+      T[q].r1 = min(D.g.ny, ((int)rank + 1) * rpc);
       T[q].f = reinterpret_cast<double2*>(p); p += n * sizeof(double2);
       T[q].u = reinterpret_cast<double2*>(p); p += n * sizeof(double2);
       T[q].s = reinterpret_cast<double2*>(p); p += n * sizeof(double2);
@@ -223,69 +330,78 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
   }
   __syncthreads();
   for (int q = 0; q < nl; ++q) {
-    const int n = T[q].g.nx * T[q].g.ny;
-    const double* kg = Ls[lt + q].k;
-    for (int p = threadIdx.x; p < n; p += blockDim.x) T[q].k[p] = kg[p];
+    const TailLevel& L = T[q];
+    const int n = (L.r1 - L.r0) * L.g.nx;
+    const double* kg = Ls[lt + q].k + (size_t)L.r0 * L.g.nx;
+    for (int p = threadIdx.x; p < n; p += blockDim.x) L.k[p] = kg[p];
   }
   {
-    const int n = T[0].g.nx * T[0].g.ny;
-    const double fs = fv.scale();
-    for (int p = threadIdx.x; p < n; p += blockDim.x) T[0].f[p] = cscale(fs, fin[p]);
+    const TailLevel& L = T[0];
+    const int n = (L.r1 - L.r0) * L.g.nx;
+    const double2* fg = fin + (size_t)L.r0 * L.g.nx;
+    for (int p = threadIdx.x; p < n; p += blockDim.x) L.f[p] = cscale(fsc, fg[p]);
   }
-  __syncthreads();
+  cl.sync();
   // ---- down
   for (int q = 0; q < nl - 1; ++q) {
     const TailLevel L = T[q];
     const TailLevel G = T[q + 1];
-    const int n = L.g.nx * L.g.ny;
+    const int nx = L.g.nx;
+    const int n = (L.r1 - L.r0) * nx;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
-      const int i = p % L.g.nx, j = p / L.g.nx;
+      const int i = p % nx, j = L.r0 + p / nx;
       const Coef c = coef_at(L.g, i, j, L.k[p], sr, si);
       L.s[p] = cscale(omega, cdiv(L.f[p], c.ap));
     }
-    __syncthreads();
+    cl.sync();
     double2* cur = L.s;
     for (int sw = 1; sw < nu_pre; ++sw) {
       double2* nxt = (cur == L.s) ? L.t : L.s;
-      tail_jacobi(L, cur, L.f, nxt, nullptr, sr, si, omega);
-      __syncthreads();
+      tail_jacobi(cl, L, cur, L.f, nxt, sr, si, omega, rank);
+      cl.sync();
       cur = nxt;
     }
     double2* rb = (cur == L.s) ? L.t : L.s;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
-      const int i = p % L.g.nx, j = p / L.g.nx;
+      const int i = p % nx, j = L.r0 + p / nx;
       const Coef c = coef_at(L.g, i, j, L.k[p], sr, si);
-      rb[p] = csub(L.f[p], stencil_apply(L.g, cur, i, j, c));
+      rb[p] = csub(L.f[p], tail_stencil(cl, L, cur, i, j, rank, c));
     }
-    __syncthreads();
-    const int nc = G.g.nx * G.g.ny;
+    cl.sync();
+    const int ncx = G.g.nx;
+    const int nc = (G.r1 - G.r0) * ncx;
     for (int P = threadIdx.x; P < nc; P += blockDim.x) {
-      const int I = P % G.g.nx, J = P / G.g.nx;
+      const int I = P % ncx, J = G.r0 + P / ncx;
       const int ci = 2 * I + L.o, cj = 2 * J + L.o;
       double2 s = czero();
       for (int b = -1; b <= 1; ++b) {
         const int jj = cj + b;
         if (jj < 0 || jj >= L.g.ny) continue;
+        const double2* rowp = tail_at(cl, L, rb, 0, jj, rank);
         for (int a = -1; a <= 1; ++a) {
           const int ii = ci + a;
-          if (ii < 0 || ii >= L.g.nx) continue;
+          if (ii < 0 || ii >= nx) continue;
           const double w = (a == 0 ? 2.0 : 1.0) * (b == 0 ? 2.0 : 1.0) * (1.0 / 16.0);
-          s = cadd(s, cscale(w, rb[jj * L.g.nx + ii]));
+          s = cadd(s, cscale(w, rowp[ii]));
         }
       }
       G.f[P] = s;
     }
     if (threadIdx.x == 0) curi[q] = (cur == L.s) ? 0 : 1;
-    __syncthreads();
+    cl.sync();
   }
-  // ---- coarsest: dense inverse (reading R8), one warp per row
+  // ---- coarsest: dense inverse (reading R8), one warp per owned row
   {
     const TailLevel Cl = T[nl - 1];
     const int n = Cl.g.nx * Cl.g.ny;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int r = warp; r < n; r += nw) {
+    const int rb0 = Cl.r0 * Cl.g.nx, rb1 = Cl.r1 * Cl.g.nx;
+    for (int r = rb0 + warp; r < rb1; r += nw) {
       double2 s = czero();
-      for (int c = lane; c < n; c += 32) s = cfma(Minv[(size_t)r * n + c], Cl.f[c], s);
+      for (int c = lane; c < n; c += 32) {
+        const double2 fc = *tail_at(cl, Cl, Cl.f, c % Cl.g.nx, c / Cl.g.nx, rank);
+        s = cfma(Minv[(size_t)r * n + c], fc, s);
+      }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
@@ -293,10 +409,10 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
       }
       if (lane == 0) {
         if (nl == 1) uout[r] = addq ? cadd(s, addq[r]) : s;
-        else Cl.u[r] = s;
+        else Cl.u[r - rb0] = s;
       }
     }
-    __syncthreads();
+    cl.sync();
   }
   // ---- up
   for (int q = nl - 2; q >= 0; --q) {
@@ -305,10 +421,11 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
     const bool top = (q == 0);
     double2* cur = curi[q] ? L.t : L.s;
     double2* ob = curi[q] ? L.s : L.t;
-    const int n = L.g.nx * L.g.ny;
+    const int nx = L.g.nx;
+    const int n = (L.r1 - L.r0) * nx;
     double2* u1 = (nu_post == 0) ? L.u : ob;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
-      const int i = p % L.g.nx, j = p / L.g.nx;
+      const int i = p % nx, j = L.r0 + p / nx;
       const int ri = i - L.o, rj = j - L.o;
       const int Ia = floordiv2(ri), Ja = floordiv2(rj);
       const bool ox = (ri & 1) != 0, oy = (rj & 1) != 0;
@@ -317,25 +434,28 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
         const int J = Ja + bj;
         if (J < 0 || J >= G.g.ny) continue;
         const double wy = oy ? 0.5 : 1.0;
+        const double2* crow = tail_at(cl, G, G.u, 0, J, rank);
         for (int ai = 0; ai <= (ox ? 1 : 0); ++ai) {
           const int I = Ia + ai;
           if (I < 0 || I >= G.g.nx) continue;
           const double wx = ox ? 0.5 : 1.0;
-          s = cadd(s, cscale(wx * wy, G.u[J * G.g.nx + I]));
+          s = cadd(s, cscale(wx * wy, crow[I]));
         }
       }
       u1[p] = cadd(s, cur[p]);
     }
-    __syncthreads();
+    cl.sync();
     double2* src = u1;
     for (int sw = 0; sw < nu_post; ++sw) {
       double2* dst = (sw == nu_post - 1) ? L.u : ((src == ob) ? cur : ob);
-      tail_jacobi(L, src, L.f, dst, nullptr, sr, si, omega);
-      __syncthreads();
+      tail_jacobi(cl, L, src, L.f, dst, sr, si, omega, rank);
+      cl.sync();
       src = dst;
     }
     if (top) {
-      for (int p = threadIdx.x; p < n; p += blockDim.x) uout[p] = addq ? cadd(L.u[p], addq[p]) : L.u[p];
+      double2* ug = uout + (size_t)L.r0 * nx;
+      const double2* qg = addq ? addq + (size_t)L.r0 * nx : nullptr;
+      for (int p = threadIdx.x; p < n; p += blockDim.x) ug[p] = qg ? cadd(L.u[p], qg[p]) : L.u[p];
     }
   }
 }

@@ -18,6 +18,7 @@ HELM_BC_DIRICHLET = 0
 HELM_BC_SOMMERFELD = 1
 COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2, "red_glk1": 3, "red_glk2": 4, "red_o6": 5, "red_cmpo4": 6}
 VECTORS = {"bilinear": 0, "high_order": 1}
+OUTER = {"fgmres": 0, "gcr": 1}
 BCS = {"dirichlet": HELM_BC_DIRICHLET, "sommerfeld": HELM_BC_SOMMERFELD}
 
 
@@ -30,7 +31,8 @@ class helm_params(ctypes.Structure):
                 ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("coarse_op", ctypes.c_int),
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int),
-                ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int), ("pdl", ctypes.c_int)]
+                ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int), ("pdl", ctypes.c_int),
+                ("coarsest_n", ctypes.c_int), ("coop", ctypes.c_int), ("outer", ctypes.c_int)]
 
 
 class helm_report(ctypes.Structure):
@@ -108,6 +110,8 @@ def default_params(**overrides) -> helm_params:
             val = COARSE_OPS[val]
         if key == "vectors" and isinstance(val, str):
             val = VECTORS[val]
+        if key == "outer" and isinstance(val, str):
+            val = OUTER[val]
         if key == "beta":
             p.beta1, p.beta2 = val
             continue
@@ -247,7 +251,7 @@ class Helm:
                                           ctypes.byref(us), ctypes.byref(nb)))
         return us.value, nb.value
 
-    REGIONS = {"vcycle": 0, "apply_E": 1, "apply_A": 2}
+    REGIONS = {"vcycle": 0, "apply_E": 1, "apply_A": 2, "dcgs": 3}
 
     def helm_bench_graph(self, which, arg=0, reps=50):
         """Mean in-graph device time (us) of one instance of a region (warm, back-to-back)."""

@@ -118,9 +118,11 @@ def test_vcycle(case):
         assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11, l
 
 
-@pytest.mark.parametrize("nu,tail", [((1, 1), 0), ((2, 2), 8192), ((2, 2), 0), ((1, 0), 8192), ((3, 1), 0)])
+@pytest.mark.parametrize("nu,tail", [((1, 1), 65536), ((1, 1), 8192), ((2, 2), 8192), ((2, 2), 0), ((1, 0), 8192),
+                                     ((3, 1), 0)])
 def test_vcycle_variants(lib, nu, tail):
-    """Generic sweep counts (unfused kernels) and the per-level path without the tail."""
+    """Generic sweep counts (unfused kernels), the per-level path (tail 0, the default) and the
+    thread-block-cluster tail (levels distributed over the cluster's shared memories)."""
     for p in (GRIDS[1], GRIDS[2], GRIDS[5]):
         H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"nu_pre": nu[0], "nu_post": nu[1], "tail_max_n": tail})
         levels = oracle.build_hierarchy(p.k, p.h, p.bc)
@@ -201,17 +203,27 @@ def test_solve(lib, name, vec, op, itol, imax):
     H.close()
 
 
-@pytest.mark.parametrize("name,vec,op", [("c0_tiny", "bilinear", "galerkin"), ("mp_som_k40", "high_order", "red_glk2"),
-                                         ("wedge_f10", "high_order", "galerkin")])
-def test_graph_and_host_loop_agree(lib, name, vec, op):
+@pytest.mark.parametrize("name,vec,op,tail,coop", [("c0_tiny", "bilinear", "galerkin", 0, 0),
+                                                   ("mp_som_k40", "high_order", "red_glk2", 0, 0),
+                                                   ("wedge_f10", "high_order", "galerkin", 0, 1),
+                                                   ("c1_k50", "high_order", "galerkin", 65536, 0)])
+def test_graph_and_host_loop_agree(lib, name, vec, op, tail, coop):
     """The CUDA-graph solve (conditional while nodes) and the host-polled loop run the same
-    kernels in the same order: identical iteration counts and bitwise-identical solutions."""
+    kernels in the same order: identical iteration counts and bitwise-identical solutions
+    (with the cluster tail, and with the cooperative one-kernel Gram-Schmidt step)."""
     p = _problem(name)
-    prm = {"coarse_op": op, "vectors": vec, "inner_tol": 1e-1, "inner_maxit": 300}
+    prm = {"coarse_op": op, "vectors": vec, "inner_tol": 1e-1, "inner_maxit": 300, "tail_max_n": tail,
+           "coop": coop}
     Hg = lib.helm_setup(p, dict(prm, graph=1))
     He = lib.helm_setup(p, dict(prm, graph=0))
     xg, rg = Hg.solve(gpu(p.b), tol=1e-6, maxit=200)
     xe, re_ = He.solve(gpu(p.b), tol=1e-6, maxit=200)
+    if coop:   # the cooperative step also matches the oracle (outer count and true residual)
+        so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=1e-1,
+                                                               inner_maxit=300, maxit=200))
+        xo, ro = so.solve(p.b)
+        assert abs(rg["outer_iterations"] - ro["outer_iterations"]) <= 1
+        assert rel(oracle.apply_A(xg.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
     for key in ("outer_iterations", "inner_iterations_total", "inner_iterations_max", "converged"):
         assert rg[key] == re_[key], key
     assert torch.equal(xg, xe)
@@ -263,3 +275,50 @@ def test_invalid_arguments(lib):
     with pytest.raises(lib.HelmError):
         H.solve(b, x=b)                                             # aliasing
     H.close()
+
+
+def test_coarsest_n_hierarchy_and_solve(lib):
+    """A predefined coarsest size (coarsest_n, §4; bench.py uses 512): same hierarchy as
+    the oracle's, and the bench method (APD + Galerkin, inner CSLP-FGMRES to 1e-1 capped at 50)
+    on c1_k50 agrees with the oracle (outer count +-1 at 1e-6, solutions at 1e-10)."""
+    p = config_problem("c1_k50")
+    prm = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 50,
+           "coarsest_n": 100}
+    H = lib.helm_setup(p, prm)
+    levels = oracle.build_hierarchy(p.k, p.h, p.bc, coarsest_n=100)
+    assert [L.shape for L in levels] == [lv[:2] for lv in H.levels]
+    assert levels[-1].shape[0] * levels[-1].shape[1] <= 100 < levels[-2].shape[0] * levels[-2].shape[1]
+    op = dict(vectors="high_order", coarse_op="galerkin", inner_tol=1e-1, inner_maxit=50, coarsest_n=100)
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=400)
+    xo, rep_o = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(maxit=400, **op)).solve(p.b)
+    assert abs(rep["outer_iterations"] - rep_o["outer_iterations"]) <= 1
+    xt, _ = H.solve(gpu(p.b), tol=1e-10, maxit=600)
+    xot, _ = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(maxit=600, tol=1e-10, **op)).solve(p.b)
+    assert rel(xt.cpu().numpy(), xot) < 1e-6
+    H.close()
+
+
+@pytest.mark.parametrize("name,vec,op,itol,imax", [("c0_tiny", "bilinear", "galerkin", 1e-1, 200),
+                                                    ("mp_som_k40", "high_order", "galerkin", 1e-1, 200),
+                                                    ("c1_k50", "high_order", "red_glk2", 0.0, 40)])
+def test_solve_gcr(lib, name, vec, op, itol, imax):
+    """GCR outer (§6.3) against the oracle's GCR: outer count +-1 at 1e-6, the true
+    residual, solutions at 1e-10; graph and host-polled loops agree bitwise."""
+    p = _problem(name)
+    prm = {"coarse_op": op, "vectors": vec, "inner_tol": itol, "inner_maxit": imax, "outer": "gcr"}
+    H = lib.helm_setup(p, prm)
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=400)
+    op_ = dict(coarse_op=op, vectors=vec, inner_tol=itol, inner_maxit=imax, outer="gcr")
+    xo, rep_o = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(maxit=400, **op_)).solve(p.b)
+    assert rep["converged"] and rep_o["converged"]
+    assert abs(rep["outer_iterations"] - rep_o["outer_iterations"]) <= 1, (rep, rep_o["outer_iterations"])
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    xt, _ = H.solve(gpu(p.b), tol=1e-10, maxit=600)
+    xot, _ = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(maxit=600, tol=1e-10, **op_)).solve(p.b)
+    assert rel(xt.cpu().numpy(), xot) < 1e-6
+    He = lib.helm_setup(p, dict(prm, graph=0))
+    xe, re_ = He.solve(gpu(p.b), tol=1e-6, maxit=400)
+    x2, rep2 = H.solve(gpu(p.b), tol=1e-6, maxit=400)
+    assert re_["outer_iterations"] == rep2["outer_iterations"] and torch.equal(xe, x2)
+    H.close()
+    He.close()

@@ -81,3 +81,44 @@ def test_solver_matches_dense_solve(bc, op):
     x, rep = oracle.solve(p, oracle.SolverParams(coarse_op=op, tol=1e-11, inner_tol=1e-3))
     assert rep["converged"] and rep["relres"] < 1e-10
     assert np.linalg.norm(x.ravel() - xd) / np.linalg.norm(xd) < 1e-8
+
+
+def test_coarsest_n_stops_coarsening():
+    """R7: coarsening stops at the first level with <= coarsest_n unknowns (§4)."""
+    import numpy as np
+    k = np.full((63, 63), 5.0)
+    full = oracle.build_hierarchy(k, 1 / 64, "dirichlet")
+    assert [L.shape for L in full][-1] == (1, 1)
+    cut = oracle.build_hierarchy(k, 1 / 64, "dirichlet", coarsest_n=300)
+    assert [L.shape for L in cut] == [(63, 63), (31, 31), (15, 15)]
+
+
+def test_gcr_dense_exactness_and_minimal_residual():
+    """GCR on a small dense complex system: converges to the dense solution; with the identity
+    preconditioner its residuals equal GMRES's (both minimise ||b - Ax|| over the Krylov space,
+    Eisenstat-Elman-Schultz), so the iteration counts agree with FGMRES's."""
+    import numpy as np
+    rng = np.random.default_rng(4)
+    n = 30
+    A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + 8 * np.eye(n)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    mv = lambda v: A @ v
+    ident = lambda v: v.copy()
+    hg, hf = [], []
+    x, its, conv = oracle.gcr(mv, ident, b, 1e-12, 200, history=hg)
+    xf, itsf, convf = oracle.fgmres(mv, ident, b, 1e-12, 200, history=hf)
+    assert conv and convf
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-9)
+    np.testing.assert_allclose(hg[:6], hf[:6], rtol=1e-8)
+    assert its == itsf
+
+
+def test_gcr_outer_solver_matches_dense_solve():
+    """The A-DEF1 preconditioned GCR (§6.3) solves the model problem to its tolerance."""
+    import numpy as np
+    from workloads import mp_problem
+    p = mp_problem(10.0, 16, "sommerfeld")
+    x, rep = oracle.solve(p, oracle.SolverParams(outer="gcr", inner_solver="direct", tol=1e-10))
+    assert rep["converged"]
+    r = p.b - oracle.apply_A(x, p.k, p.h, p.bc)
+    assert np.linalg.norm(r) / np.linalg.norm(p.b) <= 1e-10

@@ -19,8 +19,8 @@ ap.add_argument("--inner-maxit", type=int, default=50)
 args = ap.parse_args()
 p = config_problem(args.workload)
 b = torch.from_numpy(p.b).cuda()
-VARIANTS = [{"graph": 1}, {"graph": 1, "pdl": 0}, {"graph": 0}, {"graph": 1, "tail_max_n": 0},
-            {"graph": 1, "tail_max_n": 2048}, {"graph": 1, "tail_max_n": 400}]
+VARIANTS = [{"coarsest_n": 512}, {"coarsest_n": 512, "coop": 0}, {"coarsest_n": 512, "pdl": 0},
+            {"coarsest_n": 512, "graph": 0}, {"coarsest_n": 0}]
 for v in VARIANTS:
     prm = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": args.inner_maxit, **v}
     H = helm.helm_setup(p, prm)
