@@ -95,6 +95,9 @@ typedef struct {
                           slower on B200 than the kernel chain, so 0 by default */
   int outer;           /* HELM_OUTER_FGMRES (default) or HELM_OUTER_GCR; the coarse solve is
                           always CSLP-preconditioned FGMRES */
+  int col_min_n;       /* V-cycle levels with at least this many unknowns use the column-streaming
+                          legs (registers + warp shuffles, no shared memory); smaller levels the
+                          tiled legs; -1 disables (default 1 << 20) */
 } helm_params;
 
 typedef struct {

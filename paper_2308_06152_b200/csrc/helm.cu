@@ -330,6 +330,17 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
     return post_launch(C);
   }
   Level& G = C.L[l + 1];
+  if (fused_vcycle(C) && C.p.col_min_n >= 0 && (long long)L.n >= C.p.col_min_n) {
+    // large levels: column-streaming legs (no shared-memory staging)
+    const int wcols = (L.g.nx + COL_OWN - 1) / COL_OWN;
+    const dim3 gc((wcols + 3) / 4, (L.g.ny + COL_SEG - 1) / COL_SEG);
+    launch_k(C, k_vc_down_col, gc, 128, 0, L.g, G.g, L.o, f, (const double*)L.k, sr, si, w, L.s, G.f);
+    CKR(post_launch(C));
+    CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
+    launch_k(C, k_vc_up_col, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f,
+             (const double*)L.k, sr, si, w, addq, u_out);
+    return post_launch(C);
+  }
   if (fused_vcycle(C)) {
     // small levels: smaller tiles so that more SMs share the (latency-bound) work
     const bool small = (size_t)((G.g.nx + DOWN_TX - 1) / DOWN_TX) * ((G.g.ny + DOWN_TY - 1) / DOWN_TY) < (size_t)2 * C.sm_count;
@@ -380,6 +391,10 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
 }
 
 // ------------------------------------------------------------------ device FGMRES
+size_t dcgs_update_smem(int m) { return std::max((size_t)(2 * m + 2) * sizeof(double2), dcgs_smem(m)); }
+
+size_t dcgs_dots_smem(const Fgm& K) { return K.geo.chunk > DC_SUB ? (size_t)(2 * K.m + 4) * sizeof(double2) : 0; }
+
 // Raise a kernel's dynamic shared-memory limit to its maximum (227 KB minus its static usage);
 // fails if `need` does not fit.
 int raise_dyn_smem(const void* func, size_t need) {
@@ -422,6 +437,12 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
+  {
+    // pass 2 in one wave: at most as many blocks as can be resident
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_update, DU_THREADS, dcgs_update_smem(m)));
+    if (bps > 0) K.geo.gu = std::max(1, std::min(K.geo.gu, bps * C.sm_count));
+  }
   // cooperative one-kernel step for small vectors (latency-bound regime)
   K.coop = 0;
   if (C.p.coop && n <= ((size_t)1 << 22)) {
@@ -436,10 +457,6 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   CK(cudaMemsetAsync(K.cnt, 0, 2 * sizeof(unsigned), C.s));
   return HELM_OK;
 }
-
-size_t dcgs_update_smem(int m) { return std::max((size_t)(2 * m + 2) * sizeof(double2), dcgs_smem(m)); }
-
-size_t dcgs_dots_smem(const Fgm& K) { return K.geo.chunk > DC_SUB ? (size_t)(2 * K.m + 4) * sizeof(double2) : 0; }
 
 void fgm_free(Fgm& K) {
   cudaFree(K.V);
@@ -703,6 +720,7 @@ void helm_default_params(helm_params* p) {
   p->coarsest_n = 0;
   p->coop = 0;
   p->outer = HELM_OUTER_FGMRES;
+  p->col_min_n = 1 << 20;
   p->pdl = 1;
 }
 
@@ -1264,6 +1282,13 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         const Level& Fl = X.L[lv];
         const Level& Gl = X.L[lv + 1];
         bytes = (double)Fl.n * 40.0 + (double)Gl.n * 16.0;
+        if (X.p.col_min_n >= 0 && (long long)Fl.n >= X.p.col_min_n) {
+          const int wcols = (Fl.g.nx + COL_OWN - 1) / COL_OWN;
+          const dim3 gc((wcols + 3) / 4, (Fl.g.ny + COL_SEG - 1) / COL_SEG);
+          k_vc_down_col<<<gc, 128, 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2, X.p.omega,
+                                             Fl.s, Gl.f);
+          return post_launch(X);
+        }
         dim3 gd((Gl.g.nx + DOWN_TX - 1) / DOWN_TX, (Gl.g.ny + DOWN_TY - 1) / DOWN_TY);
         k_vc_down<DOWN_TX, DOWN_TY><<<gd, dim3(32, 8), 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
                                                            X.p.omega, Fl.s, Gl.f);
@@ -1273,6 +1298,13 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         const Level& Fl = X.L[lv];
         const Level& Gl = X.L[lv + 1];
         bytes = (double)Fl.n * 56.0 + (double)Gl.n * 16.0;
+        if (X.p.col_min_n >= 0 && (long long)Fl.n >= X.p.col_min_n) {
+          const int wcols = (Fl.g.nx + COL_OWN - 1) / COL_OWN;
+          const dim3 gc((wcols + 3) / 4, (Fl.g.ny + COL_SEG - 1) / COL_SEG);
+          k_vc_up_col<<<gc, 128, 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
+                                           X.p.omega, nullptr, DVec(lv == 0 ? X.bbuf : Fl.u));
+          return post_launch(X);
+        }
         dim3 gu((Fl.g.nx + UP_TX - 1) / UP_TX, (Fl.g.ny + UP_TY - 1) / UP_TY);
         k_vc_up<UP_TX, UP_TY><<<gu, dim3(32, 8), 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1,
                                                      X.p.beta2, X.p.omega, nullptr, DVec(lv == 0 ? X.bbuf : Fl.u));

@@ -69,9 +69,9 @@ inline GsGeom gs_geom(long long n, int sms) {
   const long long per = (subs + 65535) / 65536;
   g.chunk = per * 256;
   g.gx = (int)((n + g.chunk - 1) / g.chunk);
-  const int target = 4 * sms;
+  const int target = 8 * sms;
   g.gy = std::max(1, std::min(16, target / std::max(1, g.gx)));
-  const long long tiles = (n + 255) / 256;
+  const long long tiles = (n + 127) / 128;   // DU_ELEMS
   g.gu = (int)std::max<long long>(1, std::min<long long>(tiles, (long long)8 * sms));
   return g;
 }
@@ -335,38 +335,42 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restr
 // 4 warps owns 256 elements (8 per lane, accumulators in registers); the warps split the basis
 // (warp q takes c = q, q+4, ...) streaming two vectors at a time (16 loads in flight per lane)
 // and their sums are combined in a fixed order through shared memory.
-constexpr int DU_THREADS = 128;
+constexpr int DU_THREADS = 256;   // standalone update: 8 warps, 128-element tiles (4 per lane)
 constexpr int DU_WARPS = DU_THREADS / 32;
-constexpr int DU_ELEMS = 256;
+constexpr int DU_ELEMS = 128;
 
+template <int NW, int EPL>
 struct DuRed {
-  double2 v[DU_WARPS][2][DU_ELEMS];
+  double2 v[NW][2][32 * EPL];
 };
 
-// one 256-element tile; sab = coefficients in shared memory; returns this thread's |w'|^2 share
+// one tile of 32*EPL elements by a block of NW warps; sab = coefficients in shared memory;
+// returns this thread's |w'|^2 share
+template <int NW, int EPL>
 __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V, long long ld, int j,
                                                    const double2* sab, double ib, double2 hjj, double2* x, double2* w,
-                                                   long long n, long long tile, DuRed& red) {
+                                                   long long n, long long tile, DuRed<NW, EPL>& red) {
+  constexpr int TE = 32 * EPL;
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const long long eb = tile * DU_ELEMS + lane;
-  double2 sa[8], sb[8];
+  const long long eb = tile * TE + lane;
+  double2 sa[EPL], sb[EPL];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) sa[q] = sb[q] = make_double2(0.0, 0.0);
+  for (int q = 0; q < EPL; ++q) sa[q] = sb[q] = make_double2(0.0, 0.0);
   int c = wq;
-  for (; c + DU_WARPS < j; c += 2 * DU_WARPS) {
+  for (; c + NW < j; c += 2 * NW) {
     const double2 ca0 = sab[2 * c], cb0 = sab[2 * c + 1];
-    const double2 ca1 = sab[2 * (c + DU_WARPS)], cb1 = sab[2 * (c + DU_WARPS) + 1];
+    const double2 ca1 = sab[2 * (c + NW)], cb1 = sab[2 * (c + NW) + 1];
     const double2* v0p = V + (long long)c * ld + eb;
-    const double2* v1p = V + (long long)(c + DU_WARPS) * ld + eb;
-    double2 v0[8], v1[8];
+    const double2* v1p = V + (long long)(c + NW) * ld + eb;
+    double2 v0[EPL], v1[EPL];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < EPL; ++q) {
       const bool ok = eb + 32 * q < n;
       v0[q] = ok ? v0p[32 * q] : make_double2(0.0, 0.0);
       v1[q] = ok ? v1p[32 * q] : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < EPL; ++q) {
       sa[q] = cfma(ca0, v0[q], sa[q]);
       sb[q] = cfma(cb0, v0[q], sb[q]);
       sa[q] = cfma(ca1, v1[q], sa[q]);
@@ -377,27 +381,25 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
     const double2 ca0 = sab[2 * c], cb0 = sab[2 * c + 1];
     const double2* v0p = V + (long long)c * ld + eb;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < EPL; ++q) {
       const double2 v0 = (eb + 32 * q < n) ? v0p[32 * q] : make_double2(0.0, 0.0);
       sa[q] = cfma(ca0, v0, sa[q]);
       sb[q] = cfma(cb0, v0, sb[q]);
     }
   }
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < EPL; ++q) {
     red.v[wq][0][lane + 32 * q] = sa[q];
     red.v[wq][1][lane + 32 * q] = sb[q];
   }
   __syncthreads();
   double nrm = 0.0;
-#pragma unroll
-  for (int rr = 0; rr < DU_ELEMS / DU_THREADS; ++rr) {
-    const int el = threadIdx.x + DU_THREADS * rr;
-    const long long e = tile * DU_ELEMS + el;
+  for (int el = threadIdx.x; el < TE; el += 32 * NW) {
+    const long long e = tile * TE + el;
     if (e < n) {
       double2 ta = make_double2(0.0, 0.0), tb = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int q = 0; q < DU_WARPS; ++q) {
+      for (int q = 0; q < NW; ++q) {
         ta = cadd(ta, red.v[q][0][el]);
         tb = cadd(tb, red.v[q][1][el]);
       }
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(DU_THREADS) k_dcgs_update(const double2* __res
                                                             cudaGraphConditionalHandle hcond, int use_h) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 sab[];
-  __shared__ DuRed red;
+  __shared__ DuRed<DU_WARPS, DU_ELEMS / 32> red;
   const int j = *jptr;
   for (int c = threadIdx.x; c < 2 * j; c += DU_THREADS) sab[c] = coef[c];
   __syncthreads();
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(DU_THREADS) k_dcgs_update(const double2* __res
   double nrm = 0.0;
   const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
   for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x)
-    nrm += dcgs_update_tile(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
+    nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
   const double t = block_sum(nrm);
   if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
   // step B in the last block to finish (sab is free again: it doubles as step B's scratch)
@@ -471,7 +473,8 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_step(const double2* __restr
   HELM_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double2 dsm[];
-  __shared__ DuRed red;
+  constexpr int CE = 256;   // tile of the cooperative pass 2: 4 warps x 8 elements per lane
+  __shared__ DuRed<DC_WARPS, CE / 32> red;
   const int j = st->j;
   const int nvec = j + 1;
   // pass 1
@@ -507,9 +510,9 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_step(const double2* __restr
     double2* x = xv.get();
     double2* w = wv.get();
     double nrm = 0.0;
-    const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
+    const long long tiles = (n + CE - 1) / CE;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x)
-      nrm += dcgs_update_tile(V, ld, j, dsm, ib, hjj, x, w, n, tile, red);
+      nrm += dcgs_update_tile<DC_WARPS, CE / 32>(V, ld, j, dsm, ib, hjj, x, w, n, tile, red);
     const double t = block_sum(nrm);
     if (threadIdx.x == 0) npart[blockIdx.x] = make_double2(t, 0.0);
   }

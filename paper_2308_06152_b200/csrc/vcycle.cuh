@@ -227,6 +227,197 @@ __global__ void __launch_bounds__(256) k_vc_up(Geo F, Geo G, int o, const double
   }
 }
 
+// ------------------------------------------------------------------ column-streaming legs
+// For large levels the tiled legs are limited by the L1/shared-memory pipe (every u/r value is
+// staged and re-read from shared memory).  Here a warp owns 28 fine columns (lanes cover the
+// 32 columns xo-2 .. xo+29: a 2-column halo each side) and streams down a segment of rows;
+// x-neighbours come from warp shuffles, y-neighbours from registers (a ring of the last rows),
+// so each f, k, u value is read from global memory once and shared memory is not used.
+constexpr int COL_OWN = 28;   // fine columns owned per warp
+constexpr int COL_SEG = 64;   // fine rows owned per warp
+
+__device__ __forceinline__ double2 shfl_up2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+__device__ __forceinline__ double2 shfl_dn2(double2 v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+
+// Down leg, column-streaming form (same arithmetic as k_vc_down):
+//   u = omega f / D,  r = f - M u,  f_c = I_h^{2h} r.
+// Grid: x = ceil(nx / 28) warp-columns (4 warps per block along x), y = ceil(ny / 64) segments.
+__global__ void __launch_bounds__(128) k_vc_down_col(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
+                                                     double sr, double si, double omega, double2* __restrict__ u,
+                                                     double2* __restrict__ fc) {
+  HELM_PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int wcol = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int xo = wcol * COL_OWN;
+  if (xo >= F.nx) return;
+  const int x = xo - 2 + lane;
+  const bool xin = (x >= 0 && x < F.nx);
+  const bool xown = (lane >= 2 && lane < 2 + COL_OWN && x < F.nx);
+  const int ya = blockIdx.y * COL_SEG;
+  const int yb = min(F.ny, ya + COL_SEG);
+  const double2* __restrict__ f = fv.get();
+  const double fs = fv.scale();
+  // coarse column of this lane's fine column (restriction centre when even relative index)
+  const int ri = x - o;
+  const bool xcentre = ((ri & 1) == 0) && ri >= 0 && (ri >> 1) < G.nx && xown;
+  const int I = ri >> 1;
+  // rings: u at rows y-2, y-1, y; f, k at row y-1; r at rows y-3, y-2, y-1
+  double2 um2 = czero(), um1 = czero(), fm1 = czero(), rm3 = czero(), rm2 = czero();
+  double km1 = 0.0;
+  // software pipeline: f and k of rows y and y+1 are loaded one and two iterations ahead
+  auto ldf = [&](int yy, double2& fo, double& ko) {
+    if (xin && yy >= 0 && yy < F.ny) {
+      const size_t p = (size_t)yy * F.nx + x;
+      fo = f[p];
+      ko = k[p];
+    } else {
+      fo = czero();
+      ko = 0.0;
+    }
+  };
+  double2 fA, fB;
+  double kA, kB;
+  ldf(ya - 2, fA, kA);
+  ldf(ya - 1, fB, kB);
+  for (int y = ya - 2; y <= yb + 1; ++y) {
+    const bool yin = (y >= 0 && y < F.ny);
+    const double2 fraw = fA;
+    const double k0 = kA;
+    fA = fB;
+    kA = kB;
+    ldf(y + 2, fB, kB);
+    double2 f0 = czero(), u0 = czero();
+    if (xin && yin) {
+      f0 = cscale(fs, fraw);
+      const Coef c = coef_at(F, x, y, k0, sr, si);
+      u0 = cscale(omega, cdiv(f0, c.ap));   // reading R9: first sweep from u = 0
+      if (xown && y >= ya && y < yb) u[(size_t)y * F.nx + x] = u0;
+    }
+    // residual at row y-1 (needs u rows y-2, y-1, y)
+    const int yr = y - 1;
+    const double2 uw = shfl_up2(um1, 1), ue = shfl_dn2(um1, 1);
+    double2 r = czero();                      // reading R4: out-of-array taps dropped
+    if (xin && yr >= 0 && yr < F.ny && lane >= 1 && lane <= 30) {
+      const Coef c = coef_at(F, x, yr, km1, sr, si);
+      r = csub(fm1, stencil5(c, um1, uw, ue, um2, u0));
+    }
+    // restriction for the coarse row whose centre is fine row y-2 (needs r rows y-3, y-2, y-1)
+    const int yc = y - 2;
+    const int rj = yc - o;
+    {
+      const double2 a0 = shfl_up2(rm3, 1), a2 = shfl_dn2(rm3, 1);
+      const double2 b0 = shfl_up2(rm2, 1), b2 = shfl_dn2(rm2, 1);
+      const double2 c0 = shfl_up2(r, 1), c2 = shfl_dn2(r, 1);
+      if (xcentre && yc >= ya && yc < yb && ((rj & 1) == 0) && rj >= 0 && (rj >> 1) < G.ny) {
+        double2 s = czero();
+        // same tap order as k_vc_down: b = -1, 0, 1 outer; a = -1, 0, 1 inner
+        s = cadd(s, cscale(1.0 / 16.0, a0));
+        s = cadd(s, cscale(2.0 / 16.0, rm3));
+        s = cadd(s, cscale(1.0 / 16.0, a2));
+        s = cadd(s, cscale(2.0 / 16.0, b0));
+        s = cadd(s, cscale(4.0 / 16.0, rm2));
+        s = cadd(s, cscale(2.0 / 16.0, b2));
+        s = cadd(s, cscale(1.0 / 16.0, c0));
+        s = cadd(s, cscale(2.0 / 16.0, r));
+        s = cadd(s, cscale(1.0 / 16.0, c2));
+        fc[(size_t)(rj >> 1) * G.nx + I] = s;
+      }
+    }
+    rm3 = rm2;
+    rm2 = r;
+    um2 = um1;
+    um1 = u0;
+    fm1 = f0;
+    km1 = k0;
+  }
+}
+
+// Up leg, column-streaming form (same arithmetic as k_vc_up):
+//   u1 = u + I_{2h}^h e,  y = u1 + omega (f - M u1)/D (+ q).
+__global__ void __launch_bounds__(128) k_vc_up_col(Geo F, Geo G, int o, const double2* __restrict__ u,
+                                                   const double2* __restrict__ e, DVec fv,
+                                                   const double* __restrict__ k, double sr, double si, double omega,
+                                                   const double2* __restrict__ addq, DVec yv) {
+  HELM_PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int wcol = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int xo = wcol * COL_OWN;
+  if (xo >= F.nx) return;
+  const int x = xo - 2 + lane;
+  const bool xin = (x >= 0 && x < F.nx);
+  const bool xown = (lane >= 2 && lane < 2 + COL_OWN && x < F.nx);
+  const int ya = blockIdx.y * COL_SEG;
+  const int yb = min(F.ny, ya + COL_SEG);
+  const double2* __restrict__ f = fv.get();
+  const double fs = fv.scale();
+  double2* __restrict__ yo = yv.get();
+  const int ri = x - o;
+  const int Ia = floordiv2(ri);
+  const bool ox = (ri & 1) != 0;
+  const bool i0in = Ia >= 0 && Ia < G.nx, i1in = (Ia + 1) >= 0 && (Ia + 1) < G.nx;
+  // bilinear interpolation of e at fine (x, y): weights 1, 1/2, 1/4 by parity (Eq. 3.9),
+  // same operation order as k_vc_up (coarse values come from L1: adjacent lanes share them)
+  auto interp = [&](int yy) -> double2 {
+    const int rj = yy - o;
+    const int Ja = floordiv2(rj);
+    const bool oy = (rj & 1) != 0;
+    auto ev = [&](int J, int Ii, bool iin) -> double2 {
+      return (iin && J >= 0 && J < G.ny) ? e[(size_t)J * G.nx + Ii] : czero();
+    };
+    const double2 e00 = ev(Ja, Ia, i0in);
+    if (!ox && !oy) return e00;
+    if (ox && !oy) return cadd(cscale(0.5, e00), cscale(0.5, ev(Ja, Ia + 1, i1in)));
+    if (!ox && oy) return cadd(cscale(0.5, e00), cscale(0.5, ev(Ja + 1, Ia, i0in)));
+    return cadd(cadd(cscale(0.25, e00), cscale(0.25, ev(Ja, Ia + 1, i1in))),
+                cadd(cscale(0.25, ev(Ja + 1, Ia, i0in)), cscale(0.25, ev(Ja + 1, Ia + 1, i1in))));
+  };
+  double2 v1m2 = czero(), v1m1 = czero();   // u1 at rows y-2, y-1
+  auto ldu = [&](int yy) -> double2 { return (xin && yy >= 0 && yy < F.ny) ? u[(size_t)yy * F.nx + x] : czero(); };
+  auto ldo = [&](int yy, double2& fo, double& ko, double2& qo) {
+    if (xown && yy >= ya && yy < yb) {
+      const size_t p = (size_t)yy * F.nx + x;
+      fo = f[p];
+      ko = k[p];
+      qo = addq ? addq[p] : czero();
+    } else {
+      fo = czero();
+      ko = 0.0;
+      qo = czero();
+    }
+  };
+  double2 uA = ldu(ya - 1);
+  double2 fO, qO;
+  double kO;
+  ldo(ya - 2, fO, kO, qO);
+  for (int y = ya - 1; y <= yb; ++y) {
+    const bool yin = (y >= 0 && y < F.ny);
+    const double2 ucur = uA;
+    uA = ldu(y + 1);
+    const double2 fcur = fO, qcur = qO;
+    const double kcur = kO;
+    ldo(y, fO, kO, qO);
+    double2 v10 = czero();
+    if (xin && yin) v10 = cadd(interp(y), ucur);
+    // post-smoothing at row y-1 (needs u1 rows y-2, y-1, y)
+    const int yr = y - 1;
+    const double2 uw = shfl_up2(v1m1, 1), ue = shfl_dn2(v1m1, 1);
+    if (xown && yr >= ya && yr < yb) {
+      const size_t p = (size_t)yr * F.nx + x;
+      const Coef c = coef_at(F, x, yr, kcur, sr, si);
+      const double2 res = csub(cscale(fs, fcur), stencil5(c, v1m1, uw, ue, v1m2, v10));
+      double2 out = cadd(v1m1, cscale(omega, cdiv(res, c.ap)));
+      if (addq) out = cadd(out, qcur);
+      yo[p] = out;
+    }
+    v1m2 = v1m1;
+    v1m1 = v10;
+  }
+}
+
 // ------------------------------------------------------------------ cluster tail
 // The remaining levels lt..last of a V-cycle (small grids) run in ONE thread-block cluster of
 // CS CTAs (CS = 16 on B200, one CTA per SM): every level's arrays (f, u, two scratch fields and

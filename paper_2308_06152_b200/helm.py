@@ -32,7 +32,8 @@ class helm_params(ctypes.Structure):
                 ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int),
                 ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int), ("pdl", ctypes.c_int),
-                ("coarsest_n", ctypes.c_int), ("coop", ctypes.c_int), ("outer", ctypes.c_int)]
+                ("coarsest_n", ctypes.c_int), ("coop", ctypes.c_int), ("outer", ctypes.c_int),
+                ("col_min_n", ctypes.c_int)]
 
 
 class helm_report(ctypes.Structure):

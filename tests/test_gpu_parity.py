@@ -118,18 +118,20 @@ def test_vcycle(case):
         assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11, l
 
 
-@pytest.mark.parametrize("nu,tail", [((1, 1), 65536), ((1, 1), 8192), ((2, 2), 8192), ((2, 2), 0), ((1, 0), 8192),
-                                     ((3, 1), 0)])
-def test_vcycle_variants(lib, nu, tail):
-    """Generic sweep counts (unfused kernels), the per-level path (tail 0, the default) and the
-    thread-block-cluster tail (levels distributed over the cluster's shared memories)."""
+@pytest.mark.parametrize("nu,tail,col", [((1, 1), 65536, -1), ((1, 1), 8192, -1), ((2, 2), 8192, -1), ((2, 2), 0, -1),
+                                         ((1, 0), 8192, -1), ((3, 1), 0, -1), ((1, 1), 0, 0), ((1, 1), 0, 500)])
+def test_vcycle_variants(lib, nu, tail, col):
+    """Generic sweep counts (unfused kernels), the per-level path (tail 0, the default), the
+    thread-block-cluster tail (levels distributed over the cluster's shared memories) and the
+    column-streaming legs (col_min_n: 0 = every level, 500 = the larger ones)."""
     for p in (GRIDS[1], GRIDS[2], GRIDS[5]):
-        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"nu_pre": nu[0], "nu_post": nu[1], "tail_max_n": tail})
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"nu_pre": nu[0], "nu_post": nu[1], "tail_max_n": tail,
+                                                  "col_min_n": col})
         levels = oracle.build_hierarchy(p.k, p.h, p.bc)
         for l in range(min(3, len(levels))):
             f = random_field(levels[l].shape, 50 + l)
             u = H.vcycle(l, gpu(f)).cpu().numpy()
-            assert rel(u, oracle.vcycle(levels, f, l, nu_pre=nu[0], nu_post=nu[1])) < 1e-11, (p.shape, l, nu, tail)
+            assert rel(u, oracle.vcycle(levels, f, l, nu_pre=nu[0], nu_post=nu[1])) < 1e-11, (p.shape, l, nu, tail, col)
         H.close()
 
 
@@ -203,17 +205,17 @@ def test_solve(lib, name, vec, op, itol, imax):
     H.close()
 
 
-@pytest.mark.parametrize("name,vec,op,tail,coop", [("c0_tiny", "bilinear", "galerkin", 0, 0),
-                                                   ("mp_som_k40", "high_order", "red_glk2", 0, 0),
-                                                   ("wedge_f10", "high_order", "galerkin", 0, 1),
-                                                   ("c1_k50", "high_order", "galerkin", 65536, 0)])
-def test_graph_and_host_loop_agree(lib, name, vec, op, tail, coop):
+@pytest.mark.parametrize("name,vec,op,tail,coop,col", [("c0_tiny", "bilinear", "galerkin", 0, 0, -1),
+                                                       ("mp_som_k40", "high_order", "red_glk2", 0, 0, 0),
+                                                       ("wedge_f10", "high_order", "galerkin", 0, 1, 1 << 20),
+                                                       ("c1_k50", "high_order", "galerkin", 65536, 0, 1 << 20)])
+def test_graph_and_host_loop_agree(lib, name, vec, op, tail, coop, col):
     """The CUDA-graph solve (conditional while nodes) and the host-polled loop run the same
     kernels in the same order: identical iteration counts and bitwise-identical solutions
     (with the cluster tail, and with the cooperative one-kernel Gram-Schmidt step)."""
     p = _problem(name)
     prm = {"coarse_op": op, "vectors": vec, "inner_tol": 1e-1, "inner_maxit": 300, "tail_max_n": tail,
-           "coop": coop}
+           "coop": coop, "col_min_n": col}
     Hg = lib.helm_setup(p, dict(prm, graph=1))
     He = lib.helm_setup(p, dict(prm, graph=0))
     xg, rg = Hg.solve(gpu(p.b), tol=1e-6, maxit=200)
