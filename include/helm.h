@@ -1,7 +1,9 @@
 /*
  * helm.h — C ABI of the B200 (sm_100a) hot path of arXiv:2308.06152:
- * matrix-free two-level deflation (A-DEF1) + CSLP-multigrid preconditioned FGMRES for the
- * 2D finite-difference Helmholtz equation  -Delta u - k(x,y)^2 u = b  (Eq. 2.1).
+ * matrix-free two-level deflation (A-DEF1 with bilinear vectors, APD with the higher-order
+ * vectors) + CSLP-multigrid preconditioned FGMRES / GCR for the 2D finite-difference Helmholtz
+ * equation  -Delta u - k(x,y)^2 u = b  (Eq. 2.1).  The whole solve runs on the device
+ * (one CUDA graph; outer and inner Krylov loops are conditional while nodes).
  *
  * Conventions shared by every entry point
  * ---------------------------------------
@@ -33,7 +35,7 @@ extern "C" {
 #define HELM_BC_DIRICHLET 0   /* PAPER.md Eq. 2.2 (homogeneous) */
 #define HELM_BC_SOMMERFELD 1  /* PAPER.md Eq. 2.3, ghost elimination Eq. 2.8-2.10 */
 
-#define HELM_COARSE_GALERKIN 0 /* E = I_h^{2h} A_h I_{2h}^h, stored 9-point stencil (§3.2.1, §5.2.2) */
+#define HELM_COARSE_GALERKIN 0 /* str-Glk E = I_h^{2h} A_h I_{2h}^h applied as Z, A, Z^T fused (§3.2.1, §5.2.1) */
 #define HELM_COARSE_RED_O2 1   /* second-order re-discretisation at 2h (§5.2.3) */
 #define HELM_COARSE_RED_O4 2   /* fourth-order re-discretisation, Eq. 5.11 (§5.2.3) */
 #define HELM_COARSE_RED_GLK1 3 /* ReD-Glk1, Eq. 5.12/5.14, 2nd order on two layers (§5.2.4) */
@@ -46,7 +48,7 @@ extern "C" {
 #define HELM_OUTER_FGMRES 0 /* flexible GMRES, Algorithm 1 (flexible form, §6.3) */
 #define HELM_OUTER_GCR 1    /* preconditioned GCR, PAPER.md:427 and §6.3 */
 
-#define HELM_VECTORS_BILINEAR 0   /* A-DEF1: Z = Eq. 3.9, Z^T/4 = full weighting Eq. 3.8 */
+#define HELM_VECTORS_BILINEAR 0   /* A-DEF1: Z = Eq. 3.9, restriction Z^T (Eq. 3.7 per direction) */
 #define HELM_VECTORS_HIGH_ORDER 1 /* APD: Z = Eq. 3.12, Z^T = Eq. 3.14 (§3.2.1, §3.2.2) */
 
 #define HELM_OK 0
@@ -150,7 +152,7 @@ int helm_deflate(helm_ctx ctx, const double* v_dev, double* z_dev, int* inner_it
  * alias b).  rep may be NULL. */
 int helm_solve(helm_ctx ctx, const double* b_dev, double* x_dev, double tol, int maxit, helm_report* rep);
 /* Deflation vectors of the configured kind between level 0 and the coarse grid (level 1):
- * coarse = R Z^T fine (R = 1/4 bilinear, 1 high order), fine = Z coarse. */
+ * coarse = Z^T fine, fine = Z coarse (reading R10). */
 int helm_apply_Zt(helm_ctx ctx, const double* fine_dev, double* coarse_dev);
 int helm_apply_Z(helm_ctx ctx, const double* coarse_dev, double* fine_dev);
 /* Same with host buffers: H2D copy of b, solve, D2H copy of x (end-to-end path). */

@@ -17,7 +17,8 @@ Rules:
 Pins (tests/test_oracle_*.py, -m "not gpu"): discrete Dirichlet eigenfunctions with the
 closed-form eigenvalues of Appendix B; textbook Kronecker-sum assembly of A (both BCs) and
 of the bilinear prolongation; ghost-point form of the Sommerfeld rows (Eq. 2.8);
-R = Z^T/4; tensor-product closed form of the Galerkin coarse operator R A P; dense
+full weighting = Z^T/4 and the deflation restriction = Z^T exactly; tensor-product closed form of
+the Galerkin coarse operator Z^T A Z; dense
 two-grid operator vs the V-cycle; deflation identities P A Z = 0 and Q A Z = Z; dense
 solves on tiny grids; printed iteration counts of Tables 1 and 2 (tests/golden/).
 
@@ -30,7 +31,7 @@ from .operators import (  # noqa: F401
     apply_A,
     apply_M,
 )
-from .transfer import (coarsenable, coarse_shape, coarse_k, restrict_fw, prolong_bilinear,  # noqa: F401
+from .transfer import (coarsenable, coarse_shape, coarse_k, restrict_fw, restrict_bilinear_zt, prolong_bilinear,  # noqa: F401
                        restrict_high_order, prolong_high_order)
 from .coarse import apply_coarse_E  # noqa: F401
 from .multigrid import Level, build_hierarchy, vcycle, jacobi_diagonal  # noqa: F401

@@ -29,7 +29,7 @@ from __future__ import annotations
 import numpy as np
 
 from .operators import apply_A
-from .transfer import (coarse_k, coarse_shape, prolong_bilinear, prolong_high_order, restrict_fw,
+from .transfer import (coarse_k, coarse_shape, prolong_bilinear, prolong_high_order, restrict_bilinear_zt,
                        restrict_high_order)
 
 COARSE_OPS = ("galerkin", "red_o2", "red_o4", "red_o6", "red_cmpo4", "red_glk1", "red_glk2")
@@ -57,10 +57,12 @@ def _red_glk(x, kc, H, bc, variant):
     u_1 = (u_0 + u_2)/2 for Dirichlet) with ghost wavenumber 0, second-order stencil only on
     the first layer (Dirichlet: the first layer is the boundary node itself, which is not an
     unknown, so every unknown uses the 5x5 stencil).
-    Reading R14: the second-order fallback uses 4 A_{2h} so that all rows share the scale
-    of Z^T A Z (the 5x5 stencils approximate 4(-Delta - k^2), Eq. 5.13)."""
+    Reading R14: the boundary layers use "the standard second-order discretization"
+     literally, i.e. A_{2h} of Eq. 2.7/2.9/2.10 at mesh 2h, although the 5x5
+    interior stencils carry the factor 4 of Z^T A Z (Eq. 5.13); the paper attributes the extra
+    ReD-Glk1 iterations to this "simplified boundary treatment"."""
     ny, nx = x.shape
-    y2 = 4.0 * apply_A(x, kc, H, bc)
+    y2 = apply_A(x, kc, H, bc)
     # extended arrays with 2 ghost layers
     X = np.zeros((ny + 4, nx + 4), dtype=np.complex128)
     K = np.zeros((ny + 4, nx + 4))
@@ -171,7 +173,7 @@ def _red_cmpo4(x, kc, H, bc):
 def apply_coarse_E(x: np.ndarray, k_fine: np.ndarray, h: float, bc: str, op: str = "galerkin",
                    vectors: str = "bilinear") -> np.ndarray:
     """y = E x on the deflation coarse grid (mesh width 2h).
-    vectors="bilinear": A-DEF1 (Z = Eq. 3.9, R = Eq. 3.8 = Z^T/4);
+    vectors="bilinear": A-DEF1 (Z = Eq. 3.9, restriction Z^T = Eq. 3.7 per direction, R10);
     vectors="high_order": APD (Z = Eq. 3.12, R = Eq. 3.14 = Z^T).
     The re-discretised operators (RED_OPS) are the same for both vector kinds: they replace
     A_{2h} as printed, without the factor 4 that Z^T A Z carries for the higher-order vectors
@@ -198,5 +200,5 @@ def apply_coarse_E(x: np.ndarray, k_fine: np.ndarray, h: float, bc: str, op: str
     if op == "galerkin":
         v1 = prolong_bilinear(x, fine_shape, bc)      # Eq. 5.7a
         v2 = apply_A(v1, k_fine, h, bc)               # Eq. 5.7b
-        return restrict_fw(v2, bc)                    # Eq. 5.7c
+        return restrict_bilinear_zt(v2, bc)           # Eq. 5.7c
     raise ValueError(op)

@@ -10,8 +10,13 @@ the coarse-grid operator"; §6.3: with a flexible outer method the coarse tolera
 loose (1e-1) while the outer solution still meets 1e-6.
 
 Readings:
-  R10 E = A_{2h} uses the paper's scaling I_h^{2h} A_h I_{2h}^h (= Z^T A Z / 4 since the
-      full weighting is Z^T / 4); Q_h is the same operator as Z (Z^T A Z)^{-1} Z^T.
+  R10 The deflation restriction is Z^T for both kinds of vectors: "Z^T will be the full-weighting
+      restriction operator" names the operator, Eq. 3.7 fixes its scale (weights
+      1/2, 1, 1/2 per direction, i.e. 4x the 1/16-normalised stencil of Eq. 3.8 that the CSLP
+      V-cycle uses).  str-Glk is E = Z^T A Z (Q = Z E^{-1} Z^T is independent of that scale);
+      the re-discretised operators replace E as printed (R21), so with them Q carries the
+      factor 4 and P_h "is no longer a projection" -- which reproduces the ReD-O2
+      counts of Tables 1-2 (the 1/16 scaling would make ReD-O2 as fast as str-Glk).
   R11 The coarse problem E e = c is solved by right-preconditioned FGMRES from e = 0 to the
       relative residual inner_tol, preconditioned by one CSLP V-cycle starting at level 1
       of the CSLP hierarchy (mesh 2h); inner_solver="direct" replaces it by a dense solve.
@@ -34,7 +39,7 @@ from .coarse import apply_coarse_E
 from .krylov import fgmres, gcr
 from .multigrid import build_hierarchy, vcycle
 from .operators import apply_A
-from .transfer import coarse_shape, prolong_bilinear, prolong_high_order, restrict_fw, restrict_high_order
+from .transfer import coarse_shape, prolong_bilinear, prolong_high_order, restrict_bilinear_zt, restrict_high_order
 
 
 @dataclasses.dataclass
@@ -79,7 +84,7 @@ class Solver:
         return apply_coarse_E(x, self.k, self.h, self.bc, self.p.coarse_op, self.p.vectors)
 
     def Zt(self, v):
-        return restrict_fw(v, self.bc) if self.p.vectors == "bilinear" else restrict_high_order(v, self.bc)
+        return restrict_bilinear_zt(v, self.bc) if self.p.vectors == "bilinear" else restrict_high_order(v, self.bc)
 
     def Zp(self, e):
         if self.p.vectors == "bilinear":

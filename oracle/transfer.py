@@ -60,6 +60,27 @@ def restrict_fw(v: np.ndarray, bc: str) -> np.ndarray:
     return out
 
 
+def restrict_bilinear_zt(v: np.ndarray, bc: str) -> np.ndarray:
+    """Z^T for the bilinear deflation vectors: PAPER.md Eq. 3.7, I_h^{2h} u_i =
+    (1/2)(u_{2i-1} + 2 u_{2i} + u_{2i+1}), applied in both directions, i.e. the 9 taps
+    (1/4, 1/2, 1/4) (x) (1/4, 1/2, 1/4) x 4 = [1 2 1; 2 4 2; 1 2 1]/4 around fine node (2I+o, 2J+o).
+    It is the exact transpose of prolong_bilinear (taps outside the array dropped, R4) and 4x the
+    full weighting of Eq. 3.8 that the CSLP V-cycle uses (reading R10)."""
+    o = unknown_offset(bc)
+    ny, nx = v.shape
+    nyc, nxc = coarse_shape(v.shape, bc)
+    vp = np.zeros((ny + 2, nx + 2), dtype=np.complex128)
+    vp[1:-1, 1:-1] = v
+    out = np.zeros((nyc, nxc), dtype=np.complex128)
+    w1 = {-1: 0.5, 0: 1.0, 1: 0.5}
+    for b in (-1, 0, 1):
+        for a in (-1, 0, 1):
+            r0 = o + 1 + b
+            c0 = o + 1 + a
+            out += (w1[a] * w1[b]) * vp[r0:r0 + 2 * nyc:2, c0:c0 + 2 * nxc:2]
+    return out
+
+
 def prolong_bilinear(e: np.ndarray, fine_shape, bc: str) -> np.ndarray:
     """Bilinear interpolation I_{2h}^h (Eq. 3.9 / Eq. 3.6 in each direction): coincident
     fine nodes copy, edge midpoints average 2 coarse values, cell centres average 4."""

@@ -239,16 +239,15 @@ __global__ void k_sample_k(Geo gf, Geo gc, int o, const double* __restrict__ kf,
 // 1D weight of coarse node c at fine node 2c + o + d (a column of Z):
 //   bilinear (R = 1): Eq. 3.6/3.9      w(0) = 1,   w(+-1) = 1/2
 //   high order (R = 2): Eq. 3.11a/3.12 w(0) = 3/4, w(+-1) = 1/2, w(+-2) = 1/8
-// Restriction = RS * Z^T: RS = 1/4 (full weighting, Eq. 3.8), RS = 1 (Eq. 3.14).
+// The deflation restriction is Z^T for both (Eq. 3.7 per direction / Eq. 3.14; reading R10) --
+// 4x the 1/16-normalised full weighting the V-cycle uses for the bilinear vectors.
 template <int R>
 __device__ __forceinline__ double zw(int d) {
   if (R == 1) return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 : 0.0);
   return d == 0 ? 0.75 : ((d == 1 || d == -1) ? 0.5 : ((d == 2 || d == -2) ? 0.125 : 0.0));
 }
-template <int R>
-__device__ __forceinline__ double zrs() { return R == 1 ? 0.25 : 1.0; }
 
-// vc = RS * Z^T v  (gather of the (2R+1)^2 fine taps; out-of-array taps dropped, reading R4)
+// vc = Z^T v  (gather of the (2R+1)^2 fine taps; out-of-array taps dropped, reading R4)
 template <int R>
 __global__ void k_restrict_z(Geo gf, Geo gc, int o, DVec vv, double2* __restrict__ vc) {
   HELM_PDL_ENTRY();
@@ -271,7 +270,7 @@ __global__ void k_restrict_z(Geo gf, Geo gc, int o, DVec vv, double2* __restrict
       s = cadd(s, cscale(wy * zw<R>(a), v[(size_t)jj * gf.nx + ii]));
     }
   }
-  vc[(size_t)J * gc.nx + I] = cscale(zrs<R>() * vs, s);
+  vc[(size_t)J * gc.nx + I] = cscale(vs, s);
 }
 
 // y = Z e (MODE 0) or y = base + Z e (MODE 1), gather at each fine node.
@@ -298,10 +297,10 @@ __global__ void k_prolong_z(Geo gf, Geo gc, int o, const double2* __restrict__ e
 }
 
 // ------------------------------------------------------------------ Galerkin coarse operator
-// y = E x = RS Z^T A Z x (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; str-Glk §5.2.1,
+// y = E x = Z^T A Z x (§3.2.1 "A_{2h} = I_h^{2h} A_h I_{2h}^h"; str-Glk §5.2.1,
 // Eq. 5.7a-c: interpolation, fine-grid operator, restriction) applied matrix-free in ONE kernel:
 // for a tile of TCX x TCY coarse outputs, x (coarse, with halo) -> t = Z x on the fine footprint
-// plus one node -> s = A t on the footprint -> y = RS Z^T s, all in shared memory.  HBM traffic
+// plus one node -> s = A t on the footprint -> y = Z^T s, all in shared memory.  HBM traffic
 // per coarse unknown: x 16 + k 4 x 8 + y 16 B (the paper's three passes, or a stored 25-point
 // stencil, would move ~10x more).  MODE 1: y = f - E x.
 __device__ __forceinline__ int ceildiv2(int a) { return (a >= 0) ? ((a + 1) >> 1) : -((-a) >> 1); }
@@ -433,7 +432,6 @@ __global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, c
       double2 s = zero;
 #pragma unroll
       for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
-      s = cscale(zrs<R>(), s);
       const size_t p = (size_t)J * gc.nx + I;
       y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
     }
@@ -487,7 +485,9 @@ __device__ double2 glk2_val(const Geo& g, const double2* __restrict__ x, const d
   return colv(ii, jj);
 }
 
-// VARIANT 1: ReD-Glk1, VARIANT 2: ReD-Glk2 (reading R14: second-order rows scaled by 4).
+// VARIANT 1: ReD-Glk1, VARIANT 2: ReD-Glk2 (reading R14: the boundary layers use the plain
+// second-order stencil A_2h, as PAPER.md:748 states, while the interior 5x5 rows carry the
+// factor 4 of Z^T A Z).
 template <int VARIANT, int MODE>
 __global__ void k_apply_red_glk(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
   HELM_PDL_ENTRY();
@@ -520,7 +520,7 @@ __global__ void k_apply_red_glk(Geo g, DVec xv, DVec fv, DVec yv, const double* 
       }
   } else {
     Coef c = coef_at(g, i, j, k[p], 1.0, 0.0);
-    v = cscale(4.0, stencil_apply(g, x, i, j, c));
+    v = stencil_apply(g, x, i, j, c);
   }
   if (MODE == 1) v = csub(cscale(fv.scale(), f[p]), v);
   y[p] = v;

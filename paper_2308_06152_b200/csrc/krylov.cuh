@@ -35,8 +35,6 @@ struct FgmState {
   int its;      // iterations over all cycles
   int done;     // loop finished (converged, breakdown, maxit or basis full)
   int conv;     // converged (relres <= tol or happy breakdown)
-  int reorth;   // this column needs the second Gram-Schmidt pass
-  int nreorth;  // columns that took it
   int maxit, m;
   int cond;     // mirror of the graph conditional (host-loop mode reads it)
   double tol, bnorm, beta, relres, hn, inv_hn, inv_beta;
@@ -736,7 +734,6 @@ __global__ void k_fgm_begin(FgmState* st, const double2* __restrict__ nrm2, int 
   st->beta = beta;
   st->j = 0;
   st->ncols = 0;
-  st->reorth = 0;
   st->inv_hn = 1.0;   // v~_0 = r/||r|| is stored normalised
   g[0] = make_double2(beta, 0.0);
   const double bn = st->bnorm;
@@ -911,7 +908,6 @@ __global__ void k_fgm_reset(FgmState* st, double tol, int maxit, int m) {
   st->its = 0;
   st->conv = 0;
   st->done = 0;
-  st->nreorth = 0;
   st->tol = tol;
   st->maxit = maxit;
   st->m = m;

@@ -100,7 +100,7 @@ def test_coarse_operator_and_vectors(lib, vec, op):
         yo = oracle.apply_coarse_E(x, p.k, p.h, p.bc, op, vec)
         assert rel(y, yo) < OP_TOL, (vec, op, p.shape, p.bc)
         v = random_field(p.shape, 6)
-        zt = oracle.restrict_fw(v, p.bc) if vec == "bilinear" else oracle.restrict_high_order(v, p.bc)
+        zt = oracle.restrict_bilinear_zt(v, p.bc) if vec == "bilinear" else oracle.restrict_high_order(v, p.bc)
         assert rel(H.apply_Zt(gpu(v)).cpu().numpy(), zt) < 1e-14
         z = oracle.prolong_bilinear(x, p.shape, p.bc) if vec == "bilinear" else \
             oracle.prolong_high_order(x, p.shape, p.bc)

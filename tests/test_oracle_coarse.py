@@ -18,13 +18,13 @@ def _A_dense(shape, h, kval, bc):
 
 @pytest.mark.parametrize("bc,shape", [("dirichlet", (7, 11)), ("sommerfeld", (9, 7))])
 def test_galerkin_equals_dense_RAP(bc, shape):
-    """E = I_h^{2h} A_h I_{2h}^h (§3.2.1) with all three factors assembled densely from
-    independent textbook forms (Kronecker sum for A, tensor linear interpolation for Z,
-    Z^T/4 for the restriction)."""
+    """E = I_h^{2h} A_h I_{2h}^h = Z^T A Z (§3.2.1, reading R10) with all three factors assembled
+    densely from independent textbook forms (Kronecker sum for A, tensor linear interpolation
+    for Z, its transpose for the restriction)."""
     h, kval = 1 / 8, 5.0
     Z = np.kron(_interp_1d(shape[0], bc), _interp_1d(shape[1], bc))
     A = _A_dense(shape, h, kval, bc)
-    E = (Z.T / 4) @ A @ Z
+    E = Z.T @ A @ Z
     k = np.full(shape, kval)
     cshape = oracle.coarse_shape(shape, bc)
     Eo = _dense(lambda x: oracle.apply_coarse_E(x, k, h, bc, "galerkin"), cshape)
@@ -33,15 +33,15 @@ def test_galerkin_equals_dense_RAP(bc, shape):
 
 def test_galerkin_tensor_closed_form():
     """For a tensor-product operator the Galerkin coarse operator is the tensor product of
-    1D Galerkin operators.  In 1D (FW/linear) R1 P1 = [1 6 1]/8 and R1 T P1 = [-1 2 -1]/4,
-    so for homogeneous Dirichlet and constant k:
-      E = [ (R1TP1)_y (x) (R1P1)_x + (R1P1)_y (x) (R1TP1)_x ] / h^2 - k^2 (R1P1)_y (x) (R1P1)_x.
-    (Classic result; at H = 2h the interior Laplacian row is [-1 2 -1]/H^2 (x) [1 6 1]/8.)"""
+    1D Galerkin operators.  In 1D (linear interpolation P1 and its transpose) P1^T P1 = [1 6 1]/4
+    and P1^T T P1 = [-1 2 -1]/2, so for homogeneous Dirichlet and constant k:
+      E = [ (P^T T P)_y (x) (P^T P)_x + (P^T P)_y (x) (P^T T P)_x ] / h^2 - k^2 (P^T P)_y (x) (P^T P)_x.
+    (Classic result; at H = 2h the interior Laplacian row is 4 x [-1 2 -1]/H^2 (x) [1 6 1]/8.)"""
     shape, h, kval = (15, 7), 1 / 16, 11.0
     def m1(n):
-        return (6 * np.eye(n) + np.eye(n, k=1) + np.eye(n, k=-1)) / 8
+        return (6 * np.eye(n) + np.eye(n, k=1) + np.eye(n, k=-1)) / 4
     def t1(n):
-        return (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)) / 4
+        return (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)) / 2
     nyc, nxc = oracle.coarse_shape(shape, "dirichlet")
     E = (np.kron(t1(nyc), m1(nxc)) + np.kron(m1(nyc), t1(nxc))) / h**2 - kval**2 * np.kron(m1(nyc), m1(nxc))
     k = np.full(shape, kval)

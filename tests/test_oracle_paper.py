@@ -26,3 +26,15 @@ def test_outer_iterations_match_paper(bc, row):
     assert rep["converged"] and rep["relres"] <= 1e-6
     tol = max(2, int(0.15 * row["outer"] + 0.999))
     assert abs(rep["outer_iterations"] - row["outer"]) <= tol, (rep["outer_iterations"], row)
+
+
+@pytest.mark.parametrize("row", GOLD["tables12_adef1_red_o2"]["rows"], ids=lambda r: f"{r['bc']}-{r['nodes']}")
+def test_red_o2_costs_about_2_5x_str_glk(row):
+    """Tables 1-2: with bilinear vectors the re-discretised ReD-O2 coarse operator needs ~2.5x
+    the str-Glk outer iterations (paper: 21/8, 41/16, 20/9, 26/13).  The oracle must show
+    ReD-O2 >= 2x str-Glk and stay within 30% of the printed ReD-O2 count (reading R10)."""
+    p = mp_problem(float(row["k"]), row["nodes"] - 1, row["bc"])
+    _, rg = oracle.solve(p, oracle.SolverParams(coarse_op="galerkin", inner_solver="direct", maxit=300))
+    _, rr = oracle.solve(p, oracle.SolverParams(coarse_op="red_o2", inner_solver="direct", maxit=300))
+    assert rr["outer_iterations"] >= 2 * rg["outer_iterations"], (rr["outer_iterations"], rg["outer_iterations"])
+    assert abs(rr["outer_iterations"] - row["red_o2"]) <= 0.3 * row["red_o2"] + 1, (rr["outer_iterations"], row)

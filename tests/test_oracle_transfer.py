@@ -62,6 +62,18 @@ def test_restriction_is_quarter_transpose(bc, shape):
     np.testing.assert_array_equal(R, Z.T / 4)
 
 
+@pytest.mark.parametrize("bc,shape", [("dirichlet", (7, 15)), ("sommerfeld", (9, 5)), ("sommerfeld", (5, 5))])
+def test_deflation_restriction_is_transpose(bc, shape):
+    """Reading R10: the deflation restriction is Z^T (Eq. 3.7, (1/2)(u_{2i-1} + 2u_{2i} + u_{2i+1})
+    in each direction) -- exactly the transpose of the bilinear interpolation, 4x Eq. 3.8."""
+    cshape = oracle.coarse_shape(shape, bc)
+    Z = _dense(lambda e: oracle.prolong_bilinear(e, shape, bc), cshape)
+    R = _dense(lambda v: oracle.restrict_bilinear_zt(v, bc), shape)
+    np.testing.assert_array_equal(R, Z.T)
+    one = np.ones(shape, complex)
+    np.testing.assert_allclose(oracle.restrict_bilinear_zt(one, bc)[1:-1, 1:-1], 4.0, atol=1e-15)
+
+
 def test_constant_and_linear_reproduction():
     """Full weighting keeps constants at coarse points whose 9 taps are unknowns
     (weights sum to 1); bilinear interpolation reproduces linear functions."""
