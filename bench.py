@@ -240,6 +240,108 @@ def microbench(peaks, n=16385, reps=10):
     return out
 
 
+def run_decomposed(args, rank, world, local):
+    """Weak scaling of ONE solve over the ranks: the workload's unit square
+    stacked `world` times in y (strip_problem: same h and k, point source at the centre), one
+    row strip per GPU; halos by grouped ncclSend/ncclRecv, dots by ncclAllReduce, the coarse
+    levels below the decomposed ones all-gathered and replicated.  value = world x outer
+    iterations / device time: each outer iteration covers `world` blocks of the N = 1
+    workload, so value / (N x value at N = 1) is the time-per-iteration efficiency."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2308_06152_b200 import helm
+    from workloads import config_problem, strip_problem
+    torch.cuda.set_device(local)
+    peaks = load_peaks()
+    base = config_problem(args.workload)
+    p = strip_problem(base.meta["k"], base.meta["n_cells"], world, f"{args.workload}_x{world}")
+    if world > 1:
+        obj = [helm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = helm.nccl_unique_id()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        H = helm.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, rank, world, nccl_id=uid, params=method_of(args),
+                          stream=stream)
+        bo = np.ascontiguousarray(p.b[H.row0:H.row0 + H.nrows])
+        b = torch.from_numpy(bo).cuda()
+        x = torch.empty_like(b)
+        for _ in range(args.warmup):
+            H.solve(b, 1e-6, args.maxit, x)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        reps = []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        with ClockSampler(local) as clk:
+            for s in range(args.steps):
+                H.helm_flush_l2(256 << 20)
+                ev[s][0].record(stream)
+                _, rep = H.solve(b, 1e-6, args.maxit, x)
+                ev[s][1].record(stream)
+                reps.append(rep)
+            torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        dev_s = sum(a.elapsed_time(b_) for a, b_ in ev) * 1e-3
+        if world > 1:
+            tt = torch.tensor([dev_s], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dev_s = float(tt.item())
+        its = sum(r["outer_iterations"] for r in reps)
+        value = world * its / dev_s
+        bh = torch.from_numpy(bo).pin_memory().numpy()
+        xh = torch.empty(bo.shape, dtype=torch.complex128).pin_memory().numpy()
+        H.solve_host(bh, xh, 1e-6, args.maxit)
+        e2e_t, e2e_its = [], 0
+        for s in range(args.steps):
+            H.helm_flush_l2(256 << 20)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            _, r2 = H.solve_host(bh, xh, 1e-6, args.maxit)
+            e2e_t.append(time.perf_counter() - t0)
+            e2e_its += r2["outer_iterations"]
+        e2e_s = sum(e2e_t)
+        if world > 1:
+            tt = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        launches = sum(r["kernels"] for r in reps)
+        H.close()
+        roof = roof_all = None
+        if rank == 0:   # kernel rooflines at the per-GPU block size (single-GPU context)
+            Hs = helm.helm_setup(base, method_of(args), stream=stream)
+            roof, roof_all = kernel_roofline(Hs, reps[-1], peaks)
+            Hs.close()
+    if rank != 0:
+        return
+    line = {
+        "metric": "fgmres_outer_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
+        "time_to_solution_s": dev_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": p.name, "per_gpu_block": args.workload, **method_of(args), "nx": p.nx, "ny": p.ny,
+                   "h": p.h, "k": p.meta["k"], "tol": 1e-6, "l2": "flushed between timed steps (256 MiB read)",
+                   "outer_iterations": reps[-1]["outer_iterations"],
+                   "inner_iterations_mean": reps[-1]["inner_iterations_total"] / max(1, reps[-1]["inner_solves"]),
+                   "parallelism": f"row-strip decomposition x{world} (NCCL halos + allreduce)",
+                   "value_definition": "world x outer iterations / max-over-ranks device time"},
+        "wall_s": wall,
+        "gpu_launches": launches,
+        "e2e": {"value": world * e2e_its / e2e_s, "unit": "it/s", "h2d_bytes_per_step": int(bo.nbytes) * world,
+                "d2h_bytes_per_step": int(bo.nbytes) * world},
+        "roofline": roof,
+        "roofline_kernels": roof_all,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -256,6 +358,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--decomp", default="auto", choices=["auto", "on", "off"],
+                    help="row-strip decomposed solve over the ranks (NCCL); auto = on when N > 1")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -263,6 +367,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
+    if args.decomp == "on" or (args.decomp == "auto" and world > 1):
+        return run_decomposed(args, rank, world, local)
     import numpy as np
     import torch
     from paper_2308_06152_b200 import helm

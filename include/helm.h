@@ -100,6 +100,11 @@ typedef struct {
   int col_min_n;       /* V-cycle levels with at least this many unknowns use the column-streaming
                           legs (registers + warp shuffles, no shared memory); smaller levels the
                           tiled legs; -1 disables (default 1 << 20) */
+  int dist_levels;     /* decomposed contexts (helm_setup_dist): number of multigrid levels split
+                          into row strips (0 = automatic: every level on which each rank owns at
+                          least dist_min_rows rows, at most all but the coarsest); the levels below
+                          are replicated on every rank.  Must be >= 2 (levels 0 and 1). */
+  int dist_min_rows;   /* fewest rows a rank may own on a decomposed level (default 16, >= 6) */
 } helm_params;
 
 typedef struct {
@@ -190,6 +195,62 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_DCGS 3      /* one delayed-CGS2 step (pass 1, reduction + step A, pass 2 + step B)
                                of the inner FGMRES from column `arg` (arg + reps < inner_maxit) */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
+
+/* ---------------------------------------------------------------------------------------
+ * Row-strip domain decomposition over ranks (DESIGN.md §7; §4, :463-469: the
+ * (i, j)-ordered grid is distributed over processes by blocks with ghost layers, coarsening
+ * stops at a predefined size).  Every rank holds the GLOBAL problem description; level l <= D
+ * is split into nranks contiguous row strips (rank q owns global rows [row0, row0 + nrows) of
+ * level l, see helm_dist_rows), stored with >= 6 ghost rows that are refreshed from the
+ * neighbours before every kernel that reads them; the levels below D are replicated (each rank
+ * completes its copy by an all-gather of the owned rows and runs the rest of the V-cycle and
+ * the dense coarsest solve itself).  Dots and norms are summed over the ranks; every rank then
+ * takes the same scalar steps.  The outer method must be FGMRES; loops are host-polled
+ * (params.graph is forced to 0) and PDL is off.
+ *
+ * Transports:
+ *  HELM_COMM_NCCL    one process per GPU; nccl_id = 128 bytes from helm_nccl_unique_id() on
+ *                    rank 0, broadcast by the caller (e.g. torch.distributed); halos are grouped
+ *                    ncclSend/ncclRecv, dots ncclAllReduce, the all-gather ncclBroadcast per
+ *                    rank.  libnccl.so.2 is loaded at run time (the copy already in the process
+ *                    if any, else $HELM_NCCL_LIB, else the default search path).
+ *  HELM_COMM_THREADS nranks host threads of ONE process sharing one device (group from
+ *                    helm_group_create(nranks)); each thread calls every entry point of its own
+ *                    context in the same order.  Exchanges are device copies from the peers'
+ *                    buffers ordered by CUDA events and host barriers: no kernel waits on
+ *                    another rank, so this is safe on a single GPU.  It exercises the whole
+ *                    decomposed path on one B200 (parity tests).
+ * On a decomposed context helm_apply_A, helm_vcycle (level 0), helm_deflate, helm_solve and
+ * helm_solve_host take and return THIS RANK'S OWNED ROWS of level 0 (nrows * nx values,
+ * contiguous); the other per-level entry points and the benchmarks return HELM_EINVAL.
+ * Errors: setup fails on every rank of a thread group if it fails on one; a rank that fails
+ * later leaves its peers waiting (callers of thread groups must abort the process).
+ * --------------------------------------------------------------------------------------- */
+#define HELM_COMM_THREADS 0
+#define HELM_COMM_NCCL 1
+typedef struct helm_group_s* helm_group;
+int helm_group_create(int nranks, helm_group* out);
+void helm_group_destroy(helm_group g);
+int helm_nccl_unique_id(unsigned char id[128]);
+
+typedef struct {
+  int kind;                     /* HELM_COMM_* */
+  int rank, nranks;             /* 0 <= rank < nranks <= 16 */
+  helm_group group;             /* HELM_COMM_THREADS */
+  const unsigned char* nccl_id; /* HELM_COMM_NCCL: 128 bytes, identical on every rank */
+} helm_dist;
+
+/* As helm_setup, on the global grid and the global k (nx*ny, host or device), for rank
+ * dist->rank of a decomposed solve.  Collective: every rank must call it. */
+int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k_on_device,
+                    const helm_params* params, void* stream, const helm_dist* dist);
+/* Global rows [*row0, *row0 + *nrows) of `level` owned by this rank (single-GPU context: all). */
+int helm_dist_rows(helm_ctx ctx, int level, int* row0, int* nrows);
+/* Host-only plan of the decomposition (no device needed): returns the number of levels L
+ * (or a negative error), *D = deepest decomposed level, and table[(l * nranks + q) * 4 + i]
+ * = {owned row begin, owned row end, stored row begin, stored row end} for l < min(L, cap). */
+int helm_dist_plan(const helm_grid* grid, const helm_params* params, int nranks, int* D, int* table,
+                   int cap_levels);
 
 const char* helm_last_error(void);
 const char* helm_build_info(void);

@@ -15,7 +15,7 @@ DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+    "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-ldl", "-lpthread",
 ]
 
 

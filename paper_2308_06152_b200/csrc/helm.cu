@@ -19,6 +19,7 @@
 
 #include "../../include/helm.h"
 #include "kernels.cuh"
+#include "dist.cuh"
 #include "krylov.cuh"
 #include "vcycle.cuh"
 
@@ -61,12 +62,21 @@ struct Level {
   double2* u = nullptr;  // solution when reached by recursion
   double2* s = nullptr;  // scratch (pre-smoothed iterate)
   double2* t = nullptr;  // scratch (residual / correction)
+  // row-strip decomposition (dist.cuh): block = 1 if this rank stores only its row block
+  int block = 0;
+  int own0 = 0, nown = 0;  // owned rows [own0, own0 + nown) of the stored array
+  int row0 = 0;            // global row of stored row 0
+  int gny = 0;             // global rows of the level
+  double2 *hs_up = nullptr, *hs_dn = nullptr, *hr_up = nullptr, *hr_dn = nullptr;  // halo staging
 };
 
 // One device-resident FGMRES instance (basis, Hessenberg, rotations, state).
 struct Fgm {
   int m = 0;
-  size_t n = 0;
+  size_t n = 0;              // owned length (dots, norms, updates run over [off, off + n))
+  size_t ld = 0;             // stored length of a basis vector (block rows incl. ghosts)
+  size_t off = 0;            // offset of the owned rows in a stored vector
+  bool dist = false;         // dots are summed over the ranks
   double2* V = nullptr;      // (m+1) x n
   double2* Z = nullptr;      // m x n
   double2* H = nullptr;      // (m+1) x m, column-major
@@ -123,6 +133,15 @@ struct helm_ctx_s {
   long long body_launches[4] = {0, 0, 0, 0};
   long long cnt_top = 0, cnt_outer = 0, cnt_inner = 0;
   long long cnt[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  // row-strip decomposition over ranks (dist.cuh); dist == 0: single GPU
+  int dist = 0, kind = -1, rank = 0, nranks = 1, D = -1;
+  std::vector<DistRows> plan;          // plan[l * nranks + q]
+  helm_group_s* grp = nullptr;
+  ncclComm_t nccl = nullptr;
+  const NcclApi* api = nullptr;
+  cudaEvent_t dev_ev = nullptr;
+  double2* red = nullptr;              // allreduce staging (thread groups)
+  size_t red_cap = 0;
 };
 
 namespace {
@@ -210,6 +229,19 @@ int coarse_n(int n, int bc) {
   return bc == BC_DIRICHLET ? (n - 1) / 2 : (n + 1) / 2;
 }
 
+// (nx, ny) of every level: coarsen while both directions allow it, up to max_levels, stopping
+// at the first level with at most coarsest_n unknowns (reading R7)
+void hierarchy_sizes(const helm_grid& grid, const helm_params& p, std::vector<std::pair<int, int>>& sz) {
+  sz.assign(1, {grid.nx, grid.ny});
+  while ((int)sz.size() < p.max_levels) {
+    const auto f = sz.back();
+    if (p.coarsest_n > 0 && (long long)f.first * f.second <= p.coarsest_n) break;
+    const int cx = coarse_n(f.first, grid.bc), cy = coarse_n(f.second, grid.bc);
+    if (cx < 0 || cy < 0) break;
+    sz.push_back({cx, cy});
+  }
+}
+
 template <class T>
 int dalloc(T** p, size_t count) {
   if (count == 0) count = 1;
@@ -219,8 +251,141 @@ int dalloc(T** p, size_t count) {
 
 bool fused_vcycle(const helm_ctx_s& C) { return C.p.nu_pre == 1 && C.p.nu_post == 1; }
 
+// ------------------------------------------------------------------ row-strip decomposition
+DVec shift(DVec v, size_t off) {
+  if (v.p) v.p += off;
+  return v;
+}
+
+const DistRows& prow(const helm_ctx_s& C, int l, int q) { return C.plan[(size_t)l * C.nranks + q]; }
+
+#define NCK(call)                                                                                          \
+  do {                                                                                                     \
+    ncclResult_t r_ = (call);                                                                              \
+    if (r_ != ncclSuccess) return fail(HELM_ECUDA, "%s: %s", #call, C.api->GetErrorString(r_));            \
+  } while (0)
+
+// Thread group: every rank's stream waits for all work the other ranks enqueued before this
+// point (event per rank, host barriers so that no event is re-recorded before all waits).
+int dist_sync(helm_ctx_s& C) {
+  helm_group_s* g = C.grp;
+  CK(cudaEventRecord(C.dev_ev, C.s));
+  g->bar.wait();
+  for (int q = 0; q < C.nranks; ++q)
+    if (q != C.rank) CK(cudaStreamWaitEvent(C.s, g->rank[q].ev, 0));
+  g->bar.wait();
+  return HELM_OK;
+}
+
+// In-place sum over the ranks of n complex values (the same bits on every rank).
+int allreduce(helm_ctx_s& C, double2* buf, int n) {
+  if (!C.dist || C.nranks == 1) return HELM_OK;
+  if (C.kind == HELM_COMM_NCCL) {
+    NCK(C.api->AllReduce(buf, buf, 2 * (size_t)n, ncclFloat64, ncclSum, C.nccl, C.s));
+    return HELM_OK;
+  }
+  if ((size_t)n > C.red_cap) return fail(HELM_EINVAL, "allreduce of %d values exceeds the staging buffer", n);
+  CK(cudaMemcpyAsync(C.red, buf, (size_t)n * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
+  CKR(dist_sync(C));
+  PeerPtrs pp{};
+  for (int q = 0; q < C.nranks; ++q) pp.p[q] = C.grp->rank[q].red;
+  launch_k(C, k_sum_ranks, (n + 255) / 256, 256, 0, pp, C.nranks, n, buf);
+  CKR(post_launch(C));
+  return dist_sync(C);
+}
+
+// Refresh the GHOST rows on each side of this rank's owned rows of x (a level-l block) from
+// the neighbouring ranks.  No-op on replicated levels and on one rank.
+int halo(helm_ctx_s& C, int l, DVec x) {
+  if (!C.dist || C.nranks == 1 || !C.L[l].block) return HELM_OK;
+  const Level& L = C.L[l];
+  const int nx = L.g.nx;
+  const int up = C.rank > 0, dn = C.rank < C.nranks - 1;
+  const int n = GHOST * nx;
+  const int grid = std::max(1, std::min((n + 255) / 256, C.sm_count * 4));
+  launch_k(C, k_halo_pack, grid, 256, 0, x, nx, L.own0, L.nown, up, dn, L.hs_up, L.hs_dn);
+  CKR(post_launch(C));
+  const double2* src_up = nullptr;
+  const double2* src_dn = nullptr;
+  if (C.kind == HELM_COMM_NCCL) {
+    const size_t cnt = 2 * (size_t)n;
+    NCK(C.api->GroupStart());
+    if (up) {
+      NCK(C.api->Send(L.hs_up, cnt, ncclFloat64, C.rank - 1, C.nccl, C.s));
+      NCK(C.api->Recv(L.hr_up, cnt, ncclFloat64, C.rank - 1, C.nccl, C.s));
+    }
+    if (dn) {
+      NCK(C.api->Send(L.hs_dn, cnt, ncclFloat64, C.rank + 1, C.nccl, C.s));
+      NCK(C.api->Recv(L.hr_dn, cnt, ncclFloat64, C.rank + 1, C.nccl, C.s));
+    }
+    NCK(C.api->GroupEnd());
+    src_up = L.hr_up;
+    src_dn = L.hr_dn;
+  } else {
+    CKR(dist_sync(C));
+    if (up) src_up = C.grp->rank[C.rank - 1].send_dn[l];
+    if (dn) src_dn = C.grp->rank[C.rank + 1].send_up[l];
+  }
+  launch_k(C, k_halo_unpack, grid, 256, 0, x, nx, L.own0, L.nown, up, dn, src_up, src_dn);
+  CKR(post_launch(C));
+  if (C.kind != HELM_COMM_NCCL) CKR(dist_sync(C));   // peers done reading our send buffers
+  return HELM_OK;
+}
+
+// Complete the replicas of a replicated level's f: every rank contributes its owned rows.
+int allgather(helm_ctx_s& C, int l) {
+  if (!C.dist || C.nranks == 1) return HELM_OK;
+  Level& L = C.L[l];
+  const size_t nx = (size_t)L.g.nx;
+  if (C.kind == HELM_COMM_NCCL) {
+    NCK(C.api->GroupStart());
+    for (int q = 0; q < C.nranks; ++q) {
+      const DistRows& r = prow(C, l, q);
+      if (r.b > r.a)
+        NCK(C.api->Broadcast(L.f + r.a * nx, L.f + r.a * nx, 2 * (size_t)(r.b - r.a) * nx, ncclFloat64, q, C.nccl,
+                             C.s));
+    }
+    NCK(C.api->GroupEnd());
+    return HELM_OK;
+  }
+  CKR(dist_sync(C));
+  for (int q = 0; q < C.nranks; ++q) {
+    const DistRows& r = prow(C, l, q);
+    if (q == C.rank || r.b <= r.a) continue;
+    CK(cudaMemcpyAsync(L.f + r.a * nx, C.grp->rank[q].gathered[l] + r.a * nx, (size_t)(r.b - r.a) * nx * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, C.s));
+  }
+  return dist_sync(C);
+}
+
+// Level l + 1 as the transfer kernels of level l see it: on a decomposed context, the coarse
+// window of this rank's level-l block (a row range of the stored level l + 1: its block, or
+// the replica when l + 1 is replicated).
+Level coarse_of(const helm_ctx_s& C, int l) {
+  Level G = C.L[l + 1];
+  if (!C.dist || !C.L[l].block) return G;
+  const Level& F = C.L[l];
+  int ws, we;
+  coarse_window(F.row0, F.row0 + F.g.ny, F.g.bc == BC_DIRICHLET, ws, we);
+  const size_t off = (size_t)(ws - G.row0) * G.g.nx;
+  G.g.ny = we - ws;
+  G.n = (size_t)G.g.nx * G.g.ny;
+  G.k += off;
+  if (G.f) G.f += off;
+  if (G.u) G.u += off;
+  if (G.s) G.s += off;
+  if (G.t) G.t += off;
+  G.own0 -= ws - G.row0;
+  G.row0 = ws;
+  return G;
+}
+
+bool gathers(const helm_ctx_s& C, int l) { return C.dist && C.L[l].block && !C.L[l + 1].block; }
+
 // ------------------------------------------------------------------ operator launches
-int op_apply(helm_ctx_s& C, const Level& L, DVec u, DVec f, DVec y, double sr, double si) {
+int op_apply(helm_ctx_s& C, int l, DVec u, DVec f, DVec y, double sr, double si) {
+  const Level& L = C.L[l];
+  CKR(halo(C, l, u));
   const unsigned blocks = (unsigned)((L.n + 255) / 256);
   if (f.p) launch_k(C, k_apply_op<1>, blocks, 256, 0, L.g, u, f, y, L.k, sr, si);
   else launch_k(C, k_apply_op<0>, blocks, 256, 0, L.g, u, DVec(), y, L.k, sr, si);
@@ -229,23 +394,31 @@ int op_apply(helm_ctx_s& C, const Level& L, DVec u, DVec f, DVec y, double sr, d
 
 int restrict_(helm_ctx_s& C, int l, const double2* v, double2* vc) {
   const Level& F = C.L[l];
-  const Level& G = C.L[l + 1];
+  const Level G = coarse_of(C, l);
+  CKR(halo(C, l, DVec(v)));
   launch_k(C, k_restrict, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, v, vc);
   return post_launch(C);
 }
 
 int prolong_(helm_ctx_s& C, int l, const double2* e, const double2* base, DVec y, const double2* addq) {
   const Level& F = C.L[l];
-  const Level& G = C.L[l + 1];
+  const Level G = coarse_of(C, l);   // e: the coarse window (callers refresh its halo)
   if (base) launch_k(C, k_prolong<1>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, base, y, addq);
   else launch_k(C, k_prolong<0>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, nullptr, y, addq);
   return post_launch(C);
 }
 
 // Deflation vectors level 0 <-> level 1 (bilinear: R=1, high order: R=2)
+// offset (elements) of coarse_of(C, l) in the stored arrays of level l + 1
+size_t win_off(const helm_ctx_s& C, int l) {
+  return (size_t)(coarse_of(C, l).row0 - C.L[l + 1].row0) * C.L[l + 1].g.nx;
+}
+
 int defl_restrict(helm_ctx_s& C, DVec v, double2* vc) {
   const Level& F = C.L[0];
-  const Level& G = C.L[1];
+  const Level G = coarse_of(C, 0);
+  CKR(halo(C, 0, v));
+  vc += win_off(C, 0);
   if (C.p.vectors == HELM_VECTORS_BILINEAR)
     launch_k(C, k_restrict_z<1>, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, v, vc);
   else
@@ -255,7 +428,9 @@ int defl_restrict(helm_ctx_s& C, DVec v, double2* vc) {
 
 int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
   const Level& F = C.L[0];
-  const Level& G = C.L[1];
+  const Level G = coarse_of(C, 0);
+  CKR(halo(C, 1, DVec(e)));
+  e += win_off(C, 0);
   if (C.p.vectors == HELM_VECTORS_BILINEAR)
     launch_k(C, k_prolong_z<1, 0>, grd2d(F.g.nx, F.g.ny), blk2d(), 0, F.g, G.g, F.o, e, nullptr, y);
   else
@@ -270,16 +445,24 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
   const Level& G = C.L[1];
   const dim3 gg = grd2d(G.g.nx, G.g.ny);
   const bool res = f.p != nullptr;
+  CKR(halo(C, 1, x));
   switch (C.p.coarse_op) {
     case HELM_COARSE_GALERKIN: {
+      // on a decomposed context: the coarse window of the level-0 block (contains the owned
+      // rows of level 1 and the 2 rows the operator reads around them)
       const Level& F = C.L[0];
-      const dim3 gt((G.g.nx + GLK_TX - 1) / GLK_TX, (G.g.ny + GLK_TY - 1) / GLK_TY);
+      const Level Gw = coarse_of(C, 0);
+      const size_t wo = win_off(C, 0);
+      x = shift(x, wo);
+      f = shift(f, wo);
+      y = shift(y, wo);
+      const dim3 gt((Gw.g.nx + GLK_TX - 1) / GLK_TX, (Gw.g.ny + GLK_TY - 1) / GLK_TY);
       if (C.p.vectors == HELM_VECTORS_BILINEAR) {
-        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
-        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
+        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
       } else {
-        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
-        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
+        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
       }
       return post_launch(C);
     }
@@ -292,7 +475,7 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       else launch_k(C, k_apply_red_glk<2, 0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_O2:
-      return op_apply(C, G, x, f, y, 1.0, 0.0);
+      return op_apply(C, 1, x, f, y, 1.0, 0.0);
     case HELM_COARSE_RED_O4:
       if (res) launch_k(C, k_apply_red_o4<1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       else launch_k(C, k_apply_red_o4<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
@@ -329,14 +512,21 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
     launch_k(C, k_gemv, (n * 32 + 255) / 256, 256, 0, C.Minv, n, f, u_out, addq);
     return post_launch(C);
   }
-  Level& G = C.L[l + 1];
+  // G: the coarse level as the transfer kernels see it (a window of the replica when level
+  // l + 1 is replicated and l is decomposed); the recursion runs on the stored level
+  const Level G = coarse_of(C, l);
+  Level& Gs = C.L[l + 1];
+  const bool gather = gathers(C, l);
+  CKR(halo(C, l, f));
   if (fused_vcycle(C) && C.p.col_min_n >= 0 && (long long)L.n >= C.p.col_min_n) {
     // large levels: column-streaming legs (no shared-memory staging)
     const int wcols = (L.g.nx + COL_OWN - 1) / COL_OWN;
     const dim3 gc((wcols + 3) / 4, (L.g.ny + COL_SEG - 1) / COL_SEG);
     launch_k(C, k_vc_down_col, gc, 128, 0, L.g, G.g, L.o, f, (const double*)L.k, sr, si, w, L.s, G.f);
     CKR(post_launch(C));
-    CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
+    if (gather) CKR(allgather(C, l + 1));
+    CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
+    CKR(halo(C, l + 1, DVec(Gs.u)));
     launch_k(C, k_vc_up_col, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f,
              (const double*)L.k, sr, si, w, addq, u_out);
     return post_launch(C);
@@ -352,7 +542,9 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
       launch_k(C, k_vc_down<DOWN_TX, DOWN_TY>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
     }
     CKR(post_launch(C));
-    CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
+    if (gather) CKR(allgather(C, l + 1));
+    CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
+    CKR(halo(C, l + 1, DVec(Gs.u)));
     if (small) {
       dim3 gu((L.g.nx + 15) / 16, (L.g.ny + 7) / 8);
       launch_k(C, k_vc_up<16, 8>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
@@ -368,14 +560,17 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   CKR(post_launch(C));
   for (int sw = 1; sw < C.p.nu_pre; ++sw) {
     double2* nxt = (cur == L.s) ? L.t : L.s;
+    CKR(halo(C, l, DVec(cur)));
     launch_k(C, k_jacobi, grd2d(L.g.nx, L.g.ny), blk2d(), 0, L.g, cur, f, DVec(nxt), L.k, sr, si, w, nullptr);
     CKR(post_launch(C));
     cur = nxt;
   }
   double2* ob = (cur == L.s) ? L.t : L.s;
-  CKR(op_apply(C, L, DVec(cur), f, DVec(ob), sr, si));
+  CKR(op_apply(C, l, DVec(cur), f, DVec(ob), sr, si));
   CKR(restrict_(C, l, ob, G.f));
-  CKR(vcycle(C, l + 1, DVec(G.f), DVec(G.u), nullptr));
+  if (gather) CKR(allgather(C, l + 1));
+  CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
+  CKR(halo(C, l + 1, DVec(Gs.u)));
   const int np = C.p.nu_post;
   if (np == 0) return prolong_(C, l, G.u, cur, u_out, addq);
   CKR(prolong_(C, l, G.u, cur, DVec(ob), nullptr));
@@ -383,6 +578,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   for (int sw = 0; sw < np; ++sw) {
     const bool lastsw = (sw == np - 1);
     DVec dst = lastsw ? u_out : DVec((src == ob) ? cur : ob);
+    CKR(halo(C, l, DVec(src)));
     launch_k(C, k_jacobi, grd2d(L.g.nx, L.g.ny), blk2d(), 0, L.g, src, f, dst, L.k, sr, si, w, lastsw ? addq : nullptr);
     CKR(post_launch(C));
     src = dst.p;
@@ -407,11 +603,19 @@ int raise_dyn_smem(const void* func, size_t need) {
   return HELM_OK;
 }
 
-int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
+// n: owned length; ld: stored length of a basis vector; off: owned offset; dist: rank-summed dots
+int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, bool dist) {
   K.m = m;
   K.n = n;
-  CKR(dalloc(&K.V, (size_t)(m + 1) * n));
-  CKR(dalloc(&K.Z, (size_t)m * n));
+  K.ld = ld;
+  K.off = off;
+  K.dist = dist;
+  CKR(dalloc(&K.V, (size_t)(m + 1) * ld));
+  CKR(dalloc(&K.Z, (size_t)m * ld));
+  if (dist) {   // ghost rows are read by the operators before any halo fills them: keep them finite
+    CK(cudaMemsetAsync(K.V, 0, (size_t)(m + 1) * ld * sizeof(double2), C.s));
+    CK(cudaMemsetAsync(K.Z, 0, (size_t)m * ld * sizeof(double2), C.s));
+  }
   CKR(dalloc(&K.H, (size_t)(m + 1) * m));
   CKR(dalloc(&K.g, (size_t)m + 1));
   CKR(dalloc(&K.sn, (size_t)m));
@@ -437,6 +641,8 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_stepA, asmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_stepB, usmem));
   {
     // pass 2 in one wave: at most as many blocks as can be resident
     int bps = 0;
@@ -445,7 +651,7 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n) {
   }
   // cooperative one-kernel step for small vectors (latency-bound regime)
   K.coop = 0;
-  if (C.p.coop && n <= ((size_t)1 << 22)) {
+  if (C.p.coop && !dist && n <= ((size_t)1 << 22)) {
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_step, DC_THREADS, asmem));
     if (bps > 0) {
@@ -481,12 +687,14 @@ void fgm_free(Fgm& K) {
 int gs_dots(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, DVec w, int want_norm,
             double2* out, const int* gate) {
   const GsGeom& g = K.geo;
-  launch_k(C, k_gs_dots, dim3(g.gx, g.gy), GS_THREADS, 0, V, (long long)K.n, nptr, nadd, w, (long long)K.n, g.chunk,
+  launch_k(C, k_gs_dots, dim3(g.gx, g.gy), GS_THREADS, 0, V, (long long)K.ld, nptr, nadd, w, (long long)K.n, g.chunk,
                                                         want_norm, K.part, gate);
   CKR(post_launch(C));
   const int maxout = K.m + 2;
   launch_k(C, k_gs_reduce, (maxout * 32 + 255) / 256, 256, 0, K.part, g.gx, nptr, nadd, 1, want_norm ? 1 : 0, out, gate);
-  return post_launch(C);
+  CKR(post_launch(C));
+  if (K.dist) CKR(allreduce(C, out, nptr ? maxout : nadd + (want_norm ? 1 : 0)));
+  return HELM_OK;
 }
 
 // w_out = w_in + sign * V coeff; with want_norm the per-block |w_out|^2 partials are left in
@@ -494,7 +702,7 @@ int gs_dots(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, 
 int gs_update(helm_ctx_s& C, Fgm& K, const double2* V, const int* nptr, int nadd, const double2* coeff, double sign,
               DVec win, DVec wout, int want_norm, const int* gate) {
   const size_t smem = (size_t)(K.m + 2) * sizeof(double2);
-  launch_k(C, k_gs_update, K.geo.gu, GS_THREADS, smem, V, (long long)K.n, nptr, nadd, coeff, sign, win, wout,
+  launch_k(C, k_gs_update, K.geo.gu, GS_THREADS, smem, V, (long long)K.ld, nptr, nadd, coeff, sign, win, wout,
                                                     (long long)K.n, want_norm, K.part, gate);
   return post_launch(C);
 }
@@ -559,56 +767,77 @@ int run_while(helm_ctx_s& C, FgmState* st, Begin&& begin, Body&& body) {
 
 template <class OpA, class OpP>
 int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x, bool first, FgmState* outer_stats) {
-  const size_t n = K.n;
+  // vectors are stored with length K.ld (a rank's row block incl. ghost rows); the operators get
+  // whole stored vectors, the Krylov kernels the owned rows [off, off + n)
+  const size_t n = K.n, off = K.off;
+  const long long ld = (long long)K.ld, ln = (long long)n;
+  double2* Vo = K.V + off;
   FgmState* st = K.st;
   auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     if (first) {
-      CKR(gs_dots(C, K, nullptr, nullptr, 0, b, 1, K.nrm, nullptr));
+      CKR(gs_dots(C, K, nullptr, nullptr, 0, shift(b, off), 1, K.nrm, nullptr));
       launch_k(C, k_fgm_begin, 1, 32, 0, st, K.nrm, 1, K.g, h, use_h);
       CKR(post_launch(C));
-      launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, b, &st->inv_beta, DVec(K.V), (long long)n, nullptr);
+      launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, shift(b, off), &st->inv_beta, DVec(Vo), ln, nullptr);
       return post_launch(C);
     }
     CKR(opA(DVec(x), b, DVec(K.V)));
-    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(K.V), 1, K.nrm, nullptr));
+    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(Vo), 1, K.nrm, nullptr));
     launch_k(C, k_fgm_begin, 1, 32, 0, st, K.nrm, 0, K.g, h, use_h);
     CKR(post_launch(C));
-    launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, DVec(K.V), &st->inv_beta, DVec(K.V), (long long)n, nullptr);
+    launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, DVec(Vo), &st->inv_beta, DVec(Vo), ln, nullptr);
     return post_launch(C);
   };
   auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
-    const long long ln = (long long)n;
     // v~_j is consumed through the scale 1/h_{j,j-1} left by the previous step B (no
     // normalisation pass); pass 2 writes the final v_j over it
-    DVec vj(K.V, &st->j, ln, &st->inv_hn), zj(K.Z, &st->j, ln), w(K.V + n, &st->j, ln);
+    DVec vj(K.V, &st->j, ld, &st->inv_hn), zj(K.Z, &st->j, ld), w(K.V + K.ld, &st->j, ld);
     CKR(opP(vj, zj));
     CKR(opA(zj, DVec(), w));
+    const DVec vjo = shift(vj, off), wo = shift(w, off);
     // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
     const GsGeom& gg = K.geo;
     const size_t asm_ = dcgs_smem(K.m);
     if (K.coop > 0) {
       // the whole step in one cooperative kernel (grid-wide barriers between its phases)
-      launch_coop(C, k_dcgs_step, K.coop, DC_THREADS, asm_, (const double2*)K.V, ln, st, vj, w, ln, gg.chunk, gg.gx,
+      launch_coop(C, k_dcgs_step, K.coop, DC_THREADS, asm_, (const double2*)Vo, ld, st, vjo, wo, ln, gg.chunk, gg.gx,
                   gg.gy, K.part, K.npart, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, h, use_h);
-    } else {
-      launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, &st->j, 1, vj, w, ln,
-               gg.chunk, K.part);
-      CKR(post_launch(C));
-      // reduction of the pass-1 partials + step A (last block), pass 2 + step B (last block)
-      launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H,
-               K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.cnt);
-      CKR(post_launch(C));
-      launch_k(C, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
-               (const double2*)K.coef, (const double2*)K.sc2, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g,
-               (const double2*)K.dots1, K.rawc, K.cnt + 1, h, use_h);
+      return post_launch(C);
     }
-    return post_launch(C);
+    launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
+             gg.chunk, K.part);
+    CKR(post_launch(C));
+    // reduction of the pass-1 partials + step A (last block), pass 2 + step B (last block);
+    // decomposed: the per-rank sums are summed over the ranks before each step
+    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H,
+             K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.dist ? nullptr : K.cnt);
+    CKR(post_launch(C));
+    if (K.dist) {
+      CKR(allreduce(C, K.dots1, 2 * K.m + 2));
+      launch_k(C, k_dcgs_stepA, 1, 32, asm_, st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1, K.coef, K.sc2,
+               K.rawc);
+      CKR(post_launch(C));
+    }
+    launch_k(C, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), Vo, ld, (const int*)&st->j,
+             (const double2*)K.coef, (const double2*)K.sc2, vjo, wo, ln, K.part, K.dist ? nullptr : st, K.H, K.cs,
+             K.sn, K.g, (const double2*)K.dots1, K.rawc, K.cnt + 1, h, use_h);
+    CKR(post_launch(C));
+    if (K.dist) {
+      launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu, K.nrm);
+      CKR(post_launch(C));
+      CKR(allreduce(C, K.nrm, 1));
+      launch_k(C, k_dcgs_stepB, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
+               (const double2*)K.sc2, (const double2*)K.nrm, 1, K.rawc, h, use_h);
+      CKR(post_launch(C));
+    }
+    return HELM_OK;
   };
   CKR(run_while(C, st, begin, body));
   launch_k(C, k_fgm_backsub, 1, 32, 0, st, K.H, K.g, K.y, outer_stats);
   CKR(post_launch(C));
   // x = (x or 0) + Z y
-  return gs_update(C, K, K.Z, &st->ncols, 0, K.y, 1.0, first ? DVec() : DVec(x), DVec(x), 0, nullptr);
+  const DVec xo = shift(DVec(x), off);
+  return gs_update(C, K, K.Z + off, &st->ncols, 0, K.y, 1.0, first ? DVec() : xo, xo, 0, nullptr);
 }
 
 // e = E^{-1} c on level 1 by CSLP(V-cycle from level 1)-preconditioned FGMRES from e = 0
@@ -628,7 +857,7 @@ int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
   CKR(defl_restrict(C, v, C.cc));                              // v1 = I_h^{2h} v
   CKR(coarse_solve(C, C.cc, C.ce, outer_stats));               // v2 = A_{2h}^{-1} v1
   CKR(defl_prolong(C, C.ce, C.dq));                            // v' = I_{2h}^h v2  (= Q v)
-  CKR(op_apply(C, F, DVec(C.dq), v, DVec(C.dt), 1.0, 0.0));    // t = v - A Q v  (= P_h v)
+  CKR(op_apply(C, 0, DVec(C.dq), v, DVec(C.dt), 1.0, 0.0));    // t = v - A Q v  (= P_h v)
   return vcycle(C, 0, DVec(C.dt), z, C.dq);                    // z = M^{-1} t + Q v
 }
 
@@ -651,7 +880,7 @@ int gcr_cycle(helm_ctx_s& C, bool first) {
   auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     DVec zj(K.Z, &st->j, ln), cj(K.V, &st->j, ln);
     CKR(adef1(C, DVec(C.rbuf), zj, C.outer.st));               // z_j = P r
-    CKR(op_apply(C, F, zj, DVec(), cj, 1.0, 0.0));             // c_j = A z_j
+    CKR(op_apply(C, 0, zj, DVec(), cj, 1.0, 0.0));             // c_j = A z_j
     for (int pass = 0; pass < 2; ++pass) {                     // CGS2, same coefficients on z_j
       double2* al = pass == 0 ? K.dots1 : K.coef;
       CKR(gs_dots(C, K, K.V, &st->j, 0, cj, 0, al, nullptr));
@@ -674,7 +903,7 @@ int gcr_cycle(helm_ctx_s& C, bool first) {
 int outer_cycle(helm_ctx_s& C, bool first) {
   if (C.p.outer == HELM_OUTER_GCR) return gcr_cycle(C, first);
   Level& F = C.L[0];
-  auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, F, x, f, y, 1.0, 0.0); };
+  auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, 0, x, f, y, 1.0, 0.0); };
   auto opP = [&](DVec v, DVec z) { return adef1(C, v, z, C.outer.st); };
   return fgmres_cycle(C, C.outer, opA, opP, DVec(C.bbuf), C.xbuf, first, nullptr);
 }
@@ -692,8 +921,12 @@ int ensure_outer(helm_ctx_s& C, int maxit) {
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
   const size_t per = 2 * C.L[0].n * sizeof(double2);
-  m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), fr / 2 / per));
-  return fgm_alloc(C, C.outer, m, C.L[0].n);
+  // decomposed: every rank must size the basis alike (the rank-summed dots and the restart
+  // points depend on it), so the cap comes from the total, not the free, memory
+  const size_t budget = C.dist ? tot / 4 : fr / 2;
+  m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), budget / per));
+  const Level& F = C.L[0];
+  return fgm_alloc(C, C.outer, m, (size_t)F.nown * F.g.nx, F.n, (size_t)F.own0 * F.g.nx, C.dist && C.nranks > 1);
 }
 
 }  // namespace
@@ -722,6 +955,8 @@ void helm_default_params(helm_params* p) {
   p->outer = HELM_OUTER_FGMRES;
   p->col_min_n = 1 << 20;
   p->pdl = 1;
+  p->dist_levels = 0;
+  p->dist_min_rows = 16;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -738,7 +973,14 @@ static void destroy_ctx(helm_ctx_s* C) {
     cudaFree(L.u);
     cudaFree(L.s);
     cudaFree(L.t);
+    cudaFree(L.hs_up);
+    cudaFree(L.hs_dn);
+    cudaFree(L.hr_up);
+    cudaFree(L.hr_dn);
   }
+  cudaFree(C->red);
+  if (C->dev_ev) cudaEventDestroy(C->dev_ev);
+  if (C->nccl && C->api) C->api->CommDestroy(C->nccl);
   cudaFree(C->dlev);
   cudaFree(C->Minv);
   cudaFree(C->dq);
@@ -788,26 +1030,51 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   C.s = C.user;
   CK(cudaMallocHost((void**)&C.hst, sizeof(FgmState)));
   // hierarchy (reading R7)
-  Level L0;
-  L0.g = Geo{grid->nx, grid->ny, grid->h, grid->bc};
-  L0.o = grid->bc == HELM_BC_DIRICHLET ? 1 : 0;
-  L0.n = (size_t)grid->nx * grid->ny;
-  C.L.push_back(L0);
-  while ((int)C.L.size() < p.max_levels) {
-    const Level& F = C.L.back();
-    if (p.coarsest_n > 0 && (long long)F.n <= p.coarsest_n) break;   // predefined coarsest size (R7)
-    int cx = coarse_n(F.g.nx, F.g.bc), cy = coarse_n(F.g.ny, F.g.bc);
-    if (cx < 0 || cy < 0) break;
-    Level G;
-    G.g = Geo{cx, cy, 2.0 * F.g.h, F.g.bc};
-    G.o = F.o;
-    G.n = (size_t)cx * cy;
-    C.L.push_back(G);
+  {
+    std::vector<std::pair<int, int>> sz;
+    hierarchy_sizes(*grid, p, sz);
+    double h = grid->h;
+    for (const auto& s : sz) {
+      Level Lv;
+      Lv.g = Geo{s.first, s.second, h, grid->bc};
+      Lv.o = grid->bc == HELM_BC_DIRICHLET ? 1 : 0;
+      Lv.n = (size_t)s.first * s.second;
+      Lv.gny = s.second;
+      C.L.push_back(Lv);
+      h *= 2.0;
+    }
   }
   if (C.L.size() < 2) return fail(HELM_ESHAPE, "fine grid %dx%d is not coarsenable", grid->nx, grid->ny);
   const Level& Cst = C.L.back();
   if ((long long)Cst.n > p.max_coarsest)
     return fail(HELM_ESHAPE, "coarsest grid %dx%d exceeds max_coarsest=%d", Cst.g.nx, Cst.g.ny, p.max_coarsest);
+  for (auto& Lv : C.L) {
+    Lv.own0 = 0;
+    Lv.nown = Lv.g.ny;
+  }
+  std::vector<Geo> gglob;   // global geometry of every level
+  for (const auto& Lv : C.L) gglob.push_back(Lv.g);
+  if (C.dist) {
+    // row-strip decomposition (dist.cuh): levels 0..D become this rank's row blocks
+    std::vector<int> nys;
+    for (const auto& Lv : C.L) nys.push_back(Lv.g.ny);
+    std::string why;
+    C.D = dist_plan(nys, grid->bc == HELM_BC_DIRICHLET, C.nranks, p.dist_min_rows, p.dist_levels, C.plan, why);
+    if (C.D < 0) return fail(HELM_ESHAPE, "decomposition: %s", why.c_str());
+    for (int l = 0; l < (int)C.L.size(); ++l) {
+      Level& Lv = C.L[l];
+      const DistRows& r = prow(C, l, C.rank);
+      Lv.own0 = r.a;
+      Lv.nown = r.b - r.a;
+      if (l <= C.D) {
+        Lv.block = 1;
+        Lv.row0 = r.s;
+        Lv.own0 = r.a - r.s;
+        Lv.g.ny = r.e - r.s;
+        Lv.n = (size_t)Lv.g.nx * Lv.g.ny;
+      }
+    }
+  }
   for (size_t l = 0; l < C.L.size(); ++l) {
     Level& Lv = C.L[l];
     CKR(dalloc(&Lv.k, Lv.n));
@@ -817,14 +1084,45 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
       CKR(dalloc(&Lv.f, Lv.n));
       CKR(dalloc(&Lv.u, Lv.n));
     }
+    if (C.dist) {   // rows no rank writes stay finite
+      for (double2* b : {Lv.s, Lv.t, Lv.f, Lv.u})
+        if (b) CK(cudaMemsetAsync(b, 0, Lv.n * sizeof(double2), C.s));
+      if (Lv.block) {
+        const size_t hn = (size_t)GHOST * Lv.g.nx;
+        CKR(dalloc(&Lv.hs_up, hn));
+        CKR(dalloc(&Lv.hs_dn, hn));
+        CKR(dalloc(&Lv.hr_up, hn));
+        CKR(dalloc(&Lv.hr_dn, hn));
+      }
+    }
   }
-  CK(cudaMemcpyAsync(C.L[0].k, k, C.L[0].n * sizeof(double),
-                     k_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, C.s));
-  for (size_t l = 1; l < C.L.size(); ++l) {
-    const Level& F = C.L[l - 1];
-    Level& G = C.L[l];
-    launch_k(C, k_sample_k, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, F.k, G.k);
-    CKR(post_launch(C));
+  if (!C.dist) {
+    CK(cudaMemcpyAsync(C.L[0].k, k, C.L[0].n * sizeof(double),
+                       k_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, C.s));
+    for (size_t l = 1; l < C.L.size(); ++l) {
+      const Level& F = C.L[l - 1];
+      Level& G = C.L[l];
+      launch_k(C, k_sample_k, grd2d(G.g.nx, G.g.ny), blk2d(), 0, F.g, G.g, F.o, F.k, G.k);
+      CKR(post_launch(C));
+    }
+  } else {
+    // global wavenumber hierarchy (coarse k sampled at coincident nodes), then this rank's rows
+    std::vector<double*> tk(C.L.size(), nullptr);
+    for (size_t l = 0; l < C.L.size(); ++l) CKR(dalloc(&tk[l], (size_t)gglob[l].nx * gglob[l].ny));
+    CK(cudaMemcpyAsync(tk[0], k, (size_t)gglob[0].nx * gglob[0].ny * sizeof(double),
+                       k_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, C.s));
+    for (size_t l = 1; l < C.L.size(); ++l) {
+      launch_k(C, k_sample_k, grd2d(gglob[l].nx, gglob[l].ny), blk2d(), 0, gglob[l - 1], gglob[l], C.L[l - 1].o,
+               (const double*)tk[l - 1], tk[l]);
+      CKR(post_launch(C));
+    }
+    for (size_t l = 0; l < C.L.size(); ++l) {
+      Level& Lv = C.L[l];
+      CK(cudaMemcpyAsync(Lv.k, tk[l] + (size_t)Lv.row0 * Lv.g.nx, Lv.n * sizeof(double), cudaMemcpyDeviceToDevice,
+                         C.s));
+    }
+    CK(cudaStreamSynchronize(C.s));
+    for (double* b : tk) cudaFree(b);
   }
   // level descriptors for the single-CTA tail
   {
@@ -921,8 +1219,16 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   CKR(dalloc(&C.bbuf, C.L[0].n));
   CKR(dalloc(&C.xbuf, C.L[0].n));
   CKR(dalloc(&C.rbuf, C.L[0].n));
+  if (C.dist) {
+    for (double2* b : {C.dq, C.dt, C.bbuf, C.xbuf, C.rbuf}) CK(cudaMemsetAsync(b, 0, C.L[0].n * sizeof(double2), C.s));
+    for (double2* b : {C.cc, C.ce}) CK(cudaMemsetAsync(b, 0, C.L[1].n * sizeof(double2), C.s));
+  }
   // inner FGMRES: full (unrestarted) basis of inner_maxit columns, as the oracle (reading R11)
-  CKR(fgm_alloc(C, C.inner, p.inner_maxit, C.L[1].n));
+  {
+    const Level& G1 = C.L[1];
+    CKR(fgm_alloc(C, C.inner, p.inner_maxit, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
+                  C.dist && C.nranks > 1 && G1.block));
+  }
   CK(cudaStreamSynchronize(C.s));
   return HELM_OK;
 }
@@ -949,43 +1255,70 @@ int helm_num_levels(helm_ctx C) { return C ? (int)C->L.size() : fail(HELM_EINVAL
 int helm_level_info(helm_ctx C, int level, int* nx, int* ny, double* h) {
   if (!C || level < 0 || level >= (int)C->L.size()) return fail(HELM_EINVAL, "bad level");
   if (nx) *nx = C->L[level].g.nx;
-  if (ny) *ny = C->L[level].g.ny;
+  if (ny) *ny = C->L[level].gny;
   if (h) *h = C->L[level].g.h;
   return HELM_OK;
 }
 
+extern "C++" {
+// Decomposed contexts: level-0 fields in and out as this rank's owned rows (staged through
+// the stored blocks bbuf -> xbuf, which only a solve uses otherwise).
+template <class Fn>
+static int dist_io0(helm_ctx_s& C, const double* in, double* out, Fn&& fn) {
+  const Level& L = C.L[0];
+  const size_t off = (size_t)L.own0 * L.g.nx, own = (size_t)L.nown * L.g.nx;
+  CK(cudaMemcpyAsync(C.bbuf + off, in, own * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
+  CKR(fn(DVec(C.bbuf), DVec(C.xbuf)));
+  CK(cudaMemcpyAsync(out, C.xbuf + off, own * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
+  return HELM_OK;
+}
+
+static int no_dist(helm_ctx C, const char* what) {
+  return fail(HELM_EINVAL, "%s is not available on a decomposed context", what);
+}
+
+}  // extern "C++"
+
 int helm_apply_A(helm_ctx C, const double* x, double* y) {
   if (!C || !x || !y) return fail(HELM_EINVAL, "null argument");
-  return op_apply(*C, C->L[0], DVec((const double2*)x), DVec(), DVec((double2*)y), 1.0, 0.0);
+  if (C->dist)
+    return dist_io0(*C, x, y, [&](DVec in, DVec out) { return op_apply(*C, 0, in, DVec(), out, 1.0, 0.0); });
+  return op_apply(*C, 0, DVec((const double2*)x), DVec(), DVec((double2*)y), 1.0, 0.0);
 }
 
 int helm_apply_M(helm_ctx C, int level, const double* x, double* y) {
   if (!C || !x || !y || level < 0 || level >= (int)C->L.size()) return fail(HELM_EINVAL, "bad argument");
-  return op_apply(*C, C->L[level], DVec((const double2*)x), DVec(), DVec((double2*)y), C->p.beta1, C->p.beta2);
+  if (C->dist) return no_dist(C, "helm_apply_M");
+  return op_apply(*C, level, DVec((const double2*)x), DVec(), DVec((double2*)y), C->p.beta1, C->p.beta2);
 }
 
 int helm_restrict(helm_ctx C, int level, const double* v, double* vc) {
   if (!C || !v || !vc || level < 0 || level + 1 >= (int)C->L.size()) return fail(HELM_EINVAL, "bad argument");
+  if (C->dist) return no_dist(C, "helm_restrict");
   return restrict_(*C, level, (const double2*)v, (double2*)vc);
 }
 
 int helm_prolong(helm_ctx C, int level, const double* e, double* v) {
   if (!C || !v || !e || level < 0 || level + 1 >= (int)C->L.size()) return fail(HELM_EINVAL, "bad argument");
+  if (C->dist) return no_dist(C, "helm_prolong");
   return prolong_(*C, level, (const double2*)e, nullptr, DVec((double2*)v), nullptr);
 }
 
 int helm_apply_Zt(helm_ctx C, const double* v, double* vc) {
   if (!C || !v || !vc) return fail(HELM_EINVAL, "null argument");
+  if (C->dist) return no_dist(C, "helm_apply_Zt");
   return defl_restrict(*C, DVec((const double2*)v), (double2*)vc);
 }
 
 int helm_apply_Z(helm_ctx C, const double* e, double* v) {
   if (!C || !v || !e) return fail(HELM_EINVAL, "null argument");
+  if (C->dist) return no_dist(C, "helm_apply_Z");
   return defl_prolong(*C, (const double2*)e, (double2*)v);
 }
 
 int helm_apply_E(helm_ctx C, const double* x, double* y) {
   if (!C || !x || !y) return fail(HELM_EINVAL, "null argument");
+  if (C->dist) return no_dist(C, "helm_apply_E");
   return apply_E(*C, DVec((const double2*)x), DVec(), DVec((double2*)y));
 }
 
@@ -997,12 +1330,19 @@ int helm_vcycle(helm_ctx C, int level, const double* f, double* u) {
     for (const double* b : bufs)
       if (b && (f == b || u == b)) return fail(HELM_EINVAL, "aliasing internal buffers");
   }
+  if (C->dist) {
+    if (level != 0) return no_dist(C, "helm_vcycle below level 0");
+    return dist_io0(*C, f, u, [&](DVec in, DVec out) { return vcycle(*C, 0, in, out, nullptr); });
+  }
   return vcycle(*C, level, DVec((const double2*)f), DVec((double2*)u), nullptr);
 }
 
 int helm_deflate(helm_ctx C, const double* v, double* z, int* inner_its) {
   if (!C || !v || !z) return fail(HELM_EINVAL, "null argument");
-  CKR(adef1(*C, DVec((const double2*)v), DVec((double2*)z), nullptr));
+  if (C->dist)
+    CKR(dist_io0(*C, v, z, [&](DVec in, DVec out) { return adef1(*C, in, out, nullptr); }));
+  else
+    CKR(adef1(*C, DVec((const double2*)v), DVec((double2*)z), nullptr));
   if (inner_its) {
     CKR(read_state(*C, C->inner.st));
     *inner_its = C->hst->its;
@@ -1102,7 +1442,8 @@ int helm_solve(helm_ctx C, const double* b, double* x, double tol, int maxit, he
   if (b == x) return fail(HELM_EINVAL, "x may not alias b");
   if (maxit < 1 || !(tol >= 0)) return fail(HELM_EINVAL, "bad tol/maxit");
   const size_t n = C->L[0].n;
-  CK(cudaMemcpyAsync(C->bbuf, b, n * sizeof(double2), cudaMemcpyDeviceToDevice, C->s));
+  const size_t off = (size_t)C->L[0].own0 * C->L[0].g.nx, own = (size_t)C->L[0].nown * C->L[0].g.nx;
+  CK(cudaMemcpyAsync(C->bbuf + off, b, own * sizeof(double2), cudaMemcpyDeviceToDevice, C->s));
   CK(cudaMemsetAsync(C->xbuf, 0, n * sizeof(double2), C->s));
   // the graph runs on the private stream: order it after the caller's stream and back
   cudaEvent_t ev;
@@ -1116,7 +1457,7 @@ int helm_solve(helm_ctx C, const double* b, double* x, double tol, int maxit, he
   if (r == HELM_OK) {
     CK(cudaEventRecord(ev, C->own));
     CK(cudaStreamWaitEvent(user, ev, 0));
-    CK(cudaMemcpyAsync(x, C->xbuf, n * sizeof(double2), cudaMemcpyDeviceToDevice, user));
+    CK(cudaMemcpyAsync(x, C->xbuf + off, own * sizeof(double2), cudaMemcpyDeviceToDevice, user));
     CK(cudaStreamSynchronize(user));
   }
   cudaEventDestroy(ev);
@@ -1127,14 +1468,15 @@ int helm_solve_host(helm_ctx C, const double* b_host, double* x_host, double tol
   if (!C || !b_host || !x_host) return fail(HELM_EINVAL, "null argument");
   if (maxit < 1 || !(tol >= 0)) return fail(HELM_EINVAL, "bad tol/maxit");
   const size_t n = C->L[0].n;
+  const size_t off = (size_t)C->L[0].own0 * C->L[0].g.nx, own = (size_t)C->L[0].nown * C->L[0].g.nx;
   cudaStream_t user = C->s;
   C->s = C->own;
   CK(cudaStreamSynchronize(user));
-  CK(cudaMemcpyAsync(C->bbuf, b_host, n * sizeof(double2), cudaMemcpyHostToDevice, C->s));
+  CK(cudaMemcpyAsync(C->bbuf + off, b_host, own * sizeof(double2), cudaMemcpyHostToDevice, C->s));
   CK(cudaMemsetAsync(C->xbuf, 0, n * sizeof(double2), C->s));
   int r = solve_device(*C, tol, maxit, rep);
   if (r == HELM_OK) {
-    CK(cudaMemcpyAsync(x_host, C->xbuf, n * sizeof(double2), cudaMemcpyDeviceToHost, C->s));
+    CK(cudaMemcpyAsync(x_host, C->xbuf + off, own * sizeof(double2), cudaMemcpyDeviceToHost, C->s));
     CK(cudaStreamSynchronize(C->s));
   }
   C->s = user;
@@ -1158,6 +1500,7 @@ long long helm_launch_count(helm_ctx C) { return C ? C->launches : 0; }
 
 int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_region) {
   if (!C || reps < 1 || !us_per_region) return fail(HELM_EINVAL, "bad argument");
+  if (C->dist) return no_dist(C, "helm_bench_graph");
   helm_ctx_s& X = *C;
   if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
   if (which == HELM_GB_DCGS && (arg < 0 || arg + reps >= X.inner.m)) return fail(HELM_EINVAL, "bad column");
@@ -1183,7 +1526,7 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         r = apply_E(X, DVec(X.cc), DVec(), DVec(X.ce));
         break;
       case HELM_GB_APPLY_A:
-        r = op_apply(X, F, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
+        r = op_apply(X, 0, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
         break;
       case HELM_GB_DCGS: {
         // one delayed-CGS2 step of the inner FGMRES at column j = arg (+ the reps before it)
@@ -1258,6 +1601,7 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
 int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, double* us_per_launch,
                       double* bytes_per_launch) {
   if (!C || reps < 1 || !us_per_launch) return fail(HELM_EINVAL, "bad argument");
+  if (C->dist) return no_dist(C, "helm_bench_kernel");
   helm_ctx_s& X = *C;
   const Level& F = X.L[0];
   const Level& G = X.L[1];
@@ -1277,7 +1621,7 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
     switch (which) {
       case HELM_KB_APPLY_A:
         bytes = (double)F.n * 40.0;
-        return op_apply(X, F, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
+        return op_apply(X, 0, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
       case HELM_KB_VC_DOWN: {
         const Level& Fl = X.L[lv];
         const Level& Gl = X.L[lv + 1];
@@ -1362,6 +1706,152 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
   *us_per_launch = 1e3 * total_ms / reps;
   if (bytes_per_launch) *bytes_per_launch = bytes;
   return HELM_OK;
+}
+
+
+// ---------------------------------------------------------------------- decomposed contexts
+int helm_group_create(int nranks, helm_group* out) {
+  if (!out || nranks < 1 || nranks > DIST_MAX_RANKS) return fail(HELM_EINVAL, "nranks must be in [1, %d]", DIST_MAX_RANKS);
+  helm_group_s* g = new helm_group_s();
+  g->n = nranks;
+  g->bar.n = nranks;
+  g->rank.resize(nranks);
+  g->status.assign(nranks, HELM_OK);
+  *out = g;
+  return HELM_OK;
+}
+
+void helm_group_destroy(helm_group g) { delete g; }
+
+int helm_nccl_unique_id(unsigned char id[128]) {
+  if (!id) return fail(HELM_EINVAL, "null argument");
+  std::string why;
+  const NcclApi* api = nccl_api(why);
+  if (!api) return fail(HELM_EINVAL, "%s", why.c_str());
+  ncclUniqueId u;
+  const ncclResult_t r = api->GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(HELM_ECUDA, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  return HELM_OK;
+}
+
+// per-rank registration of the buffers its peers read (thread groups) + the staging slot
+static int dist_register(helm_ctx_s& C) {
+  CK(cudaEventCreateWithFlags(&C.dev_ev, cudaEventDisableTiming));
+  if (C.kind != HELM_COMM_THREADS) return HELM_OK;
+  C.red_cap = 2 * 4096 + 8;   // 2m + 2 values for the largest outer basis (ensure_outer caps m at 4096)
+  CKR(dalloc(&C.red, C.red_cap));
+  GroupRank& gr = C.grp->rank[C.rank];
+  gr.ev = C.dev_ev;
+  gr.red = C.red;
+  gr.send_up.assign(C.L.size(), nullptr);
+  gr.send_dn.assign(C.L.size(), nullptr);
+  gr.gathered.assign(C.L.size(), nullptr);
+  for (size_t l = 0; l < C.L.size(); ++l) {
+    gr.send_up[l] = C.L[l].hs_up;
+    gr.send_dn[l] = C.L[l].hs_dn;
+    gr.gathered[l] = C.L[l].f;
+  }
+  CK(cudaStreamSynchronize(C.s));
+  return HELM_OK;
+}
+
+int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k_on_device, const helm_params* params,
+                    void* stream, const helm_dist* d) {
+  if (!out || !grid || !k || !d) return fail(HELM_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->nranks < 1 || d->nranks > DIST_MAX_RANKS || d->rank < 0 || d->rank >= d->nranks)
+    return fail(HELM_EINVAL, "bad rank %d of %d", d->rank, d->nranks);
+  if (d->kind == HELM_COMM_THREADS) {
+    if (!d->group || d->group->n != d->nranks) return fail(HELM_EINVAL, "thread group of the wrong size");
+  } else if (d->kind == HELM_COMM_NCCL) {
+    if (!d->nccl_id) return fail(HELM_EINVAL, "NCCL transport needs nccl_id");
+  } else {
+    return fail(HELM_EINVAL, "bad transport %d", d->kind);
+  }
+  helm_ctx_s* C = new helm_ctx_s();
+  if (params) C->p = *params;
+  else helm_default_params(&C->p);
+  C->user = (cudaStream_t)stream;
+  C->dist = 1;
+  C->kind = d->kind;
+  C->rank = d->rank;
+  C->nranks = d->nranks;
+  C->grp = d->kind == HELM_COMM_THREADS ? d->group : nullptr;
+  // decomposed solves: host-polled loops, no PDL, no cluster tail / cooperative step
+  C->p.graph = 0;
+  C->p.pdl = 0;
+  C->p.tail_max_n = 0;
+  C->p.coop = 0;
+  if (C->p.dist_min_rows <= 0) C->p.dist_min_rows = 16;
+  int r = HELM_OK;
+  if (C->p.outer != HELM_OUTER_FGMRES) r = fail(HELM_EINVAL, "decomposed contexts support the FGMRES outer method only");
+  if (r == HELM_OK && C->p.dist_levels == 1) r = fail(HELM_EINVAL, "dist_levels must be 0 or >= 2");
+  if (r == HELM_OK && d->kind == HELM_COMM_NCCL) {
+    std::string why;
+    C->api = nccl_api(why);
+    if (!C->api) {
+      r = fail(HELM_EINVAL, "%s", why.c_str());
+    } else {
+      ncclUniqueId id;
+      memcpy(&id, d->nccl_id, sizeof id);
+      const ncclResult_t nr = C->api->CommInitRank(&C->nccl, d->nranks, id, d->rank);
+      if (nr != ncclSuccess) r = fail(HELM_ECUDA, "ncclCommInitRank: %s", C->api->GetErrorString(nr));
+    }
+  }
+  if (r == HELM_OK) r = setup_impl(*C, grid, k, k_on_device);
+  if (r == HELM_OK) r = dist_register(*C);
+  if (d->kind == HELM_COMM_THREADS) {
+    // all ranks agree on success before anyone exchanges with a peer
+    C->grp->status[d->rank] = r;
+    C->grp->bar.wait();
+    for (int q = 0; q < d->nranks && r == HELM_OK; ++q)
+      if (C->grp->status[q] != HELM_OK) r = fail(HELM_EINVAL, "setup failed on rank %d", q);
+    C->grp->bar.wait();
+  }
+  if (r != HELM_OK) {
+    destroy_ctx(C);
+    return r;
+  }
+  *out = C;
+  return HELM_OK;
+}
+
+int helm_dist_rows(helm_ctx C, int level, int* row0, int* nrows) {
+  if (!C || level < 0 || level >= (int)C->L.size()) return fail(HELM_EINVAL, "bad level");
+  const Level& L = C->L[level];
+  if (row0) *row0 = L.row0 + L.own0;
+  if (nrows) *nrows = L.nown;
+  return HELM_OK;
+}
+
+int helm_dist_plan(const helm_grid* grid, const helm_params* params, int nranks, int* D, int* table, int cap_levels) {
+  if (!grid || nranks < 1) return fail(HELM_EINVAL, "bad argument");
+  helm_params p;
+  if (params) p = *params;
+  else helm_default_params(&p);
+  if (p.dist_min_rows <= 0) p.dist_min_rows = 16;
+  std::vector<std::pair<int, int>> sz;
+  hierarchy_sizes(*grid, p, sz);
+  std::vector<int> nys;
+  for (const auto& s : sz) nys.push_back(s.second);
+  std::vector<DistRows> plan;
+  std::string why;
+  const int d = dist_plan(nys, grid->bc == HELM_BC_DIRICHLET, nranks, p.dist_min_rows, p.dist_levels, plan, why);
+  if (d < 0) return fail(HELM_ESHAPE, "decomposition: %s", why.c_str());
+  if (D) *D = d;
+  if (table)
+    for (int l = 0; l < std::min((int)sz.size(), cap_levels); ++l)
+      for (int q = 0; q < nranks; ++q) {
+        const DistRows& r = plan[(size_t)l * nranks + q];
+        int* o = table + ((size_t)l * nranks + q) * 4;
+        o[0] = r.a;
+        o[1] = r.b;
+        o[2] = r.s;
+        o[3] = r.e;
+      }
+  return (int)sz.size();
 }
 
 }  // extern "C"

@@ -535,8 +535,40 @@ __global__ void __launch_bounds__(256) k_dcgs_reduceA(const double2* __restrict_
     for (long long b = lane; b < P; b += 32) s = cadd(s, part[(long long)c * P + b]);
     s = warp_sum2(s);
     if (lane == 0) dots[c] = s;
+  } else if (lane == 0) {
+    dots[c] = make_double2(0.0, 0.0);   // unused tail zeroed: a rank-sum over all slots stays finite
   }
-  if (last_block(counter) && threadIdx.x < 32) dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, sra);
+  // counter == null (decomposed solve): the sums are per rank; step A runs after the allreduce
+  if (counter && last_block(counter) && threadIdx.x < 32)
+    dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, sra);
+}
+
+// Step A / step B as one-warp kernels (decomposed solve: they follow the rank-sum of the dots
+// and of |w'|^2; same code as the last-block forms above).
+__global__ void k_dcgs_stepA(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                             const double2* __restrict__ dots, double2* __restrict__ coef,
+                             double2* __restrict__ sc2, double2* __restrict__ rawc) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 sra[];
+  if (threadIdx.x < 32) dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, sra);
+}
+
+__global__ void k_dcgs_stepB(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                             const double2* __restrict__ dots, const double2* __restrict__ sc2,
+                             const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
+                             cudaGraphConditionalHandle hcond, int use_h) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 srb[];
+  if (threadIdx.x < 32) dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, npart, np, rawc, hcond, use_h, srb);
+}
+
+// out[0] = sum of np partials (one warp, fixed order)
+__global__ void k_sum_part(const double2* __restrict__ part, int np, double2* __restrict__ out) {
+  HELM_PDL_ENTRY();
+  double2 s = make_double2(0.0, 0.0);
+  for (int b = threadIdx.x; b < np; b += 32) s = cadd(s, part[b]);
+  s = warp_sum2(s);
+  if (threadIdx.x == 0) out[0] = s;
 }
 
 // Apply rotations G_0..G_{nrot-1} to a raw Hessenberg column (in shared memory, lane 0).

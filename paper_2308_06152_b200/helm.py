@@ -33,7 +33,16 @@ class helm_params(ctypes.Structure):
                 ("restart", ctypes.c_int), ("max_coarsest", ctypes.c_int), ("vectors", ctypes.c_int),
                 ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int), ("pdl", ctypes.c_int),
                 ("coarsest_n", ctypes.c_int), ("coop", ctypes.c_int), ("outer", ctypes.c_int),
-                ("col_min_n", ctypes.c_int)]
+                ("col_min_n", ctypes.c_int), ("dist_levels", ctypes.c_int), ("dist_min_rows", ctypes.c_int)]
+
+
+class helm_dist(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+                ("group", ctypes.c_void_p), ("nccl_id", ctypes.c_void_p)]
+
+
+HELM_COMM_THREADS = 0
+HELM_COMM_NCCL = 1
 
 
 class helm_report(ctypes.Structure):
@@ -70,6 +79,14 @@ EXPORTS = {
     "helm_launch_count": (ctypes.c_longlong, [_P]),
     "helm_bench_kernel": (_I, [_P, _I, _I, _I, _I, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "helm_bench_graph": (_I, [_P, _I, _I, _I, ctypes.POINTER(_D)]),
+    "helm_group_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "helm_group_destroy": (None, [_P]),
+    "helm_nccl_unique_id": (_I, [ctypes.c_char_p]),
+    "helm_setup_dist": (_I, [ctypes.POINTER(_P), ctypes.POINTER(helm_grid), _P, _I, ctypes.POINTER(helm_params), _P,
+                             ctypes.POINTER(helm_dist)]),
+    "helm_dist_rows": (_I, [_P, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "helm_dist_plan": (_I, [ctypes.POINTER(helm_grid), ctypes.POINTER(helm_params), _I, ctypes.POINTER(_I),
+                            ctypes.POINTER(_I), _I]),
     "helm_last_error": (ctypes.c_char_p, []),
     "helm_build_info": (ctypes.c_char_p, []),
 }
@@ -292,3 +309,93 @@ class Helm:
 def helm_setup(problem, params=None, stream=None) -> Helm:
     """Build a context from a workloads.Problem-like object (k, h, bc, nx, ny)."""
     return Helm(problem.nx, problem.ny, problem.h, problem.bc, problem.k, params, stream)
+
+
+# ---------------------------------------------------------------------- decomposed solves
+def dist_plan(nx, ny, h, bc, nranks, params=None):
+    """Host-only row-strip plan (helm_dist_plan): (D, table[l][q] = (a, b, s, e))."""
+    lib = load_library()
+    p = params if isinstance(params, helm_params) else default_params(**(params or {}))
+    g = helm_grid(int(nx), int(ny), float(h), BCS[bc])
+    cap = 64
+    table = (_I * (cap * nranks * 4))()
+    D = _I()
+    nl = lib.helm_dist_plan(ctypes.byref(g), ctypes.byref(p), int(nranks), ctypes.byref(D), table, cap)
+    if nl < 0:
+        _check(nl)
+    rows = [[tuple(table[(l * nranks + q) * 4 + i] for i in range(4)) for q in range(nranks)] for l in range(nl)]
+    return D.value, rows
+
+
+class ThreadGroup:
+    """helm_group_create: nranks ranks living as host threads of this process (one device)."""
+
+    def __init__(self, nranks):
+        lib = load_library()
+        self.lib = lib
+        self.nranks = int(nranks)
+        g = ctypes.c_void_p()
+        _check(lib.helm_group_create(self.nranks, ctypes.byref(g)))
+        self.handle = g
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.helm_group_destroy(self.handle)
+            self.handle = None
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.helm_nccl_unique_id(buf))
+    return buf.raw
+
+
+class HelmDist(Helm):
+    """One rank of a row-strip decomposed solver (helm_setup_dist).  Level-0 fields passed to
+    and returned by the entry points are this rank's owned rows, shape (nrows, nx)."""
+
+    def __init__(self, nx, ny, h, bc, k, rank, nranks, group: ThreadGroup | None = None, nccl_id: bytes | None = None,
+                 params=None, stream=None):
+        import torch
+        self.torch = torch
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise HelmError("no CUDA device: libhelm has no CPU fallback")
+        self.lib = lib
+        self.nx, self.ny, self.h, self.bc = int(nx), int(ny), float(h), bc
+        if isinstance(params, dict) or params is None:
+            params = default_params(**(params or {}))
+        self.params = params
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        kt = torch.as_tensor(np.ascontiguousarray(k, dtype=np.float64)) if not isinstance(k, torch.Tensor) else k
+        kt = kt.to(device="cuda", dtype=torch.float64).contiguous()
+        assert kt.shape == (self.ny, self.nx)
+        g = helm_grid(self.nx, self.ny, self.h, BCS[bc])
+        self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        d = helm_dist(HELM_COMM_NCCL if nccl_id is not None else HELM_COMM_THREADS, int(rank), int(nranks),
+                      group.handle if group is not None else None,
+                      ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None)
+        ctx = ctypes.c_void_p()
+        _check(lib.helm_setup_dist(ctypes.byref(ctx), ctypes.byref(g), _ptr(kt), 1, ctypes.byref(params),
+                                   ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(d)))
+        self.ctx = ctx
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.levels = [self.level_info(l) for l in range(lib.helm_num_levels(ctx))]
+        self.row0, self.nrows = self.dist_rows(0)
+
+    def dist_rows(self, level=0):
+        r0, nr = _I(), _I()
+        _check(self.lib.helm_dist_rows(self.ctx, int(level), ctypes.byref(r0), ctypes.byref(nr)))
+        return r0.value, nr.value
+
+    def field(self, level=0):
+        assert level == 0
+        return self.torch.zeros((self.nrows, self.nx), dtype=self.torch.complex128, device="cuda")
+
+    def _in(self, x, level=0):
+        t = self.torch
+        assert level == 0
+        x = t.as_tensor(x).to(device="cuda", dtype=t.complex128).contiguous()
+        assert tuple(x.shape) == (self.nrows, self.nx), (x.shape, (self.nrows, self.nx))
+        return x

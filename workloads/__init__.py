@@ -14,6 +14,7 @@ Both `oracle/` and the CUDA path consume these arrays; neither imports the other
 from .media import (  # noqa: F401
     Problem,
     mp_problem,
+    strip_problem,
     wedge_problem,
     marmousi_like_problem,
     random_field,

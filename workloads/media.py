@@ -80,6 +80,21 @@ def mp_problem(k: float, n_cells: int, bc: str = "dirichlet", name: str | None =
                    {"k": float(k), "n_cells": n_cells, "source": src})
 
 
+def strip_problem(k: float, n_cells: int, strips: int, name: str | None = None) -> Problem:
+    """Weak-scaling family of the Dirichlet model problem (BASELINE configs[4], row-strip
+    decomposition): the domain (0,1) x (0,strips) at the same h = 1/n_cells and k, i.e.
+    `strips` unit squares stacked in y -- one per GPU -- with the point source at the centre
+    (0.5, strips/2).  strips = 1 is mp_problem(k, n_cells)."""
+    if n_cells % 2:
+        raise ValueError("n_cells must be even")
+    h = 1.0 / n_cells
+    nx, ny = n_cells - 1, strips * n_cells - 1
+    kk = np.full((ny, nx), float(k))
+    b, src = _point_source("dirichlet", h, nx, ny, h, h, 0.5, 0.5 * strips)
+    return Problem(name or f"strip{strips}_k{k:g}_n{n_cells}", "dirichlet", h, nx, ny, h, h, kk, b,
+                   {"k": float(k), "n_cells": n_cells, "strips": strips, "source": src})
+
+
 # --------------------------------------------------------------------------------------
 # Wedge (PAPER.md §2.3, Eq. 2.14): Omega = (0,600) x (-1000,0), three layers with
 # velocities 2000 / 1500 / 3000 m/s top to bottom separated by two sloping straight
