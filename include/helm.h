@@ -105,6 +105,10 @@ typedef struct {
                           least dist_min_rows rows, at most all but the coarsest); the levels below
                           are replicated on every rank.  Must be >= 2 (levels 0 and 1). */
   int dist_min_rows;   /* fewest rows a rank may own on a decomposed level (default 16, >= 6) */
+  int col_pipe;        /* column-streaming legs: 0 = rows prefetched in registers; 1 (default) = rows
+                          staged through a per-warp cp.async shared-memory ring, 4 rows in flight,
+                          segments of 256 (down) / 128 (up) rows; 3, 4, 5, 14, 24: other depths /
+                          segment lengths (measurement) */
 } helm_params;
 
 typedef struct {

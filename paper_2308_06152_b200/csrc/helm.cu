@@ -497,6 +497,55 @@ constexpr size_t TAIL_SMEM_MAX = 200 * 1024;
 constexpr int DOWN_TX = 16, DOWN_TY = 8;   // coarse points per k_vc_down CTA
 constexpr int UP_TX = 32, UP_TY = 8;       // fine points per k_vc_up CTA
 
+
+// Column-streaming legs: col_pipe selects the register-prefetch form (0) or the cp.async ring
+// (rows in flight, segment length): 1 (default, tuned on 16383^2) -> down (4, 256), up (4, 128);
+// 3/4/5 -> (3/4/5, 64), 14 -> (4, 128), 24 -> (4, 256).
+template <int PF, int SEG>
+void col_down_t(helm_ctx_s& C, const Level& L, const Level& G, DVec f, double sr, double si, double w) {
+  const int wcols = (L.g.nx + COL_OWN - 1) / COL_OWN;
+  const dim3 gc((wcols + 3) / 4, (L.g.ny + SEG - 1) / SEG);
+  if (PF == 0) launch_k(C, k_vc_down_col, gc, 128, 0, L.g, G.g, L.o, f, (const double*)L.k, sr, si, w, L.s, G.f);
+  else launch_k(C, k_vc_down_cpa<PF ? PF : 1, SEG>, gc, 128, 0, L.g, G.g, L.o, f, (const double*)L.k, sr, si, w, L.s, G.f);
+}
+template <int PF, int SEG>
+void col_up_t(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2* addq, DVec u_out, double sr,
+              double si, double w) {
+  const int wcols = (L.g.nx + COL_OWN - 1) / COL_OWN;
+  const dim3 gc((wcols + 3) / 4, (L.g.ny + SEG - 1) / SEG);
+  if (PF == 0)
+    launch_k(C, k_vc_up_col, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f, (const double*)L.k,
+             sr, si, w, addq, u_out);
+  else
+    launch_k(C, k_vc_up_cpa<PF ? PF : 1, SEG>, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f,
+             (const double*)L.k, sr, si, w, addq, u_out);
+}
+int col_down(helm_ctx_s& C, const Level& L, const Level& G, DVec f, double sr, double si, double w) {
+  switch (C.p.col_pipe) {
+    case 1: col_down_t<4, 256>(C, L, G, f, sr, si, w); break;
+    case 3: col_down_t<3, 64>(C, L, G, f, sr, si, w); break;
+    case 4: col_down_t<4, 64>(C, L, G, f, sr, si, w); break;
+    case 5: col_down_t<5, 64>(C, L, G, f, sr, si, w); break;
+    case 14: col_down_t<4, 128>(C, L, G, f, sr, si, w); break;
+    case 24: col_down_t<4, 256>(C, L, G, f, sr, si, w); break;
+    default: col_down_t<0, COL_SEG>(C, L, G, f, sr, si, w);
+  }
+  return post_launch(C);
+}
+int col_up(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2* addq, DVec u_out, double sr,
+           double si, double w) {
+  switch (C.p.col_pipe) {
+    case 1: col_up_t<4, 128>(C, L, G, f, addq, u_out, sr, si, w); break;
+    case 3: col_up_t<3, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
+    case 4: col_up_t<4, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
+    case 5: col_up_t<5, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
+    case 14: col_up_t<4, 128>(C, L, G, f, addq, u_out, sr, si, w); break;
+    case 24: col_up_t<4, 256>(C, L, G, f, addq, u_out, sr, si, w); break;
+    default: col_up_t<0, COL_SEG>(C, L, G, f, addq, u_out, sr, si, w);
+  }
+  return post_launch(C);
+}
+
 // u_out = V-cycle approximation of M_l^{-1} f (+ addq), starting at level l.
 int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   const int last = (int)C.L.size() - 1;
@@ -520,16 +569,11 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   CKR(halo(C, l, f));
   if (fused_vcycle(C) && C.p.col_min_n >= 0 && (long long)L.n >= C.p.col_min_n) {
     // large levels: column-streaming legs (no shared-memory staging)
-    const int wcols = (L.g.nx + COL_OWN - 1) / COL_OWN;
-    const dim3 gc((wcols + 3) / 4, (L.g.ny + COL_SEG - 1) / COL_SEG);
-    launch_k(C, k_vc_down_col, gc, 128, 0, L.g, G.g, L.o, f, (const double*)L.k, sr, si, w, L.s, G.f);
-    CKR(post_launch(C));
+    CKR(col_down(C, L, G, f, sr, si, w));
     if (gather) CKR(allgather(C, l + 1));
     CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
     CKR(halo(C, l + 1, DVec(Gs.u)));
-    launch_k(C, k_vc_up_col, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f,
-             (const double*)L.k, sr, si, w, addq, u_out);
-    return post_launch(C);
+    return col_up(C, L, G, f, addq, u_out, sr, si, w);
   }
   if (fused_vcycle(C)) {
     // small levels: smaller tiles so that more SMs share the (latency-bound) work
@@ -957,6 +1001,7 @@ void helm_default_params(helm_params* p) {
   p->pdl = 1;
   p->dist_levels = 0;
   p->dist_min_rows = 16;
+  p->col_pipe = 1;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1626,13 +1671,8 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         const Level& Fl = X.L[lv];
         const Level& Gl = X.L[lv + 1];
         bytes = (double)Fl.n * 40.0 + (double)Gl.n * 16.0;
-        if (X.p.col_min_n >= 0 && (long long)Fl.n >= X.p.col_min_n) {
-          const int wcols = (Fl.g.nx + COL_OWN - 1) / COL_OWN;
-          const dim3 gc((wcols + 3) / 4, (Fl.g.ny + COL_SEG - 1) / COL_SEG);
-          k_vc_down_col<<<gc, 128, 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2, X.p.omega,
-                                             Fl.s, Gl.f);
-          return post_launch(X);
-        }
+        if (X.p.col_min_n >= 0 && (long long)Fl.n >= X.p.col_min_n)
+          return col_down(X, Fl, Gl, DVec(Fl.t), X.p.beta1, X.p.beta2, X.p.omega);
         dim3 gd((Gl.g.nx + DOWN_TX - 1) / DOWN_TX, (Gl.g.ny + DOWN_TY - 1) / DOWN_TY);
         k_vc_down<DOWN_TX, DOWN_TY><<<gd, dim3(32, 8), 0, X.s>>>(Fl.g, Gl.g, Fl.o, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
                                                            X.p.omega, Fl.s, Gl.f);
@@ -1642,13 +1682,9 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         const Level& Fl = X.L[lv];
         const Level& Gl = X.L[lv + 1];
         bytes = (double)Fl.n * 56.0 + (double)Gl.n * 16.0;
-        if (X.p.col_min_n >= 0 && (long long)Fl.n >= X.p.col_min_n) {
-          const int wcols = (Fl.g.nx + COL_OWN - 1) / COL_OWN;
-          const dim3 gc((wcols + 3) / 4, (Fl.g.ny + COL_SEG - 1) / COL_SEG);
-          k_vc_up_col<<<gc, 128, 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1, X.p.beta2,
-                                           X.p.omega, nullptr, DVec(lv == 0 ? X.bbuf : Fl.u));
-          return post_launch(X);
-        }
+        if (X.p.col_min_n >= 0 && (long long)Fl.n >= X.p.col_min_n)
+          return col_up(X, Fl, Gl, DVec(Fl.t), nullptr, DVec(lv == 0 ? X.bbuf : Fl.u), X.p.beta1, X.p.beta2,
+                        X.p.omega);
         dim3 gu((Fl.g.nx + UP_TX - 1) / UP_TX, (Fl.g.ny + UP_TY - 1) / UP_TY);
         k_vc_up<UP_TX, UP_TY><<<gu, dim3(32, 8), 0, X.s>>>(Fl.g, Gl.g, Fl.o, Fl.s, Gl.u, DVec(Fl.t), Fl.k, X.p.beta1,
                                                      X.p.beta2, X.p.omega, nullptr, DVec(lv == 0 ? X.bbuf : Fl.u));

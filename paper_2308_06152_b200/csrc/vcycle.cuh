@@ -336,6 +336,125 @@ __global__ void __launch_bounds__(128) k_vc_down_col(Geo F, Geo G, int o, DVec f
   }
 }
 
+// ---- cp.async-pipelined column legs: the rows ahead are staged in a per-warp shared-memory
+// ring by asynchronous copies (LDGSTS; each lane copies and later reads only its own slots, so
+// no barrier), PF rows in flight per warp without holding them in registers.
+__device__ __forceinline__ void cpa16(void* smem, const void* g, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(pred ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* g, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Down leg (same arithmetic and tap order as k_vc_down_col), f and k staged PF rows ahead.
+// INT: every node the warp touches is interior (all four neighbours in the grid, no boundary
+// row), so the multipliers are the branch-free interior ones (identical values and operation
+// order); the restriction's shuffles run only on the rows that end a coarse row.
+template <int PF, int SEG, bool INT>
+__device__ __forceinline__ void down_cpa_body(const Geo& F, const Geo& G, int o, const double2* __restrict__ f,
+                                              double fs, const double* __restrict__ k, double sr, double si,
+                                              double omega, double2* __restrict__ u, double2* __restrict__ fc,
+                                              double2 (*rf)[32], double (*rk)[32], int lane, int xo, int ya, int yb) {
+  const int x = xo - 2 + lane;
+  const bool xin = (x >= 0 && x < F.nx);
+  const bool xown = (lane >= 2 && lane < 2 + COL_OWN && x < F.nx);
+  const int ri = x - o;
+  const bool xcentre = ((ri & 1) == 0) && ri >= 0 && (ri >> 1) < G.nx && xown;
+  const int I = ri >> 1;
+  const double ih2 = 1.0 / (F.h * F.h);
+  const int y0 = ya - 2, y1 = yb + 1;   // rows consumed
+  auto issue = [&](int yy) {
+    const int slot = (yy - y0) % PF;
+    const bool ok = xin && yy >= 0 && yy < F.ny && yy <= y1;
+    const size_t p = ok ? (size_t)yy * F.nx + x : 0;
+    cpa16(&rf[slot][lane], f + p, ok);
+    cpa8(&rk[slot][lane], k + p, ok);
+    cpa_commit();
+  };
+#pragma unroll
+  for (int q = 0; q < PF; ++q) issue(y0 + q);
+  double2 um2 = czero(), um1 = czero(), fm1 = czero(), rm3 = czero(), rm2 = czero();
+  double km1 = 0.0;
+  for (int y = y0; y <= y1; ++y) {
+    cpa_wait<PF - 1>();
+    const int slot = (y - y0) % PF;
+    const double2 fraw = rf[slot][lane];
+    const double k0 = rk[slot][lane];
+    issue(y + PF);   // refills this lane's slot (already read)
+    double2 f0 = czero(), u0 = czero();
+    if (INT || (xin && y >= 0 && y < F.ny)) {
+      f0 = cscale(fs, fraw);
+      const double2 ap = INT ? interior_ap(ih2, k0, sr, si) : coef_at(F, x, y, k0, sr, si).ap;
+      u0 = cscale(omega, cdiv(f0, ap));   // reading R9: first sweep from u = 0
+      if (xown && y >= ya && y < yb) u[(size_t)y * F.nx + x] = u0;
+    }
+    const int yr = y - 1;
+    const double2 uw = shfl_up2(um1, 1), ue = shfl_dn2(um1, 1);
+    double2 r = czero();
+    if (lane >= 1 && lane <= 30) {
+      if (INT) {
+        r = csub(fm1, interior_stencil(ih2, interior_ap(ih2, km1, sr, si), um1, uw, ue, um2, u0));
+      } else if (xin && yr >= 0 && yr < F.ny) {
+        const Coef c = coef_at(F, x, yr, km1, sr, si);
+        r = csub(fm1, stencil5(c, um1, uw, ue, um2, u0));
+      }
+    }
+    const int yc = y - 2;
+    const int rj = yc - o;
+    if (((rj & 1) == 0) && yc >= ya && yc < yb && rj >= 0 && (rj >> 1) < G.ny) {   // warp-uniform
+      const double2 a0 = shfl_up2(rm3, 1), a2 = shfl_dn2(rm3, 1);
+      const double2 b0 = shfl_up2(rm2, 1), b2 = shfl_dn2(rm2, 1);
+      const double2 c0 = shfl_up2(r, 1), c2 = shfl_dn2(r, 1);
+      if (xcentre) {
+        double2 s = czero();
+        s = cadd(s, cscale(1.0 / 16.0, a0));
+        s = cadd(s, cscale(2.0 / 16.0, rm3));
+        s = cadd(s, cscale(1.0 / 16.0, a2));
+        s = cadd(s, cscale(2.0 / 16.0, b0));
+        s = cadd(s, cscale(4.0 / 16.0, rm2));
+        s = cadd(s, cscale(2.0 / 16.0, b2));
+        s = cadd(s, cscale(1.0 / 16.0, c0));
+        s = cadd(s, cscale(2.0 / 16.0, r));
+        s = cadd(s, cscale(1.0 / 16.0, c2));
+        fc[(size_t)(rj >> 1) * G.nx + I] = s;
+      }
+    }
+    rm3 = rm2;
+    rm2 = r;
+    um2 = um1;
+    um1 = u0;
+    fm1 = f0;
+    km1 = k0;
+  }
+  cpa_wait<0>();
+}
+
+template <int PF, int SEG = COL_SEG>
+__global__ void __launch_bounds__(128) k_vc_down_cpa(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
+                                                     double sr, double si, double omega, double2* __restrict__ u,
+                                                     double2* __restrict__ fc) {
+  HELM_PDL_ENTRY();
+  __shared__ double2 rf[4][PF][32];
+  __shared__ double rk[4][PF][32];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int xo = (blockIdx.x * 4 + wq) * COL_OWN;
+  if (xo >= F.nx) return;
+  const int ya = blockIdx.y * SEG;
+  const int yb = min(F.ny, ya + SEG);
+  const bool interior = xo - 2 >= 1 && xo + 29 <= F.nx - 2 && ya - 3 >= 1 && yb + 1 <= F.ny - 2;
+  if (interior)
+    down_cpa_body<PF, SEG, true>(F, G, o, fv.get(), fv.scale(), k, sr, si, omega, u, fc, rf[wq], rk[wq], lane, xo,
+                                 ya, yb);
+  else
+    down_cpa_body<PF, SEG, false>(F, G, o, fv.get(), fv.scale(), k, sr, si, omega, u, fc, rf[wq], rk[wq], lane, xo,
+                                  ya, yb);
+}
+
 // Up leg, column-streaming form (same arithmetic as k_vc_up):
 //   u1 = u + I_{2h}^h e,  y = u1 + omega (f - M u1)/D (+ q).
 __global__ void __launch_bounds__(128) k_vc_up_col(Geo F, Geo G, int o, const double2* __restrict__ u,
@@ -416,6 +535,142 @@ __global__ void __launch_bounds__(128) k_vc_up_col(Geo F, Geo G, int o, const do
     v1m2 = v1m1;
     v1m1 = v10;
   }
+}
+
+// Up leg (same arithmetic as k_vc_up_col): u staged PF rows ahead, f, k (and q) staged with it.
+// INT as in the down leg (branch-free interior multipliers for the post-smoothing).
+template <int PF, int SEG, bool INT>
+__device__ __forceinline__ void up_cpa_body(const Geo& F, const Geo& G, int o, const double2* __restrict__ u,
+                                            const double2* __restrict__ e, const double2* __restrict__ f, double fs,
+                                            const double* __restrict__ k, double sr, double si, double omega,
+                                            const double2* __restrict__ addq, double2* __restrict__ yo,
+                                            double2 (*ru)[32], double2 (*rf)[32], double2 (*rq)[32], double (*rk)[32],
+                                            int lane, int xo, int ya, int yb) {
+  const int x = xo - 2 + lane;
+  const bool xin = (x >= 0 && x < F.nx);
+  const bool xown = (lane >= 2 && lane < 2 + COL_OWN && x < F.nx);
+  const double ih2 = 1.0 / (F.h * F.h);
+  const int ri = x - o;
+  const int Ia = floordiv2(ri);
+  const bool ox = (ri & 1) != 0;
+  const bool i0in = Ia >= 0 && Ia < G.nx, i1in = (Ia + 1) >= 0 && (Ia + 1) < G.nx;
+  auto interp = [&](int yy) -> double2 {
+    const int rj = yy - o;
+    const int Ja = floordiv2(rj);
+    const bool oy = (rj & 1) != 0;
+    auto ev = [&](int J, int Ii, bool iin) -> double2 {
+      return (iin && J >= 0 && J < G.ny) ? e[(size_t)J * G.nx + Ii] : czero();
+    };
+    const double2 e00 = ev(Ja, Ia, i0in);
+    if (!ox && !oy) return e00;
+    if (ox && !oy) return cadd(cscale(0.5, e00), cscale(0.5, ev(Ja, Ia + 1, i1in)));
+    if (!ox && oy) return cadd(cscale(0.5, e00), cscale(0.5, ev(Ja + 1, Ia, i0in)));
+    return cadd(cadd(cscale(0.25, e00), cscale(0.25, ev(Ja, Ia + 1, i1in))),
+                cadd(cscale(0.25, ev(Ja + 1, Ia, i0in)), cscale(0.25, ev(Ja + 1, Ia + 1, i1in))));
+  };
+  const int y0 = ya - 1, y1 = yb;   // rows of u consumed; f, k, q of row y are used one row later
+  auto issue = [&](int yy) {
+    const int slot = (yy - y0) % PF;
+    const bool uok = xin && yy >= 0 && yy < F.ny && yy <= y1;
+    const bool ook = xown && yy >= ya && yy < yb;
+    const size_t pu = uok ? (size_t)yy * F.nx + x : 0;
+    const size_t po = ook ? (size_t)yy * F.nx + x : 0;
+    cpa16(&ru[slot][lane], u + pu, uok);
+    cpa16(&rf[slot][lane], f + po, ook);
+    cpa8(&rk[slot][lane], k + po, ook);
+    if (addq) cpa16(&rq[slot][lane], addq + po, ook);
+    cpa_commit();
+  };
+#pragma unroll
+  for (int q = 0; q < PF; ++q) issue(y0 + q);
+  double2 v1m2 = czero(), v1m1 = czero();
+  double2 fcur = czero(), qcur = czero();
+  double kcur = 0.0;
+  double2 e0 = czero(), e1 = czero();   // INT: e at (Ja, Ia), (Ja + 1, Ia)
+  int eJ = -1 << 30;
+  for (int y = y0; y <= y1; ++y) {
+    cpa_wait<PF - 1>();
+    const int slot = (y - y0) % PF;
+    const double2 ucur = ru[slot][lane];
+    const double2 fnew = rf[slot][lane];
+    const double knew = rk[slot][lane];
+    const double2 qnew = addq ? rq[slot][lane] : czero();
+    issue(y + PF);
+    double2 v10 = czero();
+    if (INT) {
+      // coarse rows Ja, Ja + 1 of this fine row: each coarse value is loaded once (kept while
+      // two fine rows use it) and column Ia + 1 comes from the next lane (whose base column
+      // it is when ri is odd; lanes 0 and 31 only feed halo lanes, which store nothing)
+      const int rj = y - o;
+      const int Ja = floordiv2(rj);
+      const bool oy = (rj & 1) != 0;
+      if (Ja != eJ) {
+        if (Ja == eJ + 1) {
+          e0 = e1;
+        } else {
+          e0 = (Ja >= 0 && Ja < G.ny && i0in) ? e[(size_t)Ja * G.nx + Ia] : czero();
+        }
+        e1 = (Ja + 1 < G.ny && Ja + 1 >= 0 && i0in) ? e[(size_t)(Ja + 1) * G.nx + Ia] : czero();
+        eJ = Ja;
+      }
+      const double2 e01 = shfl_dn2(e0, 1), e11 = shfl_dn2(e1, 1);
+      double2 ip;
+      if (!ox && !oy) ip = e0;
+      else if (ox && !oy) ip = cadd(cscale(0.5, e0), cscale(0.5, e01));
+      else if (!ox && oy) ip = cadd(cscale(0.5, e0), cscale(0.5, e1));
+      else ip = cadd(cadd(cscale(0.25, e0), cscale(0.25, e01)), cadd(cscale(0.25, e1), cscale(0.25, e11)));
+      v10 = cadd(ip, ucur);
+    } else if (xin && y >= 0 && y < F.ny) {
+      v10 = cadd(interp(y), ucur);
+    }
+    const int yr = y - 1;
+    const double2 uw = shfl_up2(v1m1, 1), ue = shfl_dn2(v1m1, 1);
+    if (xown && yr >= ya && yr < yb) {
+      const size_t p = (size_t)yr * F.nx + x;
+      double2 res, ap;
+      if (INT) {
+        ap = interior_ap(ih2, kcur, sr, si);
+        res = csub(cscale(fs, fcur), interior_stencil(ih2, ap, v1m1, uw, ue, v1m2, v10));
+      } else {
+        const Coef c = coef_at(F, x, yr, kcur, sr, si);
+        ap = c.ap;
+        res = csub(cscale(fs, fcur), stencil5(c, v1m1, uw, ue, v1m2, v10));
+      }
+      double2 out = cadd(v1m1, cscale(omega, cdiv(res, ap)));
+      if (addq) out = cadd(out, qcur);
+      yo[p] = out;
+    }
+    v1m2 = v1m1;
+    v1m1 = v10;
+    fcur = fnew;
+    kcur = knew;
+    qcur = qnew;
+  }
+  cpa_wait<0>();
+}
+
+template <int PF, int SEG = COL_SEG>
+__global__ void __launch_bounds__(128) k_vc_up_cpa(Geo F, Geo G, int o, const double2* __restrict__ u,
+                                                   const double2* __restrict__ e, DVec fv,
+                                                   const double* __restrict__ k, double sr, double si, double omega,
+                                                   const double2* __restrict__ addq, DVec yv) {
+  HELM_PDL_ENTRY();
+  __shared__ double2 ru[4][PF][32];
+  __shared__ double2 rf[4][PF][32];
+  __shared__ double2 rq[4][PF][32];
+  __shared__ double rk[4][PF][32];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int xo = (blockIdx.x * 4 + wq) * COL_OWN;
+  if (xo >= F.nx) return;
+  const int ya = blockIdx.y * SEG;
+  const int yb = min(F.ny, ya + SEG);
+  const bool interior = xo - 2 >= 1 && xo + 29 <= F.nx - 2 && ya - 2 >= 1 && yb <= F.ny - 2;
+  if (interior)
+    up_cpa_body<PF, SEG, true>(F, G, o, u, e, fv.get(), fv.scale(), k, sr, si, omega, addq, yv.get(), ru[wq], rf[wq],
+                               rq[wq], rk[wq], lane, xo, ya, yb);
+  else
+    up_cpa_body<PF, SEG, false>(F, G, o, u, e, fv.get(), fv.scale(), k, sr, si, omega, addq, yv.get(), ru[wq],
+                                rf[wq], rq[wq], rk[wq], lane, xo, ya, yb);
 }
 
 // ------------------------------------------------------------------ cluster tail

@@ -118,20 +118,23 @@ def test_vcycle(case):
         assert rel(u, oracle.vcycle(levels, f, l)) < 1e-11, l
 
 
-@pytest.mark.parametrize("nu,tail,col", [((1, 1), 65536, -1), ((1, 1), 8192, -1), ((2, 2), 8192, -1), ((2, 2), 0, -1),
-                                         ((1, 0), 8192, -1), ((3, 1), 0, -1), ((1, 1), 0, 0), ((1, 1), 0, 500)])
-def test_vcycle_variants(lib, nu, tail, col):
+@pytest.mark.parametrize("nu,tail,col,pipe", [((1, 1), 65536, -1, 0), ((1, 1), 8192, -1, 0), ((2, 2), 8192, -1, 0),
+                                              ((2, 2), 0, -1, 0), ((1, 0), 8192, -1, 0), ((3, 1), 0, -1, 0),
+                                              ((1, 1), 0, 0, 0), ((1, 1), 0, 500, 0), ((1, 1), 0, 0, 1), ((1, 1), 0, 0, 24), ((1, 1), 0, 0, 4),
+                                              ((1, 1), 0, 0, 6)])
+def test_vcycle_variants(lib, nu, tail, col, pipe):
     """Generic sweep counts (unfused kernels), the per-level path (tail 0, the default), the
     thread-block-cluster tail (levels distributed over the cluster's shared memories) and the
     column-streaming legs (col_min_n: 0 = every level, 500 = the larger ones)."""
     for p in (GRIDS[1], GRIDS[2], GRIDS[5]):
         H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"nu_pre": nu[0], "nu_post": nu[1], "tail_max_n": tail,
-                                                  "col_min_n": col})
+                                                  "col_min_n": col, "col_pipe": pipe})
         levels = oracle.build_hierarchy(p.k, p.h, p.bc)
         for l in range(min(3, len(levels))):
             f = random_field(levels[l].shape, 50 + l)
             u = H.vcycle(l, gpu(f)).cpu().numpy()
-            assert rel(u, oracle.vcycle(levels, f, l, nu_pre=nu[0], nu_post=nu[1])) < 1e-11, (p.shape, l, nu, tail, col)
+            assert rel(u, oracle.vcycle(levels, f, l, nu_pre=nu[0], nu_post=nu[1])) < 1e-11, (p.shape, l, nu, tail, col,
+                                                                                                  pipe)
         H.close()
 
 
@@ -324,3 +327,18 @@ def test_solve_gcr(lib, name, vec, op, itol, imax):
     assert re_["outer_iterations"] == rep2["outer_iterations"] and torch.equal(xe, x2)
     H.close()
     He.close()
+
+
+@pytest.mark.parametrize("pipe", [1, 24, 0])
+def test_column_legs_interior_segments(lib, pipe):
+    """Grids large enough that whole column segments (256 / 128 rows, 28 columns) lie in the
+    interior, so the branch-free interior forms of the cp.async legs run next to the boundary
+    forms (col_min_n = 0: every level uses the column legs)."""
+    for p in (P(255, 767, 1 / 256, "dirichlet", random_k((767, 255), 7, 10, 200)),
+              P(257, 769, 1 / 256, "sommerfeld", random_k((769, 257), 8, 10, 200))):
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"col_min_n": 0, "col_pipe": pipe})
+        levels = oracle.build_hierarchy(p.k, p.h, p.bc)
+        f = random_field(p.shape, 77)
+        u = H.vcycle(0, gpu(f)).cpu().numpy()
+        assert rel(u, oracle.vcycle(levels, f, 0)) < 1e-11, (p.shape, pipe)
+        H.close()
