@@ -335,7 +335,7 @@ __device__ __forceinline__ void interp_w(int r, double& wm, double& w0, double& 
 // Block = 32 x 8 threads; every phase walks its region row by row (threadIdx.y) and column by
 // column (threadIdx.x), so no division/modulo in the index math.
 template <int R, int MODE, int TCX, int TCY>
-__global__ void __launch_bounds__(256) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
+__global__ void __launch_bounds__(256, 6) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
                                                         DVec fv, DVec yv) {
   HELM_PDL_ENTRY();
   constexpr int SX = 2 * TCX - 1 + 2 * R, SY = 2 * TCY - 1 + 2 * R;   // s = A t region (fine)

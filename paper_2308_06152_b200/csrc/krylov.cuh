@@ -16,6 +16,7 @@
 // chunking, fixed warp trees, one warp per output in a second stage).
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -67,7 +68,7 @@ inline GsGeom gs_geom(long long n, int sms) {
   const long long per = (subs + 65535) / 65536;
   g.chunk = per * 256;
   g.gx = (int)((n + g.chunk - 1) / g.chunk);
-  const int target = 8 * sms;
+  const int target = (getenv("HELM_GS_TARGET") ? atoi(getenv("HELM_GS_TARGET")) : 8) * sms;
   g.gy = std::max(1, std::min(16, target / std::max(1, g.gx)));
   const long long tiles = (n + 127) / 128;   // DU_ELEMS
   g.gu = (int)std::max<long long>(1, std::min<long long>(tiles, (long long)8 * sms));
@@ -315,7 +316,13 @@ __device__ __forceinline__ void dcgs_dots_item(const double2* __restrict__ V, lo
   }
 }
 
-__global__ void __launch_bounds__(DC_THREADS) k_dcgs_dots(const double2* __restrict__ V, long long ld,
+#ifndef HELM_DC_MINB
+#define HELM_DC_MINB 1
+#endif
+#ifndef HELM_DU_MINB
+#define HELM_DU_MINB 1
+#endif
+__global__ void __launch_bounds__(DC_THREADS, HELM_DC_MINB) k_dcgs_dots(const double2* __restrict__ V, long long ld,
                                                           const int* __restrict__ nptr, int nadd, DVec xv, DVec wv,
                                                           long long n, long long chunk, double2* __restrict__ part) {
   HELM_PDL_ENTRY();
@@ -426,7 +433,7 @@ __device__ __forceinline__ double block_sum(double v) {
   return t;
 }
 
-__global__ void __launch_bounds__(DU_THREADS) k_dcgs_update(const double2* __restrict__ V, long long ld,
+__global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const double2* __restrict__ V, long long ld,
                                                             const int* __restrict__ jptr,
                                                             const double2* __restrict__ coef,
                                                             const double2* __restrict__ sc2, DVec xv, DVec wv,
@@ -452,8 +459,12 @@ __global__ void __launch_bounds__(DU_THREADS) k_dcgs_update(const double2* __res
   const double t = block_sum(nrm);
   if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
   // step B in the last block to finish (sab is free again: it doubles as step B's scratch)
+#ifndef HELM_PROBE_NO_STEPB
   if (st && last_block(counter) && threadIdx.x < 32)
     dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, part, gridDim.x, rawc, hcond, use_h, sab);
+#else
+  if (st && last_block(counter) && threadIdx.x == 0) st->j = min(st->j + 1, st->m - 1);
+#endif
 }
 
 // The whole delayed-CGS2 step of one iteration as ONE cooperative kernel (small grids, where
@@ -539,8 +550,10 @@ __global__ void __launch_bounds__(256) k_dcgs_reduceA(const double2* __restrict_
     dots[c] = make_double2(0.0, 0.0);   // unused tail zeroed: a rank-sum over all slots stays finite
   }
   // counter == null (decomposed solve): the sums are per rank; step A runs after the allreduce
+#ifndef HELM_PROBE_NO_STEPA
   if (counter && last_block(counter) && threadIdx.x < 32)
     dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, sra);
+#endif
 }
 
 // Step A / step B as one-warp kernels (decomposed solve: they follow the rank-sum of the dots
@@ -614,6 +627,54 @@ __device__ __forceinline__ double new_rotation(int j, double2 a, double hn, doub
 // dots[2c] = a_c = V_c^H v~_j, dots[2c+1] = b_c = V_c^H w (c <= j); out: coef (a, b for c < j),
 // sc2 = {1/beta, h_jj}.  rawc holds the raw (unrotated) column j-1 from step B.
 // (executed by one warp; sdc = dcgs_smem(m) bytes of shared memory)
+// Apply the rotations G_0..G_{nrot-1} to col[0..nrot] (shared memory) with the whole warp: the
+// carried entry obeys the linear recurrence a_{i+1} = -conj(s_i) a_i + c_i col[i+1] (a_0 =
+// col[0]), evaluated as an inclusive scan of affine maps over 32 rotations at a time; then
+// col[i] = c_i a_i + s_i col[i+1].  Returns a_nrot (the entry at position nrot before the new
+// rotation) on every lane.  Replaces the 1-lane loop (j dependent steps) by ceil(j/32) x 5.
+__device__ __forceinline__ double2 rotate_column_warp(double2* col, int nrot, const double* scs, const double2* ssn) {
+  const int lane = threadIdx.x & 31;
+  double2 carry = col[0];
+  for (int base = 0; base < nrot; base += 32) {
+    const int i = base + lane;
+    double c = 0.0;
+    double2 s = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+    double2 al = make_double2(1.0, 0.0), be = make_double2(0.0, 0.0);
+    if (i < nrot) {
+      c = scs[i];
+      s = ssn[i];
+      b = col[i + 1];
+      al = make_double2(-s.x, s.y);   // -conj(s)
+      be = cscale(c, b);
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {   // F_lane = f_lane o ... o f_base
+      const double2 alp = make_double2(__shfl_up_sync(0xffffffffu, al.x, d), __shfl_up_sync(0xffffffffu, al.y, d));
+      const double2 bep = make_double2(__shfl_up_sync(0xffffffffu, be.x, d), __shfl_up_sync(0xffffffffu, be.y, d));
+      if (lane >= d) {
+        be = cadd(cmul(al, bep), be);
+        al = cmul(al, alp);
+      }
+    }
+    const double2 anext = cadd(cmul(al, carry), be);   // a_{i+1}
+    double2 ai = make_double2(__shfl_up_sync(0xffffffffu, anext.x, 1), __shfl_up_sync(0xffffffffu, anext.y, 1));
+    if (lane == 0) ai = carry;
+    __syncwarp();
+    if (i < nrot) col[i] = cadd(cscale(c, ai), cmul(s, b));
+    const int last = min(31, nrot - 1 - base);
+    carry = make_double2(__shfl_sync(0xffffffffu, anext.x, last), __shfl_sync(0xffffffffu, anext.y, last));
+    __syncwarp();
+  }
+  return carry;
+}
+
+// Step A (after pass 1): beta, h_jj, the pass-2 coefficients, and the delayed correction of
+// column j-1:  A z_{j-1} = V h + h_{j,j-1} v~_j = V (h + h_{j,j-1} a) + (h_{j,j-1} beta) v_j.
+// The rotation of column j-1 is undone on g and recomputed from the corrected column.
+// dots[2c] = a_c = V_c^H v~_j, dots[2c+1] = b_c = V_c^H w (c <= j); out: coef (a, b for c < j),
+// sc2 = {1/beta, h_jj}.  rawc holds the raw (unrotated) column j-1 from step B.
+// (executed by one warp; sdc = dcgs_smem(m) bytes of shared memory.)  Every global load that
+// does not depend on the dots is issued up front, so the step costs ~2 memory round trips.
 __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
                                 const double2* __restrict__ dots, double2* __restrict__ coef,
                                 double2* __restrict__ sc2, double2* __restrict__ rawc, double2* sdc) {
@@ -623,6 +684,28 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
   double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
   const int lane = threadIdx.x & 31;
   const int j = st->j;
+  const int jm = j - 1;
+  // independent loads first
+  const double hold = j > 0 ? rawc[j].x : 0.0;   // h_{j,j-1} (real)
+  double c0 = 0.0, bnorm = 0.0;
+  double2 s0 = make_double2(0.0, 0.0), gjm = s0, gj = s0, g0 = s0;
+  if (lane == 0) {
+    bnorm = st->bnorm;
+    g0 = g[0];
+    if (j > 0) {
+      c0 = cs[jm];
+      s0 = sn[jm];
+      gjm = g[jm];
+      gj = g[j];
+    }
+  }
+  for (int i = lane; i < jm; i += 32) {
+    ssn[i] = sn[i];
+    scs[i] = cs[i];
+  }
+  for (int c = lane; c < j; c += 32) scol[c] = rawc[c];
+  const double alpha = dots[2 * j].x;
+  const double2 d = dots[2 * j + 1];
   // ||a||^2 and a^H b over c < j
   double na = 0.0;
   double2 ab = make_double2(0.0, 0.0);
@@ -636,8 +719,6 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
   ab = warp_sum2(ab);
-  const double alpha = dots[2 * j].x;
-  const double2 d = dots[2 * j + 1];
   double b2 = alpha - na;
   if (!(b2 > 0.0)) b2 = alpha;               // guard (cannot happen for an orthonormal basis)
   const double beta = sqrt(b2);
@@ -645,41 +726,30 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
   for (int c = lane; c < j; c += 32) {
     const double2 a = dots[2 * c];
     coef[2 * c] = make_double2(-a.x / beta, -a.y / beta);
+    scol[c] = cadd(scol[c], cscale(hold, a));   // corrected raw column j-1
   }
   if (lane == 0) {
     sc2[0] = make_double2(1.0 / beta, 0.0);
     sc2[1] = hjj;
-    if (j == 0) g[0] = cscale(beta, g[0]);   // r = ||r|| v~_0 = (||r|| beta) v_0
+    if (j == 0) g[0] = cscale(beta, g0);     // r = ||r|| v~_0 = (||r|| beta) v_0
   }
   if (j == 0) return;
   // delayed correction of column j-1
-  const int jm = j - 1;
-  const double hold = rawc[j].x;             // h_{j,j-1} (real)
-  for (int c = lane; c < j; c += 32) {
-    const double2 a = dots[2 * c];
-    scol[c] = cadd(rawc[c], cscale(hold, a));
-  }
-  for (int i = lane; i < jm; i += 32) {
-    ssn[i] = sn[i];
-    scs[i] = cs[i];
-  }
+  const double hnew = hold * beta;
+  if (lane == 0) scol[j] = make_double2(hnew, 0.0);
   __syncwarp();
+  for (int c = lane; c <= j; c += 32) rawc[c] = scol[c];   // corrected raw column (kept for the record)
+  __syncwarp();
+  const double2 a = rotate_column_warp(scol, jm, scs, ssn);
   if (lane == 0) {
-    const double hnew = hold * beta;
-    scol[j] = make_double2(hnew, 0.0);
     // undo the old rotation G_{j-1} on g: g_{j-1}^old = c g_{j-1} - s g_j
-    const double c0 = cs[jm];
-    const double2 s0 = sn[jm];
-    const double2 gjm = g[jm], gj = g[j];
     g[jm] = csub(cscale(c0, gjm), cmul(s0, gj));
     g[j] = make_double2(0.0, 0.0);
-    for (int c = 0; c <= j; ++c) rawc[c] = scol[c];   // corrected raw column (kept for the record)
-    const double2 a = rotate_column(scol, jm, scs, ssn);
     double2 hjj1;
     const double gn = new_rotation(jm, a, hnew, cs, sn, g, &hjj1);
     scol[jm] = hjj1;
     scol[j] = make_double2(0.0, 0.0);
-    st->relres = st->bnorm > 0.0 ? gn / st->bnorm : 0.0;
+    st->relres = bnorm > 0.0 ? gn / bnorm : 0.0;
   }
   __syncwarp();
   const int ld = m + 1;
@@ -700,36 +770,47 @@ __device__ void dcgs_stepB_warp(FgmState* st, double2* H, double* cs, double2* s
   double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
   const int lane = threadIdx.x & 31;
   const int j = st->j;
-  double nsum = 0.0;
-  for (int b = lane; b < np; b += 32) nsum += npart[b].x;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-  const double hn = sqrt(fmax(nsum, 0.0));
+  double bnorm = 0.0, tol = 0.0;
+  int its = 0, maxit = 0;
+  if (lane == 0) {
+    bnorm = st->bnorm;
+    tol = st->tol;
+    its = st->its;
+    maxit = st->maxit;
+  }
   for (int c = lane; c < j; c += 32) scol[c] = dots[2 * c + 1];
   for (int i = lane; i < j; i += 32) {
     ssn[i] = sn[i];
     scs[i] = cs[i];
   }
+  if (lane == 0) scol[j] = sc2[1];
+  double nsum = 0.0;
+  for (int b = lane; b < np; b += 32) nsum += npart[b].x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+  const double hn = sqrt(fmax(nsum, 0.0));
   __syncwarp();
+  for (int c = lane; c <= j; c += 32) rawc[c] = scol[c];
+  if (lane == 0) rawc[j + 1] = make_double2(hn, 0.0);
+  __syncwarp();
+  const double2 a = rotate_column_warp(scol, j, scs, ssn);
   if (lane == 0) {
-    scol[j] = sc2[1];
-    for (int c = 0; c <= j; ++c) rawc[c] = scol[c];
-    rawc[j + 1] = make_double2(hn, 0.0);
-    const double2 a = rotate_column(scol, j, scs, ssn);
     double2 rjj;
     const double gn = new_rotation(j, a, hn, cs, sn, g, &rjj);
     scol[j] = rjj;
     scol[j + 1] = make_double2(0.0, 0.0);
-    st->its += 1;
+    its += 1;
+    st->its = its;
     st->ncols = j + 1;
-    st->relres = st->bnorm > 0.0 ? gn / st->bnorm : 0.0;
+    const double relres = bnorm > 0.0 ? gn / bnorm : 0.0;
+    st->relres = relres;
     st->hn = hn;
     st->inv_hn = hn > 0.0 ? 1.0 / hn : 0.0;
     int done = 0;
-    if (st->relres <= st->tol || hn == 0.0) {
+    if (relres <= tol || hn == 0.0) {
       done = 1;
       st->conv = 1;
-    } else if (st->its >= st->maxit || j + 1 >= st->m) {
+    } else if (its >= maxit || j + 1 >= m) {
       done = 1;
     }
     st->done = done;

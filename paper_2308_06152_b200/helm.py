@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libhelm.so")
+_LIB_PATH = os.environ.get("HELM_LIB") or os.path.join(_HERE, "libhelm.so")
 
 HELM_BC_DIRICHLET = 0
 HELM_BC_SOMMERFELD = 1

@@ -1,0 +1,36 @@
+"""A/B of the delayed-CGS2 step: in-graph DCGS step time at several basis sizes and the full
+c1_k400 solve, for the library in $HELM_LIB (tools/build_variants.py) and $HELM_GS_TARGET."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2308_06152_b200 import helm  # noqa: E402
+from workloads import config_problem  # noqa: E402
+
+p = config_problem("c1_k400")
+H = helm.helm_setup(p, {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": 50,
+                        "coarsest_n": 512})
+out = {"lib": os.path.basename(os.environ.get("HELM_LIB", "libhelm.so")), "target": os.environ.get("HELM_GS_TARGET", "8")}
+for j in (5, 25, 45):
+    out[f"dcgs{j}"] = round(H.helm_bench_graph("dcgs", j, 3), 2)
+out["vcycle1"] = round(H.helm_bench_graph("vcycle", 1, 20), 2)
+out["apply_E"] = round(H.helm_bench_graph("apply_E", 0, 50), 2)
+if os.environ.get("HELM_PROBE_NOSOLVE"):
+    print(json.dumps(out), flush=True)
+    sys.exit(0)
+b = torch.from_numpy(p.b).cuda()
+x = torch.empty_like(b)
+for _ in range(2):
+    H.solve(b, 1e-6, 2000, x)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(3):
+    _, rep = H.solve(b, 1e-6, 2000, x)
+torch.cuda.synchronize()
+out["solve_s"] = round((time.perf_counter() - t0) / 3, 4)
+out["its"] = rep["outer_iterations"]
+print(json.dumps(out), flush=True)
