@@ -671,7 +671,7 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(dalloc(&K.rawc, (size_t)m + 2));
   CKR(dalloc(&K.nrm, 2));
   K.geo = gs_geom((long long)n, C.sm_count);
-  CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * K.geo.gx, (size_t)K.geo.gu)));
+  CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * K.geo.gx, (size_t)K.geo.gu + 1)));
   CKR(dalloc(&K.st, 1));
   CK(cudaMemsetAsync(K.st, 0, sizeof(FgmState), C.s));
   // dynamic shared memory grows with the basis; the limits are raised once to the largest
@@ -685,13 +685,13 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
-  CKR(raise_dyn_smem((const void*)k_dcgs_stepA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_stepB, usmem));
+  CKR(raise_dyn_smem((const void*)k_fgm_backsub, std::min<size_t>(96 * 1024, ((size_t)m * (m + 1) / 2 + m) * 16)));
   {
     // pass 2 in one wave: at most as many blocks as can be resident
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_update, DU_THREADS, dcgs_update_smem(m)));
-    if (bps > 0) K.geo.gu = std::max(1, std::min(K.geo.gu, bps * C.sm_count));
+    if (bps > 0) K.geo.gu = std::max(1, std::min(K.geo.gu, bps * C.sm_count - 1));   // + the step-A block
   }
   // cooperative one-kernel step for small vectors (latency-bound regime)
   K.coop = 0;
@@ -851,33 +851,34 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
     launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
              gg.chunk, K.part);
     CKR(post_launch(C));
-    // reduction of the pass-1 partials + step A (last block), pass 2 + step B (last block);
-    // decomposed: the per-rank sums are summed over the ranks before each step
+    // reduction of the pass-1 partials; pass 2 with the rotation part of step A in an extra
+    // block and step B in the last block.  Decomposed: the dots are summed over the ranks
+    // before pass 2, |w'|^2 before step B (then a separate one-warp kernel)
     launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H,
-             K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.dist ? nullptr : K.cnt);
+             K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
+    CKR(post_launch(C));
+    if (K.dist) CKR(allreduce(C, K.dots1, 2 * K.m + 2));
+    launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), Vo, ld, (const int*)&st->j,
+             (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1, h, use_h,
+             K.dist ? 2 : 3);
     CKR(post_launch(C));
     if (K.dist) {
-      CKR(allreduce(C, K.dots1, 2 * K.m + 2));
-      launch_k(C, k_dcgs_stepA, 1, 32, asm_, st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1, K.coef, K.sc2,
-               K.rawc);
-      CKR(post_launch(C));
-    }
-    launch_k(C, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), Vo, ld, (const int*)&st->j,
-             (const double2*)K.coef, (const double2*)K.sc2, vjo, wo, ln, K.part, K.dist ? nullptr : st, K.H, K.cs,
-             K.sn, K.g, (const double2*)K.dots1, K.rawc, K.cnt + 1, h, use_h);
-    CKR(post_launch(C));
-    if (K.dist) {
-      launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu, K.nrm);
+      launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu + 1, K.nrm);
       CKR(post_launch(C));
       CKR(allreduce(C, K.nrm, 1));
       launch_k(C, k_dcgs_stepB, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
-               (const double2*)K.sc2, (const double2*)K.nrm, 1, K.rawc, h, use_h);
+               (const double2*)K.nrm, 1, K.rawc, h, use_h);
       CKR(post_launch(C));
     }
     return HELM_OK;
   };
   CKR(run_while(C, st, begin, body));
-  launch_k(C, k_fgm_backsub, 1, 32, 0, st, K.H, K.g, K.y, outer_stats);
+  {
+    // the triangle of an m-column basis in shared memory when it fits (the inner solves)
+    const size_t bs = ((size_t)K.m * (K.m + 1) / 2 + K.m) * sizeof(double2);
+    const bool staged = bs <= 96 * 1024;
+    launch_k(C, k_fgm_backsub, 1, 256, staged ? bs : 0, st, K.H, K.g, K.y, outer_stats, staged ? 1 : 0);
+  }
   CKR(post_launch(C));
   // x = (x or 0) + Z y
   const DVec xo = shift(DVec(x), off);
@@ -1593,12 +1594,12 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         r = post_launch(X);
         if (r != HELM_OK) break;
         launch_k(X, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, dcgs_smem(K.m), K.part, (long long)gg.gx,
-                 st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, K.cnt);
+                 st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
         r = post_launch(X);
         if (r != HELM_OK) break;
-        launch_k(X, k_dcgs_update, gg.gu, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
-                 (const double2*)K.coef, (const double2*)K.sc2, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g,
-                 (const double2*)K.dots1, K.rawc, K.cnt + 1, cudaGraphConditionalHandle(0), 0);
+        launch_k(X, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
+                 (const double2*)K.dots1, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1,
+                 cudaGraphConditionalHandle(0), 0, 3);
         r = post_launch(X);
         break;
       }
@@ -1708,18 +1709,20 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
       case HELM_KB_GS_UPDATE: {
         bytes = (double)G.n * 16.0 * (arg + 3);
         k_dcgs_update<<<K.geo.gu, DU_THREADS, dcgs_update_smem(K.m), X.s>>>(
-            K.V, (long long)K.n, dn, K.coef, K.sc2, DVec(K.V + (size_t)(arg - 1) * K.n), DVec(K.V + (size_t)arg * K.n),
-            (long long)K.n, K.part, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-            cudaGraphConditionalHandle(0), 0);
+            K.V, (long long)K.n, dn, K.dots1, DVec(K.V + (size_t)(arg - 1) * K.n), DVec(K.V + (size_t)arg * K.n),
+            (long long)K.n, K.part, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+            cudaGraphConditionalHandle(0), 0, 0);
         return post_launch(X);
       }
     }
     return fail(HELM_EINVAL, "unknown kernel id %d", which);
   };
   if (which == HELM_KB_GS_UPDATE) {
-    CK(cudaMemsetAsync(K.coef, 0, (size_t)(2 * K.m + 4) * sizeof(double2), X.s));
-    const double2 sc[2] = {make_double2(1.0, 0.0), make_double2(0.0, 0.0)};
-    CK(cudaMemcpyAsync(K.sc2, sc, sizeof sc, cudaMemcpyHostToDevice, X.s));
+    // pass-1 dots giving beta = 1, zero coefficients
+    std::vector<double2> d((size_t)2 * K.m + 4, make_double2(0.0, 0.0));
+    d[(size_t)2 * (arg - 1)] = make_double2(1.0, 0.0);
+    CK(cudaMemcpyAsync(K.dots1, d.data(), d.size() * sizeof(double2), cudaMemcpyHostToDevice, X.s));
+    CK(cudaStreamSynchronize(X.s));
   }
   CKR(launch());   // warm-up
   cudaEvent_t e0, e1;

@@ -215,9 +215,14 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
                                 const double2* __restrict__ dots, double2* __restrict__ coef,
                                 double2* __restrict__ sc2, double2* __restrict__ rawc, double2* sdc);
 __device__ void dcgs_stepB_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
-                                const double2* __restrict__ dots, const double2* __restrict__ sc2,
+                                const double2* __restrict__ dots, double2 hjj,
                                 const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
                                 cudaGraphConditionalHandle h, int use_h, double2* sdc);
+__device__ void dcgs_coefs_warp(int j, const double2* __restrict__ dots, double2* coefs, double* sbeta,
+                                double2* shjj);
+__device__ void dcgs_stepA_rot_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                    const double2* __restrict__ dots, double2* __restrict__ rawc, double beta,
+                                    double2* sdc);
 
 
 constexpr int DC_THREADS = 128;           // dots: 4 warps per block
@@ -433,38 +438,46 @@ __device__ __forceinline__ double block_sum(double v) {
   return t;
 }
 
+// flags: 1 = step B in the last block to finish; 2 = the grid has one extra block (block 0) that runs
+// the rotation part of step A (column j-1) while the others stream pass 2 -- off the critical
+// path, since only step B needs it.  Every block derives the pass-2 coefficients from the
+// pass-1 dots itself (warp 0, identical arithmetic in every block).
 __global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const double2* __restrict__ V, long long ld,
                                                             const int* __restrict__ jptr,
-                                                            const double2* __restrict__ coef,
-                                                            const double2* __restrict__ sc2, DVec xv, DVec wv,
+                                                            const double2* __restrict__ dots, DVec xv, DVec wv,
                                                             long long n, double2* __restrict__ part,
                                                             FgmState* st, double2* H, double* cs, double2* sn,
-                                                            double2* g, const double2* __restrict__ dots,
-                                                            double2* __restrict__ rawc, unsigned* counter,
-                                                            cudaGraphConditionalHandle hcond, int use_h) {
+                                                            double2* g, double2* __restrict__ rawc, unsigned* counter,
+                                                            cudaGraphConditionalHandle hcond, int use_h, int flags) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 sab[];
   __shared__ DuRed<DU_WARPS, DU_ELEMS / 32> red;
+  __shared__ double s_beta;
+  __shared__ double2 s_hjj;
   const int j = *jptr;
-  for (int c = threadIdx.x; c < 2 * j; c += DU_THREADS) sab[c] = coef[c];
+  if (threadIdx.x < 32) dcgs_coefs_warp(j, dots, sab, &s_beta, &s_hjj);
   __syncthreads();
-  const double ib = sc2[0].x * xv.scale();
-  const double2 hjj = sc2[1];
-  double2* x = xv.get();
-  double2* w = wv.get();
+  // the extra block is block 0, so that it is scheduled first
+  const bool extra = (flags & 2) && blockIdx.x == 0;
+  const int nb = (flags & 2) ? (int)gridDim.x - 1 : (int)gridDim.x;
+  const int tb = (flags & 2) ? (int)blockIdx.x - 1 : (int)blockIdx.x;
   double nrm = 0.0;
-  const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
-  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x)
-    nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
+  if (extra) {
+    if (threadIdx.x < 32) dcgs_stepA_rot_warp(st, H, cs, sn, g, dots, rawc, s_beta, sab);
+  } else {
+    const double ib = (1.0 / s_beta) * xv.scale();
+    const double2 hjj = s_hjj;
+    double2* x = xv.get();
+    double2* w = wv.get();
+    const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
+    for (long long tile = tb; tile < tiles; tile += nb)
+      nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
+  }
   const double t = block_sum(nrm);
   if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
   // step B in the last block to finish (sab is free again: it doubles as step B's scratch)
-#ifndef HELM_PROBE_NO_STEPB
-  if (st && last_block(counter) && threadIdx.x < 32)
-    dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, part, gridDim.x, rawc, hcond, use_h, sab);
-#else
-  if (st && last_block(counter) && threadIdx.x == 0) st->j = min(st->j + 1, st->m - 1);
-#endif
+  if ((flags & 1) && last_block(counter) && threadIdx.x < 32)
+    dcgs_stepB_warp(st, H, cs, sn, g, dots, s_hjj, part, gridDim.x, rawc, hcond, use_h, sab);
 }
 
 // The whole delayed-CGS2 step of one iteration as ONE cooperative kernel (small grids, where
@@ -527,7 +540,7 @@ __global__ void __launch_bounds__(DC_THREADS) k_dcgs_step(const double2* __restr
   }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x < 32)
-    dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, npart, gridDim.x, rawc, hcond, use_h, dsm);
+    dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2[1], npart, gridDim.x, rawc, hcond, use_h, dsm);
 }
 
 // Pass-1 reduction (2(j+1) outputs, one warp each) with step A in the last block to finish.
@@ -550,29 +563,24 @@ __global__ void __launch_bounds__(256) k_dcgs_reduceA(const double2* __restrict_
     dots[c] = make_double2(0.0, 0.0);   // unused tail zeroed: a rank-sum over all slots stays finite
   }
   // counter == null (decomposed solve): the sums are per rank; step A runs after the allreduce
-#ifndef HELM_PROBE_NO_STEPA
   if (counter && last_block(counter) && threadIdx.x < 32)
     dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, sra);
-#endif
 }
 
-// Step A / step B as one-warp kernels (decomposed solve: they follow the rank-sum of the dots
-// and of |w'|^2; same code as the last-block forms above).
-__global__ void k_dcgs_stepA(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
-                             const double2* __restrict__ dots, double2* __restrict__ coef,
-                             double2* __restrict__ sc2, double2* __restrict__ rawc) {
-  HELM_PDL_ENTRY();
-  extern __shared__ double2 sra[];
-  if (threadIdx.x < 32) dcgs_stepA_warp(st, H, cs, sn, g, dots, coef, sc2, rawc, sra);
-}
-
+// Step B as a one-warp kernel (decomposed solve: after the rank-sum of |w'|^2); h_jj is
+// recomputed from the (rank-summed) dots exactly as the update kernel's blocks do.
 __global__ void k_dcgs_stepB(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
-                             const double2* __restrict__ dots, const double2* __restrict__ sc2,
-                             const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
-                             cudaGraphConditionalHandle hcond, int use_h) {
+                             const double2* __restrict__ dots, const double2* __restrict__ npart, int np,
+                             double2* __restrict__ rawc, cudaGraphConditionalHandle hcond, int use_h) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 srb[];
-  if (threadIdx.x < 32) dcgs_stepB_warp(st, H, cs, sn, g, dots, sc2, npart, np, rawc, hcond, use_h, srb);
+  __shared__ double s_beta;
+  __shared__ double2 s_hjj;
+  if (threadIdx.x < 32) {
+    dcgs_coefs_warp(st->j, dots, srb, &s_beta, &s_hjj);
+    __syncwarp();
+    dcgs_stepB_warp(st, H, cs, sn, g, dots, s_hjj, npart, np, rawc, hcond, use_h, srb);
+  }
 }
 
 // out[0] = sum of np partials (one warp, fixed order)
@@ -675,38 +683,13 @@ __device__ __forceinline__ double2 rotate_column_warp(double2* col, int nrot, co
 // sc2 = {1/beta, h_jj}.  rawc holds the raw (unrotated) column j-1 from step B.
 // (executed by one warp; sdc = dcgs_smem(m) bytes of shared memory.)  Every global load that
 // does not depend on the dots is issued up front, so the step costs ~2 memory round trips.
-__device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
-                                const double2* __restrict__ dots, double2* __restrict__ coef,
-                                double2* __restrict__ sc2, double2* __restrict__ rawc, double2* sdc) {
-  const int m = st->m;
-  double2* scol = sdc;                       // m + 2
-  double2* ssn = sdc + (m + 2);              // m + 2
-  double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
+// Pass-2 coefficients from the pass-1 dots (one warp): coefs[2c] = -a_c/beta,
+// coefs[2c+1] = -b_c (c < j); beta = sqrt(dots[2j] - ||a||^2), h_jj = (dots[2j+1] - a^H b)/beta.
+__device__ void dcgs_coefs_warp(int j, const double2* __restrict__ dots, double2* coefs, double* sbeta,
+                                double2* shjj) {
   const int lane = threadIdx.x & 31;
-  const int j = st->j;
-  const int jm = j - 1;
-  // independent loads first
-  const double hold = j > 0 ? rawc[j].x : 0.0;   // h_{j,j-1} (real)
-  double c0 = 0.0, bnorm = 0.0;
-  double2 s0 = make_double2(0.0, 0.0), gjm = s0, gj = s0, g0 = s0;
-  if (lane == 0) {
-    bnorm = st->bnorm;
-    g0 = g[0];
-    if (j > 0) {
-      c0 = cs[jm];
-      s0 = sn[jm];
-      gjm = g[jm];
-      gj = g[j];
-    }
-  }
-  for (int i = lane; i < jm; i += 32) {
-    ssn[i] = sn[i];
-    scs[i] = cs[i];
-  }
-  for (int c = lane; c < j; c += 32) scol[c] = rawc[c];
   const double alpha = dots[2 * j].x;
   const double2 d = dots[2 * j + 1];
-  // ||a||^2 and a^H b over c < j
   double na = 0.0;
   double2 ab = make_double2(0.0, 0.0);
   for (int c = lane; c < j; c += 32) {
@@ -714,7 +697,7 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
     na = fma(a.x, a.x, fma(a.y, a.y, na));
     ab.x = fma(a.x, b.x, fma(a.y, b.y, ab.x));
     ab.y = fma(a.x, b.y, fma(-a.y, b.x, ab.y));
-    coef[2 * c + 1] = make_double2(-b.x, -b.y);   // pass 2 accumulates +coef * V
+    coefs[2 * c + 1] = make_double2(-b.x, -b.y);   // pass 2 accumulates +coef * V
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
@@ -722,19 +705,50 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
   double b2 = alpha - na;
   if (!(b2 > 0.0)) b2 = alpha;               // guard (cannot happen for an orthonormal basis)
   const double beta = sqrt(b2);
-  const double2 hjj = cscale(1.0 / beta, csub(d, ab));
   for (int c = lane; c < j; c += 32) {
     const double2 a = dots[2 * c];
-    coef[2 * c] = make_double2(-a.x / beta, -a.y / beta);
-    scol[c] = cadd(scol[c], cscale(hold, a));   // corrected raw column j-1
+    coefs[2 * c] = make_double2(-a.x / beta, -a.y / beta);
   }
   if (lane == 0) {
-    sc2[0] = make_double2(1.0 / beta, 0.0);
-    sc2[1] = hjj;
-    if (j == 0) g[0] = cscale(beta, g0);     // r = ||r|| v~_0 = (||r|| beta) v_0
+    *sbeta = beta;
+    *shjj = cscale(1.0 / beta, csub(d, ab));
   }
-  if (j == 0) return;
-  // delayed correction of column j-1
+}
+
+// Rotation part of step A: the delayed correction of column j-1,
+//   A z_{j-1} = V h + h_{j,j-1} v~_j = V (h + h_{j,j-1} a) + (h_{j,j-1} beta) v_j,
+// with the rotation of column j-1 undone on g and recomputed from the corrected column (j = 0:
+// g_0 scaled by beta).  rawc holds the raw (unrotated) column j-1 from step B.  One warp; sdc =
+// dcgs_smem(m) bytes; every global load that does not depend on the dots is issued up front.
+__device__ void dcgs_stepA_rot_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                    const double2* __restrict__ dots, double2* __restrict__ rawc, double beta,
+                                    double2* sdc) {
+  const int m = st->m;
+  double2* scol = sdc;                       // m + 2
+  double2* ssn = sdc + (m + 2);              // m + 2
+  double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
+  const int lane = threadIdx.x & 31;
+  const int j = st->j;
+  const int jm = j - 1;
+  if (j == 0) {
+    if (lane == 0) g[0] = cscale(beta, g[0]);   // r = ||r|| v~_0 = (||r|| beta) v_0
+    return;
+  }
+  const double hold = rawc[j].x;             // h_{j,j-1} (real)
+  double c0 = 0.0, bnorm = 0.0;
+  double2 s0 = make_double2(0.0, 0.0), gjm = s0, gj = s0;
+  if (lane == 0) {
+    bnorm = st->bnorm;
+    c0 = cs[jm];
+    s0 = sn[jm];
+    gjm = g[jm];
+    gj = g[j];
+  }
+  for (int i = lane; i < jm; i += 32) {
+    ssn[i] = sn[i];
+    scs[i] = cs[i];
+  }
+  for (int c = lane; c < j; c += 32) scol[c] = cadd(rawc[c], cscale(hold, dots[2 * c]));   // corrected column
   const double hnew = hold * beta;
   if (lane == 0) scol[j] = make_double2(hnew, 0.0);
   __syncwarp();
@@ -757,11 +771,27 @@ __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* s
   for (int i = lane; i <= j; i += 32) Hc[i] = scol[i];
 }
 
+// Step A (after pass 1) in one warp: the pass-2 coefficients into coef / sc2 = {1/beta, h_jj}
+// and the rotation part (cooperative one-kernel step).
+__device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                const double2* __restrict__ dots, double2* __restrict__ coef,
+                                double2* __restrict__ sc2, double2* __restrict__ rawc, double2* sdc) {
+  __shared__ double s_beta;
+  __shared__ double2 s_hjj;
+  dcgs_coefs_warp(st->j, dots, coef, &s_beta, &s_hjj);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    sc2[0] = make_double2(1.0 / s_beta, 0.0);
+    sc2[1] = s_hjj;
+  }
+  dcgs_stepA_rot_warp(st, H, cs, sn, g, dots, rawc, s_beta, sdc);
+}
+
 // Step B (after pass 2): column j = [b_0..b_{j-1}, h_jj] with h_{j+1,j} = ||w'|| (from the
 // pass-2 partials), its rotations, the residual estimate and the loop decision.
 // (executed by one warp; sdc = dcgs_smem(m) bytes of shared memory)
 __device__ void dcgs_stepB_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
-                                const double2* __restrict__ dots, const double2* __restrict__ sc2,
+                                const double2* __restrict__ dots, double2 hjj,
                                 const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
                                 cudaGraphConditionalHandle h, int use_h, double2* sdc) {
   const int m = st->m;
@@ -783,7 +813,7 @@ __device__ void dcgs_stepB_warp(FgmState* st, double2* H, double* cs, double2* s
     ssn[i] = sn[i];
     scs[i] = cs[i];
   }
-  if (lane == 0) scol[j] = sc2[1];
+  if (lane == 0) scol[j] = hjj;
   double nsum = 0.0;
   for (int b = lane; b < np; b += 32) nsum += npart[b].x;
 #pragma unroll
@@ -865,21 +895,45 @@ __global__ void k_fgm_begin(FgmState* st, const double2* __restrict__ nrm2, int 
 
 // Back substitution y = R^{-1} g over the ncols completed columns (one warp), and the
 // inner-solve statistics when `outer` is given.
+// Back substitution R y = g of the rotated Hessenberg matrix (column-major, ld = m + 1).
+// staged != 0 (the triangle fits in the dynamic shared memory): the block loads the triangle
+// and g into shared memory in one parallel sweep, then one warp runs the column-oriented
+// substitution from shared memory (y_q = s_q / R_qq, s_r -= R_rq y_q for r < q) -- the row
+// form below pays a global-memory round trip per row (~70 us for 50 rows).
 __global__ void k_fgm_backsub(FgmState* st, const double2* __restrict__ H, const double2* __restrict__ g,
-                              double2* __restrict__ y, FgmState* outer) {
+                              double2* __restrict__ y, FgmState* outer, int staged) {
   HELM_PDL_ENTRY();
+  extern __shared__ double2 sbs[];
   const int lane = threadIdx.x & 31;
-  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  if (blockIdx.x != 0) return;
   const int mm = st->ncols;
   const int ld = st->m + 1;
-  for (int i = mm - 1; i >= 0; --i) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int q = i + 1 + lane; q < mm; q += 32) s = cfma(H[(long long)q * ld + i], y[q], s);
-    s = warp_sum2(s);
-    if (lane == 0) y[i] = cdiv(csub(g[i], s), H[(long long)i * ld + i]);
-    __syncwarp();
+  if (staged) {
+    double2* tri = sbs;                                  // column q at q (q + 1) / 2, rows 0..q
+    double2* s = sbs + (size_t)mm * (mm + 1) / 2;        // running right-hand side
+    for (int q = 0; q < mm; ++q)
+      for (int r = threadIdx.x; r <= q; r += blockDim.x) tri[q * (q + 1) / 2 + r] = H[(long long)q * ld + r];
+    for (int r = threadIdx.x; r < mm; r += blockDim.x) s[r] = g[r];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      for (int q = mm - 1; q >= 0; --q) {
+        const double2* col = tri + q * (q + 1) / 2;
+        const double2 yq = cdiv(s[q], col[q]);
+        if (lane == 0) y[q] = yq;
+        for (int r = lane; r < q; r += 32) s[r] = csub(s[r], cmul(col[r], yq));
+        __syncwarp();
+      }
+    }
+  } else if (threadIdx.x < 32) {
+    for (int i = mm - 1; i >= 0; --i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int q = i + 1 + lane; q < mm; q += 32) s = cfma(H[(long long)q * ld + i], y[q], s);
+      s = warp_sum2(s);
+      if (lane == 0) y[i] = cdiv(csub(g[i], s), H[(long long)i * ld + i]);
+      __syncwarp();
+    }
   }
-  if (lane == 0 && outer) {
+  if (threadIdx.x == 0 && outer) {
     outer->inner_total += st->its;
     outer->inner_max = max(outer->inner_max, st->its);
     outer->inner_solves += 1;
