@@ -686,7 +686,7 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_stepB, usmem));
-  CKR(raise_dyn_smem((const void*)k_fgm_backsub, std::min<size_t>(96 * 1024, ((size_t)m * (m + 1) / 2 + m) * 16)));
+  CKR(raise_dyn_smem((const void*)k_fgm_backsub, std::min<size_t>(96 * 1024, ((size_t)m * (m + 1) + m) * 16)));
   {
     // pass 2 in one wave: at most as many blocks as can be resident
     int bps = 0;
@@ -875,7 +875,7 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
   CKR(run_while(C, st, begin, body));
   {
     // the triangle of an m-column basis in shared memory when it fits (the inner solves)
-    const size_t bs = ((size_t)K.m * (K.m + 1) / 2 + K.m) * sizeof(double2);
+    const size_t bs = ((size_t)K.m * (K.m + 1) + K.m) * sizeof(double2);
     const bool staged = bs <= 96 * 1024;
     launch_k(C, k_fgm_backsub, 1, 256, staged ? bs : 0, st, K.H, K.g, K.y, outer_stats, staged ? 1 : 0);
   }

@@ -53,6 +53,20 @@ __device__ __forceinline__ double2 warp_sum2(double2 s) {
   return s;
 }
 
+// block sum of a per-thread double (any blockDim <= 1024, multiple of 32), result in thread 0
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double bs[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) bs[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += bs[q];
+  __syncthreads();
+  return t;
+}
+
 // Launch geometry of the Gram-Schmidt passes for a vector length n (host side).
 struct GsGeom {
   long long chunk;  // elements per dots block (x)
@@ -141,7 +155,6 @@ __global__ void __launch_bounds__(GS_THREADS) k_gs_update(const double2* __restr
                                                           double2* __restrict__ part, const int* __restrict__ gate) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 sc[];
-  __shared__ double2 red[GS_WARPS][32];
   if (gate && !*gate) return;
   const int nvec = (nptr ? *nptr : 0) + nadd;
   const double2* win = winv.get();
@@ -150,40 +163,60 @@ __global__ void __launch_bounds__(GS_THREADS) k_gs_update(const double2* __restr
   __syncthreads();
   const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
   double nrm = 0.0;
-  const long long tiles = (n + 31) / 32;
+  // tiles of 128 elements: a lane holds 4 of them and streams its warp's share of the basis
+  // (warp sl takes c = sl, sl + 8, ...; two vectors per step: 8 independent loads in flight);
+  // the 8 warps' sums are combined in a fixed order through shared memory
+  constexpr int EPL = 4, TE = 32 * EPL;
+  __shared__ double2 acc[GS_WARPS][TE];
+  const long long tiles = (n + TE - 1) / TE;
   for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const long long e = tile * 32 + lane;
-    double2 s = make_double2(0.0, 0.0);
-    if (e < n) {
-      const double2* vp = V + e;
-      int c = sl;
-      for (; c + 8 * 3 < nvec; c += 8 * 4) {
-        const double2 v0 = vp[(long long)(c + 0) * ld];
-        const double2 v1 = vp[(long long)(c + 8) * ld];
-        const double2 v2 = vp[(long long)(c + 16) * ld];
-        const double2 v3 = vp[(long long)(c + 24) * ld];
-        s = cfma(sc[c + 0], v0, s);
-        s = cfma(sc[c + 8], v1, s);
-        s = cfma(sc[c + 16], v2, s);
-        s = cfma(sc[c + 24], v3, s);
-      }
-      for (; c < nvec; c += 8) s = cfma(sc[c], vp[(long long)c * ld], s);
-    }
-    red[sl][lane] = s;
-    __syncthreads();
-    if (sl == 0 && e < n) {
-      double2 t = win ? win[e] : make_double2(0.0, 0.0);
+    const long long e0 = tile * TE + lane;
+    double2 s[EPL];
 #pragma unroll
-      for (int q = 0; q < GS_WARPS; ++q) t = cadd(t, red[q][lane]);
-      wout[e] = t;
-      nrm = fma(t.x, t.x, fma(t.y, t.y, nrm));
+    for (int q = 0; q < EPL; ++q) s[q] = make_double2(0.0, 0.0);
+    int c = sl;
+    for (; c + GS_WARPS < nvec; c += 2 * GS_WARPS) {
+      const double2 c0 = sc[c], c1 = sc[c + GS_WARPS];
+      const double2* v0p = V + (long long)c * ld + e0;
+      const double2* v1p = V + (long long)(c + GS_WARPS) * ld + e0;
+      double2 v0[EPL], v1[EPL];
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        const bool ok = e0 + 32 * q < n;
+        v0[q] = ok ? v0p[32 * q] : make_double2(0.0, 0.0);
+        v1[q] = ok ? v1p[32 * q] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        s[q] = cfma(c0, v0[q], s[q]);
+        s[q] = cfma(c1, v1[q], s[q]);
+      }
+    }
+    if (c < nvec) {
+      const double2 c0 = sc[c];
+      const double2* v0p = V + (long long)c * ld + e0;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q)
+        if (e0 + 32 * q < n) s[q] = cfma(c0, v0p[32 * q], s[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) acc[sl][lane + 32 * q] = s[q];
+    __syncthreads();
+    if (threadIdx.x < TE) {
+      const long long e = tile * TE + threadIdx.x;
+      if (e < n) {
+        double2 t = win ? win[e] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < GS_WARPS; ++q) t = cadd(t, acc[q][threadIdx.x]);
+        wout[e] = t;
+        nrm = fma(t.x, t.x, fma(t.y, t.y, nrm));
+      }
     }
     __syncthreads();
   }
-  if (want_norm && sl == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-    if (lane == 0) part[blockIdx.x] = make_double2(nrm, 0.0);
+  if (want_norm) {
+    const double tb = block_sum(nrm);
+    if (threadIdx.x == 0) part[blockIdx.x] = make_double2(tb, 0.0);
   }
 }
 
@@ -424,19 +457,6 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
   return nrm;
 }
 
-// block sum of a per-thread double (any blockDim <= 1024, multiple of 32), result in thread 0
-__device__ __forceinline__ double block_sum(double v) {
-  __shared__ double bs[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) bs[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0)
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += bs[q];
-  __syncthreads();
-  return t;
-}
 
 // flags: 1 = step B in the last block to finish; 2 = the grid has one extra block (block 0) that runs
 // the rotation part of step A (column j-1) while the others stream pass 2 -- off the critical
@@ -896,7 +916,7 @@ __global__ void k_fgm_begin(FgmState* st, const double2* __restrict__ nrm2, int 
 // Back substitution y = R^{-1} g over the ncols completed columns (one warp), and the
 // inner-solve statistics when `outer` is given.
 // Back substitution R y = g of the rotated Hessenberg matrix (column-major, ld = m + 1).
-// staged != 0 (the triangle fits in the dynamic shared memory): the block loads the triangle
+// staged != 0 (the first ncols columns fit in the dynamic shared memory): the block copies them
 // and g into shared memory in one parallel sweep, then one warp runs the column-oriented
 // substitution from shared memory (y_q = s_q / R_qq, s_r -= R_rq y_q for r < q) -- the row
 // form below pays a global-memory round trip per row (~70 us for 50 rows).
@@ -909,15 +929,16 @@ __global__ void k_fgm_backsub(FgmState* st, const double2* __restrict__ H, const
   const int mm = st->ncols;
   const int ld = st->m + 1;
   if (staged) {
-    double2* tri = sbs;                                  // column q at q (q + 1) / 2, rows 0..q
-    double2* s = sbs + (size_t)mm * (mm + 1) / 2;        // running right-hand side
-    for (int q = 0; q < mm; ++q)
-      for (int r = threadIdx.x; r <= q; r += blockDim.x) tri[q * (q + 1) / 2 + r] = H[(long long)q * ld + r];
+    double2* sh = sbs;                                   // columns 0..mm-1 (ld rows each)
+    double2* s = sbs + (size_t)mm * ld;                  // running right-hand side
+    const int tot = mm * ld;
+#pragma unroll 8
+    for (int i = threadIdx.x; i < tot; i += blockDim.x) sh[i] = H[i];
     for (int r = threadIdx.x; r < mm; r += blockDim.x) s[r] = g[r];
     __syncthreads();
     if (threadIdx.x < 32) {
       for (int q = mm - 1; q >= 0; --q) {
-        const double2* col = tri + q * (q + 1) / 2;
+        const double2* col = sh + (size_t)q * ld;
         const double2 yq = cdiv(s[q], col[q]);
         if (lane == 0) y[q] = yq;
         for (int r = lane; r < q; r += 32) s[r] = csub(s[r], cmul(col[r], yq));
