@@ -42,6 +42,7 @@ extern "C" {
 #define HELM_COARSE_RED_GLK2 4 /* ReD-Glk2, Eq. 5.12/5.14 with ghost points (§5.2.4) */
 #define HELM_COARSE_RED_O6 5   /* sixth-order re-discretisation, Eq. 5.10 (§5.2.3) */
 #define HELM_COARSE_RED_CMPO4 6 /* compact fourth-order re-discretisation, Eq. 5.19 (§5.2.5) */
+#define HELM_COARSE_RED_9PTO2 7 /* nine-point eigenvalue-aligned re-discretisation, Appendix B */
 /* The re-discretised operators (RED_O2/O4/O6/CMPO4) replace A_{2h} as printed for either kind of
  * deflation vectors (no factor 4 for the higher-order vectors; reading R21). */
 

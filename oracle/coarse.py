@@ -16,6 +16,9 @@ A_{2h} = I_h^{2h} A_h I_{2h}^h" and §5.2 (matrix-free coarse operators):
   "red_cmpo4" ReD-cmpO4, §5.2.5 Eq. 5.19 with the Singer-Turkel coefficients (gamma = 1):
               a 9-point compact stencil; Sommerfeld ghosts by the fourth-order condition
               u_0 = 2ikh(1 - k^2h^2/6) u_1 + u_2 and the corner ghost u_00 = (u_10 + u_01)/2.
+  "red_9pto2" ReD-9ptO2, Appendix B: the same general 3x3 form (Eq. 5.19)
+              with the eigenvalue-aligned coefficients a = (4.632, -1.316, 0.158), b = (1, 0, 0);
+              Sommerfeld ghosts by the second-order condition u_0 = 2ikh u_1 + u_2 (reading R22).
 
 Reading R5: Eq. 5.11 prints the centre as "60 - k^2 (2h)^2" inside the
 prefactor 1/(12 (2h)^2); a consistent discretisation of -Delta - k^2 needs
@@ -32,8 +35,8 @@ from .operators import apply_A
 from .transfer import (coarse_k, coarse_shape, prolong_bilinear, prolong_high_order, restrict_bilinear_zt,
                        restrict_high_order)
 
-COARSE_OPS = ("galerkin", "red_o2", "red_o4", "red_o6", "red_cmpo4", "red_glk1", "red_glk2")
-RED_OPS = ("red_o2", "red_o4", "red_o6", "red_cmpo4")   # re-discretisations of A at mesh 2h
+COARSE_OPS = ("galerkin", "red_o2", "red_o4", "red_o6", "red_cmpo4", "red_9pto2", "red_glk1", "red_glk2")
+RED_OPS = ("red_o2", "red_o4", "red_o6", "red_cmpo4", "red_9pto2")   # re-discretisations of A at mesh 2h
 
 # PAPER.md Eq. 5.12 (Laplacian part, printed) and Eq. 5.14 (wavenumber part, printed).
 GLK_LAP = np.array([[-3, -44, -98, -44, -3],
@@ -142,18 +145,38 @@ CMP_A = {"0": 10.0 / 3.0, "s": -2.0 / 3.0, "c": -1.0 / 6.0}
 CMP_B = {"0": 2.0 / 3.0 + CMP_GAMMA / 36.0, "s": 1.0 / 12.0 - CMP_GAMMA / 72.0, "c": CMP_GAMMA / 144.0}
 
 
+# PAPER.md Appendix B, Eq. optstcl_k80 (:1300-1304): a_0 = 4.632, a_s = -1.316, a_c = 0.158 with
+# b_s = b_c = 0, b_0 = 1 (constraints Eq. CommonConstraints_A/B, :1273-1277)
+OPT9_A = {"0": 4.632, "s": -1.316, "c": 0.158}
+OPT9_B = {"0": 1.0, "s": 0.0, "c": 0.0}
+
+
 def _red_cmpo4(x, kc, H, bc):
-    """ReD-cmpO4: y = (1/H^2) sum a_tap u_tap - k_c^2 sum b_tap u_tap over the 3x3 compact
-    stencil (a_0, a_s, a_c / b_0, b_s, b_c), k_c the wavenumber of the centre node (reading
-    R19: Eq. 5.19 carries one k^2 per stencil).  Dirichlet: taps on the boundary hold 0.
-    Sommerfeld: ghost nodes one layer outside the domain from the fourth-order condition
-    u_ghost = u_inner + 2 i k H (1 - k^2 H^2 / 6) u_boundary (k of the boundary node), the corner
-    ghost as the mean of its two edge-ghost neighbours."""
+    """ReD-cmpO4 (Eq. 5.19, Singer-Turkel coefficients, fourth-order ghosts)."""
+    return _red_9point(x, kc, H, bc, CMP_A, CMP_B, fourth_order_ghost=True)
+
+
+def _red_9pto2(x, kc, H, bc):
+    """ReD-9ptO2 (Appendix B): the general form with the eigenvalue-aligned
+    coefficients; second-order Sommerfeld ghosts (reading R22)."""
+    return _red_9point(x, kc, H, bc, OPT9_A, OPT9_B, fourth_order_ghost=False)
+
+
+def _red_9point(x, kc, H, bc, A, B, fourth_order_ghost):
+    """General 3x3 form (Eq. 5.19): y = (1/H^2) sum a_tap u_tap - k_c^2 sum b_tap u_tap
+    (a_0, a_s, a_c / b_0, b_s, b_c), k_c the wavenumber of the centre node (reading R19: the form
+    carries one k^2 per stencil).  Dirichlet: taps on the boundary hold 0.  Sommerfeld: ghost
+    nodes one layer outside the domain, u_ghost = u_inner + 2 i k H (1 - k^2 H^2 / 6) u_boundary
+    (fourth-order condition) or u_inner + 2 i k H u_boundary (second order), k
+    of the boundary node; the corner ghost is the mean of its two edge-ghost neighbours."""
     ny, nx = x.shape
     X = np.zeros((ny + 2, nx + 2), dtype=np.complex128)
     X[1:-1, 1:-1] = x
     if bc == "sommerfeld":
-        fac = lambda kk: 2j * kk * H * (1.0 - kk * kk * H * H / 6.0)
+        if fourth_order_ghost:
+            fac = lambda kk: 2j * kk * H * (1.0 - kk * kk * H * H / 6.0)
+        else:
+            fac = lambda kk: 2j * kk * H
         X[1:-1, 0] = x[:, 1] + fac(kc[:, 0]) * x[:, 0]
         X[1:-1, -1] = x[:, -2] + fac(kc[:, -1]) * x[:, -1]
         X[0, 1:-1] = x[1, :] + fac(kc[0, :]) * x[0, :]
@@ -165,8 +188,8 @@ def _red_cmpo4(x, kc, H, bc):
     c = X[1:-1, 1:-1]
     side = X[1:-1, :-2] + X[1:-1, 2:] + X[:-2, 1:-1] + X[2:, 1:-1]
     corner = X[:-2, :-2] + X[:-2, 2:] + X[2:, :-2] + X[2:, 2:]
-    lap = (CMP_A["0"] * c + CMP_A["s"] * side + CMP_A["c"] * corner) / (H * H)
-    mass = CMP_B["0"] * c + CMP_B["s"] * side + CMP_B["c"] * corner
+    lap = (A["0"] * c + A["s"] * side + A["c"] * corner) / (H * H)
+    mass = B["0"] * c + B["s"] * side + B["c"] * corner
     return lap - kc * kc * mass
 
 
@@ -190,6 +213,8 @@ def apply_coarse_E(x: np.ndarray, k_fine: np.ndarray, h: float, bc: str, op: str
             return _red_o4(x, kc, H, bc)
         if op == "red_o6":
             return _red_o6(x, kc, H, bc)
+        if op == "red_9pto2":
+            return _red_9pto2(x, kc, H, bc)
         return _red_cmpo4(x, kc, H, bc)
     if vectors == "high_order":
         if op == "galerkin":

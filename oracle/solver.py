@@ -49,7 +49,7 @@ class SolverParams:
     nu_pre: int = 1
     nu_post: int = 1
     vectors: str = "bilinear"         # bilinear (A-DEF1) | high_order (APD)
-    coarse_op: str = "galerkin"       # galerkin | red_o2 | red_o4 | red_o6 | red_cmpo4; red_glk1 | red_glk2 (high_order)
+    coarse_op: str = "galerkin"       # galerkin | red_o2 | red_o4 | red_o6 | red_cmpo4 | red_9pto2; red_glk1 | red_glk2 (high_order)
     inner_solver: str = "fgmres"      # fgmres | direct
     inner_tol: float = 1e-1           # 0 -> fixed inner_maxit iterations (reading R15)
     inner_maxit: int = 200

@@ -485,8 +485,12 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       else launch_k(C, k_apply_red_o6<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_CMPO4:
-      if (res) launch_k(C, k_apply_red_cmpo4<1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
-      else launch_k(C, k_apply_red_cmpo4<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      if (res) launch_k(C, k_apply_red_cmpo4<1, 0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_cmpo4<0, 0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      return post_launch(C);
+    case HELM_COARSE_RED_9PTO2:
+      if (res) launch_k(C, k_apply_red_cmpo4<1, 1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
+      else launch_k(C, k_apply_red_cmpo4<0, 1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
   }
   return fail(HELM_EINVAL, "bad coarse_op");
@@ -1060,7 +1064,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.nu_pre < 1 || p.nu_post < 0) return fail(HELM_EINVAL, "nu_pre >= 1, nu_post >= 0");
   if (p.inner_maxit < 1) return fail(HELM_EINVAL, "inner_maxit >= 1");
   if (p.outer != HELM_OUTER_FGMRES && p.outer != HELM_OUTER_GCR) return fail(HELM_EINVAL, "bad outer %d", p.outer);
-  if (p.coarse_op < HELM_COARSE_GALERKIN || p.coarse_op > HELM_COARSE_RED_CMPO4)
+  if (p.coarse_op < HELM_COARSE_GALERKIN || p.coarse_op > HELM_COARSE_RED_9PTO2)
     return fail(HELM_EINVAL, "bad coarse_op %d", p.coarse_op);
   if (p.vectors == HELM_VECTORS_BILINEAR) {
     if (p.coarse_op == HELM_COARSE_RED_GLK1 || p.coarse_op == HELM_COARSE_RED_GLK2)

@@ -600,25 +600,30 @@ __global__ void k_apply_red_o6(Geo g, DVec xv, DVec fv, DVec yv, const double* _
   y[p] = v;
 }
 
-// ReD-cmpO4 (Eq. 5.19, Singer-Turkel coefficients with gamma = 1):
+// General 3x3 re-discretisation (Eq. 5.19):
 //   y = (1/H^2) sum a_tap u_tap - k_c^2 sum b_tap u_tap over the 3x3 compact stencil, k_c the
-// centre wavenumber (reading R19).  Dirichlet: boundary taps hold 0.  Sommerfeld: ghosts from
-// u_ghost = u_inner + 2 i k H (1 - k^2 H^2/6) u_boundary, corner ghost = mean of its two edge
-// ghosts.
+// centre wavenumber (reading R19).  VAR 0: ReD-cmpO4, Singer-Turkel coefficients with gamma = 1,
+// Sommerfeld ghosts u_ghost = u_inner + 2 i k H (1 - k^2 H^2/6) u_boundary;
+// VAR 1: ReD-9ptO2 (Appendix B: a = (4.632, -1.316, 0.158), b = (1, 0, 0)),
+// second-order ghosts u_ghost = u_inner + 2 i k H u_boundary (reading R22).  Dirichlet: boundary
+// taps hold 0.  Corner ghost = mean of its two edge ghosts.
+template <int VAR>
 __device__ __forceinline__ double2 cmp_ghost_fac(double kk, double H) {
+  if (VAR == 1) return make_double2(0.0, 2.0 * kk * H);
   return make_double2(0.0, 2.0 * kk * H * (1.0 - kk * kk * H * H / 6.0));
 }
 
 // value at (ii, jj) in [-1, nx] x [-1, ny] for the Sommerfeld compact stencil
+template <int VAR>
 __device__ __forceinline__ double2 cmp_val(const Geo& g, const double2* __restrict__ x, const double* __restrict__ k,
                                            int ii, int jj) {
   auto inside = [&](int a, int b) { return a >= 0 && a < g.nx && b >= 0 && b < g.ny; };
   auto X = [&](int a, int b) { return x[(size_t)b * g.nx + a]; };
   auto edge = [&](int a, int b) -> double2 {   // exactly one of a, b is outside by one layer
-    if (a == -1) return cfma(cmp_ghost_fac(k[(size_t)b * g.nx + 0], g.h), X(0, b), X(1, b));
-    if (a == g.nx) return cfma(cmp_ghost_fac(k[(size_t)b * g.nx + g.nx - 1], g.h), X(g.nx - 1, b), X(g.nx - 2, b));
-    if (b == -1) return cfma(cmp_ghost_fac(k[a], g.h), X(a, 0), X(a, 1));
-    return cfma(cmp_ghost_fac(k[(size_t)(g.ny - 1) * g.nx + a], g.h), X(a, g.ny - 1), X(a, g.ny - 2));
+    if (a == -1) return cfma(cmp_ghost_fac<VAR>(k[(size_t)b * g.nx + 0], g.h), X(0, b), X(1, b));
+    if (a == g.nx) return cfma(cmp_ghost_fac<VAR>(k[(size_t)b * g.nx + g.nx - 1], g.h), X(g.nx - 1, b), X(g.nx - 2, b));
+    if (b == -1) return cfma(cmp_ghost_fac<VAR>(k[a], g.h), X(a, 0), X(a, 1));
+    return cfma(cmp_ghost_fac<VAR>(k[(size_t)(g.ny - 1) * g.nx + a], g.h), X(a, g.ny - 1), X(a, g.ny - 2));
   };
   if (inside(ii, jj)) return X(ii, jj);
   const bool ox = (ii < 0 || ii >= g.nx), oy = (jj < 0 || jj >= g.ny);
@@ -629,7 +634,7 @@ __device__ __forceinline__ double2 cmp_val(const Geo& g, const double2* __restri
   return edge(ii, jj);
 }
 
-template <int MODE>
+template <int MODE, int VAR>
 __global__ void k_apply_red_cmpo4(Geo g, DVec xv, DVec fv, DVec yv, const double* __restrict__ k) {
   HELM_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -639,8 +644,10 @@ __global__ void k_apply_red_cmpo4(Geo g, DVec xv, DVec fv, DVec yv, const double
   const double2* __restrict__ f = fv.get();
   double2* __restrict__ y = yv.get();
   const size_t p = (size_t)j * g.nx + i;
-  constexpr double A0 = 10.0 / 3.0, AS = -2.0 / 3.0, AC = -1.0 / 6.0;
-  constexpr double B0 = 2.0 / 3.0 + 1.0 / 36.0, BS = 1.0 / 12.0 - 1.0 / 72.0, BC = 1.0 / 144.0;
+  constexpr double A0 = VAR == 1 ? 4.632 : 10.0 / 3.0, AS = VAR == 1 ? -1.316 : -2.0 / 3.0,
+                   AC = VAR == 1 ? 0.158 : -1.0 / 6.0;
+  constexpr double B0 = VAR == 1 ? 1.0 : 2.0 / 3.0 + 1.0 / 36.0, BS = VAR == 1 ? 0.0 : 1.0 / 12.0 - 1.0 / 72.0,
+                   BC = VAR == 1 ? 0.0 : 1.0 / 144.0;
   double2 c, side, corner;
   if (g.bc == BC_DIRICHLET) {
     auto at = [&](int ii, int jj) -> double2 {
@@ -652,10 +659,10 @@ __global__ void k_apply_red_cmpo4(Geo g, DVec xv, DVec fv, DVec yv, const double
     corner = cadd(cadd(at(i - 1, j - 1), at(i + 1, j - 1)), cadd(at(i - 1, j + 1), at(i + 1, j + 1)));
   } else {
     c = x[p];
-    side = cadd(cadd(cmp_val(g, x, k, i - 1, j), cmp_val(g, x, k, i + 1, j)),
-                cadd(cmp_val(g, x, k, i, j - 1), cmp_val(g, x, k, i, j + 1)));
-    corner = cadd(cadd(cmp_val(g, x, k, i - 1, j - 1), cmp_val(g, x, k, i + 1, j - 1)),
-                  cadd(cmp_val(g, x, k, i - 1, j + 1), cmp_val(g, x, k, i + 1, j + 1)));
+    side = cadd(cadd(cmp_val<VAR>(g, x, k, i - 1, j), cmp_val<VAR>(g, x, k, i + 1, j)),
+                cadd(cmp_val<VAR>(g, x, k, i, j - 1), cmp_val<VAR>(g, x, k, i, j + 1)));
+    corner = cadd(cadd(cmp_val<VAR>(g, x, k, i - 1, j - 1), cmp_val<VAR>(g, x, k, i + 1, j - 1)),
+                  cadd(cmp_val<VAR>(g, x, k, i - 1, j + 1), cmp_val<VAR>(g, x, k, i + 1, j + 1)));
   }
   const double iH2 = 1.0 / (g.h * g.h);
   const double k2 = k[p] * k[p];

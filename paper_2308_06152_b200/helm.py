@@ -16,7 +16,7 @@ _LIB_PATH = os.environ.get("HELM_LIB") or os.path.join(_HERE, "libhelm.so")
 
 HELM_BC_DIRICHLET = 0
 HELM_BC_SOMMERFELD = 1
-COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2, "red_glk1": 3, "red_glk2": 4, "red_o6": 5, "red_cmpo4": 6}
+COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2, "red_glk1": 3, "red_glk2": 4, "red_o6": 5, "red_cmpo4": 6, "red_9pto2": 7}
 VECTORS = {"bilinear": 0, "high_order": 1}
 OUTER = {"fgmres": 0, "gcr": 1}
 BCS = {"dirichlet": HELM_BC_DIRICHLET, "sommerfeld": HELM_BC_SOMMERFELD}

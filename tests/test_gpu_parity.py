@@ -87,7 +87,7 @@ def test_transfers(case):
 VARIANTS = [("bilinear", "galerkin"), ("bilinear", "red_o2"), ("bilinear", "red_o4"), ("bilinear", "red_o6"),
             ("bilinear", "red_cmpo4"), ("high_order", "galerkin"), ("high_order", "red_glk1"),
             ("high_order", "red_glk2"), ("high_order", "red_o2"), ("high_order", "red_o4"), ("high_order", "red_o6"),
-            ("high_order", "red_cmpo4")]
+            ("high_order", "red_cmpo4"), ("bilinear", "red_9pto2"), ("high_order", "red_9pto2")]
 
 
 @pytest.mark.parametrize("vec,op", VARIANTS)
@@ -173,6 +173,7 @@ SOLVE_CASES = [
     ("wedge_f10", "bilinear", "galerkin", 0.0, 40), ("wedge_f10", "high_order", "red_glk2", 1e-1, 300),
     ("mp_som_k40", "high_order", "red_cmpo4", 1e-1, 200), ("mp_som_k40", "high_order", "red_o6", 0.0, 40),
     ("wedge_f10", "high_order", "red_cmpo4", 0.0, 40), ("c1_k50", "bilinear", "red_o6", 1e-1, 200),
+    ("c1_k50", "high_order", "red_9pto2", 1e-1, 200), ("mp_som_k40", "bilinear", "red_9pto2", 0.0, 40),
 ]
 
 

@@ -162,3 +162,81 @@ def test_cmpo4_sommerfeld_ghost_is_high_order_for_outgoing_waves():
         Hs.append(H)
     slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
     assert slope > 2.7, slope
+
+
+# ---------------------------------------------------------------- ReD-9ptO2 (Appendix B)
+def _lam_H(a, b, kval, H, p, q):
+    """PAPER.md Appendix B, eigenvalues of the general 3x3 form with homogeneous Dirichlet
+    conditions (Eq. eigs_A2h_optstcl, :1285-1290)."""
+    cp, cq = np.cos(p * np.pi * H), np.cos(q * np.pi * H)
+    k2H2 = kval * kval * H * H
+    return ((a["0"] - b["0"] * k2H2) + 2 * (a["s"] - b["s"] * k2H2) * (cp + cq)
+            + 4 * (a["c"] - b["c"] * k2H2) * cp * cq) / (H * H)
+
+
+def test_9pto2_coefficients_meet_appendix_b_constraints():
+    """PAPER.md:1273-1277: a_0 + 4a_s + 4a_c = 0, a_s + 2a_c = -1, b_0 + 4b_s + 4b_c = 1."""
+    from oracle.coarse import OPT9_A, OPT9_B
+    assert abs(OPT9_A["0"] + 4 * OPT9_A["s"] + 4 * OPT9_A["c"]) < 1e-12
+    assert abs(OPT9_A["s"] + 2 * OPT9_A["c"] + 1.0) < 1e-12
+    assert abs(OPT9_B["0"] + 4 * OPT9_B["s"] + 4 * OPT9_B["c"] - 1.0) < 1e-15
+
+
+def test_9pto2_printed_eigenvalues():
+    """The coefficients reproduce the eigenvalues Appendix B prints: for k = 80 and h -> 0,
+    lambda_H^{18,18} = -4.5 (the alignment target, :1296-1299); for k = 100 the smallest
+    |lambda_H^{p,q}| is ~2.1 at (p, q) = (22, 23) (:1306-1308)."""
+    from oracle.coarse import OPT9_A, OPT9_B
+    H = 2e-5
+    assert abs(_lam_H(OPT9_A, OPT9_B, 80.0, H, 18, 18) + 4.5) < 0.01
+    P = np.arange(1, 200)
+    pp, qq = np.meshgrid(P, P, indexing="ij")
+    lam = _lam_H(OPT9_A, OPT9_B, 100.0, H, pp, qq)
+    i = np.unravel_index(np.argmin(np.abs(lam)), lam.shape)
+    assert {int(P[i[0]]), int(P[i[1]])} == {22, 23}
+    assert abs(abs(lam[i]) - 2.1) < 0.05
+
+
+def test_9pto2_dirichlet_eigenvectors():
+    """Closed form: with constant k and homogeneous Dirichlet conditions the modes
+    sin(p pi x) sin(q pi y) are eigenvectors of the 3x3 form with the eigenvalues of
+    Eq. eigs_A2h_optstcl (the implementation, including its zero boundary taps)."""
+    from oracle.coarse import OPT9_A, OPT9_B
+    n, kval = 16, 9.0
+    h = 1.0 / (2 * n)
+    H = 2 * h
+    xc = np.arange(1, n) * H
+    X, Y = np.meshgrid(xc, xc)
+    kf = np.full((2 * n - 1, 2 * n - 1), kval)
+    for p, q in ((1, 1), (3, 7), (15, 2), (8, 8)):
+        u = np.sin(p * np.pi * X) * np.sin(q * np.pi * Y) + 0j
+        y = oracle.apply_coarse_E(u, kf, h, "dirichlet", "red_9pto2")
+        lam = _lam_H(OPT9_A, OPT9_B, kval, H, p, q)
+        np.testing.assert_allclose(y, lam * u, atol=1e-9 * abs(lam) + 1e-9)
+
+
+def test_9pto2_second_order_on_helmholtz_solutions():
+    """Consistency: on a plane wave the interior residual of ReD-9ptO2 decays like H^2 (a
+    second-order scheme, unlike ReD-cmpO4's H^4)."""
+    errs, Hs = [], []
+    for n in (16, 32, 64):
+        h, H, k, u = _plane_wave(n, 6.0, 0.7, "dirichlet")
+        y = oracle.apply_coarse_E(u, k, h, "dirichlet", "red_9pto2")
+        errs.append(np.max(np.abs(y)[1:-1, 1:-1]))
+        Hs.append(H)
+    slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
+    assert abs(slope - 2.0) < 0.25, slope
+
+
+def test_9pto2_sommerfeld_ghost_is_second_order():
+    """Reading R22: the second-order ghost u_0 = 2ikH u_1 + u_2 leaves an O(H) residual on the
+    boundary for the outgoing wave (ghost error O(H^3) / H^2), against O(H^3) with ReD-cmpO4's
+    fourth-order ghost."""
+    errs, Hs = [], []
+    for n in (16, 32, 64):
+        h, H, k, u = _plane_wave(n, 6.0, math.pi, "sommerfeld")
+        y = oracle.apply_coarse_E(u, k, h, "sommerfeld", "red_9pto2")
+        errs.append(np.max(np.abs(y[2:-2, 0])))
+        Hs.append(H)
+    slope = np.polyfit(np.log(Hs), np.log(errs), 1)[0]
+    assert 0.7 < slope < 1.5, slope
