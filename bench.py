@@ -208,6 +208,19 @@ def kernel_roofline(H, rep, peaks, reps=20):
                        "us_per_launch": us, "launches_per_step": count, "est_ms_per_step": count * us * 1e-3,
                        "timing": "in-graph, warm (helm_bench_graph)", "peak_src": peaks["src"]}
     dom = max(rows.values(), key=lambda r: r["est_ms_per_step"])
+    # DRAM traffic of the dominant component from the committed ncu --set full capture of the
+    # same component (cold caches): the kernels of one delayed-CGS2 step at inner column jm, or
+    # of the first inner V-cycle from level 1 (tools/ncu_dcgs_summary.py)
+    prof_name = ("dcgs_j%d" % jm) if dom["kernel"].startswith("dcgs2 step") else \
+        ("vcycle1" if dom["kernel"].startswith("V-cycle from level 1") else None)
+    if prof_name:
+        try:
+            with open(os.path.join(ROOT, "profiles", f"r01_ncu_{prof_name}.json")) as fh:
+                prof = json.load(fh)
+            dom["traffic"] = prof["dram_bytes_per_step"]
+            dom["traffic_src"] = f"profiles/r01_ncu_{prof_name}.json (ncu --set full, cold caches)"
+        except (OSError, KeyError, ValueError):
+            pass
     iso = {}
     for name, arg in (("gs_dots", jm + 1), ("gs_update", jm + 1), ("apply_E", 0), ("apply_A", 0), ("vc_down", 0),
                       ("vc_up", 0), ("vc_down", 1), ("vc_up", 1)):

@@ -16,7 +16,6 @@
 // chunking, fixed warp trees, one warp per output in a second stage).
 #pragma once
 #include <algorithm>
-#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -82,7 +81,7 @@ inline GsGeom gs_geom(long long n, int sms) {
   const long long per = (subs + 65535) / 65536;
   g.chunk = per * 256;
   g.gx = (int)((n + g.chunk - 1) / g.chunk);
-  const int target = (getenv("HELM_GS_TARGET") ? atoi(getenv("HELM_GS_TARGET")) : 8) * sms;
+  const int target = 8 * sms;
   g.gy = std::max(1, std::min(16, target / std::max(1, g.gx)));
   const long long tiles = (n + 127) / 128;   // DU_ELEMS
   g.gu = (int)std::max<long long>(1, std::min<long long>(tiles, (long long)8 * sms));
@@ -354,11 +353,15 @@ __device__ __forceinline__ void dcgs_dots_item(const double2* __restrict__ V, lo
   }
 }
 
+// Minimum resident blocks per SM (register caps) of the two Gram-Schmidt passes: 3 x 128-thread
+// dots blocks (<= 168 registers) and 2 x 256-thread update blocks (<= 128 registers; the step
+// code in the last / extra block would otherwise raise the whole kernel to ~180 and halve its
+// occupancy).  Measured on the c1_k400 bench: -5 % time to solution (tools/dcgs_probe.py).
 #ifndef HELM_DC_MINB
-#define HELM_DC_MINB 1
+#define HELM_DC_MINB 3
 #endif
 #ifndef HELM_DU_MINB
-#define HELM_DU_MINB 1
+#define HELM_DU_MINB 2
 #endif
 __global__ void __launch_bounds__(DC_THREADS, HELM_DC_MINB) k_dcgs_dots(const double2* __restrict__ V, long long ld,
                                                           const int* __restrict__ nptr, int nadd, DVec xv, DVec wv,

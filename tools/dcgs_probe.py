@@ -14,7 +14,7 @@ from workloads import config_problem  # noqa: E402
 p = config_problem("c1_k400")
 H = helm.helm_setup(p, {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": 50,
                         "coarsest_n": 512})
-out = {"lib": os.path.basename(os.environ.get("HELM_LIB", "libhelm.so")), "target": os.environ.get("HELM_GS_TARGET", "8")}
+out = {"lib": os.path.basename(os.environ.get("HELM_LIB", "libhelm.so"))}
 for j in (5, 25, 45):
     out[f"dcgs{j}"] = round(H.helm_bench_graph("dcgs", j, 3), 2)
 out["vcycle1"] = round(H.helm_bench_graph("vcycle", 1, 20), 2)
