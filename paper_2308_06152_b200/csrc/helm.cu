@@ -581,7 +581,11 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   }
   if (fused_vcycle(C)) {
     // small levels: smaller tiles so that more SMs share the (latency-bound) work
-    const bool small = (size_t)((G.g.nx + DOWN_TX - 1) / DOWN_TX) * ((G.g.ny + DOWN_TY - 1) / DOWN_TY) < (size_t)2 * C.sm_count;
+#ifndef HELM_SMALL_TILES_X   // measured: 1 (small tiles only below one wave of big tiles) -1.3 % per solve vs 2
+#define HELM_SMALL_TILES_X 1
+#endif
+    const bool small = (size_t)((G.g.nx + DOWN_TX - 1) / DOWN_TX) * ((G.g.ny + DOWN_TY - 1) / DOWN_TY) <
+                       (size_t)HELM_SMALL_TILES_X * C.sm_count;
     if (small) {
       dim3 gd((G.g.nx + 7) / 8, (G.g.ny + 3) / 4);
       launch_k(C, k_vc_down<8, 4>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
