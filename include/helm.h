@@ -110,6 +110,9 @@ typedef struct {
                           staged through a per-warp cp.async shared-memory ring, 4 rows in flight,
                           segments of 256 (down) / 128 (up) rows; 3, 4, 5, 14, 24: other depths /
                           segment lengths (measurement) */
+  int fuse_dots;       /* 1: with str-Glk, the inner FGMRES applies E and pass 1 of the delayed CGS2
+                          (the dots against the basis) in one kernel; measured slower on B200
+                          than the two kernels (0.577 vs 0.568 s per bench solve), so 0 (default) */
 } helm_params;
 
 typedef struct {

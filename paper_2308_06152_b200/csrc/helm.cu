@@ -440,6 +440,31 @@ int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
 
 constexpr int GLK_TX = 16, GLK_TY = 8;   // coarse outputs per k_galerkin_apply CTA
 
+// Fused inner-solve step (single GPU, str-Glk): w = E x and pass 1 of the delayed CGS2 of the
+// inner FGMRES (dots of s v~_j and w against V_0..V_j) in one kernel; partials per E tile.
+bool fused_E_dots(const helm_ctx_s& C) {
+  return C.p.coarse_op == HELM_COARSE_GALERKIN && !C.dist && C.p.fuse_dots;
+}
+
+dim3 glk_tiles(const helm_ctx_s& C) {
+  const Level& G = C.L[1];
+  return dim3((G.g.nx + GLK_TX - 1) / GLK_TX, (G.g.ny + GLK_TY - 1) / GLK_TY);
+}
+
+int apply_E_dots(helm_ctx_s& C, DVec x, DVec y, DVec vt, const double2* V, long long ldv, const int* jptr,
+                 double2* part) {
+  const Level& F = C.L[0];
+  const Level& G = C.L[1];
+  const dim3 gt = glk_tiles(C);
+  if (C.p.vectors == HELM_VECTORS_BILINEAR)
+    launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY, true>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, DVec(), y, V,
+             ldv, jptr, vt, part);
+  else
+    launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY, true>, gt, dim3(32, 8), 0, F.g, G.g, F.o, F.k, x, DVec(), y, V,
+             ldv, jptr, vt, part);
+  return post_launch(C);
+}
+
 // y = E x (f.p == null) or y = f - E x on level 1
 int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
   const Level& G = C.L[1];
@@ -458,11 +483,15 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       y = shift(y, wo);
       const dim3 gt((Gw.g.nx + GLK_TX - 1) / GLK_TX, (Gw.g.ny + GLK_TY - 1) / GLK_TY);
       if (C.p.vectors == HELM_VECTORS_BILINEAR) {
-        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
-        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y,
+                          (const double2*)nullptr, 0LL, (const int*)nullptr, DVec(), (double2*)nullptr);
+        else launch_k(C, k_galerkin_apply<1, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y,
+                          (const double2*)nullptr, 0LL, (const int*)nullptr, DVec(), (double2*)nullptr);
       } else {
-        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
-        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y);
+        if (res) launch_k(C, k_galerkin_apply<2, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y,
+                          (const double2*)nullptr, 0LL, (const int*)nullptr, DVec(), (double2*)nullptr);
+        else launch_k(C, k_galerkin_apply<2, 0, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y,
+                          (const double2*)nullptr, 0LL, (const int*)nullptr, DVec(), (double2*)nullptr);
       }
       return post_launch(C);
     }
@@ -656,7 +685,8 @@ int raise_dyn_smem(const void* func, size_t need) {
 }
 
 // n: owned length; ld: stored length of a basis vector; off: owned offset; dist: rank-summed dots
-int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, bool dist) {
+// P: pass-1 partials per output when the dots come from the fused E kernel (0: dots kernel only)
+int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, bool dist, int P = 0) {
   K.m = m;
   K.n = n;
   K.ld = ld;
@@ -679,7 +709,7 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(dalloc(&K.rawc, (size_t)m + 2));
   CKR(dalloc(&K.nrm, 2));
   K.geo = gs_geom((long long)n, C.sm_count);
-  CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * K.geo.gx, (size_t)K.geo.gu + 1)));
+  CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * std::max(K.geo.gx, P), (size_t)K.geo.gu + 1)));
   CKR(dalloc(&K.st, 1));
   CK(cudaMemsetAsync(K.st, 0, sizeof(FgmState), C.s));
   // dynamic shared memory grows with the basis; the limits are raised once to the largest
@@ -817,8 +847,10 @@ int run_while(helm_ctx_s& C, FgmState* st, Begin&& begin, Body&& body) {
 // One FGMRES cycle for A x = b with x0 = 0 (first) or the current x (restart), x (+)= Z y.
 // opA(x, f, y): y = A x (f null) or y = f - A x;  opP(v, z): z = P v.
 
+// fuse: opA is the inner str-Glk E, applied together with pass 1 (apply_E_dots)
 template <class OpA, class OpP>
-int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x, bool first, FgmState* outer_stats) {
+int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x, bool first, FgmState* outer_stats,
+                 bool fuse = false) {
   // vectors are stored with length K.ld (a rank's row block incl. ghost rows); the operators get
   // whole stored vectors, the Krylov kernels the owned rows [off, off + n)
   const size_t n = K.n, off = K.off;
@@ -844,25 +876,34 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
     // v~_j is consumed through the scale 1/h_{j,j-1} left by the previous step B (no
     // normalisation pass); pass 2 writes the final v_j over it
     DVec vj(K.V, &st->j, ld, &st->inv_hn), zj(K.Z, &st->j, ld), w(K.V + K.ld, &st->j, ld);
-    CKR(opP(vj, zj));
-    CKR(opA(zj, DVec(), w));
     const DVec vjo = shift(vj, off), wo = shift(w, off);
-    // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
+    CKR(opP(vj, zj));
     const GsGeom& gg = K.geo;
     const size_t asm_ = dcgs_smem(K.m);
+    long long nparts = gg.gx;
+    if (fuse && K.coop == 0) {
+      CKR(apply_E_dots(C, zj, w, vjo, Vo, ld, &st->j, K.part));
+      const dim3 gt = glk_tiles(C);
+      nparts = (long long)gt.x * gt.y;
+    } else {
+      CKR(opA(zj, DVec(), w));
+    }
+    // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
     if (K.coop > 0) {
       // the whole step in one cooperative kernel (grid-wide barriers between its phases)
       launch_coop(C, k_dcgs_step, K.coop, DC_THREADS, asm_, (const double2*)Vo, ld, st, vjo, wo, ln, gg.chunk, gg.gx,
                   gg.gy, K.part, K.npart, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, h, use_h);
       return post_launch(C);
     }
-    launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
-             gg.chunk, K.part);
-    CKR(post_launch(C));
+    if (!(fuse && K.coop == 0)) {
+      launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
+               gg.chunk, K.part);
+      CKR(post_launch(C));
+    }
     // reduction of the pass-1 partials; pass 2 with the rotation part of step A in an extra
     // block and step B in the last block.  Decomposed: the dots are summed over the ranks
     // before pass 2, |w'|^2 before step B (then a separate one-warp kernel)
-    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, (long long)gg.gx, st, K.H,
+    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, nparts, st, K.H,
              K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
     CKR(post_launch(C));
     if (K.dist) CKR(allreduce(C, K.dots1, 2 * K.m + 2));
@@ -901,7 +942,7 @@ int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_st
   CKR(post_launch(C));
   auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y); };
   auto opP = [&](DVec v, DVec z) { return vcycle(C, 1, v, z, nullptr); };
-  return fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats);
+  return fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C));
 }
 
 // z = P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v  (Eq. 3.21 / 5.2-5.5)
@@ -1011,6 +1052,7 @@ void helm_default_params(helm_params* p) {
   p->dist_levels = 0;
   p->dist_min_rows = 16;
   p->col_pipe = 1;
+  p->fuse_dots = 0;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1280,8 +1322,9 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   // inner FGMRES: full (unrestarted) basis of inner_maxit columns, as the oracle (reading R11)
   {
     const Level& G1 = C.L[1];
+    const dim3 gt = glk_tiles(C);
     CKR(fgm_alloc(C, C.inner, p.inner_maxit, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
-                  C.dist && C.nranks > 1 && G1.block));
+                  C.dist && C.nranks > 1 && G1.block, fused_E_dots(C) ? (int)(gt.x * gt.y) : 0));
   }
   CK(cudaStreamSynchronize(C.s));
   return HELM_OK;

@@ -334,9 +334,18 @@ __device__ __forceinline__ void interp_w(int r, double& wm, double& w0, double& 
 
 // Block = 32 x 8 threads; every phase walks its region row by row (threadIdx.y) and column by
 // column (threadIdx.x), so no division/modulo in the index math.
-template <int R, int MODE, int TCX, int TCY>
-__global__ void __launch_bounds__(256, 6) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
-                                                        DVec fv, DVec yv) {
+// DOTS (MODE 0, inner FGMRES): the tile also runs pass 1 of the delayed CGS2 for its coarse
+// points -- part[(2c) T + tile] = sum conj(V_c) (s v~_j), part[(2c+1) T + tile] = sum conj(V_c) w
+// for c <= j, with V_j read as s v~_j (T tiles; w = E x is this tile's output) -- so the E output
+// is dotted while it is still on chip and the separate dots kernel disappears from the iteration.
+#ifndef HELM_GLKD_MINB   // DOTS variant: 3 CTAs/SM (80 registers, no spills) measured best
+#define HELM_GLKD_MINB 3
+#endif
+template <int R, int MODE, int TCX, int TCY, bool DOTS = false>
+__global__ void __launch_bounds__(256, DOTS ? HELM_GLKD_MINB : 6) k_galerkin_apply(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
+                                                        DVec fv, DVec yv, const double2* __restrict__ V = nullptr,
+                                                        long long ldv = 0, const int* __restrict__ jptr = nullptr,
+                                                        DVec vt = DVec(), double2* __restrict__ part = nullptr) {
   HELM_PDL_ENTRY();
   constexpr int SX = 2 * TCX - 1 + 2 * R, SY = 2 * TCY - 1 + 2 * R;   // s = A t region (fine)
   constexpr int TXR = SX + 2, TYR = SY + 2;                          // t = Z x region (A halo)
@@ -346,6 +355,7 @@ __global__ void __launch_bounds__(256, 6) k_galerkin_apply(Geo gf, Geo gc, int o
   __shared__ double2 txss[TXN > SSN ? TXN : SSN];   // tx (x-interpolated coarse rows), later s = A t
   __shared__ double2 stt[TYR * TXR];               // t = Z x
   __shared__ double2 ry[TCY * SX];                 // s restricted along y
+  __shared__ double2 wt[DOTS ? TCX * TCY : 1];     // DOTS: this tile's E x
   double2* const tx = txss;
   double2* const ss = txss;
   const int tx_ = threadIdx.x, ty_ = threadIdx.y;
@@ -434,6 +444,59 @@ __global__ void __launch_bounds__(256, 6) k_galerkin_apply(Geo gf, Geo gc, int o
       for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
       const size_t p = (size_t)J * gc.nx + I;
       y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
+      if (DOTS) wt[jl * TCX + il] = s;
+    }
+  }
+  if (DOTS) {
+    static_assert(TCX * TCY == 128, "pass-1 dots map 4 coarse points to each lane");
+    __syncthreads();
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = (blockDim.x * blockDim.y) >> 5;
+    const int ntiles = gridDim.x * gridDim.y, tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const int j = *jptr;
+    const double2* __restrict__ xt = vt.get();
+    const double xsc = vt.scale();
+    double2 xr[4], wr[4];
+    long long pp[4];
+    bool ok[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int q = lane + 32 * r;
+      const int I = I0 + q % TCX, J = J0 + q / TCX;
+      ok[r] = I < gc.nx && J < gc.ny;
+      pp[r] = ok[r] ? (long long)J * gc.nx + I : 0;
+      xr[r] = ok[r] ? cscale(xsc, xt[pp[r]]) : zero;
+      wr[r] = ok[r] ? wt[q] : zero;
+    }
+#pragma unroll 2
+    for (int c = warp; c <= j; c += nwarps) {
+      const double2* __restrict__ vc = V + (long long)c * ldv;
+      double2 v[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[r] = ok[r] ? vc[pp[r]] : zero;
+      double2 ax = zero, aw = zero;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // conj(v) x, conj(v) w
+        ax.x = fma(v[r].x, xr[r].x, fma(v[r].y, xr[r].y, ax.x));
+        ax.y = fma(v[r].x, xr[r].y, fma(-v[r].y, xr[r].x, ax.y));
+        aw.x = fma(v[r].x, wr[r].x, fma(v[r].y, wr[r].y, aw.x));
+        aw.y = fma(v[r].x, wr[r].y, fma(-v[r].y, wr[r].x, aw.y));
+      }
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) {
+        ax.x += __shfl_xor_sync(0xffffffffu, ax.x, sh);
+        ax.y += __shfl_xor_sync(0xffffffffu, ax.y, sh);
+        aw.x += __shfl_xor_sync(0xffffffffu, aw.x, sh);
+        aw.y += __shfl_xor_sync(0xffffffffu, aw.y, sh);
+      }
+      if (c == j) {   // V_j is v~_j itself: read through the same scale as x (as k_dcgs_dots)
+        ax = cscale(xsc, ax);
+        aw = cscale(xsc, aw);
+      }
+      if (lane == 0) {
+        part[(long long)(2 * c) * ntiles + tile] = ax;
+        part[(long long)(2 * c + 1) * ntiles + tile] = aw;
+      }
     }
   }
 }

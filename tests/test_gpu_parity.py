@@ -343,3 +343,20 @@ def test_column_legs_interior_segments(lib, pipe):
         u = H.vcycle(0, gpu(f)).cpu().numpy()
         assert rel(u, oracle.vcycle(levels, f, 0)) < 1e-11, (p.shape, pipe)
         H.close()
+
+
+@pytest.mark.parametrize("vec", ["bilinear", "high_order"])
+def test_fused_E_dots_matches(lib, vec):
+    """fuse_dots = 1 (E apply and pass 1 of the delayed CGS2 in one kernel) gives the same inner
+    solve as the separate kernels: same inner iterations, solutions equal to rounding."""
+    p = GRIDS[0]
+    v = random_field(p.shape, 7)
+    out = {}
+    for fuse in (0, 1):
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"coarse_op": "galerkin", "vectors": vec, "inner_tol": 1e-8,
+                                                  "inner_maxit": 200, "fuse_dots": fuse})
+        z, its = H.deflate(gpu(v))
+        out[fuse] = (z.cpu().numpy(), its)
+        H.close()
+    assert out[0][1] == out[1][1]
+    assert rel(out[1][0], out[0][0]) < 1e-10
