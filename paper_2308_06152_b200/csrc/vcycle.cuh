@@ -695,7 +695,7 @@ __host__ __device__ inline size_t tail_smem_bytes(const LevelDesc* Ls, int lt, i
     const size_t n = (size_t)tail_rpc(Ls[l].g.ny, cs) * Ls[l].g.nx;
     b += n * 4 * sizeof(double2) + ((n * sizeof(double) + 15) / 16) * 16;   // keep 16-byte alignment
   }
-  return b;
+  return b + (size_t)Ls[last].g.nx * Ls[last].g.ny * sizeof(double2);   // + the gathered coarsest rhs
 }
 
 struct TailLevel {
@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
   extern __shared__ double2 tsm[];
   __shared__ TailLevel T[TAIL_MAX_LEVELS];
   __shared__ int curi[TAIL_MAX_LEVELS];   // 0: pre-smoothed iterate in s, 1: in t
+  __shared__ double2* s_gat;               // the whole coarsest rhs, gathered into this CTA
   double2* const uout = uv.get();
   const double2* const fin = fv.get();
   const double fsc = fv.scale();
@@ -773,6 +774,7 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
       T[q].t = reinterpret_cast<double2*>(p); p += n * sizeof(double2);
       T[q].k = reinterpret_cast<double*>(p); p += ((n * sizeof(double) + 15) / 16) * 16;
     }
+    s_gat = reinterpret_cast<double2*>(p);
   }
   __syncthreads();
   for (int q = 0; q < nl; ++q) {
@@ -836,18 +838,21 @@ __global__ void __launch_bounds__(1024) k_vc_tail(const LevelDesc* __restrict__ 
     if (threadIdx.x == 0) curi[q] = (cur == L.s) ? 0 : 1;
     cl.sync();
   }
-  // ---- coarsest: dense inverse (reading R8), one warp per owned row
+  // ---- coarsest: dense inverse (reading R8), one warp per owned row; the rhs is first gathered
+  // from the cluster into this CTA's shared memory (one distributed-shared-memory pass)
   {
     const TailLevel Cl = T[nl - 1];
     const int n = Cl.g.nx * Cl.g.ny;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int rb0 = Cl.r0 * Cl.g.nx, rb1 = Cl.r1 * Cl.g.nx;
+    double2* fl = s_gat;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) fl[c] = *tail_at(cl, Cl, Cl.f, c % Cl.g.nx, c / Cl.g.nx, rank);
+    __syncthreads();
     for (int r = rb0 + warp; r < rb1; r += nw) {
       double2 s = czero();
-      for (int c = lane; c < n; c += 32) {
-        const double2 fc = *tail_at(cl, Cl, Cl.f, c % Cl.g.nx, c / Cl.g.nx, rank);
-        s = cfma(Minv[(size_t)r * n + c], fc, s);
-      }
+      const double2* __restrict__ mrow = Minv + (size_t)r * n;
+#pragma unroll 4
+      for (int c = lane; c < n; c += 32) s = cfma(mrow[c], fl[c], s);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
