@@ -214,7 +214,7 @@ int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_
  * completes its copy by an all-gather of the owned rows and runs the rest of the V-cycle and
  * the dense coarsest solve itself).  Dots and norms are summed over the ranks; every rank then
  * takes the same scalar steps.  The outer method must be FGMRES; loops are host-polled
- * (params.graph is forced to 0) and PDL is off.
+ * (params.graph is forced to 0).
  *
  * Transports:
  *  HELM_COMM_NCCL    one process per GPU; nccl_id = 128 bytes from helm_nccl_unique_id() on

@@ -1869,9 +1869,10 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   C->rank = d->rank;
   C->nranks = d->nranks;
   C->grp = d->kind == HELM_COMM_THREADS ? d->group : nullptr;
-  // decomposed solves: host-polled loops, no PDL, no cluster tail / cooperative step
+  // decomposed solves: host-polled loops, no cluster tail / cooperative step.  PDL stays as
+  // requested: a kernel launched with it waits (griddepcontrol.wait) for its predecessor kernel
+  // -- ours or NCCL's -- to complete; event waits and copies serialise as usual.
   C->p.graph = 0;
-  C->p.pdl = 0;
   C->p.tail_max_n = 0;
   C->p.coop = 0;
   if (C->p.dist_min_rows <= 0) C->p.dist_min_rows = 16;
