@@ -1600,7 +1600,8 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
   if (C->dist) return no_dist(C, "helm_bench_graph");
   helm_ctx_s& X = *C;
   if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
-  if (which == HELM_GB_DCGS && (arg < 0 || arg + reps >= X.inner.m)) return fail(HELM_EINVAL, "bad column");
+  if ((which == HELM_GB_DCGS || which == HELM_GB_INNER_ITER) && (arg < 0 || arg + reps >= X.inner.m))
+    return fail(HELM_EINVAL, "bad column");
   const Level& F = X.L[0];
   const Level& G = X.L[1];
   cudaStream_t saved = X.s;
@@ -1625,8 +1626,10 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
       case HELM_GB_APPLY_A:
         r = op_apply(X, 0, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
         break;
-      case HELM_GB_DCGS: {
-        // one delayed-CGS2 step of the inner FGMRES at column j = arg (+ the reps before it)
+      case HELM_GB_DCGS:
+      case HELM_GB_INNER_ITER: {
+        // one delayed-CGS2 step of the inner FGMRES at column j = arg (+ the reps before it);
+        // HELM_GB_INNER_ITER: the whole inner iteration (V-cycle from level 1, E, DCGS2 step)
         Fgm& K = X.inner;
         FgmState* st = K.st;
         if (i == 0) {
@@ -1640,6 +1643,13 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         const long long ln = (long long)K.n;
         DVec vj(K.V, &st->j, ln, &st->inv_hn), w(K.V + K.n, &st->j, ln);
         const GsGeom& gg = K.geo;
+        if (which == HELM_GB_INNER_ITER) {
+          DVec zj(K.Z, &st->j, ln);
+          r = vcycle(X, 1, vj, zj, nullptr);
+          if (r != HELM_OK) break;
+          r = apply_E(X, zj, DVec(), w);
+          if (r != HELM_OK) break;
+        }
         launch_k(X, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, (const int*)&st->j, 1,
                  vj, w, ln, gg.chunk, K.part);
         r = post_launch(X);

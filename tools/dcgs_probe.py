@@ -19,6 +19,7 @@ for j in (5, 25, 45):
     out[f"dcgs{j}"] = round(H.helm_bench_graph("dcgs", j, 3), 2)
 out["vcycle1"] = round(H.helm_bench_graph("vcycle", 1, 20), 2)
 out["apply_E"] = round(H.helm_bench_graph("apply_E", 0, 50), 2)
+out["inner_iter25"] = round(H.helm_bench_graph("inner_iter", 25, 3), 2)
 if os.environ.get("HELM_PROBE_NOSOLVE"):
     print(json.dumps(out), flush=True)
     sys.exit(0)
