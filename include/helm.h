@@ -215,7 +215,7 @@ int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_
  * neighbours before every kernel that reads them; the levels below D are replicated (each rank
  * completes its copy by an all-gather of the owned rows and runs the rest of the V-cycle and
  * the dense coarsest solve itself).  Dots and norms are summed over the ranks; every rank then
- * takes the same scalar steps.  The outer method must be FGMRES; loops are host-polled
+ * takes the same scalar steps.  Both outer methods (FGMRES, GCR); loops are host-polled
  * (params.graph is forced to 0).
  *
  * Transports:

@@ -961,33 +961,56 @@ int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
 int gcr_cycle(helm_ctx_s& C, bool first) {
   Fgm& K = C.outer;
   FgmState* st = K.st;
-  const size_t n = K.n;
-  const long long ln = (long long)n;
-  Level& F = C.L[0];
+  // stored vectors are blocks of length K.ld (decomposed) with the owned rows at K.off; the
+  // operators get whole blocks, the vector kernels the owned rows; on a decomposed context the
+  // per-rank sums are summed over the ranks before each scalar kernel
+  const size_t n = K.n, off = K.off;
+  const long long ln = (long long)n, ld = (long long)K.ld;
   const int gp = grid1d(C, n);
+  double2* ro = C.rbuf + off;
+  double2* xo = C.xbuf + off;
   auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
-    if (first) CK(cudaMemcpyAsync(C.rbuf, C.bbuf, n * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
-    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(C.rbuf), 1, K.nrm, nullptr));
+    if (first) CK(cudaMemcpyAsync(C.rbuf, C.bbuf, K.ld * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
+    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(ro), 1, K.nrm, nullptr));
     launch_k(C, k_gcr_begin, 1, 32, 0, st, (const double2*)K.nrm, first ? 1 : 0, h, use_h);
     return post_launch(C);
   };
   auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
-    DVec zj(K.Z, &st->j, ln), cj(K.V, &st->j, ln);
+    DVec zj(K.Z, &st->j, ld), cj(K.V, &st->j, ld);
+    const DVec zjo = shift(zj, off), cjo = shift(cj, off);
     CKR(adef1(C, DVec(C.rbuf), zj, C.outer.st));               // z_j = P r
     CKR(op_apply(C, 0, zj, DVec(), cj, 1.0, 0.0));             // c_j = A z_j
     for (int pass = 0; pass < 2; ++pass) {                     // CGS2, same coefficients on z_j
       double2* al = pass == 0 ? K.dots1 : K.coef;
-      CKR(gs_dots(C, K, K.V, &st->j, 0, cj, 0, al, nullptr));
-      CKR(gs_update(C, K, K.V, &st->j, 0, al, -1.0, cj, cj, 0, nullptr));
-      CKR(gs_update(C, K, K.Z, &st->j, 0, al, -1.0, zj, zj, 0, nullptr));
+      CKR(gs_dots(C, K, K.V + off, &st->j, 0, cjo, 0, al, nullptr));
+      CKR(gs_update(C, K, K.V + off, &st->j, 0, al, -1.0, cjo, cjo, 0, nullptr));
+      CKR(gs_update(C, K, K.Z + off, &st->j, 0, al, -1.0, zjo, zjo, 0, nullptr));
     }
-    launch_k(C, k_gcr_pair, gp, 256, 0, cj, (const double2*)C.rbuf, ln, K.part);
+    launch_k(C, k_gcr_pair, gp, 256, 0, cjo, (const double2*)ro, ln, K.part);
     CKR(post_launch(C));
-    launch_k(C, k_gcr_scalars, 1, 32, 0, (const double2*)K.part, gp, K.sc2, st);
+    const double2* pr = K.part;
+    int np = gp;
+    if (K.dist) {
+      launch_k(C, k_sum_pairs, 1, 32, 0, (const double2*)K.part, gp, K.nrm);
+      CKR(post_launch(C));
+      CKR(allreduce(C, K.nrm, 2));
+      pr = K.nrm;
+      np = 1;
+    }
+    launch_k(C, k_gcr_scalars, 1, 32, 0, pr, np, K.sc2, st);
     CKR(post_launch(C));
-    launch_k(C, k_gcr_finish, gp, 256, 0, cj, zj, C.xbuf, C.rbuf, (const double2*)K.sc2, ln, K.part);
+    launch_k(C, k_gcr_finish, gp, 256, 0, cjo, zjo, xo, ro, (const double2*)K.sc2, ln, K.part);
     CKR(post_launch(C));
-    launch_k(C, k_gcr_check, 1, 32, 0, st, (const double2*)K.part, gp, h, use_h);
+    pr = K.part;
+    np = gp;
+    if (K.dist) {
+      launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gp, K.nrm);
+      CKR(post_launch(C));
+      CKR(allreduce(C, K.nrm, 1));
+      pr = K.nrm;
+      np = 1;
+    }
+    launch_k(C, k_gcr_check, 1, 32, 0, st, pr, np, h, use_h);
     return post_launch(C);
   };
   return run_while(C, st, begin, body);
@@ -1887,7 +1910,6 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   C->p.coop = 0;
   if (C->p.dist_min_rows <= 0) C->p.dist_min_rows = 16;
   int r = HELM_OK;
-  if (C->p.outer != HELM_OUTER_FGMRES) r = fail(HELM_EINVAL, "decomposed contexts support the FGMRES outer method only");
   if (r == HELM_OK && C->p.dist_levels == 1) r = fail(HELM_EINVAL, "dist_levels must be 0 or >= 2");
   if (r == HELM_OK && d->kind == HELM_COMM_NCCL) {
     std::string why;

@@ -136,7 +136,10 @@ __global__ void __launch_bounds__(256) k_gs_reduce(const double2* __restrict__ p
   const int ntot = mult * ((nptr ? *nptr : 0) + nadd) + extra;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (c >= ntot) return;
+  if (c >= ntot) {   // device-sized output: zero the unused tail (a rank-sum over all slots stays finite)
+    if (nptr && lane == 0 && c < (int)(gridDim.x * blockDim.x >> 5)) out[c] = make_double2(0.0, 0.0);
+    return;
+  }
   double2 s = make_double2(0.0, 0.0);
   for (long long b = lane; b < P; b += 32) s = cadd(s, part[(long long)c * P + b]);
   s = warp_sum2(s);
@@ -993,6 +996,22 @@ __global__ void __launch_bounds__(256) k_gcr_pair(DVec cv, const double2* __rest
     }
     part[2 * blockIdx.x] = a;
     part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// out[0] = sum_q part[2q], out[1] = sum_q part[2q+1] (one warp, fixed order; decomposed GCR)
+__global__ void k_sum_pairs(const double2* __restrict__ part, int np, double2* __restrict__ out) {
+  HELM_PDL_ENTRY();
+  double2 a = make_double2(0.0, 0.0), b = a;
+  for (int q = threadIdx.x; q < np; q += 32) {
+    a = cadd(a, part[2 * q]);
+    b = cadd(b, part[2 * q + 1]);
+  }
+  a = warp_sum2(a);
+  b = warp_sum2(b);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
   }
 }
 

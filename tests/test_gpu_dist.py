@@ -143,19 +143,21 @@ def _problem(name):
     return config_problem(name)
 
 
-@pytest.mark.parametrize("name,P,vec,op,itol,imax", [
-    ("c0_tiny", 2, "bilinear", "galerkin", 1e-1, 200),
-    ("c1_k50", 2, "high_order", "galerkin", 1e-1, 200),
-    ("c1_k50", 3, "bilinear", "red_o4", 0.0, 40),
-    ("mp_som_k40", 2, "high_order", "red_glk1", 0.0, 30),
-    ("wedge_f10", 4, "high_order", "galerkin", 1e-1, 300),
+@pytest.mark.parametrize("name,P,vec,op,itol,imax,outer", [
+    ("c0_tiny", 2, "bilinear", "galerkin", 1e-1, 200, "fgmres"),
+    ("c1_k50", 2, "high_order", "galerkin", 1e-1, 200, "fgmres"),
+    ("c1_k50", 3, "bilinear", "red_o4", 0.0, 40, "fgmres"),
+    ("mp_som_k40", 2, "high_order", "red_glk1", 0.0, 30, "fgmres"),
+    ("wedge_f10", 4, "high_order", "galerkin", 1e-1, 300, "fgmres"),
+    ("c1_k50", 2, "high_order", "galerkin", 1e-1, 200, "gcr"),
+    ("mp_som_k40", 3, "bilinear", "red_o4", 0.0, 30, "gcr"),
 ])
-def test_dist_solve(lib, name, P, vec, op, itol, imax):
+def test_dist_solve(lib, name, P, vec, op, itol, imax, outer):
     """Outer iteration counts within +-1 of the oracle's, the true residual met, and at tol 1e-10
     the solution within 1e-6 of the oracle's (reading R16), with every rank reporting the same
     counts."""
     p = _problem(name)
-    prm = dict(SMALL, coarse_op=op, vectors=vec, inner_tol=itol, inner_maxit=imax)
+    prm = dict(SMALL, coarse_op=op, vectors=vec, inner_tol=itol, inner_maxit=imax, outer=outer)
 
     def go(tol):
         def fn(H):
@@ -169,14 +171,14 @@ def test_dist_solve(lib, name, P, vec, op, itol, imax):
 
     x, rep = go(1e-6)
     so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
-                                                           inner_maxit=imax, maxit=600))
+                                                           inner_maxit=imax, maxit=600, outer=outer))
     xo, ro = so.solve(p.b)
     assert rep["converged"] and ro["converged"]
     assert abs(rep["outer_iterations"] - ro["outer_iterations"]) <= 1, (rep, ro["outer_iterations"])
     assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
     xt, rt = go(1e-10)
     so_t = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
-                                                             inner_maxit=imax, maxit=600, tol=1e-10))
+                                                             inner_maxit=imax, maxit=600, tol=1e-10, outer=outer))
     xo_t, _ = so_t.solve(p.b)
     assert rt["converged"]
     assert rel(xt, xo_t) < 1e-6
@@ -184,7 +186,7 @@ def test_dist_solve(lib, name, P, vec, op, itol, imax):
 
 def test_dist_rejects_unsupported(lib):
     p, P = GRIDS[0]
-    with pytest.raises(lib.HelmError):
-        run_ranks(lib, 2, p, dict(SMALL, outer="gcr"), lambda H: None)
+    with pytest.raises(lib.HelmError):   # dist_levels = 1 (level 1 must be decomposed)
+        run_ranks(lib, 2, p, dict(SMALL, dist_levels=1), lambda H: None)
     with pytest.raises(lib.HelmError):   # 8 ranks cannot own >= 16 rows of a 63-row grid
         run_ranks(lib, 8, p, {}, lambda H: None)
