@@ -19,6 +19,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef HELM_VC_MINB
+#define HELM_VC_MINB 1
+#endif
 namespace helm {
 
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
@@ -59,7 +62,7 @@ __device__ __forceinline__ double2 interior_stencil(double ih2, double2 ap, doub
 // 2I+o-1 .. 2I+o+1; the residual there needs u one node further out.  f (scaled) and k of the
 // region are kept in shared memory for the residual phase.
 template <int TCX, int TCY>
-__global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
+__global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
                                                  double sr, double si, double omega, double2* __restrict__ u,
                                                  double2* __restrict__ fc) {
   HELM_PDL_ENTRY();
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(256) k_vc_down(Geo F, Geo G, int o, DVec fv, c
 // ------------------------------------------------------------------ up leg
 // CTA = TX x TY fine points, 32 x 8 threads; u1 is formed on the tile plus a 1-node halo.
 template <int TX, int TY>
-__global__ void __launch_bounds__(256) k_vc_up(Geo F, Geo G, int o, const double2* __restrict__ u,
+__global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o, const double2* __restrict__ u,
                                                const double2* __restrict__ e, DVec fv,
                                                const double* __restrict__ k, double sr, double si, double omega,
                                                const double2* __restrict__ addq, DVec yv) {
