@@ -49,6 +49,9 @@ extern "C" {
 #define HELM_OUTER_FGMRES 0 /* flexible GMRES, Algorithm 1 (flexible form, §6.3) */
 #define HELM_OUTER_GCR 1    /* preconditioned GCR, PAPER.md:427 and §6.3 */
 
+#define HELM_PRECOND_ADEF1 0 /* P = M^-1 (I - A Q) + Q, Eq. 3.21 */
+#define HELM_PRECOND_TLKM 1  /* P = [(I - A~ Q~) + gamma Q~] M^-1, Eq. 3.15-3.18 (practical form) */
+
 #define HELM_VECTORS_BILINEAR 0   /* A-DEF1: Z = Eq. 3.9, restriction Z^T (Eq. 3.7 per direction) */
 #define HELM_VECTORS_HIGH_ORDER 1 /* APD: Z = Eq. 3.12, Z^T = Eq. 3.14 (§3.2.1, §3.2.2) */
 
@@ -113,6 +116,11 @@ typedef struct {
   int fuse_dots;       /* 1: with str-Glk, the inner FGMRES applies E and pass 1 of the delayed CGS2
                           (the dots against the basis) in one kernel; measured slower on B200
                           than the two kernels (0.577 vs 0.568 s per bench solve), so 0 (default) */
+  int precond;         /* HELM_PRECOND_ADEF1 (default; A-DEF1, or APD with the higher-order vectors)
+                          or HELM_PRECOND_TLKM (practical two-level Krylov method, §3.2.2
+                          and Tables 1-2: coarse matrix Z^T Z M_2h^-1 A_2h solved by unpreconditioned
+                          FGMRES; two fine V-cycles per application; single-GPU contexts only) */
+  double gamma;        /* TLKM shift (1) */
 } helm_params;
 
 typedef struct {
@@ -154,7 +162,7 @@ int helm_apply_E(helm_ctx ctx, const double* x_dev, double* y_dev);
 int helm_vcycle(helm_ctx ctx, int level, const double* f_dev, double* u_dev);
 /* z = P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v, Q = Z E^{-1} Z^T (Eq. 3.21, Eq. 5.3-5.5),
  * E^{-1} by CSLP-preconditioned FGMRES to inner_tol (writes the inner count to
- * *inner_its if non-NULL). */
+ * *inner_its if non-NULL); with params.precond = HELM_PRECOND_TLKM the TLKM preconditioner. */
 int helm_deflate(helm_ctx ctx, const double* v_dev, double* z_dev, int* inner_its);
 /* Solve A x = b by A-DEF1/APD-preconditioned FGMRES (or GCR, params.outer) from x0 = 0 to
  * ||b - A x||/||b|| <= tol

@@ -26,6 +26,14 @@ Readings:
       preconditioner of E), the rounding-insensitive alternative to the tolerance stop.
   APD (vectors="high_order", §3.2.2 "When the higher-order deflation vector is employed, it
       will be denoted as Adapted Preconditioned Deflation"): Z = Eq. 3.12, Z^T = Eq. 3.14.
+
+TLKM (preconditioner="tlkm"), §3.2.2 (:385-406) and Tables 1-2 (:856-901), in the
+paper's practical form: P_TLKM = P~_{h,gamma} M^{-1} with P~_{h,gamma} = (I - A~ Q~) + gamma Q~,
+A~ = M^{-1} A, Q~ = I_{2h}^h A~_{2h}^{-1} I_h^{2h}, gamma = 1 (:398), and the coarse matrix of
+the practical method I_h^{2h} I_{2h}^h M_{2h}^{-1} A_{2h} (:880) with A_{2h} the configured coarse
+operator (ReD-O2 in Tables 1-2) and M_{2h}^{-1} one CSLP V-cycle from level 1 (reading R23); the
+coarse problem by unpreconditioned GMRES ("(GMRES)" column of Tables 1-2).  One application:
+t = M^{-1} v, e = A~_{2h}^{-1} Z^T t, q = Z e, z = t - M^{-1} A q + gamma q.
 """
 from __future__ import annotations
 
@@ -59,6 +67,8 @@ class SolverParams:
     max_levels: int = 64
     coarsest_n: int = 0               # stop coarsening at the first level with <= coarsest_n unknowns (R7)
     outer: str = "fgmres"             # fgmres | gcr (§6.3)
+    preconditioner: str = "adef1"     # adef1 (A-DEF1 / APD) | tlkm (practical TLKM, §3.2.2)
+    gamma: float = 1.0                # TLKM shift
 
 
 class Solver:
@@ -116,6 +126,32 @@ class Solver:
         self.inner_its.append(its)
         return e
 
+    def tlkm_coarse(self, x):
+        """Coarse matrix of the practical TLKM: I_h^{2h} I_{2h}^h M_{2h}^{-1} A_{2h} x."""
+        return self.Zt(self.Zp(self.vcycle(self.E(x), 1)))
+
+    def tlkm(self, v):
+        """P_TLKM v = P~_{h,gamma} M^{-1} v (Eq. 3.17-3.18, practical form, reading R23)."""
+        t = self.vcycle(v, 0)
+        c = self.Zt(t)
+        if self.p.inner_solver == "direct":
+            n = self.cshape[0] * self.cshape[1]
+            Td = np.zeros((n, n), dtype=np.complex128)
+            for col in range(n):
+                u = np.zeros(n, dtype=np.complex128)
+                u[col] = 1.0
+                Td[:, col] = self.tlkm_coarse(u.reshape(self.cshape)).ravel()
+            e = np.linalg.solve(Td, c.ravel()).reshape(self.cshape)
+        else:
+            e, its, _ = fgmres(self.tlkm_coarse, lambda w: w, c, self.p.inner_tol, self.p.inner_maxit,
+                               orth=self.p.orth)
+            self.inner_its.append(its)
+        q = self.Zp(e)
+        return t - self.vcycle(self.A(q), 0) + self.p.gamma * q
+
+    def precond(self, v):
+        return self.tlkm(v) if self.p.preconditioner == "tlkm" else self.adef1(v)
+
     def Q(self, v):
         """Q_h v = I_{2h}^h A_{2h}^{-1} I_h^{2h} v (Eq. 5.3-5.5)."""
         v1 = self.Zt(v)
@@ -133,10 +169,10 @@ class Solver:
         self.inner_its = []
         t0 = time.perf_counter()
         if self.p.outer == "gcr":
-            x, its, conv = gcr(self.A, self.adef1, np.asarray(b, dtype=np.complex128), self.p.tol, self.p.maxit,
+            x, its, conv = gcr(self.A, self.precond, np.asarray(b, dtype=np.complex128), self.p.tol, self.p.maxit,
                                history=history)
         else:
-            x, its, conv = fgmres(self.A, self.adef1, np.asarray(b, dtype=np.complex128),
+            x, its, conv = fgmres(self.A, self.precond, np.asarray(b, dtype=np.complex128),
                                   self.p.tol, self.p.maxit, history=history, orth=self.p.orth)
         t1 = time.perf_counter()
         r = np.asarray(b) - self.A(x)

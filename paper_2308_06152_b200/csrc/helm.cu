@@ -118,6 +118,8 @@ struct helm_ctx_s {
   double2 *cc = nullptr, *ce = nullptr;   // coarse rhs / solution
   double2 *bbuf = nullptr, *xbuf = nullptr;  // solve input/output (graph-stable addresses)
   double2* rbuf = nullptr;        // GCR residual
+  double2 *tl_f[3] = {nullptr, nullptr, nullptr};   // TLKM fine scratch
+  double2 *tl_c[3] = {nullptr, nullptr, nullptr};   // TLKM coarse (level 1) scratch
   Fgm outer, inner;
   FgmState* hst = nullptr;        // pinned host mirror of a state
   uint4* flush = nullptr;
@@ -945,6 +947,46 @@ int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_st
   return fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C));
 }
 
+// Practical TLKM (§3.2.2, :385-406, Tables 1-2; oracle/solver.py Solver.tlkm, reading
+// R23): z = P~_{h,gamma} M^{-1} v = t - M^{-1} A q + gamma q with t = M^{-1} v, q = Z e and e the
+// solution of (Z^T Z) M_{2h}^{-1} A_{2h} e = Z^T t by unpreconditioned FGMRES (inner basis).
+int tlkm(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
+  const Level& F = C.L[0];
+  const size_t n0 = F.n, n1 = C.L[1].n;
+  double2 *t = C.tl_f[0], *s = C.tl_f[1];
+  CKR(vcycle(C, 0, v, DVec(t), nullptr));                      // t = M^{-1} v
+  CKR(defl_restrict(C, DVec(t), C.cc));                        // c = Z^T t
+  Fgm& K = C.inner;
+  launch_k(C, k_fgm_reset, 1, 1, 0, K.st, C.p.inner_tol, C.p.inner_maxit, K.m);
+  CKR(post_launch(C));
+  auto opA = [&](DVec x, DVec f, DVec y) -> int {             // y = Z^T Z M_{2h}^{-1} A_{2h} x
+    if (f.p) return fail(HELM_EINVAL, "TLKM coarse operator has no residual form");
+    CKR(apply_E(C, x, DVec(), DVec(C.tl_c[0])));
+    CKR(vcycle(C, 1, DVec(C.tl_c[0]), DVec(C.tl_c[1]), nullptr));
+    CKR(defl_prolong(C, C.tl_c[1], C.tl_f[2]));
+    CKR(defl_restrict(C, DVec(C.tl_f[2]), C.tl_c[2]));
+    launch_k(C, k_copy_dvec, grid1d(C, n1), 256, 0, DVec(C.tl_c[2]), y, (long long)n1);
+    return post_launch(C);
+  };
+  auto opP = [&](DVec x, DVec y) -> int {                      // unpreconditioned ("(GMRES)")
+    launch_k(C, k_copy_dvec, grid1d(C, n1), 256, 0, x, y, (long long)n1);
+    return post_launch(C);
+  };
+  CKR(fgmres_cycle(C, K, opA, opP, DVec(C.cc), C.ce, true, outer_stats));
+  CKR(defl_prolong(C, C.ce, C.dq));                            // q = Z e
+  CKR(op_apply(C, 0, DVec(C.dq), DVec(), DVec(C.dt), 1.0, 0.0));   // A q
+  CKR(vcycle(C, 0, DVec(C.dt), DVec(s), nullptr));             // M^{-1} A q
+  launch_k(C, k_tlkm_combine, grid1d(C, n0), 256, 0, (const double2*)t, (const double2*)s, (const double2*)C.dq,
+           C.p.gamma, z, (long long)n0);
+  return post_launch(C);
+}
+
+// The configured two-level preconditioner (A-DEF1/APD or TLKM)
+int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats);
+int precond(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
+  return C.p.precond == HELM_PRECOND_TLKM ? tlkm(C, v, z, outer_stats) : adef1(C, v, z, outer_stats);
+}
+
 // z = P_{A-DEF1} v = M^{-1}(v - A Q v) + Q v  (Eq. 3.21 / 5.2-5.5)
 int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
   Level& F = C.L[0];
@@ -978,7 +1020,7 @@ int gcr_cycle(helm_ctx_s& C, bool first) {
   auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     DVec zj(K.Z, &st->j, ld), cj(K.V, &st->j, ld);
     const DVec zjo = shift(zj, off), cjo = shift(cj, off);
-    CKR(adef1(C, DVec(C.rbuf), zj, C.outer.st));               // z_j = P r
+    CKR(precond(C, DVec(C.rbuf), zj, C.outer.st));             // z_j = P r
     CKR(op_apply(C, 0, zj, DVec(), cj, 1.0, 0.0));             // c_j = A z_j
     for (int pass = 0; pass < 2; ++pass) {                     // CGS2, same coefficients on z_j
       double2* al = pass == 0 ? K.dots1 : K.coef;
@@ -1021,7 +1063,7 @@ int outer_cycle(helm_ctx_s& C, bool first) {
   if (C.p.outer == HELM_OUTER_GCR) return gcr_cycle(C, first);
   Level& F = C.L[0];
   auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, 0, x, f, y, 1.0, 0.0); };
-  auto opP = [&](DVec v, DVec z) { return adef1(C, v, z, C.outer.st); };
+  auto opP = [&](DVec v, DVec z) { return precond(C, v, z, C.outer.st); };
   return fgmres_cycle(C, C.outer, opA, opP, DVec(C.bbuf), C.xbuf, first, nullptr);
 }
 
@@ -1076,6 +1118,8 @@ void helm_default_params(helm_params* p) {
   p->dist_min_rows = 16;
   p->col_pipe = 1;
   p->fuse_dots = 0;
+  p->precond = HELM_PRECOND_ADEF1;
+  p->gamma = 1.0;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1109,6 +1153,8 @@ static void destroy_ctx(helm_ctx_s* C) {
   cudaFree(C->bbuf);
   cudaFree(C->xbuf);
   cudaFree(C->rbuf);
+  for (auto b : C->tl_f) cudaFree(b);
+  for (auto b : C->tl_c) cudaFree(b);
   cudaFree(C->flush);
   if (C->hst) cudaFreeHost(C->hst);
   fgm_free(C->outer);
@@ -1133,6 +1179,8 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.nu_pre < 1 || p.nu_post < 0) return fail(HELM_EINVAL, "nu_pre >= 1, nu_post >= 0");
   if (p.inner_maxit < 1) return fail(HELM_EINVAL, "inner_maxit >= 1");
   if (p.outer != HELM_OUTER_FGMRES && p.outer != HELM_OUTER_GCR) return fail(HELM_EINVAL, "bad outer %d", p.outer);
+  if (p.precond != HELM_PRECOND_ADEF1 && p.precond != HELM_PRECOND_TLKM) return fail(HELM_EINVAL, "bad precond %d", p.precond);
+  if (p.precond == HELM_PRECOND_TLKM && C.dist) return fail(HELM_EINVAL, "TLKM is not available on a decomposed context");
   if (p.coarse_op < HELM_COARSE_GALERKIN || p.coarse_op > HELM_COARSE_RED_9PTO2)
     return fail(HELM_EINVAL, "bad coarse_op %d", p.coarse_op);
   if (p.vectors == HELM_VECTORS_BILINEAR) {
@@ -1338,6 +1386,10 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   CKR(dalloc(&C.bbuf, C.L[0].n));
   CKR(dalloc(&C.xbuf, C.L[0].n));
   CKR(dalloc(&C.rbuf, C.L[0].n));
+  if (p.precond == HELM_PRECOND_TLKM) {
+    for (auto& b : C.tl_f) CKR(dalloc(&b, C.L[0].n));
+    for (auto& b : C.tl_c) CKR(dalloc(&b, C.L[1].n));
+  }
   if (C.dist) {
     for (double2* b : {C.dq, C.dt, C.bbuf, C.xbuf, C.rbuf}) CK(cudaMemsetAsync(b, 0, C.L[0].n * sizeof(double2), C.s));
     for (double2* b : {C.cc, C.ce}) CK(cudaMemsetAsync(b, 0, C.L[1].n * sizeof(double2), C.s));
@@ -1460,9 +1512,9 @@ int helm_vcycle(helm_ctx C, int level, const double* f, double* u) {
 int helm_deflate(helm_ctx C, const double* v, double* z, int* inner_its) {
   if (!C || !v || !z) return fail(HELM_EINVAL, "null argument");
   if (C->dist)
-    CKR(dist_io0(*C, v, z, [&](DVec in, DVec out) { return adef1(*C, in, out, nullptr); }));
+    CKR(dist_io0(*C, v, z, [&](DVec in, DVec out) { return precond(*C, in, out, nullptr); }));
   else
-    CKR(adef1(*C, DVec((const double2*)v), DVec((double2*)z), nullptr));
+    CKR(precond(*C, DVec((const double2*)v), DVec((double2*)z), nullptr));
   if (inner_its) {
     CKR(read_state(*C, C->inner.st));
     *inner_its = C->hst->its;

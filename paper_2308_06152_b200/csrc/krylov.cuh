@@ -609,6 +609,25 @@ __global__ void k_dcgs_stepB(FgmState* st, double2* H, double* cs, double2* sn, 
   }
 }
 
+// z = t - s + gamma q (TLKM combine; t may alias z)
+__global__ void k_tlkm_combine(const double2* __restrict__ t, const double2* __restrict__ s,
+                               const double2* __restrict__ q, double gamma, DVec zv, long long n) {
+  HELM_PDL_ENTRY();
+  double2* z = zv.get();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    z[e] = cadd(csub(t[e], s[e]), cscale(gamma, q[e]));
+}
+
+// y = x (DVec slots)
+__global__ void k_copy_dvec(DVec xv, DVec yv, long long n) {
+  HELM_PDL_ENTRY();
+  const double2* x = xv.get();
+  double2* y = yv.get();
+  const double sc = xv.scale();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    y[e] = cscale(sc, x[e]);
+}
+
 // out[0] = sum of np partials (one warp, fixed order)
 __global__ void k_sum_part(const double2* __restrict__ part, int np, double2* __restrict__ out) {
   HELM_PDL_ENTRY();

@@ -19,6 +19,7 @@ HELM_BC_SOMMERFELD = 1
 COARSE_OPS = {"galerkin": 0, "red_o2": 1, "red_o4": 2, "red_glk1": 3, "red_glk2": 4, "red_o6": 5, "red_cmpo4": 6, "red_9pto2": 7}
 VECTORS = {"bilinear": 0, "high_order": 1}
 OUTER = {"fgmres": 0, "gcr": 1}
+PRECOND = {"adef1": 0, "tlkm": 1}
 BCS = {"dirichlet": HELM_BC_DIRICHLET, "sommerfeld": HELM_BC_SOMMERFELD}
 
 
@@ -34,7 +35,8 @@ class helm_params(ctypes.Structure):
                 ("graph", ctypes.c_int), ("tail_max_n", ctypes.c_int), ("pdl", ctypes.c_int),
                 ("coarsest_n", ctypes.c_int), ("coop", ctypes.c_int), ("outer", ctypes.c_int),
                 ("col_min_n", ctypes.c_int), ("dist_levels", ctypes.c_int), ("dist_min_rows", ctypes.c_int),
-                ("col_pipe", ctypes.c_int), ("fuse_dots", ctypes.c_int)]
+                ("col_pipe", ctypes.c_int), ("fuse_dots", ctypes.c_int), ("precond", ctypes.c_int),
+                ("gamma", ctypes.c_double)]
 
 
 class helm_dist(ctypes.Structure):
@@ -131,6 +133,8 @@ def default_params(**overrides) -> helm_params:
             val = VECTORS[val]
         if key == "outer" and isinstance(val, str):
             val = OUTER[val]
+        if key == "precond" and isinstance(val, str):
+            val = PRECOND[val]
         if key == "beta":
             p.beta1, p.beta2 = val
             continue

@@ -360,3 +360,36 @@ def test_fused_E_dots_matches(lib, vec):
         H.close()
     assert out[0][1] == out[1][1]
     assert rel(out[1][0], out[0][0]) < 1e-10
+
+
+
+@pytest.mark.parametrize("vec", ["bilinear", "high_order"])
+def test_tlkm_apply_and_solve(lib, vec):
+    """Practical TLKM (reading R23): one application at a tight coarse tolerance matches the
+    oracle's; solves match its outer counts (+-1) and, at 1e-10, its solution."""
+    for p in GRIDS[:3]:
+        prm = {"precond": "tlkm", "coarse_op": "red_o2", "vectors": vec, "inner_tol": 1e-10, "inner_maxit": 600}
+        H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, prm)
+        s = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(preconditioner="tlkm", coarse_op="red_o2", vectors=vec,
+                                                              inner_tol=1e-10, inner_maxit=600))
+        v = random_field(p.shape, 21)
+        z, its = H.deflate(gpu(v))
+        assert rel(z.cpu().numpy(), s.tlkm(v)) < 1e-8, p.shape
+        H.close()
+    for name in ("c0_tiny", "mp_som_k20"):
+        pr = _problem(name)
+        prm = {"precond": "tlkm", "coarse_op": "red_o2", "vectors": vec, "inner_tol": 1e-8, "inner_maxit": 600}
+        H = lib.helm_setup(pr, prm)
+        x, rep = H.solve(gpu(pr.b), tol=1e-6, maxit=300)
+        so = oracle.Solver(pr.k, pr.h, pr.bc, oracle.SolverParams(preconditioner="tlkm", coarse_op="red_o2", vectors=vec,
+                                                                  inner_tol=1e-8, inner_maxit=600, maxit=300))
+        xo, ro = so.solve(pr.b)
+        assert rep["converged"] and ro["converged"]
+        assert abs(rep["outer_iterations"] - ro["outer_iterations"]) <= 1, (rep, ro["outer_iterations"])
+        xt, _ = H.solve(gpu(pr.b), tol=1e-10, maxit=400)
+        so_t = oracle.Solver(pr.k, pr.h, pr.bc, oracle.SolverParams(preconditioner="tlkm", coarse_op="red_o2",
+                                                                    vectors=vec, inner_tol=1e-8, inner_maxit=600,
+                                                                    maxit=400, tol=1e-10))
+        xo_t, _ = so_t.solve(pr.b)
+        assert rel(xt.cpu().numpy(), xo_t) < 1e-6
+        H.close()

@@ -122,3 +122,39 @@ def test_gcr_outer_solver_matches_dense_solve():
     assert rep["converged"]
     r = p.b - oracle.apply_A(x, p.k, p.h, p.bc)
     assert np.linalg.norm(r) / np.linalg.norm(p.b) <= 1e-10
+
+
+def test_tlkm_composition_dense():
+    """Practical TLKM (reading R23) against its definition assembled from dense matrices:
+    P = [I - M0^-1 A Z T^-1 Z^T + gamma Z T^-1 Z^T] M0^-1 with T = Z^T Z M1^-1 A_2h (PAPER.md
+    Eq. 3.15-3.18 and :880), every factor built by applying the oracle's primitives to unit
+    vectors -- pins the composition order (which operator is inverted where, the extra M^-1 on
+    the deflation term, the shift gamma)."""
+    import numpy as np
+    from workloads import random_field, random_k
+    shape, h, bc = (15, 15), 1 / 16, "dirichlet"
+    k = random_k(shape, 3, 4, 12)
+    s = oracle.Solver(k, h, bc, oracle.SolverParams(preconditioner="tlkm", coarse_op="red_o2", inner_solver="direct",
+                                                    gamma=0.7))
+    n0 = shape[0] * shape[1]
+    cs = s.cshape
+    n1 = cs[0] * cs[1]
+
+    def dense(fn, nin, sin):
+        cols = []
+        for c in range(nin):
+            e = np.zeros(nin, complex)
+            e[c] = 1
+            cols.append(fn(e.reshape(sin)).ravel())
+        return np.array(cols).T
+    M0 = dense(lambda v: s.vcycle(v, 0), n0, shape)
+    M1 = dense(lambda v: s.vcycle(v, 1), n1, cs)
+    A = dense(s.A, n0, shape)
+    E = dense(s.E, n1, cs)
+    Z = dense(s.Zp, n1, cs)
+    Zt = dense(s.Zt, n0, shape)
+    T = Zt @ Z @ M1 @ E
+    Qt = Z @ np.linalg.solve(T, Zt)
+    P = (np.eye(n0) - M0 @ A @ Qt + 0.7 * Qt) @ M0
+    v = random_field(shape, 9)
+    np.testing.assert_allclose(s.tlkm(v).ravel(), P @ v.ravel(), rtol=1e-9, atol=1e-9 * np.abs(P @ v.ravel()).max())

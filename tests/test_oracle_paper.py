@@ -54,3 +54,14 @@ def test_appendix_b_red9pt_between_o4_and_o2():
         assert r["converged"]
         its[op] = r["outer_iterations"]
     assert its["red_o4"] <= its["red_9pto2"] <= its["red_o2"], its
+
+
+@pytest.mark.parametrize("row", GOLD["tables12_tlkm_red_o2"]["rows"], ids=lambda r: f"{r['bc']}-{r['nodes']}-{r['k']}")
+def test_tlkm_tables12(row):
+    """Tables 1-2, TLKM column: the practical TLKM with ReD-O2 (reading R23, exact coarse solve)
+    takes the printed outer iteration counts within 3 (the band of the Table 4 pins)."""
+    p = mp_problem(float(row["k"]), row["nodes"] - 1, row["bc"])
+    _, r = oracle.solve(p, oracle.SolverParams(preconditioner="tlkm", coarse_op="red_o2", inner_solver="direct",
+                                               maxit=300))
+    assert r["converged"]
+    assert abs(r["outer_iterations"] - row["tlkm"]) <= 3, (r["outer_iterations"], row)

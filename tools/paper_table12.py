@@ -17,15 +17,17 @@ from paper_2308_06152_b200 import helm  # noqa: E402
 from workloads import mp_problem  # noqa: E402
 
 # PAPER.md:862-870 (Table 1, CSLP-GMRES columns) and :893-901 (Table 2)
-T1 = {(33, 20): (8, 21), (65, 40): (16, 41), (129, 80): (44, 95), (65, 20): (6, 17), (129, 40): (9, 20)}
-T2 = {(33, 20): (9, 20), (65, 40): (13, 26), (129, 80): (22, 41), (65, 20): (6, 17), (129, 40): (7, 19),
-      (257, 80): (10, 20)}
+T1 = {(33, 20): (8, 21, 9), (65, 40): (16, 41, 20), (129, 80): (44, 95, 70), (65, 20): (6, 17, 6),
+      (129, 40): (9, 20, 9)}
+T2 = {(33, 20): (9, 20, 9), (65, 40): (13, 26, 13), (129, 80): (22, 41, 24), (65, 20): (6, 17, 6), (129, 40): (7, 19, 7),
+      (257, 80): (10, 20, 8)}
 # PAPER.md:1323-1327 (Appendix B): ReD-9ptO2, ReD-O2, ReD-O4
 TB = {(129, 40): (15, 17, 14), (257, 80): (20, 28, 19), (321, 100): (27, 37, 22)}
 
 
-def run(p, vec, op):
-    H = helm.helm_setup(p, {"vectors": vec, "coarse_op": op, "inner_tol": 1e-8, "inner_maxit": 3000})
+def run(p, vec, op, precond="adef1"):
+    H = helm.helm_setup(p, {"vectors": vec, "coarse_op": op, "inner_tol": 1e-8, "inner_maxit": 3000,
+                            "precond": precond})
     b = torch.from_numpy(p.b).cuda()
     t0 = time.perf_counter()
     _, rep = H.solve(b, 1e-6, 400)
@@ -37,14 +39,16 @@ def run(p, vec, op):
 lines = []
 for bc, table, name in (("dirichlet", T1, "Table 1 (MP-2a)"), ("sommerfeld", T2, "Table 2 (MP-2b)")):
     lines.append(f"\n{name}, A-DEF1, bilinear vectors: outer its (mean coarse its) -- paper / B200\n")
-    lines.append("| grid | k | kh | str-Glk paper | str-Glk B200 | ReD-O2 paper | ReD-O2 B200 |")
-    lines.append("|---|---|---|---|---|---|---|")
-    for (nodes, k), (pg, pr) in table.items():
+    lines.append("| grid | k | kh | str-Glk paper | str-Glk B200 | ReD-O2 paper | ReD-O2 B200 | TLKM paper | TLKM B200 |")
+    lines.append("|---|---|---|---|---|---|---|---|---|")
+    for (nodes, k), (pg, pr, pt) in table.items():
         p = mp_problem(float(k), nodes - 1, bc)
         g = run(p, "bilinear", "galerkin")
         r = run(p, "bilinear", "red_o2")
-        print(json.dumps({"table": name, "nodes": nodes, "k": k, "galerkin": g, "red_o2": r}), flush=True)
-        lines.append(f"| {nodes}² | {k} | {k / (nodes - 1):.4g} | {pg} | {g[0]} ({g[2]}) | {pr} | {r[0]} ({r[2]}) |")
+        tl = run(p, "bilinear", "red_o2", "tlkm")
+        print(json.dumps({"table": name, "nodes": nodes, "k": k, "galerkin": g, "red_o2": r, "tlkm": tl}), flush=True)
+        lines.append(f"| {nodes}² | {k} | {k / (nodes - 1):.4g} | {pg} | {g[0]} ({g[2]}) | {pr} | {r[0]} ({r[2]}) | "
+                     f"{pt} | {tl[0]} ({tl[2]}) |")
 lines.append("\nAppendix B (MP-2a, APD vectors): outer its -- paper / B200\n")
 lines.append("| grid | k | 9ptO2 paper | 9ptO2 B200 | O2 paper | O2 B200 | O4 paper | O4 B200 |")
 lines.append("|---|---|---|---|---|---|---|---|")
