@@ -190,3 +190,21 @@ def test_dist_rejects_unsupported(lib):
         run_ranks(lib, 2, p, dict(SMALL, dist_levels=1), lambda H: None)
     with pytest.raises(lib.HelmError):   # 8 ranks cannot own >= 16 rows of a 63-row grid
         run_ranks(lib, 8, p, {}, lambda H: None)
+
+
+def test_dist_restarted_outer(lib):
+    """Decomposed FGMRES(m) restarts (the restart cycle applies A to the current x through the
+    halo path) still meet the tolerance, with every rank agreeing."""
+    p = _problem("c1_k50")
+    prm = dict(SMALL, coarse_op="galerkin", vectors="high_order", inner_tol=1e-1, inner_maxit=200, restart=4)
+
+    def fn(H):
+        x, rep = H.solve(rows_of(p.b)(H), tol=1e-6, maxit=200)
+        return x.cpu().numpy(), rep
+
+    parts = run_ranks(lib, 2, p, prm, fn)
+    reps = [res[1] for _, _, res in parts]
+    assert all(r["outer_iterations"] == reps[0]["outer_iterations"] for r in reps)
+    assert reps[0]["converged"] and reps[0]["restarts"] > 0
+    x = assemble([(r0, nr, res[0]) for r0, nr, res in parts], p.ny, p.nx)
+    assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
