@@ -385,9 +385,10 @@ Level coarse_of(const helm_ctx_s& C, int l) {
 bool gathers(const helm_ctx_s& C, int l) { return C.dist && C.L[l].block && !C.L[l + 1].block; }
 
 // ------------------------------------------------------------------ operator launches
-int op_apply(helm_ctx_s& C, int l, DVec u, DVec f, DVec y, double sr, double si) {
+// fresh: u's ghost rows are already exact (a V-cycle or Z output, see vcycle): no halo
+int op_apply(helm_ctx_s& C, int l, DVec u, DVec f, DVec y, double sr, double si, bool fresh = false) {
   const Level& L = C.L[l];
-  CKR(halo(C, l, u));
+  if (!fresh) CKR(halo(C, l, u));
   const unsigned blocks = (unsigned)((L.n + 255) / 256);
   if (f.p) launch_k(C, k_apply_op<1>, blocks, 256, 0, L.g, u, f, y, L.k, sr, si);
   else launch_k(C, k_apply_op<0>, blocks, 256, 0, L.g, u, DVec(), y, L.k, sr, si);
@@ -468,11 +469,11 @@ int apply_E_dots(helm_ctx_s& C, DVec x, DVec y, DVec vt, const double2* V, long 
 }
 
 // y = E x (f.p == null) or y = f - E x on level 1
-int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
+int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y, bool fresh = false) {
   const Level& G = C.L[1];
   const dim3 gg = grd2d(G.g.nx, G.g.ny);
   const bool res = f.p != nullptr;
-  CKR(halo(C, 1, x));
+  if (!fresh) CKR(halo(C, 1, x));
   switch (C.p.coarse_op) {
     case HELM_COARSE_GALERKIN: {
       // on a decomposed context: the coarse window of the level-0 block (contains the owned
@@ -506,7 +507,7 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y) {
       else launch_k(C, k_apply_red_glk<2, 0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       return post_launch(C);
     case HELM_COARSE_RED_O2:
-      return op_apply(C, 1, x, f, y, 1.0, 0.0);
+      return op_apply(C, 1, x, f, y, 1.0, 0.0, true);
     case HELM_COARSE_RED_O4:
       if (res) launch_k(C, k_apply_red_o4<1>, gg, blk2d(), 0, G.g, x, f, y, G.k);
       else launch_k(C, k_apply_red_o4<0>, gg, blk2d(), 0, G.g, x, f, y, G.k);
@@ -582,6 +583,12 @@ int col_up(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2*
 }
 
 // u_out = V-cycle approximation of M_l^{-1} f (+ addq), starting at level l.
+// Decomposed contexts -- fresh ghosts: the legs compute every row of a block, so an output is
+// exact wherever its inputs are; with f's halo refreshed (GHOST = 6 rows) and the coarse
+// correction exact on its owned rows +- 4 (induction; replicated levels are exact everywhere),
+// the up leg's output is exact on the owned rows +- 4 (+5 minus the block's edge row, whose
+// boundary treatment is artificial).  So a V-cycle output needs no halo before a consumer that
+// reads <= 3 rows away: the up leg's coarse correction, E (apply_E fresh), A (op_apply fresh).
 int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   const int last = (int)C.L.size() - 1;
   Level& L = C.L[l];
@@ -607,7 +614,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
     CKR(col_down(C, L, G, f, sr, si, w));
     if (gather) CKR(allgather(C, l + 1));
     CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
-    CKR(halo(C, l + 1, DVec(Gs.u)));
+    // no halo for Gs.u: a V-cycle output is valid on its owned rows +- 4 (fresh ghosts, below)
     return col_up(C, L, G, f, addq, u_out, sr, si, w);
   }
   if (fused_vcycle(C)) {
@@ -627,7 +634,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
     CKR(post_launch(C));
     if (gather) CKR(allgather(C, l + 1));
     CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
-    CKR(halo(C, l + 1, DVec(Gs.u)));
+    // no halo for Gs.u: a V-cycle output is valid on its owned rows +- 4 (fresh ghosts, below)
     if (small) {
       dim3 gu((L.g.nx + 15) / 16, (L.g.ny + 7) / 8);
       launch_k(C, k_vc_up<16, 8>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
@@ -653,7 +660,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   CKR(restrict_(C, l, ob, G.f));
   if (gather) CKR(allgather(C, l + 1));
   CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
-  CKR(halo(C, l + 1, DVec(Gs.u)));
+  // no halo for Gs.u (fresh ghosts, see vcycle's header)
   const int np = C.p.nu_post;
   if (np == 0) return prolong_(C, l, G.u, cur, u_out, addq);
   CKR(prolong_(C, l, G.u, cur, DVec(ob), nullptr));
@@ -942,7 +949,8 @@ int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_st
   Fgm& K = C.inner;
   launch_k(C, k_fgm_reset, 1, 1, 0, K.st, C.p.inner_tol, C.p.inner_maxit, K.m);
   CKR(post_launch(C));
-  auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y); };
+  // x is z_j (a V-cycle output, fresh ghosts) in the Arnoldi step; restarts do not occur here
+  auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y, f.p == nullptr); };
   auto opP = [&](DVec v, DVec z) { return vcycle(C, 1, v, z, nullptr); };
   return fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C));
 }
@@ -993,7 +1001,7 @@ int adef1(helm_ctx_s& C, DVec v, DVec z, FgmState* outer_stats) {
   CKR(defl_restrict(C, v, C.cc));                              // v1 = I_h^{2h} v
   CKR(coarse_solve(C, C.cc, C.ce, outer_stats));               // v2 = A_{2h}^{-1} v1
   CKR(defl_prolong(C, C.ce, C.dq));                            // v' = I_{2h}^h v2  (= Q v)
-  CKR(op_apply(C, 0, DVec(C.dq), v, DVec(C.dt), 1.0, 0.0));    // t = v - A Q v  (= P_h v)
+  CKR(op_apply(C, 0, DVec(C.dq), v, DVec(C.dt), 1.0, 0.0, true));   // t = v - A Q v (= P_h v); q = Z e is fresh
   return vcycle(C, 0, DVec(C.dt), z, C.dq);                    // z = M^{-1} t + Q v
 }
 
@@ -1062,7 +1070,8 @@ int gcr_cycle(helm_ctx_s& C, bool first) {
 int outer_cycle(helm_ctx_s& C, bool first) {
   if (C.p.outer == HELM_OUTER_GCR) return gcr_cycle(C, first);
   Level& F = C.L[0];
-  auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, 0, x, f, y, 1.0, 0.0); };
+  // Arnoldi step: x = z_j, the preconditioner's (V-cycle) output, fresh; restart (f set): x = x_m
+  auto opA = [&](DVec x, DVec f, DVec y) { return op_apply(C, 0, x, f, y, 1.0, 0.0, f.p == nullptr); };
   auto opP = [&](DVec v, DVec z) { return precond(C, v, z, C.outer.st); };
   return fgmres_cycle(C, C.outer, opA, opP, DVec(C.bbuf), C.xbuf, first, nullptr);
 }
