@@ -121,6 +121,8 @@ typedef struct {
                           and Tables 1-2: coarse matrix Z^T Z M_2h^-1 A_2h solved by unpreconditioned
                           FGMRES; two fine V-cycles per application; single-GPU contexts only) */
   double gamma;        /* TLKM shift (1) */
+  int tail_cluster;    /* CTAs of the tail kernel (tail_max_n > 0): 0 = 16, else 8 (default); 1, 2,
+                          4, 8 or 16 = exactly that many (1: one CTA, no cluster) */
 } helm_params;
 
 typedef struct {

@@ -1129,6 +1129,7 @@ void helm_default_params(helm_params* p) {
   p->fuse_dots = 0;
   p->precond = HELM_PRECOND_ADEF1;
   p->gamma = 1.0;
+  p->tail_cluster = 0;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1320,7 +1321,10 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
       CKR(raise_dyn_smem((const void*)k_vc_tail, TAIL_SMEM_MAX));
       CK(cudaFuncSetAttribute((const void*)k_vc_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       C.tail_cs = 1;
-      for (int cs : {16, 8}) {
+      std::vector<int> sizes = {16, 8};
+      if (p.tail_cluster > 0) sizes.assign(1, p.tail_cluster);
+      for (int cs : sizes) {
+        if (cs == 1) break;   // C.tail_cs = 1: one CTA (no cluster launch needed)
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cs);
         cfg.blockDim = dim3(1024);

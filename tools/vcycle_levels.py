@@ -8,7 +8,9 @@ from paper_2308_06152_b200 import helm  # noqa: E402
 from workloads import config_problem  # noqa: E402
 
 p = config_problem("c1_k400")
-for extra in ({}, {"tail_max_n": 512}, {"tail_max_n": 2048}, {"tail_max_n": 8192}, {"tail_max_n": 32768}):
+for extra in ({}, {"coarsest_n": 128}, {"coarsest_n": 128, "tail_max_n": 2048, "tail_cluster": 1},
+              {"coarsest_n": 128, "tail_max_n": 512, "tail_cluster": 1}, {"coarsest_n": 128, "tail_max_n": 8192, "tail_cluster": 1},
+              {"coarsest_n": 128, "tail_max_n": 2048, "tail_cluster": 4}, {"coarsest_n": 32, "tail_max_n": 2048, "tail_cluster": 1}):
     prm = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": 50, "coarsest_n": 512}
     prm.update(extra)
     H = helm.helm_setup(p, prm)
