@@ -253,7 +253,30 @@ def microbench(peaks, n=16385, reps=10):
     return out
 
 
+class _StdoutToStderr:
+    """Route fd 1 to stderr while libraries (NCCL prints a version banner on stdout) run, so that
+    rank 0's stdout carries exactly the one JSON line of the contract."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def run_decomposed(args, rank, world, local):
+    with _StdoutToStderr():
+        line = _run_decomposed(args, rank, world, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def _run_decomposed(args, rank, world, local):
     """Weak scaling of ONE solve over the ranks: the workload's unit square
     stacked `world` times in y (strip_problem: same h and k, point source at the centre), one
     row strip per GPU; halos by grouped ncclSend/ncclRecv, dots by ncclAllReduce, the coarse
@@ -334,7 +357,7 @@ def run_decomposed(args, rank, world, local):
             roof, roof_all = kernel_roofline(Hs, reps[-1], peaks)
             Hs.close()
     if rank != 0:
-        return
+        return None
     line = {
         "metric": "fgmres_outer_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
@@ -355,7 +378,7 @@ def run_decomposed(args, rank, world, local):
         "roofline_kernels": roof_all,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def main():
@@ -383,7 +406,8 @@ def main():
         return run_reference(args, rank, world)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        with _StdoutToStderr():
+            dist.init_process_group("nccl")
     if args.decomp == "on" or (args.decomp == "auto" and world > 1):
         return run_decomposed(args, rank, world, local)
     import numpy as np

@@ -16,7 +16,9 @@ def test_bench_line(lib, extra):
                           "--workload", "c1_k100", "--no-micro", "--no-cpu-baseline", *extra],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
-    line = json.loads(out.stdout.strip().splitlines()[-1])
+    lines = [s for s in out.stdout.splitlines() if s.strip()]
+    assert len(lines) == 1, lines[:3]          # exactly one JSON line on stdout (library banners go to stderr)
+    line = json.loads(lines[0])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
                 "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches"):
         assert key in line, key
