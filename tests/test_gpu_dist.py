@@ -80,8 +80,9 @@ GRIDS = [
     (Prob(47, 127, 1 / 128, "dirichlet", random_k((127, 47), 1, 10, 60)), 4),       # ragged, 4 ranks
     (Prob(65, 129, 1 / 128, "sommerfeld", random_k((129, 65), 2, 5, 40)), 3),
     (Prob(33, 65, 1 / 64, "sommerfeld", random_k((65, 33), 3, 5, 30)), 1),          # one rank, all levels blocks
+    (Prob(65, 257, 1 / 256, "sommerfeld", random_k((257, 65), 4, 10, 90)), 5),     # odd rank count, ragged rows
 ]
-GIDS = ["dir63-P2", "dir47x127-P4", "som65x129-P3", "som33x65-P1"]
+GIDS = ["dir63-P2", "dir47x127-P4", "som65x129-P3", "som33x65-P1", "som65x257-P5"]
 SMALL = {"dist_min_rows": 6}
 
 
