@@ -23,6 +23,12 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef HELM_DU_THREADS
+#define HELM_DU_THREADS 256
+#endif
+#ifndef HELM_DU_ELEMS
+#define HELM_DU_ELEMS 128
+#endif
 namespace helm {
 
 constexpr int GS_NV = 8;         // basis vectors per sweep of a chunk in the dot pass
@@ -83,7 +89,7 @@ inline GsGeom gs_geom(long long n, int sms) {
   g.gx = (int)((n + g.chunk - 1) / g.chunk);
   const int target = 8 * sms;
   g.gy = std::max(1, std::min(16, target / std::max(1, g.gx)));
-  const long long tiles = (n + 127) / 128;   // DU_ELEMS
+  const long long tiles = (n + HELM_DU_ELEMS - 1) / HELM_DU_ELEMS;   // DU_ELEMS
   g.gu = (int)std::max<long long>(1, std::min<long long>(tiles, (long long)8 * sms));
   return g;
 }
@@ -384,9 +390,9 @@ __global__ void __launch_bounds__(DC_THREADS, HELM_DC_MINB) k_dcgs_dots(const do
 // 4 warps owns 256 elements (8 per lane, accumulators in registers); the warps split the basis
 // (warp q takes c = q, q+4, ...) streaming two vectors at a time (16 loads in flight per lane)
 // and their sums are combined in a fixed order through shared memory.
-constexpr int DU_THREADS = 256;   // standalone update: 8 warps, 128-element tiles (4 per lane)
+constexpr int DU_THREADS = HELM_DU_THREADS;   // standalone update: 8 warps, 128-element tiles (4 per lane)
 constexpr int DU_WARPS = DU_THREADS / 32;
-constexpr int DU_ELEMS = 128;
+constexpr int DU_ELEMS = HELM_DU_ELEMS;
 
 template <int NW, int EPL>
 struct DuRed {
