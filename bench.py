@@ -292,7 +292,15 @@ def _run_decomposed(args, rank, world, local):
     peaks = load_peaks()
     base = config_problem(args.workload)
     p = strip_problem(base.meta["k"], base.meta["n_cells"], world, f"{args.workload}_x{world}")
-    if world > 1:
+    uid = peer_exchange = None
+    if args.transport == "peer":        # NVLink peer memory through CUDA IPC (peer.cuh), no NCCL
+        def peer_exchange(handle):
+            if world == 1:
+                return [handle]
+            out = [None] * world
+            dist.all_gather_object(out, handle)
+            return out
+    elif world > 1:
         obj = [helm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
@@ -303,7 +311,8 @@ def _run_decomposed(args, rank, world, local):
         # levels 0-2 decomposed, level 3 (79 x (80 N - 1) unknowns) and below replicated: 7 small
         # collectives per inner iteration instead of ~11 with the deepest possible split
         prm = dict(method_of(args), dist_levels=args.dist_levels or 3)
-        H = helm.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, rank, world, nccl_id=uid, params=prm, stream=stream)
+        H = helm.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, rank, world, nccl_id=uid, params=prm, stream=stream,
+                          peer_exchange=peer_exchange)
         bo = np.ascontiguousarray(p.b[H.row0:H.row0 + H.nrows])
         b = torch.from_numpy(bo).cuda()
         x = torch.empty_like(b)
@@ -367,7 +376,7 @@ def _run_decomposed(args, rank, world, local):
                    "h": p.h, "k": p.meta["k"], "tol": 1e-6, "l2": "flushed between timed steps (256 MiB read)",
                    "outer_iterations": reps[-1]["outer_iterations"],
                    "inner_iterations_mean": reps[-1]["inner_iterations_total"] / max(1, reps[-1]["inner_solves"]),
-                   "parallelism": f"row-strip decomposition x{world} (NCCL halos + allreduce)",
+                   "parallelism": f"row-strip decomposition x{world} ({args.transport} transport)",
                    "dist_levels": prm["dist_levels"],
                    "value_definition": "world x outer iterations / max-over-ranks device time"},
         "wall_s": wall,
@@ -398,6 +407,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
     ap.add_argument("--dist-levels", type=int, default=0, help="decomposed levels (0: 3)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="decomposed solve: NCCL collectives or NVLink peer memory (CUDA IPC)")
     ap.add_argument("--decomp", default="auto", choices=["auto", "on", "off"],
                     help="row-strip decomposed solve over the ranks (NCCL); auto = on when N > 1")
     args = ap.parse_args()

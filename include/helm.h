@@ -240,6 +240,14 @@ int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_
  *                    buffers ordered by CUDA events and host barriers: no kernel waits on
  *                    another rank, so this is safe on a single GPU.  It exercises the whole
  *                    decomposed path on one B200 (parity tests).
+ *  HELM_COMM_PEER    one process per GPU of one NVLink/NVSwitch node, no NCCL: every rank's
+ *                    exchange arena (halo rows, rank-sum and all-gather slots, epoch flags) is
+ *                    mapped into its peers through CUDA IPC (helm_peer_handle on every rank,
+ *                    gather the 64-byte handles, helm_peer_connect); an exchange is a producer
+ *                    kernel that writes its slot and publishes an epoch flag and a consumer kernel
+ *                    that waits for the peers' flags and reads their slots directly over NVLink
+ *                    (peer.cuh).  Needs one GPU per rank (its kernels wait on other ranks');
+ *                    waits give up after ~10 s and the solve returns HELM_ECUDA.
  * On a decomposed context helm_apply_A, helm_vcycle (level 0), helm_deflate, helm_solve and
  * helm_solve_host take and return THIS RANK'S OWNED ROWS of level 0 (nrows * nx values,
  * contiguous); the other per-level entry points and the benchmarks return HELM_EINVAL.
@@ -248,6 +256,7 @@ int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_
  * --------------------------------------------------------------------------------------- */
 #define HELM_COMM_THREADS 0
 #define HELM_COMM_NCCL 1
+#define HELM_COMM_PEER 2
 typedef struct helm_group_s* helm_group;
 int helm_group_create(int nranks, helm_group* out);
 void helm_group_destroy(helm_group g);
@@ -264,6 +273,17 @@ typedef struct {
  * dist->rank of a decomposed solve.  Collective: every rank must call it. */
 int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k_on_device,
                     const helm_params* params, void* stream, const helm_dist* dist);
+/* Peer transport: this rank's 64-byte CUDA IPC handle of its exchange arena; then, with the
+ * handles of all ranks (nranks * 64 bytes, rank order), map the peers' arenas.  Both collective
+ * in the sense that every rank must call them before its first exchange.  helm_peer_error: 1 if
+ * a peer wait timed out. */
+int helm_peer_handle(helm_ctx ctx, unsigned char out[64]);
+int helm_peer_connect(helm_ctx ctx, const unsigned char* handles);
+int helm_peer_error(helm_ctx ctx);
+/* Host-only: the peer arena layout (bytes, flags, rank-sum slot, all-gather slot and its length,
+ * then per decomposed level the up / down halo slots) -- identical on every rank by construction;
+ * returns the number of entries (or a negative error). */
+int helm_peer_layout(const helm_grid* grid, const helm_params* params, int nranks, size_t* out, int cap);
 /* Global rows [*row0, *row0 + *nrows) of `level` owned by this rank (single-GPU context: all). */
 int helm_dist_rows(helm_ctx ctx, int level, int* row0, int* nrows);
 /* Host-only plan of the decomposition (no device needed): returns the number of levels L

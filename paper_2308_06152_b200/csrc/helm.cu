@@ -21,6 +21,7 @@
 #include "kernels.cuh"
 #include "dist.cuh"
 #include "krylov.cuh"
+#include "peer.cuh"
 #include "vcycle.cuh"
 
 using namespace helm;
@@ -144,6 +145,13 @@ struct helm_ctx_s {
   cudaEvent_t dev_ev = nullptr;
   double2* red = nullptr;              // allreduce staging (thread groups)
   size_t red_cap = 0;
+  // peer-memory transport (HELM_COMM_PEER, peer.cuh)
+  char* arena = nullptr;
+  PeerLayout playout;
+  PeerSet peers{};
+  bool peer_connected = false;
+  unsigned long long ep_halo = 0, ep_red = 0, ep_gat = 0;
+  unsigned* pcnt = nullptr;            // ticket counters: halo put/get, gather put/get
 };
 
 namespace {
@@ -286,6 +294,15 @@ int allreduce(helm_ctx_s& C, double2* buf, int n) {
     NCK(C.api->AllReduce(buf, buf, 2 * (size_t)n, ncclFloat64, ncclSum, C.nccl, C.s));
     return HELM_OK;
   }
+  if (C.kind == HELM_COMM_PEER) {
+    if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
+    if ((size_t)n > PEER_RED_CAP) return fail(HELM_EINVAL, "rank sum of %d values exceeds the peer slot", n);
+    const unsigned long long e = ++C.ep_red;
+    launch_k(C, k_peer_red_put, 1, 256, 0, (const double2*)buf, n, C.peers, C.rank, C.nranks, C.playout.red, e);
+    CKR(post_launch(C));
+    launch_k(C, k_peer_red_sum, 1, 256, 0, buf, n, C.peers, C.rank, C.nranks, C.playout.red, e);
+    return post_launch(C);
+  }
   if ((size_t)n > C.red_cap) return fail(HELM_EINVAL, "allreduce of %d values exceeds the staging buffer", n);
   CK(cudaMemcpyAsync(C.red, buf, (size_t)n * sizeof(double2), cudaMemcpyDeviceToDevice, C.s));
   CKR(dist_sync(C));
@@ -305,6 +322,17 @@ int halo(helm_ctx_s& C, int l, DVec x) {
   const int up = C.rank > 0, dn = C.rank < C.nranks - 1;
   const int n = GHOST * nx;
   const int grid = std::max(1, std::min((n + 255) / 256, C.sm_count * 4));
+  if (C.kind == HELM_COMM_PEER) {
+    if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
+    const unsigned long long e = ++C.ep_halo;
+    const int pg = std::min(grid, C.sm_count);
+    launch_k(C, k_peer_halo_put, pg, 256, 0, x, nx, L.own0, L.nown, up, dn, C.peers, C.rank, C.playout.up[l],
+             C.playout.dn[l], e, C.pcnt);
+    CKR(post_launch(C));
+    launch_k(C, k_peer_halo_get, pg, 256, 0, x, nx, L.own0, L.nown, up, dn, C.peers, C.rank, C.playout.up[l],
+             C.playout.dn[l], e, C.pcnt + 1);
+    return post_launch(C);
+  }
   launch_k(C, k_halo_pack, grid, 256, 0, x, nx, L.own0, L.nown, up, dn, L.hs_up, L.hs_dn);
   CKR(post_launch(C));
   const double2* src_up = nullptr;
@@ -339,6 +367,22 @@ int allgather(helm_ctx_s& C, int l) {
   if (!C.dist || C.nranks == 1) return HELM_OK;
   Level& L = C.L[l];
   const size_t nx = (size_t)L.g.nx;
+  if (C.kind == HELM_COMM_PEER) {
+    if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
+    PeerRows rows{};
+    for (int q = 0; q < C.nranks; ++q) {
+      rows.a[q] = prow(C, l, q).a;
+      rows.b[q] = prow(C, l, q).b;
+    }
+    const unsigned long long e = ++C.ep_gat;
+    const int pg = std::max(1, std::min(grid1d(C, L.n), C.sm_count));
+    launch_k(C, k_peer_gat_put, pg, 256, 0, (const double2*)L.f, (int)nx, rows, C.peers, C.rank, C.nranks,
+             C.playout.gat, e, C.pcnt + 2);
+    CKR(post_launch(C));
+    launch_k(C, k_peer_gat_get, pg, 256, 0, L.f, (int)nx, rows, C.peers, C.rank, C.nranks, C.playout.gat, e,
+             C.pcnt + 3);
+    return post_launch(C);
+  }
   if (C.kind == HELM_COMM_NCCL) {
     NCK(C.api->GroupStart());
     for (int q = 0; q < C.nranks; ++q) {
@@ -1152,6 +1196,12 @@ static void destroy_ctx(helm_ctx_s* C) {
     cudaFree(L.hr_dn);
   }
   cudaFree(C->red);
+  if (C->arena) {
+    for (int q = 0; q < C->nranks; ++q)
+      if (q != C->rank && C->peers.a[q]) cudaIpcCloseMemHandle(C->peers.a[q]);
+    cudaFree(C->arena);
+  }
+  cudaFree(C->pcnt);
   if (C->dev_ev) cudaEventDestroy(C->dev_ev);
   if (C->nccl && C->api) C->api->CommDestroy(C->nccl);
   cudaFree(C->dlev);
@@ -1639,6 +1689,7 @@ int helm_solve(helm_ctx C, const double* b, double* x, double tol, int maxit, he
   C->s = C->own;
   int r = solve_device(*C, tol, maxit, rep);
   C->s = user;
+  if (r == HELM_OK && helm_peer_error(C)) r = fail(HELM_ECUDA, "peer exchange timed out (a peer rank stalled)");
   if (r == HELM_OK) {
     CK(cudaEventRecord(ev, C->own));
     CK(cudaStreamWaitEvent(user, ev, 0));
@@ -1927,6 +1978,18 @@ int helm_nccl_unique_id(unsigned char id[128]) {
 // per-rank registration of the buffers its peers read (thread groups) + the staging slot
 static int dist_register(helm_ctx_s& C) {
   CK(cudaEventCreateWithFlags(&C.dev_ev, cudaEventDisableTiming));
+  if (C.kind == HELM_COMM_PEER) {
+    std::vector<int> nx;
+    for (const auto& Lv : C.L) nx.push_back(Lv.g.nx);
+    C.playout = peer_layout(nx, C.D, C.plan, C.nranks);
+    CK(cudaMalloc((void**)&C.arena, C.playout.bytes));
+    CK(cudaMemsetAsync(C.arena, 0, C.playout.bytes, C.s));
+    CKR(dalloc(&C.pcnt, 4));
+    CK(cudaMemsetAsync(C.pcnt, 0, 4 * sizeof(unsigned), C.s));
+    C.peers.a[C.rank] = C.arena;
+    CK(cudaStreamSynchronize(C.s));
+    return HELM_OK;
+  }
   if (C.kind != HELM_COMM_THREADS) return HELM_OK;
   C.red_cap = 2 * 4096 + 8;   // 2m + 2 values for the largest outer basis (ensure_outer caps m at 4096)
   CKR(dalloc(&C.red, C.red_cap));
@@ -1955,6 +2018,8 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
     if (!d->group || d->group->n != d->nranks) return fail(HELM_EINVAL, "thread group of the wrong size");
   } else if (d->kind == HELM_COMM_NCCL) {
     if (!d->nccl_id) return fail(HELM_EINVAL, "NCCL transport needs nccl_id");
+  } else if (d->kind == HELM_COMM_PEER) {
+    // connected later (helm_peer_handle / helm_peer_connect)
   } else {
     return fail(HELM_EINVAL, "bad transport %d", d->kind);
   }
@@ -1990,6 +2055,7 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   }
   if (r == HELM_OK) r = setup_impl(*C, grid, k, k_on_device);
   if (r == HELM_OK) r = dist_register(*C);
+  if (r == HELM_OK && d->kind == HELM_COMM_PEER && d->nranks == 1) C->peer_connected = true;
   if (d->kind == HELM_COMM_THREADS) {
     // all ranks agree on success before anyone exchanges with a peer
     C->grp->status[d->rank] = r;
@@ -2006,12 +2072,72 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   return HELM_OK;
 }
 
+int helm_peer_handle(helm_ctx C, unsigned char out[64]) {
+  if (!C || !out || C->kind != HELM_COMM_PEER || !C->arena) return fail(HELM_EINVAL, "not a peer-transport context");
+  cudaIpcMemHandle_t hdl;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  CK(cudaIpcGetMemHandle(&hdl, C->arena));
+  memcpy(out, &hdl, 64);
+  return HELM_OK;
+}
+
+int helm_peer_connect(helm_ctx C, const unsigned char* handles) {
+  if (!C || !handles || C->kind != HELM_COMM_PEER) return fail(HELM_EINVAL, "not a peer-transport context");
+  for (int q = 0; q < C->nranks; ++q) {
+    if (q == C->rank) continue;
+    cudaIpcMemHandle_t hdl;
+    memcpy(&hdl, handles + (size_t)q * 64, 64);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, hdl, cudaIpcMemLazyEnablePeerAccess));
+    C->peers.a[q] = static_cast<char*>(p);
+  }
+  C->peer_connected = true;
+  return HELM_OK;
+}
+
+int helm_peer_error(helm_ctx C) {
+  if (!C || C->kind != HELM_COMM_PEER || !C->arena) return 0;
+  unsigned long long e = 0;
+  if (cudaMemcpy(&e, C->arena + (size_t)PF_ERROR * PF_STRIDE * sizeof(unsigned long long), sizeof e,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 1;
+  return e ? 1 : 0;
+}
+
 int helm_dist_rows(helm_ctx C, int level, int* row0, int* nrows) {
   if (!C || level < 0 || level >= (int)C->L.size()) return fail(HELM_EINVAL, "bad level");
   const Level& L = C->L[level];
   if (row0) *row0 = L.row0 + L.own0;
   if (nrows) *nrows = L.nown;
   return HELM_OK;
+}
+
+int helm_peer_layout(const helm_grid* grid, const helm_params* params, int nranks, size_t* out, int cap) {
+  if (!grid || !out || nranks < 1) return fail(HELM_EINVAL, "bad argument");
+  helm_params p;
+  if (params) p = *params;
+  else helm_default_params(&p);
+  if (p.dist_min_rows <= 0) p.dist_min_rows = 16;
+  std::vector<std::pair<int, int>> sz;
+  hierarchy_sizes(*grid, p, sz);
+  std::vector<int> nys, nxs;
+  for (const auto& s : sz) {
+    nxs.push_back(s.first);
+    nys.push_back(s.second);
+  }
+  std::vector<DistRows> plan;
+  std::string why;
+  const int d = dist_plan(nys, grid->bc == HELM_BC_DIRICHLET, nranks, p.dist_min_rows, p.dist_levels, plan, why);
+  if (d < 0) return fail(HELM_ESHAPE, "decomposition: %s", why.c_str());
+  const PeerLayout L = peer_layout(nxs, d, plan, nranks);
+  std::vector<size_t> v = {L.bytes, L.flags, L.red, L.gat, L.gat_n};
+  for (int l = 0; l <= d; ++l) {
+    v.push_back(L.up[l]);
+    v.push_back(L.dn[l]);
+  }
+  const int n = std::min<int>((int)v.size(), cap);
+  for (int i = 0; i < n; ++i) out[i] = v[i];
+  return (int)v.size();
 }
 
 int helm_dist_plan(const helm_grid* grid, const helm_params* params, int nranks, int* D, int* table, int cap_levels) {

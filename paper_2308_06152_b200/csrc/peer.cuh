@@ -1,0 +1,224 @@
+// Peer-memory transport for the row-strip decomposition (HELM_COMM_PEER): one
+// process per GPU of one NVLink/NVSwitch node.  Every rank owns an "arena" (one cudaMalloc'd
+// allocation, mapped into every peer through CUDA IPC) holding its outgoing halo rows, its
+// rank-sum slot, its all-gather slot and its flags.  An exchange is two kernels with no host in
+// the loop and no NCCL: the producer kernel writes its slot and then publishes an epoch flag
+// (release, system scope); the consumer kernel waits for the peers' flags (acquire), reads
+// their slots directly over NVLink and publishes an acknowledgement, which the next producer
+// of the same slot waits for (no slot is overwritten before every reader is done).  Epochs
+// are host counters: every rank issues the same exchanges in the same order.
+//
+// Kernels of different ranks wait on each other here, so this transport needs one GPU per rank
+// (never several ranks on one GPU).  Waits give up after ~10 s of GPU clock and raise an error
+// flag the host checks after each solve, so a broken peer cannot hang the job forever.
+#pragma once
+#include <cuda/atomic>
+
+#include "dist.cuh"
+#include "kernels.cuh"
+
+namespace helm {
+
+enum PeerFlag { PF_HALO_READY = 0, PF_HALO_ACK, PF_RED_READY, PF_RED_ACK, PF_GAT_READY, PF_GAT_ACK, PF_ERROR, PF_COUNT };
+constexpr int PF_STRIDE = 16;                       // one 128-byte line per flag
+constexpr size_t PEER_RED_CAP = 2 * 4096 + 8;      // rank-sum slot (complex values)
+constexpr long long PEER_TIMEOUT_CYCLES = 20000000000LL;   // ~10 s at 2 GHz
+
+// Byte offsets inside an arena (identical on every rank: computed from the global plan).
+struct PeerLayout {
+  size_t flags = 0;                 // PF_COUNT * PF_STRIDE uint64
+  std::vector<size_t> up, dn;       // per level: outgoing GHOST rows (to rank - 1 / rank + 1)
+  size_t red = 0;                   // PEER_RED_CAP complex
+  size_t gat = 0, gat_n = 0;        // all-gather slot (complex values)
+  size_t bytes = 0;
+};
+
+inline PeerLayout peer_layout(const std::vector<int>& nx, int D, const std::vector<DistRows>& plan, int P) {
+  PeerLayout L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += (bytes + 255) / 256 * 256;
+    return at;
+  };
+  L.flags = take(PF_COUNT * PF_STRIDE * sizeof(unsigned long long));
+  L.up.assign(nx.size(), 0);
+  L.dn.assign(nx.size(), 0);
+  for (int l = 0; l <= D; ++l) {
+    L.up[l] = take((size_t)GHOST * nx[l] * sizeof(double2));
+    L.dn[l] = take((size_t)GHOST * nx[l] * sizeof(double2));
+  }
+  L.red = take(PEER_RED_CAP * sizeof(double2));
+  size_t rows = 0;
+  for (int q = 0; q < P; ++q) {
+    const DistRows& r = plan[(size_t)(D + 1) * P + q];
+    rows = std::max<size_t>(rows, (size_t)(r.b - r.a));
+  }
+  L.gat_n = rows * nx[D + 1];
+  L.gat = take(L.gat_n * sizeof(double2));
+  L.bytes = o;
+  return L;
+}
+
+__device__ __forceinline__ unsigned long long* pflag(char* arena, int f) {
+  return reinterpret_cast<unsigned long long*>(arena) + (size_t)f * PF_STRIDE;
+}
+
+// (every thread of the block has executed __threadfence_system() after its slot writes and the
+// block has synchronised before thread 0 publishes)
+__device__ __forceinline__ void peer_publish(char* arena, int f, unsigned long long e) {
+  __threadfence_system();
+  cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> a(*pflag(arena, f));
+  a.store(e, cuda::memory_order_release);
+}
+
+// thread 0 of the calling block waits until the peer's flag reaches e (acquire); on timeout
+// the local error flag is raised and the wait abandoned
+__device__ __forceinline__ void peer_wait(char* peer, int f, unsigned long long e, char* me) {
+  if (e == 0) return;
+  cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> a(*pflag(peer, f));
+  const long long t0 = clock64();
+  while (a.load(cuda::memory_order_acquire) < e) {
+    if (clock64() - t0 > PEER_TIMEOUT_CYCLES) {
+      cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> err(*pflag(me, PF_ERROR));
+      err.store(1ull, cuda::memory_order_relaxed);
+      return;
+    }
+    __nanosleep(64);
+  }
+  __threadfence_system();
+}
+
+struct PeerSet {
+  char* a[DIST_MAX_RANKS];   // every rank's arena, mapped into this process (own arena included)
+};
+
+// last CTA to arrive (ticket in `counter`, reset by the last one); every thread's prior writes
+// are made visible system-wide first (the peers read them over NVLink)
+__device__ __forceinline__ bool peer_last_block(unsigned* counter) {
+  __shared__ bool last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last && threadIdx.x == 0) *counter = 0u;
+  return last;
+}
+
+// ---- halo: (1) pack my boundary rows into my arena, publish HALO_READY = e
+__global__ void k_peer_halo_put(DVec xv, int nx, int own0, int nown, int up, int dn, PeerSet ps, int me, size_t off_up,
+                                size_t off_dn, unsigned long long e, unsigned* counter) {
+  HELM_PDL_ENTRY();
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0) {   // the readers of my previous slots are done (acknowledged epoch e - 1)
+    if (up) peer_wait(ps.a[me - 1], PF_HALO_ACK, e - 1, mine);
+    if (dn) peer_wait(ps.a[me + 1], PF_HALO_ACK, e - 1, mine);
+  }
+  __syncthreads();
+  const double2* x = xv.get();
+  double2* sup = reinterpret_cast<double2*>(mine + off_up);
+  double2* sdn = reinterpret_cast<double2*>(mine + off_dn);
+  const int n = GHOST * nx;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    if (up) sup[t] = x[(size_t)own0 * nx + t];
+    if (dn) sdn[t] = x[(size_t)(own0 + nown - GHOST) * nx + t];
+  }
+  if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_HALO_READY, e);
+}
+
+// ---- halo: (2) wait for the neighbours' rows of epoch e, copy them into my ghost rows, ack
+__global__ void k_peer_halo_get(DVec xv, int nx, int own0, int nown, int up, int dn, PeerSet ps, int me, size_t off_up,
+                                size_t off_dn, unsigned long long e, unsigned* counter) {
+  HELM_PDL_ENTRY();
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0) {
+    if (up) peer_wait(ps.a[me - 1], PF_HALO_READY, e, mine);
+    if (dn) peer_wait(ps.a[me + 1], PF_HALO_READY, e, mine);
+  }
+  __syncthreads();
+  double2* x = xv.get();
+  // rank - 1 wrote its bottom rows into its "dn" slot, rank + 1 its top rows into its "up" slot
+  const double2* rup = up ? reinterpret_cast<const double2*>(ps.a[me - 1] + off_dn) : nullptr;
+  const double2* rdn = dn ? reinterpret_cast<const double2*>(ps.a[me + 1] + off_up) : nullptr;
+  const int n = GHOST * nx;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    if (up) x[(size_t)(own0 - GHOST) * nx + t] = rup[t];
+    if (dn) x[(size_t)(own0 + nown) * nx + t] = rdn[t];
+  }
+  if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_HALO_ACK, e);
+}
+
+// ---- rank sum of n values (one block each): put my values, then sum every rank's in rank order
+__global__ void k_peer_red_put(const double2* __restrict__ buf, int n, PeerSet ps, int me, int P, size_t off_red,
+                               unsigned long long e) {
+  HELM_PDL_ENTRY();
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0)
+    for (int q = 0; q < P; ++q)
+      if (q != me) peer_wait(ps.a[q], PF_RED_ACK, e - 1, mine);
+  __syncthreads();
+  double2* slot = reinterpret_cast<double2*>(mine + off_red);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) slot[i] = buf[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) peer_publish(mine, PF_RED_READY, e);
+}
+
+__global__ void k_peer_red_sum(double2* __restrict__ buf, int n, PeerSet ps, int me, int P, size_t off_red,
+                               unsigned long long e) {
+  HELM_PDL_ENTRY();
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0)
+    for (int q = 0; q < P; ++q)
+      if (q != me) peer_wait(ps.a[q], PF_RED_READY, e, mine);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double2 s = reinterpret_cast<const double2*>(ps.a[0] + off_red)[i];
+    for (int q = 1; q < P; ++q) s = cadd(s, reinterpret_cast<const double2*>(ps.a[q] + off_red)[i]);
+    buf[i] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) peer_publish(mine, PF_RED_ACK, e);
+}
+
+struct PeerRows {
+  int a[DIST_MAX_RANKS], b[DIST_MAX_RANKS];   // owned rows of the all-gathered level, per rank
+};
+
+// ---- all-gather of a replicated level's f: put my owned rows, then fetch every peer's
+__global__ void k_peer_gat_put(const double2* __restrict__ f, int nx, PeerRows rows, PeerSet ps, int me, int P,
+                               size_t off_gat, unsigned long long e, unsigned* counter) {
+  HELM_PDL_ENTRY();
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0)
+    for (int q = 0; q < P; ++q)
+      if (q != me) peer_wait(ps.a[q], PF_GAT_ACK, e - 1, mine);
+  __syncthreads();
+  double2* slot = reinterpret_cast<double2*>(mine + off_gat);
+  const long long n = (long long)(rows.b[me] - rows.a[me]) * nx;
+  const double2* src = f + (size_t)rows.a[me] * nx;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    slot[t] = src[t];
+  if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_GAT_READY, e);
+}
+
+__global__ void k_peer_gat_get(double2* __restrict__ f, int nx, PeerRows rows, PeerSet ps, int me, int P,
+                               size_t off_gat, unsigned long long e, unsigned* counter) {
+  HELM_PDL_ENTRY();
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0)
+    for (int q = 0; q < P; ++q)
+      if (q != me) peer_wait(ps.a[q], PF_GAT_READY, e, mine);
+  __syncthreads();
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const double2* slot = reinterpret_cast<const double2*>(ps.a[q] + off_gat);
+    double2* dst = f + (size_t)rows.a[q] * nx;
+    const long long n = (long long)(rows.b[q] - rows.a[q]) * nx;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+      dst[t] = slot[t];
+  }
+  if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_GAT_ACK, e);
+}
+
+}  // namespace helm

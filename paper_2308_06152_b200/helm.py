@@ -46,6 +46,7 @@ class helm_dist(ctypes.Structure):
 
 HELM_COMM_THREADS = 0
 HELM_COMM_NCCL = 1
+HELM_COMM_PEER = 2
 
 
 class helm_report(ctypes.Structure):
@@ -88,6 +89,11 @@ EXPORTS = {
     "helm_setup_dist": (_I, [ctypes.POINTER(_P), ctypes.POINTER(helm_grid), _P, _I, ctypes.POINTER(helm_params), _P,
                              ctypes.POINTER(helm_dist)]),
     "helm_dist_rows": (_I, [_P, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "helm_peer_handle": (_I, [_P, ctypes.c_char_p]),
+    "helm_peer_connect": (_I, [_P, ctypes.c_char_p]),
+    "helm_peer_error": (_I, [_P]),
+    "helm_peer_layout": (_I, [ctypes.POINTER(helm_grid), ctypes.POINTER(helm_params), _I,
+                              ctypes.POINTER(ctypes.c_size_t), _I]),
     "helm_dist_plan": (_I, [ctypes.POINTER(helm_grid), ctypes.POINTER(helm_params), _I, ctypes.POINTER(_I),
                             ctypes.POINTER(_I), _I]),
     "helm_last_error": (ctypes.c_char_p, []),
@@ -317,6 +323,18 @@ def helm_setup(problem, params=None, stream=None) -> Helm:
 
 
 # ---------------------------------------------------------------------- decomposed solves
+def peer_layout(nx, ny, h, bc, nranks, params=None):
+    """Host-only peer-arena layout (helm_peer_layout): [bytes, flags, red, gat, gat_n, up0, dn0, ...]."""
+    lib = load_library()
+    p = params if isinstance(params, helm_params) else default_params(**(params or {}))
+    g = helm_grid(int(nx), int(ny), float(h), BCS[bc])
+    out = (ctypes.c_size_t * 256)()
+    n = lib.helm_peer_layout(ctypes.byref(g), ctypes.byref(p), int(nranks), out, 256)
+    if n < 0:
+        _check(n)
+    return [int(out[i]) for i in range(n)]
+
+
 def dist_plan(nx, ny, h, bc, nranks, params=None):
     """Host-only row-strip plan (helm_dist_plan): (D, table[l][q] = (a, b, s, e))."""
     lib = load_library()
@@ -361,7 +379,10 @@ class HelmDist(Helm):
     and returned by the entry points are this rank's owned rows, shape (nrows, nx)."""
 
     def __init__(self, nx, ny, h, bc, k, rank, nranks, group: ThreadGroup | None = None, nccl_id: bytes | None = None,
-                 params=None, stream=None):
+                 params=None, stream=None, peer_exchange=None):
+        """Transport: a ThreadGroup (ranks as threads on one GPU), an NCCL unique id, or
+        peer_exchange = callable(bytes) -> list of every rank's bytes (e.g. through
+        torch.distributed.all_gather_object) for the NVLink peer-memory transport."""
         import torch
         self.torch = torch
         lib = load_library()
@@ -378,7 +399,9 @@ class HelmDist(Helm):
         assert kt.shape == (self.ny, self.nx)
         g = helm_grid(self.nx, self.ny, self.h, BCS[bc])
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        d = helm_dist(HELM_COMM_NCCL if nccl_id is not None else HELM_COMM_THREADS, int(rank), int(nranks),
+        kind = HELM_COMM_NCCL if nccl_id is not None else (HELM_COMM_PEER if peer_exchange is not None else
+                                                           HELM_COMM_THREADS)
+        d = helm_dist(kind, int(rank), int(nranks),
                       group.handle if group is not None else None,
                       ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None)
         ctx = ctypes.c_void_p()
@@ -386,6 +409,12 @@ class HelmDist(Helm):
                                    ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(d)))
         self.ctx = ctx
         self.rank, self.nranks = int(rank), int(nranks)
+        if kind == HELM_COMM_PEER:
+            hbuf = ctypes.create_string_buffer(64)
+            _check(lib.helm_peer_handle(ctx, hbuf))
+            handles = peer_exchange(hbuf.raw)
+            assert len(handles) == self.nranks and all(len(x) == 64 for x in handles)
+            _check(lib.helm_peer_connect(ctx, b"".join(handles)))
         self.levels = [self.level_info(l) for l in range(lib.helm_num_levels(ctx))]
         self.row0, self.nrows = self.dist_rows(0)
 

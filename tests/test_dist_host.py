@@ -151,3 +151,50 @@ def test_gloo_world2_exchange_pattern():
             assert err < 1e-15, (r, bc, err)
             assert derr < 1e-13, (r, bc, derr)
             assert gerr == 0.0 and whole, (r, bc)
+
+
+def _layout_rank(rank, world, port, q):
+    import torch.distributed as dist
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        helm = _lib()
+        res = {}
+        for n, ny, bc, P in ((639, 1279, "dirichlet", 2), (2047, 8191, "dirichlet", 4), (257, 513, "sommerfeld", 3)):
+            lay = helm.peer_layout(n, ny, 1.0 / (n + 1), bc, P, {"dist_levels": 3})
+            allv = [None] * world
+            dist.all_gather_object(allv, lay)
+            # the IPC handle exchange of the peer transport: 64 opaque bytes per rank, rank order
+            h = bytes([rank]) * 64
+            hs = [None] * world
+            dist.all_gather_object(hs, h)
+            res[(n, ny, bc, P)] = (all(a == allv[0] for a in allv), lay,
+                                   [x == bytes([r]) * 64 for r, x in enumerate(hs)])
+        q.put((rank, res))
+        dist.destroy_process_group()
+    except BaseException as ex:   # noqa: BLE001
+        q.put((rank, repr(ex)))
+
+
+def test_gloo_world2_peer_layout_agrees():
+    """The peer transport addresses a peer's slots by offsets it computes itself: every rank
+    must derive the same arena layout from the global plan; the 64-byte IPC handles travel in
+    rank order.  Slots are disjoint, 256-byte aligned and inside the arena."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_layout_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(60)
+    for r in range(2):
+        assert isinstance(out[r], dict), out[r]
+        for key, (same, lay, handles_ok) in out[r].items():
+            assert same, key
+            assert all(handles_ok), key
+            total, offsets = lay[0], sorted(lay[1:4] + lay[5:])
+            assert all(o % 256 == 0 and o < total for o in offsets), key
+            assert len(set(offsets)) == len(offsets), key

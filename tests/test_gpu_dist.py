@@ -209,3 +209,22 @@ def test_dist_restarted_outer(lib):
     assert reps[0]["converged"] and reps[0]["restarts"] > 0
     x = assemble([(r0, nr, res[0]) for r0, nr, res in parts], p.ny, p.nx)
     assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
+
+
+def test_peer_transport_single_rank(lib):
+    """The NVLink peer-memory transport (HELM_COMM_PEER) with one rank: the arena is created,
+    exported and connected, every exchange runs its producer / consumer kernels and epoch flags
+    (no peer to wait for), and the solve matches the oracle like the other transports.  (With
+    several ranks its kernels wait on each other: one GPU per rank, never tested here.)"""
+    p = _problem("c1_k50")
+    prm = dict(coarse_op="galerkin", vectors="high_order", inner_tol=1e-1, inner_maxit=200)
+    H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=prm, peer_exchange=lambda h: [h])
+    x, rep = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
+    assert rep["converged"]
+    so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op="galerkin", vectors="high_order", inner_tol=1e-1,
+                                                           inner_maxit=200, maxit=200))
+    xo, ro = so.solve(p.b)
+    assert abs(rep["outer_iterations"] - ro["outer_iterations"]) <= 1
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    assert lib.load_library().helm_peer_error(H.ctx) == 0
+    H.close()
