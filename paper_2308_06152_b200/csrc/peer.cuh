@@ -142,8 +142,8 @@ __global__ void k_peer_halo_get(DVec xv, int nx, int own0, int nown, int up, int
   const double2* rdn = dn ? reinterpret_cast<const double2*>(ps.a[me + 1] + off_up) : nullptr;
   const int n = GHOST * nx;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    if (up) x[(size_t)(own0 - GHOST) * nx + t] = rup[t];
-    if (dn) x[(size_t)(own0 + nown) * nx + t] = rdn[t];
+    if (up) x[(size_t)(own0 - GHOST) * nx + t] = __ldcg(rup + t);   // L2 / NVLink, never a stale L1 line
+    if (dn) x[(size_t)(own0 + nown) * nx + t] = __ldcg(rdn + t);
   }
   if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_HALO_ACK, e);
 }
@@ -173,8 +173,8 @@ __global__ void k_peer_red_sum(double2* __restrict__ buf, int n, PeerSet ps, int
       if (q != me) peer_wait(ps.a[q], PF_RED_READY, e, mine);
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double2 s = reinterpret_cast<const double2*>(ps.a[0] + off_red)[i];
-    for (int q = 1; q < P; ++q) s = cadd(s, reinterpret_cast<const double2*>(ps.a[q] + off_red)[i]);
+    double2 s = __ldcg(reinterpret_cast<const double2*>(ps.a[0] + off_red) + i);
+    for (int q = 1; q < P; ++q) s = cadd(s, __ldcg(reinterpret_cast<const double2*>(ps.a[q] + off_red) + i));
     buf[i] = s;
   }
   __syncthreads();
@@ -216,7 +216,7 @@ __global__ void k_peer_gat_get(double2* __restrict__ f, int nx, PeerRows rows, P
     double2* dst = f + (size_t)rows.a[q] * nx;
     const long long n = (long long)(rows.b[q] - rows.a[q]) * nx;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
-      dst[t] = slot[t];
+      dst[t] = __ldcg(slot + t);
   }
   if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_GAT_ACK, e);
 }
