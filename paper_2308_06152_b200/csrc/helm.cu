@@ -150,7 +150,6 @@ struct helm_ctx_s {
   PeerLayout playout;
   PeerSet peers{};
   bool peer_connected = false;
-  unsigned long long ep_halo = 0, ep_red = 0, ep_gat = 0;
   unsigned* pcnt = nullptr;            // ticket counters: halo put/get, gather put/get
 };
 
@@ -297,10 +296,9 @@ int allreduce(helm_ctx_s& C, double2* buf, int n) {
   if (C.kind == HELM_COMM_PEER) {
     if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
     if ((size_t)n > PEER_RED_CAP) return fail(HELM_EINVAL, "rank sum of %d values exceeds the peer slot", n);
-    const unsigned long long e = ++C.ep_red;
-    launch_k(C, k_peer_red_put, 1, 256, 0, (const double2*)buf, n, C.peers, C.rank, C.nranks, C.playout.red, e);
+    launch_k(C, k_peer_red_put, 1, 256, 0, (const double2*)buf, n, C.peers, C.rank, C.nranks, C.playout.red);
     CKR(post_launch(C));
-    launch_k(C, k_peer_red_sum, 1, 256, 0, buf, n, C.peers, C.rank, C.nranks, C.playout.red, e);
+    launch_k(C, k_peer_red_sum, 1, 256, 0, buf, n, C.peers, C.rank, C.nranks, C.playout.red);
     return post_launch(C);
   }
   if ((size_t)n > C.red_cap) return fail(HELM_EINVAL, "allreduce of %d values exceeds the staging buffer", n);
@@ -324,13 +322,12 @@ int halo(helm_ctx_s& C, int l, DVec x) {
   const int grid = std::max(1, std::min((n + 255) / 256, C.sm_count * 4));
   if (C.kind == HELM_COMM_PEER) {
     if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
-    const unsigned long long e = ++C.ep_halo;
     const int pg = std::min(grid, C.sm_count);
     launch_k(C, k_peer_halo_put, pg, 256, 0, x, nx, L.own0, L.nown, up, dn, C.peers, C.rank, C.playout.up[l],
-             C.playout.dn[l], e, C.pcnt);
+             C.playout.dn[l], C.pcnt);
     CKR(post_launch(C));
     launch_k(C, k_peer_halo_get, pg, 256, 0, x, nx, L.own0, L.nown, up, dn, C.peers, C.rank, C.playout.up[l],
-             C.playout.dn[l], e, C.pcnt + 1);
+             C.playout.dn[l], C.pcnt + 1);
     return post_launch(C);
   }
   launch_k(C, k_halo_pack, grid, 256, 0, x, nx, L.own0, L.nown, up, dn, L.hs_up, L.hs_dn);
@@ -374,12 +371,11 @@ int allgather(helm_ctx_s& C, int l) {
       rows.a[q] = prow(C, l, q).a;
       rows.b[q] = prow(C, l, q).b;
     }
-    const unsigned long long e = ++C.ep_gat;
     const int pg = std::max(1, std::min(grid1d(C, L.n), C.sm_count));
     launch_k(C, k_peer_gat_put, pg, 256, 0, (const double2*)L.f, (int)nx, rows, C.peers, C.rank, C.nranks,
-             C.playout.gat, e, C.pcnt + 2);
+             C.playout.gat, C.pcnt + 2);
     CKR(post_launch(C));
-    launch_k(C, k_peer_gat_get, pg, 256, 0, L.f, (int)nx, rows, C.peers, C.rank, C.nranks, C.playout.gat, e,
+    launch_k(C, k_peer_gat_get, pg, 256, 0, L.f, (int)nx, rows, C.peers, C.rank, C.nranks, C.playout.gat,
              C.pcnt + 3);
     return post_launch(C);
   }
@@ -2032,10 +2028,11 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   C->rank = d->rank;
   C->nranks = d->nranks;
   C->grp = d->kind == HELM_COMM_THREADS ? d->group : nullptr;
-  // decomposed solves: host-polled loops, no cluster tail / cooperative step.  PDL stays as
-  // requested: a kernel launched with it waits (griddepcontrol.wait) for its predecessor kernel
-  // -- ours or NCCL's -- to complete; event waits and copies serialise as usual.
-  C->p.graph = 0;
+  // decomposed solves: host-polled loops (thread groups and NCCL; the peer transport is pure
+  // kernels with device-side epochs, so its solves may run as CUDA graphs), no cluster tail /
+  // cooperative step.  PDL stays as requested: a kernel launched with it waits
+  // (griddepcontrol.wait) for its predecessor kernel -- ours or NCCL's -- to complete.
+  if (d->kind != HELM_COMM_PEER) C->p.graph = 0;
   C->p.tail_max_n = 0;
   C->p.coop = 0;
   if (C->p.dist_min_rows <= 0) C->p.dist_min_rows = 16;

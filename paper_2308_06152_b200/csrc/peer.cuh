@@ -6,7 +6,9 @@
 // (release, system scope); the consumer kernel waits for the peers' flags (acquire), reads
 // their slots directly over NVLink and publishes an acknowledgement, which the next producer
 // of the same slot waits for (no slot is overwritten before every reader is done).  Epochs
-// are host counters: every rank issues the same exchanges in the same order.
+// are device counters in each rank's own arena, advanced by the producer kernels: every rank
+// issues the same exchanges in the same order, so the counters stay in lockstep, and a solve
+// captured in a CUDA graph replays correctly.
 //
 // Kernels of different ranks wait on each other here, so this transport needs one GPU per rank
 // (never several ranks on one GPU).  Waits give up after ~10 s of GPU clock and raise an error
@@ -19,7 +21,11 @@
 
 namespace helm {
 
-enum PeerFlag { PF_HALO_READY = 0, PF_HALO_ACK, PF_RED_READY, PF_RED_ACK, PF_GAT_READY, PF_GAT_ACK, PF_ERROR, PF_COUNT };
+enum PeerFlag {
+  PF_HALO_READY = 0, PF_HALO_ACK, PF_RED_READY, PF_RED_ACK, PF_GAT_READY, PF_GAT_ACK, PF_ERROR,
+  PF_EP_HALO, PF_EP_RED, PF_EP_GAT,   // this rank's epoch counters (device-side, so graph replays advance them)
+  PF_COUNT
+};
 constexpr int PF_STRIDE = 16;                       // one 128-byte line per flag
 constexpr size_t PEER_RED_CAP = 2 * 4096 + 8;      // rank-sum slot (complex values)
 constexpr long long PEER_TIMEOUT_CYCLES = 20000000000LL;   // ~10 s at 2 GHz
@@ -89,6 +95,13 @@ __device__ __forceinline__ void peer_wait(char* peer, int f, unsigned long long 
   __threadfence_system();
 }
 
+// producer: epoch of this exchange = counter + 1 (read by every block before the last one
+// advances it); consumer: the counter as the producer left it
+__device__ __forceinline__ unsigned long long peer_epoch(char* me, int ch) {
+  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*pflag(me, ch));
+  return a.load(cuda::memory_order_relaxed);
+}
+
 struct PeerSet {
   char* a[DIST_MAX_RANKS];   // every rank's arena, mapped into this process (own arena included)
 };
@@ -107,9 +120,10 @@ __device__ __forceinline__ bool peer_last_block(unsigned* counter) {
 
 // ---- halo: (1) pack my boundary rows into my arena, publish HALO_READY = e
 __global__ void k_peer_halo_put(DVec xv, int nx, int own0, int nown, int up, int dn, PeerSet ps, int me, size_t off_up,
-                                size_t off_dn, unsigned long long e, unsigned* counter) {
+                                size_t off_dn, unsigned* counter) {
   HELM_PDL_ENTRY();
   char* mine = ps.a[me];
+  const unsigned long long e = peer_epoch(mine, PF_EP_HALO) + 1;
   if (threadIdx.x == 0) {   // the readers of my previous slots are done (acknowledged epoch e - 1)
     if (up) peer_wait(ps.a[me - 1], PF_HALO_ACK, e - 1, mine);
     if (dn) peer_wait(ps.a[me + 1], PF_HALO_ACK, e - 1, mine);
@@ -123,14 +137,18 @@ __global__ void k_peer_halo_put(DVec xv, int nx, int own0, int nown, int up, int
     if (up) sup[t] = x[(size_t)own0 * nx + t];
     if (dn) sdn[t] = x[(size_t)(own0 + nown - GHOST) * nx + t];
   }
-  if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_HALO_READY, e);
+  if (peer_last_block(counter) && threadIdx.x == 0) {
+    *pflag(mine, PF_EP_HALO) = e;
+    peer_publish(mine, PF_HALO_READY, e);
+  }
 }
 
 // ---- halo: (2) wait for the neighbours' rows of epoch e, copy them into my ghost rows, ack
 __global__ void k_peer_halo_get(DVec xv, int nx, int own0, int nown, int up, int dn, PeerSet ps, int me, size_t off_up,
-                                size_t off_dn, unsigned long long e, unsigned* counter) {
+                                size_t off_dn, unsigned* counter) {
   HELM_PDL_ENTRY();
   char* mine = ps.a[me];
+  const unsigned long long e = peer_epoch(mine, PF_EP_HALO);
   if (threadIdx.x == 0) {
     if (up) peer_wait(ps.a[me - 1], PF_HALO_READY, e, mine);
     if (dn) peer_wait(ps.a[me + 1], PF_HALO_READY, e, mine);
@@ -149,10 +167,10 @@ __global__ void k_peer_halo_get(DVec xv, int nx, int own0, int nown, int up, int
 }
 
 // ---- rank sum of n values (one block each): put my values, then sum every rank's in rank order
-__global__ void k_peer_red_put(const double2* __restrict__ buf, int n, PeerSet ps, int me, int P, size_t off_red,
-                               unsigned long long e) {
+__global__ void k_peer_red_put(const double2* __restrict__ buf, int n, PeerSet ps, int me, int P, size_t off_red) {
   HELM_PDL_ENTRY();
   char* mine = ps.a[me];
+  const unsigned long long e = peer_epoch(mine, PF_EP_RED) + 1;
   if (threadIdx.x == 0)
     for (int q = 0; q < P; ++q)
       if (q != me) peer_wait(ps.a[q], PF_RED_ACK, e - 1, mine);
@@ -161,13 +179,16 @@ __global__ void k_peer_red_put(const double2* __restrict__ buf, int n, PeerSet p
   for (int i = threadIdx.x; i < n; i += blockDim.x) slot[i] = buf[i];
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) peer_publish(mine, PF_RED_READY, e);
+  if (threadIdx.x == 0) {
+    *pflag(mine, PF_EP_RED) = e;
+    peer_publish(mine, PF_RED_READY, e);
+  }
 }
 
-__global__ void k_peer_red_sum(double2* __restrict__ buf, int n, PeerSet ps, int me, int P, size_t off_red,
-                               unsigned long long e) {
+__global__ void k_peer_red_sum(double2* __restrict__ buf, int n, PeerSet ps, int me, int P, size_t off_red) {
   HELM_PDL_ENTRY();
   char* mine = ps.a[me];
+  const unsigned long long e = peer_epoch(mine, PF_EP_RED);
   if (threadIdx.x == 0)
     for (int q = 0; q < P; ++q)
       if (q != me) peer_wait(ps.a[q], PF_RED_READY, e, mine);
@@ -187,9 +208,10 @@ struct PeerRows {
 
 // ---- all-gather of a replicated level's f: put my owned rows, then fetch every peer's
 __global__ void k_peer_gat_put(const double2* __restrict__ f, int nx, PeerRows rows, PeerSet ps, int me, int P,
-                               size_t off_gat, unsigned long long e, unsigned* counter) {
+                               size_t off_gat, unsigned* counter) {
   HELM_PDL_ENTRY();
   char* mine = ps.a[me];
+  const unsigned long long e = peer_epoch(mine, PF_EP_GAT) + 1;
   if (threadIdx.x == 0)
     for (int q = 0; q < P; ++q)
       if (q != me) peer_wait(ps.a[q], PF_GAT_ACK, e - 1, mine);
@@ -199,13 +221,17 @@ __global__ void k_peer_gat_put(const double2* __restrict__ f, int nx, PeerRows r
   const double2* src = f + (size_t)rows.a[me] * nx;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     slot[t] = src[t];
-  if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_GAT_READY, e);
+  if (peer_last_block(counter) && threadIdx.x == 0) {
+    *pflag(mine, PF_EP_GAT) = e;
+    peer_publish(mine, PF_GAT_READY, e);
+  }
 }
 
 __global__ void k_peer_gat_get(double2* __restrict__ f, int nx, PeerRows rows, PeerSet ps, int me, int P,
-                               size_t off_gat, unsigned long long e, unsigned* counter) {
+                               size_t off_gat, unsigned* counter) {
   HELM_PDL_ENTRY();
   char* mine = ps.a[me];
+  const unsigned long long e = peer_epoch(mine, PF_EP_GAT);
   if (threadIdx.x == 0)
     for (int q = 0; q < P; ++q)
       if (q != me) peer_wait(ps.a[q], PF_GAT_READY, e, mine);

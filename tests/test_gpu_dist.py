@@ -228,3 +228,17 @@ def test_peer_transport_single_rank(lib):
     assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
     assert lib.load_library().helm_peer_error(H.ctx) == 0
     H.close()
+    # device-side epochs: the peer transport's solve also runs as a CUDA graph, with the same
+    # counts and bits as the host-polled loop; a second replay advances the epochs correctly
+    out = {}
+    for graph in (0, 1):
+        H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=dict(prm, graph=graph),
+                         peer_exchange=lambda h: [h])
+        x1, r1 = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
+        x2, r2 = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
+        assert torch.equal(x1, x2) and r1["outer_iterations"] == r2["outer_iterations"]
+        out[graph] = (x1, r1)
+        H.close()
+    assert out[0][1]["outer_iterations"] == out[1][1]["outer_iterations"]
+    assert out[0][1]["inner_iterations_total"] == out[1][1]["inner_iterations_total"]
+    assert torch.equal(out[0][0], out[1][0])
