@@ -270,8 +270,19 @@ class _StdoutToStderr:
 
 
 def run_decomposed(args, rank, world, local):
+    from paper_2308_06152_b200 import helm
     with _StdoutToStderr():
-        line = _run_decomposed(args, rank, world, local)
+        try:
+            line = _run_decomposed(args, rank, world, local)
+        except helm.HelmError as exc:
+            # the peer transport reports a stalled peer (wait timeout) on every rank; the job then
+            # reruns over NCCL instead of producing nothing
+            if args.transport != "peer":
+                raise
+            print(f"[bench] peer transport failed ({exc}); rerunning over NCCL", file=sys.stderr, flush=True)
+            args.transport = "nccl"
+            args.transport_note = f"peer transport failed: {exc}"
+            line = _run_decomposed(args, rank, world, local)
     if line is not None:
         print(json.dumps(line), flush=True)
 
@@ -377,7 +388,8 @@ def _run_decomposed(args, rank, world, local):
                    "outer_iterations": reps[-1]["outer_iterations"],
                    "inner_iterations_mean": reps[-1]["inner_iterations_total"] / max(1, reps[-1]["inner_solves"]),
                    "parallelism": f"row-strip decomposition x{world} ({args.transport} transport)",
-                   "dist_levels": prm["dist_levels"],
+                   "dist_levels": prm["dist_levels"], "transport": args.transport,
+                   **({"transport_note": args.transport_note} if getattr(args, "transport_note", None) else {}),
                    "value_definition": "world x outer iterations / max-over-ranks device time"},
         "wall_s": wall,
         "gpu_launches": launches,
@@ -407,8 +419,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
     ap.add_argument("--dist-levels", type=int, default=0, help="decomposed levels (0: 3)")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
-                    help="decomposed solve: NCCL collectives or NVLink peer memory (CUDA IPC)")
+    ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
+                    help="decomposed solve: NVLink peer memory through CUDA IPC (default; reruns over NCCL if a "
+                         "peer stalls) or NCCL collectives")
     ap.add_argument("--decomp", default="auto", choices=["auto", "on", "off"],
                     help="row-strip decomposed solve over the ranks (NCCL); auto = on when N > 1")
     args = ap.parse_args()

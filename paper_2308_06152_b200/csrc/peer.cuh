@@ -82,6 +82,10 @@ __device__ __forceinline__ void peer_publish(char* arena, int f, unsigned long l
 // the local error flag is raised and the wait abandoned
 __device__ __forceinline__ void peer_wait(char* peer, int f, unsigned long long e, char* me) {
   if (e == 0) return;
+  {   // after one timeout every later wait fails fast: the solve ends quickly and reports it
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> err(*pflag(me, PF_ERROR));
+    if (err.load(cuda::memory_order_relaxed)) return;
+  }
   cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> a(*pflag(peer, f));
   const long long t0 = clock64();
   while (a.load(cuda::memory_order_acquire) < e) {
@@ -160,8 +164,8 @@ __global__ void k_peer_halo_get(DVec xv, int nx, int own0, int nown, int up, int
   const double2* rdn = dn ? reinterpret_cast<const double2*>(ps.a[me + 1] + off_up) : nullptr;
   const int n = GHOST * nx;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    if (up) x[(size_t)(own0 - GHOST) * nx + t] = __ldcg(rup + t);   // L2 / NVLink, never a stale L1 line
-    if (dn) x[(size_t)(own0 + nown) * nx + t] = __ldcg(rdn + t);
+    if (up) x[(size_t)(own0 - GHOST) * nx + t] = __ldcv(rup + t);   // fetched again every time (peer memory: no stale cached line)
+    if (dn) x[(size_t)(own0 + nown) * nx + t] = __ldcv(rdn + t);
   }
   if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_HALO_ACK, e);
 }
@@ -194,8 +198,8 @@ __global__ void k_peer_red_sum(double2* __restrict__ buf, int n, PeerSet ps, int
       if (q != me) peer_wait(ps.a[q], PF_RED_READY, e, mine);
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double2 s = __ldcg(reinterpret_cast<const double2*>(ps.a[0] + off_red) + i);
-    for (int q = 1; q < P; ++q) s = cadd(s, __ldcg(reinterpret_cast<const double2*>(ps.a[q] + off_red) + i));
+    double2 s = __ldcv(reinterpret_cast<const double2*>(ps.a[0] + off_red) + i);
+    for (int q = 1; q < P; ++q) s = cadd(s, __ldcv(reinterpret_cast<const double2*>(ps.a[q] + off_red) + i));
     buf[i] = s;
   }
   __syncthreads();
@@ -242,7 +246,7 @@ __global__ void k_peer_gat_get(double2* __restrict__ f, int nx, PeerRows rows, P
     double2* dst = f + (size_t)rows.a[q] * nx;
     const long long n = (long long)(rows.b[q] - rows.a[q]) * nx;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
-      dst[t] = __ldcg(slot + t);
+      dst[t] = __ldcv(slot + t);
   }
   if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_GAT_ACK, e);
 }

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("extra", [[], ["--decomp", "on"], ["--decomp", "on", "--transport", "peer"]],
+@pytest.mark.parametrize("extra", [[], ["--decomp", "on", "--transport", "nccl"], ["--decomp", "on", "--transport", "peer"]],
                          ids=["single", "decomposed-nccl-1rank", "decomposed-peer-1rank"])
 def test_bench_line(lib, extra):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "3",
