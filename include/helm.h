@@ -267,7 +267,13 @@ typedef struct {
   int rank, nranks;             /* 0 <= rank < nranks <= 16 */
   helm_group group;             /* HELM_COMM_THREADS */
   const unsigned char* nccl_id; /* HELM_COMM_NCCL: 128 bytes, identical on every rank */
+  int flags;                    /* HELM_DIST_* bits, 0 for production */
 } helm_dist;
+/* HELM_COMM_PEER with nranks == 1: run the exchange kernels (halo, rank sums, all-gather, the
+ * fused peer DCGS kernels) against the rank's own arena instead of skipping them -- a test
+ * mode that exercises the peer transport on one GPU.  Without it a single rank exchanges
+ * nothing (identical results, fewer launches). */
+#define HELM_DIST_EXCHANGE_AT_ONE_RANK 1
 
 /* As helm_setup, on the global grid and the global k (nx*ny, host or device), for rank
  * dist->rank of a decomposed solve.  Collective: every rank must call it. */

@@ -138,6 +138,7 @@ struct helm_ctx_s {
   long long cnt[2][3] = {{0, 0, 0}, {0, 0, 0}};
   // row-strip decomposition over ranks (dist.cuh); dist == 0: single GPU
   int dist = 0, kind = -1, rank = 0, nranks = 1, D = -1;
+  bool x1 = false;                     // HELM_DIST_EXCHANGE_AT_ONE_RANK (peer transport tests)
   std::vector<DistRows> plan;          // plan[l * nranks + q]
   helm_group_s* grp = nullptr;
   ncclComm_t nccl = nullptr;
@@ -286,9 +287,12 @@ int dist_sync(helm_ctx_s& C) {
   return HELM_OK;
 }
 
+// Whether this rank exchanges at all: P > 1, or the one-rank peer test mode.
+inline bool exchanges(const helm_ctx_s& C) { return C.nranks > 1 || C.x1; }
+
 // In-place sum over the ranks of n complex values (the same bits on every rank).
 int allreduce(helm_ctx_s& C, double2* buf, int n) {
-  if (!C.dist || C.nranks == 1) return HELM_OK;
+  if (!C.dist || !exchanges(C)) return HELM_OK;
   if (C.kind == HELM_COMM_NCCL) {
     NCK(C.api->AllReduce(buf, buf, 2 * (size_t)n, ncclFloat64, ncclSum, C.nccl, C.s));
     return HELM_OK;
@@ -314,7 +318,8 @@ int allreduce(helm_ctx_s& C, double2* buf, int n) {
 // Refresh the GHOST rows on each side of this rank's owned rows of x (a level-l block) from
 // the neighbouring ranks.  No-op on replicated levels and on one rank.
 int halo(helm_ctx_s& C, int l, DVec x) {
-  if (!C.dist || C.nranks == 1 || !C.L[l].block) return HELM_OK;
+  // (one rank: nothing to exchange, but the peer transport still runs its kernels and flags)
+  if (!C.dist || !exchanges(C) || !C.L[l].block) return HELM_OK;
   const Level& L = C.L[l];
   const int nx = L.g.nx;
   const int up = C.rank > 0, dn = C.rank < C.nranks - 1;
@@ -361,7 +366,7 @@ int halo(helm_ctx_s& C, int l, DVec x) {
 
 // Complete the replicas of a replicated level's f: every rank contributes its owned rows.
 int allgather(helm_ctx_s& C, int l) {
-  if (!C.dist || C.nranks == 1) return HELM_OK;
+  if (!C.dist || !exchanges(C)) return HELM_OK;
   Level& L = C.L[l];
   const size_t nx = (size_t)L.g.nx;
   if (C.kind == HELM_COMM_PEER) {
@@ -421,6 +426,10 @@ Level coarse_of(const helm_ctx_s& C, int l) {
   G.row0 = ws;
   return G;
 }
+
+// Krylov sums go through the rank-sum path: with several ranks, and always with the peer
+// transport (so that its fused kernels also run -- and are tested -- with one rank)
+bool rank_summed(const helm_ctx_s& C) { return C.dist && exchanges(C); }
 
 bool gathers(const helm_ctx_s& C, int l) { return C.dist && C.L[l].block && !C.L[l + 1].block; }
 
@@ -773,6 +782,8 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_stepB, usmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_stepB_peer, usmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_update_peer, dcgs_update_smem_dev(m) + (size_t)(2 * m + 4) * sizeof(double2)));
   CKR(raise_dyn_smem((const void*)k_fgm_backsub, std::min<size_t>(96 * 1024, ((size_t)m * (m + 1) + m) * 16)));
   {
     // pass 2 in one wave: at most as many blocks as can be resident
@@ -952,6 +963,20 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
     // reduction of the pass-1 partials; pass 2 with the rotation part of step A in an extra
     // block and step B in the last block.  Decomposed: the dots are summed over the ranks
     // before pass 2, |w'|^2 before step B (then a separate one-warp kernel)
+    if (K.dist && C.kind == HELM_COMM_PEER) {
+      // rank sums fused into the step's kernels over peer memory (peer.cuh): 4 kernels per step
+      if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
+      launch_k(C, k_dcgs_reduce_peer, ((2 * K.m + 2) * 32 + 255) / 256, 256, 0, (const double2*)K.part, nparts,
+               (const FgmState*)st, K.dots1, K.cnt, C.peers, C.rank, C.nranks, C.playout.red);
+      CKR(post_launch(C));
+      const size_t us = dcgs_update_smem_dev(K.m) + (size_t)(2 * K.m + 4) * sizeof(double2);
+      launch_k(C, k_dcgs_update_peer, gg.gu + 1, DU_THREADS, us, Vo, ld, (const int*)&st->j, K.dots1, vjo, wo, ln,
+               K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1, K.m, C.peers, C.rank, C.nranks, C.playout.red);
+      CKR(post_launch(C));
+      launch_k(C, k_dcgs_stepB_peer, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
+               K.rawc, h, use_h, C.peers, C.rank, C.nranks, C.playout.red);
+      return post_launch(C);
+    }
     launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, nparts, st, K.H,
              K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
     CKR(post_launch(C));
@@ -1134,7 +1159,7 @@ int ensure_outer(helm_ctx_s& C, int maxit) {
   const size_t budget = C.dist ? tot / 4 : fr / 2;
   m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), budget / per));
   const Level& F = C.L[0];
-  return fgm_alloc(C, C.outer, m, (size_t)F.nown * F.g.nx, F.n, (size_t)F.own0 * F.g.nx, C.dist && C.nranks > 1);
+  return fgm_alloc(C, C.outer, m, (size_t)F.nown * F.g.nx, F.n, (size_t)F.own0 * F.g.nx, rank_summed(C));
 }
 
 }  // namespace
@@ -1458,7 +1483,7 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     const Level& G1 = C.L[1];
     const dim3 gt = glk_tiles(C);
     CKR(fgm_alloc(C, C.inner, p.inner_maxit, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
-                  C.dist && C.nranks > 1 && G1.block, fused_E_dots(C) ? (int)(gt.x * gt.y) : 0));
+                  rank_summed(C) && G1.block, fused_E_dots(C) ? (int)(gt.x * gt.y) : 0));
   }
   CK(cudaStreamSynchronize(C.s));
   return HELM_OK;
@@ -2027,6 +2052,7 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   C->kind = d->kind;
   C->rank = d->rank;
   C->nranks = d->nranks;
+  C->x1 = d->kind == HELM_COMM_PEER && (d->flags & HELM_DIST_EXCHANGE_AT_ONE_RANK);
   C->grp = d->kind == HELM_COMM_THREADS ? d->group : nullptr;
   // decomposed solves: host-polled loops (thread groups and NCCL; the peer transport is pure
   // kernels with device-side epochs, so its solves may run as CUDA graphs), no cluster tail /

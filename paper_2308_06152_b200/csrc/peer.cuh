@@ -70,8 +70,8 @@ __device__ __forceinline__ unsigned long long* pflag(char* arena, int f) {
   return reinterpret_cast<unsigned long long*>(arena) + (size_t)f * PF_STRIDE;
 }
 
-// (every thread of the block has executed __threadfence_system() after its slot writes and the
-// block has synchronised before thread 0 publishes)
+// (the block has synchronised after its slot writes; thread 0's system-scope fence here orders
+// them -- cumulatively, through the barrier -- before the flag)
 __device__ __forceinline__ void peer_publish(char* arena, int f, unsigned long long e) {
   __threadfence_system();
   cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> a(*pflag(arena, f));
@@ -114,9 +114,11 @@ struct PeerSet {
 // are made visible system-wide first (the peers read them over NVLink)
 __device__ __forceinline__ bool peer_last_block(unsigned* counter) {
   __shared__ bool last;
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();   // the block's writes, then one system-scope fence by the signalling thread
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
   if (last && threadIdx.x == 0) *counter = 0u;
   return last;
@@ -181,7 +183,6 @@ __global__ void k_peer_red_put(const double2* __restrict__ buf, int n, PeerSet p
   __syncthreads();
   double2* slot = reinterpret_cast<double2*>(mine + off_red);
   for (int i = threadIdx.x; i < n; i += blockDim.x) slot[i] = buf[i];
-  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
     *pflag(mine, PF_EP_RED) = e;
@@ -249,6 +250,152 @@ __global__ void k_peer_gat_get(double2* __restrict__ f, int nx, PeerRows rows, P
       dst[t] = __ldcv(slot + t);
   }
   if (peer_last_block(counter) && threadIdx.x == 0) peer_publish(mine, PF_GAT_ACK, e);
+}
+
+}  // namespace helm
+
+// ------------------------------------------------------------------ fused Krylov rank sums
+// The delayed-CGS2 step of a decomposed inner / outer FGMRES with the two rank sums fused into
+// its kernels over peer memory (no separate exchange kernels): the pass-1 reduction publishes
+// this rank's dots in its arena; every pass-2 block waits for the peers' dots and sums them (rank
+// order) before deriving the coefficients; pass 2's last block publishes the local |w'|^2; the
+// step-B kernel sums the norms.  4 kernels per step instead of 8.
+namespace helm {
+
+// dynamic shared memory of k_dcgs_update (as helm.cu's dcgs_update_smem), 16-byte aligned
+__host__ __device__ inline size_t dcgs_update_smem_dev(int m) {
+  const size_t a = (size_t)(2 * m + 2) * sizeof(double2), b = dcgs_smem(m);
+  return ((a > b ? a : b) + 15) / 16 * 16;
+}
+
+__device__ __forceinline__ void peer_wait_all(const PeerSet& ps, int me, int P, int f, unsigned long long e) {
+  for (int q = 0; q < P; ++q)
+    if (q != me) peer_wait(ps.a[q], f, e, ps.a[me]);
+}
+
+// pass-1 reduction (one warp per output) + publish of this rank's sums (last block)
+__global__ void __launch_bounds__(256) k_dcgs_reduce_peer(const double2* __restrict__ part, long long np,
+                                                          const FgmState* st, double2* __restrict__ dots,
+                                                          unsigned* counter, PeerSet ps, int me, int P,
+                                                          size_t off_red) {
+  HELM_PDL_ENTRY();
+  const int ntot = 2 * (st->j + 1);
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c < ntot) {
+    double2 s = make_double2(0.0, 0.0);
+    for (long long b = lane; b < np; b += 32) s = cadd(s, part[(long long)c * np + b]);
+    s = warp_sum2(s);
+    if (lane == 0) dots[c] = s;
+  }
+  if (!last_block(counter)) return;
+  char* mine = ps.a[me];
+  __shared__ unsigned long long se;
+  if (threadIdx.x == 0) {
+    se = peer_epoch(mine, PF_EP_RED) + 1;
+    peer_wait_all(ps, me, P, PF_RED_ACK, se - 1);   // every reader of my previous slot is done
+  }
+  __syncthreads();
+  double2* slot = reinterpret_cast<double2*>(mine + off_red);
+  for (int i = threadIdx.x; i < ntot; i += blockDim.x) slot[i] = dots[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *pflag(mine, PF_EP_RED) = se;
+    peer_publish(mine, PF_RED_READY, se);
+  }
+}
+
+// pass 2 with the rank sum of the dots in every block's prologue; extra block 0 runs the
+// rotation part of step A (and leaves the summed dots in `dots` for step B); the last block
+// acknowledges the dots and publishes this rank's |w'|^2.  Dynamic shared memory:
+// dcgs_update_smem(m) + (2m + 4) complex.
+__global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update_peer(
+    const double2* __restrict__ V, long long ld, const int* __restrict__ jptr, double2* __restrict__ dots, DVec xv,
+    DVec wv, long long n, double2* __restrict__ part, FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+    double2* __restrict__ rawc, unsigned* counter, int m, PeerSet ps, int me, int P, size_t off_red) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 sab[];
+  double2* sd = sab + (dcgs_update_smem_dev(m) / sizeof(double2));   // summed dots
+  __shared__ DuRed<DU_WARPS, DU_ELEMS / 32> red;
+  __shared__ double s_beta;
+  __shared__ double2 s_hjj;
+  __shared__ unsigned long long se;
+  char* mine = ps.a[me];
+  const int j = *jptr;
+  const int ntot = 2 * (j + 1);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      se = peer_epoch(mine, PF_EP_RED);
+      peer_wait_all(ps, me, P, PF_RED_READY, se);
+    }
+    __syncwarp();
+    for (int c = threadIdx.x; c < ntot; c += 32) {
+      double2 s = __ldcv(reinterpret_cast<const double2*>(ps.a[0] + off_red) + c);
+      for (int q = 1; q < P; ++q) s = cadd(s, __ldcv(reinterpret_cast<const double2*>(ps.a[q] + off_red) + c));
+      sd[c] = s;
+    }
+    __syncwarp();
+    dcgs_coefs_warp(j, sd, sab, &s_beta, &s_hjj);
+  }
+  __syncthreads();
+  const bool extra = blockIdx.x == 0;
+  const int nb = (int)gridDim.x - 1, tb = (int)blockIdx.x - 1;
+  double nrm = 0.0;
+  if (extra) {
+    for (int c = threadIdx.x; c < ntot; c += blockDim.x) dots[c] = sd[c];   // for step B
+    if (threadIdx.x < 32) dcgs_stepA_rot_warp(st, H, cs, sn, g, sd, rawc, s_beta, sab);
+  } else {
+    const double ib = (1.0 / s_beta) * xv.scale();
+    const double2 hjj = s_hjj;
+    double2* x = xv.get();
+    double2* w = wv.get();
+    const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
+    for (long long tile = tb; tile < tiles; tile += nb)
+      nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
+  }
+  const double t = block_sum(nrm);
+  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
+  if (!last_block(counter)) return;
+  if (threadIdx.x < 32) {
+    double s = 0.0;   // this rank's |w'|^2 (fixed order)
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += part[b].x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      peer_publish(mine, PF_RED_ACK, se);                 // every block of this rank read the dots
+      const unsigned long long e2 = se + 1;
+      peer_wait_all(ps, me, P, PF_RED_ACK, se);           // and every peer: my slot is free again
+      reinterpret_cast<double2*>(mine + off_red)[0] = make_double2(s, 0.0);
+      *pflag(mine, PF_EP_RED) = e2;
+      peer_publish(mine, PF_RED_READY, e2);
+    }
+  }
+}
+
+// step B after the rank sum of |w'|^2 (one warp); h_jj from the summed dots
+__global__ void k_dcgs_stepB_peer(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                  const double2* __restrict__ dots, double2* __restrict__ rawc,
+                                  cudaGraphConditionalHandle hcond, int use_h, PeerSet ps, int me, int P,
+                                  size_t off_red) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 srb[];
+  __shared__ double s_beta;
+  __shared__ double2 s_hjj;
+  __shared__ double2 snorm[1];
+  if (threadIdx.x >= 32) return;
+  char* mine = ps.a[me];
+  if (threadIdx.x == 0) {
+    const unsigned long long e2 = peer_epoch(mine, PF_EP_RED);
+    peer_wait_all(ps, me, P, PF_RED_READY, e2);
+    double2 s = __ldcv(reinterpret_cast<const double2*>(ps.a[0] + off_red));
+    for (int q = 1; q < P; ++q) s = cadd(s, __ldcv(reinterpret_cast<const double2*>(ps.a[q] + off_red)));
+    snorm[0] = s;
+    peer_publish(mine, PF_RED_ACK, e2);
+  }
+  __syncwarp();
+  dcgs_coefs_warp(st->j, dots, srb, &s_beta, &s_hjj);
+  __syncwarp();
+  dcgs_stepB_warp(st, H, cs, sn, g, dots, s_hjj, snorm, 1, rawc, hcond, use_h, srb);
 }
 
 }  // namespace helm

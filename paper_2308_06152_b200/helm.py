@@ -41,12 +41,14 @@ class helm_params(ctypes.Structure):
 
 class helm_dist(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
-                ("group", ctypes.c_void_p), ("nccl_id", ctypes.c_void_p)]
+                ("group", ctypes.c_void_p), ("nccl_id", ctypes.c_void_p),
+                ("flags", ctypes.c_int)]
 
 
 HELM_COMM_THREADS = 0
 HELM_COMM_NCCL = 1
 HELM_COMM_PEER = 2
+HELM_DIST_EXCHANGE_AT_ONE_RANK = 1
 
 
 class helm_report(ctypes.Structure):
@@ -379,10 +381,12 @@ class HelmDist(Helm):
     and returned by the entry points are this rank's owned rows, shape (nrows, nx)."""
 
     def __init__(self, nx, ny, h, bc, k, rank, nranks, group: ThreadGroup | None = None, nccl_id: bytes | None = None,
-                 params=None, stream=None, peer_exchange=None):
+                 params=None, stream=None, peer_exchange=None, exchange_at_one_rank=False):
         """Transport: a ThreadGroup (ranks as threads on one GPU), an NCCL unique id, or
         peer_exchange = callable(bytes) -> list of every rank's bytes (e.g. through
-        torch.distributed.all_gather_object) for the NVLink peer-memory transport."""
+        torch.distributed.all_gather_object) for the NVLink peer-memory transport.
+        exchange_at_one_rank: with the peer transport and nranks == 1, run the exchange kernels
+        against the rank's own arena (HELM_DIST_EXCHANGE_AT_ONE_RANK; tests)."""
         import torch
         self.torch = torch
         lib = load_library()
@@ -403,7 +407,8 @@ class HelmDist(Helm):
                                                            HELM_COMM_THREADS)
         d = helm_dist(kind, int(rank), int(nranks),
                       group.handle if group is not None else None,
-                      ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None)
+                      ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None,
+                      HELM_DIST_EXCHANGE_AT_ONE_RANK if exchange_at_one_rank else 0)
         ctx = ctypes.c_void_p()
         _check(lib.helm_setup_dist(ctypes.byref(ctx), ctypes.byref(g), _ptr(kt), 1, ctypes.byref(params),
                                    ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(d)))

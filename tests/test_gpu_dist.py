@@ -213,12 +213,13 @@ def test_dist_restarted_outer(lib):
 
 def test_peer_transport_single_rank(lib):
     """The NVLink peer-memory transport (HELM_COMM_PEER) with one rank: the arena is created,
-    exported and connected, every exchange runs its producer / consumer kernels and epoch flags
-    (no peer to wait for), and the solve matches the oracle like the other transports.  (With
-    several ranks its kernels wait on each other: one GPU per rank, never tested here.)"""
+    exported and connected, every exchange -- halos, rank sums, all-gathers and the Krylov step
+    with its fused rank sums -- runs its producer / consumer kernels and epoch flags (no peer to
+    wait for), and the solve matches the oracle like the other transports.  (With several ranks
+    its kernels wait on each other: one GPU per rank, never tested here.)"""
     p = _problem("c1_k50")
     prm = dict(coarse_op="galerkin", vectors="high_order", inner_tol=1e-1, inner_maxit=200)
-    H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=prm, peer_exchange=lambda h: [h])
+    H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=prm, peer_exchange=lambda h: [h], exchange_at_one_rank=True)
     x, rep = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
     assert rep["converged"]
     so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op="galerkin", vectors="high_order", inner_tol=1e-1,
@@ -233,7 +234,7 @@ def test_peer_transport_single_rank(lib):
     out = {}
     for graph in (0, 1):
         H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=dict(prm, graph=graph),
-                         peer_exchange=lambda h: [h])
+                         peer_exchange=lambda h: [h], exchange_at_one_rank=True)
         x1, r1 = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
         x2, r2 = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
         assert torch.equal(x1, x2) and r1["outer_iterations"] == r2["outer_iterations"]
@@ -242,3 +243,14 @@ def test_peer_transport_single_rank(lib):
     assert out[0][1]["outer_iterations"] == out[1][1]["outer_iterations"]
     assert out[0][1]["inner_iterations_total"] == out[1][1]["inner_iterations_total"]
     assert torch.equal(out[0][0], out[1][0])
+    # GCR over the peer transport (its scalar rank sums through the peer exchange kernels)
+    H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=dict(prm, outer="gcr"), peer_exchange=lambda h: [h], exchange_at_one_rank=True)
+    x, rep = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
+    assert rep["converged"] and rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    H.close()
+    # production mode (no HELM_DIST_EXCHANGE_AT_ONE_RANK): one rank exchanges nothing
+    H = lib.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, 0, 1, params=dict(prm, graph=1), peer_exchange=lambda h: [h])
+    x, rep = H.solve(torch.from_numpy(p.b).cuda(), tol=1e-6, maxit=200)
+    assert rep["converged"] and abs(rep["outer_iterations"] - ro["outer_iterations"]) <= 1
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    H.close()
