@@ -649,7 +649,7 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   }
   if (l == last) {
     const int n = (int)L.n;
-    launch_k(C, k_gemv, (n * 32 + 255) / 256, 256, 0, C.Minv, n, f, u_out, addq);
+    launch_k(C, k_gemv, n, HELM_GEMV_T, 0, C.Minv, n, f, u_out, addq);
     return post_launch(C);
   }
   // G: the coarse level as the transfer kernels see it (a window of the replica when level

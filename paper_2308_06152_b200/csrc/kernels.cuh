@@ -829,23 +829,36 @@ __global__ void k_gj_extract(const double2* __restrict__ Aug, int n, double2* __
 }
 
 // y = Minv f, one warp per row.
-__global__ void k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv, const double2* __restrict__ addq) {
+// One CTA of HELM_GEMV_T threads per row: the coarsest M^-1 (n <= a few hundred) is re-read from
+// L2 every V-cycle, so the row is split over the CTA (n CTAs instead of n/8) to have enough loads
+// in flight; warp shuffles + one shared-memory step reduce it.
+#define HELM_GEMV_T 128
+__global__ void __launch_bounds__(HELM_GEMV_T) k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv,
+                                                      const double2* __restrict__ addq) {
   HELM_PDL_ENTRY();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= n) return;
+  __shared__ double2 part[HELM_GEMV_T / 32];
+  const int row = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double2* __restrict__ f = fv.get();
-  double2* __restrict__ y = yv.get();
-  const double2* row = Minv + (size_t)warp * n;
+  const double2* __restrict__ r = Minv + (size_t)row * n;
   double2 s = make_double2(0.0, 0.0);
-  for (int c = lane; c < n; c += 32) s = cfma(row[c], f[c], s);
-  s = cscale(fv.scale(), s);
+#pragma unroll 4
+  for (int c = threadIdx.x; c < n; c += HELM_GEMV_T) s = cfma(r[c], f[c], s);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
     s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
   }
-  if (lane == 0) y[warp] = addq ? cadd(s, addq[warp]) : s;
+  if (lane == 0) part[w] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = part[0];
+#pragma unroll
+    for (int q = 1; q < HELM_GEMV_T / 32; ++q) t = cadd(t, part[q]);
+    t = cscale(fv.scale(), t);
+    double2* __restrict__ y = yv.get();
+    y[row] = addq ? cadd(t, addq[row]) : t;
+  }
 }
 
 // y = a + b
