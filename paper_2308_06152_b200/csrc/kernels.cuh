@@ -332,8 +332,7 @@ __device__ __forceinline__ void interp_w(int r, double& wm, double& w0, double& 
   wp = odd ? 0.5 : (R == 2 ? 0.125 : 0.0);
 }
 
-// Block = 32 x 8 threads; every phase walks its region row by row (threadIdx.y) and column by
-// column (threadIdx.x), so no division/modulo in the index math.
+// Block = 32 x 8 threads.
 // DOTS (MODE 0, inner FGMRES): the tile also runs pass 1 of the delayed CGS2 for its coarse
 // points -- part[(2c) T + tile] = sum conj(V_c) (s v~_j), part[(2c+1) T + tile] = sum conj(V_c) w
 // for c <= j, with V_j read as s v~_j (T tiles; w = E x is this tile's output) -- so the E output
@@ -365,87 +364,81 @@ __global__ void __launch_bounds__(256, DOTS ? HELM_GLKD_MINB : 6) k_galerkin_app
   const int fx0t = fx0s - 1, fy0t = fy0s - 1;
   const int cx0 = I0 - R - 1, cy0 = J0 - R - 1;   // coarse index of sx column / row 0
   const double2 zero = make_double2(0.0, 0.0);
-  for (int r = ty_; r < CYW; r += 8) {
-    const int J = cy0 + r;
-    const bool jin = (J >= 0 && J < gc.ny);
-    for (int c = tx_; c < CXW; c += 32) {
-      const int I = cx0 + c;
-      sx[r * CXW + c] = (jin && I >= 0 && I < gc.nx) ? x[(size_t)J * gc.nx + I] : zero;
-    }
+  // every phase walks its region as one flat index over the CTA's 256 threads (constant row
+  // widths: the division is a multiply-shift), so no lanes idle on the ragged region widths
+  const int tid = ty_ * 32 + tx_;
+  for (int q = tid; q < CYW * CXW; q += 256) {
+    const int r = q / CXW, c = q - r * CXW;
+    const int J = cy0 + r, I = cx0 + c;
+    sx[q] = (J >= 0 && J < gc.ny && I >= 0 && I < gc.nx) ? x[(size_t)J * gc.nx + I] : zero;
   }
   __syncthreads();
   // Z = tensor product of the 1D interpolations (Eq. 3.9 / 3.12): along x ...
-  for (int c = tx_; c < TXR; c += 32) {
+  for (int q = tid; q < CYW * TXR; q += 256) {
+    const int r = q / TXR, c = q - r * TXR;
     const int fx = fx0t + c;
     const int rr = fx - o;
     const int li = floordiv2i(rr) - cx0;
     double wm, w0, wp;
     interp_w<R>(rr, wm, w0, wp);
     if (fx < 0 || fx >= gf.nx) wm = w0 = wp = 0.0;
-    for (int r = ty_; r < CYW; r += 8) {
-      const double2* line = sx + r * CXW + li;
-      tx[r * TXR + c] = cadd(cadd(cscale(wm, line[-1]), cscale(w0, line[0])), cscale(wp, line[1]));
-    }
+    const double2* line = sx + r * CXW + li;
+    tx[q] = cadd(cadd(cscale(wm, line[-1]), cscale(w0, line[0])), cscale(wp, line[1]));
   }
   __syncthreads();
   // ... then along y
-  for (int r = ty_; r < TYR; r += 8) {
+  for (int q = tid; q < TYR * TXR; q += 256) {
+    const int r = q / TXR, c = q - r * TXR;
     const int fy = fy0t + r;
     const int rr = fy - o;
     const int lj = floordiv2i(rr) - cy0;
     double wm, w0, wp;
     interp_w<R>(rr, wm, w0, wp);
     if (fy < 0 || fy >= gf.ny) wm = w0 = wp = 0.0;
-    for (int c = tx_; c < TXR; c += 32)
-      stt[r * TXR + c] = cadd(cadd(cscale(wm, tx[(lj - 1) * TXR + c]), cscale(w0, tx[lj * TXR + c])),
-                              cscale(wp, tx[(lj + 1) * TXR + c]));
+    stt[q] = cadd(cadd(cscale(wm, tx[(lj - 1) * TXR + c]), cscale(w0, tx[lj * TXR + c])),
+                  cscale(wp, tx[(lj + 1) * TXR + c]));
   }
   __syncthreads();
-  for (int r = ty_; r < SY; r += 8) {
-    const int fy = fy0s + r;
-    for (int c = tx_; c < SX; c += 32) {
-      const int fx = fx0s + c;
-      double2 v = zero;   // reading R4: restriction taps outside the array dropped
-      if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
-        const Coef cf = coef_at(gf, fx, fy, kf[(size_t)fy * gf.nx + fx], 1.0, 0.0);
-        const int q = (r + 1) * TXR + (c + 1);
-        v = cmul(cf.ap, stt[q]);
-        if (cf.aw != 0.0) v = cadd(v, cscale(cf.aw, stt[q - 1]));
-        if (cf.ae != 0.0) v = cadd(v, cscale(cf.ae, stt[q + 1]));
-        if (cf.as != 0.0) v = cadd(v, cscale(cf.as, stt[q - TXR]));
-        if (cf.an != 0.0) v = cadd(v, cscale(cf.an, stt[q + TXR]));
-      }
-      ss[r * SX + c] = v;
+  for (int q = tid; q < SY * SX; q += 256) {
+    const int r = q / SX, c = q - r * SX;
+    const int fy = fy0s + r, fx = fx0s + c;
+    double2 v = zero;   // reading R4: restriction taps outside the array dropped
+    if (fx >= 0 && fx < gf.nx && fy >= 0 && fy < gf.ny) {
+      const Coef cf = coef_at(gf, fx, fy, kf[(size_t)fy * gf.nx + fx], 1.0, 0.0);
+      const int t = (r + 1) * TXR + (c + 1);
+      v = cmul(cf.ap, stt[t]);
+      if (cf.aw != 0.0) v = cadd(v, cscale(cf.aw, stt[t - 1]));
+      if (cf.ae != 0.0) v = cadd(v, cscale(cf.ae, stt[t + 1]));
+      if (cf.as != 0.0) v = cadd(v, cscale(cf.as, stt[t - TXR]));
+      if (cf.an != 0.0) v = cadd(v, cscale(cf.an, stt[t + TXR]));
     }
+    ss[q] = v;
   }
   __syncthreads();
   // Z^T = tensor product of the transposed 1D interpolations: along y ...
-  for (int jl = ty_; jl < TCY; jl += 8) {
+  for (int q = tid; q < TCY * SX; q += 256) {
+    const int jl = q / SX, c = q - jl * SX;
     const int iy = 2 * jl + R;
-    for (int c = tx_; c < SX; c += 32) {
-      double2 v = zero;
+    double2 v = zero;
 #pragma unroll
-      for (int b = -R; b <= R; ++b) v = cadd(v, cscale(zw<R>(b), ss[(iy + b) * SX + c]));
-      ry[jl * SX + c] = v;
-    }
+    for (int b = -R; b <= R; ++b) v = cadd(v, cscale(zw<R>(b), ss[(iy + b) * SX + c]));
+    ry[q] = v;
   }
   __syncthreads();
   // ... then along x
   const double2* __restrict__ f = fv.get();
   double2* __restrict__ y = yv.get();
-  for (int jl = ty_; jl < TCY; jl += 8) {
-    const int J = J0 + jl;
-    for (int il = tx_; il < TCX; il += 32) {
-      const int I = I0 + il;
-      if (I >= gc.nx || J >= gc.ny) continue;
-      const int ix = 2 * il + R;
-      double2 s = zero;
+  for (int q = tid; q < TCY * TCX; q += 256) {
+    const int jl = q / TCX, il = q - jl * TCX;
+    const int J = J0 + jl, I = I0 + il;
+    if (I >= gc.nx || J >= gc.ny) continue;
+    const int ix = 2 * il + R;
+    double2 s = zero;
 #pragma unroll
-      for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
-      const size_t p = (size_t)J * gc.nx + I;
-      y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
-      if (DOTS) wt[jl * TCX + il] = s;
-    }
+    for (int a = -R; a <= R; ++a) s = cadd(s, cscale(zw<R>(a), ry[jl * SX + ix + a]));
+    const size_t p = (size_t)J * gc.nx + I;
+    y[p] = (MODE == 1) ? csub(cscale(fv.scale(), f[p]), s) : s;
+    if (DOTS) wt[q] = s;
   }
   if (DOTS) {
     static_assert(TCX * TCY == 128, "pass-1 dots map 4 coarse points to each lane");
