@@ -123,6 +123,11 @@ typedef struct {
   double gamma;        /* TLKM shift (1) */
   int tail_cluster;    /* CTAs of the tail kernel (tail_max_n > 0): 0 = 16, else 8 (default); 1, 2,
                           4, 8 or 16 = exactly that many (1: one CTA, no cluster) */
+  int lag_stepb;       /* inner solve (single GPU): the Arnoldi step's loop decision taken one
+                          iteration late from the corrected column (the rotation leaves the serial
+                          tail of every iteration; a converged inner solve runs one discarded
+                          iteration).  Same iteration counts as the immediate test on the corrected
+                          column.  1 = on, 0 = off */
 } helm_params;
 
 typedef struct {

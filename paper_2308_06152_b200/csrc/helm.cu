@@ -917,6 +917,11 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
   const long long ld = (long long)K.ld, ln = (long long)n;
   double2* Vo = K.V + off;
   FgmState* st = K.st;
+  // lagged step B (helm_params.lag_stepb): the inner solve on one GPU (fresh start, staged back
+  // substitution, whose shared memory then also holds the last column's rotation)
+  const size_t bs = ((size_t)K.m * (K.m + 1) + K.m) * sizeof(double2);
+  const bool staged = bs <= 96 * 1024;
+  const bool lag = C.p.lag_stepb && &K == &C.inner && first && !K.dist && K.coop == 0 && staged && K.m >= 3;
   auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     if (first) {
       CKR(gs_dots(C, K, nullptr, nullptr, 0, shift(b, off), 1, K.nrm, nullptr));
@@ -983,7 +988,7 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
     if (K.dist) CKR(allreduce(C, K.dots1, 2 * K.m + 2));
     launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), Vo, ld, (const int*)&st->j,
              (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1, h, use_h,
-             K.dist ? 2 : 3);
+             K.dist ? 2 : (lag ? 7 : 3));
     CKR(post_launch(C));
     if (K.dist) {
       launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu + 1, K.nrm);
@@ -996,12 +1001,9 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
     return HELM_OK;
   };
   CKR(run_while(C, st, begin, body));
-  {
-    // the triangle of an m-column basis in shared memory when it fits (the inner solves)
-    const size_t bs = ((size_t)K.m * (K.m + 1) + K.m) * sizeof(double2);
-    const bool staged = bs <= 96 * 1024;
-    launch_k(C, k_fgm_backsub, 1, 256, staged ? bs : 0, st, K.H, K.g, K.y, outer_stats, staged ? 1 : 0);
-  }
+  // the triangle of an m-column basis in shared memory when it fits (the inner solves)
+  launch_k(C, k_fgm_backsub, 1, 256, staged ? bs : 0, st, K.H, K.g, K.y, outer_stats, staged ? 1 : 0, K.cs, K.sn,
+           lag ? (const double2*)K.rawc : (const double2*)nullptr);
   CKR(post_launch(C));
   // x = (x or 0) + Z y
   const DVec xo = shift(DVec(x), off);
@@ -1195,6 +1197,7 @@ void helm_default_params(helm_params* p) {
   p->precond = HELM_PRECOND_ADEF1;
   p->gamma = 1.0;
   p->tail_cluster = 0;
+  p->lag_stepb = 1;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1820,7 +1823,7 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         if (r != HELM_OK) break;
         launch_k(X, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
                  (const double2*)K.dots1, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1,
-                 cudaGraphConditionalHandle(0), 0, 3);
+                 cudaGraphConditionalHandle(0), 0, X.p.lag_stepb ? 7 : 3);
         r = post_launch(X);
         break;
       }

@@ -47,6 +47,10 @@ struct FgmState {
   // inner-solve statistics accumulated into the outer state
   long long inner_total;
   int inner_max, inner_solves;
+  // lagged step B (inner solve, flags & 4 of k_dcgs_update): lagc = step A of this iteration found
+  // the corrected residual of the previous column below tol; pend = the last column still awaits
+  // its rotation (done by k_fgm_backsub)
+  int lagc, pend;
 };
 
 __device__ __forceinline__ double2 warp_sum2(double2 s) {
@@ -255,6 +259,9 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
 __device__ void dcgs_stepA_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
                                 const double2* __restrict__ dots, double2* __restrict__ coef,
                                 double2* __restrict__ sc2, double2* __restrict__ rawc, double2* sdc);
+__device__ void dcgs_stepB_lag_warp(FgmState* st, const double2* __restrict__ dots, double2 hjj,
+                                    const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
+                                    cudaGraphConditionalHandle h, int use_h);
 __device__ void dcgs_stepB_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
                                 const double2* __restrict__ dots, double2 hjj,
                                 const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
@@ -263,7 +270,7 @@ __device__ void dcgs_coefs_warp(int j, const double2* __restrict__ dots, double2
                                 double2* shjj);
 __device__ void dcgs_stepA_rot_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
                                     const double2* __restrict__ dots, double2* __restrict__ rawc, double beta,
-                                    double2* sdc);
+                                    double2* sdc, int lag = 0);
 
 
 constexpr int DC_THREADS = 128;           // dots: 4 warps per block
@@ -470,7 +477,8 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
 }
 
 
-// flags: 1 = step B in the last block to finish; 2 = the grid has one extra block (block 0) that runs
+// flags: 1 = step B in the last block to finish (4: lagged, dcgs_stepB_lag_warp; needs 2); 2 = the
+// grid has one extra block (block 0) that runs
 // the rotation part of step A (column j-1) while the others stream pass 2 -- off the critical
 // path, since only step B needs it.  Every block derives the pass-2 coefficients from the
 // pass-1 dots itself (warp 0, identical arithmetic in every block).
@@ -495,7 +503,7 @@ __global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const 
   const int tb = (flags & 2) ? (int)blockIdx.x - 1 : (int)blockIdx.x;
   double nrm = 0.0;
   if (extra) {
-    if (threadIdx.x < 32) dcgs_stepA_rot_warp(st, H, cs, sn, g, dots, rawc, s_beta, sab);
+    if (threadIdx.x < 32) dcgs_stepA_rot_warp(st, H, cs, sn, g, dots, rawc, s_beta, sab, (flags & 4) ? 1 : 0);
   } else {
     const double ib = (1.0 / s_beta) * xv.scale();
     const double2 hjj = s_hjj;
@@ -508,8 +516,10 @@ __global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const 
   const double t = block_sum(nrm);
   if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);
   // step B in the last block to finish (sab is free again: it doubles as step B's scratch)
-  if ((flags & 1) && last_block(counter) && threadIdx.x < 32)
-    dcgs_stepB_warp(st, H, cs, sn, g, dots, s_hjj, part, gridDim.x, rawc, hcond, use_h, sab);
+  if ((flags & 1) && last_block(counter) && threadIdx.x < 32) {
+    if (flags & 4) dcgs_stepB_lag_warp(st, dots, s_hjj, part, gridDim.x, rawc, hcond, use_h);
+    else dcgs_stepB_warp(st, H, cs, sn, g, dots, s_hjj, part, gridDim.x, rawc, hcond, use_h, sab);
+  }
 }
 
 // The whole delayed-CGS2 step of one iteration as ONE cooperative kernel (small grids, where
@@ -773,7 +783,7 @@ __device__ void dcgs_coefs_warp(int j, const double2* __restrict__ dots, double2
 // dcgs_smem(m) bytes; every global load that does not depend on the dots is issued up front.
 __device__ void dcgs_stepA_rot_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
                                     const double2* __restrict__ dots, double2* __restrict__ rawc, double beta,
-                                    double2* sdc) {
+                                    double2* sdc, int lag) {
   const int m = st->m;
   double2* scol = sdc;                       // m + 2
   double2* ssn = sdc + (m + 2);              // m + 2
@@ -782,7 +792,10 @@ __device__ void dcgs_stepA_rot_warp(FgmState* st, double2* H, double* cs, double
   const int j = st->j;
   const int jm = j - 1;
   if (j == 0) {
-    if (lane == 0) g[0] = cscale(beta, g[0]);   // r = ||r|| v~_0 = (||r|| beta) v_0
+    if (lane == 0) {
+      g[0] = cscale(beta, g[0]);   // r = ||r|| v~_0 = (||r|| beta) v_0
+      if (lag) st->lagc = 0;
+    }
     return;
   }
   const double hold = rawc[j].x;             // h_{j,j-1} (real)
@@ -807,14 +820,17 @@ __device__ void dcgs_stepA_rot_warp(FgmState* st, double2* H, double* cs, double
   __syncwarp();
   const double2 a = rotate_column_warp(scol, jm, scs, ssn);
   if (lane == 0) {
-    // undo the old rotation G_{j-1} on g: g_{j-1}^old = c g_{j-1} - s g_j
-    g[jm] = csub(cscale(c0, gjm), cmul(s0, gj));
+    // undo the old rotation G_{j-1} on g: g_{j-1}^old = c g_{j-1} - s g_j (lagged step B: column
+    // j-1 was never rotated, g_{j-1} is still the old value)
+    if (!lag) g[jm] = csub(cscale(c0, gjm), cmul(s0, gj));
     g[j] = make_double2(0.0, 0.0);
     double2 hjj1;
     const double gn = new_rotation(jm, a, hnew, cs, sn, g, &hjj1);
     scol[jm] = hjj1;
     scol[j] = make_double2(0.0, 0.0);
-    st->relres = bnorm > 0.0 ? gn / bnorm : 0.0;
+    const double relres = bnorm > 0.0 ? gn / bnorm : 0.0;
+    st->relres = relres;
+    if (lag) st->lagc = relres <= st->tol ? 1 : 0;
   }
   __syncwarp();
   const int ld = m + 1;
@@ -904,6 +920,89 @@ __device__ void dcgs_stepB_warp(FgmState* st, double2* H, double* cs, double2* s
   for (int i = lane; i <= j + 1; i += 32) Hc[i] = scol[i];
 }
 
+// Lagged step B (inner solve; k_dcgs_update flags & 4).  The rotation of column j is NOT done
+// here: step A of iteration j+1 re-does it from the corrected column anyway (the rotation step B
+// would apply is undone there), so only the loop decision needs it -- and that decision is taken
+// one iteration late from step A's corrected residual (st->lagc, written by the extra block of
+// this same kernel): if column j-1 already met tol, column j is discarded (ncols = j, exactly
+// the count of the non-lagged test on the corrected column).  Stops by maxit / basis size /
+// breakdown are known here; the last column's rotation is then left to k_fgm_backsub (pend).
+// Cost: one discarded iteration per converged inner solve; gain: the rotation scan, the new
+// rotation and the H column store leave the serial tail of every iteration.
+__device__ void dcgs_stepB_lag_warp(FgmState* st, const double2* __restrict__ dots, double2 hjj,
+                                    const double2* __restrict__ npart, int np, double2* __restrict__ rawc,
+                                    cudaGraphConditionalHandle h, int use_h) {
+  const int lane = threadIdx.x & 31;
+  const int j = st->j;
+  double nsum = 0.0;
+  for (int b = lane; b < np; b += 32) nsum += npart[b].x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+  const bool lagconv = j >= 1 && st->lagc;
+  if (!lagconv) {
+    for (int c = lane; c < j; c += 32) rawc[c] = dots[2 * c + 1];
+  }
+  if (lane == 0) {
+    int done = 0;
+    if (lagconv) {   // columns 0..j-1 are the solution's; column j is dropped
+      st->ncols = j;
+      st->conv = 1;
+      st->pend = 0;
+      done = 1;
+    } else {
+      const double hn = sqrt(fmax(nsum, 0.0));
+      rawc[j] = hjj;
+      rawc[j + 1] = make_double2(hn, 0.0);
+      const int its = st->its + 1;
+      st->its = its;
+      st->ncols = j + 1;
+      st->hn = hn;
+      st->inv_hn = hn > 0.0 ? 1.0 / hn : 0.0;
+      if (hn == 0.0 || its >= st->maxit || j + 1 >= st->m) {
+        done = 1;
+        st->pend = 1;
+        if (hn == 0.0) st->conv = 1;
+      }
+      st->j = j + 1;
+    }
+    st->done = done;
+    fgm_set_cond(st, h, use_h, !done);
+  }
+}
+
+// The rotation of the last column left pending by the lagged step B (one warp): column
+// ncols-1 = rawc[0..ncols] (h_{ncols,ncols-1} last), its rotations, the residual estimate.
+__device__ void dcgs_final_rot_warp(FgmState* st, double2* H, double* cs, double2* sn, double2* g,
+                                    const double2* __restrict__ rawc, double2* sdc) {
+  const int m = st->m;
+  double2* scol = sdc;
+  double2* ssn = sdc + (m + 2);
+  double* scs = reinterpret_cast<double*>(sdc + (2 * m + 4));
+  const int lane = threadIdx.x & 31;
+  const int j = st->ncols - 1;
+  for (int c = lane; c <= j; c += 32) scol[c] = rawc[c];
+  for (int i = lane; i < j; i += 32) {
+    ssn[i] = sn[i];
+    scs[i] = cs[i];
+  }
+  __syncwarp();
+  const double hn = rawc[j + 1].x;
+  const double2 a = rotate_column_warp(scol, j, scs, ssn);
+  if (lane == 0) {
+    double2 rjj;
+    const double gn = new_rotation(j, a, hn, cs, sn, g, &rjj);
+    scol[j] = rjj;
+    scol[j + 1] = make_double2(0.0, 0.0);
+    const double relres = st->bnorm > 0.0 ? gn / st->bnorm : 0.0;
+    st->relres = relres;
+    if (relres <= st->tol) st->conv = 1;
+    st->pend = 0;
+  }
+  __syncwarp();
+  double2* Hc = H + (long long)j * (m + 1);
+  for (int i = lane; i <= j + 1; i += 32) Hc[i] = scol[i];
+}
+
 // y = x * (*scale)   (x may alias y; DVec slots)
 __global__ void k_scale_dvec(DVec xv, const double* __restrict__ scale, DVec yv, long long n,
                              const int* __restrict__ skip_if) {
@@ -928,6 +1027,8 @@ __global__ void k_fgm_begin(FgmState* st, const double2* __restrict__ nrm2, int 
   st->beta = beta;
   st->j = 0;
   st->ncols = 0;
+  st->lagc = 0;
+  st->pend = 0;
   st->inv_hn = 1.0;   // v~_0 = r/||r|| is stored normalised
   g[0] = make_double2(beta, 0.0);
   const double bn = st->bnorm;
@@ -951,12 +1052,18 @@ __global__ void k_fgm_begin(FgmState* st, const double2* __restrict__ nrm2, int 
 // and g into shared memory in one parallel sweep, then one warp runs the column-oriented
 // substitution from shared memory (y_q = s_q / R_qq, s_r -= R_rq y_q for r < q) -- the row
 // form below pays a global-memory round trip per row (~70 us for 50 rows).
-__global__ void k_fgm_backsub(FgmState* st, const double2* __restrict__ H, const double2* __restrict__ g,
-                              double2* __restrict__ y, FgmState* outer, int staged) {
+__global__ void k_fgm_backsub(FgmState* st, double2* __restrict__ H, double2* __restrict__ g,
+                              double2* __restrict__ y, FgmState* outer, int staged, double* cs = nullptr,
+                              double2* sn = nullptr, const double2* __restrict__ rawc = nullptr) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 sbs[];
   const int lane = threadIdx.x & 31;
   if (blockIdx.x != 0) return;
+  // lagged step B: the last column's rotation first (sbs as its scratch; staged mode only)
+  if (rawc && st->pend) {
+    if (threadIdx.x < 32) dcgs_final_rot_warp(st, H, cs, sn, g, rawc, sbs);
+    __syncthreads();
+  }
   const int mm = st->ncols;
   const int ld = st->m + 1;
   if (staged) {

@@ -393,3 +393,35 @@ def test_tlkm_apply_and_solve(lib, vec):
         xo_t, _ = so_t.solve(pr.b)
         assert rel(xt.cpu().numpy(), xo_t) < 1e-6
         H.close()
+
+
+@pytest.mark.parametrize("name,vec,op,itol", [("c1_k50", "high_order", "galerkin", 0.5),
+                                              ("mp_som_k40", "high_order", "galerkin", 0.3),
+                                              ("c0_tiny", "bilinear", "red_o4", 0.1)])
+def test_lagged_stepb_counts(lib, name, vec, op, itol):
+    """helm_params.lag_stepb (the inner Arnoldi loop decision taken one iteration late from the
+    corrected column, the discarded column dropped): the inner solves converge early here, and
+    every inner solve must stop at the oracle's own count (per outer iteration; +-1 where the
+    test is rounding-decided, reading R13), with the same outer count as lag_stepb = 0."""
+    p = _problem(name)
+    so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
+                                                           inner_maxit=200, maxit=400))
+    xo, rep_o = so.solve(p.b)
+    its_o = rep_o["inner_iterations"]
+    assert max(its_o) < 200   # the inner solves really converge (the lagged path is exercised)
+    reps = {}
+    for lag in (0, 1):
+        H = lib.helm_setup(p, {"coarse_op": op, "vectors": vec, "inner_tol": itol, "inner_maxit": 200,
+                               "lag_stepb": lag})
+        x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=400)
+        assert rep["converged"]
+        assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+        reps[lag] = rep
+        H.close()
+    for lag in (0, 1):
+        r = reps[lag]
+        assert abs(r["outer_iterations"] - rep_o["outer_iterations"]) <= 1
+        n = min(r["outer_iterations"], rep_o["outer_iterations"])
+        assert abs(r["inner_iterations_total"] - sum(its_o[:r["outer_iterations"]])) <= max(2, n // 10), (r, its_o)
+        assert r["inner_iterations_max"] <= max(its_o) + 1
+    assert reps[0]["outer_iterations"] == reps[1]["outer_iterations"]
