@@ -216,7 +216,10 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_APPLY_E 1
 #define HELM_GB_APPLY_A 2
 #define HELM_GB_DCGS 3      /* one delayed-CGS2 step (pass 1, reduction + step A, pass 2 + step B)
-                               of the inner FGMRES from column `arg` (arg + reps < inner_maxit) */
+                               of the inner FGMRES from column `arg` (arg + reps < inner_maxit).
+                               Probe knobs (environment, this region only): HELM_GB_DCGS_MASK
+                               selects its kernels (1 dots, 2 reduction, 4 update; default 7),
+                               HELM_GB_UPD_FLAGS overrides the update kernel's flags */
 #define HELM_GB_INNER_ITER 4 /* one whole inner FGMRES iteration (V-cycle from level 1, E apply,
                                 delayed-CGS2 step) from column `arg`, without the loop node */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);

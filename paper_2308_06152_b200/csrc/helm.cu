@@ -1813,17 +1813,26 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
           r = apply_E(X, zj, DVec(), w);
           if (r != HELM_OK) break;
         }
-        launch_k(X, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, (const int*)&st->j, 1,
-                 vj, w, ln, gg.chunk, K.part);
-        r = post_launch(X);
-        if (r != HELM_OK) break;
-        launch_k(X, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, dcgs_smem(K.m), K.part, (long long)gg.gx,
-                 st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
-        r = post_launch(X);
-        if (r != HELM_OK) break;
+        // probe: HELM_GB_DCGS_MASK selects the step's kernels (1 dots, 2 reduceA, 4 update; default 7)
+        const char* mk = getenv("HELM_GB_DCGS_MASK");
+        const int mask = mk ? atoi(mk) : 7;
+        if (mask & 1) {
+          launch_k(X, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, (const int*)&st->j, 1,
+                   vj, w, ln, gg.chunk, K.part);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+        }
+        if (mask & 2) {
+          launch_k(X, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, dcgs_smem(K.m), K.part,
+                   (long long)gg.gx, st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+        }
+        if (!(mask & 4)) break;
         launch_k(X, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
                  (const double2*)K.dots1, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1,
-                 cudaGraphConditionalHandle(0), 0, X.p.lag_stepb ? 7 : 3);
+                 cudaGraphConditionalHandle(0), 0,
+                 getenv("HELM_GB_UPD_FLAGS") ? atoi(getenv("HELM_GB_UPD_FLAGS")) : (X.p.lag_stepb ? 7 : 3));
         r = post_launch(X);
         break;
       }

@@ -413,8 +413,18 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
                                                    const double2* sab, double ib, double2 hjj, double2* x, double2* w,
                                                    long long n, long long tile, DuRed<NW, EPL>& red) {
   constexpr int TE = 32 * EPL;
+  constexpr bool ONE = TE <= 32 * NW;   // the final phase is one element per thread
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const long long eb = tile * TE + lane;
+  // the final phase's x / w loads issued first, so their latency overlaps the basis stream
+  double2 xpre = make_double2(0.0, 0.0), wpre = xpre;
+  if (ONE) {
+    const long long e = tile * TE + threadIdx.x;
+    if (threadIdx.x < TE && e < n) {
+      xpre = x[e];
+      wpre = w[e];
+    }
+  }
   double2 sa[EPL], sb[EPL];
 #pragma unroll
   for (int q = 0; q < EPL; ++q) sa[q] = sb[q] = make_double2(0.0, 0.0);
@@ -465,8 +475,8 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
         ta = cadd(ta, red.v[q][0][el]);
         tb = cadd(tb, red.v[q][1][el]);
       }
-      const double2 v = cadd(cscale(ib, x[e]), ta);
-      const double2 wp = csub(cadd(w[e], tb), cmul(hjj, v));
+      const double2 v = cadd(cscale(ib, ONE ? xpre : x[e]), ta);
+      const double2 wp = csub(cadd(ONE ? wpre : w[e], tb), cmul(hjj, v));
       x[e] = v;
       w[e] = wp;
       nrm = fma(wp.x, wp.x, fma(wp.y, wp.y, nrm));
