@@ -128,6 +128,11 @@ typedef struct {
                           tail of every iteration; a converged inner solve runs one discarded
                           iteration).  Same iteration counts as the immediate test on the corrected
                           column.  1 = on, 0 = off */
+  int dots_cluster;    /* inner / outer Arnoldi on one GPU: pass 1 of the delayed CGS2 sums its chunk
+                          partials on chip over 8-CTA thread-block clusters (DSMEM) and the update
+                          kernel adds the remaining 1/8 itself -- no reduction kernel.  Measured
+                          slower on B200 (the cluster pass 1 costs +5-6 us over dots + reduction:
+                          DESIGN.md §6b), so 0 (default) = the dots + reduction kernels; 1 = on */
 } helm_params;
 
 typedef struct {

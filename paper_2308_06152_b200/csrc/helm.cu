@@ -94,6 +94,8 @@ struct Fgm {
   int coop = 0;              // > 0: grid of the cooperative one-kernel DCGS2 step
   double2* npart = nullptr;  // pass-2 norm partials of the cooperative step
   double2* part = nullptr;   // max((m+2) * gx, gu) partials
+  double2* cpart = nullptr;  // (2m+4) x gxc cluster partials of pass 1 (k_dcgs_dots_cl)
+  int gxc = 0;               // clusters of DC_CL chunks (0: no cluster pass 1)
   GsGeom geo{};              // Gram-Schmidt launch geometry
   FgmState* st = nullptr;
 };
@@ -197,6 +199,27 @@ void launch_cluster(helm_ctx_s& C, void (*kern)(KArgs...), int cs, int threads, 
   attr[0].val.programmaticStreamSerializationAllowed = C.p.pdl ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = cs;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess && C.launch_err == cudaSuccess) C.launch_err = e;
+}
+
+// Launch with thread-block clusters of `clx` CTAs along x (grid.x a multiple of clx).
+template <typename... KArgs, typename... Args>
+void launch_kc(helm_ctx_s& C, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, int clx, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = C.s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = C.p.pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = clx;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -727,6 +750,10 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
 
 // ------------------------------------------------------------------ device FGMRES
 size_t dcgs_update_smem(int m) { return std::max((size_t)(2 * m + 2) * sizeof(double2), dcgs_smem(m)); }
+// k_dcgs_update's coefficient / step scratch in double2 units, and its dynamic shared memory
+// with the cluster-partial dots behind it (flags & 8)
+int dcgs_sab_len(int m) { return (int)((dcgs_update_smem(m) + 15) / 16); }
+size_t dcgs_update_smem_cl(int m) { return (size_t)dcgs_sab_len(m) * 16 + (size_t)(2 * m + 4) * sizeof(double2); }
 
 size_t dcgs_dots_smem(const Fgm& K) { return K.geo.chunk > DC_SUB ? (size_t)(2 * K.m + 4) * sizeof(double2) : 0; }
 
@@ -768,6 +795,13 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(dalloc(&K.nrm, 2));
   K.geo = gs_geom((long long)n, C.sm_count);
   CKR(dalloc(&K.part, std::max<size_t>((size_t)(2 * m + 4) * std::max(K.geo.gx, P), (size_t)K.geo.gu + 1)));
+  K.gxc = 0;
+  // every update block re-reads the (2j+2) x gxc cluster partials: only for small bases on
+  // small levels (the inner solves), where that is a few % of the basis stream
+  if (C.p.dots_cluster && !dist && m <= 64 && (K.geo.gx + DC_CL - 1) / DC_CL <= 64) {
+    K.gxc = (K.geo.gx + DC_CL - 1) / DC_CL;
+    CKR(dalloc(&K.cpart, (size_t)(2 * m + 4) * K.gxc));
+  }
   CKR(dalloc(&K.st, 1));
   CK(cudaMemsetAsync(K.st, 0, sizeof(FgmState), C.s));
   // dynamic shared memory grows with the basis; the limits are raised once to the largest
@@ -777,8 +811,9 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   const size_t dsmem = (size_t)(2 * m + 4) * sizeof(double2);
   const size_t asmem = dcgs_smem(m);
   CKR(raise_dyn_smem((const void*)k_gs_update, smem));
-  CKR(raise_dyn_smem((const void*)k_dcgs_update, usmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_update, std::max(usmem, dcgs_update_smem_cl(m))));
   CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
+  CKR(raise_dyn_smem((const void*)k_dcgs_dots_cl, dsmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_stepB, usmem));
@@ -788,7 +823,7 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   {
     // pass 2 in one wave: at most as many blocks as can be resident
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_update, DU_THREADS, dcgs_update_smem(m)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_update, DU_THREADS, dcgs_update_smem_cl(m)));
     if (bps > 0) K.geo.gu = std::max(1, std::min(K.geo.gu, bps * C.sm_count - 1));   // + the step-A block
   }
   // cooperative one-kernel step for small vectors (latency-bound regime)
@@ -820,6 +855,7 @@ void fgm_free(Fgm& K) {
   cudaFree(K.rawc);
   cudaFree(K.nrm);
   cudaFree(K.part);
+  cudaFree(K.cpart);
   cudaFree(K.cnt);
   cudaFree(K.npart);
   cudaFree(K.st);
@@ -960,7 +996,13 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
                   gg.gy, K.part, K.npart, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, h, use_h);
       return post_launch(C);
     }
-    if (!(fuse && K.coop == 0)) {
+    // pass 1 with on-chip cluster sums (no reduction kernel): single GPU, unfused
+    const bool cld = K.gxc > 0 && !K.dist && !fuse;
+    if (cld) {
+      launch_kc(C, k_dcgs_dots_cl, dim3(K.gxc * DC_CL, gg.gy), DC_THREADS, (size_t)(2 * K.m + 4) * sizeof(double2),
+                DC_CL, Vo, ld, &st->j, 1, vjo, wo, ln, gg.chunk, K.cpart);
+      CKR(post_launch(C));
+    } else if (!(fuse && K.coop == 0)) {
       launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
                gg.chunk, K.part);
       CKR(post_launch(C));
@@ -982,13 +1024,16 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
                K.rawc, h, use_h, C.peers, C.rank, C.nranks, C.playout.red);
       return post_launch(C);
     }
-    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, nparts, st, K.H,
-             K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
-    CKR(post_launch(C));
+    if (!cld) {
+      launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, nparts, st, K.H,
+               K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
+      CKR(post_launch(C));
+    }
     if (K.dist) CKR(allreduce(C, K.dots1, 2 * K.m + 2));
-    launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), Vo, ld, (const int*)&st->j,
-             (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1, h, use_h,
-             K.dist ? 2 : (lag ? 7 : 3));
+    launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), Vo, ld,
+             (const int*)&st->j, (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
+             K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0), (const double2*)K.cpart, K.gxc,
+             dcgs_sab_len(K.m));
     CKR(post_launch(C));
     if (K.dist) {
       launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu + 1, K.nrm);
@@ -1198,6 +1243,7 @@ void helm_default_params(helm_params* p) {
   p->gamma = 1.0;
   p->tail_cluster = 0;
   p->lag_stepb = 1;
+  p->dots_cluster = 0;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1816,23 +1862,31 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         // probe: HELM_GB_DCGS_MASK selects the step's kernels (1 dots, 2 reduceA, 4 update; default 7)
         const char* mk = getenv("HELM_GB_DCGS_MASK");
         const int mask = mk ? atoi(mk) : 7;
-        if (mask & 1) {
+        const bool cld = K.gxc > 0;
+        if ((mask & 1) && cld) {
+          launch_kc(X, k_dcgs_dots_cl, dim3(K.gxc * DC_CL, gg.gy), DC_THREADS, (size_t)(2 * K.m + 4) * sizeof(double2),
+                    DC_CL, K.V, ln, (const int*)&st->j, 1, vj, w, ln, gg.chunk, K.cpart);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+        } else if (mask & 1) {
           launch_k(X, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, (const int*)&st->j, 1,
                    vj, w, ln, gg.chunk, K.part);
           r = post_launch(X);
           if (r != HELM_OK) break;
         }
-        if (mask & 2) {
+        if ((mask & 2) && !cld) {
           launch_k(X, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, dcgs_smem(K.m), K.part,
                    (long long)gg.gx, st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
           r = post_launch(X);
           if (r != HELM_OK) break;
         }
         if (!(mask & 4)) break;
-        launch_k(X, k_dcgs_update, gg.gu + 1, DU_THREADS, dcgs_update_smem(K.m), K.V, ln, (const int*)&st->j,
-                 (const double2*)K.dots1, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1,
-                 cudaGraphConditionalHandle(0), 0,
-                 getenv("HELM_GB_UPD_FLAGS") ? atoi(getenv("HELM_GB_UPD_FLAGS")) : (X.p.lag_stepb ? 7 : 3));
+        launch_k(X, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), K.V,
+                 ln, (const int*)&st->j, (const double2*)K.dots1, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
+                 K.cnt + 1, cudaGraphConditionalHandle(0), 0,
+                 (getenv("HELM_GB_UPD_FLAGS") ? atoi(getenv("HELM_GB_UPD_FLAGS")) : (X.p.lag_stepb ? 7 : 3)) |
+                     (cld ? 8 : 0),
+                 (const double2*)K.cpart, K.gxc, dcgs_sab_len(K.m));
         r = post_launch(X);
         break;
       }
@@ -1944,7 +1998,7 @@ int helm_bench_kernel(helm_ctx C, int which, int arg, int reps, int flush, doubl
         k_dcgs_update<<<K.geo.gu, DU_THREADS, dcgs_update_smem(K.m), X.s>>>(
             K.V, (long long)K.n, dn, K.dots1, DVec(K.V + (size_t)(arg - 1) * K.n), DVec(K.V + (size_t)arg * K.n),
             (long long)K.n, K.part, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-            cudaGraphConditionalHandle(0), 0, 0);
+            cudaGraphConditionalHandle(0), 0, 0, (const double2*)nullptr, 0, 0);
         return post_launch(X);
       }
     }

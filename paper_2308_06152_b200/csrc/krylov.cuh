@@ -288,13 +288,14 @@ __device__ __forceinline__ void dcgs_dots_item(const double2* __restrict__ V, lo
                                                const double2* __restrict__ x, double xs,
                                                const double2* __restrict__ w, long long n, long long chunk,
                                                double2* __restrict__ part, int gx, int bx, int y, int gy,
-                                               double2* dacc) {
+                                               double2* dacc, bool to_smem = false) {
   const long long e0 = (long long)bx * chunk;
   const long long e1 = min(n, e0 + chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cstep = gy * DC_WARPS;
   const int c0 = y * DC_WARPS + warp;
-  const bool multi = (e1 - e0) > DC_SUB;
+  // to_smem: the block's sums stay in dacc (zeroed here) for a cluster reduction
+  const bool multi = to_smem || (e1 - e0) > DC_SUB;
   if (multi) {
     for (int c = threadIdx.x; c < 2 * nvec; c += DC_THREADS) dacc[c] = make_double2(0.0, 0.0);
     __syncthreads();
@@ -362,7 +363,7 @@ __device__ __forceinline__ void dcgs_dots_item(const double2* __restrict__ V, lo
       }
     }
   }
-  if (multi) {
+  if (multi && !to_smem) {
     __syncthreads();
     for (int c = threadIdx.x; c < 2 * nvec; c += DC_THREADS) part[(long long)c * gx + bx] = dacc[c];
     __syncthreads();
@@ -387,6 +388,38 @@ __global__ void __launch_bounds__(DC_THREADS, HELM_DC_MINB) k_dcgs_dots(const do
   const int nvec = (nptr ? *nptr : 0) + nadd;
   dcgs_dots_item(V, ld, nvec, xv.get(), xv.scale(), wv.get(), n, chunk, part, gridDim.x, blockIdx.x, blockIdx.y,
                  gridDim.y, dacc);
+}
+
+// Pass 1 with the chunk sums of DC_CL consecutive chunks added on chip: the blocks of a
+// thread-block cluster (DC_CL chunks of one vector slice) keep their sums in shared memory and,
+// after a cluster barrier, each block adds a share of the values over the cluster's ranks
+// (DSMEM, rank order) into part[c * (gridDim.x / DC_CL) + cluster].  DC_CL x fewer partials,
+// so the update kernel sums them itself (k_dcgs_update flags & 8) and the reduction kernel
+// disappears from the step.  Chunks past n (grid padded to whole clusters) contribute zeros.
+constexpr int DC_CL = 8;
+__global__ void __launch_bounds__(DC_THREADS, HELM_DC_MINB) k_dcgs_dots_cl(const double2* __restrict__ V, long long ld,
+                                                             const int* __restrict__ nptr, int nadd, DVec xv,
+                                                             DVec wv, long long n, long long chunk,
+                                                             double2* __restrict__ part) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 dacc[];
+  const int nvec = (nptr ? *nptr : 0) + nadd;
+  dcgs_dots_item(V, ld, nvec, xv.get(), xv.scale(), wv.get(), n, chunk, part, gridDim.x, blockIdx.x, blockIdx.y,
+                 gridDim.y, dacc, true);
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const int r = (int)cl.block_rank();
+  const int cstep = gridDim.y * DC_WARPS;
+  const int gxc = gridDim.x / DC_CL, cx = blockIdx.x / DC_CL;
+  for (int q = r * DC_THREADS + threadIdx.x; q < 2 * nvec; q += DC_CL * DC_THREADS) {
+    const int c = q >> 1;
+    if ((c % cstep) / DC_WARPS != (int)blockIdx.y) continue;   // another slice owns vector c
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int rr = 0; rr < DC_CL; ++rr) t = cadd(t, cl.map_shared_rank(dacc, rr)[q]);
+    part[(long long)q * gxc + cx] = t;
+  }
+  cl.sync();   // the peers' shared memory stays alive until every rank has read it
 }
 
 // Pass 2 of iteration j (j = *jptr): with coef[2c] = -a_c/beta, coef[2c+1] = -b_c (c < j)
@@ -498,14 +531,39 @@ __global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const 
                                                             long long n, double2* __restrict__ part,
                                                             FgmState* st, double2* H, double* cs, double2* sn,
                                                             double2* g, double2* __restrict__ rawc, unsigned* counter,
-                                                            cudaGraphConditionalHandle hcond, int use_h, int flags) {
+                                                            cudaGraphConditionalHandle hcond, int use_h, int flags,
+                                                            const double2* __restrict__ dpart, int np1, int sab_len) {
   HELM_PDL_ENTRY();
   extern __shared__ double2 sab[];
   __shared__ DuRed<DU_WARPS, DU_ELEMS / 32> red;
   __shared__ double s_beta;
   __shared__ double2 s_hjj;
   const int j = *jptr;
+  if (flags & 8) {
+    // the pass-1 dots from the cluster partials (k_dcgs_dots_cl): 8 threads per value, each
+    // adding a fixed share of the np1 partials, combined in a fixed shuffle order
+    double2* sd = sab + sab_len;
+    const int nd = 2 * j + 2;
+    const int sub = threadIdx.x & 7;
+    for (int q0 = 0; q0 < nd; q0 += DU_THREADS / 8) {
+      const int q = q0 + (threadIdx.x >> 3);
+      double2 t = make_double2(0.0, 0.0);
+      if (q < nd) {
+        const double2* pq = dpart + (long long)q * np1;
+        for (int b = sub; b < np1; b += 8) t = cadd(t, pq[b]);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        t.x += __shfl_xor_sync(0xffffffffu, t.x, o, 8);
+        t.y += __shfl_xor_sync(0xffffffffu, t.y, o, 8);
+      }
+      if (q < nd && sub == 0) sd[q] = t;
+    }
+    __syncthreads();
+    dots = sd;
+  }
   if (threadIdx.x < 32) dcgs_coefs_warp(j, dots, sab, &s_beta, &s_hjj);
+
   __syncthreads();
   // the extra block is block 0, so that it is scheduled first
   const bool extra = (flags & 2) && blockIdx.x == 0;

@@ -37,7 +37,7 @@ class helm_params(ctypes.Structure):
                 ("col_min_n", ctypes.c_int), ("dist_levels", ctypes.c_int), ("dist_min_rows", ctypes.c_int),
                 ("col_pipe", ctypes.c_int), ("fuse_dots", ctypes.c_int), ("precond", ctypes.c_int),
                 ("gamma", ctypes.c_double), ("tail_cluster", ctypes.c_int),
-                ("lag_stepb", ctypes.c_int)]
+                ("lag_stepb", ctypes.c_int), ("dots_cluster", ctypes.c_int)]
 
 
 class helm_dist(ctypes.Structure):

@@ -425,3 +425,19 @@ def test_lagged_stepb_counts(lib, name, vec, op, itol):
         assert abs(r["inner_iterations_total"] - sum(its_o[:r["outer_iterations"]])) <= max(2, n // 10), (r, its_o)
         assert r["inner_iterations_max"] <= max(its_o) + 1
     assert reps[0]["outer_iterations"] == reps[1]["outer_iterations"]
+
+
+def test_dots_cluster_option(lib):
+    """helm_params.dots_cluster (pass 1 summed over thread-block clusters, no reduction kernel;
+    off by default): same outer / inner counts as the oracle (+-1, R13), true residual met."""
+    p = _problem("c1_k50")
+    prm = {"coarse_op": "galerkin", "vectors": "high_order", "inner_tol": 1e-1, "inner_maxit": 50}
+    so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op="galerkin", vectors="high_order", inner_tol=1e-1,
+                                                           inner_maxit=50, maxit=400))
+    xo, rep_o = so.solve(p.b)
+    H = lib.helm_setup(p, dict(prm, dots_cluster=1))
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=400)
+    assert rep["converged"] and abs(rep["outer_iterations"] - rep_o["outer_iterations"]) <= 1
+    assert abs(rep["inner_iterations_total"] - sum(rep_o["inner_iterations"][:rep["outer_iterations"]])) <= 2
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    H.close()
