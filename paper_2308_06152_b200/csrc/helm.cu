@@ -811,14 +811,16 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   const size_t dsmem = (size_t)(2 * m + 4) * sizeof(double2);
   const size_t asmem = dcgs_smem(m);
   CKR(raise_dyn_smem((const void*)k_gs_update, smem));
-  CKR(raise_dyn_smem((const void*)k_dcgs_update, std::max(usmem, dcgs_update_smem_cl(m))));
+  CKR(raise_dyn_smem((const void*)k_dcgs_update, K.gxc > 0 ? std::max(usmem, dcgs_update_smem_cl(m)) : usmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
-  CKR(raise_dyn_smem((const void*)k_dcgs_dots_cl, dsmem));
+  if (K.gxc > 0) CKR(raise_dyn_smem((const void*)k_dcgs_dots_cl, dsmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_reduceA, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_step, asmem));
   CKR(raise_dyn_smem((const void*)k_dcgs_stepB, usmem));
-  CKR(raise_dyn_smem((const void*)k_dcgs_stepB_peer, usmem));
-  CKR(raise_dyn_smem((const void*)k_dcgs_update_peer, dcgs_update_smem_dev(m) + (size_t)(2 * m + 4) * sizeof(double2)));
+  if (dist && C.kind == HELM_COMM_PEER) {   // the peer transport's fused step kernels only
+    CKR(raise_dyn_smem((const void*)k_dcgs_stepB_peer, usmem));
+    CKR(raise_dyn_smem((const void*)k_dcgs_update_peer, dcgs_update_smem_dev(m) + (size_t)(2 * m + 4) * sizeof(double2)));
+  }
   CKR(raise_dyn_smem((const void*)k_fgm_backsub, std::min<size_t>(96 * 1024, ((size_t)m * (m + 1) + m) * 16)));
   {
     // pass 1 in one wave: vector slices only while the chunks leave resident slots empty
@@ -831,7 +833,8 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   {
     // pass 2 in one wave: at most as many blocks as can be resident
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_update, DU_THREADS, dcgs_update_smem_cl(m)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_update, DU_THREADS,
+                                                     K.gxc > 0 ? dcgs_update_smem_cl(m) : dcgs_update_smem(m)));
     if (bps > 0) K.geo.gu = std::max(1, std::min(K.geo.gu, bps * C.sm_count - 1));   // + the step-A block
   }
   // cooperative one-kernel step for small vectors (latency-bound regime)

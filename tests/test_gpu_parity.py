@@ -441,3 +441,15 @@ def test_dots_cluster_option(lib):
     assert abs(rep["inner_iterations_total"] - sum(rep_o["inner_iterations"][:rep["outer_iterations"]])) <= 2
     assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
     H.close()
+
+
+def test_large_inner_basis_setup(lib):
+    """A 3000-column inner basis (Tables 1-2 runs: coarse solve to 1e-8) sets up on one
+    GPU: only the kernels the context can launch get their shared-memory limits raised (the
+    peer transport's fused step kernels, the cluster pass 1 are not this context's)."""
+    p = _problem("c0_tiny")
+    H = lib.helm_setup(p, {"coarse_op": "galerkin", "vectors": "bilinear", "inner_tol": 1e-8, "inner_maxit": 3000})
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=100)
+    assert rep["converged"]
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    H.close()
