@@ -707,7 +707,12 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
     if (gather) CKR(allgather(C, l + 1));
     CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
     // no halo for Gs.u: a V-cycle output is valid on its owned rows +- 4 (fresh ghosts, below)
-    if (small) {
+#ifndef HELM_UP_SMALL_X   // up leg: small tiles also while the big up tiles are < X waves (0: as the down leg)
+#define HELM_UP_SMALL_X 0
+#endif
+    const bool small_up = small || (size_t)((L.g.nx + UP_TX - 1) / UP_TX) * ((L.g.ny + UP_TY - 1) / UP_TY) <
+                                       (size_t)HELM_UP_SMALL_X * C.sm_count;
+    if (small_up) {
       dim3 gu((L.g.nx + 15) / 16, (L.g.ny + 7) / 8);
       launch_k(C, k_vc_up<16, 8>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
     } else {
