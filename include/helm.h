@@ -114,8 +114,10 @@ typedef struct {
                           segments of 256 (down) / 128 (up) rows; 3, 4, 5, 14, 24: other depths /
                           segment lengths (measurement) */
   int fuse_dots;       /* 1: with str-Glk, the inner FGMRES applies E and pass 1 of the delayed CGS2
-                          (the dots against the basis) in one kernel; measured slower on B200
-                          than the two kernels (0.577 vs 0.568 s per bench solve), so 0 (default) */
+                          (the dots against the basis) in one kernel.  Measured slower on B200
+                          than the two kernels early in round 1 (0.577 vs 0.568 s per bench
+                          solve).  With the final round-1 step (lagged step B, one-wave pass 1)
+                          it is 1.4 % faster (0.506 vs 0.513 s); 0 (default) this round */
   int precond;         /* HELM_PRECOND_ADEF1 (default; A-DEF1, or APD with the higher-order vectors)
                           or HELM_PRECOND_TLKM (practical two-level Krylov method, §3.2.2
                           and Tables 1-2: coarse matrix Z^T Z M_2h^-1 A_2h solved by unpreconditioned
