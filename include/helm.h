@@ -117,7 +117,7 @@ typedef struct {
                           (the dots against the basis) in one kernel.  Measured slower on B200
                           than the two kernels early in round 1 (0.577 vs 0.568 s per bench
                           solve).  With the final round-1 step (lagged step B, one-wave pass 1)
-                          it is 1.4 % faster (0.506 vs 0.513 s); 0 (default) this round */
+                          it is 1.4 % faster (0.506 vs 0.513 s), so 1 (default) */
   int precond;         /* HELM_PRECOND_ADEF1 (default; A-DEF1, or APD with the higher-order vectors)
                           or HELM_PRECOND_TLKM (practical two-level Krylov method, §3.2.2
                           and Tables 1-2: coarse matrix Z^T Z M_2h^-1 A_2h solved by unpreconditioned

@@ -1254,7 +1254,7 @@ void helm_default_params(helm_params* p) {
   p->dist_levels = 0;
   p->dist_min_rows = 16;
   p->col_pipe = 1;
-  p->fuse_dots = 0;
+  p->fuse_dots = 1;
   p->precond = HELM_PRECOND_ADEF1;
   p->gamma = 1.0;
   p->tail_cluster = 0;
