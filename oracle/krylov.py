@@ -16,23 +16,51 @@ tolerance-stopped inner solve the integer inner iteration counts are decided by 
 (tests show MGS and CGS2 differ there), so both sides use CGS2; orth="mgs" keeps the
 literal Algorithm-1 loop, and a pin checks that the two agree when the decisions are not
 rounding-sensitive.
+
+Restarts (reading R25): Algorithm 1 is written for a full Krylov basis ("for
+j = 1, ..., m" followed by "if not converged, restart with u_0 = u_m" is the textbook GMRES(m)
+of Saad & Schultz 1986 that Algorithm 1's "m" denotes).  `restart = m > 0` runs FGMRES(m):
+cycles of at most m Arnoldi steps, each started from the current iterate with r = b - A x and
+v_1 = r/||r||, the iterate updated x := x + Z_m y_m at the end of every cycle.  The stopping
+test stays ||r||/||b|| <= tol against the ORIGINAL ||b||, and `maxit` counts iterations over
+all cycles.  restart = 0 (or >= maxit) is the full method.
 """
 from __future__ import annotations
 
 import numpy as np
 
 
-def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, history=None, orth="cgs2"):
-    """Solve A x = b.  Returns (x, iterations, converged)."""
+def fgmres(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, history=None, orth="cgs2",
+           restart: int = 0):
+    """Solve A x = b.  Returns (x, iterations, converged).  restart = m > 0: FGMRES(m) (R25)."""
+    if restart and restart < maxit:
+        return _fgmres_restarted(apply_A, apply_P, b, tol, maxit, restart, x0, history, orth)
+    return _fgmres_cycle(apply_A, apply_P, b, tol, maxit, x0, history, orth, np.linalg.norm(b.ravel()))
+
+
+def _fgmres_restarted(apply_A, apply_P, b, tol, maxit, m, x0, history, orth):
+    """FGMRES(m): cycles of <= m steps from the current iterate, tol against the original ||b||."""
+    bnorm = np.linalg.norm(b.ravel())
+    x = x0
+    its_total = 0
+    while True:
+        x, its, conv = _fgmres_cycle(apply_A, apply_P, b, tol, min(m, maxit - its_total), x, history, orth, bnorm,
+                                     first=its_total == 0)
+        its_total += its
+        if conv or its == 0 or its_total >= maxit:
+            return x, its_total, conv
+
+
+def _fgmres_cycle(apply_A, apply_P, b, tol, maxit, x0, history, orth, bnorm, first=True):
+    """One FGMRES cycle of at most maxit steps from x0 (None = 0); relres against bnorm."""
     shape = b.shape
     bvec = b.ravel()
-    bnorm = np.linalg.norm(bvec)
     x = np.zeros_like(bvec) if x0 is None else x0.ravel().astype(np.complex128).copy()
     if bnorm == 0.0:
         return x.reshape(shape), 0, True
     r = bvec - apply_A(x.reshape(shape)).ravel() if x0 is not None else bvec.copy()
     beta = np.linalg.norm(r)
-    if history is not None:
+    if history is not None and first:
         history.append(beta / bnorm)
     if beta / bnorm <= tol:
         return x.reshape(shape), 0, True

@@ -20,6 +20,9 @@ Readings:
   R11 The coarse problem E e = c is solved by right-preconditioned FGMRES from e = 0 to the
       relative residual inner_tol, preconditioned by one CSLP V-cycle starting at level 1
       of the CSLP hierarchy (mesh 2h); inner_solver="direct" replaces it by a dense solve.
+  R25 inner_restart = m > 0 makes that coarse solve FGMRES(m) (restarted from the current
+      iterate every m steps, tolerance against ||c||, inner_maxit over all cycles); restart = m
+      does the same for the outer FGMRES (oracle/krylov.py).
   R12 Outer FGMRES from u0 = 0 stops at ||b - A u||/||b|| <= tol (right preconditioning:
       the Arnoldi residual is the true residual).
   R15 inner_tol = 0 runs exactly inner_maxit inner iterations (a fixed polynomial
@@ -61,6 +64,8 @@ class SolverParams:
     inner_solver: str = "fgmres"      # fgmres | direct
     inner_tol: float = 1e-1           # 0 -> fixed inner_maxit iterations (reading R15)
     inner_maxit: int = 200
+    inner_restart: int = 0            # coarse solve FGMRES(m); 0 = full basis (reading R25)
+    restart: int = 0                  # outer FGMRES(m); 0 = full basis (reading R25)
     orth: str = "cgs2"                # cgs2 | mgs (reading R13)
     tol: float = 1e-6
     maxit: int = 600
@@ -122,7 +127,7 @@ class Solver:
                 self._Elu = scipy.linalg.lu_factor(self.E_dense())
             return scipy.linalg.lu_solve(self._Elu, c.ravel()).reshape(self.cshape)
         e, its, _ = fgmres(self.E, lambda v: self.vcycle(v, 1), c, self.p.inner_tol, self.p.inner_maxit,
-                           orth=self.p.orth)
+                           orth=self.p.orth, restart=self.p.inner_restart)
         self.inner_its.append(its)
         return e
 
@@ -173,7 +178,7 @@ class Solver:
                                history=history)
         else:
             x, its, conv = fgmres(self.A, self.precond, np.asarray(b, dtype=np.complex128),
-                                  self.p.tol, self.p.maxit, history=history, orth=self.p.orth)
+                                  self.p.tol, self.p.maxit, history=history, orth=self.p.orth, restart=self.p.restart)
         t1 = time.perf_counter()
         r = np.asarray(b) - self.A(x)
         relres = np.linalg.norm(r) / np.linalg.norm(b) if np.linalg.norm(b) > 0 else 0.0

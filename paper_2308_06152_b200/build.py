@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libhelm.so")
     os.replace(LIB + ".tmp", LIB)
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(res.stderr)
+        # compile times vary run to run: keep only the resource lines (registers, smem, spills)
+        fh.write("".join(l for l in res.stderr.splitlines(True) if "Compile time" not in l))
     if verbose:
         sys.stderr.write(res.stderr)
     return LIB

@@ -158,3 +158,87 @@ def test_tlkm_composition_dense():
     P = (np.eye(n0) - M0 @ A @ Qt + 0.7 * Qt) @ M0
     v = random_field(shape, 9)
     np.testing.assert_allclose(s.tlkm(v).ravel(), P @ v.ravel(), rtol=1e-9, atol=1e-9 * np.abs(P @ v.ravel()).max())
+
+
+# ---------------------------------------------------------------- restarted FGMRES(m), reading R25
+
+def _dense_system(n, seed, shift):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + shift * np.eye(n)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    return A, b
+
+
+def test_restart_beyond_iterations_is_the_full_method():
+    """FGMRES(m) with m >= the iterations the full method needs is the full method (bitwise)."""
+    A, b = _dense_system(24, 5, 7.0)
+    x0, it0, c0 = oracle.fgmres(lambda v: A @ v, lambda v: v, b, 1e-10, 200)
+    x1, it1, c1 = oracle.fgmres(lambda v: A @ v, lambda v: v, b, 1e-10, 200, restart=it0)
+    assert c0 and c1 and it0 == it1
+    assert np.array_equal(x0, x1)
+
+
+def test_restart_one_is_the_minimal_residual_iteration():
+    """GMRES(1) is the minimal-residual iteration (Saad, Iterative Methods §5.3.2, closed form):
+    alpha = (A r, r) / (A r, A r), x += alpha r, r -= alpha A r."""
+    A, b = _dense_system(16, 6, 9.0)
+    x, its, conv = oracle.fgmres(lambda v: A @ v, lambda v: v, b, 0.0, 7, restart=1)
+    xm = np.zeros(16, complex)
+    r = b.copy()
+    for _ in range(7):
+        ar = A @ r
+        alpha = np.vdot(ar, r) / np.vdot(ar, ar)
+        xm = xm + alpha * r
+        r = r - alpha * ar
+    assert its == 7 and not conv
+    np.testing.assert_allclose(x, xm, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("m", [2, 3])
+def test_flexible_restart_cycles_minimise_over_preconditioned_krylov(m):
+    """With a fixed preconditioner P, each FGMRES(m) cycle from x minimises ||b - A(x + P K c)||
+    over K = [r, (AP) r, ..., (AP)^{m-1} r] (right-preconditioned GMRES; Saad 1993 flexible
+    GMRES reduces to it for constant P).  Reference: dense least squares per cycle."""
+    A, b = _dense_system(20, 7, 5.0)
+    rng = np.random.default_rng(8)
+    P = np.eye(20) + 0.1 * (rng.standard_normal((20, 20)) + 1j * rng.standard_normal((20, 20)))
+    ncyc = 4
+    x, its, conv = oracle.fgmres(lambda v: A @ v, lambda v: P @ v, b, 0.0, m * ncyc, restart=m)
+    xr = np.zeros(20, complex)
+    for _ in range(ncyc):
+        r = b - A @ xr
+        K = [r]
+        for _i in range(m - 1):
+            K.append(A @ (P @ K[-1]))
+        PK = P @ np.array(K).T
+        c = np.linalg.lstsq(A @ PK, r, rcond=None)[0]
+        xr = xr + PK @ c
+    assert its == m * ncyc
+    np.testing.assert_allclose(x, xr, rtol=1e-9, atol=1e-12)
+
+
+def test_restarted_converges_to_dense_solution_with_original_norm():
+    """A positive-real system (Hermitian part positive definite): GMRES(m) converges for every m
+    (Elman 1982).  The stop is relative to the ORIGINAL ||b||: the true residual of the result
+    meets tol * ||b||."""
+    A, b = _dense_system(30, 9, 12.0)
+    hist = []
+    x, its, conv = oracle.fgmres(lambda v: A @ v, lambda v: v, b, 1e-9, 500, restart=3, history=hist)
+    assert conv and its > 3
+    assert np.linalg.norm(b - A @ x) <= 1e-9 * np.linalg.norm(b) * (1 + 1e-6)
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-7)
+    assert len(hist) == its + 1 and hist[-1] <= 1e-9
+
+
+def test_restarted_inner_solve_in_the_solver():
+    """The restarted coarse solve is used by the solver (inner_restart) and still meets the
+    outer tolerance; with inner_restart >= inner_maxit it is the unrestarted method bitwise."""
+    p = mp_problem(12.0, 16, "sommerfeld")
+    base = dict(vectors="high_order", inner_tol=1e-6, inner_maxit=40, tol=1e-8)
+    x0, r0 = oracle.solve(p, oracle.SolverParams(**base))
+    x1, r1 = oracle.solve(p, oracle.SolverParams(**base, inner_restart=40))
+    assert np.array_equal(x0, x1) and r0["inner_iterations"] == r1["inner_iterations"]
+    x2, r2 = oracle.solve(p, oracle.SolverParams(**base, inner_restart=4))
+    assert r2["converged"] and r2["relres"] <= 1e-8
+    assert max(r2["inner_iterations"]) > 4
+    np.testing.assert_allclose(x2, x0, rtol=0, atol=1e-6 * np.abs(x0).max())
