@@ -135,6 +135,11 @@ typedef struct {
                           kernel adds the remaining 1/8 itself -- no reduction kernel.  Measured
                           slower on B200 (the cluster pass 1 costs +5-6 us over dots + reduction:
                           DESIGN.md §6b), so 0 (default) = the dots + reduction kernels; 1 = on */
+  int inner_restart;   /* coarse solve as FGMRES(m) (reading R25): m > 0 restarts the inner
+                          Arnoldi process from the current iterate every m steps (basis of m + 1
+                          level-1 vectors, Gram-Schmidt cost O(m) per step), the tolerance stays
+                          relative to ||c|| and inner_maxit counts steps over all cycles; 0 (default)
+                          or m >= inner_maxit = one full cycle.  A-DEF1/APD only (TLKM: 0) */
 } helm_params;
 
 typedef struct {
@@ -147,6 +152,7 @@ typedef struct {
   int restarts;
   double seconds;         /* host wall time of the solve (stream synchronised) */
   long long kernels;      /* kernels executed by the solve (graph replays counted per node run) */
+  long long inner_restarts; /* restart cycles of the coarse solves (params.inner_restart), summed */
 } helm_report;
 
 void helm_default_params(helm_params* p);

@@ -136,8 +136,11 @@ struct helm_ctx_s {
   int g_maxit = -1;
   // kernels captured per region (graph replays execute a data-dependent number of them)
   long long body_launches[4] = {0, 0, 0, 0};
-  long long cnt_top = 0, cnt_outer = 0, cnt_inner = 0;
-  long long cnt[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  long long cnt_top = 0, cnt_outer = 0, cnt_inner = 0, cnt_restart = 0;
+  long long cnt[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  long long last_body = 0;        // kernels in the body of the last captured while loop
+  long long inner_iter_body = 0;  // ... of one inner Arnoldi step; of one inner restart cycle
+  long long inner_restart_body = 0;  // (excluding its nested Arnoldi loop body)
   // row-strip decomposition over ranks (dist.cuh); dist == 0: single GPU
   int dist = 0, kind = -1, rank = 0, nranks = 1, D = -1;
   bool x1 = false;                     // HELM_DIST_EXCHANGE_AT_ONE_RANK (peer transport tests)
@@ -947,6 +950,7 @@ int run_while(helm_ctx_s& C, FgmState* st, Begin&& begin, Body&& body) {
   const long long l0 = C.launches;
   int r = body(h, 1);
   C.body_launches[d] += C.launches - l0;
+  C.last_body = C.launches - l0;
   C.depth--;
   C.s = saved;
   cudaGraph_t outg;
@@ -1072,15 +1076,32 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
 }
 
 // e = E^{-1} c on level 1 by CSLP(V-cycle from level 1)-preconditioned FGMRES from e = 0
-// (reading R11), no restart (capacity inner_maxit, as the oracle).
+// (reading R11).  inner_restart = m < inner_maxit: FGMRES(m) (reading R25) -- the first cycle
+// from e = 0, then a device-controlled while loop of restart cycles from the current e
+// (r = c - E e) until converged against ||c|| or inner_maxit steps in total.
 int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_stats) {
   Fgm& K = C.inner;
   launch_k(C, k_fgm_reset, 1, 1, 0, K.st, C.p.inner_tol, C.p.inner_maxit, K.m);
   CKR(post_launch(C));
-  // x is z_j (a V-cycle output, fresh ghosts) in the Arnoldi step; restarts do not occur here
+  // x is z_j (a V-cycle output, fresh ghosts) in the Arnoldi step; a restart's residual reads e
+  // (updated on the owned rows only: halo exchange)
   auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y, f.p == nullptr); };
   auto opP = [&](DVec v, DVec z) { return vcycle(C, 1, v, z, nullptr); };
-  return fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C));
+  CKR(fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C)));
+  C.inner_iter_body = C.last_body;
+  if (K.m >= C.p.inner_maxit) return HELM_OK;
+  auto rbegin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    launch_k(C, k_fgm_restart_cond, 1, 32, 0, K.st, outer_stats, h, use_h);
+    return post_launch(C);
+  };
+  auto rbody = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    CKR(fgmres_cycle(C, K, opA, opP, DVec(c), e, false, outer_stats, fused_E_dots(C)));
+    launch_k(C, k_fgm_restart_cond, 1, 32, 0, K.st, outer_stats, h, use_h);
+    return post_launch(C);
+  };
+  CKR(run_while(C, K.st, rbegin, rbody));
+  C.inner_restart_body = C.last_body - C.inner_iter_body;
+  return HELM_OK;
 }
 
 // Practical TLKM (§3.2.2, :385-406, Tables 1-2; oracle/solver.py Solver.tlkm, reading
@@ -1260,6 +1281,7 @@ void helm_default_params(helm_params* p) {
   p->tail_cluster = 0;
   p->lag_stepb = 1;
   p->dots_cluster = 0;
+  p->inner_restart = 0;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1324,6 +1346,9 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
   if (p.max_levels < 2) return fail(HELM_EINVAL, "max_levels must be >= 2");
   if (p.nu_pre < 1 || p.nu_post < 0) return fail(HELM_EINVAL, "nu_pre >= 1, nu_post >= 0");
   if (p.inner_maxit < 1) return fail(HELM_EINVAL, "inner_maxit >= 1");
+  if (p.inner_restart < 0) return fail(HELM_EINVAL, "inner_restart >= 0");
+  if (p.inner_restart > 0 && p.inner_restart < p.inner_maxit && p.precond == HELM_PRECOND_TLKM)
+    return fail(HELM_EINVAL, "inner_restart is available for A-DEF1/APD only");
   if (p.outer != HELM_OUTER_FGMRES && p.outer != HELM_OUTER_GCR) return fail(HELM_EINVAL, "bad outer %d", p.outer);
   if (p.precond != HELM_PRECOND_ADEF1 && p.precond != HELM_PRECOND_TLKM) return fail(HELM_EINVAL, "bad precond %d", p.precond);
   if (p.precond == HELM_PRECOND_TLKM && C.dist) return fail(HELM_EINVAL, "TLKM is not available on a decomposed context");
@@ -1543,11 +1568,13 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     for (double2* b : {C.dq, C.dt, C.bbuf, C.xbuf, C.rbuf}) CK(cudaMemsetAsync(b, 0, C.L[0].n * sizeof(double2), C.s));
     for (double2* b : {C.cc, C.ce}) CK(cudaMemsetAsync(b, 0, C.L[1].n * sizeof(double2), C.s));
   }
-  // inner FGMRES: full (unrestarted) basis of inner_maxit columns, as the oracle (reading R11)
+  // inner FGMRES: a basis of inner_maxit columns (one full cycle, reading R11), or of
+  // inner_restart columns for FGMRES(m) (reading R25)
   {
     const Level& G1 = C.L[1];
     const dim3 gt = glk_tiles(C);
-    CKR(fgm_alloc(C, C.inner, p.inner_maxit, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
+    const int im = p.inner_restart > 0 ? std::min(p.inner_restart, p.inner_maxit) : p.inner_maxit;
+    CKR(fgm_alloc(C, C.inner, im, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
                   rank_summed(C) && G1.block, fused_E_dots(C) ? (int)(gt.x * gt.y) : 0));
   }
   CK(cudaStreamSynchronize(C.s));
@@ -1675,6 +1702,7 @@ int helm_deflate(helm_ctx C, const double* v, double* z, int* inner_its) {
 static int capture_cycle(helm_ctx_s& C, bool first, cudaGraphExec_t* out) {
   C.capturing = true;
   C.body_launches[0] = C.body_launches[1] = 0;
+  C.inner_iter_body = C.inner_restart_body = 0;
   CK(cudaStreamBeginCapture(C.s, cudaStreamCaptureModeRelaxed));
   const long long l0 = C.launches;
   int r = outer_cycle(C, first);
@@ -1691,7 +1719,9 @@ static int capture_cycle(helm_ctx_s& C, bool first, cudaGraphExec_t* out) {
   // kernels per replay = top + outer_its * (outer body excl. inner loop) + inner_its * inner body
   C.cnt_top = total - C.body_launches[0];
   C.cnt_outer = C.body_launches[0] - C.body_launches[1];
-  C.cnt_inner = C.body_launches[1];
+  // depth 1 holds the first inner cycle's Arnoldi body and (restarted inner) the restart body
+  C.cnt_inner = C.inner_iter_body ? C.inner_iter_body : C.body_launches[1];
+  C.cnt_restart = C.inner_restart_body;
   if (getenv("HELM_DEBUG_COUNTS"))
     fprintf(stderr, "[helm] captured kernels: total %lld top %lld outer-body %lld inner-body %lld\n", total, C.cnt_top,
             C.cnt_outer, C.cnt_inner);
@@ -1723,12 +1753,15 @@ static int solve_device(helm_ctx_s& C, double tol, int maxit, helm_report* rep) 
         C.cnt[gi][0] = C.cnt_top;
         C.cnt[gi][1] = C.cnt_outer;
         C.cnt[gi][2] = C.cnt_inner;
+        C.cnt[gi][3] = C.cnt_restart;
       }
       const int its0 = cycles == 0 ? 0 : C.hst->its;
       const long long in0 = cycles == 0 ? 0 : C.hst->inner_total;
+      const long long rs0 = cycles == 0 ? 0 : C.hst->inner_restarts;
       CK(cudaGraphLaunch(C.gexec[gi], C.s));
       CKR(read_state(C, C.outer.st));
-      kernels += C.cnt[gi][0] + (C.hst->its - its0) * C.cnt[gi][1] + (C.hst->inner_total - in0) * C.cnt[gi][2];
+      kernels += C.cnt[gi][0] + (C.hst->its - its0) * C.cnt[gi][1] + (C.hst->inner_total - in0) * C.cnt[gi][2] +
+                 (C.hst->inner_restarts - rs0) * C.cnt[gi][3];
     } else {
       const long long l0 = C.launches;
       CKR(outer_cycle(C, first));
@@ -1752,6 +1785,7 @@ static int solve_device(helm_ctx_s& C, double tol, int maxit, helm_report* rep) 
     rep->inner_iterations_total = s.inner_total;
     rep->inner_iterations_max = s.inner_max;
     rep->restarts = cycles - 1;
+    rep->inner_restarts = s.inner_restarts;
     rep->seconds = std::chrono::duration<double>(t1 - t0).count();
     rep->kernels = kernels;
   }

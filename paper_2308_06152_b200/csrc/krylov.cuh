@@ -47,6 +47,7 @@ struct FgmState {
   // inner-solve statistics accumulated into the outer state
   long long inner_total;
   int inner_max, inner_solves;
+  long long inner_restarts;   // restart cycles of the coarse solves (FGMRES(m), reading R25)
   // lagged step B (inner solve, flags & 4 of k_dcgs_update): lagc = step A of this iteration found
   // the corrected residual of the previous column below tol; pend = the last column still awaits
   // its rotation (done by k_fgm_backsub)
@@ -1160,7 +1161,9 @@ __global__ void k_fgm_backsub(FgmState* st, double2* __restrict__ H, double2* __
       __syncwarp();
     }
   }
-  if (threadIdx.x == 0 && outer) {
+  // statistics once per solve: after its last cycle (converged or out of iterations; a cycle that
+  // only filled its basis is followed by a restart, reading R25)
+  if (threadIdx.x == 0 && outer && (st->conv || st->its >= st->maxit)) {
     outer->inner_total += st->its;
     outer->inner_max = max(outer->inner_max, st->its);
     outer->inner_solves += 1;
@@ -1305,6 +1308,16 @@ __global__ void k_gcr_begin(FgmState* st, const double2* __restrict__ nrm2, int 
   fgm_set_cond(st, h, use_h, !done);
 }
 
+// Restart decision of an FGMRES(m) solve (reading R25), after a cycle's x += Z y: another cycle
+// unless converged or out of iterations.  Counts the restarts into `outer`'s statistics.
+__global__ void k_fgm_restart_cond(FgmState* st, FgmState* outer, cudaGraphConditionalHandle h, int use_h) {
+  HELM_PDL_ENTRY();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int cont = !st->conv && st->its < st->maxit;
+  if (cont && outer) outer->inner_restarts += 1;
+  fgm_set_cond(st, h, use_h, cont);
+}
+
 __global__ void k_set_j(FgmState* st, int j) {
   HELM_PDL_ENTRY();
   st->j = j;
@@ -1324,6 +1337,7 @@ __global__ void k_fgm_reset(FgmState* st, double tol, int maxit, int m) {
   st->inner_total = 0;
   st->inner_max = 0;
   st->inner_solves = 0;
+  st->inner_restarts = 0;
   st->relres = 0.0;
 }
 

@@ -37,7 +37,7 @@ class helm_params(ctypes.Structure):
                 ("col_min_n", ctypes.c_int), ("dist_levels", ctypes.c_int), ("dist_min_rows", ctypes.c_int),
                 ("col_pipe", ctypes.c_int), ("fuse_dots", ctypes.c_int), ("precond", ctypes.c_int),
                 ("gamma", ctypes.c_double), ("tail_cluster", ctypes.c_int),
-                ("lag_stepb", ctypes.c_int), ("dots_cluster", ctypes.c_int)]
+                ("lag_stepb", ctypes.c_int), ("dots_cluster", ctypes.c_int), ("inner_restart", ctypes.c_int)]
 
 
 class helm_dist(ctypes.Structure):
@@ -56,7 +56,7 @@ class helm_report(ctypes.Structure):
     _fields_ = [("outer_iterations", ctypes.c_int), ("converged", ctypes.c_int), ("relres", ctypes.c_double),
                 ("inner_solves", ctypes.c_int), ("inner_iterations_total", ctypes.c_longlong),
                 ("inner_iterations_max", ctypes.c_int), ("restarts", ctypes.c_int), ("seconds", ctypes.c_double),
-                ("kernels", ctypes.c_longlong)]
+                ("kernels", ctypes.c_longlong), ("inner_restarts", ctypes.c_longlong)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
