@@ -1,19 +1,23 @@
 #!/usr/bin/env python
-"""Benchmark: A-DEF1 + CSLP preconditioned FGMRES time-to-1e-6 on B200 (BASELINE.json).
+"""Benchmark: APD (A-DEF1 with higher-order deflation vectors) + CSLP preconditioned FGMRES
+time-to-1e-6 on B200 (BASELINE.json metric "FGMRES time-to-1e-6 & its/s at 1-8 GPUs").
 
-One "step" = one complete solve A x = b to ||b - Ax||/||b|| <= 1e-6 from x0 = 0 (every row
-of the hot path: stencil applies, V-cycles, deflation Z/Z^T and the coarse solve, Krylov
-dots/axpys) for the workload of BASELINE.json configs[1] at its largest size (k = 400,
-h = 1/640, kh = 0.625, Dirichlet point source, Galerkin E), inputs resident in HBM.
-`value` = outer FGMRES iterations per second over the K timed steps; `ms_per_step` is
-the time-to-solution.  The L2 (126 MB) is flushed between timed steps (outside the
-events).
+One "step" = one complete solve A x = b to ||b - Ax||/||b|| <= 1e-6 from x0 = 0 (every row of
+the hot path: stencil applies, V-cycles, deflation Z/Z^T and the coarse solve, Krylov
+dots/axpys).  Default workload: BASELINE.json configs[4]'s weak-scaling block on one GPU,
+`c4_weak_2049` = the unit-square Dirichlet point-source problem with a 2047 x 2047 interior
+grid (h = 1/2048) and k = 1280 (kh = 0.625), complex128, inputs resident in HBM (the 126 MB L2
+is flushed between timed steps, outside the events).
+`value` = `ms_per_step` / 1000 = mean time to 1e-6 in seconds (lower is better); the outer
+FGMRES iterations per second ("its/s") are reported beside it.  N > 1 (torchrun): weak scaling,
+one 2047 x 2048 row strip per GPU of N unit squares stacked in y at the same h and k (kh =
+0.625 at every N), decomposed solve over NCCL; value = max-over-ranks time to 1e-6.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c1_k400] [--coarse-op galerkin]
+                  [--workload c4_weak_2049] [--inner-maxit 200] [--inner-restart 50] ...
 
 --impl reference times the oracle (numpy, host cores) on a bounded sample of the same
-workload: the base contract's reference arm for this tier (DESIGN.md §7).
+workload (DESIGN.md §9): the base contract's reference arm for this tier.
 """
 from __future__ import annotations
 
@@ -29,14 +33,16 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Method of the timed workload: higher-order deflation vectors (APD, the
-# paper's wavenumber-independent variant, Table 4) with the Galerkin coarse operator E; the
-# coarse problem solved by CSLP-FGMRES to 1e-1 (§6.3, the GCR/FGMRES setting) capped
-# at 50 iterations, the inner counts the paper reports for that setting (Tables 9-10); the
-# CSLP hierarchy stops at the first level with <= 512 unknowns (§4 "predefined
-# coarsest grid size"), solved exactly (R8).
-DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 50,
-                  "coarsest_n": 512}
+# Method of the timed workload: higher-order deflation vectors (APD, the paper's
+# wavenumber-independent variant, Table 4) with the Galerkin coarse operator E; outer flexible
+# GMRES (§6.3: a flexible outer method keeps the outer accuracy with a loose coarse
+# tolerance); the coarse problem by CSLP-FGMRES(50) (reading R25) to 1e-1 capped at 200 steps;
+# the CSLP hierarchy stops at the first level with <= 512 unknowns (§4 "predefined
+# coarsest grid size"), solved exactly (R8).  Chosen by the time-to-1e-6 sweep on c4_weak_2049
+# (profiles/r02_c4_sweep.jsonl).
+DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 200,
+                  "inner_restart": 50, "coarsest_n": 512, "restart": 0}
+DEFAULT_WORKLOAD = "c4_weak_2049"
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 
@@ -96,14 +102,14 @@ class ClockSampler:
 
 def method_of(args):
     return {"vectors": args.vectors, "coarse_op": args.coarse_op, "inner_tol": args.inner_tol,
-            "inner_maxit": args.inner_maxit, "coarsest_n": args.coarsest_n}
+            "inner_maxit": args.inner_maxit, "inner_restart": args.inner_restart, "coarsest_n": args.coarsest_n,
+            "restart": args.restart, "outer": args.outer}
 
 
 def oracle_params(args, **kw):
     import oracle
-    m = method_of(args)
-    return oracle.SolverParams(vectors=m["vectors"], coarse_op=m["coarse_op"], inner_tol=m["inner_tol"],
-                               inner_maxit=m["inner_maxit"], coarsest_n=m["coarsest_n"], **kw)
+    m = dict(method_of(args), **kw)
+    return oracle.SolverParams(**m)
 
 
 def dist_env():
@@ -111,94 +117,158 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def run_reference(args, rank, world):
-    """The oracle (numpy) on the host cores, bounded sample: full solves of the same
-    workload family at a size the oracle finishes in seconds is NOT the same workload, so
-    we time whole outer FGMRES iterations of the real workload (c1_k400) instead."""
-    import numpy as np
-    import oracle
-    from workloads import config_problem
-    if rank != 0:
-        return
-    p = config_problem(args.workload)
-    prm = oracle_params(args, maxit=args.ref_iters)
-    s = oracle.Solver(p.k, p.h, p.bc, prm)
-    times, iters = [], []
-    for step in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        x, rep = s.solve(p.b)
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            times.append(dt)
-            iters.append(rep["outer_iterations"])
-    total = sum(times)
-    its = sum(iters)
-    cores = 1
+COUNTS_FILE = os.path.join(ROOT, "profiles", "r02_bench_counts.json")
+
+
+def method_counts(args):
+    """Outer / inner iteration counts of a converged GPU solve of this workload with this method
+    (profiles/r02_bench_counts.json, written by `bench.py --record-counts`): the reference arm
+    extrapolates the oracle's per-iteration cost with them.  None if unrecorded."""
+    try:
+        with open(COUNTS_FILE) as fh:
+            d = json.load(fh)
+        e = d.get(args.workload)
+        if e and e.get("method") == method_of(args):
+            return e
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def oracle_cores():
     try:
         import threadpoolctl
-        info = threadpoolctl.threadpool_info()
-        cores = max([i.get("num_threads", 1) for i in info] or [1])
+        return max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] or [1])
     except Exception:
-        pass
-    val = its / total
+        return 1
+
+
+class OracleSample:
+    """The oracle (numpy, host cores) on a bounded sample of the workload: the first outer FGMRES
+    iteration from x0 = 0 with its coarse solve truncated to c inner iterations.  Two sample sizes
+    separate the cost of one inner iteration from the rest of an outer iteration:
+        t_inner = (T(c2) - T(c1)) / (c2 - c1),   t_outer = T(c1) - c1 t_inner,
+    and the time to 1e-6 is extrapolated as N_outer t_outer + N_inner t_inner with the method's
+    iteration counts on this workload (method_counts).  The Gram-Schmidt work of the sampled
+    iterations is that of the first basis columns only, so the estimate is a lower bound for
+    the oracle."""
+
+    def __init__(self, args, c1=1, c2=2):
+        import oracle
+        from workloads import config_problem
+        self.args = args
+        self.p = config_problem(args.workload)
+        self.c1, self.c2 = c1, c2
+        prm = oracle_params(args, maxit=1)
+        self.solver = oracle.Solver(self.p.k, self.p.h, self.p.bc, prm)
+
+    def run(self, c):
+        s = self.solver
+        s.p.inner_maxit = c
+        s.p.inner_tol = 0.0          # exactly c inner iterations (reading R15)
+        t0 = time.perf_counter()
+        s.solve(self.p.b)
+        return time.perf_counter() - t0
+
+    def estimate(self, t1, t2):
+        t_inner = max(0.0, (t2 - t1) / (self.c2 - self.c1))
+        t_outer = max(0.0, t1 - self.c1 * t_inner)
+        cnt = method_counts(self.args)
+        if cnt is None:
+            return None, t_inner, t_outer, None
+        return cnt["outer"] * t_outer + cnt["inner_total"] * t_inner, t_inner, t_outer, cnt
+
+    def describe(self, t_inner, t_outer, cnt, secs):
+        c = f"counts outer {cnt['outer']}, inner {cnt['inner_total']} ({os.path.basename(COUNTS_FILE)})" if cnt \
+            else "no recorded counts"
+        return (f"oracle on {self.args.workload}: first outer FGMRES iteration from x0=0 with the coarse solve "
+                f"truncated to {self.c1} and {self.c2} inner iterations ({secs:.1f} s of CPU work); "
+                f"{t_inner:.2f} s per inner iteration, {t_outer:.2f} s per outer iteration otherwise; "
+                f"time to 1e-6 extrapolated with the method's {c} (a lower bound: later basis columns "
+                f"cost more Gram-Schmidt)")
+
+
+def run_reference(args, rank, world):
+    """The oracle (numpy) on the host cores: each step one bounded sample (OracleSample, the larger
+    truncation); value = the extrapolated time to 1e-6 in seconds, like the GPU arm's."""
+    if rank != 0:
+        return
+    smp = OracleSample(args)
+    t1 = smp.run(smp.c1)                          # the split needs the smaller sample once
+    times = []
+    for step in range(args.warmup + args.steps):
+        dt = smp.run(smp.c2)
+        if step >= args.warmup:
+            times.append(dt)
+    t2 = statistics.mean(times)
+    est, t_inner, t_outer, cnt = smp.estimate(t1, t2)
+    val = est if est is not None else t2
+    vdef = ("extrapolated time to 1e-6 (s); ms_per_step = one bounded sample" if est is not None else
+            "no recorded iteration counts for this workload/method: value = one bounded sample (s)")
+    cores = oracle_cores()
+    p = smp.p
+    desc = smp.describe(t_inner, t_outer, cnt, t1 + sum(times))
     line = {
-        "impl": "reference", "metric": "fgmres_outer_iterations_per_s", "value": val, "unit": "it/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "impl": "reference", "metric": "fgmres_time_to_1e-6_s", "value": val, "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t2,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": args.workload, **method_of(args), "nx": p.nx, "ny": p.ny, "h": p.h,
-                   "k": p.meta.get("k"), "l2": "n/a (host)"},
-        "cpu_baseline": {"value": val, "unit": "it/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {args.ref_iters} outer FGMRES iterations of {args.workload} per step"},
-        "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "k": p.meta.get("k"), "tol": 1e-6, "l2": "n/a (host)",
+                   "value_definition": vdef},
+        "cpu_baseline": {"value": val, "unit": "s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(args, n_outer=1):
-    """Oracle timed on the host cores on a bounded sample of the workload: its first
-    `n_outer` outer FGMRES iteration(s) from x0 = 0, each including its full inner coarse
-    solve (same method parameters as the GPU run)."""
-    import oracle
-    from workloads import config_problem
-    p = config_problem(args.workload)
-    prm = oracle_params(args, maxit=n_outer)
-    s = oracle.Solver(p.k, p.h, p.bc, prm)
-    t0 = time.perf_counter()
-    x, rep = s.solve(p.b)
-    dt = time.perf_counter() - t0
-    cores = 1
-    try:
-        import threadpoolctl
-        cores = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] or [1])
-    except Exception:
-        pass
-    inner = rep["inner_iterations"]
-    return {"value": rep["outer_iterations"] / dt, "unit": "it/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {rep['outer_iterations']} outer FGMRES iteration(s) of {args.workload} from x0=0 "
-                      f"(inner coarse solve: {sum(inner)} iterations), {dt:.1f} s"}
+def cpu_baseline_sample(args):
+    """cpu_baseline of the GPU arm's line: the oracle on the host cores, one bounded sample of
+    each size (OracleSample), extrapolated to the time to 1e-6."""
+    smp = OracleSample(args)
+    t1 = smp.run(smp.c1)
+    t2 = smp.run(smp.c2)
+    est, t_inner, t_outer, cnt = smp.estimate(t1, t2)
+    return {"value": est, "unit": "s", "cores": oracle_cores(), "kind": "oracle",
+            "sample": smp.describe(t_inner, t_outer, cnt, t1 + t2)}
 
 
-def kernel_roofline(H, rep, peaks, reps=20):
-    """The roofline line of the step's dominant component, measured live here with CUDA events.
+def mean_inner_column(rep, method):
+    """Mean Arnoldi column j over the solve's inner iterations: a coarse solve of I steps in
+    cycles of m (inner_restart) visits j = 0..min(I, m)-1 per cycle."""
+    I = rep["inner_iterations_total"] / max(1, rep["inner_solves"])
+    m = method.get("inner_restart") or 0
+    span = min(I, m) if m > 0 else I
+    return max(1, int(round((span - 1) / 2)))
 
-    The solve is a chain of small dependent kernels, so each component is timed the way it runs
-    inside the solve: `reps` back-to-back instances captured into one CUDA graph and replayed
-    (helm_bench_graph, warm).  Components: one delayed-CGS2 step of the inner FGMRES at the
-    mean basis size (pass 1, reduction + step A, pass 2 + step B), one V-cycle from level 1,
-    one E apply, one A apply.  Counts per step come from the solve's own iteration counts.
-    Algorithmic bytes: DCGS2 step (2j + 7) * 16 n1; V-cycle sum over levels of
-    (40 + 56) n_l + 32 n_{l+1} plus the dense coarsest inverse; E 32 n1 + 8 n0; A 40 n0.  The
-    isolated per-kernel timings (L2 flushed before each launch) are reported beside it."""
+
+def kernel_roofline(H, rep, method, peaks, workload):
+    """The roofline line of the step's dominant kernel, measured live here with CUDA events.
+
+    The solve is a chain of dependent kernels inside one CUDA graph, so each kernel is timed the
+    way it runs there: back-to-back instances of exactly the solve's launch (helm_bench_graph
+    regions that call the solve's own Arnoldi-step code) captured into a graph and replayed warm,
+    at the solve's mean inner basis column.  Launch counts per step are the solve's own counts;
+    the dominant kernel is the one with the largest count x time.  Algorithmic bytes per launch
+    (DESIGN.md §5, per coarse unknown n1 / fine unknown n0): fused E + pass 1 (64 + 16(j+1) + 16);
+    pass 2 (16 j + 64); V-cycle from level 1 sum_l 104 n_l + the dense coarsest inverse; A 40 n0."""
     inner_its = rep["inner_iterations_total"]
     outer_its = rep["outer_iterations"]
-    jm = max(1, int(round(rep["inner_iterations_total"] / max(1, rep["inner_solves"]) / 2)))
+    jm = mean_inner_column(rep, method)
     lv = [ny * nx for (ny, nx, _) in H.levels]
     n0, n1 = lv[0], lv[1]
-    vbytes = sum(96.0 * lv[l] + 32.0 * lv[l + 1] for l in range(1, len(lv) - 1)) + 16.0 * lv[-1] ** 2
-    comps = [("dcgs2 step (inner, j=%d)" % jm, "dcgs", jm, 10, inner_its, (2 * jm + 7) * 16.0 * n1),
-             ("V-cycle from level 1 (inner preconditioner)", "vcycle", 1, 20, inner_its + outer_its, vbytes),
-             ("galerkin_apply E (level 1)", "apply_E", 0, 50, inner_its, 32.0 * n1 + 8.0 * n0),
-             ("apply_op A (level 0)", "apply_A", 0, 50, 2 * outer_its, 40.0 * n0)]
+    tiles = -(-H.levels[1][1] // 16) * -(-H.levels[1][0] // 8)
+    vbytes = sum(104.0 * lv[l] for l in range(1, len(lv) - 1)) + 16.0 * lv[-1] ** 2 + 32.0 * lv[-1]
+    fused = method.get("coarse_op", "galerkin") == "galerkin"
+    comps = [
+        ("k_galerkin_apply<2,0,16,8,true> (E = Z^T A Z fused with DCGS2 pass 1)" if fused else
+         "E apply + k_dcgs_dots (DCGS2 pass 1)", "e_dots", jm, 4, inner_its, (64.0 + 16 * (jm + 1) + 16) * n1),
+        ("k_dcgs_update (DCGS2 pass 2 + step B)", "dcgs_update", jm, 4, inner_its, (16.0 * jm + 64) * n1),
+        ("k_dcgs_reduceA (pass-1 partial sums + step A)", "dcgs_reduce", jm, 4, inner_its,
+         (2 * jm + 2) * 16.0 * (tiles if fused else 1) + 0.0),
+        ("V-cycle from level 1 (inner CSLP preconditioner, 13 kernels)", "vcycle", 1, 10, inner_its + outer_its,
+         vbytes),
+        ("k_apply_op A (level 0)", "apply_A", 0, 10, 2 * outer_its, 40.0 * n0),
+    ]
     rows = {}
     for label, region, arg, nrep, count, nbytes in comps:
         us = H.helm_bench_graph(region, arg, nrep)
@@ -206,47 +276,51 @@ def kernel_roofline(H, rep, peaks, reps=20):
         rows[label] = {"kernel": label, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                        "frac": gbs / peaks["hbm_gbs"], "traffic": None, "bytes_per_launch": nbytes,
                        "us_per_launch": us, "launches_per_step": count, "est_ms_per_step": count * us * 1e-3,
-                       "timing": "in-graph, warm (helm_bench_graph)", "peak_src": peaks["src"]}
+                       "column": arg if region in ("e_dots", "dcgs_update", "dcgs_reduce") else None,
+                       "timing": "in-graph, warm (helm_bench_graph: the solve's own launch, replayed)",
+                       "peak_src": peaks["src"]}
     dom = max(rows.values(), key=lambda r: r["est_ms_per_step"])
-    # DRAM traffic of the dominant component from the committed ncu --set full capture of the
-    # same component (cold caches): the kernels of one delayed-CGS2 step at inner column jm, or
-    # of the first inner V-cycle from level 1 (tools/ncu_dcgs_summary.py)
-    prof_name = ("dcgs_j%d" % jm) if dom["kernel"].startswith("dcgs2 step") else \
-        ("vcycle1" if dom["kernel"].startswith("V-cycle from level 1") else None)
-    if prof_name:
-        try:
-            with open(os.path.join(ROOT, "profiles", f"r01_ncu_{prof_name}.json")) as fh:
-                prof = json.load(fh)
-            dom["traffic"] = prof["dram_bytes_per_step"]
-            dom["traffic_src"] = f"profiles/r01_ncu_{prof_name}.json (ncu --set full, cold caches)"
-        except (OSError, KeyError, ValueError):
-            pass
-    iso = {}
-    for name, arg in (("gs_dots", jm + 1), ("gs_update", jm + 1), ("apply_E", 0), ("apply_A", 0), ("vc_down", 0),
-                      ("vc_up", 0), ("vc_down", 1), ("vc_up", 1)):
-        us, nbytes = H.helm_bench_kernel(name, arg=arg, reps=reps, flush=True)
-        gbs = nbytes / (us * 1e-6) / 1e9
-        iso[f"{name}[{arg}]"] = {"us": us, "GB/s": gbs, "frac": gbs / peaks["hbm_gbs"]}
-    return dict(dom), {"components": {k: {kk: v[kk] for kk in ("achieved", "frac", "us_per_launch",
+    # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture of
+    # the same launch at this workload (tools/ncu_regions.py; cold caches)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as fh:
+            prof = json.load(fh)
+        key = f"{workload}:{dom['kernel'].split(' ')[0]}"
+        if key in prof:
+            e = prof[key]
+            # per basis column the kernel streams 16 n1 bytes more: scale to this column
+            dom["traffic"] = e["dram_bytes"] + e.get("bytes_per_column", 0.0) * ((dom["column"] or 0) - e.get("column", 0))
+            dom["traffic_src"] = e["src"]
+    except (OSError, KeyError, ValueError, TypeError):
+        pass
+    return dict(dom), {"components": {k: {kk: v[kk] for kk in ("achieved", "frac", "us_per_launch", "bytes_per_launch",
                                                               "launches_per_step", "est_ms_per_step")}
                                       for k, v in rows.items()},
-                       "isolated_kernels_l2_flushed": iso}
+                       "mean_inner_column": jm}
 
 
 def microbench(peaks, n=16385, reps=10):
-    """BASELINE configs[4] microbenchmark: isolated stencil apply and fused V-cycle legs on a
-    16385^2-node (16383^2 Dirichlet unknowns) complex128 grid, L2 flushed before each launch."""
+    """BASELINE configs[4] microbenchmark: isolated stencil apply, fused V-cycle legs and one whole
+    V-cycle from level 0 on a 16385^2-node (16383^2 Dirichlet unknowns) complex128 grid.  Single
+    kernels: L2 flushed before each launch.  Whole V-cycle: 5 back-to-back cycles in a graph (the
+    4.3 GB fields are 34x the L2).  Algorithmic bytes of a V-cycle: 104 B per unknown of every
+    level above the coarsest (down leg 44, up leg 60) + the dense coarsest inverse."""
     import torch
     from paper_2308_06152_b200 import helm
     m = n - 2
     h = 1.0 / (n - 1)
     k = torch.full((m, m), 0.625 / h, dtype=torch.float64, device="cuda")
-    H = helm.Helm(m, m, h, "dirichlet", k, {"inner_maxit": 2})
+    H = helm.Helm(m, m, h, "dirichlet", k, {"inner_maxit": 2, "coarsest_n": 512})
     out = {"grid": f"{m}x{m} unknowns (h=1/{n - 1}), complex128"}
     for name, arg in (("apply_A", 0), ("vc_down", 0), ("vc_up", 0)):
         us, nb = H.helm_bench_kernel(name, arg=arg, reps=reps, flush=True)
         gbs = nb / (us * 1e-6) / 1e9
         out[name] = {"us": us, "GB/s": gbs, "frac": gbs / peaks["hbm_gbs"], "bytes": nb}
+    lv = [ny * nx for (ny, nx, _) in H.levels]
+    vb = sum(104.0 * lv[l] for l in range(len(lv) - 1)) + 16.0 * lv[-1] ** 2 + 32.0 * lv[-1]
+    us = H.helm_bench_graph("vcycle", 0, 5)
+    out["vcycle_from_level0"] = {"us": us, "GB/s": vb / (us * 1e-6) / 1e9, "frac": vb / (us * 1e-6) / 1e9 / peaks["hbm_gbs"],
+                                 "bytes": vb, "levels": len(lv)}
     H.close()
     del k
     torch.cuda.empty_cache()
@@ -272,28 +346,18 @@ class _StdoutToStderr:
 def run_decomposed(args, rank, world, local):
     from paper_2308_06152_b200 import helm
     with _StdoutToStderr():
-        try:
-            line = _run_decomposed(args, rank, world, local)
-        except helm.HelmError as exc:
-            # the peer transport reports a stalled peer (wait timeout) on every rank; the job then
-            # reruns over NCCL instead of producing nothing
-            if args.transport != "peer":
-                raise
-            print(f"[bench] peer transport failed ({exc}); rerunning over NCCL", file=sys.stderr, flush=True)
-            args.transport = "nccl"
-            args.transport_note = f"peer transport failed: {exc}"
-            line = _run_decomposed(args, rank, world, local)
+        line = _run_decomposed(args, rank, world, local)
     if line is not None:
         print(json.dumps(line), flush=True)
 
 
 def _run_decomposed(args, rank, world, local):
     """Weak scaling of ONE solve over the ranks: the workload's unit square
-    stacked `world` times in y (strip_problem: same h and k, point source at the centre), one
-    row strip per GPU; halos by grouped ncclSend/ncclRecv, dots by ncclAllReduce, the coarse
-    levels below the decomposed ones all-gathered and replicated.  value = world x outer
-    iterations / device time: each outer iteration covers `world` blocks of the N = 1
-    workload, so value / (N x value at N = 1) is the time-per-iteration efficiency."""
+    stacked `world` times in y (strip_problem: same h and k, so kh = 0.625 and one 2047 x 2048
+    block per GPU at every N; point source at the centre), one row strip per GPU; halos by
+    grouped ncclSend/ncclRecv, dots by ncclAllReduce, the coarse levels below the decomposed ones
+    all-gathered and replicated.  value = max-over-ranks device time to 1e-6 (s).  The same
+    outer restart length at every N.  A transport failure raises on every rank (no rerun)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -303,6 +367,7 @@ def _run_decomposed(args, rank, world, local):
     peaks = load_peaks()
     base = config_problem(args.workload)
     p = strip_problem(base.meta["k"], base.meta["n_cells"], world, f"{args.workload}_x{world}")
+    method = method_of(args)
     uid = peer_exchange = None
     if args.transport == "peer":        # NVLink peer memory through CUDA IPC (peer.cuh), no NCCL
         def peer_exchange(handle):
@@ -319,81 +384,86 @@ def _run_decomposed(args, rank, world, local):
         uid = helm.nccl_unique_id()
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        # levels 0-2 decomposed, level 3 (79 x (80 N - 1) unknowns) and below replicated: 7 small
-        # collectives per inner iteration instead of ~11 with the deepest possible split
-        prm = dict(method_of(args), dist_levels=args.dist_levels or 3)
+        # levels 0-2 decomposed, the rest replicated
+        prm = dict(method, dist_levels=args.dist_levels or 3)
         H = helm.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, rank, world, nccl_id=uid, params=prm, stream=stream,
                           peer_exchange=peer_exchange)
-        bo = np.ascontiguousarray(p.b[H.row0:H.row0 + H.nrows])
-        b = torch.from_numpy(bo).cuda()
-        x = torch.empty_like(b)
-        for _ in range(args.warmup):
-            H.solve(b, 1e-6, args.maxit, x)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        reps = []
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        wall0 = time.perf_counter()
-        with ClockSampler(local) as clk:
-            for s in range(args.steps):
-                H.helm_flush_l2(256 << 20)
-                ev[s][0].record(stream)
-                _, rep = H.solve(b, 1e-6, args.maxit, x)
-                ev[s][1].record(stream)
-                reps.append(rep)
-            torch.cuda.synchronize()
-        wall = time.perf_counter() - wall0
-        dev_s = sum(a.elapsed_time(b_) for a, b_ in ev) * 1e-3
-        if world > 1:
-            tt = torch.tensor([dev_s], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dev_s = float(tt.item())
-        its = sum(r["outer_iterations"] for r in reps)
-        value = world * its / dev_s
-        bh = torch.from_numpy(bo).pin_memory().numpy()
-        xh = torch.empty(bo.shape, dtype=torch.complex128).pin_memory().numpy()
-        H.solve_host(bh, xh, 1e-6, args.maxit)
-        e2e_t, e2e_its = [], 0
-        for s in range(args.steps):
-            H.helm_flush_l2(256 << 20)
-            torch.cuda.synchronize()
+        try:
+            bo = np.ascontiguousarray(p.b[H.row0:H.row0 + H.nrows])
+            b = torch.from_numpy(bo).cuda()
+            x = torch.empty_like(b)
+            for _ in range(args.warmup):
+                H.solve(b, 1e-6, args.maxit, x)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            reps = []
             if world > 1:
                 dist.barrier()
-            t0 = time.perf_counter()
-            _, r2 = H.solve_host(bh, xh, 1e-6, args.maxit)
-            e2e_t.append(time.perf_counter() - t0)
-            e2e_its += r2["outer_iterations"]
-        e2e_s = sum(e2e_t)
-        if world > 1:
-            tt = torch.tensor([e2e_s], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
-        launches = sum(r["kernels"] for r in reps)
-        H.close()
+            torch.cuda.synchronize()
+            wall0 = time.perf_counter()
+            with ClockSampler(local) as clk:
+                for s in range(args.steps):
+                    H.helm_flush_l2(256 << 20)
+                    ev[s][0].record(stream)
+                    _, rep = H.solve(b, 1e-6, args.maxit, x)
+                    ev[s][1].record(stream)
+                    reps.append(rep)
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+            wall = time.perf_counter() - wall0
+            dev_s = sum(a.elapsed_time(b_) for a, b_ in ev) * 1e-3
+            if world > 1:
+                tt = torch.tensor([dev_s], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dev_s = float(tt.item())
+            its = sum(r["outer_iterations"] for r in reps)
+            bh = torch.from_numpy(bo).pin_memory().numpy()
+            xh = torch.empty(bo.shape, dtype=torch.complex128).pin_memory().numpy()
+            e2e_t = []
+            for s in range(max(1, args.e2e_steps)):
+                H.helm_flush_l2(256 << 20)
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                H.solve_host(bh, xh, 1e-6, args.maxit)
+                e2e_t.append(time.perf_counter() - t0)
+            e2e_s = statistics.mean(e2e_t)
+            if world > 1:
+                tt = torch.tensor([e2e_s], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                e2e_s = float(tt.item())
+            launches = sum(r["kernels"] for r in reps)
+        finally:
+            H.close()
         roof = roof_all = None
         if rank == 0:   # kernel rooflines at the per-GPU block size (single-GPU context)
-            Hs = helm.helm_setup(base, method_of(args), stream=stream)
-            roof, roof_all = kernel_roofline(Hs, reps[-1], peaks)
+            Hs = helm.helm_setup(base, method, stream=stream)
+            roof, roof_all = kernel_roofline(Hs, reps[-1], method, peaks, args.workload)
             Hs.close()
     if rank != 0:
         return None
+    tts = dev_s / args.steps
+    r = reps[-1]
     line = {
-        "metric": "fgmres_outer_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
-        "time_to_solution_s": dev_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": p.name, "per_gpu_block": args.workload, **method_of(args), "nx": p.nx, "ny": p.ny,
-                   "h": p.h, "k": p.meta["k"], "tol": 1e-6, "l2": "flushed between timed steps (256 MiB read)",
-                   "outer_iterations": reps[-1]["outer_iterations"],
-                   "inner_iterations_mean": reps[-1]["inner_iterations_total"] / max(1, reps[-1]["inner_solves"]),
+        "metric": "fgmres_time_to_1e-6_s", "value": tts, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tts,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "outer_its_per_s": its / dev_s, "time_to_solution_s": tts,
+        "converged": all(x_["converged"] for x_ in reps),
+        "config": {"workload": p.name, "per_gpu_block": args.workload, **method, "nx": p.nx, "ny": p.ny,
+                   "h": p.h, "k": p.meta["k"], "tol": 1e-6, "maxit": args.maxit,
+                   "l2": "flushed between timed steps (256 MiB read)",
+                   "outer_iterations": r["outer_iterations"],
+                   "inner_iterations_total": r["inner_iterations_total"],
+                   "inner_iterations_mean": r["inner_iterations_total"] / max(1, r["inner_solves"]),
                    "parallelism": f"row-strip decomposition x{world} ({args.transport} transport)",
                    "dist_levels": prm["dist_levels"], "transport": args.transport,
-                   **({"transport_note": args.transport_note} if getattr(args, "transport_note", None) else {}),
-                   "value_definition": "world x outer iterations / max-over-ranks device time"},
+                   "value_definition": "max-over-ranks device time to 1e-6 (s)"},
         "wall_s": wall,
         "gpu_launches": launches,
-        "e2e": {"value": world * e2e_its / e2e_s, "unit": "it/s", "h2d_bytes_per_step": int(bo.nbytes) * world,
+        "e2e": {"value": e2e_s, "unit": "s", "steps": len(e2e_t), "h2d_bytes_per_step": int(bo.nbytes) * world,
                 "d2h_bytes_per_step": int(bo.nbytes) * world},
         "roofline": roof,
         "roofline_kernels": roof_all,
@@ -405,25 +475,30 @@ def _run_decomposed(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c1_k400")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--coarse-op", default=DEFAULT_METHOD["coarse_op"])
     ap.add_argument("--vectors", default=DEFAULT_METHOD["vectors"])
+    ap.add_argument("--outer", default="fgmres", choices=["fgmres", "gcr"])
     ap.add_argument("--inner-tol", type=float, default=DEFAULT_METHOD["inner_tol"])
     ap.add_argument("--inner-maxit", type=int, default=DEFAULT_METHOD["inner_maxit"])
+    ap.add_argument("--inner-restart", type=int, default=DEFAULT_METHOD["inner_restart"])
+    ap.add_argument("--restart", type=int, default=DEFAULT_METHOD["restart"],
+                    help="outer FGMRES(m); 0 = full basis (the same at every N)")
     ap.add_argument("--coarsest-n", type=int, default=DEFAULT_METHOD["coarsest_n"])
-    ap.add_argument("--maxit", type=int, default=2000)
-    ap.add_argument("--ref-iters", type=int, default=1)
+    ap.add_argument("--maxit", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=1, help="end-to-end solves (host buffers) after the timed ones")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--record-counts", action="store_true",
+                    help="write this run's iteration counts to profiles/r02_bench_counts.json (reference arm)")
     ap.add_argument("--dist-levels", type=int, default=0, help="decomposed levels (0: 3)")
-    ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
-                    help="decomposed solve: NVLink peer memory through CUDA IPC (default; reruns over NCCL if a "
-                         "peer stalls) or NCCL collectives")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="decomposed solve: NCCL collectives (default) or NVLink peer memory through CUDA IPC")
     ap.add_argument("--decomp", default="auto", choices=["auto", "on", "off"],
-                    help="row-strip decomposed solve over the ranks (NCCL); auto = on when N > 1")
+                    help="row-strip decomposed solve over the ranks; auto = on when N > 1")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -434,26 +509,23 @@ def main():
             dist.init_process_group("nccl")
     if args.decomp == "on" or (args.decomp == "auto" and world > 1):
         return run_decomposed(args, rank, world, local)
-    import numpy as np
     import torch
     from paper_2308_06152_b200 import helm
     from workloads import config_problem
     torch.cuda.set_device(local)
     peaks = load_peaks()
     p = config_problem(args.workload)
+    method = method_of(args)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        H = helm.helm_setup(p, method_of(args), stream=stream)
+        H = helm.helm_setup(p, method, stream=stream)
         b = torch.from_numpy(p.b).cuda()
         x = torch.empty_like(b)
         torch.cuda.synchronize()
         for _ in range(args.warmup):
             H.solve(b, 1e-6, args.maxit, x)
-        launches0 = H.helm_launch_count()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         reps = []
-        if world > 1:
-            torch.distributed.barrier()
         torch.cuda.synchronize()
         wall0 = time.perf_counter()
         with ClockSampler(local) as clk:
@@ -467,43 +539,51 @@ def main():
         wall = time.perf_counter() - wall0
         launches = sum(r["kernels"] for r in reps)
         dev_s = sum(a.elapsed_time(b_) for a, b_ in ev) * 1e-3
-        if world > 1:
-            t = torch.tensor([dev_s], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dev_s = float(t.item())
         its = sum(r["outer_iterations"] for r in reps)
-        value = its * world / dev_s
-        # end-to-end through the public API with host buffers (H2D of b, D2H of x)
+        converged = all(r["converged"] for r in reps)
+        # true residual of the last solution (the device estimate is the stopping test)
+        rr = float(torch.linalg.vector_norm(H.apply_A(x) - b) / torch.linalg.vector_norm(b))
+        # end-to-end through the public API with host buffers (H2D of b, D2H of x inside)
         bh = torch.from_numpy(p.b).pin_memory().numpy()
         xh = torch.empty(p.shape, dtype=torch.complex128).pin_memory().numpy()
-        H.solve_host(bh, xh, 1e-6, args.maxit)
         e2e_t = []
-        e2e_its = 0
-        for s in range(args.steps):
+        for s in range(max(1, args.e2e_steps)):
             H.helm_flush_l2(256 << 20)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             _, r2 = H.solve_host(bh, xh, 1e-6, args.maxit)
             e2e_t.append(time.perf_counter() - t0)
-            e2e_its += r2["outer_iterations"]
-        roof, roof_all = kernel_roofline(H, reps[-1], peaks)
-    if rank != 0:
-        return
+        roof, roof_all = kernel_roofline(H, reps[-1], method, peaks, args.workload)
+        H.close()
+    tts = dev_s / args.steps
+    r = reps[-1]
+    if args.record_counts and converged:
+        try:
+            with open(COUNTS_FILE) as fh:
+                d = json.load(fh)
+        except (OSError, ValueError):
+            d = {}
+        d[args.workload] = {"method": method, "outer": r["outer_iterations"], "inner_total": r["inner_iterations_total"],
+                            "inner_solves": r["inner_solves"], "time_to_solution_s": tts}
+        with open(COUNTS_FILE, "w") as fh:
+            json.dump(d, fh, indent=1, sort_keys=True)
     line = {
-        "metric": "fgmres_outer_iterations_per_s", "value": value, "unit": "it/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
-        "time_to_solution_s": dev_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": args.workload, **method_of(args), "nx": p.nx, "ny": p.ny, "h": p.h,
-                   "k": p.meta.get("k"), "tol": 1e-6, "l2": "flushed between timed steps (256 MiB write)",
-                   "outer_iterations": reps[-1]["outer_iterations"],
-                   "inner_iterations_mean": reps[-1]["inner_iterations_total"] / max(1, reps[-1]["inner_solves"]),
-                   "inner_iterations_max": reps[-1]["inner_iterations_max"],
-                   "parallelism": "replicas" if world > 1 else "single"},
+        "metric": "fgmres_time_to_1e-6_s", "value": tts, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tts,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "outer_its_per_s": its / dev_s, "time_to_solution_s": tts, "converged": converged, "true_relres": rr,
+        "config": {"workload": args.workload, **method, "nx": p.nx, "ny": p.ny, "h": p.h,
+                   "k": p.meta.get("k"), "tol": 1e-6, "maxit": args.maxit,
+                   "l2": "flushed between timed steps (256 MiB read)",
+                   "outer_iterations": r["outer_iterations"],
+                   "inner_iterations_total": r["inner_iterations_total"],
+                   "inner_iterations_mean": r["inner_iterations_total"] / max(1, r["inner_solves"]),
+                   "inner_iterations_max": r["inner_iterations_max"], "inner_restarts": r["inner_restarts"],
+                   "outer_restarts": r["restarts"], "parallelism": "single"},
         "wall_s": wall,
         "gpu_launches": launches,
-        "e2e": {"value": e2e_its / sum(e2e_t), "unit": "it/s", "h2d_bytes_per_step": p.nx * p.ny * 16,
-                "d2h_bytes_per_step": p.nx * p.ny * 16},
+        "e2e": {"value": statistics.mean(e2e_t), "unit": "s", "steps": len(e2e_t),
+                "h2d_bytes_per_step": p.nx * p.ny * 16, "d2h_bytes_per_step": p.nx * p.ny * 16},
         "roofline": roof,
         "roofline_kernels": roof_all,
         "clocks": clk.summary(),

@@ -228,13 +228,20 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_VCYCLE 0
 #define HELM_GB_APPLY_E 1
 #define HELM_GB_APPLY_A 2
-#define HELM_GB_DCGS 3      /* one delayed-CGS2 step (pass 1, reduction + step A, pass 2 + step B)
-                               of the inner FGMRES from column `arg` (arg + reps < inner_maxit).
+#define HELM_GB_DCGS 3      /* one Arnoldi step of the inner FGMRES after the V-cycle, as the solve
+                               runs it: E apply + pass 1 (fused by default), reduction + step A,
+                               pass 2 + step B, from column `arg` (arg + reps < basis size).
                                Probe knobs (environment, this region only): HELM_GB_DCGS_MASK
                                selects its kernels (1 dots, 2 reduction, 4 update; default 7),
                                HELM_GB_UPD_FLAGS overrides the update kernel's flags */
 #define HELM_GB_INNER_ITER 4 /* one whole inner FGMRES iteration (V-cycle from level 1, E apply,
                                 delayed-CGS2 step) from column `arg`, without the loop node */
+/* The kernels of the inner Arnoldi step one at a time, exactly as the solve launches them
+ * (HELM_GB_DCGS is their sequence): */
+#define HELM_GB_E_DOTS 5      /* w = E z_j with pass 1 of the delayed CGS2 (one fused kernel with
+                                 str-Glk and fuse_dots; else the E apply and the dots kernel) */
+#define HELM_GB_DCGS_REDUCE 6 /* reduction of the pass-1 partials + step A coefficients */
+#define HELM_GB_DCGS_UPDATE 7 /* pass 2 (v_j, w') + step B (advances the column) */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 /* ---------------------------------------------------------------------------------------

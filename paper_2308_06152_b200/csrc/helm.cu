@@ -780,6 +780,16 @@ int raise_dyn_smem(const void* func, size_t need) {
 // n: owned length; ld: stored length of a basis vector; off: owned offset; dist: rank-summed dots
 // P: pass-1 partials per output when the dots come from the fused E kernel (0: dots kernel only)
 int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, bool dist, int P = 0) {
+  if (dist && C.kind == HELM_COMM_PEER) {
+    // k_dcgs_update_peer keeps the pass-2 coefficients and the summed dots in shared memory
+    const size_t need = dcgs_update_smem_dev(m) + (size_t)(2 * m + 4) * sizeof(double2);
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    if (need + 40 * 1024 > (size_t)optin)
+      return fail(HELM_EINVAL, "peer transport: a Krylov basis of %d columns needs %zu B of shared memory per "
+                  "block (limit %d); use a restart length of at most ~%d or the NCCL transport", m, need, optin,
+                  (int)((optin - 40 * 1024) / 72));
+  }
   K.m = m;
   K.n = n;
   K.ld = ld;
@@ -796,7 +806,8 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
   CKR(dalloc(&K.sn, (size_t)m));
   CKR(dalloc(&K.cs, (size_t)m));
   CKR(dalloc(&K.y, (size_t)m));
-  CKR(dalloc(&K.dots1, (size_t)2 * m + 4));
+  // k_dcgs_reduceA zeroes whole warps of slots: round up to a multiple of 8
+  CKR(dalloc(&K.dots1, ((size_t)2 * m + 4 + 7) / 8 * 8));
   CKR(dalloc(&K.coef, (size_t)2 * m + 4));
   CKR(dalloc(&K.sc2, 2));
   CKR(dalloc(&K.rawc, (size_t)m + 2));
@@ -960,6 +971,97 @@ int run_while(helm_ctx_s& C, FgmState* st, Begin&& begin, Body&& body) {
   return HELM_OK;
 }
 
+// Lagged step B (helm_params.lag_stepb) applies to the first cycle of the inner solve on one GPU
+// (fresh start, staged back substitution, whose shared memory then also holds the last column's
+// rotation)
+bool inner_lag(const helm_ctx_s& C) {
+  const Fgm& K = C.inner;
+  const size_t bs = ((size_t)K.m * (K.m + 1) + K.m) * sizeof(double2);
+  return C.p.lag_stepb && !K.dist && K.coop == 0 && bs <= 96 * 1024 && K.m >= 3;
+}
+
+// One Arnoldi step of an FGMRES cycle after the preconditioner (z_j = P v~_j is in K.Z[j]):
+// w = A z_j and the delayed CGS2 of column j -- pass 1 (a = V^H v~_j, b = V^H w; fused into the
+// inner E apply when `fuse`), reduction + step A, pass 2 + step B.  Shared by fgmres_cycle and
+// the helm_bench_graph regions, so a region replays exactly the solve's kernels.  `mask` (bench
+// regions, plain single-GPU step only): 1 = the apply (+ pass 1), 2 = reduction, 4 = pass 2.
+template <class OpA>
+int arnoldi_step(helm_ctx_s& C, Fgm& K, OpA&& opA, bool fuse, bool lag, cudaGraphConditionalHandle h, int use_h,
+                 int mask = 7) {
+  const size_t n = K.n, off = K.off;
+  const long long ld = (long long)K.ld, ln = (long long)n;
+  double2* Vo = K.V + off;
+  FgmState* st = K.st;
+  DVec vj(K.V, &st->j, ld, &st->inv_hn), zj(K.Z, &st->j, ld), w(K.V + K.ld, &st->j, ld);
+  const DVec vjo = shift(vj, off), wo = shift(w, off);
+  const GsGeom& gg = K.geo;
+  const size_t asm_ = dcgs_smem(K.m);
+  long long nparts = gg.gx;
+  if (fuse && K.coop == 0) {
+    if (mask & 1) CKR(apply_E_dots(C, zj, w, vjo, Vo, ld, &st->j, K.part));
+    const dim3 gt = glk_tiles(C);
+    nparts = (long long)gt.x * gt.y;
+  } else if (mask & 1) {
+    CKR(opA(zj, DVec(), w));
+  }
+  // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
+  if (K.coop > 0) {
+    // the whole step in one cooperative kernel (grid-wide barriers between its phases)
+    launch_coop(C, k_dcgs_step, K.coop, DC_THREADS, asm_, (const double2*)Vo, ld, st, vjo, wo, ln, gg.chunk, gg.gx,
+                gg.gy, K.part, K.npart, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, h, use_h);
+    return post_launch(C);
+  }
+  // pass 1 with on-chip cluster sums (no reduction kernel): single GPU, unfused
+  const bool cld = K.gxc > 0 && !K.dist && !fuse;
+  if (cld) {
+    launch_kc(C, k_dcgs_dots_cl, dim3(K.gxc * DC_CL, gg.gy), DC_THREADS, (size_t)(2 * K.m + 4) * sizeof(double2),
+              DC_CL, Vo, ld, &st->j, 1, vjo, wo, ln, gg.chunk, K.cpart);
+    CKR(post_launch(C));
+  } else if (!(fuse && K.coop == 0) && (mask & 1)) {
+    launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
+             gg.chunk, K.part);
+    CKR(post_launch(C));
+  }
+  // reduction of the pass-1 partials; pass 2 with the rotation part of step A in an extra
+  // block and step B in the last block.  Decomposed: the dots are summed over the ranks
+  // before pass 2, |w'|^2 before step B (then a separate one-warp kernel)
+  if (K.dist && C.kind == HELM_COMM_PEER) {
+    // rank sums fused into the step's kernels over peer memory (peer.cuh): 4 kernels per step
+    if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
+    launch_k(C, k_dcgs_reduce_peer, ((2 * K.m + 2) * 32 + 255) / 256, 256, 0, (const double2*)K.part, nparts,
+             (const FgmState*)st, K.dots1, K.cnt, C.peers, C.rank, C.nranks, C.playout.red);
+    CKR(post_launch(C));
+    const size_t us = dcgs_update_smem_dev(K.m) + (size_t)(2 * K.m + 4) * sizeof(double2);
+    launch_k(C, k_dcgs_update_peer, gg.gu + 1, DU_THREADS, us, Vo, ld, (const int*)&st->j, K.dots1, vjo, wo, ln,
+             K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1, K.m, C.peers, C.rank, C.nranks, C.playout.red);
+    CKR(post_launch(C));
+    launch_k(C, k_dcgs_stepB_peer, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
+             K.rawc, h, use_h, C.peers, C.rank, C.nranks, C.playout.red);
+    return post_launch(C);
+  }
+  if (!cld && (mask & 2)) {
+    launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, nparts, st, K.H,
+             K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
+    CKR(post_launch(C));
+  }
+  if (K.dist) CKR(allreduce(C, K.dots1, 2 * K.m + 2));
+  if (!(mask & 4)) return HELM_OK;
+  launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), Vo, ld,
+           (const int*)&st->j, (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
+           K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0), (const double2*)K.cpart, K.gxc,
+           dcgs_sab_len(K.m));
+  CKR(post_launch(C));
+  if (K.dist) {
+    launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu + 1, K.nrm);
+    CKR(post_launch(C));
+    CKR(allreduce(C, K.nrm, 1));
+    launch_k(C, k_dcgs_stepB, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
+             (const double2*)K.nrm, 1, K.rawc, h, use_h);
+    CKR(post_launch(C));
+  }
+  return HELM_OK;
+}
+
 // One FGMRES cycle for A x = b with x0 = 0 (first) or the current x (restart), x (+)= Z y.
 // opA(x, f, y): y = A x (f null) or y = f - A x;  opP(v, z): z = P v.
 
@@ -977,7 +1079,7 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
   // substitution, whose shared memory then also holds the last column's rotation)
   const size_t bs = ((size_t)K.m * (K.m + 1) + K.m) * sizeof(double2);
   const bool staged = bs <= 96 * 1024;
-  const bool lag = C.p.lag_stepb && &K == &C.inner && first && !K.dist && K.coop == 0 && staged && K.m >= 3;
+  const bool lag = first && &K == &C.inner && inner_lag(C);
   auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     if (first) {
       CKR(gs_dots(C, K, nullptr, nullptr, 0, shift(b, off), 1, K.nrm, nullptr));
@@ -996,74 +1098,9 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
   auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
     // v~_j is consumed through the scale 1/h_{j,j-1} left by the previous step B (no
     // normalisation pass); pass 2 writes the final v_j over it
-    DVec vj(K.V, &st->j, ld, &st->inv_hn), zj(K.Z, &st->j, ld), w(K.V + K.ld, &st->j, ld);
-    const DVec vjo = shift(vj, off), wo = shift(w, off);
+    DVec vj(K.V, &st->j, ld, &st->inv_hn), zj(K.Z, &st->j, ld);
     CKR(opP(vj, zj));
-    const GsGeom& gg = K.geo;
-    const size_t asm_ = dcgs_smem(K.m);
-    long long nparts = gg.gx;
-    if (fuse && K.coop == 0) {
-      CKR(apply_E_dots(C, zj, w, vjo, Vo, ld, &st->j, K.part));
-      const dim3 gt = glk_tiles(C);
-      nparts = (long long)gt.x * gt.y;
-    } else {
-      CKR(opA(zj, DVec(), w));
-    }
-    // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
-    if (K.coop > 0) {
-      // the whole step in one cooperative kernel (grid-wide barriers between its phases)
-      launch_coop(C, k_dcgs_step, K.coop, DC_THREADS, asm_, (const double2*)Vo, ld, st, vjo, wo, ln, gg.chunk, gg.gx,
-                  gg.gy, K.part, K.npart, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, h, use_h);
-      return post_launch(C);
-    }
-    // pass 1 with on-chip cluster sums (no reduction kernel): single GPU, unfused
-    const bool cld = K.gxc > 0 && !K.dist && !fuse;
-    if (cld) {
-      launch_kc(C, k_dcgs_dots_cl, dim3(K.gxc * DC_CL, gg.gy), DC_THREADS, (size_t)(2 * K.m + 4) * sizeof(double2),
-                DC_CL, Vo, ld, &st->j, 1, vjo, wo, ln, gg.chunk, K.cpart);
-      CKR(post_launch(C));
-    } else if (!(fuse && K.coop == 0)) {
-      launch_k(C, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), Vo, ld, &st->j, 1, vjo, wo, ln,
-               gg.chunk, K.part);
-      CKR(post_launch(C));
-    }
-    // reduction of the pass-1 partials; pass 2 with the rotation part of step A in an extra
-    // block and step B in the last block.  Decomposed: the dots are summed over the ranks
-    // before pass 2, |w'|^2 before step B (then a separate one-warp kernel)
-    if (K.dist && C.kind == HELM_COMM_PEER) {
-      // rank sums fused into the step's kernels over peer memory (peer.cuh): 4 kernels per step
-      if (!C.peer_connected) return fail(HELM_EINVAL, "peer transport: helm_peer_connect not called");
-      launch_k(C, k_dcgs_reduce_peer, ((2 * K.m + 2) * 32 + 255) / 256, 256, 0, (const double2*)K.part, nparts,
-               (const FgmState*)st, K.dots1, K.cnt, C.peers, C.rank, C.nranks, C.playout.red);
-      CKR(post_launch(C));
-      const size_t us = dcgs_update_smem_dev(K.m) + (size_t)(2 * K.m + 4) * sizeof(double2);
-      launch_k(C, k_dcgs_update_peer, gg.gu + 1, DU_THREADS, us, Vo, ld, (const int*)&st->j, K.dots1, vjo, wo, ln,
-               K.part, st, K.H, K.cs, K.sn, K.g, K.rawc, K.cnt + 1, K.m, C.peers, C.rank, C.nranks, C.playout.red);
-      CKR(post_launch(C));
-      launch_k(C, k_dcgs_stepB_peer, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
-               K.rawc, h, use_h, C.peers, C.rank, C.nranks, C.playout.red);
-      return post_launch(C);
-    }
-    if (!cld) {
-      launch_k(C, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, asm_, K.part, nparts, st, K.H,
-               K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
-      CKR(post_launch(C));
-    }
-    if (K.dist) CKR(allreduce(C, K.dots1, 2 * K.m + 2));
-    launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), Vo, ld,
-             (const int*)&st->j, (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
-             K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0), (const double2*)K.cpart, K.gxc,
-             dcgs_sab_len(K.m));
-    CKR(post_launch(C));
-    if (K.dist) {
-      launch_k(C, k_sum_part, 1, 32, 0, (const double2*)K.part, gg.gu + 1, K.nrm);
-      CKR(post_launch(C));
-      CKR(allreduce(C, K.nrm, 1));
-      launch_k(C, k_dcgs_stepB, 1, 32, dcgs_update_smem(K.m), st, K.H, K.cs, K.sn, K.g, (const double2*)K.dots1,
-               (const double2*)K.nrm, 1, K.rawc, h, use_h);
-      CKR(post_launch(C));
-    }
-    return HELM_OK;
+    return arnoldi_step(C, K, opA, fuse, lag, h, use_h);
   };
   CKR(run_while(C, st, begin, body));
   // the triangle of an m-column basis in shared memory when it fits (the inner solves)
@@ -1240,8 +1277,14 @@ int ensure_outer(helm_ctx_s& C, int maxit) {
   const size_t per = 2 * C.L[0].n * sizeof(double2);
   // decomposed: every rank must size the basis alike (the rank-summed dots and the restart
   // points depend on it), so the cap comes from the total, not the free, memory
-  const size_t budget = C.dist ? tot / 4 : fr / 2;
-  m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), budget / per));
+  // an explicit restart length is the method (no cap: fails if it does not fit); a full basis
+  // (restart = 0) is capped by the memory and then restarts, which the report shows
+  const size_t budget = C.dist ? tot / 4 : fr / 100 * 85;
+  const int mreq = m;
+  if (C.p.restart > 0) m = std::min(m, 4096);
+  else m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), budget / per));
+  if (m < mreq && getenv("HELM_VERBOSE"))
+    fprintf(stderr, "[helm] outer basis capped at %d columns (memory); FGMRES(%d)\n", m, m);
   const Level& F = C.L[0];
   return fgm_alloc(C, C.outer, m, (size_t)F.nown * F.g.nx, F.n, (size_t)F.own0 * F.g.nx, rank_summed(C));
 }
@@ -1859,7 +1902,8 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
   if (C->dist) return no_dist(C, "helm_bench_graph");
   helm_ctx_s& X = *C;
   if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
-  if ((which == HELM_GB_DCGS || which == HELM_GB_INNER_ITER) && (arg < 0 || arg + reps >= X.inner.m))
+  if ((which == HELM_GB_DCGS || which == HELM_GB_INNER_ITER || which == HELM_GB_E_DOTS ||
+       which == HELM_GB_DCGS_REDUCE || which == HELM_GB_DCGS_UPDATE) && (arg < 0 || arg + reps >= X.inner.m))
     return fail(HELM_EINVAL, "bad column");
   const Level& F = X.L[0];
   const Level& G = X.L[1];
@@ -1886,7 +1930,10 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         r = op_apply(X, 0, DVec(X.dq), DVec(), DVec(X.dt), 1.0, 0.0);
         break;
       case HELM_GB_DCGS:
-      case HELM_GB_INNER_ITER: {
+      case HELM_GB_INNER_ITER:
+      case HELM_GB_E_DOTS:
+      case HELM_GB_DCGS_REDUCE:
+      case HELM_GB_DCGS_UPDATE: {
         // one delayed-CGS2 step of the inner FGMRES at column j = arg (+ the reps before it);
         // HELM_GB_INNER_ITER: the whole inner iteration (V-cycle from level 1, E, DCGS2 step)
         Fgm& K = X.inner;
@@ -1900,44 +1947,21 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
           if (r != HELM_OK) break;
         }
         const long long ln = (long long)K.n;
-        DVec vj(K.V, &st->j, ln, &st->inv_hn), w(K.V + K.n, &st->j, ln);
-        const GsGeom& gg = K.geo;
+        DVec vj(K.V, &st->j, ln, &st->inv_hn), zj(K.Z, &st->j, ln);
         if (which == HELM_GB_INNER_ITER) {
-          DVec zj(K.Z, &st->j, ln);
           r = vcycle(X, 1, vj, zj, nullptr);
           if (r != HELM_OK) break;
-          r = apply_E(X, zj, DVec(), w);
-          if (r != HELM_OK) break;
         }
-        // probe: HELM_GB_DCGS_MASK selects the step's kernels (1 dots, 2 reduceA, 4 update; default 7)
+        // the solve's own Arnoldi step (fused E + pass 1 when the solve fuses them, lagged step B
+        // as in the first inner cycle); HELM_GB_DCGS_MASK (probe) or the per-kernel regions
+        // select its kernels
         const char* mk = getenv("HELM_GB_DCGS_MASK");
-        const int mask = mk ? atoi(mk) : 7;
-        const bool cld = K.gxc > 0;
-        if ((mask & 1) && cld) {
-          launch_kc(X, k_dcgs_dots_cl, dim3(K.gxc * DC_CL, gg.gy), DC_THREADS, (size_t)(2 * K.m + 4) * sizeof(double2),
-                    DC_CL, K.V, ln, (const int*)&st->j, 1, vj, w, ln, gg.chunk, K.cpart);
-          r = post_launch(X);
-          if (r != HELM_OK) break;
-        } else if (mask & 1) {
-          launch_k(X, k_dcgs_dots, dim3(gg.gx, gg.gy), DC_THREADS, dcgs_dots_smem(K), K.V, ln, (const int*)&st->j, 1,
-                   vj, w, ln, gg.chunk, K.part);
-          r = post_launch(X);
-          if (r != HELM_OK) break;
-        }
-        if ((mask & 2) && !cld) {
-          launch_k(X, k_dcgs_reduceA, ((2 * K.m + 2) * 32 + 255) / 256, 256, dcgs_smem(K.m), K.part,
-                   (long long)gg.gx, st, K.H, K.cs, K.sn, K.g, K.dots1, K.coef, K.sc2, K.rawc, (unsigned*)nullptr);
-          r = post_launch(X);
-          if (r != HELM_OK) break;
-        }
-        if (!(mask & 4)) break;
-        launch_k(X, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), K.V,
-                 ln, (const int*)&st->j, (const double2*)K.dots1, vj, w, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
-                 K.cnt + 1, cudaGraphConditionalHandle(0), 0,
-                 (getenv("HELM_GB_UPD_FLAGS") ? atoi(getenv("HELM_GB_UPD_FLAGS")) : (X.p.lag_stepb ? 7 : 3)) |
-                     (cld ? 8 : 0),
-                 (const double2*)K.cpart, K.gxc, dcgs_sab_len(K.m));
-        r = post_launch(X);
+        int mask = mk ? atoi(mk) : 7;
+        if (which == HELM_GB_E_DOTS) mask = 1;
+        if (which == HELM_GB_DCGS_REDUCE) mask = 2;
+        if (which == HELM_GB_DCGS_UPDATE) mask = 4;
+        auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(X, x, f, y, f.p == nullptr); };
+        r = arnoldi_step(X, K, opA, fused_E_dots(X), inner_lag(X), cudaGraphConditionalHandle(0), 0, mask);
         break;
       }
       default:

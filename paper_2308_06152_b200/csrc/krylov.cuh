@@ -670,8 +670,8 @@ __global__ void __launch_bounds__(256) k_dcgs_reduceA(const double2* __restrict_
     for (long long b = lane; b < P; b += 32) s = cadd(s, part[(long long)c * P + b]);
     s = warp_sum2(s);
     if (lane == 0) dots[c] = s;
-  } else if (lane == 0) {
-    dots[c] = make_double2(0.0, 0.0);   // unused tail zeroed: a rank-sum over all slots stays finite
+  } else if (lane == 0 && c < ((2 * st->m + 4 + 7) & ~7)) {
+    dots[c] = make_double2(0.0, 0.0);   // unused tail zeroed (allocation rounded up to 8 slots)
   }
   // counter == null (decomposed solve): the sums are per rank; step A runs after the allreduce
   if (counter && last_block(counter) && threadIdx.x < 32)
