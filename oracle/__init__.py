@@ -35,5 +35,5 @@ from .transfer import (coarsenable, coarse_shape, coarse_k, restrict_fw, restric
                        restrict_high_order, prolong_high_order)
 from .coarse import apply_coarse_E  # noqa: F401
 from .multigrid import Level, build_hierarchy, vcycle, jacobi_diagonal  # noqa: F401
-from .krylov import fgmres, gcr  # noqa: F401
+from .krylov import fgmres, gcr, gmres_left  # noqa: F401
 from .solver import SolverParams, Solver, solve  # noqa: F401

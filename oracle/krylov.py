@@ -124,6 +124,53 @@ def _fgmres_cycle(apply_A, apply_P, b, tol, maxit, x0, history, orth, bnorm, fir
     return x.reshape(shape), its, converged
 
 
+def gmres_left(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, x0=None, history=None):
+    """Algorithm 1 as printed (§3.3): LEFT-preconditioned GMRES with modified
+    Gram-Schmidt, "r_0 = P(b - A u_0), v_1 = r_0/||r_0||; for j: v~_j = A v_j, w := P v~_j;
+    for i <= j: h_ij = (w, v_i), w := w - h_ij v_i; h_{j+1,j} = ||w||, v_{j+1} = w/h_{j+1,j}",
+    then "minimize ||beta e_1 - H_k y||" and u_k = u_0 + V_k y_k.  The convergence test is on
+    the PRECONDITIONED relative residual ||P r_k|| / ||P r_0|| ("the residual vectors
+    computed by left preconditioning ... correspond to the preconditioned ... residuals"; :1065
+    "we employ left preconditioning and use the preconditioned relative residual as the
+    criterion for convergence").  P must be a fixed operator (an exact coarse solve or a fixed
+    coarse step count).  The least-squares problem is solved directly (numpy lstsq) every step.
+    Returns (x, iterations, converged)."""
+    shape = b.shape
+    bvec = b.ravel()
+    x = np.zeros_like(bvec) if x0 is None else x0.ravel().astype(np.complex128).copy()
+    r = bvec - apply_A(x.reshape(shape)).ravel()
+    r0 = apply_P(r.reshape(shape)).ravel()
+    beta = np.linalg.norm(r0)
+    if history is not None:
+        history.append(1.0)
+    if beta == 0.0:
+        return x.reshape(shape), 0, True
+    V = [r0 / beta]
+    H = np.zeros((maxit + 1, maxit), dtype=np.complex128)
+    y = np.zeros(0, dtype=np.complex128)
+    its, converged = 0, False
+    for j in range(maxit):
+        w = apply_P(apply_A(V[j].reshape(shape))).ravel()
+        for i in range(j + 1):                             # modified Gram-Schmidt
+            H[i, j] = np.vdot(V[i], w)
+            w = w - H[i, j] * V[i]
+        H[j + 1, j] = np.linalg.norm(w)
+        e1 = np.zeros(j + 2, dtype=np.complex128)
+        e1[0] = beta
+        y = np.linalg.lstsq(H[:j + 2, :j + 1], e1, rcond=None)[0]
+        res = np.linalg.norm(H[:j + 2, :j + 1] @ y - e1) / beta
+        its = j + 1
+        if history is not None:
+            history.append(res)
+        if res <= tol or H[j + 1, j] == 0.0:
+            converged = True
+            break
+        V.append(w / H[j + 1, j])
+    for i in range(its):
+        x = x + y[i] * V[i]
+    return x.reshape(shape), its, converged
+
+
 def gcr(apply_A, apply_P, b: np.ndarray, tol: float, maxit: int, history=None):
     """Preconditioned generalised conjugate residual method ("the preconditioned
     Generalized Conjugate Residual method (GCR) [Eisenstat 1983] ... allows for variable

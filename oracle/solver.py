@@ -47,7 +47,7 @@ import numpy as np
 import scipy.linalg
 
 from .coarse import apply_coarse_E
-from .krylov import fgmres, gcr
+from .krylov import fgmres, gcr, gmres_left
 from .multigrid import build_hierarchy, vcycle
 from .operators import apply_A
 from .transfer import coarse_shape, prolong_bilinear, prolong_high_order, restrict_bilinear_zt, restrict_high_order
@@ -71,7 +71,7 @@ class SolverParams:
     maxit: int = 600
     max_levels: int = 64
     coarsest_n: int = 0               # stop coarsening at the first level with <= coarsest_n unknowns (R7)
-    outer: str = "fgmres"             # fgmres | gcr (§6.3)
+    outer: str = "fgmres"             # fgmres | gcr (§6.3) | gmres_left (Algorithm 1 as printed, reading R26)
     preconditioner: str = "adef1"     # adef1 (A-DEF1 / APD) | tlkm (practical TLKM, §3.2.2)
     gamma: float = 1.0                # TLKM shift
 
@@ -176,6 +176,9 @@ class Solver:
         if self.p.outer == "gcr":
             x, its, conv = gcr(self.A, self.precond, np.asarray(b, dtype=np.complex128), self.p.tol, self.p.maxit,
                                history=history)
+        elif self.p.outer == "gmres_left":
+            x, its, conv = gmres_left(self.A, self.precond, np.asarray(b, dtype=np.complex128), self.p.tol,
+                                      self.p.maxit, history=history)
         else:
             x, its, conv = fgmres(self.A, self.precond, np.asarray(b, dtype=np.complex128),
                                   self.p.tol, self.p.maxit, history=history, orth=self.p.orth, restart=self.p.restart)

@@ -242,3 +242,31 @@ def test_restarted_inner_solve_in_the_solver():
     assert r2["converged"] and r2["relres"] <= 1e-8
     assert max(r2["inner_iterations"]) > 4
     np.testing.assert_allclose(x2, x0, rtol=0, atol=1e-6 * np.abs(x0).max())
+
+
+def test_gmres_left_minimises_preconditioned_residual():
+    """Algorithm 1 as printed (oracle.gmres_left, reading R26): the k-th iterate minimises the
+    PRECONDITIONED residual ||P(b - A x)|| over x in K_k(PA, Pb) (Saad 1993, left-preconditioned
+    GMRES).  Reference: dense least squares over the explicit Krylov basis, for k = 1..5; and
+    exactness in n steps, with the stop on ||P r|| / ||P b||."""
+    A, b = _dense_system(20, 11, 5.0)
+    rng = np.random.default_rng(12)
+    P = np.eye(20) + 0.2 * (rng.standard_normal((20, 20)) + 1j * rng.standard_normal((20, 20)))
+    for kk in range(1, 6):
+        x, its, conv = oracle.gmres_left(lambda v: A @ v, lambda v: P @ v, b, 0.0, kk)
+        K = [P @ b]
+        for _i in range(kk - 1):
+            K.append(P @ (A @ K[-1]))
+        Kb = np.array(K).T
+        c = np.linalg.lstsq(P @ A @ Kb, P @ b, rcond=None)[0]
+        assert its == kk
+        np.testing.assert_allclose(x, Kb @ c, rtol=1e-8, atol=1e-12)
+    hist = []
+    x, its, conv = oracle.gmres_left(lambda v: A @ v, lambda v: P @ v, b, 1e-12, 40, history=hist)
+    assert conv and its <= 20
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-9)
+    # the stopping quantity is the preconditioned relative residual
+    assert np.linalg.norm(P @ (b - A @ x)) / np.linalg.norm(P @ b) <= 1e-12 * 1.01
+    # exact preconditioner: one step
+    x, its, conv = oracle.gmres_left(lambda v: A @ v, lambda v: np.linalg.solve(A, v), b, 1e-10, 5)
+    assert its == 1 and conv
