@@ -249,8 +249,9 @@ def kernel_roofline(H, rep, method, peaks, workload):
     regions that call the solve's own Arnoldi-step code) captured into a graph and replayed warm,
     at the solve's mean inner basis column.  Launch counts per step are the solve's own counts;
     the dominant kernel is the one with the largest count x time.  Algorithmic bytes per launch
-    (DESIGN.md §5, per coarse unknown n1 / fine unknown n0): fused E + pass 1 (64 + 16(j+1) + 16);
-    pass 2 (16 j + 64); V-cycle from level 1 sum_l 104 n_l + the dense coarsest inverse; A 40 n0."""
+    (DESIGN.md §5, per coarse unknown n1 / fine unknown n0): E 64 (x 16, fine k 4 x 8, y 16);
+    pass 1 16 (j + 2) (V_0..V_j and w); fused E + pass 1 (64 + 16(j+1) + 16); pass 2 (16 j + 64);
+    V-cycle from level 1 sum_l 104 n_l + the dense coarsest inverse; A 40 n0."""
     inner_its = rep["inner_iterations_total"]
     outer_its = rep["outer_iterations"]
     jm = mean_inner_column(rep, method)
@@ -258,13 +259,21 @@ def kernel_roofline(H, rep, method, peaks, workload):
     n0, n1 = lv[0], lv[1]
     tiles = -(-H.levels[1][1] // 16) * -(-H.levels[1][0] // 8)
     vbytes = sum(104.0 * lv[l] for l in range(1, len(lv) - 1)) + 16.0 * lv[-1] ** 2 + 32.0 * lv[-1]
-    fused = method.get("coarse_op", "galerkin") == "galerkin"
-    comps = [
-        ("k_galerkin_apply<2,0,16,8,true> (E = Z^T A Z fused with DCGS2 pass 1)" if fused else
-         "E apply + k_dcgs_dots (DCGS2 pass 1)", "e_dots", jm, 4, inner_its, (64.0 + 16 * (jm + 1) + 16) * n1),
+    prm = H.params
+    galerkin = method.get("coarse_op", "galerkin") == "galerkin"
+    fused = galerkin and bool(prm.fuse_dots)
+    comps = []
+    if fused:
+        comps.append(("k_galerkin_apply<2,0,16,8,true> (E = Z^T A Z fused with DCGS2 pass 1)", "e_dots", jm, 4,
+                      inner_its, (64.0 + 16 * (jm + 1) + 16) * n1))
+    else:
+        comps.append(("k_glk_stream<2,0> (E = Z^T A Z, column streaming)" if galerkin and prm.e_stream else
+                      "E apply (coarse operator)", "apply_E", 0, 10, inner_its, 64.0 * n1))
+        comps.append(("k_dcgs_dots (DCGS2 pass 1)", "dcgs_dots", jm, 4, inner_its, 16.0 * (jm + 2) * n1))
+    comps += [
         ("k_dcgs_update (DCGS2 pass 2 + step B)", "dcgs_update", jm, 4, inner_its, (16.0 * jm + 64) * n1),
         ("k_dcgs_reduceA (pass-1 partial sums + step A)", "dcgs_reduce", jm, 4, inner_its,
-         (2 * jm + 2) * 16.0 * (tiles if fused else 1) + 0.0),
+         (2 * jm + 2) * 16.0 * (tiles if fused else -(-n1 // 256))),
         ("V-cycle from level 1 (inner CSLP preconditioner, 13 kernels)", "vcycle", 1, 10, inner_its + outer_its,
          vbytes),
         ("k_apply_op A (level 0)", "apply_A", 0, 10, 2 * outer_its, 40.0 * n0),
@@ -276,7 +285,7 @@ def kernel_roofline(H, rep, method, peaks, workload):
         rows[label] = {"kernel": label, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                        "frac": gbs / peaks["hbm_gbs"], "traffic": None, "bytes_per_launch": nbytes,
                        "us_per_launch": us, "launches_per_step": count, "est_ms_per_step": count * us * 1e-3,
-                       "column": arg if region in ("e_dots", "dcgs_update", "dcgs_reduce") else None,
+                       "column": arg if region in ("e_dots", "dcgs_dots", "dcgs_update", "dcgs_reduce") else None,
                        "timing": "in-graph, warm (helm_bench_graph: the solve's own launch, replayed)",
                        "peak_src": peaks["src"]}
     dom = max(rows.values(), key=lambda r: r["est_ms_per_step"])

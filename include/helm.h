@@ -117,7 +117,10 @@ typedef struct {
                           (the dots against the basis) in one kernel.  Measured slower on B200
                           than the two kernels early in round 1 (0.577 vs 0.568 s per bench
                           solve).  With the final round-1 step (lagged step B, one-wave pass 1)
-                          it is 1.4 % faster (0.506 vs 0.513 s), so 1 (default) */
+                          it was 1.4 % faster (0.506 vs 0.513 s).  Round 2: the column-streaming E
+                          kernel (e_stream) plus the separate dots kernel is faster still at the
+                          configs[4] sizes (E 30 vs 83 us on 1023^2; the fused kernel keeps the
+                          tile form), so 0 (default) */
   int precond;         /* HELM_PRECOND_ADEF1 (default; A-DEF1, or APD with the higher-order vectors)
                           or HELM_PRECOND_TLKM (practical two-level Krylov method, §3.2.2
                           and Tables 1-2: coarse matrix Z^T Z M_2h^-1 A_2h solved by unpreconditioned
@@ -140,6 +143,10 @@ typedef struct {
                           level-1 vectors, Gram-Schmidt cost O(m) per step), the tolerance stays
                           relative to ||c|| and inner_maxit counts steps over all cycles; 0 (default)
                           or m >= inner_maxit = one full cycle.  A-DEF1/APD only (TLKM: 0) */
+  int e_stream;        /* str-Glk E on one GPU (not fused with the dots): 1 (default) = the
+                          column-streaming kernel (fine fields in registers, neighbours by warp
+                          shuffles; the tile kernel's arithmetic), 0 = the shared-memory
+                          tile kernel */
 } helm_params;
 
 typedef struct {
@@ -242,6 +249,7 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
                                  str-Glk and fuse_dots; else the E apply and the dots kernel) */
 #define HELM_GB_DCGS_REDUCE 6 /* reduction of the pass-1 partials + step A coefficients */
 #define HELM_GB_DCGS_UPDATE 7 /* pass 2 (v_j, w') + step B (advances the column) */
+#define HELM_GB_DCGS_DOTS 8   /* pass 1 alone (k_dcgs_dots) as the unfused step launches it */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 /* ---------------------------------------------------------------------------------------

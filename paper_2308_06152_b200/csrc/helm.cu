@@ -518,6 +518,15 @@ int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
 
 constexpr int GLK_TX = 16, GLK_TY = 8;   // coarse outputs per k_galerkin_apply CTA
 
+// Rows per warp segment of k_glk_stream: enough warps for ~16 per SM (28 columns per warp),
+// at least 8 rows (4 rows of warm-up per segment), at most 64.
+int glk_stream_rows(const helm_ctx_s& C, int ncx, int ncy) {
+  const long long nb = (ncx + 27) / 28;
+  const long long target = 16LL * C.sm_count;
+  long long S = (ncy * nb + target - 1) / target;
+  return (int)std::max(8LL, std::min(64LL, S));
+}
+
 // Fused inner-solve step (single GPU, str-Glk): w = E x and pass 1 of the delayed CGS2 of the
 // inner FGMRES (dots of s v~_j and w against V_0..V_j) in one kernel; partials per E tile.
 bool fused_E_dots(const helm_ctx_s& C) {
@@ -559,6 +568,20 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y, bool fresh = false) {
       x = shift(x, wo);
       f = shift(f, wo);
       y = shift(y, wo);
+      if (C.p.e_stream && !C.dist) {   // column-streaming kernel (registers, no shared-memory tiles)
+        const int nb = (Gw.g.nx + 27) / 28;
+        const int S = glk_stream_rows(C, Gw.g.nx, Gw.g.ny);
+        const long long warps = (long long)nb * ((Gw.g.ny + S - 1) / S);
+        const dim3 gs((unsigned)((warps + 3) / 4));
+        if (C.p.vectors == HELM_VECTORS_BILINEAR) {
+          if (res) launch_k(C, k_glk_stream<1, 1>, gs, dim3(128), 0, F.g, Gw.g, F.o, F.k, x, f, y, S, nb);
+          else launch_k(C, k_glk_stream<1, 0>, gs, dim3(128), 0, F.g, Gw.g, F.o, F.k, x, f, y, S, nb);
+        } else {
+          if (res) launch_k(C, k_glk_stream<2, 1>, gs, dim3(128), 0, F.g, Gw.g, F.o, F.k, x, f, y, S, nb);
+          else launch_k(C, k_glk_stream<2, 0>, gs, dim3(128), 0, F.g, Gw.g, F.o, F.k, x, f, y, S, nb);
+        }
+        return post_launch(C);
+      }
       const dim3 gt((Gw.g.nx + GLK_TX - 1) / GLK_TX, (Gw.g.ny + GLK_TY - 1) / GLK_TY);
       if (C.p.vectors == HELM_VECTORS_BILINEAR) {
         if (res) launch_k(C, k_galerkin_apply<1, 1, GLK_TX, GLK_TY>, gt, dim3(32, 8), 0, F.g, Gw.g, F.o, F.k, x, f, y,
@@ -631,9 +654,38 @@ void col_up_t(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const doubl
     launch_k(C, k_vc_up_cpa<PF ? PF : 1, SEG>, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f,
              (const double*)L.k, sr, si, w, addq, u_out);
 }
+// Segment length for a level of nx x ny fine unknowns: the longest of 256/128/64/32/16 rows that
+// still gives ~16 warps per SM (28 columns per warp); large levels keep the tuned (4, 256/128).
+int col_seg(const helm_ctx_s& C, const Level& L, int longest) {
+  const long long wcols = (L.g.nx + COL_OWN - 1) / COL_OWN;
+  const long long target = 16LL * C.sm_count;
+  int seg = longest;
+  while (seg > 16 && wcols * ((L.g.ny + seg - 1) / seg) < target) seg >>= 1;
+  return seg;
+}
 int col_down(helm_ctx_s& C, const Level& L, const Level& G, DVec f, double sr, double si, double w) {
+  if (C.p.col_pipe == 2 || C.p.col_pipe == 6) {   // 8 / 6 rows in flight, adaptive segments
+    const bool p8 = C.p.col_pipe == 2;
+    switch (col_seg(C, L, 256)) {
+      case 256: p8 ? col_down_t<8, 256>(C, L, G, f, sr, si, w) : col_down_t<6, 256>(C, L, G, f, sr, si, w); break;
+      case 128: p8 ? col_down_t<8, 128>(C, L, G, f, sr, si, w) : col_down_t<6, 128>(C, L, G, f, sr, si, w); break;
+      case 64: p8 ? col_down_t<8, 64>(C, L, G, f, sr, si, w) : col_down_t<6, 64>(C, L, G, f, sr, si, w); break;
+      case 32: p8 ? col_down_t<8, 32>(C, L, G, f, sr, si, w) : col_down_t<6, 32>(C, L, G, f, sr, si, w); break;
+      default: p8 ? col_down_t<8, 16>(C, L, G, f, sr, si, w) : col_down_t<6, 16>(C, L, G, f, sr, si, w);
+    }
+    return post_launch(C);
+  }
+  if (C.p.col_pipe == 1) {
+    switch (col_seg(C, L, 256)) {
+      case 256: col_down_t<4, 256>(C, L, G, f, sr, si, w); break;
+      case 128: col_down_t<4, 128>(C, L, G, f, sr, si, w); break;
+      case 64: col_down_t<4, 64>(C, L, G, f, sr, si, w); break;
+      case 32: col_down_t<4, 32>(C, L, G, f, sr, si, w); break;
+      default: col_down_t<4, 16>(C, L, G, f, sr, si, w);
+    }
+    return post_launch(C);
+  }
   switch (C.p.col_pipe) {
-    case 1: col_down_t<4, 256>(C, L, G, f, sr, si, w); break;
     case 3: col_down_t<3, 64>(C, L, G, f, sr, si, w); break;
     case 4: col_down_t<4, 64>(C, L, G, f, sr, si, w); break;
     case 5: col_down_t<5, 64>(C, L, G, f, sr, si, w); break;
@@ -645,8 +697,25 @@ int col_down(helm_ctx_s& C, const Level& L, const Level& G, DVec f, double sr, d
 }
 int col_up(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2* addq, DVec u_out, double sr,
            double si, double w) {
+  if (C.p.col_pipe == 2 || C.p.col_pipe == 6) {   // 6 rows in flight (8 exceeds the static shared memory)
+    switch (col_seg(C, L, 128)) {
+      case 128: col_up_t<6, 128>(C, L, G, f, addq, u_out, sr, si, w); break;
+      case 64: col_up_t<6, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
+      case 32: col_up_t<6, 32>(C, L, G, f, addq, u_out, sr, si, w); break;
+      default: col_up_t<6, 16>(C, L, G, f, addq, u_out, sr, si, w);
+    }
+    return post_launch(C);
+  }
+  if (C.p.col_pipe == 1) {
+    switch (col_seg(C, L, 128)) {
+      case 128: col_up_t<4, 128>(C, L, G, f, addq, u_out, sr, si, w); break;
+      case 64: col_up_t<4, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
+      case 32: col_up_t<4, 32>(C, L, G, f, addq, u_out, sr, si, w); break;
+      default: col_up_t<4, 16>(C, L, G, f, addq, u_out, sr, si, w);
+    }
+    return post_launch(C);
+  }
   switch (C.p.col_pipe) {
-    case 1: col_up_t<4, 128>(C, L, G, f, addq, u_out, sr, si, w); break;
     case 3: col_up_t<3, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
     case 4: col_up_t<4, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
     case 5: col_up_t<5, 64>(C, L, G, f, addq, u_out, sr, si, w); break;
@@ -1001,7 +1070,7 @@ int arnoldi_step(helm_ctx_s& C, Fgm& K, OpA&& opA, bool fuse, bool lag, cudaGrap
     if (mask & 1) CKR(apply_E_dots(C, zj, w, vjo, Vo, ld, &st->j, K.part));
     const dim3 gt = glk_tiles(C);
     nparts = (long long)gt.x * gt.y;
-  } else if (mask & 1) {
+  } else if ((mask & 1) && !(mask & 8)) {   // mask bit 8 (measurement): pass 1 without E
     CKR(opA(zj, DVec(), w));
   }
   // delayed CGS2: pass 1 (a = V^H v~_j, b = V^H w), step A, pass 2, step B
@@ -1048,7 +1117,8 @@ int arnoldi_step(helm_ctx_s& C, Fgm& K, OpA&& opA, bool fuse, bool lag, cudaGrap
   if (!(mask & 4)) return HELM_OK;
   launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), Vo, ld,
            (const int*)&st->j, (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
-           K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0), (const double2*)K.cpart, K.gxc,
+           K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0) | 16,
+           (const double2*)K.cpart, K.gxc,
            dcgs_sab_len(K.m));
   CKR(post_launch(C));
   if (K.dist) {
@@ -1318,13 +1388,14 @@ void helm_default_params(helm_params* p) {
   p->dist_levels = 0;
   p->dist_min_rows = 16;
   p->col_pipe = 1;
-  p->fuse_dots = 1;
+  p->fuse_dots = 0;
   p->precond = HELM_PRECOND_ADEF1;
   p->gamma = 1.0;
   p->tail_cluster = 0;
   p->lag_stepb = 1;
   p->dots_cluster = 0;
   p->inner_restart = 0;
+  p->e_stream = 1;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1903,7 +1974,8 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
   helm_ctx_s& X = *C;
   if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
   if ((which == HELM_GB_DCGS || which == HELM_GB_INNER_ITER || which == HELM_GB_E_DOTS ||
-       which == HELM_GB_DCGS_REDUCE || which == HELM_GB_DCGS_UPDATE) && (arg < 0 || arg + reps >= X.inner.m))
+       which == HELM_GB_DCGS_REDUCE || which == HELM_GB_DCGS_UPDATE || which == HELM_GB_DCGS_DOTS) &&
+      (arg < 0 || arg + reps >= X.inner.m))
     return fail(HELM_EINVAL, "bad column");
   const Level& F = X.L[0];
   const Level& G = X.L[1];
@@ -1933,7 +2005,8 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
       case HELM_GB_INNER_ITER:
       case HELM_GB_E_DOTS:
       case HELM_GB_DCGS_REDUCE:
-      case HELM_GB_DCGS_UPDATE: {
+      case HELM_GB_DCGS_UPDATE:
+      case HELM_GB_DCGS_DOTS: {
         // one delayed-CGS2 step of the inner FGMRES at column j = arg (+ the reps before it);
         // HELM_GB_INNER_ITER: the whole inner iteration (V-cycle from level 1, E, DCGS2 step)
         Fgm& K = X.inner;
@@ -1960,6 +2033,7 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         if (which == HELM_GB_E_DOTS) mask = 1;
         if (which == HELM_GB_DCGS_REDUCE) mask = 2;
         if (which == HELM_GB_DCGS_UPDATE) mask = 4;
+        if (which == HELM_GB_DCGS_DOTS) mask = 1 | 8;   // pass 1 alone (unfused step)
         auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(X, x, f, y, f.p == nullptr); };
         r = arnoldi_step(X, K, opA, fused_E_dots(X), inner_lag(X), cudaGraphConditionalHandle(0), 0, mask);
         break;

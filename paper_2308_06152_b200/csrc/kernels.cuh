@@ -494,6 +494,173 @@ __global__ void __launch_bounds__(256, DOTS ? HELM_GLKD_MINB : 6) k_galerkin_app
   }
 }
 
+// ------------------------------------------------------------------ str-Glk E by column streaming
+// The same y = Z^T A Z x (or f - E x) as k_galerkin_apply, with the same arithmetic (x-then-y
+// interpolation, A with its zero multipliers skipped, Z^T along y then x, every sum in the same
+// order from zero; results differ only where the compiler contracts a different mul/add pair
+// into an FMA, ~1e-16), but the intermediate fine fields live in registers instead of
+// shared memory: the tile kernel measured shared-memory bound (L1/TEX pipe 78 % busy, DRAM 7 %,
+// ~98 16-byte shared accesses per coarse unknown; ncu, 1023^2 coarse grid).
+// A warp owns 32 consecutive coarse columns I = I0 - 2 + lane (lane L: fine columns
+// fe = 2I + o and fd = fe + 1) and writes the 28 outputs of lanes 2..29; x-neighbours come
+// by warp shuffles, y-neighbours from the last rows kept in registers.  The warp walks a
+// segment of S coarse output rows [J0, J1) from row J0 - 2 (4 rows of warm-up: step J loads
+// x row J + 1, forms t on fine rows fe(J) = 2J + o and fd(J), s = A t on rows fd(J - 1) and
+// fe(J), adds them into the Z^T-along-y sums of output rows J - 1, J, J + 1 and completes row
+// J - 1).  Loads of the next step are issued before the current step's arithmetic.
+#ifndef HELM_GLKS_MINB   // resident 128-thread blocks per SM the register cap aims at
+#define HELM_GLKS_MINB 4
+#endif
+template <int R, int MODE>
+__global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
+                                                    DVec fv, DVec yv, int S, int nbands) {
+  HELM_PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int band = gw % nbands, seg = gw / nbands;
+  const int J0 = seg * S;
+  if (J0 >= gc.ny) return;   // whole warp
+  const int J1 = min(gc.ny, J0 + S);
+  const int I = band * 28 - 2 + lane;
+  const bool xin = I >= 0 && I < gc.nx;
+  const int fe = 2 * I + o, fd = fe + 1;
+  const bool ein = fe >= 0 && fe < gf.nx, din = fd >= 0 && fd < gf.nx;
+  const double2* __restrict__ x = xv.get();
+  const double2 zero = make_double2(0.0, 0.0);
+  const double wm_e = R == 2 ? 0.125 : 0.0, w0_e = R == 2 ? 0.75 : 1.0, wp_e = R == 2 ? 0.125 : 0.0;
+  auto shup = [&](double2 v) {
+    return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+  };
+  auto shdn = [&](double2 v) {
+    return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+  };
+  auto load_x = [&](int J) { return (xin && J >= 0 && J < gc.ny) ? x[(size_t)J * gc.nx + I] : zero; };
+  auto row_in = [&](int fy) { return fy >= 0 && fy < gf.ny; };
+  auto load_k = [&](int fy, int fx, bool in) { return (in && row_in(fy)) ? kf[(size_t)fy * gf.nx + fx] : 0.0; };
+  // x-interpolated coarse row (t before the y interpolation) at this lane's two fine columns
+  struct TX { double2 e, d; };
+  auto xinterp = [&](double2 xs) {
+    const double2 xm = shup(xs), xp = shdn(xs);
+    TX t;
+    // even relative column: taps I-1, I, I+1 (1/8, 3/4, 1/8 | 0, 1, 0); odd: I, I+1 (1/2, 1/2)
+    t.e = ein ? cadd(cadd(cscale(wm_e, xm), cscale(w0_e, xs)), cscale(wp_e, xp)) : zero;
+    t.d = din ? cadd(cadd(cscale(0.0, xm), cscale(0.5, xs)), cscale(0.5, xp)) : zero;
+    return t;
+  };
+  // s = A t at fine row fy for both columns; c = centre row, sth / nth = the rows below / above.
+  // Interior rows of an interior band take constant off-diagonal multipliers (coef_at's values,
+  // same operation order, no boundary branches).
+  const double ih2 = 1.0 / (gf.h * gf.h);
+  const bool band_int = __all_sync(0xffffffffu, fe >= 1 && fd <= gf.nx - 2);
+  auto apply_A_row = [&](int fy, const TX& sth, const TX& c, const TX& nth, double ke, double kd, TX& s) {
+    const double2 west_e = shup(c.d), east_d = shdn(c.e);
+    if (band_int && fy >= 1 && fy <= gf.ny - 2) {
+      const double k2e = ke * ke, k2d = kd * kd;
+      double2 v = cmul(make_double2(4.0 * ih2 - 1.0 * k2e, -0.0 * k2e), c.e);
+      v = cadd(v, cscale(-ih2, west_e));
+      v = cadd(v, cscale(-ih2, c.d));
+      v = cadd(v, cscale(-ih2, sth.e));
+      s.e = cadd(v, cscale(-ih2, nth.e));
+      v = cmul(make_double2(4.0 * ih2 - 1.0 * k2d, -0.0 * k2d), c.d);
+      v = cadd(v, cscale(-ih2, c.e));
+      v = cadd(v, cscale(-ih2, east_d));
+      v = cadd(v, cscale(-ih2, sth.d));
+      s.d = cadd(v, cscale(-ih2, nth.d));
+      return;
+    }
+    s.e = zero;
+    s.d = zero;
+    if (!row_in(fy)) return;
+    if (ein) {
+      const Coef cf = coef_at(gf, fe, fy, ke, 1.0, 0.0);
+      double2 v = cmul(cf.ap, c.e);
+      if (cf.aw != 0.0) v = cadd(v, cscale(cf.aw, west_e));
+      if (cf.ae != 0.0) v = cadd(v, cscale(cf.ae, c.d));
+      if (cf.as != 0.0) v = cadd(v, cscale(cf.as, sth.e));
+      if (cf.an != 0.0) v = cadd(v, cscale(cf.an, nth.e));
+      s.e = v;
+    }
+    if (din) {
+      const Coef cf = coef_at(gf, fd, fy, kd, 1.0, 0.0);
+      double2 v = cmul(cf.ap, c.d);
+      if (cf.aw != 0.0) v = cadd(v, cscale(cf.aw, c.e));
+      if (cf.ae != 0.0) v = cadd(v, cscale(cf.ae, east_d));
+      if (cf.as != 0.0) v = cadd(v, cscale(cf.as, sth.d));
+      if (cf.an != 0.0) v = cadd(v, cscale(cf.an, nth.d));
+      s.d = v;
+    }
+  };
+  auto add = [&](TX& acc, double w, const TX& s) {
+    acc.e = cadd(acc.e, cscale(w, s.e));
+    acc.d = cadd(acc.d, cscale(w, s.d));
+  };
+  const double2* __restrict__ f = fv.get();
+  const double fsc = MODE == 1 ? fv.scale() : 1.0;
+  double2* __restrict__ y = yv.get();
+
+  int J = J0 - 2;
+  // state: tx(J-1), tx(J); t rows fe(J-1), fd(J-1); Z^T_y sums of output rows J-1, J, J+1
+  TX txm = xinterp(load_x(J - 1)), tx0 = xinterp(load_x(J));
+  const TX tz = {zero, zero};
+  TX tfe_m = tz, tfd_m = tz;   // rows fe(J-1), fd(J-1): only feed rows before J0 - 1
+  TX acc0 = tz, acc1 = tz, acc2 = tz;
+  // loads of step J: x row J+1, k on rows fd(J-1) and fe(J)
+  double2 xn = load_x(J + 1);
+  double kfd_e = load_k(2 * J + o - 1, fe, ein), kfd_d = load_k(2 * J + o - 1, fd, din);
+  double kfe_e = load_k(2 * J + o, fe, ein), kfe_d = load_k(2 * J + o, fd, din);
+  for (; J <= J1; ++J) {
+    const double2 xc = xn;
+    const double a_fd_e = kfd_e, a_fd_d = kfd_d, a_fe_e = kfe_e, a_fe_d = kfe_d;
+    if (J < J1) {   // next step's loads, in flight during this step's arithmetic
+      xn = load_x(J + 2);
+      kfd_e = load_k(2 * J + o + 1, fe, ein);
+      kfd_d = load_k(2 * J + o + 1, fd, din);
+      kfe_e = load_k(2 * J + o + 2, fe, ein);
+      kfe_d = load_k(2 * J + o + 2, fd, din);
+    }
+    const TX txp = xinterp(xc);   // tx(J+1)
+    // y interpolation: fine rows fe(J) (taps J-1, J, J+1) and fd(J) (taps J, J+1)
+    TX tfe, tfd;
+    const bool fe_row = row_in(2 * J + o), fd_row = row_in(2 * J + o + 1);
+    tfe.e = fe_row ? cadd(cadd(cscale(wm_e, txm.e), cscale(w0_e, tx0.e)), cscale(wp_e, txp.e)) : zero;
+    tfe.d = fe_row ? cadd(cadd(cscale(wm_e, txm.d), cscale(w0_e, tx0.d)), cscale(wp_e, txp.d)) : zero;
+    tfd.e = fd_row ? cadd(cadd(cscale(0.0, txm.e), cscale(0.5, tx0.e)), cscale(0.5, txp.e)) : zero;
+    tfd.d = fd_row ? cadd(cadd(cscale(0.0, txm.d), cscale(0.5, tx0.d)), cscale(0.5, txp.d)) : zero;
+    // s = A t on rows fd(J-1) (south fe(J-1), north fe(J)) and fe(J) (south fd(J-1), north fd(J))
+    TX s_fdm, s_fe;
+    apply_A_row(2 * J + o - 1, tfe_m, tfd_m, tfe, a_fd_e, a_fd_d, s_fdm);
+    apply_A_row(2 * J + o, tfd_m, tfe, tfd, a_fe_e, a_fe_d, s_fe);
+    // Z^T along y, in increasing fine-row order per output row (b = -R .. R)
+    add(acc0, zw<R>(1), s_fdm);   // output J-1: b = +1, +2
+    if (R == 2) add(acc0, zw<R>(2), s_fe);
+    add(acc1, zw<R>(-1), s_fdm);  // output J: b = -1, 0
+    add(acc1, zw<R>(0), s_fe);
+    if (R == 2) add(acc2, zw<R>(-2), s_fe);   // output J+1: b = -2
+    // output row J-1 is complete: Z^T along x (a = -R .. R), lanes 2..29
+    {
+      const double2 em = shup(acc0.e), dm = shup(acc0.d), ep = shdn(acc0.e);
+      const int Jo = J - 1;
+      if (Jo >= J0 && Jo < J1 && lane >= 2 && lane < 30 && I < gc.nx) {
+        double2 sacc = zero;
+        if (R == 2) sacc = cadd(sacc, cscale(zw<R>(-2), em));
+        sacc = cadd(sacc, cscale(zw<R>(-1), dm));
+        sacc = cadd(sacc, cscale(zw<R>(0), acc0.e));
+        sacc = cadd(sacc, cscale(zw<R>(1), acc0.d));
+        if (R == 2) sacc = cadd(sacc, cscale(zw<R>(2), ep));
+        const size_t p = (size_t)Jo * gc.nx + I;
+        y[p] = (MODE == 1) ? csub(cscale(fsc, f[p]), sacc) : sacc;
+      }
+    }
+    acc0 = acc1;
+    acc1 = acc2;
+    acc2 = tz;
+    txm = tx0;
+    tx0 = txp;
+    tfe_m = tfe;
+    tfd_m = tfd;
+  }
+}
+
 // ------------------------------------------------------------------ ReD-Glk (§5.2.4)
 // Printed stencils: Laplacian part Eq. 5.12 (x 1/(256 H^2)) and wavenumber part Eq. 5.14
 // (x 1/64^2), each tap weighted by the wavenumber at its own coarse node.

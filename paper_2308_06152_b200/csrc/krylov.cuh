@@ -579,8 +579,12 @@ __global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const 
     double2* x = xv.get();
     double2* w = wv.get();
     const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
+    // flags & 16: sweep the tiles from the top down, so that pass 2 starts on the elements whose
+    // basis values pass 1 (ascending chunks) read last and L2 still holds
+    const bool rev = (flags & 16) != 0;
     for (long long tile = tb; tile < tiles; tile += nb)
-      nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, tile, red);
+      nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, rev ? tiles - 1 - tile : tile,
+                                                       red);
   }
   const double t = block_sum(nrm);
   if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);

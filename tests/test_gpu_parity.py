@@ -362,6 +362,27 @@ def test_fused_E_dots_matches(lib, vec):
     assert rel(out[1][0], out[0][0]) < 1e-10
 
 
+@pytest.mark.parametrize("vec", ["bilinear", "high_order"])
+def test_streaming_E_bitwise_tile_kernel(lib, vec):
+    """The column-streaming str-Glk kernel (e_stream = 1, the default) performs the tile kernel's
+    arithmetic in the same order (up to the compiler's FMA contraction, which differs between the
+    two kernels): E x equal to 1e-14 relative on every parity grid, on a ragged grid
+    wider than several 28-column warp bands and taller than several row segments, and on
+    the configs[4] 2047^2 block (1023^2 coarse)."""
+    grids = GRIDS + [P(255, 127, 1 / 256, "dirichlet", random_k((127, 255), 8, 10, 90)),
+                     P(193, 97, 1 / 192, "sommerfeld", random_k((97, 193), 9, 5, 70))]
+    big = config_problem("c4_weak_2049")
+    grids.append(P(big.nx, big.ny, big.h, big.bc, big.k))
+    for p in grids:
+        ys = []
+        for es in (0, 1):
+            H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"coarse_op": "galerkin", "vectors": vec, "e_stream": es})
+            x = random_field(H.levels[1][:2], 11)
+            ys.append(H.apply_E(gpu(x)).cpu().numpy())
+            H.close()
+        assert rel(ys[1], ys[0]) < 1e-14, (p.shape, p.bc, vec, rel(ys[1], ys[0]))
+
+
 
 @pytest.mark.parametrize("vec", ["bilinear", "high_order"])
 def test_tlkm_apply_and_solve(lib, vec):
