@@ -250,6 +250,8 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_DCGS_REDUCE 6 /* reduction of the pass-1 partials + step A coefficients */
 #define HELM_GB_DCGS_UPDATE 7 /* pass 2 (v_j, w') + step B (advances the column) */
 #define HELM_GB_DCGS_DOTS 8   /* pass 1 alone (k_dcgs_dots) as the unfused step launches it */
+#define HELM_GB_VC_DOWN 9     /* the fused V-cycle down leg of level `arg`, as the V-cycle launches it */
+#define HELM_GB_VC_UP 10      /* the fused V-cycle up leg of level `arg` */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 /* ---------------------------------------------------------------------------------------

@@ -522,7 +522,8 @@ constexpr int GLK_TX = 16, GLK_TY = 8;   // coarse outputs per k_galerkin_apply 
 // at least 8 rows (4 rows of warm-up per segment), at most 64.
 int glk_stream_rows(const helm_ctx_s& C, int ncx, int ncy) {
   const long long nb = (ncx + 27) / 28;
-  const long long target = 16LL * C.sm_count;
+  static const int wps = getenv("HELM_PROBE_COL_WPS") ? atoi(getenv("HELM_PROBE_COL_WPS")) : 16;   // probe only
+  const long long target = (long long)wps * C.sm_count;
   long long S = (ncy * nb + target - 1) / target;
   return (int)std::max(8LL, std::min(64LL, S));
 }
@@ -726,6 +727,53 @@ int col_up(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2*
   return post_launch(C);
 }
 
+// The fused legs of level l (nu_pre = nu_post = 1): large levels stream columns, small levels
+// run shared-memory tiles (smaller tiles below one wave of big tiles, so that more SMs share the
+// latency-bound work).  Shared by vcycle() and the single-leg bench regions.
+#ifndef HELM_SMALL_TILES_X   // measured: 1 (small tiles only below one wave of big tiles) -1.3 % per solve vs 2
+#define HELM_SMALL_TILES_X 1
+#endif
+#ifndef HELM_UP_SMALL_X   // up leg: small tiles also while the big up tiles are < X waves (0: as the down leg)
+#define HELM_UP_SMALL_X 0
+#endif
+bool vc_col_level(const helm_ctx_s& C, const Level& L) {
+  return C.p.col_min_n >= 0 && (long long)L.n >= C.p.col_min_n;
+}
+bool vc_small_tiles(const helm_ctx_s& C, const Level& G) {
+  return (size_t)((G.g.nx + DOWN_TX - 1) / DOWN_TX) * ((G.g.ny + DOWN_TY - 1) / DOWN_TY) <
+         (size_t)HELM_SMALL_TILES_X * C.sm_count;
+}
+int vc_down_leg(helm_ctx_s& C, int l, DVec f) {
+  Level& L = C.L[l];
+  const Level G = coarse_of(C, l);
+  const double sr = C.p.beta1, si = C.p.beta2, w = C.p.omega;
+  if (vc_col_level(C, L)) return col_down(C, L, G, f, sr, si, w);
+  if (vc_small_tiles(C, G)) {
+    dim3 gd((G.g.nx + 7) / 8, (G.g.ny + 3) / 4);
+    launch_k(C, k_vc_down<8, 4>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+  } else {
+    dim3 gd((G.g.nx + DOWN_TX - 1) / DOWN_TX, (G.g.ny + DOWN_TY - 1) / DOWN_TY);
+    launch_k(C, k_vc_down<DOWN_TX, DOWN_TY>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
+  }
+  return post_launch(C);
+}
+int vc_up_leg(helm_ctx_s& C, int l, DVec f, const double2* addq, DVec u_out) {
+  Level& L = C.L[l];
+  const Level G = coarse_of(C, l);
+  const double sr = C.p.beta1, si = C.p.beta2, w = C.p.omega;
+  if (vc_col_level(C, L)) return col_up(C, L, G, f, addq, u_out, sr, si, w);
+  const bool small_up = vc_small_tiles(C, G) || (size_t)((L.g.nx + UP_TX - 1) / UP_TX) * ((L.g.ny + UP_TY - 1) / UP_TY) <
+                                                   (size_t)HELM_UP_SMALL_X * C.sm_count;
+  if (small_up) {
+    dim3 gu((L.g.nx + 15) / 16, (L.g.ny + 7) / 8);
+    launch_k(C, k_vc_up<16, 8>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+  } else {
+    dim3 gu((L.g.nx + UP_TX - 1) / UP_TX, (L.g.ny + UP_TY - 1) / UP_TY);
+    launch_k(C, k_vc_up<UP_TX, UP_TY>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
+  }
+  return post_launch(C);
+}
+
 // u_out = V-cycle approximation of M_l^{-1} f (+ addq), starting at level l.
 // Decomposed contexts -- fresh ghosts: the legs compute every row of a block, so an output is
 // exact wherever its inputs are; with f's halo refreshed (GHOST = 6 rows) and the coarse
@@ -753,45 +801,12 @@ int vcycle(helm_ctx_s& C, int l, DVec f, DVec u_out, const double2* addq) {
   Level& Gs = C.L[l + 1];
   const bool gather = gathers(C, l);
   CKR(halo(C, l, f));
-  if (fused_vcycle(C) && C.p.col_min_n >= 0 && (long long)L.n >= C.p.col_min_n) {
-    // large levels: column-streaming legs (no shared-memory staging)
-    CKR(col_down(C, L, G, f, sr, si, w));
-    if (gather) CKR(allgather(C, l + 1));
-    CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
-    // no halo for Gs.u: a V-cycle output is valid on its owned rows +- 4 (fresh ghosts, below)
-    return col_up(C, L, G, f, addq, u_out, sr, si, w);
-  }
   if (fused_vcycle(C)) {
-    // small levels: smaller tiles so that more SMs share the (latency-bound) work
-#ifndef HELM_SMALL_TILES_X   // measured: 1 (small tiles only below one wave of big tiles) -1.3 % per solve vs 2
-#define HELM_SMALL_TILES_X 1
-#endif
-    const bool small = (size_t)((G.g.nx + DOWN_TX - 1) / DOWN_TX) * ((G.g.ny + DOWN_TY - 1) / DOWN_TY) <
-                       (size_t)HELM_SMALL_TILES_X * C.sm_count;
-    if (small) {
-      dim3 gd((G.g.nx + 7) / 8, (G.g.ny + 3) / 4);
-      launch_k(C, k_vc_down<8, 4>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
-    } else {
-      dim3 gd((G.g.nx + DOWN_TX - 1) / DOWN_TX, (G.g.ny + DOWN_TY - 1) / DOWN_TY);
-      launch_k(C, k_vc_down<DOWN_TX, DOWN_TY>, gd, dim3(32, 8), 0, L.g, G.g, L.o, f, L.k, sr, si, w, L.s, G.f);
-    }
-    CKR(post_launch(C));
+    CKR(vc_down_leg(C, l, f));
     if (gather) CKR(allgather(C, l + 1));
     CKR(vcycle(C, l + 1, DVec(Gs.f), DVec(Gs.u), nullptr));
     // no halo for Gs.u: a V-cycle output is valid on its owned rows +- 4 (fresh ghosts, below)
-#ifndef HELM_UP_SMALL_X   // up leg: small tiles also while the big up tiles are < X waves (0: as the down leg)
-#define HELM_UP_SMALL_X 0
-#endif
-    const bool small_up = small || (size_t)((L.g.nx + UP_TX - 1) / UP_TX) * ((L.g.ny + UP_TY - 1) / UP_TY) <
-                                       (size_t)HELM_UP_SMALL_X * C.sm_count;
-    if (small_up) {
-      dim3 gu((L.g.nx + 15) / 16, (L.g.ny + 7) / 8);
-      launch_k(C, k_vc_up<16, 8>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
-    } else {
-      dim3 gu((L.g.nx + UP_TX - 1) / UP_TX, (L.g.ny + UP_TY - 1) / UP_TY);
-      launch_k(C, k_vc_up<UP_TX, UP_TY>, gu, dim3(32, 8), 0, L.g, G.g, L.o, L.s, G.u, f, L.k, sr, si, w, addq, u_out);
-    }
-    return post_launch(C);
+    return vc_up_leg(C, l, f, addq, u_out);
   }
   // generic sweep counts
   double2* cur = L.s;
@@ -1049,6 +1064,16 @@ bool inner_lag(const helm_ctx_s& C) {
   return C.p.lag_stepb && !K.dist && K.coop == 0 && bs <= 96 * 1024 && K.m >= 3;
 }
 
+// Pass 2 by warp strips (k_dcgs_update flags & 32) when the vectors give every resident warp
+// several strips; short vectors (the c1 inner level) keep the tile form, which splits the basis
+// over a block's warps.  HELM_PROBE_DU_STRIP=0/1 forces either (probe only).
+bool du_strips(const Fgm& K) {
+  static const int force = getenv("HELM_PROBE_DU_STRIP") ? atoi(getenv("HELM_PROBE_DU_STRIP")) : -1;
+  if (force >= 0) return force != 0;
+  const long long strips = ((long long)K.n + 32 * DU_SEPL - 1) / (32 * DU_SEPL);
+  return strips >= 4LL * K.geo.gu * DU_WARPS;
+}
+
 // One Arnoldi step of an FGMRES cycle after the preconditioner (z_j = P v~_j is in K.Z[j]):
 // w = A z_j and the delayed CGS2 of column j -- pass 1 (a = V^H v~_j, b = V^H w; fused into the
 // inner E apply when `fuse`), reduction + step A, pass 2 + step B.  Shared by fgmres_cycle and
@@ -1117,7 +1142,7 @@ int arnoldi_step(helm_ctx_s& C, Fgm& K, OpA&& opA, bool fuse, bool lag, cudaGrap
   if (!(mask & 4)) return HELM_OK;
   launch_k(C, k_dcgs_update, gg.gu + 1, DU_THREADS, cld ? dcgs_update_smem_cl(K.m) : dcgs_update_smem(K.m), Vo, ld,
            (const int*)&st->j, (const double2*)K.dots1, vjo, wo, ln, K.part, st, K.H, K.cs, K.sn, K.g, K.rawc,
-           K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0) | 16,
+           K.cnt + 1, h, use_h, (K.dist ? 2 : (lag ? 7 : 3)) | (cld ? 8 : 0) | 16 | (du_strips(K) ? 32 : 0),
            (const double2*)K.cpart, K.gxc,
            dcgs_sab_len(K.m));
   CKR(post_launch(C));
@@ -1973,6 +1998,8 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
   if (C->dist) return no_dist(C, "helm_bench_graph");
   helm_ctx_s& X = *C;
   if (which == HELM_GB_VCYCLE && (arg < 0 || arg >= (int)X.L.size())) return fail(HELM_EINVAL, "bad level");
+  if ((which == HELM_GB_VC_DOWN || which == HELM_GB_VC_UP) && (arg < 0 || arg + 1 >= (int)X.L.size() || !fused_vcycle(X)))
+    return fail(HELM_EINVAL, "bad level (or no fused legs)");
   if ((which == HELM_GB_DCGS || which == HELM_GB_INNER_ITER || which == HELM_GB_E_DOTS ||
        which == HELM_GB_DCGS_REDUCE || which == HELM_GB_DCGS_UPDATE || which == HELM_GB_DCGS_DOTS) &&
       (arg < 0 || arg + reps >= X.inner.m))
@@ -1993,6 +2020,14 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         double2* uout = arg == 0 ? X.dq : X.L[arg - 1].t;
         (void)L;
         r = vcycle(X, arg, DVec(fin), DVec(uout), nullptr);
+        break;
+      }
+      case HELM_GB_VC_DOWN:
+      case HELM_GB_VC_UP: {
+        // one fused leg of level `arg`, as vcycle() launches it
+        double2* fin = arg == 0 ? X.dt : X.L[arg - 1].s;
+        double2* uout = arg == 0 ? X.dq : X.L[arg - 1].t;
+        r = which == HELM_GB_VC_DOWN ? vc_down_leg(X, arg, DVec(fin)) : vc_up_leg(X, arg, DVec(fin), nullptr, DVec(uout));
         break;
       }
       case HELM_GB_APPLY_E:

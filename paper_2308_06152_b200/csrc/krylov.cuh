@@ -31,6 +31,17 @@ namespace cg = cooperative_groups;
 #endif
 namespace helm {
 
+// L2 eviction hints of the Gram-Schmidt basis streams (HELM_L2H bit 1: pass 1, bit 2: pass 2):
+// evict-first loads (ld.global.cs) leave the V-cycle / E fields of the step in L2.
+#ifndef HELM_L2H
+#define HELM_L2H 3   // measured on c4_weak_2049: -2.4 % per inner iteration (profiles/r02_ab_l2h.jsonl)
+#endif
+template <int BIT>
+__device__ __forceinline__ double2 ldb(const double2* p) {
+  if (HELM_L2H & BIT) return __ldcs(p);
+  return *p;
+}
+
 constexpr int GS_NV = 8;         // basis vectors per sweep of a chunk in the dot pass
 constexpr int GS_THREADS = 256;
 constexpr int GS_WARPS = GS_THREADS / 32;
@@ -318,8 +329,8 @@ __device__ __forceinline__ void dcgs_dots_item(const double2* __restrict__ V, lo
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const bool ok = sub + lane + 32 * t < e1;
-        a[t] = ok ? va[32 * t] : make_double2(0.0, 0.0);
-        b[t] = (ok && two) ? vb[32 * t] : make_double2(0.0, 0.0);
+        a[t] = ok ? ldb<1>(va + 32 * t) : make_double2(0.0, 0.0);
+        b[t] = (ok && two) ? ldb<1>(vb + 32 * t) : make_double2(0.0, 0.0);
       }
       double2 ax = make_double2(0.0, 0.0), aw = ax, bxx = ax, bw = ax;
 #pragma unroll
@@ -472,8 +483,8 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
       const bool ok = eb + 32 * q < n;
-      v0[q] = ok ? v0p[32 * q] : make_double2(0.0, 0.0);
-      v1[q] = ok ? v1p[32 * q] : make_double2(0.0, 0.0);
+      v0[q] = ok ? ldb<2>(v0p + 32 * q) : make_double2(0.0, 0.0);
+      v1[q] = ok ? ldb<2>(v1p + 32 * q) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
@@ -488,7 +499,7 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
     const double2* v0p = V + (long long)c * ld + eb;
 #pragma unroll
     for (int q = 0; q < EPL; ++q) {
-      const double2 v0 = (eb + 32 * q < n) ? v0p[32 * q] : make_double2(0.0, 0.0);
+      const double2 v0 = (eb + 32 * q < n) ? ldb<2>(v0p + 32 * q) : make_double2(0.0, 0.0);
       sa[q] = cfma(ca0, v0, sa[q]);
       sb[q] = cfma(cb0, v0, sb[q]);
     }
@@ -521,7 +532,70 @@ __device__ __forceinline__ double dcgs_update_tile(const double2* __restrict__ V
 }
 
 
-// flags: 1 = step B in the last block to finish (4: lagged, dcgs_stepB_lag_warp; needs 2); 2 = the
+// Warp-strip form of the same pass 2 (flags & 32, long vectors): a warp owns 32 * SEPL
+// consecutive elements and streams ALL j basis vectors for them (DU_U vectors per round, so
+// DU_U * SEPL independent 16-byte loads per lane are in flight), with the accumulators in
+// registers -- no cross-warp combination, no block barrier.  Needs n / (32 SEPL) >> the number of
+// resident warps (the tile form splits the basis over the warps for short vectors instead).
+constexpr int DU_SEPL = 2;   // elements per lane of a strip
+constexpr int DU_U = 8;      // basis vectors per round
+__device__ __forceinline__ double dcgs_update_strip(const double2* __restrict__ V, long long ld, int j,
+                                                    const double2* sab, double ib, double2 hjj, double2* x,
+                                                    double2* w, long long n, long long strip) {
+  constexpr int SE = 32 * DU_SEPL;
+  const int lane = threadIdx.x & 31;
+  const long long eb = strip * SE + lane;
+  bool ok[DU_SEPL];
+  double2 xr[DU_SEPL], wr[DU_SEPL], sa[DU_SEPL], sb[DU_SEPL];
+#pragma unroll
+  for (int q = 0; q < DU_SEPL; ++q) {
+    ok[q] = eb + 32 * q < n;
+    xr[q] = ok[q] ? x[eb + 32 * q] : make_double2(0.0, 0.0);
+    wr[q] = ok[q] ? w[eb + 32 * q] : make_double2(0.0, 0.0);
+    sa[q] = sb[q] = make_double2(0.0, 0.0);
+  }
+  int c = 0;
+  for (; c + DU_U <= j; c += DU_U) {
+    double2 v[DU_U][DU_SEPL];
+#pragma unroll
+    for (int u = 0; u < DU_U; ++u)
+#pragma unroll
+      for (int q = 0; q < DU_SEPL; ++q)
+        v[u][q] = ok[q] ? ldb<2>(V + (long long)(c + u) * ld + eb + 32 * q) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < DU_U; ++u) {
+      const double2 ca = sab[2 * (c + u)], cb = sab[2 * (c + u) + 1];
+#pragma unroll
+      for (int q = 0; q < DU_SEPL; ++q) {
+        sa[q] = cfma(ca, v[u][q], sa[q]);
+        sb[q] = cfma(cb, v[u][q], sb[q]);
+      }
+    }
+  }
+  for (; c < j; ++c) {
+    const double2 ca = sab[2 * c], cb = sab[2 * c + 1];
+#pragma unroll
+    for (int q = 0; q < DU_SEPL; ++q) {
+      const double2 v0 = ok[q] ? ldb<2>(V + (long long)c * ld + eb + 32 * q) : make_double2(0.0, 0.0);
+      sa[q] = cfma(ca, v0, sa[q]);
+      sb[q] = cfma(cb, v0, sb[q]);
+    }
+  }
+  double nrm = 0.0;
+#pragma unroll
+  for (int q = 0; q < DU_SEPL; ++q) {
+    if (!ok[q]) continue;
+    const double2 v = cadd(cscale(ib, xr[q]), sa[q]);
+    const double2 wp = csub(cadd(wr[q], sb[q]), cmul(hjj, v));
+    x[eb + 32 * q] = v;
+    w[eb + 32 * q] = wp;
+    nrm = fma(wp.x, wp.x, fma(wp.y, wp.y, nrm));
+  }
+  return nrm;
+}
+
+// flags: 1 = step B in the last block to finish (4: lagged, dcgs_stepB_lag_warp; needs 2); 32 = warp
+// strips (dcgs_update_strip) instead of tiles; 2 = the
 // grid has one extra block (block 0) that runs
 // the rotation part of step A (column j-1) while the others stream pass 2 -- off the critical
 // path, since only step B needs it.  Every block derives the pass-2 coefficients from the
@@ -578,13 +652,20 @@ __global__ void __launch_bounds__(DU_THREADS, HELM_DU_MINB) k_dcgs_update(const 
     const double2 hjj = s_hjj;
     double2* x = xv.get();
     double2* w = wv.get();
-    const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
     // flags & 16: sweep the tiles from the top down, so that pass 2 starts on the elements whose
     // basis values pass 1 (ascending chunks) read last and L2 still holds
     const bool rev = (flags & 16) != 0;
-    for (long long tile = tb; tile < tiles; tile += nb)
-      nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, rev ? tiles - 1 - tile : tile,
-                                                       red);
+    if (flags & 32) {   // warp strips (long vectors)
+      const long long strips = (n + 32 * DU_SEPL - 1) / (32 * DU_SEPL);
+      const long long gw = (long long)tb * DU_WARPS + (threadIdx.x >> 5), nw = (long long)nb * DU_WARPS;
+      for (long long s = gw; s < strips; s += nw)
+        nrm += dcgs_update_strip(V, ld, j, sab, ib, hjj, x, w, n, rev ? strips - 1 - s : s);
+    } else {
+      const long long tiles = (n + DU_ELEMS - 1) / DU_ELEMS;
+      for (long long tile = tb; tile < tiles; tile += nb)
+        nrm += dcgs_update_tile<DU_WARPS, DU_ELEMS / 32>(V, ld, j, sab, ib, hjj, x, w, n, rev ? tiles - 1 - tile : tile,
+                                                         red);
+    }
   }
   const double t = block_sum(nrm);
   if (threadIdx.x == 0) part[blockIdx.x] = make_double2(t, 0.0);

@@ -285,7 +285,7 @@ class Helm:
         return us.value, nb.value
 
     REGIONS = {"vcycle": 0, "apply_E": 1, "apply_A": 2, "dcgs": 3, "inner_iter": 4, "e_dots": 5, "dcgs_reduce": 6,
-               "dcgs_update": 7, "dcgs_dots": 8}
+               "dcgs_update": 7, "dcgs_dots": 8, "vc_down": 9, "vc_up": 10}
 
     def helm_bench_graph(self, which, arg=0, reps=50):
         """Mean in-graph device time (us) of one instance of a region (warm, back-to-back)."""
