@@ -543,8 +543,9 @@ __global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo 
     const double2 xm = shup(xs), xp = shdn(xs);
     TX t;
     // even relative column: taps I-1, I, I+1 (1/8, 3/4, 1/8 | 0, 1, 0); odd: I, I+1 (1/2, 1/2)
-    t.e = ein ? cadd(cadd(cscale(wm_e, xm), cscale(w0_e, xs)), cscale(wp_e, xp)) : zero;
-    t.d = din ? cadd(cadd(cscale(0.0, xm), cscale(0.5, xs)), cscale(0.5, xp)) : zero;
+    // (zero weights dropped: the odd column is 0.5 (x_I + x_{I+1}); bilinear even = x_I)
+    t.e = ein ? (R == 2 ? cadd(cadd(cscale(wm_e, xm), cscale(w0_e, xs)), cscale(wp_e, xp)) : xs) : zero;
+    t.d = din ? cscale(0.5, cadd(xs, xp)) : zero;
     return t;
   };
   // s = A t at fine row fy for both columns; c = centre row, sth / nth = the rows below / above.
@@ -555,17 +556,12 @@ __global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo 
   auto apply_A_row = [&](int fy, const TX& sth, const TX& c, const TX& nth, double ke, double kd, TX& s) {
     const double2 west_e = shup(c.d), east_d = shdn(c.e);
     if (band_int && fy >= 1 && fy <= gf.ny - 2) {
-      const double k2e = ke * ke, k2d = kd * kd;
-      double2 v = cmul(make_double2(4.0 * ih2 - 1.0 * k2e, -0.0 * k2e), c.e);
-      v = cadd(v, cscale(-ih2, west_e));
-      v = cadd(v, cscale(-ih2, c.d));
-      v = cadd(v, cscale(-ih2, sth.e));
-      s.e = cadd(v, cscale(-ih2, nth.e));
-      v = cmul(make_double2(4.0 * ih2 - 1.0 * k2d, -0.0 * k2d), c.d);
-      v = cadd(v, cscale(-ih2, c.e));
-      v = cadd(v, cscale(-ih2, east_d));
-      v = cadd(v, cscale(-ih2, sth.d));
-      s.d = cadd(v, cscale(-ih2, nth.d));
+      // A = -Delta_h - k^2 (real centre 4/h^2 - k^2, neighbours -1/h^2): 2 + 2 multiplies
+      const double ape = 4.0 * ih2 - ke * ke, apd = 4.0 * ih2 - kd * kd;
+      const double2 ne = cadd(cadd(west_e, c.d), cadd(sth.e, nth.e));
+      const double2 nd = cadd(cadd(c.e, east_d), cadd(sth.d, nth.d));
+      s.e = make_double2(fma(ape, c.e.x, -ih2 * ne.x), fma(ape, c.e.y, -ih2 * ne.y));
+      s.d = make_double2(fma(apd, c.d.x, -ih2 * nd.x), fma(apd, c.d.y, -ih2 * nd.y));
       return;
     }
     s.e = zero;
@@ -622,10 +618,10 @@ __global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo 
     // y interpolation: fine rows fe(J) (taps J-1, J, J+1) and fd(J) (taps J, J+1)
     TX tfe, tfd;
     const bool fe_row = row_in(2 * J + o), fd_row = row_in(2 * J + o + 1);
-    tfe.e = fe_row ? cadd(cadd(cscale(wm_e, txm.e), cscale(w0_e, tx0.e)), cscale(wp_e, txp.e)) : zero;
-    tfe.d = fe_row ? cadd(cadd(cscale(wm_e, txm.d), cscale(w0_e, tx0.d)), cscale(wp_e, txp.d)) : zero;
-    tfd.e = fd_row ? cadd(cadd(cscale(0.0, txm.e), cscale(0.5, tx0.e)), cscale(0.5, txp.e)) : zero;
-    tfd.d = fd_row ? cadd(cadd(cscale(0.0, txm.d), cscale(0.5, tx0.d)), cscale(0.5, txp.d)) : zero;
+    tfe.e = fe_row ? (R == 2 ? cadd(cadd(cscale(wm_e, txm.e), cscale(w0_e, tx0.e)), cscale(wp_e, txp.e)) : tx0.e) : zero;
+    tfe.d = fe_row ? (R == 2 ? cadd(cadd(cscale(wm_e, txm.d), cscale(w0_e, tx0.d)), cscale(wp_e, txp.d)) : tx0.d) : zero;
+    tfd.e = fd_row ? cscale(0.5, cadd(tx0.e, txp.e)) : zero;
+    tfd.d = fd_row ? cscale(0.5, cadd(tx0.d, txp.d)) : zero;
     // s = A t on rows fd(J-1) (south fe(J-1), north fe(J)) and fe(J) (south fd(J-1), north fd(J))
     TX s_fdm, s_fe;
     apply_A_row(2 * J + o - 1, tfe_m, tfd_m, tfe, a_fd_e, a_fd_d, s_fdm);

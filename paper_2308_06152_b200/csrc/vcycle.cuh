@@ -20,7 +20,7 @@
 namespace cg = cooperative_groups;
 
 #ifndef HELM_VC_MINB
-#define HELM_VC_MINB 1
+#define HELM_VC_MINB 4   // 64-register cap: 4 CTAs/SM (c4 level-1 legs -4 us, profiles/r02_legs_probe.jsonl)
 #endif
 namespace helm {
 
@@ -85,16 +85,37 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int
   const bool interior = gx0 >= 1 && gx0 + RX <= F.nx - 1 && gy0 >= 1 && gy0 + RY <= F.ny - 1;
   const double ih2 = 1.0 / (F.h * F.h);
   const int tid = ty * 32 + tx;
-  for (int t = tid; t < RX * RY; t += 256) {
-    {
-      const int iy = t / RX, ix = t - iy * RX;   // compile-time divisor
+  // every global load of the tile is issued before the first use (NT per thread in flight)
+#ifndef HELM_VC_DOWN_PRELOAD
+#define HELM_VC_DOWN_PRELOAD 1
+#endif
+  constexpr int NT = HELM_VC_DOWN_PRELOAD ? (RX * RY + 255) / 256 : 1;
+  for (int tb0 = 0; tb0 < RX * RY; tb0 += 256 * NT) {
+  const int tid = ty * 32 + tx + tb0;
+  double2 fl[NT];
+  double kl[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int t = tid + 256 * i;
+    const int iy = t / RX, ix = t - iy * RX;   // compile-time divisor
+    const int x = gx0 + ix, y = gy0 + iy;
+    const bool in = t < RX * RY && (interior || (x >= 0 && x < F.nx && y >= 0 && y < F.ny));
+    const size_t p = in ? (size_t)y * F.nx + x : 0;
+    fl[i] = in ? f[p] : czero();
+    kl[i] = in ? k[p] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int t = tid + 256 * i;
+    if (t < RX * RY) {
+      const int iy = t / RX, ix = t - iy * RX;
       const int x = gx0 + ix, y = gy0 + iy;
       double2 uv = czero(), fvv = czero();
       double kk = 0.0;
       if (interior || (x >= 0 && x < F.nx && y >= 0 && y < F.ny)) {
         const size_t p = (size_t)y * F.nx + x;
-        kk = k[p];
-        fvv = cscale(fs, f[p]);
+        kk = kl[i];
+        fvv = cscale(fs, fl[i]);
         const double2 ap = interior ? interior_ap(ih2, kk, sr, si) : coef_at(F, x, y, kk, sr, si).ap;
         uv = cscale(omega, cdiv(fvv, ap));   // reading R9: first sweep from u = 0
         if (x >= xs && x < xe && y >= ys && y < ye) u[p] = uv;
@@ -103,6 +124,7 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int
       sf[t] = fvv;
       sk[t] = kk;
     }
+  }
   }
   __syncthreads();
   for (int t = tid; t < QX * QY; t += 256) {
@@ -163,17 +185,42 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
                         cx0 >= 0 && cx0 + CX <= G.nx && cy0 >= 0 && cy0 + CY <= G.ny;
   const double ih2 = 1.0 / (F.h * F.h);
   const int tid = ty * 32 + tx;
-  for (int t = tid; t < CX * CY; t += 256) {
-    {
-      const int r = t / CX, c = t - r * CX;
-      const int J = cy0 + r, I = cx0 + c;
-      se[r * CX + c] =
-          (interior || (I >= 0 && I < G.nx && J >= 0 && J < G.ny)) ? e[(size_t)J * G.nx + I] : czero();
-    }
+  static_assert(TY == 8 && TX <= 32, "one output point per thread");
+  // every global load of the tile is issued up front: the coarse correction e (NE per thread),
+  // u on the tile + halo (NU per thread) and the output point's f, k (, q)
+  constexpr int NE = (CX * CY + 255) / 256, NU = (RX * RY + 255) / 256;
+  double2 el[NE], ul[NU];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int t = tid + 256 * i;
+    const int r = t / CX, c = t - r * CX;
+    const int J = cy0 + r, I = cx0 + c;
+    el[i] = (t < CX * CY && (interior || (I >= 0 && I < G.nx && J >= 0 && J < G.ny))) ? e[(size_t)J * G.nx + I] : czero();
+  }
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+    const int t = tid + 256 * i;
+    const int r = t / RX, c = t - r * RX;
+    const int yy = y0 - 1 + r, x = x0 - 1 + c;
+    ul[i] = (t < RX * RY && (interior || (x >= 0 && x < F.nx && yy >= 0 && yy < F.ny))) ? u[(size_t)yy * F.nx + x]
+                                                                                          : czero();
+  }
+  const int ox_ = x0 + tx, oy_ = y0 + ty;
+  const bool oin = tx < TX && ox_ < F.nx && oy_ < F.ny;
+  const size_t po = oin ? (size_t)oy_ * F.nx + ox_ : 0;
+  const double2 fo = oin ? f[po] : czero();
+  const double ko = oin ? k[po] : 0.0;
+  const double2 qo = (oin && addq) ? addq[po] : czero();
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int t = tid + 256 * i;
+    if (t < CX * CY) se[t] = el[i];
   }
   __syncthreads();
-  for (int t = tid; t < RX * RY; t += 256) {
-    {
+#pragma unroll
+  for (int i = 0; i < NU; ++i) {
+    const int t = tid + 256 * i;
+    if (t < RX * RY) {
       const int r = t / RX, c = t - r * RX;
       const int yy = y0 - 1 + r;
       const int rj = yy - o;
@@ -199,34 +246,27 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
         } else {
           s = cadd(cadd(cscale(0.25, e0[0]), cscale(0.25, e0[1])), cadd(cscale(0.25, e0[CX]), cscale(0.25, e0[CX + 1])));
         }
-        v = cadd(s, u[(size_t)yy * F.nx + x]);
+        v = cadd(s, ul[i]);
       }
-      s1[r * RX + c] = v;
+      s1[t] = v;
     }
   }
   __syncthreads();
-  for (int r = ty; r < TY; r += 8) {
-    const int yy = y0 + r;
-    if (yy >= F.ny) continue;
-    for (int c = tx; c < TX; c += 32) {
-      const int x = x0 + c;
-      if (x >= F.nx) continue;
-      const size_t p = (size_t)yy * F.nx + x;
-      const int q = (r + 1) * RX + (c + 1);
-      const double kk = k[p];
-      double2 ap, res;
-      if (interior) {
-        ap = interior_ap(ih2, kk, sr, si);
-        res = csub(cscale(fs, f[p]), interior_stencil(ih2, ap, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
-      } else {
-        const Coef cf = coef_at(F, x, yy, kk, sr, si);
-        ap = cf.ap;
-        res = csub(cscale(fs, f[p]), stencil5(cf, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
-      }
-      double2 v = cadd(s1[q], cscale(omega, cdiv(res, ap)));
-      if (addq) v = cadd(v, addq[p]);
-      y[p] = v;
+  if (oin) {
+    const int r = ty, c = tx;
+    const int q = (r + 1) * RX + (c + 1);
+    double2 ap, res;
+    if (interior) {
+      ap = interior_ap(ih2, ko, sr, si);
+      res = csub(cscale(fs, fo), interior_stencil(ih2, ap, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
+    } else {
+      const Coef cf = coef_at(F, ox_, oy_, ko, sr, si);
+      ap = cf.ap;
+      res = csub(cscale(fs, fo), stencil5(cf, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
     }
+    double2 v = cadd(s1[q], cscale(omega, cdiv(res, ap)));
+    if (addq) v = cadd(v, qo);
+    y[po] = v;
   }
 }
 
