@@ -931,6 +931,18 @@ int fgm_alloc(helm_ctx_s& C, Fgm& K, int m, size_t n, size_t ld, size_t off, boo
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_dcgs_dots, DC_THREADS, dcgs_dots_smem(K)));
     if (bps > 0) K.geo.gy = std::max(1, std::min(16, bps * C.sm_count / std::max(1, K.geo.gx)));
+    // long vectors: one wave of blocks, each summing several consecutive 256-element chunks
+    // (fewer partials for the reduction kernel: 4089 -> ~450 per output on the 1023^2 level)
+    static const int wave = getenv("HELM_PROBE_DC_WAVE") ? atoi(getenv("HELM_PROBE_DC_WAVE")) : 1;   // probe only
+    const long long slots = (long long)bps * C.sm_count;
+    if (wave && bps > 0 && !dist && K.gxc == 0 && K.geo.gx > 2 * slots) {
+      const long long subs = ((long long)n + DC_SUB - 1) / DC_SUB;
+      const long long per = (subs + slots - 1) / slots;
+      K.geo.chunk = per * DC_SUB;
+      K.geo.gx = (int)(((long long)n + K.geo.chunk - 1) / K.geo.chunk);
+      K.geo.gy = 1;
+      CKR(raise_dyn_smem((const void*)k_dcgs_dots, dsmem));
+    }
     if (const char* gy = getenv("HELM_PROBE_DC_GY")) K.geo.gy = std::max(1, atoi(gy));   // probe only
   }
   {
