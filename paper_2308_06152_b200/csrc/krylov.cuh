@@ -187,6 +187,52 @@ __global__ void __launch_bounds__(GS_THREADS) k_gs_update(const double2* __restr
   __syncthreads();
   const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
   double nrm = 0.0;
+  // long vectors: warp strips of 64 elements, every warp streams all nvec vectors (8 per round
+  // in flight, accumulators in registers, no block barrier); the same sums in vector order
+  constexpr int SE = 64, SU = 8;
+  const long long strips = (n + SE - 1) / SE;
+  if (strips >= 4LL * gridDim.x * GS_WARPS) {
+    for (long long st = (long long)blockIdx.x * GS_WARPS + sl; st < strips; st += (long long)gridDim.x * GS_WARPS) {
+      const long long eb = st * SE + lane;
+      const bool ok0 = eb < n, ok1 = eb + 32 < n;
+      double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+      int c = 0;
+      for (; c + SU <= nvec; c += SU) {
+        double2 a[SU], b[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          const double2* vp = V + (long long)(c + u) * ld + eb;
+          a[u] = ok0 ? ldb<2>(vp) : make_double2(0.0, 0.0);
+          b[u] = ok1 ? ldb<2>(vp + 32) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          s0 = cfma(sc[c + u], a[u], s0);
+          s1 = cfma(sc[c + u], b[u], s1);
+        }
+      }
+      for (; c < nvec; ++c) {
+        const double2* vp = V + (long long)c * ld + eb;
+        if (ok0) s0 = cfma(sc[c], vp[0], s0);
+        if (ok1) s1 = cfma(sc[c], vp[32], s1);
+      }
+      if (ok0) {
+        const double2 t = win ? cadd(win[eb], s0) : s0;
+        wout[eb] = t;
+        nrm = fma(t.x, t.x, fma(t.y, t.y, nrm));
+      }
+      if (ok1) {
+        const double2 t = win ? cadd(win[eb + 32], s1) : s1;
+        wout[eb + 32] = t;
+        nrm = fma(t.x, t.x, fma(t.y, t.y, nrm));
+      }
+    }
+    if (want_norm) {
+      const double tb = block_sum(nrm);
+      if (threadIdx.x == 0) part[blockIdx.x] = make_double2(tb, 0.0);
+    }
+    return;
+  }
   // tiles of 128 elements: a lane holds 4 of them and streams its warp's share of the basis
   // (warp sl takes c = sl, sl + 8, ...; two vectors per step: 8 independent loads in flight);
   // the 8 warps' sums are combined in a fixed order through shared memory

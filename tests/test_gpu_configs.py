@@ -1,12 +1,12 @@
 """GPU parity on BASELINE.json configs[3] and configs[4] inputs, and at the bench method's own
-setting (bench.DEFAULT_METHOD: APD vectors, str-Glk E, coarse CSLP-FGMRES(50) to 1e-1 capped at
-200 steps, coarsest level <= 512 unknowns).
+setting (bench.DEFAULT_METHOD: APD vectors, str-Glk E, coarse CSLP-FGMRES(40) to 1e-1 capped at
+160 steps, coarsest level <= 512 unknowns).
 
 * Operators on the full configs[3] / configs[4] grids (whole-grid compare with the oracle, not
   windows): A within 1e-12, E = Z^T A Z within 1e-12, V-cycles from levels 0 and 1 within 1e-11,
   the deflation z = P v with a fixed coarse step count (inner_tol = 0, reading R15) within 1e-9.
 * The bench method on a same-family smaller case (configs[1] k = 100, whose coarse solves also
-  run at or near the 200-step cap): outer count +-1 at 1e-6, true residual, solutions within
+  run at or near the step cap): outer count +-1 at 1e-6, true residual, solutions within
   1e-6 at 1e-10 (reading R16), and the 1e-6 operating point itself: the GPU's 1e-6 solution is
   no further from the 1e-10 solution than twice the oracle's own 1e-6 solution is.
 * Algorithm 1's literal modified Gram-Schmidt (oracle orth="mgs") against the GPU's delayed
