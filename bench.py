@@ -299,7 +299,7 @@ def kernel_roofline(H, rep, method, peaks, workload):
         if key in prof:
             e = prof[key]
             # per basis column the kernel streams 16 n1 bytes more: scale to this column
-            dom["traffic"] = e["dram_bytes"] + e.get("bytes_per_column", 0.0) * ((dom["column"] or 0) - e.get("column", 0))
+            dom["traffic"] = e["dram_bytes"] + e.get("bytes_per_column", 0.0) * ((dom["column"] or 0) - (e.get("column") or 0))
             dom["traffic_src"] = e["src"]
     except (OSError, KeyError, ValueError, TypeError):
         pass
