@@ -147,6 +147,12 @@ typedef struct {
                           column-streaming kernel (fine fields in registers, neighbours by warp
                           shuffles; the tile kernel's arithmetic), 0 = the shared-memory
                           tile kernel */
+  int tma;             /* column-streaming legs staged by the Tensor Memory Accelerator
+                          (cp.async.bulk.tensor: one box of 116 columns x R rows per field and stage,
+                          a CTA-wide full/empty mbarrier ring) when the level's fields are plain
+                          device arrays; bit 1 = up leg, bit 2 = down leg; otherwise the per-lane
+                          cp.async (LDGSTS) ring.  Default 1 (up leg only: measured faster there,
+                          slower for the down leg) */
 } helm_params;
 
 typedef struct {

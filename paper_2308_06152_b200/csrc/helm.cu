@@ -4,6 +4,7 @@
 // a CUDA graph whose outer and inner (coarse-solve) loops are conditional while nodes driven
 // by the device-side convergence test: no host synchronisation inside a solve.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -59,6 +60,8 @@ struct Level {
   int o;            // node offset of unknown 0 (1 Dirichlet, 0 Sommerfeld)
   size_t n;
   double* k = nullptr;
+  double* kp = nullptr;  // k with an even row stride (TMA column legs: a 2D map needs 16-B strides)
+  int kps = 0;           // its row stride (values)
   double2* f = nullptr;  // rhs when this level is reached by recursion
   double2* u = nullptr;  // solution when reached by recursion
   double2* s = nullptr;  // scratch (pre-smoothed iterate)
@@ -655,6 +658,93 @@ void col_up_t(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const doubl
     launch_k(C, k_vc_up_cpa<PF ? PF : 1, SEG>, gc, 128, 0, L.g, G.g, L.o, (const double2*)L.s, (const double2*)G.u, f,
              (const double*)L.k, sr, si, w, addq, u_out);
 }
+// ---- TMA row staging of the column legs (vcycle.cuh k_vc_down_tma / k_vc_up_tma): tensor maps
+// are encoded on the host per launch (cuTensorMapEncodeTiled through the runtime's driver entry
+// point; no device allocation, valid inside graph capture) and passed as __grid_constant__
+// kernel parameters.  Fields addressed through a device-side index or scale (Krylov basis slots)
+// keep the LDGSTS legs.
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+// complex128 field nx x ny as 2D float64 (2 nx x ny); box = bw complex x bh rows (zero fill outside)
+bool map_c128(CUtensorMap* m, const void* base, int nx, int ny, int bw, int bh) {
+  auto fn = tmap_encode();
+  if (!fn || !base || ((uintptr_t)base & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)nx * 2, (cuuint64_t)ny};
+  cuuint64_t strides[1] = {(cuuint64_t)nx * 16};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * bw), (cuuint32_t)bh}, es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// float64 field nx x ny stored with row stride ld (even); box = bw values x bh rows
+bool map_f64(CUtensorMap* m, const void* base, int nx, int ny, int ld, int bw, int bh) {
+  auto fn = tmap_encode();
+  if (!fn || !base || ((uintptr_t)base & 15) || (ld & 1)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)nx, (cuuint64_t)ny};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh}, es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// helm_params.tma bit 1: up leg, bit 2: down leg (default 1: on 16383^2 the TMA up leg streams at
+// 0.80 of HBM against 0.79 for LDGSTS, the TMA down leg at 0.77 against 0.82)
+bool tma_legs(const helm_ctx_s& C, const Level& L, DVec f, int bit) {
+  return C.p.col_pipe == 1 && (C.p.tma & bit) && !C.dist && L.kp && f.idx == nullptr && f.sc == nullptr;
+}
+// stage rows (R) and stages in flight (S) of the TMA legs
+#ifndef HELM_TMA_RD
+#define HELM_TMA_RD 4
+#endif
+#ifndef HELM_TMA_SD
+#define HELM_TMA_SD 3
+#endif
+#ifndef HELM_TMA_RU
+#define HELM_TMA_RU 2
+#endif
+#ifndef HELM_TMA_SU
+#define HELM_TMA_SU 3
+#endif
+template <int SEG>
+int tma_down_t(helm_ctx_s& C, const Level& L, const Level& G, DVec f, double sr, double si, double w) {
+  constexpr int R = HELM_TMA_RD;
+  CUtensorMap mf, mk;
+  if (!map_c128(&mf, f.p, L.g.nx, L.g.ny, TMA_W, R) || !map_f64(&mk, L.kp, L.g.nx, L.g.ny, L.kps, TMA_W, R)) return 1;
+  const dim3 gc((L.g.nx + 4 * COL_OWN - 1) / (4 * COL_OWN), (L.g.ny + SEG - 1) / SEG);
+  launch_k(C, k_vc_down_tma<R, HELM_TMA_SD, SEG>, gc, 128, 0, L.g, G.g, L.o, mf, mk, 1.0, sr, si, w, L.s, G.f);
+  return 0;
+}
+template <int SEG>
+int tma_up_t(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2* addq, DVec u_out, double sr,
+             double si, double w) {
+  constexpr int R = HELM_TMA_RU;
+  CUtensorMap mu, mf, mk, mq;
+  if (!map_c128(&mu, L.s, L.g.nx, L.g.ny, TMA_W, R) || !map_c128(&mf, f.p, L.g.nx, L.g.ny, TMA_W, R) ||
+      !map_f64(&mk, L.kp, L.g.nx, L.g.ny, L.kps, TMA_W, R))
+    return 1;
+  const dim3 gc((L.g.nx + 4 * COL_OWN - 1) / (4 * COL_OWN), (L.g.ny + SEG - 1) / SEG);
+  if (addq) {
+    if (!map_c128(&mq, addq, L.g.nx, L.g.ny, TMA_W, R)) return 1;
+    launch_k(C, k_vc_up_tma<R, HELM_TMA_SU, SEG, true>, gc, 128, 0, L.g, G.g, L.o, mu, (const double2*)G.u, mf, 1.0,
+             mk, sr, si, w, mq, u_out);
+  } else {
+    launch_k(C, k_vc_up_tma<R, HELM_TMA_SU, SEG, false>, gc, 128, 0, L.g, G.g, L.o, mu, (const double2*)G.u, mf, 1.0,
+             mk, sr, si, w, mf, u_out);
+  }
+  return 0;
+}
+
 // Segment length for a level of nx x ny fine unknowns: the longest of 256/128/64/32/16 rows that
 // still gives ~16 warps per SM (28 columns per warp); large levels keep the tuned (4, 256/128).
 int col_seg(const helm_ctx_s& C, const Level& L, int longest) {
@@ -675,6 +765,17 @@ int col_down(helm_ctx_s& C, const Level& L, const Level& G, DVec f, double sr, d
       default: p8 ? col_down_t<8, 16>(C, L, G, f, sr, si, w) : col_down_t<6, 16>(C, L, G, f, sr, si, w);
     }
     return post_launch(C);
+  }
+  if (C.p.col_pipe == 1 && tma_legs(C, L, f, 2)) {
+    int r = 1;
+    switch (col_seg(C, L, 256)) {
+      case 256: r = tma_down_t<256>(C, L, G, f, sr, si, w); break;
+      case 128: r = tma_down_t<128>(C, L, G, f, sr, si, w); break;
+      case 64: r = tma_down_t<64>(C, L, G, f, sr, si, w); break;
+      case 32: r = tma_down_t<32>(C, L, G, f, sr, si, w); break;
+      default: r = tma_down_t<16>(C, L, G, f, sr, si, w);
+    }
+    if (r == 0) return post_launch(C);
   }
   if (C.p.col_pipe == 1) {
     switch (col_seg(C, L, 256)) {
@@ -706,6 +807,16 @@ int col_up(helm_ctx_s& C, const Level& L, const Level& G, DVec f, const double2*
       default: col_up_t<6, 16>(C, L, G, f, addq, u_out, sr, si, w);
     }
     return post_launch(C);
+  }
+  if (C.p.col_pipe == 1 && tma_legs(C, L, f, 1)) {
+    int r = 1;
+    switch (col_seg(C, L, 128)) {
+      case 128: r = tma_up_t<128>(C, L, G, f, addq, u_out, sr, si, w); break;
+      case 64: r = tma_up_t<64>(C, L, G, f, addq, u_out, sr, si, w); break;
+      case 32: r = tma_up_t<32>(C, L, G, f, addq, u_out, sr, si, w); break;
+      default: r = tma_up_t<16>(C, L, G, f, addq, u_out, sr, si, w);
+    }
+    if (r == 0) return post_launch(C);
   }
   if (C.p.col_pipe == 1) {
     switch (col_seg(C, L, 128)) {
@@ -1433,6 +1544,7 @@ void helm_default_params(helm_params* p) {
   p->dots_cluster = 0;
   p->inner_restart = 0;
   p->e_stream = 1;
+  p->tma = 1;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1445,6 +1557,7 @@ static void destroy_ctx(helm_ctx_s* C) {
     if (ex) cudaGraphExecDestroy(ex);
   for (auto& L : C->L) {
     cudaFree(L.k);
+    cudaFree(L.kp);
     cudaFree(L.f);
     cudaFree(L.u);
     cudaFree(L.s);
@@ -1612,6 +1725,19 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     }
     CK(cudaStreamSynchronize(C.s));
     for (double* b : tk) cudaFree(b);
+  }
+  // TMA column legs (single GPU): a copy of k with an even row stride on every level the column
+  // legs run on, so that one 2D tensor map (16-byte row stride) serves it like the complex fields
+  if (C.p.tma && !C.dist && C.p.col_min_n >= 0 && fused_vcycle(C)) {
+    for (size_t l = 0; l + 1 < C.L.size(); ++l) {
+      Level& Lv = C.L[l];
+      if ((long long)Lv.n < C.p.col_min_n) continue;
+      Lv.kps = (Lv.g.nx + 1) & ~1;
+      CKR(dalloc(&Lv.kp, (size_t)Lv.kps * Lv.g.ny));
+      CK(cudaMemcpy2DAsync(Lv.kp, (size_t)Lv.kps * sizeof(double), Lv.k, (size_t)Lv.g.nx * sizeof(double),
+                           (size_t)Lv.g.nx * sizeof(double), Lv.g.ny, cudaMemcpyDeviceToDevice, C.s));
+    }
+    CK(cudaStreamSynchronize(C.s));
   }
   // level descriptors for the single-CTA tail
   {

@@ -14,6 +14,7 @@
 // kernels of kernels.cuh.
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "kernels.cuh"
 
@@ -714,6 +715,304 @@ __global__ void __launch_bounds__(128) k_vc_up_cpa(Geo F, Geo G, int o, const do
   else
     up_cpa_body<PF, SEG, false>(F, G, o, u, e, fv.get(), fv.scale(), k, sr, si, omega, addq, yv.get(), ru[wq],
                                 rf[wq], rq[wq], rk[wq], lane, xo, ya, yb);
+}
+
+// ---- TMA column legs: the rows ahead are staged by the Tensor Memory Accelerator
+// (cp.async.bulk.tensor, one instruction per row and field issued by lane 0; completion on a
+// per-slot mbarrier with the transaction byte count).  The tensor maps describe each field as a
+// 2D float64 array (complex128 = 2 doubles); a warp's row segment is one 32-column box whose
+// out-of-grid columns / rows the TMA unit fills with zeros -- the same values the LDGSTS legs
+// substitute.  Same arithmetic and tap order as the cp.async legs (down_cpa_body / up_cpa_body).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// k is float64 with rows of odd length, whose byte stride is not a multiple of 16 (a TMA
+// requirement): the legs read a copy with an even row stride (Level.kp), mapped in 2D like the
+// complex fields (zero fill outside the grid).
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// CTA-wide staging: the 4 warps of a CTA own 4 x 28 consecutive columns; one box of TMA_W = 116
+// columns (2 halo columns each side) x R rows per field and stage, S stages in flight.  full[s]
+// completes when the stage's bytes landed (transaction count), empty[s] when every active warp
+// has read it; thread 0 refills a stage after its empty barrier.  (A dedicated producer warp was
+// measured slower: 0.61 / 0.56 of HBM on 16383^2, its 160-thread CTAs hold fewer warps per SM.)  Warp w reads column 28 w + lane
+// of the box, i.e. the same fine column as lane `lane` of the per-warp legs.
+constexpr int TMA_W = 4 * COL_OWN + 4;
+// stage sizes padded to 128 bytes (TMA destinations); R even keeps the complex stages aligned
+template <int R>
+struct TmaStage {
+  static_assert(R % 2 == 0, "R even");
+  static constexpr int C = R * TMA_W;                 // complex values per stage (R * 1856 B)
+  static constexpr int K = (R * TMA_W + 15) / 16 * 16;   // doubles per stage, 128-B multiple
+};
+
+template <int R, int S, int SEG>
+__global__ void __launch_bounds__(128) k_vc_down_tma(Geo F, Geo G, int o, const __grid_constant__ CUtensorMap mf,
+                                                     const __grid_constant__ CUtensorMap mk, double fs, double sr,
+                                                     double si, double omega, double2* __restrict__ u,
+                                                     double2* __restrict__ fc) {
+  HELM_PDL_ENTRY();
+  using ST = TmaStage<R>;
+  __shared__ alignas(128) double2 rf[S * ST::C];
+  __shared__ alignas(128) double rk[S * ST::K];
+  __shared__ unsigned long long full[S], empty[S];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int xc = blockIdx.x * 4 * COL_OWN;
+  const int nact = min(4, (F.nx - xc + COL_OWN - 1) / COL_OWN);   // warps with columns
+  const int ya = blockIdx.y * SEG;
+  const int yb = min(F.ny, ya + SEG);
+  const int y0 = ya - 2, y1 = yb + 1;   // rows consumed
+  const int nst = (y1 - y0 + R) / R;    // stages
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], nact);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int t) {   // thread 0: stage t into slot t % S
+    const int q = t % S;
+    mbar_expect_tx(&full[q], R * TMA_W * 24);
+    tma_row(rf + q * ST::C, &mf, 2 * (xc - 2), y0 + t * R, &full[q]);
+    tma_row(rk + q * ST::K, &mk, xc - 2, y0 + t * R, &full[q]);
+  };
+  if (threadIdx.x == 0)
+    for (int t = 0; t < S && t < nst; ++t) issue(t);
+  if (wq >= nact) return;   // no columns (after the barrier set-up; not counted in empty)
+  const int xo = xc + wq * COL_OWN;
+  const int x = xo - 2 + lane;
+  const int col = wq * COL_OWN + lane;
+  const bool xin = (x >= 0 && x < F.nx);
+  const bool xown = (lane >= 2 && lane < 2 + COL_OWN && x < F.nx);
+  const int ri = x - o;
+  const bool xcentre = ((ri & 1) == 0) && ri >= 0 && (ri >> 1) < G.nx && xown;
+  const int I = ri >> 1;
+  const bool INT = xo - 2 >= 1 && xo + 29 <= F.nx - 2 && ya - 3 >= 1 && yb + 1 <= F.ny - 2;
+  const double ih2 = 1.0 / (F.h * F.h);
+  double2 um2 = czero(), um1 = czero(), fm1 = czero(), rm3 = czero(), rm2 = czero();
+  double km1 = 0.0;
+  for (int y = y0; y <= y1; ++y) {
+    const int t = (y - y0) / R, r = (y - y0) - t * R, q = t % S;
+    if (r == 0) mbar_wait(&full[q], (t / S) & 1);
+    const double2 fraw = rf[q * ST::C + r * TMA_W + col];
+    const double k0 = rk[q * ST::K + r * TMA_W + col];
+    if (r == R - 1 || y == y1) {   // this warp is done with stage t
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[q]);
+      if (threadIdx.x == 0 && t + S < nst) {   // thread 0 refills the slot once every warp left it
+        mbar_wait(&empty[q], (t / S) & 1);
+        issue(t + S);
+      }
+    }
+    double2 f0 = czero(), u0 = czero();
+    if (INT || (xin && y >= 0 && y < F.ny)) {
+      f0 = cscale(fs, fraw);
+      const double2 ap = INT ? interior_ap(ih2, k0, sr, si) : coef_at(F, x, y, k0, sr, si).ap;
+      u0 = cscale(omega, cdiv(f0, ap));   // reading R9: first sweep from u = 0
+      if (xown && y >= ya && y < yb) u[(size_t)y * F.nx + x] = u0;
+    }
+    const int yr = y - 1;
+    const double2 uw = shfl_up2(um1, 1), ue = shfl_dn2(um1, 1);
+    double2 rr = czero();
+    if (lane >= 1 && lane <= 30) {
+      if (INT) {
+        rr = csub(fm1, interior_stencil(ih2, interior_ap(ih2, km1, sr, si), um1, uw, ue, um2, u0));
+      } else if (xin && yr >= 0 && yr < F.ny) {
+        const Coef c = coef_at(F, x, yr, km1, sr, si);
+        rr = csub(fm1, stencil5(c, um1, uw, ue, um2, u0));
+      }
+    }
+    const int yc = y - 2;
+    const int rj = yc - o;
+    if (((rj & 1) == 0) && yc >= ya && yc < yb && rj >= 0 && (rj >> 1) < G.ny) {   // warp-uniform
+      const double2 a0 = shfl_up2(rm3, 1), a2 = shfl_dn2(rm3, 1);
+      const double2 b0 = shfl_up2(rm2, 1), b2 = shfl_dn2(rm2, 1);
+      const double2 c0 = shfl_up2(rr, 1), c2 = shfl_dn2(rr, 1);
+      if (xcentre) {
+        double2 sacc = czero();
+        sacc = cadd(sacc, cscale(1.0 / 16.0, a0));
+        sacc = cadd(sacc, cscale(2.0 / 16.0, rm3));
+        sacc = cadd(sacc, cscale(1.0 / 16.0, a2));
+        sacc = cadd(sacc, cscale(2.0 / 16.0, b0));
+        sacc = cadd(sacc, cscale(4.0 / 16.0, rm2));
+        sacc = cadd(sacc, cscale(2.0 / 16.0, b2));
+        sacc = cadd(sacc, cscale(1.0 / 16.0, c0));
+        sacc = cadd(sacc, cscale(2.0 / 16.0, rr));
+        sacc = cadd(sacc, cscale(1.0 / 16.0, c2));
+        fc[(size_t)(rj >> 1) * G.nx + I] = sacc;
+      }
+    }
+    rm3 = rm2;
+    rm2 = rr;
+    um2 = um1;
+    um1 = u0;
+    fm1 = f0;
+    km1 = k0;
+  }
+}
+
+// Up leg with CTA-wide TMA staging of u, f, k (and q) of each row.
+template <int R, int S, int SEG, bool Q>
+__global__ void __launch_bounds__(128) k_vc_up_tma(Geo F, Geo G, int o, const __grid_constant__ CUtensorMap mu,
+                                                   const double2* __restrict__ e, const __grid_constant__ CUtensorMap mf,
+                                                   double fs, const __grid_constant__ CUtensorMap mk, double sr,
+                                                   double si, double omega, const __grid_constant__ CUtensorMap mq,
+                                                   DVec yv) {
+  HELM_PDL_ENTRY();
+  using ST = TmaStage<R>;
+  __shared__ alignas(128) double2 ru[S * ST::C];
+  __shared__ alignas(128) double2 rf[S * ST::C];
+  __shared__ alignas(128) double2 rq[Q ? S * ST::C : 8];
+  __shared__ alignas(128) double rk[S * ST::K];
+  __shared__ unsigned long long full[S], empty[S];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int xc = blockIdx.x * 4 * COL_OWN;
+  const int nact = min(4, (F.nx - xc + COL_OWN - 1) / COL_OWN);
+  const int ya = blockIdx.y * SEG;
+  const int yb = min(F.ny, ya + SEG);
+  const int y0 = ya - 1, y1 = yb;   // rows of u consumed; f, k, q of row y are used one row later
+  const int nst = (y1 - y0 + R) / R;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], nact);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int t) {
+    const int q = t % S;
+    mbar_expect_tx(&full[q], R * TMA_W * (Q ? 56 : 40));
+    tma_row(ru + q * ST::C, &mu, 2 * (xc - 2), y0 + t * R, &full[q]);
+    tma_row(rf + q * ST::C, &mf, 2 * (xc - 2), y0 + t * R, &full[q]);
+    tma_row(rk + q * ST::K, &mk, xc - 2, y0 + t * R, &full[q]);
+    if (Q) tma_row(rq + q * ST::C, &mq, 2 * (xc - 2), y0 + t * R, &full[q]);
+  };
+  if (threadIdx.x == 0)
+    for (int t = 0; t < S && t < nst; ++t) issue(t);
+  if (wq >= nact) return;
+  double2* __restrict__ yo = yv.get();
+  const int xo = xc + wq * COL_OWN;
+  const int x = xo - 2 + lane;
+  const int col = wq * COL_OWN + lane;
+  const bool xin = (x >= 0 && x < F.nx);
+  const bool xown = (lane >= 2 && lane < 2 + COL_OWN && x < F.nx);
+  const double ih2 = 1.0 / (F.h * F.h);
+  const int ri = x - o;
+  const int Ia = floordiv2(ri);
+  const bool ox = (ri & 1) != 0;
+  const bool i0in = Ia >= 0 && Ia < G.nx, i1in = (Ia + 1) >= 0 && (Ia + 1) < G.nx;
+  const bool INT = xo - 2 >= 1 && xo + 29 <= F.nx - 2 && ya - 2 >= 1 && yb <= F.ny - 2;
+  auto interp = [&](int yy) -> double2 {
+    const int rj = yy - o;
+    const int Ja = floordiv2(rj);
+    const bool oy = (rj & 1) != 0;
+    auto ev = [&](int J, int Ii, bool iin) -> double2 {
+      return (iin && J >= 0 && J < G.ny) ? e[(size_t)J * G.nx + Ii] : czero();
+    };
+    const double2 e00 = ev(Ja, Ia, i0in);
+    if (!ox && !oy) return e00;
+    if (ox && !oy) return cadd(cscale(0.5, e00), cscale(0.5, ev(Ja, Ia + 1, i1in)));
+    if (!ox && oy) return cadd(cscale(0.5, e00), cscale(0.5, ev(Ja + 1, Ia, i0in)));
+    return cadd(cadd(cscale(0.25, e00), cscale(0.25, ev(Ja, Ia + 1, i1in))),
+                cadd(cscale(0.25, ev(Ja + 1, Ia, i0in)), cscale(0.25, ev(Ja + 1, Ia + 1, i1in))));
+  };
+  double2 v1m2 = czero(), v1m1 = czero();
+  double2 fcur = czero(), qcur = czero();
+  double kcur = 0.0;
+  double2 e0 = czero(), e1 = czero();
+  int eJ = -1 << 30;
+  for (int y = y0; y <= y1; ++y) {
+    const int t = (y - y0) / R, r = (y - y0) - t * R, q = t % S;
+    if (r == 0) mbar_wait(&full[q], (t / S) & 1);
+    const double2 ucur = ru[q * ST::C + r * TMA_W + col];
+    const double2 fnew = rf[q * ST::C + r * TMA_W + col];
+    const double knew = rk[q * ST::K + r * TMA_W + col];
+    const double2 qnew = Q ? rq[q * ST::C + r * TMA_W + col] : czero();
+    if (r == R - 1 || y == y1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[q]);
+      if (threadIdx.x == 0 && t + S < nst) {
+        mbar_wait(&empty[q], (t / S) & 1);
+        issue(t + S);
+      }
+    }
+    double2 v10 = czero();
+    if (INT) {
+      const int rj = y - o;
+      const int Ja = floordiv2(rj);
+      const bool oy = (rj & 1) != 0;
+      if (Ja != eJ) {
+        if (Ja == eJ + 1) {
+          e0 = e1;
+        } else {
+          e0 = (Ja >= 0 && Ja < G.ny && i0in) ? e[(size_t)Ja * G.nx + Ia] : czero();
+        }
+        e1 = (Ja + 1 < G.ny && Ja + 1 >= 0 && i0in) ? e[(size_t)(Ja + 1) * G.nx + Ia] : czero();
+        eJ = Ja;
+      }
+      const double2 e01 = shfl_dn2(e0, 1), e11 = shfl_dn2(e1, 1);
+      double2 ip;
+      if (!ox && !oy) ip = e0;
+      else if (ox && !oy) ip = cadd(cscale(0.5, e0), cscale(0.5, e01));
+      else if (!ox && oy) ip = cadd(cscale(0.5, e0), cscale(0.5, e1));
+      else ip = cadd(cadd(cscale(0.25, e0), cscale(0.25, e01)), cadd(cscale(0.25, e1), cscale(0.25, e11)));
+      v10 = cadd(ip, ucur);
+    } else if (xin && y >= 0 && y < F.ny) {
+      v10 = cadd(interp(y), ucur);
+    }
+    const int yr = y - 1;
+    const double2 uw = shfl_up2(v1m1, 1), ue = shfl_dn2(v1m1, 1);
+    if (xown && yr >= ya && yr < yb) {
+      const size_t p = (size_t)yr * F.nx + x;
+      double2 res, ap;
+      if (INT) {
+        ap = interior_ap(ih2, kcur, sr, si);
+        res = csub(cscale(fs, fcur), interior_stencil(ih2, ap, v1m1, uw, ue, v1m2, v10));
+      } else {
+        const Coef c = coef_at(F, x, yr, kcur, sr, si);
+        ap = c.ap;
+        res = csub(cscale(fs, fcur), stencil5(c, v1m1, uw, ue, v1m2, v10));
+      }
+      double2 out = cadd(v1m1, cscale(omega, cdiv(res, ap)));
+      if (Q) out = cadd(out, qcur);
+      yo[p] = out;
+    }
+    v1m2 = v1m1;
+    v1m1 = v10;
+    fcur = fnew;
+    kcur = knew;
+    qcur = qnew;
+  }
 }
 
 // ------------------------------------------------------------------ cluster tail

@@ -38,7 +38,7 @@ class helm_params(ctypes.Structure):
                 ("col_pipe", ctypes.c_int), ("fuse_dots", ctypes.c_int), ("precond", ctypes.c_int),
                 ("gamma", ctypes.c_double), ("tail_cluster", ctypes.c_int),
                 ("lag_stepb", ctypes.c_int), ("dots_cluster", ctypes.c_int), ("inner_restart", ctypes.c_int),
-                ("e_stream", ctypes.c_int)]
+                ("e_stream", ctypes.c_int), ("tma", ctypes.c_int)]
 
 
 class helm_dist(ctypes.Structure):

@@ -384,6 +384,35 @@ def test_streaming_E_bitwise_tile_kernel(lib, vec):
 
 
 
+def test_tma_column_legs(lib):
+    """The TMA-staged column legs (tma = 3: both legs; the default 1 stages the up leg only)
+    against the oracle's V-cycle and bitwise against the per-lane cp.async legs (tma = 0): same arithmetic,
+    only the staging differs.  Column legs on every level (col_min_n = 0), Dirichlet and
+    Sommerfeld, ragged sizes spanning several 28-column warp bands and row segments, variable k;
+    plus the configs[4] block with the default leg choice (column legs on the 2047^2 level)."""
+    cases = [P(255, 127, 1 / 256, "dirichlet", random_k((127, 255), 12, 10, 90)),
+             P(193, 97, 1 / 192, "sommerfeld", random_k((97, 193), 13, 5, 70)),
+             P(61, 45, 1 / 60, "sommerfeld", random_k((45, 61), 14, 5, 30))]
+    for p in cases:
+        s = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams())
+        u = random_field(p.shape, 15)
+        outs = []
+        for tma in (3, 0):
+            H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, {"col_min_n": 0, "tma": tma})
+            outs.append(H.vcycle(0, gpu(u)).cpu().numpy())
+            H.close()
+        assert rel(outs[0], s.vcycle(u, 0)) < 1e-11, p.shape
+        assert np.array_equal(outs[0], outs[1]), (p.shape, rel(outs[0], outs[1]))
+    big = config_problem("c4_weak_2049")
+    u = random_field(big.shape, 16)
+    outs = []
+    for tma in (3, 1, 0):
+        H = lib.Helm(big.nx, big.ny, big.h, big.bc, big.k, {"tma": tma})
+        outs.append(H.vcycle(0, gpu(u)).cpu().numpy())
+        H.close()
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[2]), rel(outs[0], outs[2])
+
+
 @pytest.mark.parametrize("vec", ["bilinear", "high_order"])
 def test_tlkm_apply_and_solve(lib, vec):
     """Practical TLKM (reading R23): one application at a tight coarse tolerance matches the
