@@ -44,6 +44,10 @@ sys.path.insert(0, ROOT)
 DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 160,
                   "inner_restart": 40, "coarsest_n": 512, "restart": 0}
 DEFAULT_WORKLOAD = "c4_weak_2049"
+# Device form of the coarse solve (reading R28, §6d): the basis generated and
+# orthogonalised 8 vectors at a time (one block Gram-Schmidt pass), measured 25.2 -> 16.9 s on
+# c4_weak_2049 (profiles/r02_sstep_probe.jsonl).
+DEFAULT_SSTEP = {"sstep": 8, "sstep_passes": 1}
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 
@@ -105,6 +109,13 @@ def method_of(args):
     return {"vectors": args.vectors, "coarse_op": args.coarse_op, "inner_tol": args.inner_tol,
             "inner_maxit": args.inner_maxit, "inner_restart": args.inner_restart, "coarsest_n": args.coarsest_n,
             "restart": args.restart, "outer": args.outer}
+
+
+def gpu_method(args):
+    """The GPU parameters of the method: the paper's method (method_of, shared with the oracle) plus
+    the form the coarse solve takes on the device (s-step blocks, reading R28: the same GMRES(m)
+    iterates in exact arithmetic), which the oracle does not have."""
+    return dict(method_of(args), sstep=args.sstep, sstep_passes=args.sstep_passes)
 
 
 def oracle_params(args, **kw):
@@ -264,17 +275,37 @@ def kernel_roofline(H, rep, method, peaks, workload):
     galerkin = method.get("coarse_op", "galerkin") == "galerkin"
     fused = galerkin and bool(prm.fuse_dots)
     comps = []
-    if fused:
+    ss = int(method.get("sstep") or 0)
+    if ss > 0:
+        # s-step coarse solve (reading R28): per step one V-cycle + E in residual mode; per block
+        # of s steps `passes` x (pass partials, reduction, update) at the mean block column
+        m = method.get("inner_restart") or method.get("inner_maxit")
+        Jm = ss * ((m // ss - 1) // 2)
+        blocks = -(-inner_its // ss)
+        passes = int(method.get("sstep_passes") or 1)
+        comps += [
+            ("k_glk_stream<2,1> (E = Z^T A Z in residual mode, w = sigma f - E x)" if galerkin and prm.e_stream else
+             "E apply (residual mode)", "ss_e", 0, 10, inner_its, 80.0 * n1),
+            ("k_bgs_dots_smem (block pass partials [Q W]^H W)", "ss_dots", Jm, 5, blocks * passes,
+             16.0 * (Jm + 1 + ss) * n1),
+            ("k_bgs_update (W <- (W - Q C) R^-1)", "ss_update", Jm, 5, blocks * passes, 16.0 * (Jm + 1 + 2 * ss) * n1),
+            ("k_bgs_reduce (partial sums + Cholesky)", "ss_reduce", Jm, 10, blocks * passes,
+             16.0 * (Jm + 1 + ss) * ss * 148),
+        ]
+    elif fused:
         comps.append(("k_galerkin_apply<2,0,16,8,true> (E = Z^T A Z fused with DCGS2 pass 1)", "e_dots", jm, 4,
                       inner_its, (64.0 + 16 * (jm + 1) + 16) * n1))
     else:
         comps.append(("k_glk_stream<2,0> (E = Z^T A Z, column streaming)" if galerkin and prm.e_stream else
                       "E apply (coarse operator)", "apply_E", 0, 10, inner_its, 64.0 * n1))
         comps.append(("k_dcgs_dots (DCGS2 pass 1)", "dcgs_dots", jm, 4, inner_its, 16.0 * (jm + 2) * n1))
+    if ss <= 0:
+        comps += [
+            ("k_dcgs_update (DCGS2 pass 2 + step B)", "dcgs_update", jm, 4, inner_its, (16.0 * jm + 64) * n1),
+            ("k_dcgs_reduceA (pass-1 partial sums + step A)", "dcgs_reduce", jm, 4, inner_its,
+             (2 * jm + 2) * 16.0 * (tiles if fused else -(-n1 // 256))),
+        ]
     comps += [
-        ("k_dcgs_update (DCGS2 pass 2 + step B)", "dcgs_update", jm, 4, inner_its, (16.0 * jm + 64) * n1),
-        ("k_dcgs_reduceA (pass-1 partial sums + step A)", "dcgs_reduce", jm, 4, inner_its,
-         (2 * jm + 2) * 16.0 * (tiles if fused else -(-n1 // 256))),
         ("V-cycle from level 1 (inner CSLP preconditioner, 13 kernels)", "vcycle", 1, 10, inner_its + outer_its,
          vbytes),
         ("k_apply_op A (level 0)", "apply_A", 0, 10, 2 * outer_its, 40.0 * n0),
@@ -286,7 +317,8 @@ def kernel_roofline(H, rep, method, peaks, workload):
         rows[label] = {"kernel": label, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                        "frac": gbs / peaks["hbm_gbs"], "traffic": None, "bytes_per_launch": nbytes,
                        "us_per_launch": us, "launches_per_step": count, "est_ms_per_step": count * us * 1e-3,
-                       "column": arg if region in ("e_dots", "dcgs_dots", "dcgs_update", "dcgs_reduce") else None,
+                       "column": arg if region in ("e_dots", "dcgs_dots", "dcgs_update", "dcgs_reduce", "ss_dots",
+                                                   "ss_update", "ss_reduce") else None,
                        "timing": "in-graph, warm (helm_bench_graph: the solve's own launch, replayed)",
                        "peak_src": peaks["src"]}
     dom = max(rows.values(), key=lambda r: r["est_ms_per_step"])
@@ -498,6 +530,9 @@ def main():
     ap.add_argument("--restart", type=int, default=DEFAULT_METHOD["restart"],
                     help="outer FGMRES(m); 0 = full basis (the same at every N)")
     ap.add_argument("--coarsest-n", type=int, default=DEFAULT_METHOD["coarsest_n"])
+    ap.add_argument("--sstep", type=int, default=DEFAULT_SSTEP["sstep"],
+                    help="coarse solve in s-step form (0 = one vector per step, delayed CGS2)")
+    ap.add_argument("--sstep-passes", type=int, default=DEFAULT_SSTEP["sstep_passes"])
     ap.add_argument("--maxit", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=1, help="end-to-end solves (host buffers) after the timed ones")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -525,7 +560,7 @@ def main():
     torch.cuda.set_device(local)
     peaks = load_peaks()
     p = config_problem(args.workload)
-    method = method_of(args)
+    method = gpu_method(args)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         H = helm.helm_setup(p, method, stream=stream)
@@ -573,7 +608,7 @@ def main():
                 d = json.load(fh)
         except (OSError, ValueError):
             d = {}
-        d[args.workload] = {"method": method, "outer": r["outer_iterations"], "inner_total": r["inner_iterations_total"],
+        d[args.workload] = {"method": method_of(args), "outer": r["outer_iterations"], "inner_total": r["inner_iterations_total"],
                             "inner_solves": r["inner_solves"], "time_to_solution_s": tts}
         with open(COUNTS_FILE, "w") as fh:
             json.dump(d, fh, indent=1, sort_keys=True)

@@ -153,6 +153,18 @@ typedef struct {
                           device arrays; bit 1 = up leg, bit 2 = down leg; otherwise the per-lane
                           cp.async (LDGSTS) ring.  Default 1 (up leg only: measured faster there,
                           slower for the down leg) */
+  int sstep;           /* coarse solve in s-step form (reading R28): 0 (default) = one basis
+                          vector per step (delayed CGS2); 4, 6 or 8 = the basis generated s vectors
+                          at a time (s V-cycles + E applies), orthogonalised as a block (one sweep
+                          over the basis for all s dot products, Cholesky of the Pythagorean Gram
+                          matrix, one update sweep), Hessenberg columns recovered from the block
+                          factors.  The same GMRES(m) iterates in exact arithmetic (the V-cycle is a
+                          fixed linear preconditioner within a coarse solve); per-step convergence
+                          test and counts.  Single GPU, A-DEF1/APD, the coarse basis size
+                          (inner_restart, else inner_maxit) a multiple of s */
+  int sstep_passes;    /* block Gram-Schmidt passes per block: 2 (default, BCGS-PIP2) or 1 */
+  double sstep_shift;  /* shift sigma of the block basis w_i = sigma w_{i-1} - A w_{i-1} (default 0.5,
+                          the centre of the CSLP-preconditioned spectrum's disc) */
 } helm_params;
 
 typedef struct {
@@ -258,6 +270,12 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_DCGS_DOTS 8   /* pass 1 alone (k_dcgs_dots) as the unfused step launches it */
 #define HELM_GB_VC_DOWN 9     /* the fused V-cycle down leg of level `arg`, as the V-cycle launches it */
 #define HELM_GB_VC_UP 10      /* the fused V-cycle up leg of level `arg` */
+/* s-step coarse solve (params.sstep > 0; `arg` = the block's first column J, a multiple of s): */
+#define HELM_GB_SS_DOTS 11    /* the block pass partials [Q_0..J, W]^H W (one sweep over the basis) */
+#define HELM_GB_SS_REDUCE 12  /* their reduction + Cholesky of the Pythagorean Gram matrix */
+#define HELM_GB_SS_UPDATE 13  /* W <- (W - Q C) R^-1 (one sweep over the basis) */
+#define HELM_GB_SS_POWER 14   /* one step of the block basis: V-cycle from level 1 + E in residual mode */
+#define HELM_GB_SS_E 15       /* E in residual mode alone, w = sigma f - E x */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 /* ---------------------------------------------------------------------------------------

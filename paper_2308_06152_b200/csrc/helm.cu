@@ -24,6 +24,7 @@
 #include "krylov.cuh"
 #include "peer.cuh"
 #include "vcycle.cuh"
+#include "sstep.cuh"
 
 using namespace helm;
 using cplx = std::complex<double>;
@@ -101,6 +102,14 @@ struct Fgm {
   int gxc = 0;               // clusters of DC_CL chunks (0: no cluster pass 1)
   GsGeom geo{};              // Gram-Schmidt launch geometry
   FgmState* st = nullptr;
+  // s-step coarse solve (sstep.cuh, reading R28): block size, dots grid (nbx chunks x gy row
+  // ranges of crows rows), update blocks; raw Hessenberg matrix, block factors, pass partials
+  int ss = 0, ss_nbx = 0, ss_gy = 0, ss_crows = 0, ss_nu = 0, ss_nred = 0, ss_ring = 0;
+  size_t ss_smem = 0;
+  long long ss_chunk = 0;
+  double2 *Hr = nullptr, *sCm = nullptr, *sRi = nullptr, *sCt = nullptr, *sRt = nullptr;
+  double *sP = nullptr, *spart = nullptr, *ssig = nullptr;
+  unsigned* sticket = nullptr;
 };
 
 }  // namespace
@@ -1096,6 +1105,9 @@ void fgm_free(Fgm& K) {
   cudaFree(K.cnt);
   cudaFree(K.npart);
   cudaFree(K.st);
+  for (void* q : {(void*)K.Hr, (void*)K.sCm, (void*)K.sRi, (void*)K.sCt, (void*)K.sRt, (void*)K.sP, (void*)K.spart,
+                  (void*)K.ssig, (void*)K.sticket})
+    cudaFree(q);
   K = Fgm();
 }
 
@@ -1330,6 +1342,168 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
   return gs_update(C, K, K.Z + off, &st->ncols, 0, K.y, 1.0, first ? DVec() : xo, xo, 0, nullptr);
 }
 
+// ------------------------------------------------------------------ s-step coarse solve
+// (sstep.cuh, reading R28): the restarted coarse GMRES(m) with its basis generated and
+// orthogonalised s vectors at a time.  Single GPU, A-DEF1/APD, m a multiple of s.
+constexpr int sstep_ept(int S) { return S <= 4 ? 4 : (S <= 8 ? 2 : 1); }
+// shared memory of k_bgs_hess: X | Ctot | Rtot | sn | cs [| raw Hessenberg rows 0..J of columns 0..J-1]
+bool sstep_hess_stage(int m) { return m <= 96; }
+size_t sstep_hess_smem(int m, int S) {
+  return ((size_t)(m + 1 + S) * S + (size_t)(m + 1) * S + S * S + m) * sizeof(double2) + (size_t)(m + 1) * sizeof(double) +
+         (sstep_hess_stage(m) ? (size_t)m * (m + 1) * sizeof(double2) : 0);
+}
+
+template <int S>
+int sstep_alloc_t(helm_ctx_s& C, Fgm& K) {
+  constexpr int EPT = sstep_ept(S);
+  constexpr int NV = BgsNV<S>::v;
+  const int m = K.m;
+  const int rows = m + 1 + S;
+  K.ss = S;
+  K.ss_crows = std::min(rows, (int)(96 * 1024 / (BG_WARPS * NV * sizeof(double))));
+  K.ss_gy = (rows + K.ss_crows - 1) / K.ss_crows;
+  const size_t dsm = (size_t)BG_WARPS * K.ss_crows * NV * sizeof(double);
+  CKR(raise_dyn_smem((const void*)k_bgs_dots<S, EPT>, dsm));
+  int bps = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bgs_dots<S, EPT>, BG_THREADS, dsm));
+  const long long n = (long long)K.n, unit = 32LL * EPT;
+  const long long nbx = std::max(1LL, (long long)std::max(1, bps) * C.sm_count / K.ss_gy);
+  K.ss_chunk = ((n + nbx - 1) / nbx + unit - 1) / unit * unit;
+  K.ss_nbx = (int)((n + K.ss_chunk - 1) / K.ss_chunk);
+  const size_t usm = ((size_t)(m + 1) * S + S * S) * sizeof(double2);
+  CKR(raise_dyn_smem((const void*)k_bgs_update<S>, usm));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bgs_update<S>, BG_THREADS, usm));
+  K.ss_nu = std::max(1, bps) * C.sm_count;
+  K.ss_nred = (int)(((long long)rows * NV * 32 + 255) / 256);
+  CKR(raise_dyn_smem((const void*)k_bgs_hess<S>, sstep_hess_smem(m, S)));
+  CKR(raise_dyn_smem((const void*)k_bgs_reduce<S>, (size_t)rows * S * sizeof(double2)));
+  // pass partials from a cp.async shared-memory ring (k_bgs_dots_smem) when NS stages of the
+  // largest block fit the shared memory, else the register form (HELM_PROBE_BGS=0 forces it: probe)
+  static const int ring = getenv("HELM_PROBE_BGS") ? atoi(getenv("HELM_PROBE_BGS")) : 1;
+  const size_t rsm = std::max((size_t)rows * BS_RS * BT_NS, (size_t)2 * BS_THREADS * S * sizeof(double2));
+  K.ss_ring = (ring && rsm <= 220 * 1024) ? 1 : 0;
+  if (K.ss_ring) {
+    K.ss_smem = rsm;
+    CKR(raise_dyn_smem((const void*)k_bgs_dots_smem<S, BT_NS>, rsm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bgs_dots_smem<S, BT_NS>, BS_THREADS, rsm));
+    K.ss_gy = 1;
+    const long long nbm = std::max(1LL, (long long)std::max(1, bps) * C.sm_count);
+    K.ss_chunk = ((n + nbm - 1) / nbm + BT_SE - 1) / BT_SE * BT_SE;
+    K.ss_nbx = (int)((n + K.ss_chunk - 1) / K.ss_chunk);
+  }
+  CKR(dalloc(&K.Hr, (size_t)(m + 1) * m));
+  CKR(dalloc(&K.sCm, (size_t)(m + 1) * S));
+  CKR(dalloc(&K.sCt, (size_t)(m + 1) * S));
+  CKR(dalloc(&K.sRi, (size_t)S * S));
+  CKR(dalloc(&K.sRt, (size_t)S * S));
+  CKR(dalloc(&K.sP, (size_t)rows * NV));
+  CKR(dalloc(&K.spart, (size_t)rows * NV * K.ss_nbx));
+  CKR(dalloc(&K.ssig, 1));
+  CKR(dalloc(&K.sticket, 1));
+  CK(cudaMemsetAsync(K.sticket, 0, sizeof(unsigned), C.s));
+  CK(cudaMemcpyAsync(K.ssig, &C.p.sstep_shift, sizeof(double), cudaMemcpyHostToDevice, C.s));
+  CK(cudaStreamSynchronize(C.s));
+  return HELM_OK;
+}
+
+int sstep_alloc(helm_ctx_s& C, Fgm& K, int s) {
+  switch (s) {
+    case 4: return sstep_alloc_t<4>(C, K);
+    case 6: return sstep_alloc_t<6>(C, K);
+    case 8: return sstep_alloc_t<8>(C, K);
+  }
+  return fail(HELM_EINVAL, "sstep must be 0, 4, 6 or 8 (got %d)", s);
+}
+
+// One block of s steps: the powers (V-cycle + E in residual mode per vector), the block
+// Gram-Schmidt pass(es), the Hessenberg columns, rotations and the loop decision.
+// mask (helm_bench_graph regions only): 1 = the pass partials, 2 = their reduction, 4 = the update
+// (one pass each), 8 = one step of the powers, 16 = one E apply in residual mode; 0 = the block.
+template <int S>
+int sstep_block(helm_ctx_s& C, Fgm& K, cudaGraphConditionalHandle h, int use_h, int mask = 0) {
+  constexpr int EPT = sstep_ept(S);
+  constexpr int NV = BgsNV<S>::v;
+  const long long ld = (long long)K.ld;
+  FgmState* st = K.st;
+  double2* Vo = K.V + K.off;
+  const int npow = mask == 0 ? S : ((mask & 24) ? 1 : 0);
+  for (int i = 1; i <= npow; ++i) {   // w_i = sigma w_{i-1} - E M^{-1} w_{i-1}  (V[J+i])
+    const DVec win(K.V + (size_t)(i - 1) * ld, &st->j, ld), wout(K.V + (size_t)i * ld, &st->j, ld);
+    if (mask != 16) CKR(vcycle(C, 1, win, DVec(K.Z), nullptr));
+    CKR(apply_E(C, DVec(K.Z), DVec(K.V + (size_t)(i - 1) * ld, &st->j, ld, K.ssig), wout, true));
+  }
+  if (mask & 24) return HELM_OK;
+  const size_t dsm = (size_t)BG_WARPS * K.ss_crows * NV * sizeof(double);
+  const size_t usm = ((size_t)(K.m + 1) * S + S * S) * sizeof(double2);
+  for (int p = 0; p < (mask ? 1 : C.p.sstep_passes); ++p) {
+    if (!mask || (mask & 1)) {
+    if (K.ss_ring)
+      launch_k(C, k_bgs_dots_smem<S, BT_NS>, dim3(K.ss_nbx), dim3(BS_THREADS), K.ss_smem, (const double2*)Vo, ld,
+               (const int*)&st->j, (long long)K.n, K.ss_chunk, K.m + 1 + S, K.spart);
+    else
+      launch_k(C, k_bgs_dots<S, EPT>, dim3(K.ss_nbx, K.ss_gy), dim3(BG_THREADS), dsm, (const double2*)Vo, ld,
+               (const int*)&st->j, (long long)K.n, K.ss_chunk, K.ss_crows, K.spart);
+    CKR(post_launch(C));
+    }
+    if (!mask || (mask & 2)) {
+      launch_k(C, k_bgs_reduce<S>, dim3(K.ss_nred), dim3(256), (size_t)(K.m + 1 + S) * S * sizeof(double2),
+               (const double*)K.spart, K.ss_nbx, st, p, K.sP, K.sCm, K.sRi, K.sCt, K.sRt, K.sticket);
+      CKR(post_launch(C));
+    }
+    if (!mask || (mask & 4)) {
+      launch_k(C, k_bgs_update<S>, dim3(K.ss_nu), dim3(BG_THREADS), usm, Vo, ld, (const int*)&st->j, (long long)K.n,
+               (const double2*)K.sCm, (const double2*)K.sRi);
+      CKR(post_launch(C));
+    }
+  }
+  if (mask) return HELM_OK;
+  launch_k(C, k_bgs_hess<S>, dim3(1), dim3(256), sstep_hess_smem(K.m, S), st,
+           (const double2*)K.sCt, (const double2*)K.sRt, (const double*)K.ssig, K.Hr, K.H, K.cs, K.sn, K.g,
+           sstep_hess_stage(K.m) ? 1 : 0, h, use_h);
+  return post_launch(C);
+}
+
+// One restart cycle of the s-step coarse GMRES(m): from e = 0 (first) or the current e; at the
+// end e (+)= M^{-1} (Q y) -- one V-cycle per cycle instead of a stored Z basis.
+template <class OpA>
+int sstep_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, DVec b, double2* x, bool first, FgmState* outer_stats) {
+  const size_t n = K.n, off = K.off;
+  const long long ln = (long long)n;
+  double2* Vo = K.V + off;
+  FgmState* st = K.st;
+  const size_t bs = ((size_t)K.m * (K.m + 1) + K.m) * sizeof(double2);
+  const bool staged = bs <= 96 * 1024;
+  auto begin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    if (first) {
+      CKR(gs_dots(C, K, nullptr, nullptr, 0, shift(b, off), 1, K.nrm, nullptr));
+      launch_k(C, k_fgm_begin, 1, 32, 0, st, K.nrm, 1, K.g, h, use_h);
+      CKR(post_launch(C));
+      launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, shift(b, off), &st->inv_beta, DVec(Vo), ln, nullptr);
+      return post_launch(C);
+    }
+    CKR(opA(DVec(x), b, DVec(K.V)));
+    CKR(gs_dots(C, K, nullptr, nullptr, 0, DVec(Vo), 1, K.nrm, nullptr));
+    launch_k(C, k_fgm_begin, 1, 32, 0, st, K.nrm, 0, K.g, h, use_h);
+    CKR(post_launch(C));
+    launch_k(C, k_scale_dvec, grid1d(C, n), 256, 0, DVec(Vo), &st->inv_beta, DVec(Vo), ln, nullptr);
+    return post_launch(C);
+  };
+  auto body = [&](cudaGraphConditionalHandle h, int use_h) -> int {
+    switch (K.ss) {
+      case 4: return sstep_block<4>(C, K, h, use_h);
+      case 6: return sstep_block<6>(C, K, h, use_h);
+      case 8: return sstep_block<8>(C, K, h, use_h);
+    }
+    return fail(HELM_EINVAL, "bad s-step block size %d", K.ss);
+  };
+  CKR(run_while(C, st, begin, body));
+  launch_k(C, k_fgm_backsub, 1, 256, staged ? bs : 0, st, K.H, K.g, K.y, outer_stats, staged ? 1 : 0, K.cs, K.sn,
+           (const double2*)nullptr);
+  CKR(post_launch(C));
+  CKR(gs_update(C, K, Vo, &st->ncols, 0, K.y, 1.0, DVec(), DVec(K.Z + off), 0, nullptr));
+  return vcycle(C, 1, DVec(K.Z), DVec(x), first ? nullptr : x);
+}
+
 // e = E^{-1} c on level 1 by CSLP(V-cycle from level 1)-preconditioned FGMRES from e = 0
 // (reading R11).  inner_restart = m < inner_maxit: FGMRES(m) (reading R25) -- the first cycle
 // from e = 0, then a device-controlled while loop of restart cycles from the current e
@@ -1342,7 +1516,8 @@ int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_st
   // (updated on the owned rows only: halo exchange)
   auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(C, x, f, y, f.p == nullptr); };
   auto opP = [&](DVec v, DVec z) { return vcycle(C, 1, v, z, nullptr); };
-  CKR(fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C)));
+  if (K.ss > 0) CKR(sstep_cycle(C, K, opA, DVec(c), e, true, outer_stats));
+  else CKR(fgmres_cycle(C, K, opA, opP, DVec(c), e, true, outer_stats, fused_E_dots(C)));
   C.inner_iter_body = C.last_body;
   if (K.m >= C.p.inner_maxit) return HELM_OK;
   auto rbegin = [&](cudaGraphConditionalHandle h, int use_h) -> int {
@@ -1350,7 +1525,8 @@ int coarse_solve(helm_ctx_s& C, const double2* c, double2* e, FgmState* outer_st
     return post_launch(C);
   };
   auto rbody = [&](cudaGraphConditionalHandle h, int use_h) -> int {
-    CKR(fgmres_cycle(C, K, opA, opP, DVec(c), e, false, outer_stats, fused_E_dots(C)));
+    if (K.ss > 0) CKR(sstep_cycle(C, K, opA, DVec(c), e, false, outer_stats));
+    else CKR(fgmres_cycle(C, K, opA, opP, DVec(c), e, false, outer_stats, fused_E_dots(C)));
     launch_k(C, k_fgm_restart_cond, 1, 32, 0, K.st, outer_stats, h, use_h);
     return post_launch(C);
   };
@@ -1545,6 +1721,9 @@ void helm_default_params(helm_params* p) {
   p->inner_restart = 0;
   p->e_stream = 1;
   p->tma = 1;
+  p->sstep = 0;
+  p->sstep_passes = 2;
+  p->sstep_shift = 0.5;
 }
 
 const char* helm_last_error(void) { return g_err.c_str(); }
@@ -1853,6 +2032,15 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     const int im = p.inner_restart > 0 ? std::min(p.inner_restart, p.inner_maxit) : p.inner_maxit;
     CKR(fgm_alloc(C, C.inner, im, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
                   rank_summed(C) && G1.block, fused_E_dots(C) ? (int)(gt.x * gt.y) : 0));
+    if (p.sstep > 0) {   // s-step coarse solve (reading R28)
+      if (C.dist) return fail(HELM_EINVAL, "sstep: single-GPU contexts only");
+      if (p.precond != HELM_PRECOND_ADEF1) return fail(HELM_EINVAL, "sstep: A-DEF1/APD only");
+      if (im % p.sstep != 0)
+        return fail(HELM_EINVAL, "sstep: the coarse basis (%d columns: inner_restart or inner_maxit) must be a multiple "
+                    "of s = %d", im, p.sstep);
+      if (p.sstep_passes < 1 || p.sstep_passes > 2) return fail(HELM_EINVAL, "sstep_passes must be 1 or 2");
+      CKR(sstep_alloc(C, C.inner, p.sstep));
+    }
   }
   CK(cudaStreamSynchronize(C.s));
   return HELM_OK;
@@ -2035,9 +2223,12 @@ static int solve_device(helm_ctx_s& C, double tol, int maxit, helm_report* rep) 
       const int its0 = cycles == 0 ? 0 : C.hst->its;
       const long long in0 = cycles == 0 ? 0 : C.hst->inner_total;
       const long long rs0 = cycles == 0 ? 0 : C.hst->inner_restarts;
+      const long long bl0 = cycles == 0 ? 0 : C.hst->inner_blocks;
       CK(cudaGraphLaunch(C.gexec[gi], C.s));
       CKR(read_state(C, C.outer.st));
-      kernels += C.cnt[gi][0] + (C.hst->its - its0) * C.cnt[gi][1] + (C.hst->inner_total - in0) * C.cnt[gi][2] +
+      // inner loop bodies run once per step (one-vector form) or once per block (s-step form)
+      const long long bodies = C.inner.ss > 0 ? C.hst->inner_blocks - bl0 : C.hst->inner_total - in0;
+      kernels += C.cnt[gi][0] + (C.hst->its - its0) * C.cnt[gi][1] + bodies * C.cnt[gi][2] +
                  (C.hst->inner_restarts - rs0) * C.cnt[gi][3];
     } else {
       const long long l0 = C.launches;
@@ -2209,6 +2400,35 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         if (which == HELM_GB_DCGS_DOTS) mask = 1 | 8;   // pass 1 alone (unfused step)
         auto opA = [&](DVec x, DVec f, DVec y) { return apply_E(X, x, f, y, f.p == nullptr); };
         r = arnoldi_step(X, K, opA, fused_E_dots(X), inner_lag(X), cudaGraphConditionalHandle(0), 0, mask);
+        break;
+      }
+      case HELM_GB_SS_DOTS:
+      case HELM_GB_SS_REDUCE:
+      case HELM_GB_SS_UPDATE:
+      case HELM_GB_SS_POWER:
+      case HELM_GB_SS_E: {
+        Fgm& K = X.inner;
+        if (K.ss <= 0) {
+          r = fail(HELM_EINVAL, "s-step regions need params.sstep > 0");
+          break;
+        }
+        if (arg < 0 || arg % K.ss || arg + K.ss > K.m) {
+          r = fail(HELM_EINVAL, "bad block column %d", arg);
+          break;
+        }
+        if (i == 0) {
+          launch_k(X, k_fgm_reset, 1, 1, 0, K.st, 0.0, 1 << 30, K.m);
+          CKR(post_launch(X));
+          launch_k(X, k_set_j, 1, 1, 0, K.st, arg);
+          CKR(post_launch(X));
+        }
+        const int mask = which == HELM_GB_SS_DOTS ? 1 : which == HELM_GB_SS_REDUCE ? 2 : which == HELM_GB_SS_UPDATE ? 4
+                       : which == HELM_GB_SS_POWER ? 8 : 16;
+        switch (K.ss) {
+          case 4: r = sstep_block<4>(X, K, cudaGraphConditionalHandle(0), 0, mask); break;
+          case 6: r = sstep_block<6>(X, K, cudaGraphConditionalHandle(0), 0, mask); break;
+          case 8: r = sstep_block<8>(X, K, cudaGraphConditionalHandle(0), 0, mask); break;
+        }
         break;
       }
       default:

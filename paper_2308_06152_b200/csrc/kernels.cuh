@@ -604,9 +604,16 @@ __global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo 
   double2 xn = load_x(J + 1);
   double kfd_e = load_k(2 * J + o - 1, fe, ein), kfd_d = load_k(2 * J + o - 1, fd, din);
   double kfe_e = load_k(2 * J + o, fe, ein), kfe_d = load_k(2 * J + o, fd, din);
+  // residual mode: f of the output row (J - 1) loaded one step ahead
+  auto load_f = [&](int Jr) {
+    return (MODE == 1 && xin && Jr >= J0 && Jr < J1) ? f[(size_t)Jr * gc.nx + I] : zero;
+  };
+  double2 fpre = load_f(J - 1);
   for (; J <= J1; ++J) {
     const double2 xc = xn;
+    const double2 fo = fpre;
     const double a_fd_e = kfd_e, a_fd_d = kfd_d, a_fe_e = kfe_e, a_fe_d = kfe_d;
+    if (MODE == 1) fpre = load_f(J);
     if (J < J1) {   // next step's loads, in flight during this step's arithmetic
       xn = load_x(J + 2);
       kfd_e = load_k(2 * J + o + 1, fe, ein);
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo 
         sacc = cadd(sacc, cscale(zw<R>(1), acc0.d));
         if (R == 2) sacc = cadd(sacc, cscale(zw<R>(2), ep));
         const size_t p = (size_t)Jo * gc.nx + I;
-        y[p] = (MODE == 1) ? csub(cscale(fsc, f[p]), sacc) : sacc;
+        y[p] = (MODE == 1) ? csub(cscale(fsc, fo), sacc) : sacc;
       }
     }
     acc0 = acc1;

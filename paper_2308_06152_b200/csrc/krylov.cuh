@@ -63,6 +63,11 @@ struct FgmState {
   // the corrected residual of the previous column below tol; pend = the last column still awaits
   // its rotation (done by k_fgm_backsub)
   int lagc, pend;
+  // s-step coarse solve (sstep.cuh): a block whose Cholesky pivot broke down (set by the
+  // reduction, consumed by the Hessenberg kernel) and the count of such blocks
+  int sbrk, sbrk_total;
+  long long blocks;         // s-step blocks run by this coarse solve
+  long long inner_blocks;   // (outer state) s-step blocks over all coarse solves
 };
 
 __device__ __forceinline__ double2 warp_sum2(double2 s) {
@@ -1298,6 +1303,7 @@ __global__ void k_fgm_backsub(FgmState* st, double2* __restrict__ H, double2* __
     outer->inner_total += st->its;
     outer->inner_max = max(outer->inner_max, st->its);
     outer->inner_solves += 1;
+    outer->inner_blocks += st->blocks;
   }
 }
 
@@ -1470,6 +1476,9 @@ __global__ void k_fgm_reset(FgmState* st, double tol, int maxit, int m) {
   st->inner_solves = 0;
   st->inner_restarts = 0;
   st->relres = 0.0;
+  st->blocks = 0;
+  st->inner_blocks = 0;
+  st->sbrk = 0;
 }
 
 // L2 flush between timed launches: READ a buffer larger than L2 (leaves clean lines, so the

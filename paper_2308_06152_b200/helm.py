@@ -38,7 +38,8 @@ class helm_params(ctypes.Structure):
                 ("col_pipe", ctypes.c_int), ("fuse_dots", ctypes.c_int), ("precond", ctypes.c_int),
                 ("gamma", ctypes.c_double), ("tail_cluster", ctypes.c_int),
                 ("lag_stepb", ctypes.c_int), ("dots_cluster", ctypes.c_int), ("inner_restart", ctypes.c_int),
-                ("e_stream", ctypes.c_int), ("tma", ctypes.c_int)]
+                ("e_stream", ctypes.c_int), ("tma", ctypes.c_int), ("sstep", ctypes.c_int),
+                ("sstep_passes", ctypes.c_int), ("sstep_shift", ctypes.c_double)]
 
 
 class helm_dist(ctypes.Structure):
@@ -285,7 +286,8 @@ class Helm:
         return us.value, nb.value
 
     REGIONS = {"vcycle": 0, "apply_E": 1, "apply_A": 2, "dcgs": 3, "inner_iter": 4, "e_dots": 5, "dcgs_reduce": 6,
-               "dcgs_update": 7, "dcgs_dots": 8, "vc_down": 9, "vc_up": 10}
+               "dcgs_update": 7, "dcgs_dots": 8, "vc_down": 9, "vc_up": 10, "ss_dots": 11, "ss_reduce": 12,
+               "ss_update": 13, "ss_power": 14, "ss_e": 15}
 
     def helm_bench_graph(self, which, arg=0, reps=50):
         """Mean in-graph device time (us) of one instance of a region (warm, back-to-back)."""

@@ -1,0 +1,107 @@
+"""GPU parity of the s-step coarse solve (helm_params.sstep, reading R28) against the
+oracle's CSLP-FGMRES(m) coarse solve (reading R25), through the C ABI.
+
+The s-step form computes the iterates of the same GMRES(m) in exact arithmetic (the V-cycle is a
+fixed linear preconditioner inside a coarse solve), so the bars are those of the one-vector form
+(tests/test_gpu_restart.py): deflation operator 1e-8 with a fixed inner step count (exactly
+inner_maxit steps) or the inner solve at 1e-10 (inner count +-2 %); solves: outer count +-1 at
+1e-6, the GPU true residual within 1.05e-6, solutions within 1e-6 at an outer tolerance of 1e-10
+(reading R16).  Covered: s = 4, 6, 8; one and two block Gram-Schmidt passes; bases that restart
+mid-solve; a step cap that is not a multiple of s (the last block's extra steps discarded)."""
+import numpy as np
+import pytest
+
+import oracle
+from tests.test_gpu_parity import GRIDS, _problem, gpu, rel
+from workloads import random_field
+
+pytestmark = pytest.mark.gpu
+
+# (grid, vectors, coarse op, inner_tol, inner_maxit, inner_restart m, s, passes)
+DEFLATE_CASES = [
+    (0, "bilinear", "galerkin", 0.0, 48, 16, 8, 2),
+    (0, "bilinear", "galerkin", 0.0, 45, 16, 8, 2),       # 45 steps: 5 steps of the last block kept
+    (1, "high_order", "galerkin", 0.0, 40, 12, 4, 2),
+    (1, "high_order", "red_glk2", 0.0, 36, 12, 6, 1),
+    (2, "high_order", "galerkin", 1e-10, 2000, 24, 8, 2),
+    (2, "bilinear", "red_o4", 1e-10, 2000, 24, 6, 2),
+    (5, "high_order", "galerkin", 0.0, 64, 32, 8, 2),
+    (5, "high_order", "galerkin", 0.0, 64, 32, 8, 1),     # one pass: orthogonality O(eps kappa^2), 1e-6
+]
+
+
+@pytest.mark.parametrize("gi,vec,op,itol,imax,m,s,passes", DEFLATE_CASES)
+def test_deflate_sstep(lib, gi, vec, op, itol, imax, m, s, passes):
+    p = GRIDS[gi]
+    prm = {"coarse_op": op, "inner_tol": itol, "inner_maxit": imax, "vectors": vec, "inner_restart": m,
+           "sstep": s, "sstep_passes": passes}
+    H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, prm)
+    so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, inner_tol=itol, inner_maxit=imax,
+                                                           vectors=vec, inner_restart=m))
+    v = random_field(p.shape, 11)
+    z, its = H.deflate(gpu(v))
+    zo = so.adef1(v)
+    bar = 1e-8 if passes == 2 or gi != 5 else 1e-6
+    assert rel(z.cpu().numpy(), zo) < bar, (op, p.shape, rel(z.cpu().numpy(), zo))
+    if itol == 0.0:
+        assert its == so.inner_its[-1] == imax
+    else:
+        assert so.inner_its[-1] < imax
+        assert abs(its - so.inner_its[-1]) <= max(1, so.inner_its[-1] // 50), (its, so.inner_its[-1])
+    H.close()
+
+
+# (problem, vectors, coarse op, inner_tol, inner_maxit, inner_restart, s, passes)
+SOLVE_CASES = [
+    ("c0_tiny", "bilinear", "galerkin", 1e-1, 200, 0, 8, 2),       # m = inner_maxit = 200
+    ("c1_k50", "high_order", "galerkin", 1e-1, 160, 40, 8, 2),     # the bench method
+    ("c1_k50", "high_order", "galerkin", 1e-1, 160, 40, 8, 1),
+    ("c1_k100", "high_order", "galerkin", 1e-1, 160, 40, 8, 1),
+    ("mp_som_k40", "high_order", "galerkin", 1e-1, 300, 24, 6, 2),
+    ("wedge_f10", "high_order", "red_glk2", 1e-1, 120, 24, 4, 2),
+]
+
+
+@pytest.mark.parametrize("name,vec,op,itol,imax,irs,s,passes", SOLVE_CASES)
+def test_solve_sstep(lib, name, vec, op, itol, imax, irs, s, passes):
+    p = _problem(name)
+    prm = {"coarse_op": op, "vectors": vec, "inner_tol": itol, "inner_maxit": imax, "inner_restart": irs,
+           "coarsest_n": 512, "sstep": s, "sstep_passes": passes}
+    op_ = dict(coarse_op=op, vectors=vec, inner_tol=itol, inner_maxit=imax, inner_restart=irs, coarsest_n=512)
+    H = lib.helm_setup(p, prm)
+    x, rep = H.solve(gpu(p.b), tol=1e-6, maxit=600)
+    xo, rep_o = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(**op_, maxit=600)).solve(p.b)
+    assert rep["converged"] and rep_o["converged"]
+    assert abs(rep["outer_iterations"] - rep_o["outer_iterations"]) <= 1, (rep, rep_o["outer_iterations"])
+    assert rel(oracle.apply_A(x.cpu().numpy(), p.k, p.h, p.bc), p.b) <= 1.05e-6
+    xt, rep_t = H.solve(gpu(p.b), tol=1e-10, maxit=1200)
+    xo_t, rep_ot = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(**op_, maxit=1200, tol=1e-10)).solve(p.b)
+    assert rep_t["converged"] and rep_ot["converged"]
+    assert rel(xt.cpu().numpy(), xo_t) < 1e-6
+    H.close()
+
+
+def test_sstep_matches_one_vector_form(lib):
+    """The same bench-method solve with and without the s-step form: identical outer count and
+    inner step totals within 1 %, solutions within 1e-6 at 1e-10."""
+    p = _problem("c1_k100")
+    base = {"coarse_op": "galerkin", "vectors": "high_order", "inner_tol": 1e-1, "inner_maxit": 160,
+            "inner_restart": 40, "coarsest_n": 512}
+    H1 = lib.helm_setup(p, base)
+    H2 = lib.helm_setup(p, dict(base, sstep=8, sstep_passes=2))
+    x1, r1 = H1.solve(gpu(p.b), tol=1e-10, maxit=800)
+    x2, r2 = H2.solve(gpu(p.b), tol=1e-10, maxit=800)
+    assert r1["converged"] and r2["converged"]
+    assert abs(r1["outer_iterations"] - r2["outer_iterations"]) <= 1, (r1, r2)
+    assert abs(r1["inner_iterations_total"] - r2["inner_iterations_total"]) <= max(2, r1["inner_iterations_total"] // 100)
+    assert rel(x2.cpu().numpy(), x1.cpu().numpy()) < 1e-6
+    H1.close()
+    H2.close()
+
+
+def test_sstep_rejects_bad_basis(lib):
+    p = _problem("c0_tiny")
+    with pytest.raises(RuntimeError, match="multiple of s"):
+        lib.helm_setup(p, {"inner_maxit": 50, "inner_restart": 20, "sstep": 8})
+    with pytest.raises(RuntimeError, match="sstep must be"):
+        lib.helm_setup(p, {"inner_maxit": 50, "inner_restart": 10, "sstep": 5})
