@@ -426,8 +426,9 @@ def _run_decomposed(args, rank, world, local):
         uid = helm.nccl_unique_id()
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        # levels 0-2 decomposed, the rest replicated
-        prm = dict(method, dist_levels=args.dist_levels or 3)
+        # decomposed levels per N (the all-gather and the replicated coarse levels
+        # shrink 4x per extra decomposed level, each extra level adds one halo exchange)
+        prm = dict(method, dist_levels=args.dist_levels or (3 if world <= 2 else 4 if world <= 4 else 5))
         H = helm.HelmDist(p.nx, p.ny, p.h, p.bc, p.k, rank, world, nccl_id=uid, params=prm, stream=stream,
                           peer_exchange=peer_exchange)
         try:
