@@ -160,8 +160,9 @@ typedef struct {
                           matrix, one update sweep), Hessenberg columns recovered from the block
                           factors.  The same GMRES(m) iterates in exact arithmetic (the V-cycle is a
                           fixed linear preconditioner within a coarse solve); per-step convergence
-                          test and counts.  Single GPU, A-DEF1/APD, the coarse basis size
-                          (inner_restart, else inner_maxit) a multiple of s */
+                          test and counts.  Decomposed contexts: one rank sum of the block's dot
+                          products per s steps (instead of two per step).  A-DEF1/APD, the coarse
+                          basis size (inner_restart, else inner_maxit) a multiple of s */
   int sstep_passes;    /* block Gram-Schmidt passes per block: 2 (default, BCGS-PIP2) or 1 */
   double sstep_shift;  /* shift sigma of the block basis w_i = sigma w_{i-1} - A w_{i-1} (default 0.5,
                           the centre of the CSLP-preconditioned spectrum's disc) */

@@ -1344,7 +1344,8 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
 
 // ------------------------------------------------------------------ s-step coarse solve
 // (sstep.cuh, reading R28): the restarted coarse GMRES(m) with its basis generated and
-// orthogonalised s vectors at a time.  Single GPU, A-DEF1/APD, m a multiple of s.
+// orthogonalised s vectors at a time.  A-DEF1/APD, m a multiple of s; decomposed contexts sum the
+// block dot products over the ranks once per block.
 constexpr int sstep_ept(int S) { return S <= 4 ? 4 : (S <= 8 ? 2 : 1); }
 // shared memory of k_bgs_hess: X | Ctot | Rtot | sn | cs [| raw Hessenberg rows 0..J of columns 0..J-1]
 bool sstep_hess_stage(int m) { return m <= 96; }
@@ -1397,6 +1398,7 @@ int sstep_alloc_t(helm_ctx_s& C, Fgm& K) {
   CKR(dalloc(&K.sRi, (size_t)S * S));
   CKR(dalloc(&K.sRt, (size_t)S * S));
   CKR(dalloc(&K.sP, (size_t)rows * NV));
+  CK(cudaMemsetAsync(K.sP, 0, (size_t)rows * NV * sizeof(double), C.s));   // rank sums read every slot
   CKR(dalloc(&K.spart, (size_t)rows * NV * K.ss_nbx));
   CKR(dalloc(&K.ssig, 1));
   CKR(dalloc(&K.sticket, 1));
@@ -1445,9 +1447,17 @@ int sstep_block(helm_ctx_s& C, Fgm& K, cudaGraphConditionalHandle h, int use_h, 
                (const int*)&st->j, (long long)K.n, K.ss_chunk, K.ss_crows, K.spart);
     CKR(post_launch(C));
     }
-    if (!mask || (mask & 2)) {
+    if ((!mask || (mask & 2)) && !K.dist) {
       launch_k(C, k_bgs_reduce<S>, dim3(K.ss_nred), dim3(256), (size_t)(K.m + 1 + S) * S * sizeof(double2),
-               (const double*)K.spart, K.ss_nbx, st, p, K.sP, K.sCm, K.sRi, K.sCt, K.sRt, K.sticket);
+               (const double*)K.spart, K.ss_nbx, st, p, K.sP, K.sCm, K.sRi, K.sCt, K.sRt, K.sticket, 3);
+      CKR(post_launch(C));
+    } else if (!mask || (mask & 2)) {   // decomposed: the block dot products summed over the ranks
+      launch_k(C, k_bgs_reduce<S>, dim3(K.ss_nred), dim3(256), 0, (const double*)K.spart, K.ss_nbx, st, p, K.sP,
+               K.sCm, K.sRi, K.sCt, K.sRt, K.sticket, 1);
+      CKR(post_launch(C));
+      CKR(allreduce(C, reinterpret_cast<double2*>(K.sP), (K.m + 1 + S) * NV / 2));
+      launch_k(C, k_bgs_reduce<S>, dim3(1), dim3(256), (size_t)(K.m + 1 + S) * S * sizeof(double2),
+               (const double*)K.spart, K.ss_nbx, st, p, K.sP, K.sCm, K.sRi, K.sCt, K.sRt, K.sticket, 2);
       CKR(post_launch(C));
     }
     if (!mask || (mask & 4)) {
@@ -2033,7 +2043,6 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
     CKR(fgm_alloc(C, C.inner, im, (size_t)G1.nown * G1.g.nx, G1.n, (size_t)G1.own0 * G1.g.nx,
                   rank_summed(C) && G1.block, fused_E_dots(C) ? (int)(gt.x * gt.y) : 0));
     if (p.sstep > 0) {   // s-step coarse solve (reading R28)
-      if (C.dist) return fail(HELM_EINVAL, "sstep: single-GPU contexts only");
       if (p.precond != HELM_PRECOND_ADEF1) return fail(HELM_EINVAL, "sstep: A-DEF1/APD only");
       if (im % p.sstep != 0)
         return fail(HELM_EINVAL, "sstep: the coarse basis (%d columns: inner_restart or inner_maxit) must be a multiple "

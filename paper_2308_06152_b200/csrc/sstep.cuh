@@ -274,11 +274,14 @@ __device__ void tri_inverse(const double2* R, double2* Ri) {   // Ri = R^{-1}, b
 // C = P(0..J, :), G = W^H W - C^H C, G = R^H R (Cholesky), R^{-1}; the accumulated factors of
 // the block (W = Q Ctot + Q_new Rtot): pass 0 Ctot = C, Rtot = R; pass 1 Ctot += C Rtot,
 // Rtot = R Rtot.  A non-positive Cholesky pivot (W numerically dependent on Q) marks st->sbrk.
+// phase 3: both parts in one launch (the last block does the dense part); decomposed contexts
+// launch phase 1 (sums), sum P over the ranks, then phase 2 (dense part, one block).
 template <int S>
 __global__ void __launch_bounds__(256) k_bgs_reduce(const double* __restrict__ part, int nparts, FgmState* st, int pass,
                                                     double* __restrict__ P, double2* __restrict__ Cm,
                                                     double2* __restrict__ Ri, double2* __restrict__ Ctot,
-                                                    double2* __restrict__ Rtot, unsigned* __restrict__ ticket) {
+                                                    double2* __restrict__ Rtot, unsigned* __restrict__ ticket,
+                                                    int phase) {
   HELM_PDL_ENTRY();
   constexpr int NV = BgsNV<S>::v;
   const int J = st->j;
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(256) k_bgs_reduce(const double* __restrict__ p
   const int lane = threadIdx.x & 31;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nout = (long long)nrows * NV;
-  if (gw < nout && (gw % NV) < 2 * S) {
+  if ((phase & 1) && gw < nout && (gw % NV) < 2 * S) {
     const double* p = part + gw * nparts;
     double s = 0.0;
     for (int b = lane; b < nparts; b += 32) s += p[b];
@@ -294,7 +297,8 @@ __global__ void __launch_bounds__(256) k_bgs_reduce(const double* __restrict__ p
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) P[gw] = s;
   }
-  if (!last_block(ticket)) return;
+  if (!(phase & 2)) return;
+  if (phase == 3 && !last_block(ticket)) return;
   __shared__ double2 G[S * S], R[S * S], Rin[S * S], Rt[S * S];
   __shared__ int brk;
   extern __shared__ double2 rsm[];   // the summed rows, complex: (J+1+S) x S

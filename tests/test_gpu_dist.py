@@ -157,8 +157,25 @@ def test_dist_solve(lib, name, P, vec, op, itol, imax, outer):
     """Outer iteration counts within +-1 of the oracle's, the true residual met, and at tol 1e-10
     the solution within 1e-6 of the oracle's (reading R16), with every rank reporting the same
     counts."""
+    _dist_solve_case(lib, name, P, vec, op, itol, imax, outer, {})
+
+
+# s-step coarse solve on decomposed contexts (reading R28): one rank sum of the block's dot
+# products per s steps; the oracle runs the one-vector FGMRES(m)
+@pytest.mark.parametrize("name,P,vec,op,itol,imax,outer,extra", [
+    ("c1_k50", 2, "high_order", "galerkin", 1e-1, 160, "fgmres", {"inner_restart": 40, "sstep": 8, "sstep_passes": 2}),
+    ("c1_k50", 3, "high_order", "galerkin", 1e-1, 160, "fgmres", {"inner_restart": 40, "sstep": 8, "sstep_passes": 1}),
+    ("wedge_f10", 4, "high_order", "galerkin", 1e-1, 120, "fgmres", {"inner_restart": 24, "sstep": 6}),
+    ("mp_som_k40", 2, "bilinear", "red_o4", 0.0, 32, "gcr", {"inner_restart": 16, "sstep": 4}),
+])
+def test_dist_solve_sstep(lib, name, P, vec, op, itol, imax, outer, extra):
+    _dist_solve_case(lib, name, P, vec, op, itol, imax, outer, extra)
+
+
+def _dist_solve_case(lib, name, P, vec, op, itol, imax, outer, extra):
     p = _problem(name)
-    prm = dict(SMALL, coarse_op=op, vectors=vec, inner_tol=itol, inner_maxit=imax, outer=outer)
+    prm = dict(SMALL, coarse_op=op, vectors=vec, inner_tol=itol, inner_maxit=imax, outer=outer, **extra)
+    irs = extra.get("inner_restart", 0)
 
     def go(tol):
         def fn(H):
@@ -172,14 +189,16 @@ def test_dist_solve(lib, name, P, vec, op, itol, imax, outer):
 
     x, rep = go(1e-6)
     so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
-                                                           inner_maxit=imax, maxit=600, outer=outer))
+                                                           inner_maxit=imax, maxit=600, outer=outer,
+                                                           inner_restart=irs))
     xo, ro = so.solve(p.b)
     assert rep["converged"] and ro["converged"]
     assert abs(rep["outer_iterations"] - ro["outer_iterations"]) <= 1, (rep, ro["outer_iterations"])
     assert rel(oracle.apply_A(x, p.k, p.h, p.bc), p.b) <= 1.05e-6
     xt, rt = go(1e-10)
     so_t = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(coarse_op=op, vectors=vec, inner_tol=itol,
-                                                             inner_maxit=imax, maxit=600, tol=1e-10, outer=outer))
+                                                             inner_maxit=imax, maxit=600, tol=1e-10, outer=outer,
+                                                             inner_restart=irs))
     xo_t, _ = so_t.solve(p.b)
     assert rt["converged"]
     assert rel(xt, xo_t) < 1e-6

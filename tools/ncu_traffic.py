@@ -43,10 +43,22 @@ def main():
     except (OSError, ValueError):
         out = {}
     for rep in sys.argv[4:]:
+        if "=" in rep:   # LABEL=rep.ncu-rep: every launch of the capture summed under one key (a V-cycle)
+            label, rep = rep.split("=", 1)
+            ds = list(rows(rep))
+            key = f"{workload}:{label}"
+            out[key] = {"dram_bytes": sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds),
+                        "dram_read": sum(d["dram__bytes_read.sum"] for d in ds),
+                        "dram_write": sum(d["dram__bytes_write.sum"] for d in ds),
+                        "us": sum(d["gpu__time_duration.sum"] for d in ds), "launches": len(ds), "column": None,
+                        "bytes_per_column": 0.0,
+                        "src": os.path.basename(rep) + f" ({len(ds)} launches summed; ncu --set full, cold caches)"}
+            print(key, json.dumps(out[key]))
+            continue
         for d in rows(rep):
             name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("helm::", "").replace(" ", "")
             base = name.split("<")[0]
-            per_col = 16.0 * n1 if base in ("k_dcgs_update", "k_dcgs_dots") else 0.0
+            per_col = 16.0 * n1 if base in ("k_dcgs_update", "k_dcgs_dots", "k_bgs_dots_smem", "k_bgs_update") else 0.0
             key = f"{workload}:{name}"
             out[key] = {"dram_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
                         "dram_read": d["dram__bytes_read.sum"], "dram_write": d["dram__bytes_write.sum"],
