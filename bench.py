@@ -36,13 +36,14 @@ sys.path.insert(0, ROOT)
 # Method of the timed workload: higher-order deflation vectors (APD, the paper's
 # wavenumber-independent variant, Table 4) with the Galerkin coarse operator E; outer flexible
 # GMRES (§6.3: a flexible outer method keeps the outer accuracy with a loose coarse
-# tolerance); the coarse problem by CSLP-FGMRES(40) (reading R25) to 1e-1 capped at 160 steps;
+# tolerance); the coarse problem by CSLP-FGMRES(48) (reading R25) to 1e-1 capped at 192 steps;
 # the CSLP hierarchy stops at the first level with <= 512 unknowns (§4 "predefined
-# coarsest grid size"), solved exactly (R8).  Chosen by the time-to-1e-6 sweep on c4_weak_2049
-# (profiles/r02_c4_sweep.jsonl: cap/restart 120/30 .. 200/50 lie within 5 %; 160/40 the fastest;
-# any outer restart stagnates).
-DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 160,
-                  "inner_restart": 40, "coarsest_n": 512, "restart": 0}
+# coarsest grid size"), solved exactly (R8).  Chosen by the time-to-1e-6 sweeps on c4_weak_2049
+# (profiles/r02_c4_sweep.jsonl, one-vector coarse solve: cap/restart 120/30 .. 200/50 within 5 %,
+# 160/40 the fastest; profiles/r02_c4_sweep_sstep.jsonl, s-step coarse solve, restart a multiple
+# of s = 8: 192/48 and 224/56 the fastest, 462 / 396 outer iterations; any outer restart stagnates).
+DEFAULT_METHOD = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 1e-1, "inner_maxit": 192,
+                  "inner_restart": 48, "coarsest_n": 512, "restart": 0}
 DEFAULT_WORKLOAD = "c4_weak_2049"
 # Device form of the coarse solve (reading R28, §6d): the basis generated and
 # orthogonalised 8 vectors at a time (one block Gram-Schmidt pass), measured 25.2 -> 16.9 s on
@@ -305,9 +306,20 @@ def kernel_roofline(H, rep, method, peaks, workload):
             ("k_dcgs_reduceA (pass-1 partial sums + step A)", "dcgs_reduce", jm, 4, inner_its,
              (2 * jm + 2) * 16.0 * (tiles if fused else -(-n1 // 256))),
         ]
+    # the inner V-cycle by kernel: the two level-1 legs (the largest V-cycle kernels of the launch
+    # list) and the rest of the cycle from level 2 (11 kernels on levels <= 511^2 + the coarsest)
+    n2 = lv[2] if len(lv) > 2 else 0
+    vbytes2 = sum(104.0 * lv[l] for l in range(2, len(lv) - 1)) + 16.0 * lv[-1] ** 2 + 32.0 * lv[-1]
+    if len(lv) > 3 and H.params.nu_pre == 1 and H.params.nu_post == 1:
+        comps += [
+            ("k_vc_down (V-cycle down leg, level 1)", "vc_down", 1, 10, inner_its + outer_its, 44.0 * n1 + 0 * n2),
+            ("k_vc_up (V-cycle up leg, level 1)", "vc_up", 1, 10, inner_its + outer_its, 60.0 * n1),
+            ("V-cycle from level 2 (11 kernels)", "vcycle", 2, 10, inner_its + outer_its, vbytes2),
+        ]
+    else:
+        comps.append(("V-cycle from level 1 (inner CSLP preconditioner)", "vcycle", 1, 10, inner_its + outer_its,
+                      vbytes))
     comps += [
-        ("V-cycle from level 1 (inner CSLP preconditioner, 13 kernels)", "vcycle", 1, 10, inner_its + outer_its,
-         vbytes),
         ("k_apply_op A (level 0)", "apply_A", 0, 10, 2 * outer_its, 40.0 * n0),
     ]
     rows = {}
@@ -321,7 +333,8 @@ def kernel_roofline(H, rep, method, peaks, workload):
                                                    "ss_update", "ss_reduce") else None,
                        "timing": "in-graph, warm (helm_bench_graph: the solve's own launch, replayed)",
                        "peak_src": peaks["src"]}
-    dom = max(rows.values(), key=lambda r: r["est_ms_per_step"])
+    # the dominant KERNEL (groups of kernels are reported, not chosen)
+    dom = max((r for r in rows.values() if "kernels)" not in r["kernel"]), key=lambda r: r["est_ms_per_step"])
     # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture of
     # the same launch at this workload (tools/ncu_regions.py; cold caches)
     try:

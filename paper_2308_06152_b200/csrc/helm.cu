@@ -530,11 +530,13 @@ int defl_prolong(helm_ctx_s& C, const double2* e, double2* y) {
 
 constexpr int GLK_TX = 16, GLK_TY = 8;   // coarse outputs per k_galerkin_apply CTA
 
-// Rows per warp segment of k_glk_stream: enough warps for ~16 per SM (28 columns per warp),
-// at least 8 rows (4 rows of warm-up per segment), at most 64.
-int glk_stream_rows(const helm_ctx_s& C, int ncx, int ncy) {
+// Rows per warp segment of k_glk_stream: one wave of resident warps (4 x the mode's blocks per SM:
+// 16 plain, 12 residual; 28 columns per warp), at least 8 rows (4 rows of warm-up per segment),
+// at most 64.
+int glk_stream_rows(const helm_ctx_s& C, int ncx, int ncy, bool res) {
   const long long nb = (ncx + 27) / 28;
-  static const int wps = getenv("HELM_PROBE_COL_WPS") ? atoi(getenv("HELM_PROBE_COL_WPS")) : 16;   // probe only
+  static const int wps_env = getenv("HELM_PROBE_COL_WPS") ? atoi(getenv("HELM_PROBE_COL_WPS")) : 0;   // probe only
+  const int wps = wps_env ? wps_env : 4 * (res ? HELM_GLKS_MINB_RES : HELM_GLKS_MINB);
   const long long target = (long long)wps * C.sm_count;
   long long S = (ncy * nb + target - 1) / target;
   return (int)std::max(8LL, std::min(64LL, S));
@@ -583,7 +585,7 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y, bool fresh = false) {
       y = shift(y, wo);
       if (C.p.e_stream && !C.dist) {   // column-streaming kernel (registers, no shared-memory tiles)
         const int nb = (Gw.g.nx + 27) / 28;
-        const int S = glk_stream_rows(C, Gw.g.nx, Gw.g.ny);
+        const int S = glk_stream_rows(C, Gw.g.nx, Gw.g.ny, res);
         const long long warps = (long long)nb * ((Gw.g.ny + S - 1) / S);
         const dim3 gs((unsigned)((warps + 3) / 4));
         if (C.p.vectors == HELM_VECTORS_BILINEAR) {

@@ -511,8 +511,13 @@ __global__ void __launch_bounds__(256, DOTS ? HELM_GLKD_MINB : 6) k_galerkin_app
 #ifndef HELM_GLKS_MINB   // resident 128-thread blocks per SM the register cap aims at
 #define HELM_GLKS_MINB 4
 #endif
+// residual mode (the s-step powers): 3 blocks per SM -- no spills (at 4 it spilled ~100 B per
+// thread), 34.2 -> 32.0 us per apply on the 1023^2 level; plain mode keeps 4 (28.5 vs 29.7 us)
+#ifndef HELM_GLKS_MINB_RES
+#define HELM_GLKS_MINB_RES 3
+#endif
 template <int R, int MODE>
-__global__ void __launch_bounds__(128, HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
+__global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
                                                     DVec fv, DVec yv, int S, int nbands) {
   HELM_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
