@@ -1349,6 +1349,9 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
 // orthogonalised s vectors at a time.  A-DEF1/APD, m a multiple of s; decomposed contexts sum the
 // block dot products over the ranks once per block.
 constexpr int sstep_ept(int S) { return S <= 4 ? 4 : (S <= 8 ? 2 : 1); }
+#ifndef BGS_RING_DEFAULT
+#define BGS_RING_DEFAULT 2
+#endif
 // shared memory of k_bgs_hess: X | Ctot | Rtot | sn | cs [| raw Hessenberg rows 0..J of columns 0..J-1]
 bool sstep_hess_stage(int m) { return m <= 96; }
 size_t sstep_hess_smem(int m, int S) {
@@ -1380,20 +1383,28 @@ int sstep_alloc_t(helm_ctx_s& C, Fgm& K) {
   K.ss_nred = (int)(((long long)rows * NV * 32 + 255) / 256);
   CKR(raise_dyn_smem((const void*)k_bgs_hess<S>, sstep_hess_smem(m, S)));
   CKR(raise_dyn_smem((const void*)k_bgs_reduce<S>, (size_t)rows * S * sizeof(double2)));
-  // pass partials from a cp.async shared-memory ring (k_bgs_dots_smem) when NS stages of the
-  // largest block fit the shared memory, else the register form (HELM_PROBE_BGS=0 forces it: probe)
-  static const int ring = getenv("HELM_PROBE_BGS") ? atoi(getenv("HELM_PROBE_BGS")) : 1;
-  const size_t rsm = std::max((size_t)rows * BS_RS * BT_NS, (size_t)2 * BS_THREADS * S * sizeof(double2));
-  K.ss_ring = (ring && rsm <= 220 * 1024) ? 1 : 0;
-  if (K.ss_ring) {
+  // pass partials from a cp.async shared-memory ring (k_bgs_dots_smem) when its stages fit the
+  // shared memory, else the register form.  Ring geometries (HELM_PROBE_BGS, probe): 1 = 3 stages
+  // of 64 elements, 1 block/SM; 2 = 2 x 48, 2 blocks/SM; 3 = 3 x 32, 2 blocks/SM; 0 = register form
+  static const int ring = getenv("HELM_PROBE_BGS") ? atoi(getenv("HELM_PROBE_BGS")) : BGS_RING_DEFAULT;
+  K.ss_ring = 0;
+  auto try_ring = [&](int id, const void* fn, size_t rsm, int se) -> int {
+    if (ring != id || rsm > 220 * 1024) return HELM_OK;
+    CKR(raise_dyn_smem(fn, rsm));
+    int b2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, fn, BS_THREADS, rsm));
+    if (b2 < 1) return HELM_OK;
+    K.ss_ring = id;
     K.ss_smem = rsm;
-    CKR(raise_dyn_smem((const void*)k_bgs_dots_smem<S, BT_NS>, rsm));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bgs_dots_smem<S, BT_NS>, BS_THREADS, rsm));
     K.ss_gy = 1;
-    const long long nbm = std::max(1LL, (long long)std::max(1, bps) * C.sm_count);
-    K.ss_chunk = ((n + nbm - 1) / nbm + BT_SE - 1) / BT_SE * BT_SE;
+    const long long nbm = (long long)b2 * C.sm_count;
+    K.ss_chunk = ((n + nbm - 1) / nbm + se - 1) / se * se;
     K.ss_nbx = (int)((n + K.ss_chunk - 1) / K.ss_chunk);
-  }
+    return HELM_OK;
+  };
+  CKR(try_ring(1, (const void*)k_bgs_dots_smem<S, BgsRing<3, 64, 1>>, BgsRing<3, 64, 1>::smem(rows, S), 64));
+  CKR(try_ring(2, (const void*)k_bgs_dots_smem<S, BgsRing<2, 48, 2>>, BgsRing<2, 48, 2>::smem(rows, S), 48));
+  CKR(try_ring(3, (const void*)k_bgs_dots_smem<S, BgsRing<3, 32, 2>>, BgsRing<3, 32, 2>::smem(rows, S), 32));
   CKR(dalloc(&K.Hr, (size_t)(m + 1) * m));
   CKR(dalloc(&K.sCm, (size_t)(m + 1) * S));
   CKR(dalloc(&K.sCt, (size_t)(m + 1) * S));
@@ -1441,9 +1452,12 @@ int sstep_block(helm_ctx_s& C, Fgm& K, cudaGraphConditionalHandle h, int use_h, 
   const size_t usm = ((size_t)(K.m + 1) * S + S * S) * sizeof(double2);
   for (int p = 0; p < (mask ? 1 : C.p.sstep_passes); ++p) {
     if (!mask || (mask & 1)) {
-    if (K.ss_ring)
-      launch_k(C, k_bgs_dots_smem<S, BT_NS>, dim3(K.ss_nbx), dim3(BS_THREADS), K.ss_smem, (const double2*)Vo, ld,
-               (const int*)&st->j, (long long)K.n, K.ss_chunk, K.m + 1 + S, K.spart);
+    if (K.ss_ring) {
+      auto fn = K.ss_ring == 1 ? k_bgs_dots_smem<S, BgsRing<3, 64, 1>>
+              : K.ss_ring == 2 ? k_bgs_dots_smem<S, BgsRing<2, 48, 2>> : k_bgs_dots_smem<S, BgsRing<3, 32, 2>>;
+      launch_k(C, fn, dim3(K.ss_nbx), dim3(BS_THREADS), K.ss_smem, (const double2*)Vo, ld, (const int*)&st->j,
+               (long long)K.n, K.ss_chunk, K.m + 1 + S, K.spart);
+    }
     else
       launch_k(C, k_bgs_dots<S, EPT>, dim3(K.ss_nbx, K.ss_gy), dim3(BG_THREADS), dsm, (const double2*)Vo, ld,
                (const int*)&st->j, (long long)K.n, K.ss_chunk, K.ss_crows, K.spart);

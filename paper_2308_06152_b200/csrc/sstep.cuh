@@ -158,18 +158,22 @@ __global__ void __launch_bounds__(BG_THREADS, 2) k_bgs_dots(const double2* __res
 // FP64 DMMA m8n8k4 forms of this sweep -- register fragments, or the same ring filled by cp.async
 // or by bulk copies -- measured slower on B200: DMMA issues at ~1 per 40 cycles per SM
 // sub-partition, ~14 TFLOP/s).
-// Stage = 64 elements x (J+1+S) rows (row stride 1040 B: consecutive rows start 4 banks apart).
+// Stage = SE elements x (J+1+S) rows (row stride 16 SE + 16 B: consecutive rows start 4 banks apart).
 // Thread (rb, eg), rb < RB = ceil(rows / 2), eg < EG = 256 / RB: rows rb and rb + RB, elements
 // eg, eg + EG, ... of every stage, all S columns in registers (2 S complex accumulators) for the
 // whole kernel; one shared-memory reduction over eg at the end.
-constexpr int BT_SE = 64;                         // elements per stage
-#ifndef BT_NS
-#define BT_NS 3                                   // stages in flight
-#endif
-constexpr int BS_RS = BT_SE * 16 + 16;
 constexpr int BS_THREADS = 256;
-template <int S, int NS>
-__global__ void __launch_bounds__(BS_THREADS, 1) k_bgs_dots_smem(const double2* __restrict__ V, long long ld,
+// ring geometry: NS stages of SE elements (SE a multiple of 8), MINB resident blocks per SM
+template <int NS_, int SE_, int MINB_>
+struct BgsRing {
+  static constexpr int NS = NS_, SE = SE_, MINB = MINB_;
+  static constexpr int RS = SE * 16 + 16;   // bytes per staged row
+  static size_t smem(int rows, int S) {
+    return std::max((size_t)rows * RS * NS, (size_t)2 * BS_THREADS * S * sizeof(double2));
+  }
+};
+template <int S, class RG>
+__global__ void __launch_bounds__(BS_THREADS, RG::MINB) k_bgs_dots_smem(const double2* __restrict__ V, long long ld,
                                                                  const int* __restrict__ jptr, long long n,
                                                                  long long chunk, int rmax, double* __restrict__ part) {
   HELM_PDL_ENTRY();
@@ -182,11 +186,11 @@ __global__ void __launch_bounds__(BS_THREADS, 1) k_bgs_dots_smem(const double2* 
   const bool act = eg < EG;
   const int c0 = rb, c1 = rb + RB;
   const bool ok1 = c1 < nrows;
-  constexpr int SE = BT_SE;
-  constexpr int RSd = BS_RS / 16;            // row stride in double2 (16 B of padding)
+  constexpr int SE = RG::SE, NS = RG::NS;
+  constexpr int RSd = RG::RS / 16;           // row stride in double2 (16 B of padding)
   const long long e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const int nst = e1 > e0 ? (int)((e1 - e0 + SE - 1) / SE) : 0;
-  const size_t stage_bytes = (size_t)rmax * BS_RS;   // >= nrows * RSd * 16
+  const size_t stage_bytes = (size_t)rmax * RG::RS;   // >= nrows * RSd * 16
   auto issue = [&](int st) {
     if (st < nst) {
       const long long es = e0 + (long long)st * SE;
