@@ -105,3 +105,23 @@ def test_sstep_rejects_bad_basis(lib):
         lib.helm_setup(p, {"inner_maxit": 50, "inner_restart": 20, "sstep": 8})
     with pytest.raises(RuntimeError, match="sstep must be"):
         lib.helm_setup(p, {"inner_maxit": 50, "inner_restart": 10, "sstep": 5})
+
+
+@pytest.mark.parametrize("name", ["c3_marm_f20_2945", "c4_weak_2049"])
+def test_sstep_full_size(lib, name):
+    """BASELINE sizes with the bench method (coarse FGMRES(48) capped at 192, s = 8, one pass):
+    the s-step and one-vector forms take the same outer count (+-1) and both meet the true
+    residual 1e-6 (configs[3] Marmousi-shaped 2945 x 929 at 20 Hz; configs[4]'s 2047^2 block)."""
+    p = _problem(name)
+    base = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": 192,
+            "inner_restart": 48, "coarsest_n": 512}
+    b = gpu(p.b)
+    out = []
+    for ss in (0, 8):
+        H = lib.helm_setup(p, dict(base, sstep=ss, sstep_passes=1))
+        x, rep = H.solve(b, tol=1e-6, maxit=1000)
+        rr = float((H.apply_A(x) - b).norm() / b.norm())
+        H.close()
+        assert rep["converged"] and rr <= 1.05e-6, (ss, rep, rr)
+        out.append(rep)
+    assert abs(out[0]["outer_iterations"] - out[1]["outer_iterations"]) <= 1, out
