@@ -422,7 +422,7 @@ def _run_decomposed(args, rank, world, local):
     peaks = load_peaks()
     base = config_problem(args.workload)
     p = strip_problem(base.meta["k"], base.meta["n_cells"], world, f"{args.workload}_x{world}")
-    method = method_of(args)
+    method = gpu_method(args)
     uid = peer_exchange = None
     if args.transport == "peer":        # NVLink peer memory through CUDA IPC (peer.cuh), no NCCL
         def peer_exchange(handle):

@@ -583,7 +583,7 @@ int apply_E(helm_ctx_s& C, DVec x, DVec f, DVec y, bool fresh = false) {
       x = shift(x, wo);
       f = shift(f, wo);
       y = shift(y, wo);
-      if (C.p.e_stream && !C.dist) {   // column-streaming kernel (registers, no shared-memory tiles)
+      if (C.p.e_stream) {   // column-streaming kernel (registers, no shared-memory tiles; blocks too)
         const int nb = (Gw.g.nx + 27) / 28;
         const int S = glk_stream_rows(C, Gw.g.nx, Gw.g.ny, res);
         const long long warps = (long long)nb * ((Gw.g.ny + S - 1) / S);
@@ -1699,7 +1699,10 @@ int ensure_outer(helm_ctx_s& C, int maxit) {
   // points depend on it), so the cap comes from the total, not the free, memory
   // an explicit restart length is the method (no cap: fails if it does not fit); a full basis
   // (restart = 0) is capped by the memory and then restarts, which the report shows
-  const size_t budget = C.dist ? tot / 4 : fr / 100 * 85;
+  // (70 % of the device: a rank's hierarchy, inner basis and NCCL buffers take a few GB; the
+  // configs[4] weak block needs ~460 columns of 2 x 67 MB -- at tot / 4 the basis capped at 335
+  // columns and the restarted FGMRES stagnated)
+  const size_t budget = C.dist ? tot / 100 * 70 : fr / 100 * 85;
   const int mreq = m;
   if (C.p.restart > 0) m = std::min(m, 4096);
   else m = (int)std::max<size_t>(4, std::min<size_t>((size_t)std::min(m, 4096), budget / per));
@@ -2684,13 +2687,14 @@ int helm_setup_dist(helm_ctx* out, const helm_grid* grid, const double* k, int k
   C->kind = d->kind;
   C->rank = d->rank;
   C->nranks = d->nranks;
-  C->x1 = d->kind == HELM_COMM_PEER && (d->flags & HELM_DIST_EXCHANGE_AT_ONE_RANK);
+  C->x1 = (d->kind == HELM_COMM_PEER || d->kind == HELM_COMM_NCCL) && (d->flags & HELM_DIST_EXCHANGE_AT_ONE_RANK);
   C->grp = d->kind == HELM_COMM_THREADS ? d->group : nullptr;
   // decomposed solves: host-polled loops (thread groups and NCCL; the peer transport is pure
   // kernels with device-side epochs, so its solves may run as CUDA graphs), no cluster tail /
   // cooperative step.  PDL stays as requested: a kernel launched with it waits
   // (griddepcontrol.wait) for its predecessor kernel -- ours or NCCL's -- to complete.
-  if (d->kind != HELM_COMM_PEER) C->p.graph = 0;
+  static const bool nccl_graph = getenv("HELM_NCCL_GRAPH") && atoi(getenv("HELM_NCCL_GRAPH"));   // probe
+  if (d->kind != HELM_COMM_PEER && !(d->kind == HELM_COMM_NCCL && nccl_graph)) C->p.graph = 0;
   C->p.tail_max_n = 0;
   C->p.coop = 0;
   if (C->p.dist_min_rows <= 0) C->p.dist_min_rows = 16;
