@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
     return (MODE == 1 && xin && Jr >= J0 && Jr < J1) ? f[(size_t)Jr * gc.nx + I] : zero;
   };
   double2 fpre = load_f(J - 1);
-  for (; J <= J1; ++J) {
+  for (; J <= J1; ++J) {   // (unrolled by 2 / 3: 33.3 / 35.7 us against 32.1 in residual mode)
     const double2 xc = xn;
     const double2 fo = fpre;
     const double a_fd_e = kfd_e, a_fd_d = kfd_d, a_fe_e = kfe_e, a_fe_d = kfe_d;
