@@ -28,6 +28,8 @@ for v in variants:
     prm = dict(base, sstep=int(s), sstep_passes=int(ps or 2))
     if "PROBE_GRAPH" in os.environ:   # 0: host-polled loops (ncu sees every kernel)
         prm["graph"] = int(os.environ["PROBE_GRAPH"])
+    if "PROBE_OUTER" in os.environ:   # fgmres | gcr
+        prm["outer"] = os.environ["PROBE_OUTER"]
     if "PROBE_SHIFT" in os.environ:
         prm["sstep_shift"] = float(os.environ["PROBE_SHIFT"])
     H = helm.helm_setup(p, prm)
