@@ -1350,7 +1350,7 @@ int fgmres_cycle(helm_ctx_s& C, Fgm& K, OpA&& opA, OpP&& opP, DVec b, double2* x
 // block dot products over the ranks once per block.
 constexpr int sstep_ept(int S) { return S <= 4 ? 4 : (S <= 8 ? 2 : 1); }
 #ifndef BGS_RING_DEFAULT
-#define BGS_RING_DEFAULT 2
+#define BGS_RING_DEFAULT 3
 #endif
 // shared memory of k_bgs_hess: X | Ctot | Rtot | sn | cs [| raw Hessenberg rows 0..J of columns 0..J-1]
 bool sstep_hess_stage(int m) { return m <= 96; }
@@ -1385,7 +1385,8 @@ int sstep_alloc_t(helm_ctx_s& C, Fgm& K) {
   CKR(raise_dyn_smem((const void*)k_bgs_reduce<S>, (size_t)rows * S * sizeof(double2)));
   // pass partials from a cp.async shared-memory ring (k_bgs_dots_smem) when its stages fit the
   // shared memory, else the register form.  Ring geometries (HELM_PROBE_BGS, probe): 1 = 3 stages
-  // of 64 elements, 1 block/SM; 2 = 2 x 48, 2 blocks/SM; 3 = 3 x 32, 2 blocks/SM; 0 = register form
+  // of 64 elements, 1 block/SM; 2 = 2 x 48, 2 blocks/SM; 3 (default) = as 2, but blocks of at most
+  // 3 s + 1 rows stage 128 elements (measured over a cycle: 1080 / 1016 / 967 us); 0 = register form
   static const int ring = getenv("HELM_PROBE_BGS") ? atoi(getenv("HELM_PROBE_BGS")) : BGS_RING_DEFAULT;
   K.ss_ring = 0;
   auto try_ring = [&](int id, const void* fn, size_t rsm, int se) -> int {
@@ -1402,9 +1403,14 @@ int sstep_alloc_t(helm_ctx_s& C, Fgm& K) {
     K.ss_nbx = (int)((n + K.ss_chunk - 1) / K.ss_chunk);
     return HELM_OK;
   };
-  CKR(try_ring(1, (const void*)k_bgs_dots_smem<S, BgsRing<3, 64, 1>>, BgsRing<3, 64, 1>::smem(rows, S), 64));
-  CKR(try_ring(2, (const void*)k_bgs_dots_smem<S, BgsRing<2, 48, 2>>, BgsRing<2, 48, 2>::smem(rows, S), 48));
-  CKR(try_ring(3, (const void*)k_bgs_dots_smem<S, BgsRing<3, 32, 2>>, BgsRing<3, 32, 2>::smem(rows, S), 32));
+  // small-row blocks (J + 1 + s <= 3 s + 1: the first blocks of a cycle) take 128-element stages
+  constexpr int RSM = 3 * S + 1;
+  CKR(try_ring(1, (const void*)k_bgs_dots_smem<S, BgsRing<3, 64, 1>, BgsRing<3, 64, 1>, 0>,
+               BgsRing<3, 64, 1>::smem(rows, S), 64));
+  CKR(try_ring(2, (const void*)k_bgs_dots_smem<S, BgsRing<2, 48, 2>, BgsRing<2, 48, 2>, 0>,
+               BgsRing<2, 48, 2>::smem(rows, S), 48));
+  CKR(try_ring(3, (const void*)k_bgs_dots_smem<S, BgsRing<2, 128, 2>, BgsRing<2, 48, 2>, RSM>,
+               std::max(BgsRing<2, 48, 2>::smem(rows, S), BgsRing<2, 128, 2>::smem(std::min(rows, RSM), S)), 48));
   CKR(dalloc(&K.Hr, (size_t)(m + 1) * m));
   CKR(dalloc(&K.sCm, (size_t)(m + 1) * S));
   CKR(dalloc(&K.sCt, (size_t)(m + 1) * S));
@@ -1453,8 +1459,9 @@ int sstep_block(helm_ctx_s& C, Fgm& K, cudaGraphConditionalHandle h, int use_h, 
   for (int p = 0; p < (mask ? 1 : C.p.sstep_passes); ++p) {
     if (!mask || (mask & 1)) {
     if (K.ss_ring) {
-      auto fn = K.ss_ring == 1 ? k_bgs_dots_smem<S, BgsRing<3, 64, 1>>
-              : K.ss_ring == 2 ? k_bgs_dots_smem<S, BgsRing<2, 48, 2>> : k_bgs_dots_smem<S, BgsRing<3, 32, 2>>;
+      auto fn = K.ss_ring == 1 ? k_bgs_dots_smem<S, BgsRing<3, 64, 1>, BgsRing<3, 64, 1>, 0>
+              : K.ss_ring == 2 ? k_bgs_dots_smem<S, BgsRing<2, 48, 2>, BgsRing<2, 48, 2>, 0>
+                               : k_bgs_dots_smem<S, BgsRing<2, 128, 2>, BgsRing<2, 48, 2>, 3 * S + 1>;
       launch_k(C, fn, dim3(K.ss_nbx), dim3(BS_THREADS), K.ss_smem, (const double2*)Vo, ld, (const int*)&st->j,
                (long long)K.n, K.ss_chunk, K.m + 1 + S, K.spart);
     }

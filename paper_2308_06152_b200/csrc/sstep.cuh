@@ -173,13 +173,10 @@ struct BgsRing {
   }
 };
 template <int S, class RG>
-__global__ void __launch_bounds__(BS_THREADS, RG::MINB) k_bgs_dots_smem(const double2* __restrict__ V, long long ld,
-                                                                 const int* __restrict__ jptr, long long n,
-                                                                 long long chunk, int rmax, double* __restrict__ part) {
-  HELM_PDL_ENTRY();
+__device__ __forceinline__ void bgs_dots_body(const double2* __restrict__ V, long long ld, int J, long long n,
+                                              long long chunk, int rmax, double* __restrict__ part,
+                                              unsigned char* ssm) {
   constexpr int NV = BgsNV<S>::v;
-  extern __shared__ __align__(128) unsigned char ssm[];
-  const int J = *jptr;
   const int nrows = J + 1 + S;
   const int RB = (nrows + 1) / 2, EG = BS_THREADS / RB;
   const int tid = threadIdx.x, rb = tid % RB, eg = tid / RB;
@@ -252,6 +249,19 @@ __global__ void __launch_bounds__(BS_THREADS, RG::MINB) k_bgs_dots_smem(const do
     part[((long long)c * NV + 2 * t) * gridDim.x + blockIdx.x] = sum.x;
     part[((long long)c * NV + 2 * t + 1) * gridDim.x + blockIdx.x] = sum.y;
   }
+}
+
+// Blocks with few rows (J + 1 + S <= RSMALL) stage longer element runs (RGS), so the bytes in
+// flight do not shrink with J; the rest RGL.  One kernel, the branch taken on the device-side J.
+template <int S, class RGS, class RGL, int RSMALL>
+__global__ void __launch_bounds__(BS_THREADS, RGL::MINB) k_bgs_dots_smem(const double2* __restrict__ V, long long ld,
+                                                                  const int* __restrict__ jptr, long long n,
+                                                                  long long chunk, int rmax, double* __restrict__ part) {
+  HELM_PDL_ENTRY();
+  extern __shared__ __align__(128) unsigned char ssm[];
+  const int J = *jptr;
+  if (J + 1 + S <= RSMALL) bgs_dots_body<S, RGS>(V, ld, J, n, chunk, RSMALL, part, ssm);
+  else bgs_dots_body<S, RGL>(V, ld, J, n, chunk, rmax, part, ssm);
 }
 
 // Upper-triangular helpers on S x S row-major complex matrices (one thread).
