@@ -377,8 +377,14 @@ __global__ void __launch_bounds__(256) k_bgs_reduce(const double* __restrict__ p
 
 // W <- (W - Q C) R^{-1} for W = V[J+1 .. J+S], Q = V[0 .. J] (in place: every element's outputs
 // depend on that element's inputs only).  One element per thread per step.
+#ifndef HELM_BGU_MINB
+#define HELM_BGU_MINB 2
+#endif
+#ifndef HELM_BGU_UNROLL
+#define HELM_BGU_UNROLL 4
+#endif
 template <int S>
-__global__ void __launch_bounds__(BG_THREADS, 2) k_bgs_update(double2* __restrict__ V, long long ld,
+__global__ void __launch_bounds__(BG_THREADS, HELM_BGU_MINB) k_bgs_update(double2* __restrict__ V, long long ld,
                                                               const int* __restrict__ jptr, long long n,
                                                               const double2* __restrict__ Cm,
                                                               const double2* __restrict__ Ri) {
@@ -396,12 +402,13 @@ __global__ void __launch_bounds__(BG_THREADS, 2) k_bgs_update(double2* __restric
 #pragma unroll
     for (int t = 0; t < S; ++t) w[t] = W[(long long)t * ld + e];
     int c = 0;
-    for (; c + 4 <= J + 1; c += 4) {
-      double2 q[4];
+    constexpr int UN = HELM_BGU_UNROLL;
+    for (; c + UN <= J + 1; c += UN) {
+      double2 q[UN];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) q[k] = ldb<2>(V + (long long)(c + k) * ld + e);
+      for (int k = 0; k < UN; ++k) q[k] = ldb<2>(V + (long long)(c + k) * ld + e);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < UN; ++k)
 #pragma unroll
         for (int t = 0; t < S; ++t) {
           const double2 cc = sC[(c + k) * S + t];
