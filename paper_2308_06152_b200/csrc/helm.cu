@@ -2074,7 +2074,13 @@ static int setup_impl(helm_ctx_s& C, const helm_grid* grid, const double* k, int
         return fail(HELM_EINVAL, "sstep: the coarse basis (%d columns: inner_restart or inner_maxit) must be a multiple "
                     "of s = %d", im, p.sstep);
       if (p.sstep_passes < 1 || p.sstep_passes > 2) return fail(HELM_EINVAL, "sstep_passes must be 1 or 2");
-      CKR(sstep_alloc(C, C.inner, p.sstep));
+      // a coarse space of fewer than 2 (m + 1 + s) unknowns becomes A-invariant inside a block (the
+      // block Gram matrix turns singular before GMRES reaches its happy breakdown): such tiny
+      // problems keep the one-vector form, which handles the breakdown exactly
+      const long long ncoarse = (long long)C.L[1].g.nx * C.L[1].g.ny;
+      if (ncoarse >= 2LL * (im + 1 + p.sstep)) CKR(sstep_alloc(C, C.inner, p.sstep));
+      else if (getenv("HELM_VERBOSE"))
+        fprintf(stderr, "[helm] sstep: %lld coarse unknowns < 2 (m + 1 + s); one-vector coarse solve\n", ncoarse);
     }
   }
   CK(cudaStreamSynchronize(C.s));

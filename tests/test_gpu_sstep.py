@@ -129,3 +129,17 @@ def test_sstep_full_size(lib, name):
     # few -- 1 % of the count (reading R13: counts of truncated inner solves are rounding-sensitive)
     n0, n1 = out[0]["outer_iterations"], out[1]["outer_iterations"]
     assert abs(n0 - n1) <= max(1, n0 // 100), out
+
+
+@pytest.mark.parametrize("gi", [3, 4])
+def test_sstep_tiny_coarse_space(lib, gi):
+    """A coarse space smaller than a block's basis (the smallest Dirichlet and Sommerfeld grids)
+    keeps the one-vector form: deflation equals the oracle's."""
+    p = GRIDS[gi]
+    prm = {"inner_tol": 1e-10, "inner_maxit": 48, "inner_restart": 16, "sstep": 8}
+    H = lib.Helm(p.nx, p.ny, p.h, p.bc, p.k, prm)
+    so = oracle.Solver(p.k, p.h, p.bc, oracle.SolverParams(inner_tol=1e-10, inner_maxit=48, inner_restart=16))
+    v = random_field(p.shape, 5)
+    z, its = H.deflate(gpu(v))
+    assert rel(z.cpu().numpy(), so.adef1(v)) < 1e-8
+    H.close()
