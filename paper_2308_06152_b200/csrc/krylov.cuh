@@ -131,6 +131,26 @@ __global__ void __launch_bounds__(GS_THREADS) k_gs_dots(const double2* __restric
   const long long e1 = min(n, e0 + chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gx = gridDim.x;
+  if (ntot == 1 && nvec == 0) {   // a norm alone (restart residuals): every warp of the block streams
+    if (blockIdx.y != 0) return;
+    double s = 0.0;
+    for (long long e = e0 + threadIdx.x; e < e1; e += GS_THREADS) {
+      const double2 v = w[e];
+      s = fma(v.x, v.x, fma(v.y, v.y, s));
+    }
+    __shared__ double wsum[GS_WARPS];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) wsum[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < GS_WARPS; ++q) t += wsum[q];
+      part[blockIdx.x] = make_double2(t, 0.0);
+    }
+    return;
+  }
   for (int c = blockIdx.y * GS_WARPS + warp; c < ntot; c += gridDim.y * GS_WARPS) {
     double2 acc = make_double2(0.0, 0.0);
     const bool isnorm = (c == nvec);
