@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace helm {
 
 // Programmatic dependent launch (PDL): every kernel first waits until the grids it depends on
@@ -544,13 +546,14 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
   auto load_k = [&](int fy, int fx, bool in) { return (in && row_in(fy)) ? kf[(size_t)fy * gf.nx + fx] : 0.0; };
   // x-interpolated coarse row (t before the y interpolation) at this lane's two fine columns
   struct TX { double2 e, d; };
-  auto xinterp = [&](double2 xs) {
+  auto xinterp = [&](double2 xs, auto allinc) {
+    constexpr bool AI = decltype(allinc)::value;
     const double2 xm = shup(xs), xp = shdn(xs);
     TX t;
     // even relative column: taps I-1, I, I+1 (1/8, 3/4, 1/8 | 0, 1, 0); odd: I, I+1 (1/2, 1/2)
     // (zero weights dropped: the odd column is 0.5 (x_I + x_{I+1}); bilinear even = x_I)
-    t.e = ein ? (R == 2 ? cadd(cadd(cscale(wm_e, xm), cscale(w0_e, xs)), cscale(wp_e, xp)) : xs) : zero;
-    t.d = din ? cscale(0.5, cadd(xs, xp)) : zero;
+    t.e = (AI || ein) ? (R == 2 ? cadd(cadd(cscale(wm_e, xm), cscale(w0_e, xs)), cscale(wp_e, xp)) : xs) : zero;
+    t.d = (AI || din) ? cscale(0.5, cadd(xs, xp)) : zero;
     return t;
   };
   // s = A t at fine row fy for both columns; c = centre row, sth / nth = the rows below / above.
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
 
   int J = J0 - 2;
   // state: tx(J-1), tx(J); t rows fe(J-1), fd(J-1); Z^T_y sums of output rows J-1, J, J+1
-  TX txm = xinterp(load_x(J - 1)), tx0 = xinterp(load_x(J));
+  TX txm = xinterp(load_x(J - 1), std::false_type()), tx0 = xinterp(load_x(J), std::false_type());
   const TX tz = {zero, zero};
   TX tfe_m = tz, tfd_m = tz;   // rows fe(J-1), fd(J-1): only feed rows before J0 - 1
   TX acc0 = tz, acc1 = tz, acc2 = tz;
@@ -614,30 +617,69 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
     return (MODE == 1 && xin && Jr >= J0 && Jr < J1) ? f[(size_t)Jr * gc.nx + I] : zero;
   };
   double2 fpre = load_f(J - 1);
-  for (; J <= J1; ++J) {   // (unrolled by 2 / 3: 33.3 / 35.7 us against 32.1 in residual mode)
+  // Steps in [Ja, Jb) touch only rows inside both grids (x rows J-1 .. J+2, fine rows
+  // 2J+o-1 .. 2J+o+2, output row J-1 in [J0, J1), f row J in [J0, J1)): they run without the
+  // row-range tests, with int offsets and A's interior form -- on interior bands (FAST 2) with
+  // no lane tests either; on the edge bands of a Dirichlet grid (FAST 1), where every
+  // multiplier of an in-grid fine node is the interior one and out-of-grid t values are zero,
+  // with the lanes outside the fine grid masked to zero.  Each warp runs at most ~4 general
+  // steps, so the one-wave grid stays balanced (Sommerfeld edge bands: general steps only).
+  const bool simpleA = gf.bc == BC_DIRICHLET || band_int;
+  const int Ja = max(J, max(J0 + 1, 1));
+  const int Jb = simpleA ? max(Ja, min(J1, min(gc.ny - 2, (gf.ny - 3 - o) / 2 + 1))) : Ja;
+  auto step = [&](const int J, auto fastc) {
+    constexpr int FAST = decltype(fastc)::value;
+    constexpr bool ALLIN = FAST == 2;   // every lane's I, fe, fd inside the grids
     const double2 xc = xn;
     const double2 fo = fpre;
     const double a_fd_e = kfd_e, a_fd_d = kfd_d, a_fe_e = kfe_e, a_fe_d = kfe_d;
-    if (MODE == 1) fpre = load_f(J);
-    if (J < J1) {   // next step's loads, in flight during this step's arithmetic
-      xn = load_x(J + 2);
-      kfd_e = load_k(2 * J + o + 1, fe, ein);
-      kfd_d = load_k(2 * J + o + 1, fd, din);
-      kfe_e = load_k(2 * J + o + 2, fe, ein);
-      kfe_d = load_k(2 * J + o + 2, fd, din);
+    if (FAST) {
+      if (MODE == 1) fpre = (ALLIN || xin) ? f[J * gc.nx + I] : zero;
+      xn = (ALLIN || xin) ? x[(J + 2) * gc.nx + I] : zero;
+      const int r1 = (2 * J + o + 1) * gf.nx;
+      kfd_e = (ALLIN || ein) ? kf[r1 + fe] : 0.0;
+      kfd_d = (ALLIN || din) ? kf[r1 + fd] : 0.0;
+      kfe_e = (ALLIN || ein) ? kf[r1 + gf.nx + fe] : 0.0;
+      kfe_d = (ALLIN || din) ? kf[r1 + gf.nx + fd] : 0.0;
+    } else {
+      if (MODE == 1) fpre = load_f(J);
+      if (J < J1) {   // next step's loads, in flight during this step's arithmetic
+        xn = load_x(J + 2);
+        kfd_e = load_k(2 * J + o + 1, fe, ein);
+        kfd_d = load_k(2 * J + o + 1, fd, din);
+        kfe_e = load_k(2 * J + o + 2, fe, ein);
+        kfe_d = load_k(2 * J + o + 2, fd, din);
+      }
     }
-    const TX txp = xinterp(xc);   // tx(J+1)
+    const TX txp = xinterp(xc, std::integral_constant<bool, ALLIN>());   // tx(J+1)
     // y interpolation: fine rows fe(J) (taps J-1, J, J+1) and fd(J) (taps J, J+1)
     TX tfe, tfd;
-    const bool fe_row = row_in(2 * J + o), fd_row = row_in(2 * J + o + 1);
+    const bool fe_row = FAST || row_in(2 * J + o), fd_row = FAST || row_in(2 * J + o + 1);
     tfe.e = fe_row ? (R == 2 ? cadd(cadd(cscale(wm_e, txm.e), cscale(w0_e, tx0.e)), cscale(wp_e, txp.e)) : tx0.e) : zero;
     tfe.d = fe_row ? (R == 2 ? cadd(cadd(cscale(wm_e, txm.d), cscale(w0_e, tx0.d)), cscale(wp_e, txp.d)) : tx0.d) : zero;
     tfd.e = fd_row ? cscale(0.5, cadd(tx0.e, txp.e)) : zero;
     tfd.d = fd_row ? cscale(0.5, cadd(tx0.d, txp.d)) : zero;
     // s = A t on rows fd(J-1) (south fe(J-1), north fe(J)) and fe(J) (south fd(J-1), north fd(J))
     TX s_fdm, s_fe;
-    apply_A_row(2 * J + o - 1, tfe_m, tfd_m, tfe, a_fd_e, a_fd_d, s_fdm);
-    apply_A_row(2 * J + o, tfd_m, tfe, tfd, a_fe_e, a_fe_d, s_fe);
+    if (FAST) {
+      auto fastA = [&](const TX& sth, const TX& c, const TX& nth, double ke, double kd, TX& s) {
+        const double2 west_e = shup(c.d), east_d = shdn(c.e);
+        const double ape = 4.0 * ih2 - ke * ke, apd = 4.0 * ih2 - kd * kd;
+        const double2 ne = cadd(cadd(west_e, c.d), cadd(sth.e, nth.e));
+        const double2 nd = cadd(cadd(c.e, east_d), cadd(sth.d, nth.d));
+        s.e = make_double2(fma(ape, c.e.x, -ih2 * ne.x), fma(ape, c.e.y, -ih2 * ne.y));
+        s.d = make_double2(fma(apd, c.d.x, -ih2 * nd.x), fma(apd, c.d.y, -ih2 * nd.y));
+        if (!ALLIN) {   // Dirichlet edge band: no fine node outside the grid
+          if (!ein) s.e = zero;
+          if (!din) s.d = zero;
+        }
+      };
+      fastA(tfe_m, tfd_m, tfe, a_fd_e, a_fd_d, s_fdm);
+      fastA(tfd_m, tfe, tfd, a_fe_e, a_fe_d, s_fe);
+    } else {
+      apply_A_row(2 * J + o - 1, tfe_m, tfd_m, tfe, a_fd_e, a_fd_d, s_fdm);
+      apply_A_row(2 * J + o, tfd_m, tfe, tfd, a_fe_e, a_fe_d, s_fe);
+    }
     // Z^T along y, in increasing fine-row order per output row (b = -R .. R)
     add(acc0, zw<R>(1), s_fdm);   // output J-1: b = +1, +2
     if (R == 2) add(acc0, zw<R>(2), s_fe);
@@ -648,14 +690,14 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
     {
       const double2 em = shup(acc0.e), dm = shup(acc0.d), ep = shdn(acc0.e);
       const int Jo = J - 1;
-      if (Jo >= J0 && Jo < J1 && lane >= 2 && lane < 30 && I < gc.nx) {
+      if ((FAST || (Jo >= J0 && Jo < J1)) && lane >= 2 && lane < 30 && (ALLIN || I < gc.nx)) {
         double2 sacc = zero;
         if (R == 2) sacc = cadd(sacc, cscale(zw<R>(-2), em));
         sacc = cadd(sacc, cscale(zw<R>(-1), dm));
         sacc = cadd(sacc, cscale(zw<R>(0), acc0.e));
         sacc = cadd(sacc, cscale(zw<R>(1), acc0.d));
         if (R == 2) sacc = cadd(sacc, cscale(zw<R>(2), ep));
-        const size_t p = (size_t)Jo * gc.nx + I;
+        const size_t p = FAST ? (size_t)(Jo * gc.nx + I) : (size_t)Jo * gc.nx + I;
         y[p] = (MODE == 1) ? csub(cscale(fsc, fo), sacc) : sacc;
       }
     }
@@ -666,7 +708,14 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
     tx0 = txp;
     tfe_m = tfe;
     tfd_m = tfd;
-  }
+  };
+  using General = std::integral_constant<int, 0>;
+  for (; J < Ja; ++J) step(J, General());
+  if (band_int)   // (loops unrolled by 2 / 3 measured slower: register pressure)
+    for (; J < Jb; ++J) step(J, std::integral_constant<int, 2>());
+  else
+    for (; J < Jb; ++J) step(J, std::integral_constant<int, 1>());
+  for (; J <= J1; ++J) step(J, General());
 }
 
 // ------------------------------------------------------------------ ReD-Glk (§5.2.4)

@@ -24,10 +24,13 @@ ap.add_argument("--inner-restart", type=int, default=0)
 ap.add_argument("--maxit", type=int, default=2000)
 ap.add_argument("--graph", type=int, default=1)
 ap.add_argument("--warm", type=int, default=0)
+ap.add_argument("--sstep", type=int, default=0)
+ap.add_argument("--sstep-passes", type=int, default=1)
 args = ap.parse_args()
 p = config_problem(args.workload)
 H = helm.helm_setup(p, {"vectors": args.vectors, "coarse_op": args.coarse_op, "inner_tol": args.inner_tol,
-                        "inner_maxit": args.inner_maxit, "inner_restart": args.inner_restart, "graph": args.graph, "coarsest_n": args.coarsest_n})
+                        "inner_maxit": args.inner_maxit, "inner_restart": args.inner_restart, "graph": args.graph, "coarsest_n": args.coarsest_n,
+                        "sstep": args.sstep, "sstep_passes": args.sstep_passes})
 b = torch.from_numpy(p.b).cuda()
 for _ in range(args.warm + 1):
     x, rep = H.solve(b, 1e-6, args.maxit)
