@@ -518,6 +518,11 @@ __global__ void __launch_bounds__(256, DOTS ? HELM_GLKD_MINB : 6) k_galerkin_app
 #ifndef HELM_GLKS_MINB_RES
 #define HELM_GLKS_MINB_RES 3
 #endif
+#ifndef HELM_GLKS_FAST_UNROLL   // unroll of the interior-step loop (probe knob)
+#define HELM_GLKS_FAST_UNROLL 2   // 22.3 vs 22.9 us (1), 22.5 (3), 23.0 (6) in residual mode
+#endif
+#define HELM_STR2(x) #x
+#define HELM_PRAGMA_UNROLL(n) _Pragma(HELM_STR2(unroll n))
 template <int R, int MODE>
 __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLKS_MINB) k_glk_stream(Geo gf, Geo gc, int o, const double* __restrict__ kf, DVec xv,
                                                     DVec fv, DVec yv, int S, int nbands) {
@@ -618,14 +623,14 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
   };
   double2 fpre = load_f(J - 1);
   // Steps in [Ja, Jb) touch only rows inside both grids (x rows J-1 .. J+2, fine rows
-  // 2J+o-1 .. 2J+o+2, output row J-1 in [J0, J1), f row J in [J0, J1)): they run without the
-  // row-range tests, with int offsets and A's interior form -- on interior bands (FAST 2) with
+  // 2J+o-1 .. 2J+o+2, output row J-1 < J1 -- stored if >= J0 --, f row J < J1): they run without
+  // the row-range tests, with int offsets and A's interior form -- on interior bands (FAST 2) with
   // no lane tests either; on the edge bands of a Dirichlet grid (FAST 1), where every
   // multiplier of an in-grid fine node is the interior one and out-of-grid t values are zero,
   // with the lanes outside the fine grid masked to zero.  Each warp runs at most ~4 general
   // steps, so the one-wave grid stays balanced (Sommerfeld edge bands: general steps only).
   const bool simpleA = gf.bc == BC_DIRICHLET || band_int;
-  const int Ja = max(J, max(J0 + 1, 1));
+  const int Ja = max(J, 1);   // the warm-up steps (output rows < J0: not stored) run fast too
   const int Jb = simpleA ? max(Ja, min(J1, min(gc.ny - 2, (gf.ny - 3 - o) / 2 + 1))) : Ja;
   auto step = [&](const int J, auto fastc) {
     constexpr int FAST = decltype(fastc)::value;
@@ -690,7 +695,7 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
     {
       const double2 em = shup(acc0.e), dm = shup(acc0.d), ep = shdn(acc0.e);
       const int Jo = J - 1;
-      if ((FAST || (Jo >= J0 && Jo < J1)) && lane >= 2 && lane < 30 && (ALLIN || I < gc.nx)) {
+      if ((FAST ? Jo >= J0 : (Jo >= J0 && Jo < J1)) && lane >= 2 && lane < 30 && (ALLIN || I < gc.nx)) {
         double2 sacc = zero;
         if (R == 2) sacc = cadd(sacc, cscale(zw<R>(-2), em));
         sacc = cadd(sacc, cscale(zw<R>(-1), dm));
@@ -711,8 +716,10 @@ __global__ void __launch_bounds__(128, MODE == 1 ? HELM_GLKS_MINB_RES : HELM_GLK
   };
   using General = std::integral_constant<int, 0>;
   for (; J < Ja; ++J) step(J, General());
-  if (band_int)   // (loops unrolled by 2 / 3 measured slower: register pressure)
+  if (band_int) {
+    HELM_PRAGMA_UNROLL(HELM_GLKS_FAST_UNROLL)
     for (; J < Jb; ++J) step(J, std::integral_constant<int, 2>());
+  }
   else
     for (; J < Jb; ++J) step(J, std::integral_constant<int, 1>());
   for (; J <= J1; ++J) step(J, General());
