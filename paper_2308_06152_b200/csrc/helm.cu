@@ -183,8 +183,11 @@ int grid1d(const helm_ctx_s& C, size_t n) {
 
 // Launch on the context stream.  With params.pdl the launch carries programmatic stream
 // serialization (PDL): the kernel's CTAs may be scheduled while its predecessor drains and
-// wait in griddepcontrol.wait (first statement of every kernel) until the predecessor's
-// results are visible; in a captured graph this becomes a programmatic edge.
+// wait in griddepcontrol.wait until the predecessor's results are visible; in a captured graph
+// this becomes a programmatic edge.  griddepcontrol.wait is the first statement of every kernel
+// except k_vc_up and k_gemv, which first load inputs written two or more launches back (set-up
+// data, this level's down-leg output and right-hand side): every kernel waits before it lets its
+// dependents be scheduled, so those writes are complete when such a dependent starts.
 template <typename... KArgs, typename... Args>
 void launch_k(helm_ctx_s& C, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
   cudaLaunchConfig_t cfg = {};

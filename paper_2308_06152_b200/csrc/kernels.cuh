@@ -1059,15 +1059,29 @@ __global__ void k_gj_extract(const double2* __restrict__ Aug, int n, double2* __
 #define HELM_GEMV_T 128
 __global__ void __launch_bounds__(HELM_GEMV_T) k_gemv(const double2* __restrict__ Minv, int n, DVec fv, DVec yv,
                                                       const double2* __restrict__ addq) {
-  HELM_PDL_ENTRY();
   __shared__ double2 part[HELM_GEMV_T / 32];
   const int row = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const double2* __restrict__ f = fv.get();
   const double2* __restrict__ r = Minv + (size_t)row * n;
+  // the inverse is set-up data: its first entries are loaded before the PDL wait (their latency
+  // overlaps the predecessor, the down leg that writes f); same summation order as the loop
+  constexpr int NP = 2;
+  double2 rp[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int c = threadIdx.x + i * HELM_GEMV_T;
+    rp[i] = c < n ? r[c] : make_double2(0.0, 0.0);
+  }
+  HELM_PDL_ENTRY();
+  const double2* __restrict__ f = fv.get();
   double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int c = threadIdx.x + i * HELM_GEMV_T;
+    if (c < n) s = cfma(rp[i], f[c], s);
+  }
 #pragma unroll 4
-  for (int c = threadIdx.x; c < n; c += HELM_GEMV_T) s = cfma(r[c], f[c], s);
+  for (int c = threadIdx.x + NP * HELM_GEMV_T; c < n; c += HELM_GEMV_T) s = cfma(r[c], f[c], s);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     s.x += __shfl_xor_sync(0xffffffffu, s.x, o);

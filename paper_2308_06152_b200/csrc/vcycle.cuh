@@ -171,7 +171,6 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
                                                const double2* __restrict__ e, DVec fv,
                                                const double* __restrict__ k, double sr, double si, double omega,
                                                const double2* __restrict__ addq, DVec yv) {
-  HELM_PDL_ENTRY();
   constexpr int RX = TX + 2, RY = TY + 2;
   constexpr int CX = TX / 2 + 3, CY = TY / 2 + 3;
   __shared__ double2 se[CY * CX];
@@ -189,15 +188,13 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
   static_assert(TY == 8 && TX <= 32, "one output point per thread");
   // every global load of the tile is issued up front: the coarse correction e (NE per thread),
   // u on the tile + halo (NU per thread) and the output point's f, k (, q)
+  // Only e is the output of the kernel launched just before this one (the coarser level's up leg
+  // or the coarsest solve).  u (this level's down leg), f (this level's right-hand side, written
+  // before the down leg), k and q (written before the V-cycle) come from kernels that completed
+  // before that predecessor passed its own griddepcontrol.wait, i.e. before it let this grid be
+  // scheduled: they are loaded before the PDL wait and their latency overlaps the predecessor.
   constexpr int NE = (CX * CY + 255) / 256, NU = (RX * RY + 255) / 256;
   double2 el[NE], ul[NU];
-#pragma unroll
-  for (int i = 0; i < NE; ++i) {
-    const int t = tid + 256 * i;
-    const int r = t / CX, c = t - r * CX;
-    const int J = cy0 + r, I = cx0 + c;
-    el[i] = (t < CX * CY && (interior || (I >= 0 && I < G.nx && J >= 0 && J < G.ny))) ? e[(size_t)J * G.nx + I] : czero();
-  }
 #pragma unroll
   for (int i = 0; i < NU; ++i) {
     const int t = tid + 256 * i;
@@ -212,6 +209,14 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
   const double2 fo = oin ? f[po] : czero();
   const double ko = oin ? k[po] : 0.0;
   const double2 qo = (oin && addq) ? addq[po] : czero();
+  HELM_PDL_ENTRY();
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int t = tid + 256 * i;
+    const int r = t / CX, c = t - r * CX;
+    const int J = cy0 + r, I = cx0 + c;
+    el[i] = (t < CX * CY && (interior || (I >= 0 && I < G.nx && J >= 0 && J < G.ny))) ? e[(size_t)J * G.nx + I] : czero();
+  }
 #pragma unroll
   for (int i = 0; i < NE; ++i) {
     const int t = tid + 256 * i;
