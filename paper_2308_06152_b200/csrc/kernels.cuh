@@ -30,10 +30,12 @@ __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_dou
 __device__ __forceinline__ double2 cconjmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
 }
-__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
-  double d = 1.0 / fma(b.x, b.x, b.y * b.y);
+__device__ __forceinline__ double cdiv_den(double2 b) { return 1.0 / fma(b.x, b.x, b.y * b.y); }
+// a / b with d = cdiv_den(b) computed beforehand (the same operations as cdiv)
+__device__ __forceinline__ double2 cdiv_d(double2 a, double2 b, double d) {
   return make_double2(fma(a.x, b.x, a.y * b.y) * d, fma(a.y, b.x, -a.x * b.y) * d);
 }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cdiv_d(a, b, cdiv_den(b)); }
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // a*b + c
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }

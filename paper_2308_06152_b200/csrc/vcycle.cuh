@@ -66,7 +66,6 @@ template <int TCX, int TCY>
 __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int o, DVec fv, const double* __restrict__ k,
                                                  double sr, double si, double omega, double2* __restrict__ u,
                                                  double2* __restrict__ fc) {
-  HELM_PDL_ENTRY();
   constexpr int RX = 2 * TCX + 3, RY = 2 * TCY + 3;  // u region
   constexpr int QX = 2 * TCX + 1, QY = 2 * TCY + 1;  // r region
   __shared__ double2 su[RY * RX];
@@ -74,8 +73,10 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int
   __shared__ double sk[RY * RX];
   __shared__ double2 sq[QY * QX];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const double2* __restrict__ f = fv.get();
-  const double fs = fv.scale();
+  // f (and its device-side column index / scale) may be written by the kernel launched just
+  // before this one: read after the PDL wait
+  const double2* __restrict__ f = nullptr;
+  double fs = 0.0;
   const int I0 = blockIdx.x * TCX, J0 = blockIdx.y * TCY;
   const int gx0 = 2 * I0 + o - 2, gy0 = 2 * J0 + o - 2;
   // fine points whose pre-smoothed u this CTA owns (a partition of the fine grid)
@@ -94,7 +95,16 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int
   for (int tb0 = 0; tb0 < RX * RY; tb0 += 256 * NT) {
   const int tid = ty * 32 + tx + tb0;
   double2 fl[NT];
-  double kl[NT];
+  double kl[NT], dl[NT];
+  // Small levels (latency-bound): k is set-up data, loaded -- and the reciprocal modulus of the
+  // Jacobi diagonal formed -- before the PDL wait (f is the output of the kernel launched just
+  // before this one).  Large levels wait first (the extra registers would spill).
+  constexpr bool PRE = TCX * TCY <= 32;
+  if (!PRE && tb0 == 0) {
+    HELM_PDL_ENTRY();
+    f = fv.get();
+    fs = fv.scale();
+  }
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
     const int t = tid + 256 * i;
@@ -102,8 +112,28 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int
     const int x = gx0 + ix, y = gy0 + iy;
     const bool in = t < RX * RY && (interior || (x >= 0 && x < F.nx && y >= 0 && y < F.ny));
     const size_t p = in ? (size_t)y * F.nx + x : 0;
-    fl[i] = in ? f[p] : czero();
     kl[i] = in ? k[p] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int t = tid + 256 * i;
+    const int iy = t / RX, ix = t - iy * RX;
+    const int x = gx0 + ix, y = gy0 + iy;
+    if (PRE) dl[i] = cdiv_den(interior ? interior_ap(ih2, kl[i], sr, si) : coef_at(F, x, y, kl[i], sr, si).ap);
+  }
+  if (PRE && tb0 == 0) {
+    HELM_PDL_ENTRY();
+    f = fv.get();
+    fs = fv.scale();
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int t = tid + 256 * i;
+    const int iy = t / RX, ix = t - iy * RX;
+    const int x = gx0 + ix, y = gy0 + iy;
+    const bool in = t < RX * RY && (interior || (x >= 0 && x < F.nx && y >= 0 && y < F.ny));
+    const size_t p = in ? (size_t)y * F.nx + x : 0;
+    fl[i] = in ? f[p] : czero();
   }
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
@@ -118,7 +148,7 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_down(Geo F, Geo G, int
         kk = kl[i];
         fvv = cscale(fs, fl[i]);
         const double2 ap = interior ? interior_ap(ih2, kk, sr, si) : coef_at(F, x, y, kk, sr, si).ap;
-        uv = cscale(omega, cdiv(fvv, ap));   // reading R9: first sweep from u = 0
+        uv = cscale(omega, PRE ? cdiv_d(fvv, ap, dl[i]) : cdiv(fvv, ap));   // reading R9: first sweep from u = 0
         if (x >= xs && x < xe && y >= ys && y < ye) u[p] = uv;
       }
       su[t] = uv;
@@ -209,6 +239,8 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
   const double2 fo = oin ? f[po] : czero();
   const double ko = oin ? k[po] : 0.0;
   const double2 qo = (oin && addq) ? addq[po] : czero();
+  const double2 apo = interior ? interior_ap(ih2, ko, sr, si) : coef_at(F, ox_, oy_, ko, sr, si).ap;
+  const double dpo = cdiv_den(apo);
   HELM_PDL_ENTRY();
 #pragma unroll
   for (int i = 0; i < NE; ++i) {
@@ -261,16 +293,14 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
   if (oin) {
     const int r = ty, c = tx;
     const int q = (r + 1) * RX + (c + 1);
-    double2 ap, res;
+    double2 res;
     if (interior) {
-      ap = interior_ap(ih2, ko, sr, si);
-      res = csub(cscale(fs, fo), interior_stencil(ih2, ap, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
+      res = csub(cscale(fs, fo), interior_stencil(ih2, apo, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
     } else {
       const Coef cf = coef_at(F, ox_, oy_, ko, sr, si);
-      ap = cf.ap;
       res = csub(cscale(fs, fo), stencil5(cf, s1[q], s1[q - 1], s1[q + 1], s1[q - RX], s1[q + RX]));
     }
-    double2 v = cadd(s1[q], cscale(omega, cdiv(res, ap)));
+    double2 v = cadd(s1[q], cscale(omega, cdiv_d(res, apo, dpo)));
     if (addq) v = cadd(v, qo);
     y[po] = v;
   }

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--problem", default="c4_weak_2049")
     ap.add_argument("--out", default="gpurun_out/c4_sweep.jsonl")
     ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--warm", type=int, default=0, help="untimed solves before the timed one (graph capture)")
     ap.add_argument("settings", nargs="+")
     a = ap.parse_args()
     settings = []
@@ -44,6 +45,8 @@ def main():
         maxit = st.pop("maxit", 1000)
         prm = dict(BASE, **st)
         H = helm.helm_setup(p, prm)
+        for _ in range(a.warm):
+            H.solve(b, a.tol, maxit)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         x, rep = H.solve(b, a.tol, maxit)
