@@ -273,17 +273,15 @@ __global__ void __launch_bounds__(256, HELM_VC_MINB) k_vc_up(Geo F, Geo G, int o
         const bool ox = (ri & 1) != 0;
         const int lx = Ia - cx0;
         const double2* e0 = se + ly * CX + lx;
-        // bilinear (Eq. 3.9): weights 1, 1/2 or 1/4 by parity; same operation order as before
-        double2 s;
-        if (!ox && !oy) {
-          s = e0[0];
-        } else if (ox && !oy) {
-          s = cadd(cscale(0.5, e0[0]), cscale(0.5, e0[1]));
-        } else if (!ox && oy) {
-          s = cadd(cscale(0.5, e0[0]), cscale(0.5, e0[CX]));
-        } else {
-          s = cadd(cadd(cscale(0.25, e0[0]), cscale(0.25, e0[1])), cadd(cscale(0.25, e0[CX]), cscale(0.25, e0[CX + 1])));
-        }
+        // bilinear (Eq. 3.9): weights 1, 1/2 or 1/4 by parity, branch-free (the parities alternate
+        // across the lanes of a warp): s = wy0 (wx0 e00 + wx1 e01) + wy1 (wx0 e10 + wx1 e11) with
+        // power-of-two weights, so every product is exact and s equals the per-parity forms
+        // e00, (e00/2 + e01/2), (e00/4 + e01/4) + (e10/4 + e11/4) bit for bit
+        const double wx0 = ox ? 0.5 : 1.0, wx1 = ox ? 0.5 : 0.0;
+        const double wy0 = oy ? 0.5 : 1.0, wy1 = oy ? 0.5 : 0.0;
+        const double2 a = cadd(cscale(wx0, e0[0]), cscale(wx1, e0[1]));
+        const double2 b = cadd(cscale(wx0, e0[CX]), cscale(wx1, e0[CX + 1]));
+        const double2 s = cadd(cscale(wy0, a), cscale(wy1, b));
         v = cadd(s, ul[i]);
       }
       s1[t] = v;
