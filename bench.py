@@ -322,15 +322,26 @@ def kernel_roofline(H, rep, method, peaks, workload):
     comps += [
         ("k_apply_op A (level 0)", "apply_A", 0, 10, 2 * outer_its, 40.0 * n0),
     ]
+    # the outer FGMRES's DCGS2 step over the level-0 basis at the solve's mean column (pass 1 reads
+    # V_0..V_j, v~_j, w; pass 2 reads V_0..V_{j-1}, v~_j, w and writes v_j, w'): a group, not chosen
+    jo = max(1, outer_its // 2)
+    if method.get("outer", "fgmres") == "fgmres" and not method.get("restart"):
+        comps.append(("outer DCGS2 step, level-0 basis (3 kernels)", "outer_dcgs", jo, 3, outer_its,
+                      (32.0 * jo + 112.0) * n0))
     rows = {}
     for label, region, arg, nrep, count, nbytes in comps:
-        us = H.helm_bench_graph(region, arg, nrep)
+        try:
+            us = H.helm_bench_graph(region, arg, nrep)
+        except RuntimeError:
+            if region != "outer_dcgs":   # needs the outer basis of a finished solve on this context
+                raise
+            continue
         gbs = nbytes / (us * 1e-6) / 1e9
         rows[label] = {"kernel": label, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                        "frac": gbs / peaks["hbm_gbs"], "traffic": None, "bytes_per_launch": nbytes,
                        "us_per_launch": us, "launches_per_step": count, "est_ms_per_step": count * us * 1e-3,
                        "column": arg if region in ("e_dots", "dcgs_dots", "dcgs_update", "dcgs_reduce", "ss_dots",
-                                                   "ss_update", "ss_reduce") else None,
+                                                   "ss_update", "ss_reduce", "outer_dcgs") else None,
                        "timing": "in-graph, warm (helm_bench_graph: the solve's own launch, replayed)",
                        "peak_src": peaks["src"]}
     # the dominant KERNEL (groups of kernels are reported, not chosen)

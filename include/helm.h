@@ -277,6 +277,10 @@ int helm_bench_kernel(helm_ctx ctx, int which, int arg, int reps, int flush, dou
 #define HELM_GB_SS_UPDATE 13  /* W <- (W - Q C) R^-1 (one sweep over the basis) */
 #define HELM_GB_SS_POWER 14   /* one step of the block basis: V-cycle from level 1 + E in residual mode */
 #define HELM_GB_SS_E 15       /* E in residual mode alone, w = sigma f - E x */
+#define HELM_GB_OUTER_DCGS 16 /* the outer FGMRES's delayed-CGS2 step at basis column `arg` (pass 1,
+                                 reduction + step A, pass 2 + step B over the level-0 basis as the
+                                 solve launches them; the operator applies are not included).  Needs
+                                 an outer basis of more than arg + reps columns: call after a solve */
 int helm_bench_graph(helm_ctx ctx, int which, int arg, int reps, double* us_per_region);
 
 /* ---------------------------------------------------------------------------------------

@@ -2446,6 +2446,27 @@ int helm_bench_graph(helm_ctx C, int which, int arg, int reps, double* us_per_re
         r = arnoldi_step(X, K, opA, fused_E_dots(X), inner_lag(X), cudaGraphConditionalHandle(0), 0, mask);
         break;
       }
+      case HELM_GB_OUTER_DCGS: {
+        // the outer FGMRES's DCGS2 step at column j = arg, without the operator applies
+        // (mask: pass 1 alone | reduction | pass 2); w = the column after v~_j, as in the solve
+        Fgm& K = X.outer;
+        if (!K.V || arg < 0 || arg + reps >= K.m) {
+          r = fail(HELM_EINVAL, "outer DCGS2 region: no outer basis of more than %d columns (run a solve first)",
+                   arg + reps);
+          break;
+        }
+        if (i == 0) {
+          launch_k(X, k_fgm_reset, 1, 1, 0, K.st, 0.0, 1 << 30, K.m);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+          launch_k(X, k_set_j, 1, 1, 0, K.st, arg);
+          r = post_launch(X);
+          if (r != HELM_OK) break;
+        }
+        auto opN = [&](DVec, DVec, DVec) { return (int)HELM_OK; };
+        r = arnoldi_step(X, K, opN, false, false, cudaGraphConditionalHandle(0), 0, 1 | 8 | 2 | 4);
+        break;
+      }
       case HELM_GB_SS_DOTS:
       case HELM_GB_SS_REDUCE:
       case HELM_GB_SS_UPDATE:

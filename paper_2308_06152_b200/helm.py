@@ -287,7 +287,7 @@ class Helm:
 
     REGIONS = {"vcycle": 0, "apply_E": 1, "apply_A": 2, "dcgs": 3, "inner_iter": 4, "e_dots": 5, "dcgs_reduce": 6,
                "dcgs_update": 7, "dcgs_dots": 8, "vc_down": 9, "vc_up": 10, "ss_dots": 11, "ss_reduce": 12,
-               "ss_update": 13, "ss_power": 14, "ss_e": 15}
+               "ss_update": 13, "ss_power": 14, "ss_e": 15, "outer_dcgs": 16}
 
     def helm_bench_graph(self, which, arg=0, reps=50):
         """Mean in-graph device time (us) of one instance of a region (warm, back-to-back)."""
