@@ -30,3 +30,6 @@ def test_bench_line(lib, extra):
         assert key in r, key
     assert 0 < r["frac"] < 1.2
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    comps = line["roofline_kernels"]["components"]
+    if not extra:   # the outer DCGS2 step is replayed on the solved context's own basis
+        assert any(k.startswith("outer DCGS2") and v["us_per_launch"] > 0 for k, v in comps.items()), list(comps)
