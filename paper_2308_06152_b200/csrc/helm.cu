@@ -105,6 +105,8 @@ struct Fgm {
   // s-step coarse solve (sstep.cuh, reading R28): block size, dots grid (nbx chunks x gy row
   // ranges of crows rows), update blocks; raw Hessenberg matrix, block factors, pass partials
   int ss = 0, ss_nbx = 0, ss_gy = 0, ss_crows = 0, ss_nu = 0, ss_nred = 0, ss_ring = 0;
+  bool ss_hess_fused = false;   // the update kernel's last block runs the Hessenberg step
+  size_t ss_usm = 0;            // dynamic shared memory of k_bgs_update
   size_t ss_smem = 0;
   long long ss_chunk = 0;
   double2 *Hr = nullptr, *sCm = nullptr, *sRi = nullptr, *sCt = nullptr, *sRt = nullptr;
@@ -1379,7 +1381,13 @@ int sstep_alloc_t(helm_ctx_s& C, Fgm& K) {
   const long long nbx = std::max(1LL, (long long)std::max(1, bps) * C.sm_count / K.ss_gy);
   K.ss_chunk = ((n + nbx - 1) / nbx + unit - 1) / unit * unit;
   K.ss_nbx = (int)((n + K.ss_chunk - 1) / K.ss_chunk);
-  const size_t usm = ((size_t)(m + 1) * S + S * S) * sizeof(double2);
+  // the update kernel's last block runs the Hessenberg step (k_bgs_hess's body) when its shared
+  // memory fits next to a second block (HELM_SS_HESS_FUSED=0: the separate kernel, probe)
+  static const int hess_fused = getenv("HELM_SS_HESS_FUSED") ? atoi(getenv("HELM_SS_HESS_FUSED")) : 1;
+  const size_t usm0 = ((size_t)(m + 1) * S + S * S) * sizeof(double2);
+  K.ss_hess_fused = hess_fused && sstep_hess_smem(m, S) <= 100 * 1024;
+  const size_t usm = K.ss_hess_fused ? std::max(usm0, sstep_hess_smem(m, S)) : usm0;
+  K.ss_usm = usm;
   CKR(raise_dyn_smem((const void*)k_bgs_update<S>, usm));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bgs_update<S>, BG_THREADS, usm));
   K.ss_nu = std::max(1, bps) * C.sm_count;
@@ -1458,7 +1466,10 @@ int sstep_block(helm_ctx_s& C, Fgm& K, cudaGraphConditionalHandle h, int use_h, 
   }
   if (mask & 24) return HELM_OK;
   const size_t dsm = (size_t)BG_WARPS * K.ss_crows * NV * sizeof(double);
-  const size_t usm = ((size_t)(K.m + 1) * S + S * S) * sizeof(double2);
+  const size_t usm = K.ss_usm;
+  const BgsHessArgs ha = {st, (const double2*)K.sCt, (const double2*)K.sRt, (const double*)K.ssig, K.Hr, K.H, K.cs,
+                          K.sn, K.g, sstep_hess_stage(K.m) ? 1 : 0, h, use_h};
+  bool hess_done = false;
   for (int p = 0; p < (mask ? 1 : C.p.sstep_passes); ++p) {
     if (!mask || (mask & 1)) {
     if (K.ss_ring) {
@@ -1487,15 +1498,19 @@ int sstep_block(helm_ctx_s& C, Fgm& K, cudaGraphConditionalHandle h, int use_h, 
       CKR(post_launch(C));
     }
     if (!mask || (mask & 4)) {
-      launch_k(C, k_bgs_update<S>, dim3(K.ss_nu), dim3(BG_THREADS), usm, Vo, ld, (const int*)&st->j, (long long)K.n,
-               (const double2*)K.sCm, (const double2*)K.sRi);
+      // the block's last update carries the Hessenberg step in its last block (off the critical
+      // path: it needs the reduction's factors only; the update then reads the reduction's
+      // snapshot of J, since that block advances st->j)
+      const bool fuse_h = !mask && K.ss_hess_fused && p == C.p.sstep_passes - 1 && K.ss_nu > 1;
+      launch_k(C, k_bgs_update<S>, dim3(K.ss_nu), dim3(BG_THREADS), usm, Vo, ld,
+               fuse_h ? (const int*)&st->jblk : (const int*)&st->j, (long long)K.n, (const double2*)K.sCm,
+               (const double2*)K.sRi, fuse_h ? 1 : 0, ha);
       CKR(post_launch(C));
+      hess_done = fuse_h;
     }
   }
-  if (mask) return HELM_OK;
-  launch_k(C, k_bgs_hess<S>, dim3(1), dim3(256), sstep_hess_smem(K.m, S), st,
-           (const double2*)K.sCt, (const double2*)K.sRt, (const double*)K.ssig, K.Hr, K.H, K.cs, K.sn, K.g,
-           sstep_hess_stage(K.m) ? 1 : 0, h, use_h);
+  if (mask || hess_done) return HELM_OK;
+  launch_k(C, k_bgs_hess<S>, dim3(1), dim3(256), sstep_hess_smem(K.m, S), ha);
   return post_launch(C);
 }
 

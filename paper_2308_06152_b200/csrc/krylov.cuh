@@ -68,6 +68,8 @@ struct FgmState {
   int sbrk, sbrk_total;
   long long blocks;         // s-step blocks run by this coarse solve
   long long inner_blocks;   // (outer state) s-step blocks over all coarse solves
+  int jblk;                 // s-step: the block's first column J, snapshot by the reduction (the update
+                            // reads it while its extra block -- the Hessenberg step -- advances j)
 };
 
 __device__ __forceinline__ double2 warp_sum2(double2 s) {

@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(256) k_bgs_reduce(const double* __restrict__ p
     }
     tri_inverse<S>(R, Rin);
     if (brk) st->sbrk = 1;
+    st->jblk = J;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < S * S; i += blockDim.x) Ri[i] = Rin[i];
@@ -375,74 +376,40 @@ __global__ void __launch_bounds__(256) k_bgs_reduce(const double* __restrict__ p
   }
 }
 
-// W <- (W - Q C) R^{-1} for W = V[J+1 .. J+S], Q = V[0 .. J] (in place: every element's outputs
-// depend on that element's inputs only).  One element per thread per step.
-#ifndef HELM_BGU_MINB
-#define HELM_BGU_MINB 2
-#endif
-#ifndef HELM_BGU_UNROLL
-#define HELM_BGU_UNROLL 4
-#endif
-template <int S>
-__global__ void __launch_bounds__(BG_THREADS, HELM_BGU_MINB) k_bgs_update(double2* __restrict__ V, long long ld,
-                                                              const int* __restrict__ jptr, long long n,
-                                                              const double2* __restrict__ Cm,
-                                                              const double2* __restrict__ Ri) {
-  HELM_PDL_ENTRY();
-  extern __shared__ double2 bsm[];   // C: (J+1) x S, then R^{-1}: S x S
-  const int J = *jptr;
-  double2* sC = bsm;
-  double2* sR = bsm + (size_t)(J + 1) * S;
-  for (int i = threadIdx.x; i < (J + 1) * S; i += blockDim.x) sC[i] = Cm[i];
-  for (int i = threadIdx.x; i < S * S; i += blockDim.x) sR[i] = Ri[i];
-  __syncthreads();
-  double2* __restrict__ W = V + (long long)(J + 1) * ld;
-  for (long long e = blockIdx.x * (long long)BG_THREADS + threadIdx.x; e < n; e += (long long)gridDim.x * BG_THREADS) {
-    double2 w[S];
-#pragma unroll
-    for (int t = 0; t < S; ++t) w[t] = W[(long long)t * ld + e];
-    int c = 0;
-    constexpr int UN = HELM_BGU_UNROLL;
-    for (; c + UN <= J + 1; c += UN) {
-      double2 q[UN];
-#pragma unroll
-      for (int k = 0; k < UN; ++k) q[k] = ldb<2>(V + (long long)(c + k) * ld + e);
-#pragma unroll
-      for (int k = 0; k < UN; ++k)
-#pragma unroll
-        for (int t = 0; t < S; ++t) {
-          const double2 cc = sC[(c + k) * S + t];
-          w[t] = cfma(make_double2(-q[k].x, -q[k].y), cc, w[t]);
-        }
-    }
-    for (; c <= J; ++c) {
-      const double2 q = ldb<2>(V + (long long)c * ld + e);
-#pragma unroll
-      for (int t = 0; t < S; ++t) w[t] = cfma(make_double2(-q.x, -q.y), sC[c * S + t], w[t]);
-    }
-#pragma unroll
-    for (int t = S - 1; t >= 0; --t) {   // x_t = sum_{u <= t} w_u Ri_ut  (descending t: in place)
-      double2 s = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int u = 0; u <= t; ++u) s = cfma(w[u], sR[u * S + t], s);
-      W[(long long)t * ld + e] = s;
-    }
-  }
-}
-
 // New Hessenberg columns J..J+S-1 from the block's factors, their Givens rotations, the residual
 // estimate after every column and the loop decision (one block).  H is the rotated (upper
 // triangular) matrix the back substitution reads, Hr the raw Hessenberg matrix (column-major,
 // ld m + 1).  Rotation k: (x_k, x_k+1) <- (c x_k + s x_k+1, -conj(s) x_k + c x_k+1).
+struct BgsHessArgs {
+  FgmState* st;
+  const double2* Ctot;
+  const double2* Rtot;
+  const double* sig;
+  double2* Hr;
+  double2* H;
+  double* cs;
+  double2* sn;
+  double2* g;
+  int stage_h;
+  cudaGraphConditionalHandle h;
+  int use_h;
+};
+
+// One 256-thread block; hsm = its dynamic shared memory (sstep_hess_smem bytes):
+// X: (J+1+S) x S column-major (ld m + 1 + S) | Ctot | Rtot | sn | cs [| raw H]
 template <int S>
-__global__ void __launch_bounds__(256) k_bgs_hess(FgmState* st, const double2* __restrict__ Ctot,
-                                                  const double2* __restrict__ Rtot, const double* __restrict__ sig,
-                                                  double2* __restrict__ Hr, double2* __restrict__ H,
-                                                  double* __restrict__ cs, double2* __restrict__ sn,
-                                                  double2* __restrict__ g, int stage_h, cudaGraphConditionalHandle h,
-                                                  int use_h) {
-  HELM_PDL_ENTRY();
-  extern __shared__ double2 hsm[];   // X: (J+1+S) x S column-major (ld m + 1 + S) | Ctot | Rtot | sn | cs
+__device__ __forceinline__ void bgs_hess_body(const BgsHessArgs& a, double2* hsm) {
+  FgmState* st = a.st;
+  const double2* __restrict__ Ctot = a.Ctot;
+  const double2* __restrict__ Rtot = a.Rtot;
+  const double* __restrict__ sig = a.sig;
+  double2* __restrict__ Hr = a.Hr;
+  double2* __restrict__ H = a.H;
+  double* __restrict__ cs = a.cs;
+  double2* __restrict__ sn = a.sn;
+  double2* __restrict__ g = a.g;
+  const int stage_h = a.stage_h, use_h = a.use_h;
+  const cudaGraphConditionalHandle h = a.h;
   const int J = st->j, m = st->m;
   const int ldh = m + 1, ldx = m + 1 + S;
   const int nr = J + 1 + S;
@@ -597,6 +564,78 @@ __global__ void __launch_bounds__(256) k_bgs_hess(FgmState* st, const double2* _
     st->done = done;
     fgm_set_cond(st, h, use_h, !done);
   }
+}
+
+// W <- (W - Q C) R^{-1} for W = V[J+1 .. J+S], Q = V[0 .. J] (in place: every element's outputs
+// depend on that element's inputs only).  One element per thread per step.  Optionally the last
+// block runs the Hessenberg step of the block instead (off the critical path).
+#ifndef HELM_BGU_MINB
+#define HELM_BGU_MINB 2
+#endif
+#ifndef HELM_BGU_UNROLL
+#define HELM_BGU_UNROLL 4
+#endif
+template <int S>
+__global__ void __launch_bounds__(BG_THREADS, HELM_BGU_MINB) k_bgs_update(double2* __restrict__ V, long long ld,
+                                                              const int* __restrict__ jptr, long long n,
+                                                              const double2* __restrict__ Cm,
+                                                              const double2* __restrict__ Ri, int hess,
+                                                              BgsHessArgs ha) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 bsm[];   // C: (J+1) x S, then R^{-1}: S x S
+  // hess: the last block runs the Hessenberg step of this s-step block (bgs_hess_body: it needs the
+  // reduction's factors only) while the others stream the basis; it advances st->j at its end, so
+  // jptr then points at the reduction's snapshot st->jblk.  The streaming blocks are all resident.
+  const int nsb = hess ? (int)gridDim.x - 1 : (int)gridDim.x;
+  if (hess && (int)blockIdx.x == nsb) {
+    bgs_hess_body<S>(ha, bsm);
+    return;
+  }
+  const int J = *jptr;
+  double2* sC = bsm;
+  double2* sR = bsm + (size_t)(J + 1) * S;
+  for (int i = threadIdx.x; i < (J + 1) * S; i += blockDim.x) sC[i] = Cm[i];
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) sR[i] = Ri[i];
+  __syncthreads();
+  double2* __restrict__ W = V + (long long)(J + 1) * ld;
+  for (long long e = blockIdx.x * (long long)BG_THREADS + threadIdx.x; e < n; e += (long long)nsb * BG_THREADS) {
+    double2 w[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) w[t] = W[(long long)t * ld + e];
+    int c = 0;
+    constexpr int UN = HELM_BGU_UNROLL;
+    for (; c + UN <= J + 1; c += UN) {
+      double2 q[UN];
+#pragma unroll
+      for (int k = 0; k < UN; ++k) q[k] = ldb<2>(V + (long long)(c + k) * ld + e);
+#pragma unroll
+      for (int k = 0; k < UN; ++k)
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const double2 cc = sC[(c + k) * S + t];
+          w[t] = cfma(make_double2(-q[k].x, -q[k].y), cc, w[t]);
+        }
+    }
+    for (; c <= J; ++c) {
+      const double2 q = ldb<2>(V + (long long)c * ld + e);
+#pragma unroll
+      for (int t = 0; t < S; ++t) w[t] = cfma(make_double2(-q.x, -q.y), sC[c * S + t], w[t]);
+    }
+#pragma unroll
+    for (int t = S - 1; t >= 0; --t) {   // x_t = sum_{u <= t} w_u Ri_ut  (descending t: in place)
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u <= t; ++u) s = cfma(w[u], sR[u * S + t], s);
+      W[(long long)t * ld + e] = s;
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) k_bgs_hess(BgsHessArgs a) {
+  HELM_PDL_ENTRY();
+  extern __shared__ double2 hsm[];
+  bgs_hess_body<S>(a, hsm);
 }
 
 }  // namespace helm
