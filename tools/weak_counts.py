@@ -1,7 +1,7 @@
 """Outer iteration counts of BASELINE configs[4]'s weak-scaling family (reading R27: N unit squares
 stacked in y at h = 1/2048, k = 1280) solved as ONE grid on one GPU with the bench method: what a
 decomposed N-GPU solve has to reproduce (the decomposition changes no arithmetic but the order of
-the rank sums).  python tools/weak_counts.py 1 2"""
+the rank sums).  python tools/weak_counts.py 1 2   (WEAK_K / WEAK_NCELLS: a smaller analogue, same kh)"""
 import json
 import os
 import sys
@@ -14,7 +14,7 @@ from paper_2308_06152_b200 import helm  # noqa: E402
 from workloads.media import strip_problem  # noqa: E402
 
 for n in [int(a) for a in sys.argv[1:]] or [1, 2]:
-    p = strip_problem(1280.0, 2048, n)
+    p = strip_problem(float(os.environ.get("WEAK_K", "1280")), int(os.environ.get("WEAK_NCELLS", "2048")), n)
     b = torch.from_numpy(p.b).cuda()
     prm = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": 192,
            "inner_restart": 48, "coarsest_n": 512, "sstep": 8, "sstep_passes": 1}
@@ -25,7 +25,7 @@ for n in [int(a) for a in sys.argv[1:]] or [1, 2]:
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     rr = float(torch.linalg.vector_norm(H.apply_A(x) - b) / torch.linalg.vector_norm(b))
-    print(json.dumps({"strips": n, "nx": p.nx, "ny": p.ny, "outer": rep["outer_iterations"],
+    print(json.dumps({"k": p.meta["k"], "strips": n, "nx": p.nx, "ny": p.ny, "outer": rep["outer_iterations"],
                       "converged": rep["converged"], "restarts": rep["restarts"], "seconds_incl_capture": round(dt, 2),
                       "inner_total": rep["inner_iterations_total"], "true_relres": rr}), flush=True)
     H.close()
