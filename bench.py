@@ -536,6 +536,11 @@ def _run_decomposed(args, rank, world, local):
         "roofline_kernels": roof_all,
         "clocks": clk.summary(),
     }
+    if not line["converged"]:
+        # DESIGN.md R27: the stacked-strip weak family gets harder with N at the N = 1 method's
+        # coarse cap (one-GPU runs of the N = 2..8 grids, profiles/r02_weak_family_counts.jsonl)
+        line["note"] = (f"not converged to 1e-6 within maxit = {args.maxit}: value is the time to maxit, "
+                        "not a time to solution (DESIGN.md R27)")
     return line
 
 

@@ -16,8 +16,9 @@ from workloads.media import strip_problem  # noqa: E402
 for n in [int(a) for a in sys.argv[1:]] or [1, 2]:
     p = strip_problem(float(os.environ.get("WEAK_K", "1280")), int(os.environ.get("WEAK_NCELLS", "2048")), n)
     b = torch.from_numpy(p.b).cuda()
-    prm = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": 192,
-           "inner_restart": 48, "coarsest_n": 512, "sstep": 8, "sstep_passes": 1}
+    cap = int(os.environ.get("WEAK_CAP", "192")) * (n if os.environ.get("WEAK_CAP_SCALE") else 1)
+    prm = {"vectors": "high_order", "coarse_op": "galerkin", "inner_tol": 0.1, "inner_maxit": cap,
+           "inner_restart": int(os.environ.get("WEAK_M", "48")), "coarsest_n": 512, "sstep": 8, "sstep_passes": 1}
     H = helm.helm_setup(p, prm)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -25,7 +26,7 @@ for n in [int(a) for a in sys.argv[1:]] or [1, 2]:
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     rr = float(torch.linalg.vector_norm(H.apply_A(x) - b) / torch.linalg.vector_norm(b))
-    print(json.dumps({"k": p.meta["k"], "strips": n, "nx": p.nx, "ny": p.ny, "outer": rep["outer_iterations"],
+    print(json.dumps({"k": p.meta["k"], "cap": cap, "strips": n, "nx": p.nx, "ny": p.ny, "outer": rep["outer_iterations"],
                       "converged": rep["converged"], "restarts": rep["restarts"], "seconds_incl_capture": round(dt, 2),
                       "inner_total": rep["inner_iterations_total"], "true_relres": rr}), flush=True)
     H.close()
