@@ -432,7 +432,12 @@ def _run_decomposed(args, rank, world, local):
     torch.cuda.set_device(local)
     peaks = load_peaks()
     base = config_problem(args.workload)
-    p = strip_problem(base.meta["k"], base.meta["n_cells"], world, f"{args.workload}_x{world}")
+    if args.scaling == "strong":
+        # strong scaling: the workload's own grid (e.g. c4_strong_8193, BASELINE configs[4]) cut
+        # into `world` row strips
+        p = base
+    else:
+        p = strip_problem(base.meta["k"], base.meta["n_cells"], world, f"{args.workload}_x{world}")
     method = gpu_method(args)
     uid = peer_exchange = None
     if args.transport == "peer":        # NVLink peer memory through CUDA IPC (peer.cuh), no NCCL
@@ -516,7 +521,7 @@ def _run_decomposed(args, rank, world, local):
     line = {
         "metric": "fgmres_time_to_1e-6_s", "value": tts, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tts,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "outer_its_per_s": its / dev_s, "time_to_solution_s": tts,
         "converged": all(x_["converged"] for x_ in reps),
         "config": {"workload": p.name, "per_gpu_block": args.workload, **method, "nx": p.nx, "ny": p.ny,
@@ -570,6 +575,9 @@ def main():
     ap.add_argument("--record-counts", action="store_true",
                     help="write this run's iteration counts to profiles/r02_bench_counts.json (reference arm)")
     ap.add_argument("--dist-levels", type=int, default=0, help="decomposed levels (0: 3)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="decomposed solve: weak = the workload's block per GPU (stacked strips, default); "
+                         "strong = the workload's own grid cut into N strips (e.g. --workload c4_strong_8193)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
                     help="decomposed solve: NCCL collectives (default) or NVLink peer memory through CUDA IPC")
     ap.add_argument("--decomp", default="auto", choices=["auto", "on", "off"],
